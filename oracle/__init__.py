@@ -1,0 +1,416 @@
+"""TEST INFRASTRUCTURE ONLY — CPU oracle for the USPG/USCG MART hot path.
+
+Two checkers, both CPU:
+
+* ``Orc``  — ctypes binding of ``liborc.so``, the plain-C generalized
+  restatement in ``uscg_oracle.c`` (ring-law table, decoupled slice count,
+  explicit first-view rays, view-angle list).
+* ``Ref``  — ctypes binding of ``_ref/libuscg_ref.so``: the UNMODIFIED reference
+  library compiled from /root/reference/proj/src (see Makefile) behind
+  ``ref_shim.cpp``. Used to pin ``Orc`` bit-exactly on the reference's own
+  configurations and as the CPU baseline.
+
+Only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py``'s cpu_baseline /
+``--impl reference`` leg may import this package. The product
+(``paper_2208_12964_b200``) never does.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ORC_SO = os.path.join(HERE, "liborc.so")
+REF_SO = os.path.join(HERE, "_ref", "libuscg_ref.so")
+REF_SRC = "/root/reference/proj"
+
+_dp = C.POINTER(C.c_double)
+_u32p = C.POINTER(C.c_uint32)
+_u16p = C.POINTER(C.c_uint16)
+_u8p = C.POINTER(C.c_uint8)
+_u64p = C.POINTER(C.c_uint64)
+
+
+def build(ref: bool | None = None) -> None:
+    """Compile liborc.so (always) and the reference library when the
+    reference sources are present (this container; never on the GPU box)."""
+    subprocess.run(["make", "-s", "-C", HERE, "all"], check=True)
+    if ref is None:
+        ref = os.path.isdir(REF_SRC)
+    if ref:
+        subprocess.run(["make", "-s", "-C", HERE, "ref"], check=True)
+
+
+def _ptr(a, t):
+    return a.ctypes.data_as(t) if a is not None else None
+
+
+class _Grid(C.Structure):
+    _fields_ = [
+        ("n_rings", C.c_int),
+        ("ring_spacing", C.c_double),
+        ("n_slices", C.c_int),
+        ("slice_height", C.c_double),
+        ("volume", C.c_int),
+        ("counts", _u32p),
+    ]
+
+
+class _Cache(C.Structure):
+    _fields_ = [("lines", C.c_int), ("offsets", _u32p), ("records", C.c_void_p), ("n_records", C.c_uint64)]
+
+
+REC_DTYPE = np.dtype([("phi_a", "<f8"), ("phi_b", "<f8"), ("slice", "<u2"), ("ring", "<u2")], align=True)
+
+
+class OrcGrid:
+    """Generalized grid: rings, ring spacing, slices, slice height, 2D/3D and a
+    sector-count table (None = reference 4(2k-1) law)."""
+
+    def __init__(self, n_rings, ring_spacing, n_slices=1, slice_height=None, volume=False, counts=None):
+        self.n_rings = int(n_rings)
+        self.ring_spacing = float(ring_spacing)
+        self.n_slices = int(n_slices) if volume else 1
+        self.slice_height = float(ring_spacing if slice_height is None else slice_height)
+        self.volume = bool(volume)
+        self.counts = None if counts is None else np.ascontiguousarray(counts, dtype=np.uint32)
+        self._c = _Grid(self.n_rings, self.ring_spacing, self.n_slices, self.slice_height,
+                        int(self.volume), _ptr(self.counts, _u32p))
+
+    @classmethod
+    def reference(cls, n, volume=False):
+        """GridSpec::square_2d(n) / cube_3d(n) (include/uscg/grid.hpp:38-43)."""
+        return cls(n // 2, 2.0 / n, n if volume else 1, 2.0 / n, volume)
+
+    def ring_counts(self):
+        if self.counts is not None:
+            return self.counts.copy()
+        k = np.arange(1, self.n_rings + 1)
+        return (4 * (2 * k - 1)).astype(np.uint32)
+
+    def cells_per_slice(self):
+        return int(self.ring_counts().astype(np.int64).sum())
+
+    def cell_count(self):
+        return self.cells_per_slice() * self.n_slices
+
+
+class Orc:
+    def __init__(self, path: str = ORC_SO):
+        if not os.path.exists(path):
+            build(ref=False)
+        L = C.CDLL(path)
+        self.L = L
+        L.orc_cache_build.argtypes = [C.POINTER(_Grid), C.c_int, _dp, _dp, C.POINTER(_Cache)]
+        L.orc_cache_free.argtypes = [C.POINTER(_Cache)]
+        L.orc_trace_line.argtypes = [C.POINTER(_Grid), C.POINTER(_Cache), C.c_int, C.c_double, _u32p,
+                                     _u32p, _u32p, _u64p]
+        L.orc_trace_line.restype = C.c_int64
+        L.orc_trace_chord.argtypes = [C.POINTER(_Grid), C.c_void_p, C.c_double, _u32p, C.c_int64]
+        L.orc_trace_chord.restype = C.c_int64
+        L.orc_project.argtypes = [C.POINTER(_Grid), C.POINTER(_Cache), C.c_int, _dp, _dp, _dp]
+        L.orc_project_length.argtypes = [C.POINTER(_Grid), C.c_int, _dp, _dp, C.c_int, _dp, _dp, _dp]
+        L.orc_reconstruct.argtypes = [C.POINTER(_Grid), C.POINTER(_Cache), C.c_int, _dp, _dp, _dp,
+                                      C.c_double, C.c_double, C.c_int, C.c_double, _dp, _dp, _u8p]
+        L.orc_reconstruct.restype = C.c_int
+        L.orc_uspg_to_cg_map.argtypes = [C.c_int, _u32p]
+        L.orc_bin_map.argtypes = [C.POINTER(_Grid), C.c_int, _u32p]
+        L.orc_field_to_cartesian.argtypes = [C.POINTER(_Grid), C.c_int, _dp, _dp]
+        L.orc_rays_flat.argtypes = [_dp, _dp, C.c_int, C.c_int, C.c_double, C.c_double, _dp, _dp]
+        L.orc_rays_arc.argtypes = [_dp, _dp, C.c_int, C.c_double, _dp, _dp]
+        L.orc_rays_parallel.argtypes = [C.c_int, C.c_double, C.c_double, _dp, _dp]
+        L.orc_ring_counts_m1.argtypes = [C.c_int, _u32p]
+        L.orc_norm360.argtypes = [C.c_double]
+        L.orc_norm360.restype = C.c_double
+        L.orc_rmse.argtypes = [C.c_size_t, _dp, _dp]
+        L.orc_rmse.restype = C.c_double
+        L.orc_ssim.argtypes = [C.c_int, C.c_int, _dp, _dp, C.c_double]
+        L.orc_ssim.restype = C.c_double
+
+    # -- ray generators -------------------------------------------------
+    def rays_flat(self, src, ctr, det_u, det_v, su, sv):
+        n = det_u * det_v
+        s = np.zeros((n, 3)); d = np.zeros((n, 3))
+        self.L.orc_rays_flat(_ptr(np.asarray(src, float), _dp), _ptr(np.asarray(ctr, float), _dp),
+                             det_u, det_v, su, sv, _ptr(s, _dp), _ptr(d, _dp))
+        return s, d
+
+    def rays_arc(self, src, ctr, det_u, du_deg):
+        s = np.zeros((det_u, 3)); d = np.zeros((det_u, 3))
+        self.L.orc_rays_arc(_ptr(np.asarray(src, float), _dp), _ptr(np.asarray(ctr, float), _dp),
+                            det_u, du_deg, _ptr(s, _dp), _ptr(d, _dp))
+        return s, d
+
+    def rays_parallel(self, det_u, su, half_len):
+        s = np.zeros((det_u, 3)); d = np.zeros((det_u, 3))
+        self.L.orc_rays_parallel(det_u, su, half_len, _ptr(s, _dp), _ptr(d, _dp))
+        return s, d
+
+    def ring_counts_m1(self, n_rings):
+        out = np.zeros(n_rings, np.uint32)
+        self.L.orc_ring_counts_m1(n_rings, _ptr(out, _u32p))
+        return out
+
+    def norm360(self, x):
+        return self.L.orc_norm360(float(x))
+
+    # -- cache / trace -----------------------------------------------------
+    def cache(self, grid: OrcGrid, src, det):
+        return OrcCache(self, grid, src, det)
+
+    def field_to_cartesian(self, grid: OrcGrid, field, npix):
+        f = np.ascontiguousarray(field, dtype=np.float64)
+        out = np.zeros((grid.n_slices, npix, npix))
+        self.L.orc_field_to_cartesian(C.byref(grid._c), npix, _ptr(f, _dp), _ptr(out, _dp))
+        return out
+
+    def uspg_to_cg_map(self, n):
+        out = np.zeros(n * n, np.uint32)
+        self.L.orc_uspg_to_cg_map(n, _ptr(out, _u32p))
+        return out
+
+    def bin_map(self, grid: OrcGrid, npix):
+        out = np.zeros(npix * npix, np.uint32)
+        self.L.orc_bin_map(C.byref(grid._c), npix, _ptr(out, _u32p))
+        return out
+
+    def rmse(self, a, b):
+        a = np.ascontiguousarray(a, float).ravel(); b = np.ascontiguousarray(b, float).ravel()
+        return self.L.orc_rmse(a.size, _ptr(a, _dp), _ptr(b, _dp))
+
+    def ssim(self, a, b, dynamic_range=-1.0):
+        a = np.ascontiguousarray(a, float); b = np.ascontiguousarray(b, float)
+        return self.L.orc_ssim(a.shape[0], a.shape[1], _ptr(a, _dp), _ptr(b, _dp), dynamic_range)
+
+
+class OrcCache:
+    """orc_cache (precompute_first_view direct build) + trace/project/reconstruct."""
+
+    def __init__(self, orc: Orc, grid: OrcGrid, src, det):
+        self.orc, self.grid = orc, grid
+        self.src = np.ascontiguousarray(src, dtype=np.float64)
+        self.det = np.ascontiguousarray(det, dtype=np.float64)
+        self.lines = self.src.shape[0]
+        self._c = _Cache()
+        orc.L.orc_cache_build(C.byref(grid._c), self.lines, _ptr(self.src, _dp), _ptr(self.det, _dp),
+                              C.byref(self._c))
+        n = int(self._c.n_records)
+        self.offsets = np.ctypeslib.as_array(self._c.offsets, shape=(self.lines + 1,)).copy()
+        if n:
+            buf = (C.c_char * (n * REC_DTYPE.itemsize)).from_address(self._c.records)
+            self.records = np.frombuffer(bytes(buf), dtype=REC_DTYPE).copy()
+        else:
+            self.records = np.zeros(0, REC_DTYPE)
+        self._stamp = np.zeros(grid.cell_count(), np.uint32)
+        self._gen = np.zeros(1, np.uint32)
+        self._out = np.zeros(max(grid.cell_count(), 1), np.uint32)
+
+    def __del__(self):
+        try:
+            self.orc.L.orc_cache_free(C.byref(self._c))
+        except Exception:
+            pass
+
+    def trace_line(self, line, theta_deg):
+        chords = np.zeros(1, np.uint64)
+        n = self.orc.L.orc_trace_line(C.byref(self.grid._c), C.byref(self._c), int(line), float(theta_deg),
+                                      _ptr(self._stamp, _u32p), _ptr(self._gen, _u32p),
+                                      _ptr(self._out, _u32p), _ptr(chords, _u64p))
+        return self._out[:n].copy()
+
+    def project(self, thetas, field):
+        th = np.ascontiguousarray(thetas, float)
+        f = np.ascontiguousarray(field, float)
+        out = np.zeros((th.size, self.lines))
+        self.orc.L.orc_project(C.byref(self.grid._c), C.byref(self._c), th.size, _ptr(th, _dp),
+                               _ptr(f, _dp), _ptr(out, _dp))
+        return out
+
+    def project_length(self, thetas, field):
+        th = np.ascontiguousarray(thetas, float)
+        f = np.ascontiguousarray(field, float)
+        out = np.zeros((th.size, self.lines))
+        self.orc.L.orc_project_length(C.byref(self.grid._c), self.lines, _ptr(self.src, _dp),
+                                      _ptr(self.det, _dp), th.size, _ptr(th, _dp), _ptr(f, _dp),
+                                      _ptr(out, _dp))
+        return out
+
+    def reconstruct(self, thetas, proj, init=None, beta=0.4, tolerance=1e-6, max_sweeps=100,
+                    f_init=1.0, p_floor=0.0):
+        th = np.ascontiguousarray(thetas, float)
+        p = np.ascontiguousarray(proj, float)
+        if init is None:
+            field = np.full(self.grid.cell_count(), float(f_init))
+        else:
+            field = np.array(init, dtype=np.float64, copy=True)
+        report = np.zeros(6)
+        residuals = np.zeros(max_sweeps)
+        crossed = np.zeros(self.grid.cell_count(), np.uint8)
+        rc = self.orc.L.orc_reconstruct(C.byref(self.grid._c), C.byref(self._c), th.size, _ptr(th, _dp),
+                                        _ptr(p, _dp), _ptr(field, _dp), beta, tolerance, max_sweeps,
+                                        p_floor, _ptr(report, _dp), _ptr(residuals, _dp),
+                                        _ptr(crossed, _u8p))
+        if rc != 0:
+            raise ValueError("invalid reconstruction input")
+        sweeps = int(report[0])
+        rep = dict(sweeps=sweeps, converged=bool(report[1]), all_zero_data=bool(report[2]),
+                   zero_measurement_skips=int(report[3]), factor_clamps=int(report[4]),
+                   updates=int(report[5]),
+                   sweep_residuals=residuals[:sweeps].copy() if tolerance > 0 else np.zeros(0),
+                   crossed=crossed)
+        return field, rep
+
+
+class Ref:
+    """The unmodified reference library (oracle/_ref/libuscg_ref.so)."""
+
+    def __init__(self, path: str = REF_SO):
+        if not os.path.exists(path):
+            raise FileNotFoundError(f"{path} not built (make -C oracle ref needs /root/reference)")
+        L = C.CDLL(path)
+        self.L = L
+        L.ref_last_error.restype = C.c_char_p
+        L.ref_tracer_create.argtypes = [C.c_int, C.c_double, C.c_double, C.c_int, _dp, _dp, C.c_int, C.c_int,
+                                        C.c_double, C.c_double, C.c_int, C.c_int, C.c_int,
+                                        C.POINTER(C.c_void_p)]
+        L.ref_tracer_destroy.argtypes = [C.c_void_p]
+        L.ref_cache_records.argtypes = [C.c_void_p]
+        L.ref_cache_records.restype = C.c_uint64
+        L.ref_cache_bytes.argtypes = [C.c_void_p]
+        L.ref_cache_bytes.restype = C.c_uint64
+        L.ref_cache_lines.argtypes = [C.c_void_p]
+        L.ref_cache_export.argtypes = [C.c_void_p, _u32p, _dp, _dp, _u16p, _u16p]
+        L.ref_trace_line.argtypes = [C.c_void_p, C.c_int, C.c_double, _u32p, C.c_int64, _u64p, _u64p]
+        L.ref_trace_line.restype = C.c_int64
+        L.ref_trace_chord.argtypes = [C.c_int, C.c_double, C.c_double, C.c_int, C.c_double, C.c_double,
+                                      C.c_int, C.c_int, C.c_double, _u32p, C.c_int64]
+        L.ref_trace_chord.restype = C.c_int64
+        L.ref_project_binary.argtypes = [C.c_void_p, _dp, _dp]
+        L.ref_project_length.argtypes = [C.c_void_p, _dp, _dp]
+        L.ref_reconstruct.argtypes = [C.c_void_p, _dp, _dp, C.c_double, C.c_double, C.c_int, C.c_double,
+                                      C.c_double, _dp, _dp, _dp, _u8p]
+        L.ref_mart_update_line.argtypes = [C.c_int, _dp, C.c_int64, _u32p, C.c_int64, C.c_double,
+                                           C.c_double, C.c_double]
+        L.ref_uspg_to_cg_map.argtypes = [C.c_int, _u32p]
+        L.ref_field_to_cartesian.argtypes = [C.c_int, C.c_double, C.c_double, C.c_int, _dp, _dp]
+        L.ref_rmse.argtypes = [C.c_int, C.c_int, _dp, _dp]
+        L.ref_rmse.restype = C.c_double
+        L.ref_ssim.argtypes = [C.c_int, C.c_int, _dp, _dp, C.c_double]
+        L.ref_ssim.restype = C.c_double
+        L.ref_phantom.argtypes = [C.c_int, C.c_double, C.c_double, C.c_int, C.c_int, _dp]
+
+    def check(self, rc):
+        if rc == 1:
+            raise ValueError(self.L.ref_last_error().decode())
+        if rc == 2:
+            raise ArithmeticError(self.L.ref_last_error().decode())
+        if rc:
+            raise RuntimeError(self.L.ref_last_error().decode())
+
+    def tracer(self, n, volume, src, ctr, det_u, det_v, su, sv, views, quarter=False, threads=1):
+        return RefTracer(self, n, volume, src, ctr, det_u, det_v, su, sv, views, quarter, threads)
+
+    def trace_chord(self, n, volume, phi_a, phi_b, slice_, ring, theta):
+        out = np.zeros(4096, np.uint32)
+        k = self.L.ref_trace_chord(n, 2.0 / n, 2.0 / n, int(volume), phi_a, phi_b, slice_, ring, theta,
+                                   _ptr(out, _u32p), out.size)
+        return out[:k].copy()
+
+    def uspg_to_cg_map(self, n):
+        out = np.zeros(n * n, np.uint32)
+        self.check(self.L.ref_uspg_to_cg_map(n, _ptr(out, _u32p)))
+        return out
+
+    def field_to_cartesian(self, n, volume, field):
+        f = np.ascontiguousarray(field, float)
+        slices = n if volume else 1
+        out = np.zeros((slices, n, n))
+        self.check(self.L.ref_field_to_cartesian(n, 2.0 / n, 2.0 / n, int(volume), _ptr(f, _dp), _ptr(out, _dp)))
+        return out
+
+    def phantom(self, n, volume):
+        out = np.zeros((n if volume else 1) * n * n)
+        self.check(self.L.ref_phantom(n, 2.0 / n, 2.0 / n, int(volume), 1 if volume else 0, _ptr(out, _dp)))
+        return out
+
+    def rmse(self, a, b):
+        a = np.ascontiguousarray(a, float); b = np.ascontiguousarray(b, float)
+        return self.L.ref_rmse(a.shape[0], a.shape[1], _ptr(a, _dp), _ptr(b, _dp))
+
+    def ssim(self, a, b, dynamic_range=-1.0):
+        a = np.ascontiguousarray(a, float); b = np.ascontiguousarray(b, float)
+        return self.L.ref_ssim(a.shape[0], a.shape[1], _ptr(a, _dp), _ptr(b, _dp), dynamic_range)
+
+
+class RefTracer:
+    def __init__(self, ref: Ref, n, volume, src, ctr, det_u, det_v, su, sv, views, quarter, threads):
+        self.ref = ref
+        self.n, self.volume, self.views = n, bool(volume), views
+        self.lines = det_u * det_v
+        self.cells = (n if volume else 1) * n * n
+        h = C.c_void_p()
+        s = np.asarray(src, float); c = np.asarray(ctr, float)
+        ref.check(ref.L.ref_tracer_create(n, 2.0 / n, 2.0 / n, int(volume), _ptr(s, _dp), _ptr(c, _dp),
+                                          det_u, det_v, su, sv, views, int(quarter), threads, C.byref(h)))
+        self.h = h
+        self._out = np.zeros(self.cells, np.uint32)
+
+    def __del__(self):
+        try:
+            self.ref.L.ref_tracer_destroy(self.h)
+        except Exception:
+            pass
+
+    def cache(self):
+        n = int(self.ref.L.ref_cache_records(self.h))
+        off = np.zeros(self.lines + 1, np.uint32)
+        pa = np.zeros(n); pb = np.zeros(n)
+        sl = np.zeros(n, np.uint16); rg = np.zeros(n, np.uint16)
+        self.ref.L.ref_cache_export(self.h, _ptr(off, _u32p), _ptr(pa, _dp), _ptr(pb, _dp),
+                                    _ptr(sl, _u16p), _ptr(rg, _u16p))
+        return off, pa, pb, sl, rg
+
+    def cache_bytes(self):
+        return int(self.ref.L.ref_cache_bytes(self.h))
+
+    def trace_line(self, line, theta):
+        n = self.ref.L.ref_trace_line(self.h, line, theta, _ptr(self._out, _u32p), self._out.size, None, None)
+        return self._out[:n].copy()
+
+    def project(self, field):
+        f = np.ascontiguousarray(field, float)
+        out = np.zeros((self.views, self.lines))
+        self.ref.check(self.ref.L.ref_project_binary(self.h, _ptr(f, _dp), _ptr(out, _dp)))
+        return out
+
+    def project_length(self, field):
+        f = np.ascontiguousarray(field, float)
+        out = np.zeros((self.views, self.lines))
+        self.ref.check(self.ref.L.ref_project_length(self.h, _ptr(f, _dp), _ptr(out, _dp)))
+        return out
+
+    def reconstruct(self, proj, init=None, beta=0.4, tolerance=1e-6, max_sweeps=100, f_init=1.0, p_floor=0.0):
+        p = np.ascontiguousarray(proj, float)
+        out = np.zeros(self.cells)
+        report = np.zeros(6)
+        residuals = np.zeros(max_sweeps)
+        crossed = np.zeros(self.cells, np.uint8)
+        i = None if init is None else np.ascontiguousarray(init, float)
+        self.ref.check(self.ref.L.ref_reconstruct(self.h, _ptr(p, _dp), _ptr(i, _dp), beta, tolerance, max_sweeps,
+                                                  f_init, p_floor, _ptr(out, _dp), _ptr(report, _dp),
+                                                  _ptr(residuals, _dp), _ptr(crossed, _u8p)))
+        sweeps = int(report[0])
+        rep = dict(sweeps=sweeps, converged=bool(report[1]), all_zero_data=bool(report[2]), seconds=report[3],
+                   zero_measurement_skips=int(report[4]), factor_clamps=int(report[5]),
+                   sweep_residuals=residuals[:sweeps].copy() if tolerance > 0 else np.zeros(0),
+                   crossed=crossed)
+        return out, rep
+
+
+def ref_thetas(views, span=360.0):
+    """View angles i*span/p (solver.cpp:101,116 uses norm360(view*360/p))."""
+    step = span / views
+    return np.array([view * step for view in range(views)], dtype=np.float64)

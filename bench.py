@@ -1,0 +1,435 @@
+#!/usr/bin/env python
+"""Benchmark: ms per Sp-MART iteration and ray-voxel updates/s on the USPG
+slice stack (BASELINE.json configs[1], "C2"), plus % of the HBM roofline.
+
+A step is one MART iteration (one full sweep over every view and line) of all
+S problems of the stack. `value` is measured on device-resident data with
+CUDA events; `e2e` runs the same step through the C ABI with pinned host
+buffers (projections + field H2D, field D2H inside the timed region).
+
+    python bench.py [--gpus N --steps K --warmup W --config c2 --impl ours|reference]
+
+Multi-GPU (torchrun, one rank per GPU): every rank reconstructs its own stack
+of S slices (weak scaling; slices are independent problems, no collective on
+the data path). Timing = max over ranks of the device time.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+PEAKS_FILE = os.path.join(ROOT, "MEASURED_PEAKS.json")
+TRAFFIC_FILE = os.path.join(ROOT, "profiles", "traffic.json")
+FALLBACK_HBM = 6650.0
+
+
+def hbm_peak():
+    try:
+        with open(PEAKS_FILE) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured"
+    except Exception:
+        return FALLBACK_HBM, "fallback"
+
+
+# ---------------------------------------------------------------------------
+# clocks sampler (nvidia-smi during the timed region)
+# ---------------------------------------------------------------------------
+class Clocks:
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except Exception:
+            self.proc.kill()
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                smax = float(parts[2])
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": smax,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------
+# CPU arm: the oracle restatement (pinned bit-exact to the reference library)
+# ---------------------------------------------------------------------------
+def cpu_run(wl, proj, sample_problems: int, sweeps: int, threads: int):
+    """Run `sample_problems` slices x `sweeps` MART sweeps of the oracle with
+    one slice per host thread; returns (updates/s, wall s, updates, problems)."""
+    import oracle
+
+    orc = oracle.Orc()
+    spec = wl.spec
+    volume = spec.mode.value == 1
+    g = oracle.OrcGrid(spec.rings(), spec.ring_spacing, spec.slices(), spec.slice_height, volume,
+                       None if spec.ring_counts is None else np.asarray(spec.ring_counts, np.uint32))
+    src, det = wl.geom.first_view_rays()
+    cache = orc.cache(g, src, det)
+    th = wl.geom.thetas()
+    caches = [cache] + [orc.cache(g, src, det) for _ in range(min(threads, sample_problems) - 1)]
+    results = [None] * sample_problems
+
+    def work(i, c):
+        f, rep = c.reconstruct(th, proj[i].astype(np.float64), beta=wl.beta, tolerance=0, max_sweeps=sweeps)
+        results[i] = rep["updates"]
+
+    t0 = time.perf_counter()
+    pending = list(range(sample_problems))
+    lock = threading.Lock()
+
+    def worker(c):
+        while True:
+            with lock:
+                if not pending:
+                    return
+                i = pending.pop(0)
+            work(i, c)
+
+    ths = [threading.Thread(target=worker, args=(c,)) for c in caches]
+    for t in ths:
+        t.start()
+    for t in ths:
+        t.join()
+    wall = time.perf_counter() - t0
+    upd = int(sum(results))
+    return upd / wall, wall, upd, len(caches)
+
+
+def ref_lib_analogue(threads: int):
+    """The unmodified reference library on the C2 reference analogue (one
+    slice, one sweep): square_2d(512), flat panel — the closest config it can
+    express."""
+    import oracle
+
+    if not os.path.exists(oracle.REF_SO):
+        return None
+    from paper_2208_12964_b200 import workloads
+    wl = workloads.make("c2-ref", problems=1)
+    ref = oracle.Ref()
+    g = wl.geom
+    rt = ref.tracer(512, False, g.source, g.detector_center, g.det_u, 1, g.spacing_u, 0.0, g.views, False, threads)
+    rng = np.random.default_rng(1)
+    truth = ref.phantom(512, False) * rng.uniform(0.5, 1.0)
+    p = rt.project(truth)
+    t0 = time.perf_counter()
+    f, rep = rt.reconstruct(p, beta=0.05, tolerance=0, max_sweeps=1)
+    wall = time.perf_counter() - t0
+    # U from the trace counters: every non-skipped line's |active|
+    upd = 0
+    th = [v * (360.0 / g.views) for v in range(g.views)]
+    for v in range(g.views):
+        for line in range(g.det_u):
+            if p[v, line] != 0:
+                upd += rt.trace_line(line, th[v]).size
+    return {"value": upd / rep["seconds"], "unit": "updates/s", "cores": 1, "kind": "reference",
+            "sample": "oracle/_ref (unmodified reference) on c2-ref: square_2d(512), flat 512-det fan, 90 views, "
+                      "1 slice x 1 sweep (reconstruct is single-threaded by design)",
+            "seconds": rep["seconds"]}
+
+
+def run_reference(args, rank, world):
+    from paper_2208_12964_b200 import workloads
+
+    if rank != 0:
+        return
+    wl = workloads.make(args.config, problems=args.problems)
+    threads = max(1, os.cpu_count() or 1)
+    S = wl.problems
+    sample = min(S, 2 * threads)
+    truth = workloads.phantom_fields(wl, sample)
+    # projections: binary model of the same tracer, on the CPU oracle
+    import oracle
+    orc = oracle.Orc()
+    spec = wl.spec
+    g = oracle.OrcGrid(spec.rings(), spec.ring_spacing, spec.slices(), spec.slice_height,
+                       spec.mode.value == 1, None if spec.ring_counts is None else spec.counts())
+    src, det = wl.geom.first_view_rays()
+    oc = orc.cache(g, src, det)
+    th = wl.geom.thetas()
+    proj = np.stack([oc.project(th, truth[i].astype(np.float32).astype(np.float64)) for i in range(sample)])
+    proj = workloads.add_noise(wl, proj.astype(np.float32))
+    vals = []
+    for _ in range(args.warmup):
+        cpu_run(wl, proj, sample, 1, threads)
+    walls = []
+    for _ in range(args.steps):
+        v, wall, upd, used = cpu_run(wl, proj, sample, 1, threads)
+        vals.append(v)
+        walls.append(wall)
+    value = float(np.median(vals))
+    # one full iteration of the whole stack at this throughput
+    ms_iter = 1e3 * float(np.median(walls)) * S / sample
+    line = {
+        "impl": "reference", "metric": metric_name(args.config), "value": value, "unit": "updates/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_iter,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic: seeded random-ellipse phantoms, binary projections, 1% Gaussian noise",
+        "config": config_dict(wl, args),
+        "cpu_baseline": {"value": value, "unit": "updates/s", "cores": used, "kind": "port",
+                         "sample": f"{sample} of {S} slices x 1 sweep per step, one slice per host thread "
+                                   f"(oracle C restatement, pinned bit-exact to the reference library; the "
+                                   f"reference cannot express the verbatim config, SURVEY.md §0.1)"},
+        "e2e": {"value": value, "unit": "updates/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def metric_name(config):
+    return f"ray-voxel updates/s per Sp-MART iteration ({config})"
+
+
+def config_dict(wl, args):
+    spec, geom = wl.spec, wl.geom
+    return {"workload": args.config, "problems": wl.problems, "rings": spec.rings(),
+            "sector_law": "reference 4(2k-1)" if spec.ring_counts is None else "round(2*pi*(i+0.5))",
+            "cells_per_slice": spec.cells_per_slice(), "slices": spec.slices(), "views": geom.views,
+            "detectors": [geom.det_u, geom.det_v], "detector": geom.detector.name.lower(), "beta": wl.beta,
+            "iterations_per_reconstruction": wl.sweeps, "l2": "flushed (256 MiB write) before every timed step",
+            "parallelism": f"{wl.problems} independent slices per GPU (weak scaling)"}
+
+
+# ---------------------------------------------------------------------------
+# GPU arm
+# ---------------------------------------------------------------------------
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="c2")
+    ap.add_argument("--problems", type=int, default=None)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_2208_12964_b200 as ub
+    from paper_2208_12964_b200 import uscg, workloads
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    wl = workloads.make(args.config, problems=args.problems)
+    S = wl.problems
+    ctx = ub.Context(local)
+    stream = torch.cuda.current_stream()
+    ctx.set_stream(stream.cuda_stream)
+
+    # ---- precompute (geometry only; reported separately like ReconReport::seconds) ----
+    t0 = time.perf_counter()
+    tracer = ub.Tracer(wl.geom, wl.spec, False, ctx=ctx)
+    torch.cuda.synchronize()
+    t_gen = time.perf_counter() - t0
+    truth = workloads.phantom_fields(wl, S) if rank == 0 or world == 1 else None
+    if truth is None:
+        rng_off = 1000 * rank
+        wl.seed += rng_off
+        truth = workloads.phantom_fields(wl, S)
+    proj = ub.project_stack(tracer, truth.astype(np.float32))
+    proj = workloads.add_noise(wl, proj).astype(np.float32)
+    t0 = time.perf_counter()
+    levels = tracer.build_schedule()
+    t_sched = time.perf_counter() - t0
+    info = tracer.info()
+    counts = tracer.trace_counts().reshape(-1).astype(np.int64)
+    units = counts.size
+    nz = proj.reshape(S, -1) != 0
+    U = int((nz * counts[None, :]).sum())            # ray-voxel updates per iteration
+    Lnz = int(nz.sum())                               # non-skipped (problem, line) pairs
+    C = int(info["chords_per_sweep"])                 # chords traced per iteration (shared by the stack)
+    B = 8 * U + 20 * C + 8 * units + 4 * Lnz         # algorithmic HBM bytes per iteration
+
+    # ---- device-resident state (interleaved, device-native layout) ----
+    Sp = ub.problem_stride(S)
+    cells = info["cell_count"]
+    pin = np.zeros((units, Sp), np.float32)
+    pin[:, :S] = proj.reshape(S, units).T
+    proj_d = torch.from_numpy(pin).cuda()
+    field_d = torch.ones((cells, Sp), dtype=torch.float32, device="cuda")
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
+    L = ub.load()
+    cfg = uscg._Cfg(wl.beta, 0.0, 1, 1.0, 0.0)
+    rep = (uscg._Report * S)()
+    flags = uscg.DEVICE_POINTERS | uscg.LAYOUT_INTERLEAVED
+
+    def step_dev():
+        uscg._check(L.uscg_reconstruct(tracer.h, uscg.C.c_void_p(proj_d.data_ptr()), S, uscg.C.byref(cfg),
+                                       uscg.C.c_void_p(field_d.data_ptr()), 1, rep, flags))
+
+    for _ in range(args.warmup):
+        step_dev()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clocks = Clocks(local)
+    clocks.start()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    launches0 = ub.launch_count()
+    mart_s = 0.0
+    torch.cuda.synchronize()
+    for k in range(args.steps):
+        flush.fill_(float(k))
+        ev[k][0].record(stream)
+        step_dev()
+        ev[k][1].record(stream)
+        mart_s += rep[0].seconds
+    torch.cuda.synchronize()
+    launches = ub.launch_count() - launches0
+    clk = clocks.stop()
+    t_ms = float(sum(a.elapsed_time(b) for a, b in ev))
+    if world > 1:
+        tt = torch.tensor([t_ms, mart_s], device="cuda", dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t_ms, mart_s = float(tt[0]), float(tt[1])
+    ms_per_step = t_ms / args.steps
+    value = U * world / (ms_per_step * 1e-3)
+
+    # ---- e2e through the C ABI with pinned host buffers ----
+    e2e = None
+    if not args.no_e2e:
+        proj_h = torch.from_numpy(proj.reshape(S, units).copy()).pin_memory()
+        field_h = torch.ones((S, cells), dtype=torch.float32).pin_memory()
+        e2e_flags = 0
+
+        def step_e2e():
+            uscg._check(L.uscg_reconstruct(tracer.h, uscg.C.c_void_p(proj_h.data_ptr()), S, uscg.C.byref(cfg),
+                                           uscg.C.c_void_p(field_h.data_ptr()), 1, rep, e2e_flags))
+
+        step_e2e()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        ee = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+              for _ in range(args.steps)]
+        for k in range(args.steps):
+            flush.fill_(float(k))
+            ee[k][0].record(stream)
+            step_e2e()
+            ee[k][1].record(stream)
+        torch.cuda.synchronize()
+        te = float(sum(a.elapsed_time(b) for a, b in ee))
+        if world > 1:
+            tt = torch.tensor([te], device="cuda", dtype=torch.float64)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            te = float(tt[0])
+        e2e = {"value": U * world / (te / args.steps * 1e-3), "unit": "updates/s",
+               "ms_per_step": te / args.steps,
+               "h2d_bytes_per_step": int(proj_h.numel() * 4 + field_h.numel() * 4),
+               "d2h_bytes_per_step": int(field_h.numel() * 4)}
+
+    if rank != 0:
+        if world > 1:
+            dist.barrier()
+            dist.destroy_process_group()
+        return
+
+    peak, peak_kind = hbm_peak()
+    t_mart = mart_s / args.steps  # graph replay of all dependency levels, CUDA events on the launching stream
+    achieved = B / t_mart / 1e9
+    traffic = None
+    try:
+        with open(TRAFFIC_FILE) as f:
+            tj = json.load(f)
+        if tj.get("config") == args.config:
+            traffic = tj.get("dram_bytes_per_launch")
+    except Exception:
+        pass
+    roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                "traffic": traffic, "peak_kind": peak_kind, "kernel": "mart_level_kernel<32,1024>",
+                "algorithmic_bytes_per_iteration": B, "launches_per_iteration": levels,
+                "avg_launch_us": 1e6 * t_mart / max(levels, 1),
+                "bytes_model": "8*U + 20*C + 8*(views*lines) + 4*L_nonzero (DESIGN.md §5)"}
+
+    cpu = None
+    if not args.no_cpu and world == 1:
+        threads = max(1, os.cpu_count() or 1)
+        sample = min(S, 2 * threads)
+        v, wall, upd, used = cpu_run(wl, proj, sample, 1, threads)
+        cpu = {"value": v, "unit": "updates/s", "cores": used, "kind": "port",
+               "sample": f"{sample} of {S} slices x 1 sweep, one slice per host thread ({wall:.1f} s wall); "
+                         f"oracle C restatement (bit-exact to the reference library on its configs)"}
+        try:
+            ra = ref_lib_analogue(1)
+            if ra:
+                cpu["reference_lib_analogue"] = ra
+        except Exception as e:  # the reference build is optional on the box
+            cpu["reference_lib_analogue"] = {"error": str(e)[:200]}
+
+    line = {
+        "metric": metric_name(args.config), "value": value, "unit": "updates/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic: seeded random-ellipse phantoms per slice, binary projections, 1% Gaussian noise",
+        "config": config_dict(wl, args),
+        "ms_per_iteration": ms_per_step, "updates_per_iteration": U * world, "chords_per_iteration": C,
+        "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
+        "clocks": clk,
+        "precompute": {"generator_s": t_gen, "schedule_s": t_sched, "levels_per_iteration": levels,
+                       "records": info["records"], "cache_bytes": info["cache_bytes"]},
+    }
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,203 @@
+/*
+ * uscg_b200 — C ABI of the B200-native USPG/USCG MART hot path.
+ *
+ * This is the drop-in boundary for the reference library's reconstruction
+ * path (/root/reference/proj, C++ namespace uscg). Plain pointers and sizes,
+ * no C++ or torch types; every entry point names the reference interface it
+ * replaces. The C++ mirror of the reference API (include/uscg_b200.hpp) and
+ * the Python mirror (paper_2208_12964_b200/uscg.py) sit on top of it.
+ *
+ * Conventions
+ *  - Status codes mirror the reference's exception types:
+ *      USCG_ERR_INVALID_ARGUMENT  <-> std::invalid_argument
+ *      USCG_ERR_DOMAIN            <-> std::domain_error
+ *    uscg_last_error() returns the message of the last failure on this thread.
+ *  - All calls are blocking and run on the context's stream (its own, or one
+ *    set with uscg_ctx_set_stream). Handles are not thread-safe (as the
+ *    reference's TraceScratch).
+ *  - The tracer owns its device-resident first-view cache; the caller owns
+ *    every buffer passed in. Buffers are host memory unless
+ *    USCG_DEVICE_POINTERS is set, in which case they are device memory.
+ *  - "problems": S independent reconstructions sharing one tracer (the
+ *    BASELINE 2D slice stack). Host-layout fields are problem-major
+ *    ([S][cell_count], each the reference flat order); host-layout
+ *    projections are [S][views][lines] (reference ProjectionSet order).
+ *    USCG_LAYOUT_INTERLEAVED selects the device-native layouts instead:
+ *    field [cell_count][S_pad], projections [views*lines][S_pad]
+ *    (S_pad from uscg_problem_stride).
+ *  - There is no CPU fallback: without a usable sm_100 device every compute
+ *    call fails with USCG_ERR_NO_DEVICE.
+ */
+#ifndef USCG_B200_H
+#define USCG_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    USCG_OK = 0,
+    USCG_ERR_INVALID_ARGUMENT = 1, /* std::invalid_argument in the reference */
+    USCG_ERR_DOMAIN = 2,           /* std::domain_error in the reference */
+    USCG_ERR_CUDA = 3,
+    USCG_ERR_NO_DEVICE = 4,
+    USCG_ERR_ALLOC = 5
+} uscg_status;
+
+enum {
+    USCG_DEVICE_POINTERS = 1u,     /* buffers are device memory */
+    USCG_LAYOUT_INTERLEAVED = 2u   /* device-native problem-minor layouts */
+};
+
+typedef struct uscg_ctx_s* uscg_ctx;
+typedef struct uscg_tracer_s* uscg_tracer;
+
+/* GridSpec (proj/include/uscg/grid.hpp:21-44), generalized at two seams:
+ * ring_counts (any sector law; NULL = the reference's 4(2k-1),
+ * proj/src/grid.cpp:18-22) and n_slices decoupled from the ring count. */
+typedef struct {
+    int32_t n_rings;
+    double ring_spacing;
+    int32_t n_slices;      /* 1 for a 2D grid */
+    double slice_height;
+    int32_t volume;        /* 0 = GridMode::Slice2D, 1 = GridMode::Volume3D */
+    const uint32_t* ring_counts;
+} uscg_grid;
+
+typedef enum {
+    USCG_DET_FLAT = 0,     /* ScanGeometry flat panel (proj/src/scan.cpp:27-36) */
+    USCG_DET_ARC = 1,      /* equiangular arc about the source; spacing_u in degrees */
+    USCG_DET_PARALLEL = 2  /* parallel beam: source and detector both shift along u */
+} uscg_detector;
+
+/* ScanGeometry (proj/include/uscg/scan.hpp:21-41) plus the detector kind and
+ * an optional view-angle list (NULL = view*360/views, proj/src/solver.cpp:101,116). */
+typedef struct {
+    int32_t detector;
+    double source[3];
+    double detector_center[3];
+    int32_t det_u, det_v;
+    double spacing_u, spacing_v;
+    int32_t views;
+    const double* view_angles_deg;
+} uscg_scan;
+
+/* SolverConfig (proj/include/uscg/solver.hpp:34-41) */
+typedef struct {
+    double beta;        /* in (0, 2) */
+    double tolerance;   /* <= 0 runs every sweep */
+    int32_t max_sweeps;
+    double f_init;
+    double p_floor;     /* <= 0: 1e-12 * mean nonzero measurement, per problem */
+} uscg_solver_config;
+
+/* ReconReport (proj/include/uscg/solver.hpp:43-52), one per problem.
+ * sweep_residuals (max_sweeps doubles) and crossed (cell_count bytes) are
+ * caller-owned and optional (NULL skips them). */
+typedef struct {
+    int32_t sweeps;
+    int32_t converged;
+    int32_t all_zero_data;
+    double seconds;                  /* device time of the sweeps (CUDA events) */
+    uint64_t zero_measurement_skips;
+    uint64_t factor_clamps;
+    uint64_t updates;                /* ray-voxel updates applied (U) */
+    double* sweep_residuals;
+    uint8_t* crossed;
+} uscg_report;
+
+typedef struct {
+    int32_t lines, views;
+    int32_t n_rings, n_slices;
+    uint64_t records;              /* chord records in the first-view cache */
+    uint64_t cells_per_slice;
+    uint64_t cell_count;
+    uint64_t cache_bytes;          /* device bytes of the record store + offsets */
+    int32_t max_line_records;
+    int32_t max_line_cells;        /* over every (view, line) */
+    uint64_t cells_per_sweep;      /* sum of |active| over every (view, line) */
+    uint64_t chords_per_sweep;     /* records * views */
+    int32_t levels;                /* MART dependency levels per sweep (0 until built) */
+} uscg_tracer_info;
+
+const char* uscg_last_error(void);
+const char* uscg_version(void);
+/* number of kernels this library has launched in the process */
+uint64_t uscg_launch_count(void);
+
+/* ---- context ----------------------------------------------------------- */
+uscg_status uscg_ctx_create(int32_t device, uscg_ctx* out);
+uscg_status uscg_ctx_destroy(uscg_ctx ctx);
+/* run on an external stream (a cudaStream_t passed as void*); NULL restores
+ * the context's own stream */
+uscg_status uscg_ctx_set_stream(uscg_ctx ctx, void* stream);
+uscg_status uscg_ctx_synchronize(uscg_ctx ctx);
+
+/* ---- rays --------------------------------------------------------------- */
+/* First-view line endpoints (ScanGeometry::line_endpoints, proj/src/scan.cpp:38-42):
+ * src_out/det_out hold lines*3 doubles, line = iv*det_u + iu. Host only. */
+uscg_status uscg_first_view_rays(const uscg_scan* scan, double* src_out, double* det_out);
+
+/* ---- tracer: FirstViewCache + Tracer (proj/include/uscg/tracer.hpp:18-105) */
+/* Tracer(geom, spec, quarter_symmetry, threads) (tracer.hpp:87) — the cache is
+ * generated on the device (K1). quarter_symmetry is validated like
+ * precompute_first_view (tracer.cpp:42-44) and yields the identical cache. */
+uscg_status uscg_tracer_create(uscg_ctx ctx, const uscg_grid* grid, const uscg_scan* scan,
+                               int32_t quarter_symmetry, uscg_tracer* out);
+/* Same, from explicit first-view rays (the ray-generator seam). */
+uscg_status uscg_tracer_create_from_rays(uscg_ctx ctx, const uscg_grid* grid, int32_t lines,
+                                         const double* src, const double* det, int32_t views,
+                                         const double* view_angles_deg, uscg_tracer* out);
+/* Adopt an existing FirstViewCache (offsets lines+1, records SoA). */
+uscg_status uscg_tracer_import_cache(uscg_ctx ctx, const uscg_grid* grid, int32_t lines,
+                                     const uint32_t* offsets, uint64_t records,
+                                     const double* phi_a, const double* phi_b,
+                                     const uint16_t* slice, const uint16_t* ring, int32_t views,
+                                     const double* view_angles_deg, uscg_tracer* out);
+uscg_status uscg_tracer_destroy(uscg_tracer tracer);
+uscg_status uscg_tracer_get_info(uscg_tracer tracer, uscg_tracer_info* info);
+/* FirstViewCache::offsets()/records() (tracer.hpp:28-29) to host arrays */
+uscg_status uscg_tracer_export_cache(uscg_tracer tracer, uint32_t* offsets, double* phi_a,
+                                     double* phi_b, uint16_t* slice, uint16_t* ring);
+/* Tracer::trace_line (tracer.cpp:148-201): deduplicated active cells of one
+ * line at theta, in the reference's emission order, computed on the device by
+ * the same trace the solver uses. *count receives the full count; at most cap
+ * indices are written. */
+uscg_status uscg_trace_line(uscg_tracer tracer, int32_t line, double theta_deg, uint32_t* out,
+                            int64_t cap, int64_t* count);
+/* |active| of every line of every view, views*lines u32 (TraceScratch::cells). */
+uscg_status uscg_trace_counts(uscg_tracer tracer, uint32_t* cells_out);
+/* Build the MART dependency schedule now (otherwise built on first use). */
+uscg_status uscg_tracer_build_schedule(uscg_tracer tracer);
+/* stride of the interleaved problem dimension for S problems */
+int32_t uscg_problem_stride(int32_t problems);
+
+/* ---- forward model: generate_projections Binary (proj/src/phantom.cpp:182-211) */
+uscg_status uscg_project(uscg_tracer tracer, const float* field, int32_t problems, float* proj_out,
+                         uint32_t flags);
+
+/* ---- Sp-MART: reconstruct / reconstruct_from (proj/src/solver.cpp:76-177) -----
+ * from_init = 0: field_inout is output only and starts at cfg->f_init
+ * (reconstruct); 1: field_inout holds the initial field (reconstruct_from,
+ * must be > 0). reports: `problems` entries (may be NULL). */
+uscg_status uscg_reconstruct(uscg_tracer tracer, const float* proj, int32_t problems,
+                             const uscg_solver_config* cfg, float* field_inout, int32_t from_init,
+                             uscg_report* reports, uint32_t flags);
+
+/* ---- resampling: uspg_to_cg_map + field_to_cartesian (proj/src/grid.cpp:75-99,
+ * proj/src/phantom.cpp:149-163). Output [S][slices][npix][npix], row 0 at the
+ * bottom. Reference law with npix = 2*n_rings: the reference permutation;
+ * any other law / size: the bin-point rule of proj/tests/oracles.hpp:36-58 at
+ * pixel centres (pixels outside the disc -> 0). */
+uscg_status uscg_resample(uscg_ctx ctx, const uscg_grid* grid, const float* field,
+                          int32_t problems, int32_t npix, float* out, uint32_t flags);
+/* uspg_to_cg_map(n) itself (grid.hpp:84), n*n u32, host output. */
+uscg_status uscg_uspg_to_cg_map(uscg_ctx ctx, int32_t n, uint32_t* out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* USCG_B200_H */

@@ -1,0 +1,20 @@
+"""B200-native USPG/USCG Sp-MART hot path (arXiv 2208.12964).
+
+The product is ``lib/libuscg_b200.so``: hand-written sm_100a CUDA kernels behind
+the C ABI declared in ``include/uscg_b200.h``. :mod:`.uscg` mirrors the
+reference library's reconstruction API on top of that ABI.
+"""
+from .uscg import (  # noqa: F401
+    Context, Detector, DomainError, Field, FirstViewCache, GridMode, GridSpec, InvalidArgument, NoDevice,
+    ProjectionSet, ReconReport, ReconResult, ScanGeometry, SolverConfig, Tracer, field_to_cartesian,
+    generate_projections, launch_count, load, problem_stride, project_stack, reconstruct, reconstruct_from,
+    reconstruct_stack, resample_stack, ring_counts_m1, uspg_to_cg_map,
+)
+
+__all__ = [
+    "Context", "Detector", "DomainError", "Field", "FirstViewCache", "GridMode", "GridSpec", "InvalidArgument",
+    "NoDevice", "ProjectionSet", "ReconReport", "ReconResult", "ScanGeometry", "SolverConfig", "Tracer",
+    "field_to_cartesian", "generate_projections", "launch_count", "load", "problem_stride", "project_stack",
+    "reconstruct", "reconstruct_from", "reconstruct_stack", "resample_stack", "ring_counts_m1",
+    "uspg_to_cg_map",
+]

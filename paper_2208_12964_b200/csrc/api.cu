@@ -1,0 +1,1078 @@
+// C ABI of uscg_b200 (include/uscg_b200.h): host orchestration in C++.
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/uscg_b200.h"
+#include "kernels.h"
+#include "schedule.h"
+
+namespace ub {
+
+namespace {
+thread_local std::string g_last_error;
+std::atomic<uint64_t> g_launches{0};
+
+struct InvalidArgument : std::invalid_argument {
+    using std::invalid_argument::invalid_argument;
+};
+struct DomainError : std::domain_error {
+    using std::domain_error::domain_error;
+};
+
+double norm360(double deg) {  // geometry.cpp:48-55
+    deg = std::fmod(deg, 360.0);
+    if (deg < 0)
+        deg += 360.0;
+    if (deg >= 360.0)
+        deg = 0.0;
+    return deg;
+}
+
+template <class T>
+struct DevBuf {
+    T* p = nullptr;
+    size_t n = 0;
+    DevBuf() = default;
+    DevBuf(const DevBuf&) = delete;
+    DevBuf& operator=(const DevBuf&) = delete;
+    ~DevBuf() { release(); }
+    void release() {
+        if (p)
+            cudaFree(p);
+        p = nullptr;
+        n = 0;
+    }
+    void alloc(size_t count) {
+        if (count == n && p)
+            return;
+        release();
+        if (count == 0)
+            return;
+        cudaError_t e = cudaMalloc(&p, count * sizeof(T));
+        if (e != cudaSuccess) {
+            p = nullptr;
+            throw CudaError(std::string("cudaMalloc ") + std::to_string(count * sizeof(T)) +
+                            " bytes: " + cudaGetErrorString(e));
+        }
+        n = count;
+    }
+    void ensure(size_t count) {
+        if (count > n)
+            alloc(count);
+    }
+};
+}  // namespace
+
+void count_launch(uint64_t n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+void set_error(const std::string& msg) { g_last_error = msg; }
+
+}  // namespace ub
+
+using namespace ub;
+
+struct uscg_ctx_s {
+    int device = 0;
+    cudaStream_t own = nullptr;
+    cudaStream_t stream = nullptr;
+};
+
+struct GraphCache {
+    cudaGraphExec_t exec = nullptr;
+    int Sp = 0, nchunks = 0;
+    uint32_t nodes = 0;
+    ~GraphCache() {
+        if (exec)
+            cudaGraphExecDestroy(exec);
+    }
+};
+
+struct uscg_tracer_s {
+    uscg_ctx ctx = nullptr;
+    int device = 0;
+    // grid
+    int n_rings = 0, n_slices = 1, volume = 0;
+    double ring_spacing = 0, slice_height = 0;
+    std::vector<uint32_t> counts;
+    std::vector<RingRow> rings;  // index = ring
+    uint32_t cps = 0;
+    uint64_t cells = 0;
+    // scan
+    int lines = 0, views = 0;
+    std::vector<double> thetas;
+    uint64_t records = 0;
+    int max_recs = 0, max_cells = 0;
+    std::vector<uint32_t> h_cells;  // per unit
+    uint64_t cells_per_sweep = 0;
+    // device
+    DevBuf<RingRow> d_rings;
+    DevBuf<uint32_t> d_off;
+    DevBuf<double> d_pa, d_pb;
+    DevBuf<uint32_t> d_key;
+    DevBuf<double> d_theta;
+    DevBuf<uint32_t> d_cells;
+    DevBuf<uint8_t> d_crossed;
+    bool crossed_built = false;
+    // schedule
+    bool sched_built = false;
+    std::vector<uint32_t> level_off;
+    DevBuf<uint32_t> d_order;
+    double schedule_seconds = 0;
+    // MART workspace
+    DevBuf<MartArgs> d_args;
+    DevBuf<float> w_field, w_proj, w_prev, w_stage;
+    DevBuf<double> w_pfloor, w_stats;
+    DevBuf<uint8_t> w_active;
+    DevBuf<unsigned long long> w_clamps, w_updates, w_tmp;
+    DevBuf<unsigned int> w_resid;
+    GraphCache graph;
+
+    DevGrid dev_grid() const {
+        DevGrid g;
+        g.n_rings = n_rings;
+        g.n_slices = volume ? n_slices : 1;
+        g.volume = volume;
+        g.ring_spacing = ring_spacing;
+        g.slice_height = slice_height;
+        g.radius = 0.5 * (2 * n_rings) * ring_spacing;
+        g.eps = 1e-9 * g.radius;
+        const double z_extent = volume ? n_slices * slice_height : slice_height;
+        g.zoff = 0.5 * z_extent;
+        g.cells_per_slice = cps;
+        g.rings = d_rings.p;
+        return g;
+    }
+    TraceArgs trace_args() const {
+        TraceArgs a;
+        a.off = d_off.p;
+        a.pa = d_pa.p;
+        a.pb = d_pb.p;
+        a.key = d_key.p;
+        a.rings = d_rings.p;
+        a.theta = d_theta.p;
+        a.cells_per_slice = cps;
+        a.lines = lines;
+        return a;
+    }
+    cudaStream_t st() const { return ctx->stream; }
+    uint64_t units() const { return uint64_t(lines) * uint64_t(views); }
+};
+
+namespace {
+
+template <class F>
+uscg_status guarded(F&& f) {
+    try {
+        f();
+        return USCG_OK;
+    } catch (const InvalidArgument& e) {
+        set_error(e.what());
+        return USCG_ERR_INVALID_ARGUMENT;
+    } catch (const DomainError& e) {
+        set_error(e.what());
+        return USCG_ERR_DOMAIN;
+    } catch (const NoDevice& e) {
+        set_error(e.what());
+        return USCG_ERR_NO_DEVICE;
+    } catch (const CudaError& e) {
+        set_error(e.what());
+        return USCG_ERR_CUDA;
+    } catch (const std::bad_alloc& e) {
+        set_error("host allocation failed");
+        return USCG_ERR_ALLOC;
+    } catch (const std::exception& e) {
+        set_error(e.what());
+        return USCG_ERR_CUDA;
+    }
+}
+
+void need(bool cond, const char* msg) {
+    if (!cond)
+        throw InvalidArgument(msg);
+}
+
+void bind(uscg_ctx ctx) {
+    need(ctx != nullptr, "null context");
+    UB_CUDA(cudaSetDevice(ctx->device));
+}
+
+// GridSpec::validate (grid.cpp:9-16) on the generalized grid
+void validate_grid(const uscg_grid* g) {
+    need(g != nullptr, "null grid");
+    if (g->n_rings < 1)
+        throw InvalidArgument("grid size must be an even integer >= 2, got " +
+                              std::to_string(2 * g->n_rings));
+    need(g->n_rings <= kMaxRings, "at most 4095 rings are supported");
+    need(g->ring_spacing > 0, "ring spacing must be positive");
+    need(g->slice_height > 0, "slice height must be positive");
+    if (g->volume)
+        need(g->n_slices >= 1 && g->n_slices <= kMaxSlices, "slice count out of range");
+    if (g->ring_counts)
+        for (int k = 0; k < g->n_rings; ++k)
+            need(g->ring_counts[k] >= 1 && g->ring_counts[k] <= 4096,
+                 "ring sector counts must lie in [1, 4096]");
+}
+
+// ScanGeometry::validate (scan.cpp:9-24)
+void validate_scan(const uscg_scan* s) {
+    need(s != nullptr, "null scan");
+    need(s->views >= 1, "number of views must be >= 1");
+    need(s->det_u >= 1 && s->det_v >= 1, "detector counts must be >= 1");
+    need(s->spacing_u > 0, "detector spacing must be positive");
+    need(!(s->det_v > 1 && !(s->spacing_v > 0)), "detector row spacing must be positive");
+    need(s->detector >= USCG_DET_FLAT && s->detector <= USCG_DET_PARALLEL, "unknown detector kind");
+    const double dot = s->source[0] * s->detector_center[0] + s->source[1] * s->detector_center[1];
+    need(dot < 0, "source and detector must sit on opposite sides of the origin");
+    const double ax = s->detector_center[0] - s->source[0];
+    const double ay = s->detector_center[1] - s->source[1];
+    need(!(ax * ax + ay * ay == 0), "central ray must not be axial");
+}
+
+void fill_grid(uscg_tracer_s* t, const uscg_grid* g) {
+    t->n_rings = g->n_rings;
+    t->ring_spacing = g->ring_spacing;
+    t->n_slices = g->volume ? g->n_slices : 1;
+    t->slice_height = g->slice_height;
+    t->volume = g->volume ? 1 : 0;
+    t->counts.resize(g->n_rings);
+    for (int k = 1; k <= g->n_rings; ++k)
+        t->counts[k - 1] = g->ring_counts ? g->ring_counts[k - 1] : uint32_t(4 * (2 * k - 1));
+    t->rings.assign(size_t(g->n_rings) + 1, RingRow{0, 0, 0});
+    uint64_t head = 0;
+    for (int k = 1; k <= g->n_rings; ++k) {
+        RingRow& r = t->rings[k];
+        r.count = t->counts[k - 1];
+        r.head = uint32_t(head);
+        r.inv_step = r.count / 360.0;  // grid.cpp:68
+        head += r.count;
+    }
+    need(head * uint64_t(t->n_slices) < (1ull << 32), "cell count must fit in 32 bits");
+    t->cps = uint32_t(head);
+    t->cells = head * uint64_t(t->n_slices);
+    t->d_rings.alloc(t->rings.size());
+    UB_CUDA(cudaMemcpy(t->d_rings.p, t->rings.data(), sizeof(RingRow) * t->rings.size(),
+                       cudaMemcpyHostToDevice));
+}
+
+void fill_views(uscg_tracer_s* t, int views, const double* angles) {
+    need(views >= 1, "number of views must be >= 1");
+    t->views = views;
+    t->thetas.resize(views);
+    const double step = 360.0 / views;  // ScanGeometry::step_deg
+    for (int v = 0; v < views; ++v)
+        t->thetas[v] = norm360(angles ? angles[v] : v * step);
+    t->d_theta.alloc(views);
+    UB_CUDA(cudaMemcpy(t->d_theta.p, t->thetas.data(), sizeof(double) * views,
+                       cudaMemcpyHostToDevice));
+}
+
+// max records per line, per-unit cell counts, cells per sweep
+void finish_tracer(uscg_tracer_s* t, const std::vector<uint32_t>& off) {
+    t->max_recs = 0;
+    for (int l = 0; l < t->lines; ++l)
+        t->max_recs = std::max<int>(t->max_recs, int(off[l + 1] - off[l]));
+    launch_annotate(t->lines, t->d_off.p, t->d_pa.p, t->d_pb.p, t->d_key.p, t->d_rings.p, t->st());
+    const uint64_t units = t->units();
+    need(units < (1ull << 32), "views * lines must fit in 32 bits");
+    t->d_cells.alloc(units);
+    launch_trace_counts(t->trace_args(), t->views, t->max_recs, t->d_cells.p, t->st());
+    t->h_cells.resize(units);
+    UB_CUDA(cudaMemcpyAsync(t->h_cells.data(), t->d_cells.p, sizeof(uint32_t) * units,
+                            cudaMemcpyDeviceToHost, t->st()));
+    UB_CUDA(cudaStreamSynchronize(t->st()));
+    t->max_cells = 1;
+    t->cells_per_sweep = 0;
+    for (uint32_t c : t->h_cells) {
+        t->max_cells = std::max<int>(t->max_cells, int(c));
+        t->cells_per_sweep += c;
+    }
+}
+
+void first_view_rays(const uscg_scan* s, double* src, double* det) {
+    // ScanGeometry::detector_position (scan.cpp:27-36); the arc and parallel
+    // generators reuse its in-plane u direction
+    const double ax = s->detector_center[0] - s->source[0];
+    const double ay = s->detector_center[1] - s->source[1];
+    const double alen = std::sqrt(ax * ax + ay * ay);
+    const double ux = -ay / alen;
+    const double uy = ax / alen;
+    const double pi = 3.141592653589793238462643383279502884;
+    for (int iv = 0; iv < s->det_v; ++iv)
+        for (int iu = 0; iu < s->det_u; ++iu) {
+            const size_t l = size_t(iv) * s->det_u + iu;
+            const double du = (iu - 0.5 * (s->det_u - 1)) * s->spacing_u;
+            const double dv = (iv - 0.5 * (s->det_v - 1)) * s->spacing_v;
+            double* o = src + 3 * l;
+            double* q = det + 3 * l;
+            o[0] = s->source[0];
+            o[1] = s->source[1];
+            o[2] = s->source[2];
+            if (s->detector == USCG_DET_FLAT) {
+                q[0] = s->detector_center[0] + du * ux;
+                q[1] = s->detector_center[1] + du * uy;
+                q[2] = s->detector_center[2] + dv;
+            } else if (s->detector == USCG_DET_ARC) {
+                // element iu at angle du (degrees) from the central ray, on
+                // the circle about the source through the detector centre
+                const double a0 = std::atan2(ay, ax);
+                const double g = a0 + du * (pi / 180.0);
+                q[0] = s->source[0] + alen * std::cos(g);
+                q[1] = s->source[1] + alen * std::sin(g);
+                q[2] = s->detector_center[2] + dv;
+            } else {
+                o[0] = s->source[0] + du * ux;
+                o[1] = s->source[1] + du * uy;
+                o[2] = s->source[2] + dv;
+                q[0] = s->detector_center[0] + du * ux;
+                q[1] = s->detector_center[1] + du * uy;
+                q[2] = s->detector_center[2] + dv;
+            }
+        }
+}
+
+uscg_tracer_s* build_from_rays(uscg_ctx ctx, const uscg_grid* grid, int lines, const double* src,
+                               const double* det, int views, const double* angles) {
+    validate_grid(grid);
+    need(lines >= 1, "line count must be >= 1");
+    need(src && det, "null ray arrays");
+    std::unique_ptr<uscg_tracer_s> t(new uscg_tracer_s);
+    t->ctx = ctx;
+    t->device = ctx->device;
+    fill_grid(t.get(), grid);
+    fill_views(t.get(), views, angles);
+    t->lines = lines;
+    DevBuf<double> d_rays;
+    d_rays.alloc(size_t(lines) * 6);
+    UB_CUDA(cudaMemcpyAsync(d_rays.p, src, sizeof(double) * 3 * lines, cudaMemcpyHostToDevice,
+                            t->st()));
+    UB_CUDA(cudaMemcpyAsync(d_rays.p + 3 * size_t(lines), det, sizeof(double) * 3 * lines,
+                            cudaMemcpyHostToDevice, t->st()));
+    const DevGrid g = t->dev_grid();
+    DevBuf<uint32_t> d_cnt;
+    d_cnt.alloc(size_t(lines));
+    launch_generate_count(g, lines, d_rays.p, d_rays.p + 3 * size_t(lines), d_cnt.p, t->st());
+    t->d_off.alloc(size_t(lines) + 1);
+    launch_exclusive_scan_u32(d_cnt.p, t->d_off.p, lines, t->st());
+    std::vector<uint32_t> off(size_t(lines) + 1);
+    UB_CUDA(cudaMemcpyAsync(off.data(), t->d_off.p, sizeof(uint32_t) * (lines + 1),
+                            cudaMemcpyDeviceToHost, t->st()));
+    UB_CUDA(cudaStreamSynchronize(t->st()));
+    t->records = off[lines];
+    const size_t R = std::max<size_t>(t->records, 1);
+    t->d_pa.alloc(R);
+    t->d_pb.alloc(R);
+    t->d_key.alloc(R);
+    launch_generate_write(g, lines, d_rays.p, d_rays.p + 3 * size_t(lines), t->d_off.p, t->d_pa.p,
+                          t->d_pb.p, t->d_key.p, t->st());
+    finish_tracer(t.get(), off);
+    return t.release();
+}
+
+void ensure_crossed(uscg_tracer_s* t) {
+    if (t->crossed_built)
+        return;
+    t->d_crossed.alloc(t->cells);
+    UB_CUDA(cudaMemsetAsync(t->d_crossed.p, 0, t->cells, t->st()));
+    launch_crossed(t->trace_args(), t->views, t->max_recs, t->max_cells, t->d_crossed.p, t->st());
+    t->crossed_built = true;
+}
+
+void build_schedule(uscg_tracer_s* t) {
+    if (t->sched_built)
+        return;
+    cudaEvent_t e0, e1;
+    UB_CUDA(cudaEventCreate(&e0));
+    UB_CUDA(cudaEventCreate(&e1));
+    const auto h0 = std::chrono::steady_clock::now();
+    AsapSchedule sched(t->cells);
+    const uint64_t units = t->units();
+    const uint64_t batch_cells = 1ull << 25;  // 128 MiB of indices per batch
+    std::vector<uint32_t> pos;
+    std::vector<uint32_t> idx;
+    DevBuf<uint32_t> d_pos, d_idx;
+    uint64_t u0 = 0;
+    while (u0 < units) {
+        uint64_t u1 = u0, tot = 0;
+        while (u1 < units && (u1 == u0 || tot + t->h_cells[u1] <= batch_cells)) {
+            tot += t->h_cells[u1];
+            ++u1;
+        }
+        const uint32_t n = uint32_t(u1 - u0);
+        pos.resize(size_t(n) + 1);
+        pos[0] = 0;
+        for (uint32_t i = 0; i < n; ++i)
+            pos[i + 1] = pos[i] + t->h_cells[u0 + i];
+        d_pos.ensure(pos.size());
+        d_idx.ensure(std::max<uint64_t>(tot, 1));
+        UB_CUDA(cudaMemcpyAsync(d_pos.p, pos.data(), sizeof(uint32_t) * pos.size(),
+                                cudaMemcpyHostToDevice, t->st()));
+        launch_trace_dump(t->trace_args(), uint32_t(u0), n, t->max_recs, t->max_cells, d_pos.p,
+                          d_idx.p, t->st());
+        idx.resize(std::max<uint64_t>(tot, 1));
+        UB_CUDA(cudaMemcpyAsync(idx.data(), d_idx.p, sizeof(uint32_t) * tot, cudaMemcpyDeviceToHost,
+                                t->st()));
+        UB_CUDA(cudaStreamSynchronize(t->st()));
+        sched.add(idx.data(), pos.data(), n);
+        u0 = u1;
+    }
+    std::vector<uint32_t> order;
+    sched.finish(order, t->level_off);
+    t->d_order.alloc(std::max<size_t>(order.size(), 1));
+    UB_CUDA(cudaMemcpy(t->d_order.p, order.data(), sizeof(uint32_t) * order.size(),
+                       cudaMemcpyHostToDevice));
+    t->sched_built = true;
+    t->schedule_seconds =
+        std::chrono::duration<double>(std::chrono::steady_clock::now() - h0).count();
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+}
+
+// One sweep = one graph replay: every dependency level is a kernel node.
+void ensure_graph(uscg_tracer_s* t, const MartArgs& h) {
+    GraphCache& G = t->graph;
+    if (G.exec && G.Sp == h.Sp && G.nchunks == h.nchunks)
+        return;
+    if (G.exec) {
+        cudaGraphExecDestroy(G.exec);
+        G.exec = nullptr;
+    }
+    mart_prepare(h);
+    cudaStream_t cap;
+    UB_CUDA(cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking));
+    UB_CUDA(cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal));
+    const uint32_t levels = uint32_t(t->level_off.size()) - 1;
+    for (uint32_t l = 0; l < levels; ++l) {
+        const uint32_t b = t->level_off[l], e = t->level_off[l + 1];
+        launch_mart_level(t->d_args.p, h, t->d_order.p + b, int(e - b), cap);
+    }
+    g_launches.fetch_sub(levels);  // captured, not launched
+    cudaGraph_t graph;
+    UB_CUDA(cudaStreamEndCapture(cap, &graph));
+    cudaError_t e = cudaGraphInstantiate(&G.exec, graph, 0);
+    cudaGraphDestroy(graph);
+    cudaStreamDestroy(cap);
+    if (e != cudaSuccess)
+        throw CudaError(std::string("cudaGraphInstantiate: ") + cudaGetErrorString(e));
+    G.Sp = h.Sp;
+    G.nchunks = h.nchunks;
+    G.nodes = levels;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* uscg_last_error(void) { return g_last_error.c_str(); }
+const char* uscg_version(void) { return "uscg_b200 0.1 (sm_100a)"; }
+uint64_t uscg_launch_count(void) { return g_launches.load(); }
+
+int32_t uscg_problem_stride(int32_t problems) { return problems < 1 ? 0 : problem_stride(problems); }
+
+uscg_status uscg_ctx_create(int32_t device, uscg_ctx* out) {
+    return guarded([&] {
+        need(out != nullptr, "null output");
+        int n = 0;
+        if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0) {
+            cudaGetLastError();
+            throw NoDevice("no CUDA device: the uscg_b200 path runs on sm_100 only (no CPU fallback)");
+        }
+        need(device >= 0 && device < n, "device index out of range");
+        cudaDeviceProp prop;
+        UB_CUDA(cudaGetDeviceProperties(&prop, device));
+        if (prop.major != 10)
+            throw NoDevice(std::string("device ") + prop.name + " is not sm_100 (Blackwell B200)");
+        UB_CUDA(cudaSetDevice(device));
+        auto* c = new uscg_ctx_s;
+        c->device = device;
+        cudaError_t e = cudaStreamCreateWithFlags(&c->own, cudaStreamNonBlocking);
+        if (e != cudaSuccess) {
+            delete c;
+            throw CudaError(cudaGetErrorString(e));
+        }
+        c->stream = c->own;
+        *out = c;
+    });
+}
+
+uscg_status uscg_ctx_destroy(uscg_ctx ctx) {
+    return guarded([&] {
+        if (!ctx)
+            return;
+        cudaSetDevice(ctx->device);
+        if (ctx->own)
+            cudaStreamDestroy(ctx->own);
+        delete ctx;
+    });
+}
+
+uscg_status uscg_ctx_set_stream(uscg_ctx ctx, void* stream) {
+    return guarded([&] {
+        need(ctx != nullptr, "null context");
+        ctx->stream = stream ? static_cast<cudaStream_t>(stream) : ctx->own;
+    });
+}
+
+uscg_status uscg_ctx_synchronize(uscg_ctx ctx) {
+    return guarded([&] {
+        bind(ctx);
+        UB_CUDA(cudaStreamSynchronize(ctx->stream));
+    });
+}
+
+uscg_status uscg_first_view_rays(const uscg_scan* scan, double* src_out, double* det_out) {
+    return guarded([&] {
+        validate_scan(scan);
+        need(src_out && det_out, "null output");
+        first_view_rays(scan, src_out, det_out);
+    });
+}
+
+uscg_status uscg_tracer_create(uscg_ctx ctx, const uscg_grid* grid, const uscg_scan* scan,
+                               int32_t quarter_symmetry, uscg_tracer* out) {
+    return guarded([&] {
+        bind(ctx);
+        need(out != nullptr, "null output");
+        validate_scan(scan);
+        validate_grid(grid);
+        if (quarter_symmetry) {
+            // precompute_first_view (tracer.cpp:42-44): the mirrored build is
+            // bit-identical to the direct one, so only the validation differs
+            const bool ok = scan->det_u % 2 == 1 && scan->det_v % 2 == 1 && scan->source[1] == 0 &&
+                            scan->source[2] == 0 && scan->detector_center[1] == 0 &&
+                            scan->detector_center[2] == 0;
+            need(ok, "quarter symmetry requires odd detector counts with source and detector "
+                     "center on the x axis");
+        }
+        const int lines = scan->det_u * scan->det_v;
+        std::vector<double> src(size_t(lines) * 3), det(size_t(lines) * 3);
+        first_view_rays(scan, src.data(), det.data());
+        *out = build_from_rays(ctx, grid, lines, src.data(), det.data(), scan->views,
+                               scan->view_angles_deg);
+    });
+}
+
+uscg_status uscg_tracer_create_from_rays(uscg_ctx ctx, const uscg_grid* grid, int32_t lines,
+                                         const double* src, const double* det, int32_t views,
+                                         const double* view_angles_deg, uscg_tracer* out) {
+    return guarded([&] {
+        bind(ctx);
+        need(out != nullptr, "null output");
+        *out = build_from_rays(ctx, grid, lines, src, det, views, view_angles_deg);
+    });
+}
+
+uscg_status uscg_tracer_import_cache(uscg_ctx ctx, const uscg_grid* grid, int32_t lines,
+                                     const uint32_t* offsets, uint64_t records,
+                                     const double* phi_a, const double* phi_b,
+                                     const uint16_t* slice, const uint16_t* ring, int32_t views,
+                                     const double* view_angles_deg, uscg_tracer* out) {
+    return guarded([&] {
+        bind(ctx);
+        need(out != nullptr, "null output");
+        validate_grid(grid);
+        need(lines >= 1 && offsets, "line count must be >= 1");
+        need(offsets[0] == 0 && offsets[lines] == records, "offsets do not match the record count");
+        for (int l = 0; l < lines; ++l)
+            need(offsets[l] <= offsets[l + 1], "offsets must be non-decreasing");
+        std::unique_ptr<uscg_tracer_s> t(new uscg_tracer_s);
+        t->ctx = ctx;
+        t->device = ctx->device;
+        fill_grid(t.get(), grid);
+        fill_views(t.get(), views, view_angles_deg);
+        t->lines = lines;
+        t->records = records;
+        std::vector<uint32_t> key(std::max<uint64_t>(records, 1));
+        for (uint64_t i = 0; i < records; ++i) {
+            need(ring[i] >= 1 && ring[i] <= t->n_rings, "record ring out of range");
+            need(slice[i] < t->n_slices, "record slice out of range");
+            key[i] = uint32_t(ring[i]) | (uint32_t(slice[i]) << kSliceShift);
+        }
+        std::vector<uint32_t> off(offsets, offsets + lines + 1);
+        const size_t R = std::max<size_t>(records, 1);
+        t->d_off.alloc(size_t(lines) + 1);
+        t->d_pa.alloc(R);
+        t->d_pb.alloc(R);
+        t->d_key.alloc(R);
+        UB_CUDA(cudaMemcpy(t->d_off.p, off.data(), sizeof(uint32_t) * off.size(),
+                           cudaMemcpyHostToDevice));
+        if (records) {
+            UB_CUDA(cudaMemcpy(t->d_pa.p, phi_a, sizeof(double) * records, cudaMemcpyHostToDevice));
+            UB_CUDA(cudaMemcpy(t->d_pb.p, phi_b, sizeof(double) * records, cudaMemcpyHostToDevice));
+            UB_CUDA(cudaMemcpy(t->d_key.p, key.data(), sizeof(uint32_t) * records,
+                               cudaMemcpyHostToDevice));
+        }
+        finish_tracer(t.get(), off);
+        *out = t.release();
+    });
+}
+
+uscg_status uscg_tracer_destroy(uscg_tracer tracer) {
+    return guarded([&] {
+        if (!tracer)
+            return;
+        cudaSetDevice(tracer->device);
+        cudaDeviceSynchronize();
+        delete tracer;
+    });
+}
+
+uscg_status uscg_tracer_get_info(uscg_tracer t, uscg_tracer_info* info) {
+    return guarded([&] {
+        need(t && info, "null argument");
+        info->lines = t->lines;
+        info->views = t->views;
+        info->n_rings = t->n_rings;
+        info->n_slices = t->n_slices;
+        info->records = t->records;
+        info->cells_per_slice = t->cps;
+        info->cell_count = t->cells;
+        info->cache_bytes = t->records * 20 + (uint64_t(t->lines) + 1) * 4;
+        info->max_line_records = t->max_recs;
+        info->max_line_cells = t->max_cells;
+        info->cells_per_sweep = t->cells_per_sweep;
+        info->chords_per_sweep = t->records * uint64_t(t->views);
+        info->levels = t->sched_built ? int32_t(t->level_off.size()) - 1 : 0;
+    });
+}
+
+uscg_status uscg_tracer_export_cache(uscg_tracer t, uint32_t* offsets, double* phi_a,
+                                     double* phi_b, uint16_t* slice, uint16_t* ring) {
+    return guarded([&] {
+        need(t != nullptr, "null tracer");
+        bind(t->ctx);
+        std::vector<uint32_t> key(t->records);
+        if (offsets)
+            UB_CUDA(cudaMemcpy(offsets, t->d_off.p, sizeof(uint32_t) * (t->lines + 1),
+                               cudaMemcpyDeviceToHost));
+        if (t->records == 0)
+            return;
+        if (phi_a)
+            UB_CUDA(cudaMemcpy(phi_a, t->d_pa.p, sizeof(double) * t->records, cudaMemcpyDeviceToHost));
+        if (phi_b)
+            UB_CUDA(cudaMemcpy(phi_b, t->d_pb.p, sizeof(double) * t->records, cudaMemcpyDeviceToHost));
+        UB_CUDA(cudaMemcpy(key.data(), t->d_key.p, sizeof(uint32_t) * t->records,
+                           cudaMemcpyDeviceToHost));
+        for (uint64_t i = 0; i < t->records; ++i) {
+            if (ring)
+                ring[i] = uint16_t(key[i] & kRingMask);
+            if (slice)
+                slice[i] = uint16_t((key[i] >> kSliceShift) & kSliceMask);
+        }
+    });
+}
+
+uscg_status uscg_trace_line(uscg_tracer t, int32_t line, double theta_deg, uint32_t* out,
+                            int64_t cap, int64_t* count) {
+    return guarded([&] {
+        need(t != nullptr, "null tracer");
+        bind(t->ctx);
+        need(line >= 0 && line < t->lines, "line index out of range");
+        // rotation changes a chord's sector count by at most one
+        const int max_cells = t->max_cells + t->max_recs + 1;
+        DevBuf<uint32_t> d_out;
+        d_out.alloc(size_t(max_cells) + 1);
+        launch_trace_one(t->trace_args(), line, norm360(theta_deg), t->max_recs, max_cells,
+                         d_out.p, d_out.p + max_cells, t->st());
+        uint32_t n = 0;
+        UB_CUDA(cudaMemcpyAsync(&n, d_out.p + max_cells, sizeof(uint32_t), cudaMemcpyDeviceToHost,
+                                t->st()));
+        UB_CUDA(cudaStreamSynchronize(t->st()));
+        if (count)
+            *count = n;
+        const int64_t m = std::min<int64_t>(n, cap);
+        if (m > 0 && out)
+            UB_CUDA(cudaMemcpy(out, d_out.p, sizeof(uint32_t) * m, cudaMemcpyDeviceToHost));
+    });
+}
+
+uscg_status uscg_trace_counts(uscg_tracer t, uint32_t* cells_out) {
+    return guarded([&] {
+        need(t && cells_out, "null argument");
+        std::memcpy(cells_out, t->h_cells.data(), sizeof(uint32_t) * t->h_cells.size());
+    });
+}
+
+uscg_status uscg_tracer_build_schedule(uscg_tracer t) {
+    return guarded([&] {
+        need(t != nullptr, "null tracer");
+        bind(t->ctx);
+        build_schedule(t);
+    });
+}
+
+uscg_status uscg_project(uscg_tracer t, const float* field, int32_t problems, float* proj_out,
+                         uint32_t flags) {
+    return guarded([&] {
+        need(t != nullptr, "null tracer");
+        bind(t->ctx);
+        need(problems >= 1, "problem count must be >= 1");
+        need(field && proj_out, "null buffer");
+        const int S = problems, Sp = problem_stride(S);
+        const bool dev = flags & USCG_DEVICE_POINTERS;
+        const bool inter = flags & USCG_LAYOUT_INTERLEAVED;
+        const uint64_t units = t->units();
+        cudaStream_t st = t->st();
+        const float* d_field = nullptr;
+        if (dev && (inter || S == 1)) {
+            d_field = field;
+        } else {
+            t->w_field.ensure(t->cells * Sp);
+            t->w_stage.ensure(std::max<uint64_t>(units * S, t->cells * S));
+            if (inter) {
+                UB_CUDA(cudaMemcpyAsync(t->w_field.p, field, sizeof(float) * t->cells * Sp,
+                                        cudaMemcpyHostToDevice, st));
+            } else if (S == 1) {
+                UB_CUDA(cudaMemcpyAsync(t->w_field.p, field, sizeof(float) * t->cells,
+                                        dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, st));
+            } else {
+                const float* src = field;
+                if (!dev) {
+                    UB_CUDA(cudaMemcpyAsync(t->w_stage.p, field, sizeof(float) * t->cells * S,
+                                            cudaMemcpyHostToDevice, st));
+                    src = t->w_stage.p;
+                }
+                launch_to_interleaved(src, t->w_field.p, t->cells, S, Sp, 0.f, st);
+            }
+            d_field = t->w_field.p;
+        }
+        float* d_out = nullptr;
+        const bool direct_out = dev && (inter || S == 1);
+        if (direct_out) {
+            d_out = proj_out;
+        } else {
+            t->w_proj.ensure(units * Sp);
+            d_out = t->w_proj.p;
+        }
+        launch_project(t->trace_args(), t->views, d_field, Sp, t->max_recs, t->max_cells, d_out, st);
+        if (!direct_out) {
+            if (inter || S == 1) {
+                UB_CUDA(cudaMemcpyAsync(proj_out, d_out, sizeof(float) * units * Sp,
+                                        dev ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, st));
+            } else {
+                float* dst = proj_out;
+                if (!dev) {
+                    t->w_stage.ensure(std::max<uint64_t>(units * S, t->cells * S));
+                    dst = t->w_stage.p;
+                }
+                launch_from_interleaved(d_out, dst, units, S, Sp, st);
+                if (!dev)
+                    UB_CUDA(cudaMemcpyAsync(proj_out, dst, sizeof(float) * units * S,
+                                            cudaMemcpyDeviceToHost, st));
+            }
+        }
+        UB_CUDA(cudaStreamSynchronize(st));
+    });
+}
+
+uscg_status uscg_reconstruct(uscg_tracer t, const float* proj, int32_t problems,
+                             const uscg_solver_config* cfg, float* field_inout, int32_t from_init,
+                             uscg_report* reports, uint32_t flags) {
+    return guarded([&] {
+        need(t != nullptr, "null tracer");
+        bind(t->ctx);
+        need(cfg != nullptr, "null config");
+        need(proj && field_inout, "null buffer");
+        need(problems >= 1, "problem count must be >= 1");
+        // validate_config (solver.cpp:55-61)
+        need(cfg->beta > 0 && cfg->beta < 2, "relaxation must lie in (0, 2)");
+        need(cfg->f_init > 0, "initial field value must be positive");
+        need(cfg->max_sweeps >= 1, "sweep budget must be >= 1");
+        const int S = problems, Sp = problem_stride(S), P = chunk_width(S);
+        const bool dev = flags & USCG_DEVICE_POINTERS;
+        const bool inter = flags & USCG_LAYOUT_INTERLEAVED;
+        const uint64_t units = t->units();
+        const uint64_t cells = t->cells;
+        cudaStream_t st = t->st();
+
+        // ---- projections -> device [units][Sp] ----
+        const float* d_proj = nullptr;
+        if (dev && (inter || S == 1)) {
+            d_proj = proj;
+        } else {
+            t->w_proj.ensure(units * Sp);
+            if (inter || S == 1) {
+                UB_CUDA(cudaMemcpyAsync(t->w_proj.p, proj, sizeof(float) * units * Sp,
+                                        dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, st));
+            } else {
+                const float* src = proj;
+                if (!dev) {
+                    t->w_stage.ensure(std::max<uint64_t>(units * S, cells * S));
+                    UB_CUDA(cudaMemcpyAsync(t->w_stage.p, proj, sizeof(float) * units * S,
+                                            cudaMemcpyHostToDevice, st));
+                    src = t->w_stage.p;
+                }
+                launch_to_interleaved(src, t->w_proj.p, units, S, Sp, 0.f, st);
+            }
+            d_proj = t->w_proj.p;
+        }
+
+        // ---- ProjectionSet::validate + auto_p_floor + all-zero check ----
+        t->w_stats.ensure(size_t(4) * Sp);
+        UB_CUDA(cudaMemsetAsync(t->w_stats.p, 0, sizeof(double) * 4 * Sp, st));
+        launch_proj_stats(d_proj, int(units), S, Sp, t->w_stats.p, st);
+        std::vector<double> stats(size_t(4) * Sp);
+        UB_CUDA(cudaMemcpyAsync(stats.data(), t->w_stats.p, sizeof(double) * 4 * Sp,
+                                cudaMemcpyDeviceToHost, st));
+
+        // ---- field -> device [cells][Sp] ----
+        float* d_field = nullptr;
+        const bool direct_field = dev && (inter || S == 1);
+        if (direct_field) {
+            d_field = field_inout;
+        } else {
+            t->w_field.ensure(cells * Sp);
+            d_field = t->w_field.p;
+        }
+        if (from_init) {
+            if (!direct_field) {
+                if (inter || S == 1) {
+                    UB_CUDA(cudaMemcpyAsync(d_field, field_inout, sizeof(float) * cells * Sp,
+                                            dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
+                                            st));
+                } else {
+                    const float* src = field_inout;
+                    if (!dev) {
+                        t->w_stage.ensure(std::max<uint64_t>(units * S, cells * S));
+                        UB_CUDA(cudaMemcpyAsync(t->w_stage.p, field_inout, sizeof(float) * cells * S,
+                                                cudaMemcpyHostToDevice, st));
+                        src = t->w_stage.p;
+                    }
+                    launch_to_interleaved(src, d_field, cells, S, Sp, 1.f, st);
+                }
+            }
+            t->w_tmp.ensure(1);
+            UB_CUDA(cudaMemsetAsync(t->w_tmp.p, 0, sizeof(unsigned long long), st));
+            launch_count_nonpositive(d_field, cells * Sp, t->w_tmp.p, st);
+            unsigned long long bad = 0;
+            UB_CUDA(cudaMemcpyAsync(&bad, t->w_tmp.p, sizeof(bad), cudaMemcpyDeviceToHost, st));
+            UB_CUDA(cudaStreamSynchronize(st));
+            need(bad == 0, "initial field must be strictly positive");
+        } else {
+            launch_fill(d_field, cells * Sp, float(cfg->f_init), st);
+        }
+        UB_CUDA(cudaStreamSynchronize(st));
+        std::vector<double> p_floor(Sp, 1e-12);
+        std::vector<uint8_t> active(Sp, 0);
+        std::vector<int> all_zero(S, 0);
+        for (int p = 0; p < S; ++p) {
+            if (stats[4 * p + 3] > 0)
+                throw InvalidArgument("projection data contains a non-finite or negative measurement");
+            const double cnt = stats[4 * p + 0], sum = stats[4 * p + 1];
+            p_floor[p] = cfg->p_floor > 0 ? cfg->p_floor : (cnt == 0 ? 1e-12 : 1e-12 * (sum / cnt));
+            all_zero[p] = stats[4 * p + 2] == 0;
+            active[p] = !all_zero[p];
+        }
+
+        build_schedule(t);
+        const bool track = cfg->tolerance > 0;
+        if (track || reports)
+            ensure_crossed(t);
+
+        // ---- per-problem updates per sweep (U counter) ----
+        t->w_updates.ensure(Sp);
+        UB_CUDA(cudaMemsetAsync(t->w_updates.p, 0, sizeof(unsigned long long) * Sp, st));
+        launch_sweep_updates(d_proj, t->d_cells.p, int(units), S, Sp, t->w_updates.p, st);
+        std::vector<unsigned long long> upd(Sp);
+        UB_CUDA(cudaMemcpyAsync(upd.data(), t->w_updates.p, sizeof(unsigned long long) * Sp,
+                                cudaMemcpyDeviceToHost, st));
+
+        t->w_pfloor.ensure(Sp);
+        t->w_active.ensure(Sp);
+        t->w_clamps.ensure(Sp);
+        UB_CUDA(cudaMemcpyAsync(t->w_pfloor.p, p_floor.data(), sizeof(double) * Sp,
+                                cudaMemcpyHostToDevice, st));
+        UB_CUDA(cudaMemcpyAsync(t->w_active.p, active.data(), Sp, cudaMemcpyHostToDevice, st));
+        UB_CUDA(cudaMemsetAsync(t->w_clamps.p, 0, sizeof(unsigned long long) * Sp, st));
+
+        MartArgs h;
+        h.tr = t->trace_args();
+        h.field = d_field;
+        h.proj = d_proj;
+        h.p_floor = t->w_pfloor.p;
+        h.active = t->w_active.p;
+        h.clamps = t->w_clamps.p;
+        h.beta = cfg->beta;
+        h.Sp = Sp;
+        h.nchunks = Sp / P;
+        h.max_recs = t->max_recs;
+        h.max_cells = t->max_cells;
+        t->d_args.ensure(1);
+        UB_CUDA(cudaMemcpyAsync(t->d_args.p, &h, sizeof(MartArgs), cudaMemcpyHostToDevice, st));
+        ensure_graph(t, h);
+
+        std::vector<int> sweeps(S, 0), converged(S, 0);
+        std::vector<std::vector<double>> resid(S);
+        if (track)
+            t->w_prev.ensure(cells * Sp), t->w_resid.ensure(Sp);
+        int n_active = 0;
+        for (int p = 0; p < S; ++p)
+            n_active += active[p];
+        cudaEvent_t e0, e1;
+        UB_CUDA(cudaEventCreate(&e0));
+        UB_CUDA(cudaEventCreate(&e1));
+        UB_CUDA(cudaEventRecord(e0, st));
+        for (int sweep = 0; sweep < cfg->max_sweeps && n_active > 0; ++sweep) {
+            if (track)
+                UB_CUDA(cudaMemcpyAsync(t->w_prev.p, d_field, sizeof(float) * cells * Sp,
+                                        cudaMemcpyDeviceToDevice, st));
+            UB_CUDA(cudaGraphLaunch(t->graph.exec, st));
+            count_launch(t->graph.nodes);
+            for (int p = 0; p < S; ++p)
+                sweeps[p] += active[p];
+            if (track) {
+                UB_CUDA(cudaMemsetAsync(t->w_resid.p, 0, sizeof(unsigned int) * Sp, st));
+                launch_residual(d_field, t->w_prev.p, t->d_crossed.p, cells, S, Sp, t->w_resid.p, st);
+                std::vector<unsigned int> bits(Sp);
+                UB_CUDA(cudaMemcpyAsync(bits.data(), t->w_resid.p, sizeof(unsigned int) * Sp,
+                                        cudaMemcpyDeviceToHost, st));
+                UB_CUDA(cudaStreamSynchronize(st));
+                bool changed = false;
+                for (int p = 0; p < S; ++p) {
+                    if (!active[p])
+                        continue;
+                    float r;
+                    std::memcpy(&r, &bits[p], sizeof(r));
+                    resid[p].push_back(double(r));
+                    if (double(r) <= cfg->tolerance) {
+                        converged[p] = 1;
+                        active[p] = 0;
+                        --n_active;
+                        changed = true;
+                    }
+                }
+                if (changed)
+                    UB_CUDA(cudaMemcpyAsync(t->w_active.p, active.data(), Sp, cudaMemcpyHostToDevice,
+                                            st));
+            }
+        }
+        UB_CUDA(cudaEventRecord(e1, st));
+
+        // ---- field back ----
+        if (!direct_field) {
+            if (inter || S == 1) {
+                UB_CUDA(cudaMemcpyAsync(field_inout, d_field, sizeof(float) * cells * Sp,
+                                        dev ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, st));
+            } else {
+                float* dst = field_inout;
+                if (!dev) {
+                    t->w_stage.ensure(std::max<uint64_t>(units * S, cells * S));
+                    dst = t->w_stage.p;
+                }
+                launch_from_interleaved(d_field, dst, cells, S, Sp, st);
+                if (!dev)
+                    UB_CUDA(cudaMemcpyAsync(field_inout, dst, sizeof(float) * cells * S,
+                                            cudaMemcpyDeviceToHost, st));
+            }
+        }
+        std::vector<unsigned long long> clamps(Sp);
+        UB_CUDA(cudaMemcpyAsync(clamps.data(), t->w_clamps.p, sizeof(unsigned long long) * Sp,
+                                cudaMemcpyDeviceToHost, st));
+        UB_CUDA(cudaStreamSynchronize(st));
+        float ms = 0;
+        UB_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+
+        if (reports) {
+            std::vector<uint8_t> crossed;
+            bool need_crossed = false;
+            for (int p = 0; p < S; ++p)
+                need_crossed |= reports[p].crossed != nullptr;
+            if (need_crossed) {
+                crossed.resize(cells);
+                UB_CUDA(cudaMemcpy(crossed.data(), t->d_crossed.p, cells, cudaMemcpyDeviceToHost));
+            }
+            for (int p = 0; p < S; ++p) {
+                uscg_report& r = reports[p];
+                r.sweeps = sweeps[p];
+                r.converged = converged[p];
+                r.all_zero_data = all_zero[p];
+                r.seconds = ms * 1e-3;
+                r.factor_clamps = clamps[p];
+                r.updates = uint64_t(upd[p]) * uint64_t(sweeps[p]);
+                // zero-measurement lines are skipped in every sweep (solver.cpp:119-127)
+                r.zero_measurement_skips = uint64_t(double(units) - stats[4 * p + 0]) * uint64_t(sweeps[p]);
+                if (r.sweep_residuals)
+                    for (size_t i = 0; i < resid[p].size(); ++i)
+                        r.sweep_residuals[i] = resid[p][i];
+                if (r.crossed) {
+                    if (all_zero[p])
+                        std::memset(r.crossed, 0, cells);
+                    else
+                        std::memcpy(r.crossed, crossed.data(), cells);
+                }
+            }
+        }
+    });
+}
+
+uscg_status uscg_resample(uscg_ctx ctx, const uscg_grid* grid, const float* field,
+                          int32_t problems, int32_t npix, float* out, uint32_t flags) {
+    return guarded([&] {
+        bind(ctx);
+        validate_grid(grid);
+        need(field && out, "null buffer");
+        need(problems >= 1, "problem count must be >= 1");
+        need(npix >= 2 && npix % 2 == 0, "image size must be even");
+        std::unique_ptr<uscg_tracer_s> t(new uscg_tracer_s);
+        t->ctx = ctx;
+        fill_grid(t.get(), grid);
+        const int S = problems;
+        const bool dev = flags & USCG_DEVICE_POINTERS;
+        const bool inter = flags & USCG_LAYOUT_INTERLEAVED;
+        const int Sp = inter ? problem_stride(S) : 0;
+        const int slices = t->n_slices;
+        const uint64_t in_n = t->cells * uint64_t(inter ? Sp : S);
+        const uint64_t out_n = uint64_t(npix) * npix * slices * S;
+        cudaStream_t st = ctx->stream;
+        DevBuf<float> d_in, d_out;
+        const float* fin = field;
+        if (!dev) {
+            d_in.alloc(in_n);
+            UB_CUDA(cudaMemcpyAsync(d_in.p, field, sizeof(float) * in_n, cudaMemcpyHostToDevice, st));
+            fin = d_in.p;
+        }
+        float* fout = out;
+        if (!dev) {
+            d_out.alloc(out_n);
+            fout = d_out.p;
+        }
+        const bool perm = grid->ring_counts == nullptr && npix == 2 * grid->n_rings;
+        if (perm) {
+            launch_perm_resample(fin, t->cps, slices, S, Sp, npix, fout, st);
+        } else {
+            DevBuf<uint32_t> map;
+            map.alloc(size_t(npix) * npix);
+            launch_bin_map(t->dev_grid(), npix, map.p, st);
+            launch_map_resample(fin, t->cps, slices, S, Sp, map.p, npix, fout, st);
+            UB_CUDA(cudaStreamSynchronize(st));
+        }
+        if (!dev)
+            UB_CUDA(cudaMemcpyAsync(out, fout, sizeof(float) * out_n, cudaMemcpyDeviceToHost, st));
+        UB_CUDA(cudaStreamSynchronize(st));
+    });
+}
+
+uscg_status uscg_uspg_to_cg_map(uscg_ctx ctx, int32_t n, uint32_t* out) {
+    return guarded([&] {
+        bind(ctx);
+        if (n < 2 || n % 2 != 0)  // grid.cpp:76-77
+            throw DomainError("image size must be even, got " + std::to_string(n));
+        need(out != nullptr, "null output");
+        DevBuf<uint32_t> d;
+        d.alloc(size_t(n) * n);
+        launch_cg_map(n, d.p, ctx->stream);
+        UB_CUDA(cudaMemcpyAsync(out, d.p, sizeof(uint32_t) * n * n, cudaMemcpyDeviceToHost,
+                                ctx->stream));
+        UB_CUDA(cudaStreamSynchronize(ctx->stream));
+    });
+}
+
+}  // extern "C"

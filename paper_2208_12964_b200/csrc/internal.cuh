@@ -1,0 +1,301 @@
+// Internal declarations shared by the uscg_b200 translation units.
+//
+// Device data layout:
+//   ring table   RingRow[n_rings + 1] {count u32, head u32, inv_step f64}, index = ring (1-based)
+//   record store SoA: phi_a f64[R], phi_b f64[R], key u32[R]
+//                key = ring (bits 0-11) | slice (bits 12-30) | dedup-check flag (bit 31)
+//   offsets      u32[lines + 1]
+//   thetas       f64[views], norm360 already applied (solver.cpp:116)
+//   field        f32 [cell_count][S_pad]  (problem-minor; S_pad = 1 for a single volume)
+//   projections  f32 [views*lines][S_pad]
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/uscg_b200.h"
+
+namespace ub {
+
+struct RingRow {
+    uint32_t count;
+    uint32_t head;
+    double inv_step;
+};
+
+constexpr uint32_t kRingMask = 0xFFFu;
+constexpr uint32_t kSliceShift = 12;
+constexpr uint32_t kSliceMask = 0x7FFFFu;
+constexpr uint32_t kFlagBit = 0x80000000u;
+constexpr int kMaxRings = 4095;
+constexpr int kMaxSlices = 0x7FFFF;
+
+struct DevGrid {
+    int n_rings;
+    int n_slices;  // 1 in 2D
+    int volume;
+    double ring_spacing;
+    double slice_height;
+    double radius;  // 0.5 * n * ring_spacing, n = 2 * n_rings (grid.hpp:31)
+    double eps;     // 1e-9 * radius (geometry.cpp:29)
+    double zoff;    // 0.5 * z_extent (grid.hpp:32-34)
+    uint32_t cells_per_slice;
+    const RingRow* rings;
+};
+
+// Everything a block-level trace needs.
+struct TraceArgs {
+    const uint32_t* off;
+    const double* pa;
+    const double* pb;
+    const uint32_t* key;
+    const RingRow* rings;
+    const double* theta;  // per view
+    uint32_t cells_per_slice;
+    int lines;
+};
+
+// ---- launch bookkeeping ------------------------------------------------------
+void count_launch(uint64_t n = 1);
+void set_error(const std::string& msg);
+
+#define UB_CUDA(expr)                                                                     \
+    do {                                                                                  \
+        cudaError_t _e = (expr);                                                          \
+        if (_e != cudaSuccess)                                                            \
+            throw ::ub::CudaError(std::string(#expr) + ": " + cudaGetErrorString(_e));    \
+    } while (0)
+
+struct CudaError : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+struct NoDevice : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+
+// ---- device helpers ------------------------------------------------------------
+
+// Tracer::trace_line per-chord rotation (tracer.cpp:160-172): add theta, one
+// -360 wrap, scale by inv_step, truncate, clamp to ng-1. The seam test is
+// |a - b| <= 180 (tracer.cpp:176). Compiled with --fmad=false so every
+// operation rounds exactly as the reference's.
+__device__ __forceinline__ void rotate_chord(double pa, double pb, double theta, uint32_t count,
+                                             double inv_step, int& lo, int& hi, bool& seam) {
+    const int ng = static_cast<int>(count);
+    double a = pa + theta;
+    if (a >= 360.0)
+        a -= 360.0;
+    double b = pb + theta;
+    if (b >= 360.0)
+        b -= 360.0;
+    int ga = static_cast<int>(a * inv_step);
+    if (ga >= ng)
+        ga = ng - 1;
+    int gb = static_cast<int>(b * inv_step);
+    if (gb >= ng)
+        gb = ng - 1;
+    lo = ga < gb ? ga : gb;
+    hi = ga < gb ? gb : ga;
+    seam = !(fabs(a - b) <= 180.0);
+}
+
+__device__ __forceinline__ bool range_has(int q, int lo, int hi, bool seam) {
+    return seam ? (q >= hi || q <= lo) : (q >= lo && q <= hi);
+}
+
+// per-record smem packing: lohi = lo | hi << 12 | seam << 24 ; cnt = count | ng << 16
+__device__ __forceinline__ uint32_t pack_lohi(int lo, int hi, bool seam, bool flag) {
+    return uint32_t(lo) | (uint32_t(hi) << 12) | (uint32_t(seam) << 24) | (uint32_t(flag) << 25);
+}
+__device__ __forceinline__ int lohi_lo(uint32_t v) { return int(v & 0xFFFu); }
+__device__ __forceinline__ int lohi_hi(uint32_t v) { return int((v >> 12) & 0xFFFu); }
+__device__ __forceinline__ bool lohi_seam(uint32_t v) { return (v >> 24) & 1u; }
+__device__ __forceinline__ bool lohi_flag(uint32_t v) { return (v >> 25) & 1u; }
+
+// Block-wide exclusive scan of a[0..n) in place; a[n] receives the total.
+// s_warp must hold NT/32 words. All threads must call it.
+template <int NT>
+__device__ __forceinline__ void block_exclusive_scan(uint32_t* a, int n, uint32_t* s_warp) {
+    constexpr int NW = NT / 32;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int per = (n + NT - 1) / NT;
+    const int beg = min(n, int(threadIdx.x) * per);
+    const int end = min(n, beg + per);
+    uint32_t sum = 0;
+    for (int i = beg; i < end; ++i)
+        sum += a[i];
+    uint32_t x = sum;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, x, o);
+        if (lane >= o)
+            x += y;
+    }
+    if (lane == 31)
+        s_warp[warp] = x;
+    __syncthreads();
+    if (warp == 0) {
+        uint32_t w = lane < NW ? s_warp[lane] : 0u;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, w, o);
+            if (lane >= o)
+                w += y;
+        }
+        if (lane < NW)
+            s_warp[lane] = w;
+    }
+    __syncthreads();
+    uint32_t excl = x - sum + (warp > 0 ? s_warp[warp - 1] : 0u);
+    for (int i = beg; i < end; ++i) {
+        const uint32_t v = a[i];
+        a[i] = excl;
+        excl += v;
+    }
+    if (threadIdx.x == 0)
+        a[n] = s_warp[NW - 1];
+    __syncthreads();
+}
+
+struct TraceSmem {
+    uint32_t* base;  // max_recs
+    uint32_t* lohi;  // max_recs
+    uint32_t* cnt;   // max_recs: count | ng << 16
+    uint32_t* pos;   // max_recs + 1
+    uint32_t* warp;  // NT / 32
+    uint32_t* idx;   // max_cells
+};
+
+// Number of cells of record i not already covered by an earlier record of the
+// same (slice, ring) in this line — the TraceScratch stamp dedup
+// (tracer.cpp:181-195) restricted to the only records that can collide.
+__device__ __forceinline__ uint32_t dedup_count(const TraceSmem& S, int i, int ng) {
+    const uint32_t b = S.base[i];
+    const uint32_t v = S.lohi[i];
+    const int lo = lohi_lo(v), hi = lohi_hi(v);
+    const bool seam = lohi_seam(v);
+    uint32_t c = 0;
+    auto visit = [&](int q) {
+        for (int j = i - 1; j >= 0; --j) {
+            if (S.base[j] != b)
+                continue;
+            const uint32_t w = S.lohi[j];
+            if (range_has(q, lohi_lo(w), lohi_hi(w), lohi_seam(w)))
+                return;
+        }
+        ++c;
+    };
+    if (!seam) {
+        for (int q = lo; q <= hi; ++q)
+            visit(q);
+    } else {
+        for (int q = hi; q < ng; ++q)
+            visit(q);
+        for (int q = 0; q <= lo; ++q)
+            visit(q);
+    }
+    return c;
+}
+
+// Trace one (line, theta) with the whole block: fills S.idx[0..n) with the
+// deduplicated active cells in the reference emission order (chord order,
+// then sector order, tracer.cpp:174-197) and returns n. With expand == false
+// only the count is produced. All threads must call it; it ends synchronized.
+template <int NT>
+__device__ int block_trace(const TraceArgs& A, int line, double theta, const TraceSmem& S,
+                           bool expand) {
+    const uint32_t r0 = __ldg(A.off + line);
+    const int n = int(__ldg(A.off + line + 1) - r0);
+    bool any_flag = false;
+    for (int i = threadIdx.x; i < n; i += NT) {
+        const uint32_t key = __ldg(A.key + r0 + i);
+        const uint32_t ring = key & kRingMask;
+        const uint32_t slice = (key >> kSliceShift) & kSliceMask;
+        const bool flag = (key & kFlagBit) != 0;
+        const RingRow rr = A.rings[ring];
+        int lo, hi;
+        bool seam;
+        rotate_chord(__ldg(A.pa + r0 + i), __ldg(A.pb + r0 + i), theta, rr.count, rr.inv_step, lo,
+                     hi, seam);
+        S.base[i] = slice * A.cells_per_slice + rr.head;
+        S.lohi[i] = pack_lohi(lo, hi, seam, flag);
+        const uint32_t ng = rr.count;
+        const uint32_t c = seam ? (ng - uint32_t(hi)) + uint32_t(lo) + 1u : uint32_t(hi - lo) + 1u;
+        S.cnt[i] = c | (ng << 16);
+        S.pos[i] = c;
+        any_flag |= flag;
+    }
+    if (__syncthreads_or(any_flag)) {
+        for (int i = threadIdx.x; i < n; i += NT)
+            if (lohi_flag(S.lohi[i]))
+                S.pos[i] = dedup_count(S, i, int(S.cnt[i] >> 16));
+        __syncthreads();
+    }
+    block_exclusive_scan<NT>(S.pos, n, S.warp);
+    const int total = int(S.pos[n]);
+    if (!expand)
+        return total;
+    for (int i = threadIdx.x; i < n; i += NT) {
+        uint32_t p = S.pos[i];
+        const uint32_t b = S.base[i];
+        const uint32_t v = S.lohi[i];
+        const int lo = lohi_lo(v), hi = lohi_hi(v);
+        const int ng = int(S.cnt[i] >> 16);
+        if (!lohi_flag(v)) {
+            if (!lohi_seam(v)) {
+                for (int q = lo; q <= hi; ++q)
+                    S.idx[p++] = b + uint32_t(q);
+            } else {
+                for (int q = hi; q < ng; ++q)
+                    S.idx[p++] = b + uint32_t(q);
+                for (int q = 0; q <= lo; ++q)
+                    S.idx[p++] = b + uint32_t(q);
+            }
+        } else {
+            auto emit = [&](int q) {
+                for (int j = i - 1; j >= 0; --j) {
+                    if (S.base[j] != b)
+                        continue;
+                    const uint32_t w = S.lohi[j];
+                    if (range_has(q, lohi_lo(w), lohi_hi(w), lohi_seam(w)))
+                        return;
+                }
+                S.idx[p++] = b + uint32_t(q);
+            };
+            if (!lohi_seam(v)) {
+                for (int q = lo; q <= hi; ++q)
+                    emit(q);
+            } else {
+                for (int q = hi; q < ng; ++q)
+                    emit(q);
+                for (int q = 0; q <= lo; ++q)
+                    emit(q);
+            }
+        }
+    }
+    __syncthreads();
+    return total;
+}
+
+// dynamic smem bytes for block_trace
+inline size_t trace_smem_bytes(int nt, int max_recs, int max_cells) {
+    return sizeof(uint32_t) * (size_t(max_recs) * 4 + 1 + nt / 32 + size_t(max_cells));
+}
+
+template <int NT>
+__device__ __forceinline__ TraceSmem carve_trace_smem(uint32_t* smem, int max_recs) {
+    TraceSmem S;
+    S.base = smem;
+    S.lohi = S.base + max_recs;
+    S.cnt = S.lohi + max_recs;
+    S.pos = S.cnt + max_recs;
+    S.warp = S.pos + max_recs + 1;
+    S.idx = S.warp + NT / 32;
+    return S;
+}
+
+}  // namespace ub

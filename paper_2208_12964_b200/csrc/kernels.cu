@@ -1,0 +1,1005 @@
+// uscg_b200 kernels for sm_100a. Built with --fmad=false: every fp64
+// statement that mirrors the reference must round exactly like g++ on x86-64.
+//
+//   K1 generate_*   first-view coefficient generator (tracer.cpp:38-102,
+//                   geometry.cpp:127-227)
+//   K2 project      binary forward projector (phantom.cpp:182-211)
+//   K3 mart_level   one dependency level of the Sp-MART row action
+//                   (solver.cpp:33-51,111-136)
+//   K4 *_resample   USPG -> Cartesian (grid.cpp:75-99, phantom.cpp:149-163)
+#include <cuda_runtime.h>
+
+#include <cfloat>
+#include <cmath>
+#include <cstdint>
+
+#include "kernels.h"
+
+namespace ub {
+
+namespace {
+constexpr double kDegPerRad = 180.0 / 3.141592653589793238462643383279502884;
+
+inline int cdiv(long long a, long long b) { return int((a + b - 1) / b); }
+
+void check_launch() {
+    count_launch();
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess)
+        throw CudaError(std::string("kernel launch: ") + cudaGetErrorString(e));
+}
+}  // namespace
+
+int chunk_width(int problems) {
+    int p = 1;
+    while (p < problems && p < 32)
+        p <<= 1;
+    return p;
+}
+
+int problem_stride(int problems) {
+    const int p = chunk_width(problems);
+    return ((problems + p - 1) / p) * p;
+}
+
+// =============================================================================
+// K1: first-view coefficient generator, one thread per ray.
+// =============================================================================
+
+// azimuth_deg (geometry.cpp:39-46)
+__device__ __forceinline__ double azimuth_deg(double x, double y) {
+    double deg = atan2(y, x) * kDegPerRad;
+    if (deg < 0)
+        deg += 360.0;
+    if (deg >= 360.0)
+        deg = 0.0;
+    return deg;
+}
+
+// The sorted crossing list of build_sorted_intersections (geometry.cpp:127-198)
+// is the merge of three monotone sequences: entry-side ring roots t - k_k
+// (non-increasing in ring k), exit-side roots t + k_k (non-decreasing in k) and
+// z-plane roots (monotone in m). Every rounding step is monotone, so merging
+// the filtered sequences yields exactly std::sort's output; no sort is needed.
+struct RaySources {
+    const DevGrid* g;
+    double s0, s1, s2, dir0, dir1, dir2;
+    double t, d2, uxy2, zlim, lim2;
+    bool volume, axial, planes;
+    int kA, kB, kmin, m, mstep, mend;
+
+    __device__ double ring_k(int ring) const {
+        const double radius = ring * g->ring_spacing;
+        const double r2 = radius * radius;
+        return sqrt((r2 - d2) / uxy2);
+    }
+    __device__ bool z_ok(double tau) const {
+        if (!volume)
+            return true;
+        const double z = s2 + tau * dir2;
+        return !(fabs(z) > zlim);
+    }
+    __device__ double nextA() {  // entry roots, ring descending
+        while (kA >= kmin) {
+            const double tau = t - ring_k(kA);
+            --kA;
+            if (tau < 0.0 || tau > 1.0)
+                continue;
+            if (!z_ok(tau))
+                continue;
+            return tau;
+        }
+        return DBL_MAX;
+    }
+    __device__ double nextB() {  // exit roots, ring ascending
+        while (kB <= g->n_rings) {
+            const double tau = t + ring_k(kB);
+            ++kB;
+            if (tau < 0.0 || tau > 1.0)
+                continue;
+            if (!z_ok(tau))
+                continue;
+            return tau;
+        }
+        return DBL_MAX;
+    }
+    __device__ double nextC() {  // slice planes
+        while (planes && m != mend) {
+            const int mm = m;
+            m += mstep;
+            const double tau = (mm * g->slice_height - g->zoff - s2) / dir2;
+            if (tau < 0.0 || tau > 1.0)
+                continue;
+            if (!axial) {
+                const double x = s0 + tau * dir0;
+                const double y = s1 + tau * dir1;
+                if (!(x * x + y * y <= lim2))
+                    continue;
+            }
+            return tau;
+        }
+        return DBL_MAX;
+    }
+};
+
+template <bool WRITE>
+__device__ uint32_t generate_ray(const DevGrid& g, const double* s, const double* d, double* pa,
+                                 double* pb, uint32_t* key) {
+    RaySources R;
+    R.g = &g;
+    R.s0 = s[0];
+    R.s1 = s[1];
+    R.s2 = s[2];
+    R.dir0 = d[0] - s[0];
+    R.dir1 = d[1] - s[1];
+    R.dir2 = d[2] - s[2];
+    R.volume = g.volume != 0;
+    // is_axial (geometry.cpp:31-37)
+    const double ux = s[0] - d[0], uy = s[1] - d[1];
+    R.uxy2 = ux * ux + uy * uy;
+    const double dd2 = R.dir0 * R.dir0 + R.dir1 * R.dir1 + R.dir2 * R.dir2;
+    R.axial = dd2 == 0.0 || R.uxy2 <= 1e-24 * dd2;
+    R.kA = 0;
+    R.kmin = 1;
+    R.kB = g.n_rings + 1;
+    R.planes = false;
+    R.m = 0;
+    R.mend = 0;
+    R.mstep = 1;
+    R.zlim = g.zoff + g.eps;
+    R.lim2 = (g.radius + g.eps) * (g.radius + g.eps);
+    R.t = 0;
+    R.d2 = 0;
+    if (R.axial) {
+        if (!R.volume)
+            return 0;
+        if (hypot(s[0], s[1]) >= g.radius)
+            return 0;
+        if (R.dir2 == 0.0)
+            return 0;
+        R.planes = true;
+    } else {
+        // circle_taus (geometry.cpp:72-85), per-ray invariants
+        R.t = (s[0] * ux + s[1] * uy) / R.uxy2;
+        const double cross = s[0] * d[1] - s[1] * d[0];
+        R.d2 = cross * cross / R.uxy2;
+        int kmin = 1;
+        while (kmin <= g.n_rings) {
+            const double radius = kmin * g.ring_spacing;
+            if (!(R.d2 > radius * radius))
+                break;
+            ++kmin;
+        }
+        R.kmin = kmin;
+        R.kA = g.n_rings;
+        R.kB = kmin;
+        R.planes = R.volume && R.dir2 != 0.0;
+    }
+    if (R.planes) {
+        if (R.dir2 > 0) {
+            R.m = 0;
+            R.mend = g.n_slices + 1;
+            R.mstep = 1;
+        } else {
+            R.m = g.n_slices;
+            R.mend = -1;
+            R.mstep = -1;
+        }
+    }
+
+    const double len = sqrt(dd2);  // norm(dir)
+    double ta = R.axial ? DBL_MAX : R.nextA();
+    double tb = R.axial ? DBL_MAX : R.nextB();
+    double tc = R.nextC();
+    int np = 0;
+    double last_tau = 0;
+    double p0 = 0, p1 = 0, p2 = 0;
+    double phi_prev = -1.0;
+    uint32_t nrec = 0;
+    while (true) {
+        double tau;
+        if (ta <= tb && ta <= tc) {
+            tau = ta;
+            if (tau == DBL_MAX)
+                break;
+            ta = R.nextA();
+        } else if (tb <= tc) {
+            tau = tb;
+            tb = R.nextB();
+        } else {
+            tau = tc;
+            tc = R.nextC();
+        }
+        // eps-merge of near-coincident crossings (geometry.cpp:188-196)
+        if (np > 0 && (tau - last_tau) * len <= g.eps)
+            continue;
+        const double q0 = R.s0 + tau * R.dir0;
+        const double q1 = R.s1 + tau * R.dir1;
+        const double q2 = R.s2 + tau * R.dir2;
+        if (np > 0) {
+            // classify_chord (geometry.cpp:200-227)
+            const double e0 = p0 - q0, e1 = p1 - q1, e2 = p2 - q2;
+            bool keep = !(sqrt(e0 * e0 + e1 * e1 + e2 * e2) <= g.eps);
+            int slice = 0, ring = 0;
+            if (keep) {
+                const double m0 = (p0 + q0) / 2, m1 = (p1 + q1) / 2, m2 = (p2 + q2) / 2;
+                if (g.volume) {
+                    const double zloc = m2 + g.zoff;
+                    const double sf = floor(zloc / g.slice_height);
+                    if (sf < 0 || sf >= g.n_slices)
+                        keep = false;
+                    else
+                        slice = int(sf);
+                }
+                if (keep) {
+                    const double dm = hypot(m0, m1);
+                    ring = int(floor(dm / g.ring_spacing)) + 1;
+                    if (ring > g.n_rings)
+                        keep = false;
+                }
+            }
+            if (keep) {
+                if (WRITE) {
+                    if (phi_prev < 0)
+                        phi_prev = azimuth_deg(p0, p1);
+                    const double phi_q = azimuth_deg(q0, q1);
+                    pa[nrec] = phi_prev;
+                    pb[nrec] = phi_q;
+                    key[nrec] = uint32_t(ring) | (uint32_t(slice) << kSliceShift);
+                    phi_prev = phi_q;
+                }
+                ++nrec;
+            } else if (WRITE) {
+                phi_prev = -1.0;
+            }
+        }
+        p0 = q0;
+        p1 = q1;
+        p2 = q2;
+        last_tau = tau;
+        ++np;
+    }
+    return nrec;
+}
+
+__global__ void generate_count_kernel(DevGrid g, int lines, const double* __restrict__ src,
+                                      const double* __restrict__ det, uint32_t* counts) {
+    const int l = blockIdx.x * blockDim.x + threadIdx.x;
+    if (l >= lines)
+        return;
+    counts[l] = generate_ray<false>(g, src + 3 * size_t(l), det + 3 * size_t(l), nullptr, nullptr,
+                                    nullptr);
+}
+
+__global__ void generate_write_kernel(DevGrid g, int lines, const double* __restrict__ src,
+                                      const double* __restrict__ det,
+                                      const uint32_t* __restrict__ off, double* pa, double* pb,
+                                      uint32_t* key) {
+    const int l = blockIdx.x * blockDim.x + threadIdx.x;
+    if (l >= lines)
+        return;
+    const uint32_t o = off[l];
+    generate_ray<true>(g, src + 3 * size_t(l), det + 3 * size_t(l), pa + o, pb + o, key + o);
+}
+
+void launch_generate_count(const DevGrid& g, int lines, const double* src, const double* det,
+                           uint32_t* counts, cudaStream_t st) {
+    if (lines <= 0)
+        return;
+    generate_count_kernel<<<cdiv(lines, 64), 64, 0, st>>>(g, lines, src, det, counts);
+    check_launch();
+}
+
+void launch_generate_write(const DevGrid& g, int lines, const double* src, const double* det,
+                           const uint32_t* off, double* pa, double* pb, uint32_t* key,
+                           cudaStream_t st) {
+    if (lines <= 0)
+        return;
+    generate_write_kernel<<<cdiv(lines, 64), 64, 0, st>>>(g, lines, src, det, off, pa, pb, key);
+    check_launch();
+}
+
+// ---- dedup annotation --------------------------------------------------------
+// Two chords of one line can share a cell only if they lie in the same
+// (slice, ring) and their short arcs are within one sector of each other (the
+// rotation shifts both by the same angle). Such records get the flag bit and
+// the trace applies the stamp dedup to them; every other record expands
+// without any check.
+__device__ __forceinline__ void short_arc(double a, double b, double& st, double& ln) {
+    const double lo = a < b ? a : b, hi = a < b ? b : a;
+    if (hi - lo <= 180.0) {
+        st = lo;
+        ln = hi - lo;
+    } else {
+        st = hi;
+        ln = 360.0 - (hi - lo);
+    }
+}
+
+__device__ __forceinline__ double wrap360(double x) { return x - 360.0 * floor(x / 360.0); }
+
+__device__ bool arcs_near(double a0, double b0, double a1, double b1, double step) {
+    double s0, l0, s1, l1;
+    short_arc(a0, b0, s0, l0);
+    short_arc(a1, b1, s1, l1);
+    if (l0 >= 179.0 || l1 >= 179.0)
+        return true;
+    const double d01 = wrap360(s1 - (s0 + l0));
+    const double d10 = wrap360(s0 - (s1 + l1));
+    if (fabs(d01 + d10 + l0 + l1 - 360.0) > 1e-6)
+        return true;  // overlapping
+    return fmin(d01, d10) <= 1.5 * step + 1e-9;
+}
+
+__global__ void annotate_kernel(int lines, const uint32_t* __restrict__ off,
+                                const double* __restrict__ pa, const double* __restrict__ pb,
+                                uint32_t* key, const RingRow* __restrict__ rings) {
+    const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (warp >= lines)
+        return;
+    const uint32_t r0 = off[warp], r1 = off[warp + 1];
+    for (uint32_t i = r0 + 1 + lane; i < r1; i += 32) {
+        const uint32_t ki = key[i] & ~kFlagBit;
+        const uint32_t ring = ki & kRingMask;
+        const double step = 360.0 / rings[ring].count;
+        for (uint32_t j = i; j-- > r0;) {
+            const uint32_t kj = key[j] & ~kFlagBit;
+            if ((kj >> kSliceShift) != (ki >> kSliceShift))
+                break;  // records of one slice are contiguous along the ray
+            if (kj != ki)
+                continue;
+            if (arcs_near(pa[i], pb[i], pa[j], pb[j], step)) {
+                atomicOr(key + i, kFlagBit);
+                break;
+            }
+        }
+    }
+}
+
+void launch_annotate(int lines, const uint32_t* off, const double* pa, const double* pb,
+                     uint32_t* key, const RingRow* rings, cudaStream_t st) {
+    if (lines <= 0)
+        return;
+    annotate_kernel<<<cdiv(lines, 8), 256, 0, st>>>(lines, off, pa, pb, key, rings);
+    check_launch();
+}
+
+// ---- exclusive scan (single block, chunked; used for the record offsets) ----
+__global__ void scan_kernel(const uint32_t* __restrict__ in, uint32_t* out, int n) {
+    __shared__ uint32_t s_warp[32];
+    __shared__ uint32_t s_carry;
+    if (threadIdx.x == 0)
+        s_carry = 0;
+    __syncthreads();
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (int base = 0; base < n; base += 1024) {
+        const int i = base + threadIdx.x;
+        const uint32_t v = i < n ? in[i] : 0u;
+        uint32_t x = v;
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, x, o);
+            if (lane >= o)
+                x += y;
+        }
+        if (lane == 31)
+            s_warp[warp] = x;
+        __syncthreads();
+        if (warp == 0) {
+            uint32_t w = s_warp[lane];
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, w, o);
+                if (lane >= o)
+                    w += y;
+            }
+            s_warp[lane] = w;
+        }
+        __syncthreads();
+        const uint32_t incl = x + (warp > 0 ? s_warp[warp - 1] : 0u) + s_carry;
+        if (i < n)
+            out[i] = incl - v;
+        __syncthreads();
+        if (threadIdx.x == 1023)
+            s_carry = incl;
+        __syncthreads();
+    }
+    if (threadIdx.x == 0)
+        out[n] = s_carry;
+}
+
+void launch_exclusive_scan_u32(const uint32_t* in, uint32_t* out, int n, cudaStream_t st) {
+    scan_kernel<<<1, 1024, 0, st>>>(in, out, n);
+    check_launch();
+}
+
+// =============================================================================
+// traces
+// =============================================================================
+
+template <int NT>
+__global__ void __launch_bounds__(NT) trace_one_kernel(TraceArgs A, int line, double theta,
+                                                       int max_recs, uint32_t* out,
+                                                       uint32_t* count) {
+    extern __shared__ uint32_t smem[];
+    const TraceSmem S = carve_trace_smem<NT>(smem, max_recs);
+    const int n = block_trace<NT>(A, line, theta, S, true);
+    for (int i = threadIdx.x; i < n; i += NT)
+        out[i] = S.idx[i];
+    if (threadIdx.x == 0)
+        *count = uint32_t(n);
+}
+
+void launch_trace_one(const TraceArgs& A, int line, double theta, int max_recs, int max_cells,
+                      uint32_t* out, uint32_t* count, cudaStream_t st) {
+    const size_t sm = trace_smem_bytes(256, max_recs, max_cells);
+    UB_CUDA(cudaFuncSetAttribute(trace_one_kernel<256>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 int(sm)));
+    trace_one_kernel<256><<<1, 256, sm, st>>>(A, line, theta, max_recs, out, count);
+    check_launch();
+}
+
+template <int NT>
+__global__ void __launch_bounds__(NT) trace_counts_kernel(TraceArgs A, int max_recs,
+                                                          uint32_t* cells) {
+    extern __shared__ uint32_t smem[];
+    const TraceSmem S = carve_trace_smem<NT>(smem, max_recs);
+    const int unit = blockIdx.x;
+    const int v = unit / A.lines, line = unit % A.lines;
+    const int n = block_trace<NT>(A, line, A.theta[v], S, false);
+    if (threadIdx.x == 0)
+        cells[unit] = uint32_t(n);
+}
+
+void launch_trace_counts(const TraceArgs& A, int views, int max_recs, uint32_t* cells,
+                         cudaStream_t st) {
+    const long long units = (long long)views * A.lines;
+    if (units <= 0)
+        return;
+    const size_t sm = trace_smem_bytes(128, max_recs, 0);
+    UB_CUDA(cudaFuncSetAttribute(trace_counts_kernel<128>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm)));
+    trace_counts_kernel<128><<<unsigned(units), 128, sm, st>>>(A, max_recs, cells);
+    check_launch();
+}
+
+template <int NT>
+__global__ void __launch_bounds__(NT) trace_dump_kernel(TraceArgs A, uint32_t unit0, int max_recs,
+                                                        const uint32_t* __restrict__ pos,
+                                                        uint32_t* out) {
+    extern __shared__ uint32_t smem[];
+    const TraceSmem S = carve_trace_smem<NT>(smem, max_recs);
+    const uint32_t unit = unit0 + blockIdx.x;
+    const int v = unit / A.lines, line = unit % A.lines;
+    const int n = block_trace<NT>(A, line, A.theta[v], S, true);
+    uint32_t* o = out + (pos[blockIdx.x] - pos[0]);
+    for (int i = threadIdx.x; i < n; i += NT)
+        o[i] = S.idx[i];
+}
+
+void launch_trace_dump(const TraceArgs& A, uint32_t unit0, uint32_t units, int max_recs,
+                       int max_cells, const uint32_t* pos, uint32_t* out, cudaStream_t st) {
+    if (units == 0)
+        return;
+    const size_t sm = trace_smem_bytes(128, max_recs, max_cells);
+    UB_CUDA(cudaFuncSetAttribute(trace_dump_kernel<128>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm)));
+    trace_dump_kernel<128><<<units, 128, sm, st>>>(A, unit0, max_recs, pos, out);
+    check_launch();
+}
+
+template <int NT>
+__global__ void __launch_bounds__(NT) crossed_kernel(TraceArgs A, int max_recs, uint8_t* crossed) {
+    extern __shared__ uint32_t smem[];
+    const TraceSmem S = carve_trace_smem<NT>(smem, max_recs);
+    const int unit = blockIdx.x;
+    const int v = unit / A.lines, line = unit % A.lines;
+    const int n = block_trace<NT>(A, line, A.theta[v], S, true);
+    for (int i = threadIdx.x; i < n; i += NT)
+        crossed[S.idx[i]] = 1;
+}
+
+void launch_crossed(const TraceArgs& A, int views, int max_recs, int max_cells, uint8_t* crossed,
+                    cudaStream_t st) {
+    const long long units = (long long)views * A.lines;
+    if (units <= 0)
+        return;
+    const size_t sm = trace_smem_bytes(128, max_recs, max_cells);
+    UB_CUDA(cudaFuncSetAttribute(crossed_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 int(sm)));
+    crossed_kernel<128><<<unsigned(units), 128, sm, st>>>(A, max_recs, crossed);
+    check_launch();
+}
+
+// =============================================================================
+// K2: binary forward projector. One block per (view, line, problem chunk).
+// =============================================================================
+
+template <int P, int NT>
+__global__ void __launch_bounds__(NT) project_kernel(TraceArgs A, const float* __restrict__ field,
+                                                     int Sp, int nchunks, int max_recs,
+                                                     float* __restrict__ out) {
+    extern __shared__ uint32_t smem[];
+    const TraceSmem S = carve_trace_smem<NT>(smem, max_recs);
+    __shared__ double s_red[NT / 32][P];
+    const int unit = blockIdx.x / nchunks, chunk = blockIdx.x % nchunks;
+    const int v = unit / A.lines, line = unit % A.lines;
+    const int n = block_trace<NT>(A, line, A.theta[v], S, true);
+    constexpr int NCL = NT / P;
+    const int p = threadIdx.x % P, cl = threadIdx.x / P;
+    const size_t col = size_t(chunk) * P + p;
+    double sum = 0;
+    for (int c = cl; c < n; c += NCL)
+        sum += double(field[size_t(S.idx[c]) * Sp + col]);
+#pragma unroll
+    for (int o = P; o < 32; o <<= 1)
+        sum += __shfl_xor_sync(0xFFFFFFFFu, sum, o);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (lane < P)
+        s_red[warp][lane] = sum;
+    __syncthreads();
+    if (threadIdx.x < P) {
+        double t = 0;
+#pragma unroll
+        for (int w = 0; w < NT / 32; ++w)
+            t += s_red[w][threadIdx.x];
+        out[size_t(unit) * Sp + size_t(chunk) * P + threadIdx.x] = float(t);
+    }
+}
+
+template <int P, int NT>
+static void project_impl(const TraceArgs& A, int views, const float* field, int Sp, int max_recs,
+                         int max_cells, float* out, cudaStream_t st) {
+    const size_t sm = trace_smem_bytes(NT, max_recs, max_cells);
+    UB_CUDA(cudaFuncSetAttribute(project_kernel<P, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 int(sm)));
+    const int nchunks = Sp / P;
+    const long long blocks = (long long)views * A.lines * nchunks;
+    project_kernel<P, NT><<<unsigned(blocks), NT, sm, st>>>(A, field, Sp, nchunks, max_recs, out);
+    check_launch();
+}
+
+void launch_project(const TraceArgs& A, int views, const float* field, int Sp, int max_recs,
+                    int max_cells, float* out, cudaStream_t st) {
+    if ((long long)views * A.lines == 0)
+        return;
+    // the chunk width is the largest power of two <= 32 dividing Sp
+    int P = 1;
+    while (P < 32 && Sp % (P * 2) == 0)
+        P *= 2;
+    switch (P) {
+        case 1: project_impl<1, 128>(A, views, field, Sp, max_recs, max_cells, out, st); break;
+        case 2: project_impl<2, 256>(A, views, field, Sp, max_recs, max_cells, out, st); break;
+        case 4: project_impl<4, 256>(A, views, field, Sp, max_recs, max_cells, out, st); break;
+        case 8: project_impl<8, 256>(A, views, field, Sp, max_recs, max_cells, out, st); break;
+        case 16: project_impl<16, 512>(A, views, field, Sp, max_recs, max_cells, out, st); break;
+        default: project_impl<32, 1024>(A, views, field, Sp, max_recs, max_cells, out, st); break;
+    }
+}
+
+// =============================================================================
+// K3: one dependency level of Sp-MART. The units of a level have pairwise
+// disjoint cell supports (host-built ASAP schedule), so applying them
+// concurrently performs exactly the reference's sequential updates
+// (solver.cpp:111-136): no atomics on the field, no reordering on any cell.
+// =============================================================================
+
+template <int P, int NT>
+__global__ void __launch_bounds__(NT) mart_level_kernel(const MartArgs* __restrict__ args,
+                                                        const uint32_t* __restrict__ units) {
+    extern __shared__ uint32_t smem[];
+    __shared__ double s_red[NT / 32][P];
+    __shared__ double s_fac[P];
+    const MartArgs& A = *args;
+    const TraceSmem S = carve_trace_smem<NT>(smem, A.max_recs);
+    const int nchunks = A.nchunks;
+    const uint32_t unit = units[blockIdx.x / nchunks];
+    const int chunk = blockIdx.x % nchunks;
+    const int v = int(unit / uint32_t(A.tr.lines)), line = int(unit % uint32_t(A.tr.lines));
+    const int n = block_trace<NT>(A.tr, line, A.tr.theta[v], S, true);
+
+    constexpr int NCL = NT / P;
+    const int p = threadIdx.x % P, cl = threadIdx.x / P;
+    const int Sp = A.Sp;
+    const size_t col = size_t(chunk) * P + p;
+    float* __restrict__ f = A.field;
+
+    // forward_project_line (solver.cpp:25-31)
+    double sum = 0;
+    for (int c = cl; c < n; c += NCL)
+        sum += double(f[size_t(S.idx[c]) * Sp + col]);
+#pragma unroll
+    for (int o = P; o < 32; o <<= 1)
+        sum += __shfl_xor_sync(0xFFFFFFFFu, sum, o);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (lane < P)
+        s_red[warp][lane] = sum;
+    __syncthreads();
+    if (threadIdx.x < P) {
+        const size_t c2 = size_t(chunk) * P + threadIdx.x;
+        double p_bar = 0;
+#pragma unroll
+        for (int w = 0; w < NT / 32; ++w)
+            p_bar += s_red[w][threadIdx.x];
+        const double m = double(A.proj[size_t(unit) * Sp + c2]);
+        double factor = 0;  // 0 marks "no update"
+        if (m != 0 && A.active[c2]) {
+            // mart_update_line (solver.cpp:36-46)
+            const double pf = A.p_floor[c2];
+            const double ratio = m / (p_bar > pf ? p_bar : pf);
+            factor = 1.0 - A.beta * (1.0 - ratio);
+            if (factor <= 0) {
+                factor = pf;
+                atomicAdd(A.clamps + c2, 1ull);
+            }
+        }
+        s_fac[threadIdx.x] = factor;
+    }
+    __syncthreads();
+    const double factor = s_fac[p];
+    if (factor != 0) {
+        for (int c = cl; c < n; c += NCL) {
+            float* q = f + size_t(S.idx[c]) * Sp + col;
+            // the reference's clamp keeps the fp64 field strictly positive
+            // (solver.cpp:42-45); in fp32 a product below FLT_MIN would
+            // underflow to 0, so it saturates at FLT_MIN instead
+            const float r = float(double(*q) * factor);
+            *q = r >= FLT_MIN ? r : FLT_MIN;
+        }
+    }
+}
+
+template <int P, int NT>
+static size_t mart_smem_t(const MartArgs& a) {
+    return trace_smem_bytes(NT, a.max_recs, a.max_cells);
+}
+
+size_t mart_smem_bytes(const MartArgs& a) {
+    const int P = a.Sp / a.nchunks;
+    switch (P) {
+        case 1: return mart_smem_t<1, 128>(a);
+        case 2: return mart_smem_t<2, 256>(a);
+        case 4: return mart_smem_t<4, 256>(a);
+        case 8: return mart_smem_t<8, 256>(a);
+        case 16: return mart_smem_t<16, 512>(a);
+        default: return mart_smem_t<32, 1024>(a);
+    }
+}
+
+template <int P, int NT>
+static void mart_prep_t(const MartArgs& a) {
+    UB_CUDA(cudaFuncSetAttribute(mart_level_kernel<P, NT>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 int(mart_smem_t<P, NT>(a))));
+}
+
+void mart_prepare(const MartArgs& a) {
+    const int P = a.Sp / a.nchunks;
+    switch (P) {
+        case 1: mart_prep_t<1, 128>(a); break;
+        case 2: mart_prep_t<2, 256>(a); break;
+        case 4: mart_prep_t<4, 256>(a); break;
+        case 8: mart_prep_t<8, 256>(a); break;
+        case 16: mart_prep_t<16, 512>(a); break;
+        default: mart_prep_t<32, 1024>(a); break;
+    }
+}
+
+template <int P, int NT>
+static void mart_launch_t(const MartArgs* d, const MartArgs& h, const uint32_t* units, int n,
+                          cudaStream_t st) {
+    mart_level_kernel<P, NT>
+        <<<unsigned(n) * unsigned(h.nchunks), NT, mart_smem_t<P, NT>(h), st>>>(d, units);
+}
+
+void launch_mart_level(const MartArgs* dargs, const MartArgs& h, const uint32_t* units, int n,
+                       cudaStream_t st) {
+    if (n <= 0)
+        return;
+    const int P = h.Sp / h.nchunks;
+    switch (P) {
+        case 1: mart_launch_t<1, 128>(dargs, h, units, n, st); break;
+        case 2: mart_launch_t<2, 256>(dargs, h, units, n, st); break;
+        case 4: mart_launch_t<4, 256>(dargs, h, units, n, st); break;
+        case 8: mart_launch_t<8, 256>(dargs, h, units, n, st); break;
+        case 16: mart_launch_t<16, 512>(dargs, h, units, n, st); break;
+        default: mart_launch_t<32, 1024>(dargs, h, units, n, st); break;
+    }
+    check_launch();
+}
+
+// =============================================================================
+// per-problem reductions over [n][Sp] arrays: blockIdx.y = 32-column tile,
+// threadIdx.x = column in the tile, threadIdx.y = row lane.
+// =============================================================================
+
+__global__ void proj_stats_kernel(const float* __restrict__ proj, int units, int S, int Sp,
+                                  double* stats) {
+    const int col = blockIdx.y * 32 + threadIdx.x;
+    if (col >= S)
+        return;
+    double cnt = 0, sum = 0, nz = 0, bad = 0;
+    for (int u = blockIdx.x * blockDim.y + threadIdx.y; u < units; u += gridDim.x * blockDim.y) {
+        const float m = proj[size_t(u) * Sp + col];
+        if (!isfinite(m) || m < 0)
+            bad = 1;
+        if (m > 0) {
+            cnt += 1;
+            sum += double(m);
+        }
+        if (m != 0)
+            nz = 1;
+    }
+    atomicAdd(stats + 4 * col + 0, cnt);
+    atomicAdd(stats + 4 * col + 1, sum);
+    if (nz > 0)
+        atomicAdd(stats + 4 * col + 2, 1.0);
+    if (bad > 0)
+        atomicAdd(stats + 4 * col + 3, 1.0);
+}
+
+void launch_proj_stats(const float* proj, int units, int S, int Sp, double* stats,
+                       cudaStream_t st) {
+    dim3 block(32, 8);
+    dim3 grid(unsigned(std::min(cdiv(units, 8), 1184)), unsigned(cdiv(S, 32)));
+    proj_stats_kernel<<<grid, block, 0, st>>>(proj, units, S, Sp, stats);
+    check_launch();
+}
+
+__global__ void sweep_updates_kernel(const float* __restrict__ proj,
+                                     const uint32_t* __restrict__ cells, int units, int S, int Sp,
+                                     unsigned long long* out) {
+    const int col = blockIdx.y * 32 + threadIdx.x;
+    if (col >= S)
+        return;
+    unsigned long long acc = 0;
+    for (int u = blockIdx.x * blockDim.y + threadIdx.y; u < units; u += gridDim.x * blockDim.y)
+        if (proj[size_t(u) * Sp + col] != 0)
+            acc += cells[u];
+    atomicAdd(out + col, acc);
+}
+
+void launch_sweep_updates(const float* proj, const uint32_t* cells, int units, int S, int Sp,
+                          unsigned long long* out, cudaStream_t st) {
+    dim3 block(32, 8);
+    dim3 grid(unsigned(std::min(cdiv(units, 8), 1184)), unsigned(cdiv(S, 32)));
+    sweep_updates_kernel<<<grid, block, 0, st>>>(proj, cells, units, S, Sp, out);
+    check_launch();
+}
+
+__global__ void residual_kernel(const float* __restrict__ f, const float* __restrict__ prev,
+                                const uint8_t* __restrict__ crossed, uint64_t cells, int S, int Sp,
+                                unsigned int* out) {
+    const int col = blockIdx.y * 32 + threadIdx.x;
+    if (col >= S)
+        return;
+    float best = 0;
+    for (uint64_t c = uint64_t(blockIdx.x) * blockDim.y + threadIdx.y; c < cells;
+         c += uint64_t(gridDim.x) * blockDim.y) {
+        if (!crossed[c])
+            continue;
+        const float a = f[c * Sp + col], b = prev[c * Sp + col];
+        const float rel = float(fabs(double(a) - double(b)) / double(b));
+        best = fmaxf(best, rel);
+    }
+    atomicMax(out + col, __float_as_uint(best));
+}
+
+void launch_residual(const float* field, const float* prev, const uint8_t* crossed, uint64_t cells,
+                     int S, int Sp, unsigned int* out, cudaStream_t st) {
+    dim3 block(32, 8);
+    dim3 grid(unsigned(std::min<long long>(cdiv((long long)cells, 8), 2368)), unsigned(cdiv(S, 32)));
+    residual_kernel<<<grid, block, 0, st>>>(field, prev, crossed, cells, S, Sp, out);
+    check_launch();
+}
+
+__global__ void nonpositive_kernel(const float* __restrict__ f, uint64_t n,
+                                   unsigned long long* out) {
+    unsigned long long c = 0;
+    for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+         i += uint64_t(gridDim.x) * blockDim.x)
+        if (!(f[i] > 0))
+            ++c;
+    if (c)
+        atomicAdd(out, c);
+}
+
+void launch_count_nonpositive(const float* field, uint64_t n, unsigned long long* out,
+                              cudaStream_t st) {
+    nonpositive_kernel<<<unsigned(std::min<long long>(cdiv((long long)n, 256), 4736)), 256, 0, st>>>(
+        field, n, out);
+    check_launch();
+}
+
+// =============================================================================
+// layout transposes [S][n] <-> [n][Sp]
+// =============================================================================
+
+__global__ void to_interleaved_kernel(const float* __restrict__ in, float* __restrict__ out,
+                                      uint64_t n, int S, int Sp, float pad) {
+    __shared__ float tile[32][33];
+    const uint64_t i0 = uint64_t(blockIdx.x) * 32;
+    const int s0 = blockIdx.y * 32;
+    for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+        const int s = s0 + r;
+        const uint64_t i = i0 + threadIdx.x;
+        tile[r][threadIdx.x] = (s < S && i < n) ? in[uint64_t(s) * n + i] : pad;
+    }
+    __syncthreads();
+    for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+        const uint64_t i = i0 + r;
+        const int s = s0 + threadIdx.x;
+        if (i < n && s < Sp)
+            out[i * Sp + s] = tile[threadIdx.x][r];
+    }
+}
+
+void launch_to_interleaved(const float* in, float* out, uint64_t n, int S, int Sp, float pad,
+                           cudaStream_t st) {
+    dim3 grid(unsigned((n + 31) / 32), unsigned(cdiv(Sp, 32)));
+    to_interleaved_kernel<<<grid, dim3(32, 8), 0, st>>>(in, out, n, S, Sp, pad);
+    check_launch();
+}
+
+__global__ void from_interleaved_kernel(const float* __restrict__ in, float* __restrict__ out,
+                                        uint64_t n, int S, int Sp) {
+    __shared__ float tile[32][33];
+    const uint64_t i0 = uint64_t(blockIdx.x) * 32;
+    const int s0 = blockIdx.y * 32;
+    for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+        const uint64_t i = i0 + r;
+        const int s = s0 + threadIdx.x;
+        tile[r][threadIdx.x] = (i < n && s < Sp) ? in[i * Sp + s] : 0.f;
+    }
+    __syncthreads();
+    for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+        const int s = s0 + r;
+        const uint64_t i = i0 + threadIdx.x;
+        if (s < S && i < n)
+            out[uint64_t(s) * n + i] = tile[threadIdx.x][r];
+    }
+}
+
+void launch_from_interleaved(const float* in, float* out, uint64_t n, int S, int Sp,
+                             cudaStream_t st) {
+    dim3 grid(unsigned((n + 31) / 32), unsigned(cdiv(S, 32)));
+    from_interleaved_kernel<<<grid, dim3(32, 8), 0, st>>>(in, out, n, S, Sp);
+    check_launch();
+}
+
+__global__ void fill_kernel(float* p, uint64_t n, float v) {
+    for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+         i += uint64_t(gridDim.x) * blockDim.x)
+        p[i] = v;
+}
+
+void launch_fill(float* p, uint64_t n, float v, cudaStream_t st) {
+    if (n == 0)
+        return;
+    fill_kernel<<<unsigned(std::min<long long>(cdiv((long long)n, 256), 4736)), 256, 0, st>>>(p, n, v);
+    check_launch();
+}
+
+// =============================================================================
+// K4: USPG -> Cartesian.
+// =============================================================================
+
+// Inverse of uspg_to_cg_map (grid.cpp:75-99): pixel (row, col) of an n x n
+// image -> flat index within a slice. Ring k is the perimeter of the centred
+// 2k x 2k block, walked counter-clockwise from (c, c+k-1).
+__device__ __forceinline__ uint32_t cg_inverse(int row, int col, int n) {
+    const int c = n / 2;
+    const int rr = row >= c ? row - c + 1 : c - row;
+    const int qq = col >= c ? col - c + 1 : c - col;
+    const int k = rr > qq ? rr : qq;
+    int pos;
+    if (col == c + k - 1 && row >= c)
+        pos = row - c;                           // right edge, upward
+    else if (row == c + k - 1)
+        pos = k + (c + k - 2 - col);             // top edge, leftward
+    else if (col == c - k)
+        pos = 3 * k - 1 + (c + k - 2 - row);     // left edge, downward
+    else if (row == c - k)
+        pos = 5 * k - 2 + (col - (c - k + 1));   // bottom edge, rightward
+    else
+        pos = 7 * k - 3 + (row - (c - k + 1));   // right edge, up to the tail
+    return 4u * uint32_t(k - 1) * uint32_t(k - 1) + uint32_t(pos);
+}
+
+// out[(p*slices + s)*n*n + pixel]; field element (p, cell) at cell*cs + p*ps
+__global__ void perm_resample_kernel(const float* __restrict__ field, uint64_t cps, int slices,
+                                     int S, uint64_t cs, uint64_t ps, int n,
+                                     float* __restrict__ out) {
+    const uint64_t npx = uint64_t(n) * n;
+    const uint64_t total = npx * slices * S;
+    for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < total;
+         i += uint64_t(gridDim.x) * blockDim.x) {
+        const uint64_t px = i % npx;
+        const uint64_t sp = i / npx;
+        const int s = int(sp % slices), p = int(sp / slices);
+        const int row = int(px / n), col = int(px % n);
+        const uint64_t cell = uint64_t(s) * cps + cg_inverse(row, col, n);
+        out[i] = field[cell * cs + uint64_t(p) * ps];
+    }
+}
+
+void launch_perm_resample(const float* field, uint64_t cps, int slices, int S, int Sp, int n,
+                          float* out, cudaStream_t st) {
+    const uint64_t total = uint64_t(n) * n * slices * S;
+    // Sp > 0: interleaved [cells][Sp]; Sp <= 0: problem-major [S][cells]
+    const uint64_t cells = cps * slices;
+    const uint64_t cs = Sp > 0 ? uint64_t(Sp) : 1, ps = Sp > 0 ? 1 : cells;
+    perm_resample_kernel<<<unsigned(std::min<uint64_t>((total + 255) / 256, 148 * 32)), 256, 0,
+                           st>>>(field, cps, slices, S, cs, ps, n, out);
+    check_launch();
+}
+
+// bin_point (tests/oracles.hpp:36-58) at pixel centres for any ring law
+__global__ void bin_map_kernel(DevGrid g, int npix, uint32_t* map) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= npix * npix)
+        return;
+    const int row = i / npix, col = i % npix;
+    const double px = 2.0 * g.radius / npix;
+    const double y = (row + 0.5 - npix / 2) * px;
+    const double x = (col + 0.5 - npix / 2) * px;
+    const double rho = hypot(x, y);
+    uint32_t v = 0xFFFFFFFFu;
+    if (rho < g.radius) {
+        const int ring = int(floor(rho / g.ring_spacing)) + 1;
+        if (ring <= g.n_rings) {
+            const int ng = int(g.rings[ring].count);
+            const double phi = azimuth_deg(x, y);
+            int sector = int(phi * (ng / 360.0));
+            if (sector >= ng)
+                sector = ng - 1;
+            v = g.rings[ring].head + uint32_t(sector);
+        }
+    }
+    map[i] = v;
+}
+
+void launch_bin_map(const DevGrid& g, int npix, uint32_t* map, cudaStream_t st) {
+    bin_map_kernel<<<cdiv((long long)npix * npix, 256), 256, 0, st>>>(g, npix, map);
+    check_launch();
+}
+
+__global__ void map_resample_kernel(const float* __restrict__ field, uint64_t cps, int slices,
+                                    int S, uint64_t cs, uint64_t ps,
+                                    const uint32_t* __restrict__ map, int npix,
+                                    float* __restrict__ out) {
+    const uint64_t npx = uint64_t(npix) * npix;
+    const uint64_t total = npx * slices * S;
+    for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < total;
+         i += uint64_t(gridDim.x) * blockDim.x) {
+        const uint64_t px = i % npx;
+        const uint64_t sp = i / npx;
+        const int s = int(sp % slices), p = int(sp / slices);
+        const uint32_t m = map[px];
+        out[i] = m == 0xFFFFFFFFu ? 0.f : field[(uint64_t(s) * cps + m) * cs + uint64_t(p) * ps];
+    }
+}
+
+void launch_map_resample(const float* field, uint64_t cps, int slices, int S, int Sp,
+                         const uint32_t* map, int npix, float* out, cudaStream_t st) {
+    const uint64_t total = uint64_t(npix) * npix * slices * S;
+    const uint64_t cells = cps * slices;
+    const uint64_t cs = Sp > 0 ? uint64_t(Sp) : 1, ps = Sp > 0 ? 1 : cells;
+    map_resample_kernel<<<unsigned(std::min<uint64_t>((total + 255) / 256, 148 * 32)), 256, 0,
+                          st>>>(field, cps, slices, S, cs, ps, map, npix, out);
+    check_launch();
+}
+
+__global__ void cg_map_kernel(int n, uint32_t* out) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n * n)
+        return;
+    const int row = i / n, col = i % n;
+    out[cg_inverse(row, col, n)] = uint32_t(i);
+}
+
+void launch_cg_map(int n, uint32_t* out, cudaStream_t st) {
+    cg_map_kernel<<<cdiv((long long)n * n, 256), 256, 0, st>>>(n, out);
+    check_launch();
+}
+
+}  // namespace ub

@@ -1,0 +1,87 @@
+// Host-callable launch wrappers for the uscg_b200 kernels (kernels.cu).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "internal.cuh"
+
+namespace ub {
+
+struct MartArgs {
+    TraceArgs tr;
+    float* field;                 // [cells][Sp]
+    const float* proj;            // [units][Sp]
+    const double* p_floor;        // [Sp]
+    const uint8_t* active;        // [Sp]
+    unsigned long long* clamps;   // [Sp]
+    double beta;
+    int Sp;
+    int nchunks;
+    int max_recs;
+    int max_cells;
+};
+
+// problem-chunk width P for S problems (power of two <= 32)
+int chunk_width(int problems);
+int problem_stride(int problems);
+
+// K1: first-view generator. rays: lines*3 src + lines*3 det (device).
+void launch_generate_count(const DevGrid& g, int lines, const double* src, const double* det,
+                           uint32_t* counts, cudaStream_t st);
+void launch_generate_write(const DevGrid& g, int lines, const double* src, const double* det,
+                           const uint32_t* off, double* pa, double* pb, uint32_t* key,
+                           cudaStream_t st);
+void launch_annotate(int lines, const uint32_t* off, const double* pa, const double* pb,
+                     uint32_t* key, const RingRow* rings, cudaStream_t st);
+void launch_exclusive_scan_u32(const uint32_t* in, uint32_t* out, int n, cudaStream_t st);
+
+// traces
+void launch_trace_one(const TraceArgs& A, int line, double theta, int max_recs, int max_cells,
+                      uint32_t* out, uint32_t* count, cudaStream_t st);
+void launch_trace_counts(const TraceArgs& A, int views, int max_recs, uint32_t* cells,
+                         cudaStream_t st);
+void launch_trace_dump(const TraceArgs& A, uint32_t unit0, uint32_t units, int max_recs,
+                       int max_cells, const uint32_t* pos, uint32_t* out, cudaStream_t st);
+void launch_crossed(const TraceArgs& A, int views, int max_recs, int max_cells, uint8_t* crossed,
+                    cudaStream_t st);
+
+// K2 projector: out [units][Sp]
+void launch_project(const TraceArgs& A, int views, const float* field, int Sp, int max_recs,
+                    int max_cells, float* out, cudaStream_t st);
+
+// K3 one MART dependency level: n units of `units`, all problem chunks
+void launch_mart_level(const MartArgs* dargs, const MartArgs& hargs, const uint32_t* units, int n,
+                       cudaStream_t st);
+size_t mart_smem_bytes(const MartArgs& a);
+void mart_prepare(const MartArgs& a);  // sets smem attributes
+
+// per-problem projection statistics: stats[p*4 + {0: count>0, 1: sum>0, 2: any!=0, 3: invalid}]
+void launch_proj_stats(const float* proj, int units, int S, int Sp, double* stats, cudaStream_t st);
+// per-problem updates per sweep: sum over units with m != 0 of cells[u]
+void launch_sweep_updates(const float* proj, const uint32_t* cells, int units, int S, int Sp,
+                          unsigned long long* out, cudaStream_t st);
+// max relative change over crossed cells, per problem (as uint bits of a float)
+void launch_residual(const float* field, const float* prev, const uint8_t* crossed, uint64_t cells,
+                     int S, int Sp, unsigned int* out, cudaStream_t st);
+// count of field values that are not > 0 (reconstruct_from check)
+void launch_count_nonpositive(const float* field, uint64_t n, unsigned long long* out,
+                              cudaStream_t st);
+
+// layout transposes: [S][n] <-> [n][Sp]
+void launch_to_interleaved(const float* in, float* out, uint64_t n, int S, int Sp, float pad,
+                           cudaStream_t st);
+void launch_from_interleaved(const float* in, float* out, uint64_t n, int S, int Sp,
+                             cudaStream_t st);
+void launch_fill(float* p, uint64_t n, float v, cudaStream_t st);
+
+// K4 resample
+void launch_perm_resample(const float* field, uint64_t cells_per_slice, int slices, int S, int Sp,
+                          int n, float* out, cudaStream_t st);
+void launch_bin_map(const DevGrid& g, int npix, uint32_t* map, cudaStream_t st);
+void launch_map_resample(const float* field, uint64_t cells_per_slice, int slices, int S, int Sp,
+                         const uint32_t* map, int npix, float* out, cudaStream_t st);
+void launch_cg_map(int n, uint32_t* out, cudaStream_t st);
+
+}  // namespace ub

@@ -1,0 +1,43 @@
+#include "schedule.h"
+
+#include <algorithm>
+
+namespace ub {
+
+void AsapSchedule::add(const uint32_t* idx, const uint32_t* pos_rel, uint32_t n) {
+    level_.reserve(level_.size() + n);
+    for (uint32_t u = 0; u < n; ++u) {
+        const uint32_t b = pos_rel[u], e = pos_rel[u + 1];
+        uint32_t lev = 0;
+        for (uint32_t i = b; i < e; ++i)
+            lev = std::max(lev, last_[idx[i]]);
+        ++lev;
+        for (uint32_t i = b; i < e; ++i)
+            last_[idx[i]] = lev;
+        level_.push_back(lev);
+        max_level_ = std::max(max_level_, lev);
+    }
+}
+
+void AsapSchedule::finish(std::vector<uint32_t>& order, std::vector<uint32_t>& level_off) const {
+    level_off.assign(size_t(max_level_) + 1, 0u);
+    for (uint32_t lev : level_)
+        ++level_off[lev];  // level_off[l] counts level l (1-based) for now
+    // exclusive offsets: level l (1-based) occupies [level_off[l-1], level_off[l])
+    uint32_t acc = 0;
+    std::vector<uint32_t> start(size_t(max_level_) + 1, 0u);
+    for (uint32_t l = 1; l <= max_level_; ++l) {
+        start[l] = acc;
+        acc += level_off[l];
+    }
+    order.assign(level_.size(), 0u);
+    std::vector<uint32_t> cur(start);
+    for (uint32_t u = 0; u < level_.size(); ++u)
+        order[cur[level_[u]]++] = u;  // stable: sweep order inside a level
+    level_off.assign(size_t(max_level_) + 1, 0u);
+    for (uint32_t l = 1; l <= max_level_; ++l)
+        level_off[l - 1] = start[l];
+    level_off[max_level_] = acc;
+}
+
+}  // namespace ub

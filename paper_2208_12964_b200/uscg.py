@@ -1,0 +1,668 @@
+"""Python mirror of the reference's reconstruction API over the uscg_b200 C ABI.
+
+Names, argument meaning and error behaviour follow the reference C++ library
+(/root/reference/proj/include/uscg/*.hpp) so that code and tests written
+against ``uscg::`` read the same here:
+
+====================================  ======================================================
+reference (C++)                       here
+====================================  ======================================================
+``GridSpec`` grid.hpp:21-44            :class:`GridSpec` (+ ``ring_counts``, ``n_slices``)
+``ScanGeometry`` scan.hpp:21-41        :class:`ScanGeometry` (+ ``detector``, ``view_angles``)
+``Tracer`` tracer.hpp:85-105           :class:`Tracer` (device-resident first-view cache)
+``FirstViewCache`` tracer.hpp:18-39    :meth:`Tracer.cache`
+``Field`` / ``ProjectionSet``          :class:`Field` / :class:`ProjectionSet`
+``SolverConfig`` / ``ReconReport``     :class:`SolverConfig` / :class:`ReconReport`
+``reconstruct`` solver.hpp:78-79       :func:`reconstruct`
+``reconstruct_from`` solver.hpp:82-83  :func:`reconstruct_from`
+``generate_projections`` phantom.hpp   :func:`generate_projections` (Binary model)
+``field_to_cartesian`` phantom.hpp:56  :func:`field_to_cartesian`
+``uspg_to_cg_map`` grid.hpp:84         :func:`uspg_to_cg_map`
+====================================  ======================================================
+
+``std::invalid_argument`` surfaces as :class:`InvalidArgument` (a ValueError)
+and ``std::domain_error`` as :class:`DomainError` (an ArithmeticError).
+
+Every compute call runs the CUDA kernels of ``lib/libuscg_b200.so``; there is
+no CPU fallback. Without the library or without an sm_100 device the calls
+raise :class:`NoDevice` / ``OSError``.
+"""
+from __future__ import annotations
+
+import atexit
+import ctypes as C
+import enum
+import os
+import weakref
+from dataclasses import dataclass, field as dc_field
+from typing import Optional, Sequence
+
+import numpy as np
+
+from . import _build
+
+# ---------------------------------------------------------------------------
+# errors
+# ---------------------------------------------------------------------------
+
+
+class UscgError(RuntimeError):
+    pass
+
+
+class InvalidArgument(ValueError):
+    """std::invalid_argument in the reference."""
+
+
+class DomainError(ArithmeticError):
+    """std::domain_error in the reference."""
+
+
+class NoDevice(UscgError):
+    """No usable sm_100 device: the path has no CPU fallback."""
+
+
+DEVICE_POINTERS = 1
+LAYOUT_INTERLEAVED = 2
+
+# ---------------------------------------------------------------------------
+# ctypes structures (include/uscg_b200.h)
+# ---------------------------------------------------------------------------
+_dp = C.POINTER(C.c_double)
+_fp = C.POINTER(C.c_float)
+_u32p = C.POINTER(C.c_uint32)
+_u16p = C.POINTER(C.c_uint16)
+_u8p = C.POINTER(C.c_uint8)
+
+
+class _Grid(C.Structure):
+    _fields_ = [("n_rings", C.c_int32), ("ring_spacing", C.c_double), ("n_slices", C.c_int32),
+                ("slice_height", C.c_double), ("volume", C.c_int32), ("ring_counts", _u32p)]
+
+
+class _Scan(C.Structure):
+    _fields_ = [("detector", C.c_int32), ("source", C.c_double * 3), ("detector_center", C.c_double * 3),
+                ("det_u", C.c_int32), ("det_v", C.c_int32), ("spacing_u", C.c_double),
+                ("spacing_v", C.c_double), ("views", C.c_int32), ("view_angles_deg", _dp)]
+
+
+class _Cfg(C.Structure):
+    _fields_ = [("beta", C.c_double), ("tolerance", C.c_double), ("max_sweeps", C.c_int32),
+                ("f_init", C.c_double), ("p_floor", C.c_double)]
+
+
+class _Report(C.Structure):
+    _fields_ = [("sweeps", C.c_int32), ("converged", C.c_int32), ("all_zero_data", C.c_int32),
+                ("seconds", C.c_double), ("zero_measurement_skips", C.c_uint64),
+                ("factor_clamps", C.c_uint64), ("updates", C.c_uint64), ("sweep_residuals", _dp),
+                ("crossed", _u8p)]
+
+
+class _Info(C.Structure):
+    _fields_ = [("lines", C.c_int32), ("views", C.c_int32), ("n_rings", C.c_int32), ("n_slices", C.c_int32),
+                ("records", C.c_uint64), ("cells_per_slice", C.c_uint64), ("cell_count", C.c_uint64),
+                ("cache_bytes", C.c_uint64), ("max_line_records", C.c_int32), ("max_line_cells", C.c_int32),
+                ("cells_per_sweep", C.c_uint64), ("chords_per_sweep", C.c_uint64), ("levels", C.c_int32)]
+
+
+EXPORTS = [
+    "uscg_last_error", "uscg_version", "uscg_launch_count", "uscg_ctx_create", "uscg_ctx_destroy",
+    "uscg_ctx_set_stream", "uscg_ctx_synchronize", "uscg_first_view_rays", "uscg_tracer_create",
+    "uscg_tracer_create_from_rays", "uscg_tracer_import_cache", "uscg_tracer_destroy",
+    "uscg_tracer_get_info", "uscg_tracer_export_cache", "uscg_trace_line", "uscg_trace_counts",
+    "uscg_tracer_build_schedule", "uscg_problem_stride", "uscg_project", "uscg_reconstruct",
+    "uscg_resample", "uscg_uspg_to_cg_map",
+]
+
+_lib = None
+
+
+def library_path() -> str:
+    return _build.LIB
+
+
+def load(build_if_missing: bool = True):
+    """Load lib/libuscg_b200.so (building it in-tree when nvcc is available)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    path = _build.LIB
+    if not os.path.exists(path) or _build._stale():
+        if not build_if_missing:
+            raise OSError(f"{path} is missing: build it with `python -m paper_2208_12964_b200._build`")
+        _build.build()
+    L = C.CDLL(path)
+    vp = C.c_void_p
+    L.uscg_last_error.restype = C.c_char_p
+    L.uscg_version.restype = C.c_char_p
+    L.uscg_launch_count.restype = C.c_uint64
+    L.uscg_ctx_create.argtypes = [C.c_int32, C.POINTER(vp)]
+    L.uscg_ctx_destroy.argtypes = [vp]
+    L.uscg_ctx_set_stream.argtypes = [vp, vp]
+    L.uscg_ctx_synchronize.argtypes = [vp]
+    L.uscg_first_view_rays.argtypes = [C.POINTER(_Scan), _dp, _dp]
+    L.uscg_tracer_create.argtypes = [vp, C.POINTER(_Grid), C.POINTER(_Scan), C.c_int32, C.POINTER(vp)]
+    L.uscg_tracer_create_from_rays.argtypes = [vp, C.POINTER(_Grid), C.c_int32, _dp, _dp, C.c_int32, _dp,
+                                               C.POINTER(vp)]
+    L.uscg_tracer_import_cache.argtypes = [vp, C.POINTER(_Grid), C.c_int32, _u32p, C.c_uint64, _dp, _dp, _u16p,
+                                           _u16p, C.c_int32, _dp, C.POINTER(vp)]
+    L.uscg_tracer_destroy.argtypes = [vp]
+    L.uscg_tracer_get_info.argtypes = [vp, C.POINTER(_Info)]
+    L.uscg_tracer_export_cache.argtypes = [vp, _u32p, _dp, _dp, _u16p, _u16p]
+    L.uscg_trace_line.argtypes = [vp, C.c_int32, C.c_double, _u32p, C.c_int64, C.POINTER(C.c_int64)]
+    L.uscg_trace_counts.argtypes = [vp, _u32p]
+    L.uscg_tracer_build_schedule.argtypes = [vp]
+    L.uscg_problem_stride.argtypes = [C.c_int32]
+    L.uscg_problem_stride.restype = C.c_int32
+    L.uscg_project.argtypes = [vp, vp, C.c_int32, vp, C.c_uint32]
+    L.uscg_reconstruct.argtypes = [vp, vp, C.c_int32, C.POINTER(_Cfg), vp, C.c_int32, C.POINTER(_Report),
+                                   C.c_uint32]
+    L.uscg_resample.argtypes = [vp, C.POINTER(_Grid), vp, C.c_int32, C.c_int32, vp, C.c_uint32]
+    L.uscg_uspg_to_cg_map.argtypes = [vp, C.c_int32, _u32p]
+    for name in EXPORTS:
+        if name not in ("uscg_last_error", "uscg_version", "uscg_launch_count", "uscg_problem_stride"):
+            getattr(L, name).restype = C.c_int
+    _lib = L
+    return L
+
+
+def _check(rc: int) -> None:
+    if rc == 0:
+        return
+    msg = load().uscg_last_error().decode()
+    if rc == 1:
+        raise InvalidArgument(msg)
+    if rc == 2:
+        raise DomainError(msg)
+    if rc == 4:
+        raise NoDevice(msg)
+    raise UscgError(f"uscg_b200 error {rc}: {msg}")
+
+
+def launch_count() -> int:
+    return int(load().uscg_launch_count())
+
+
+def problem_stride(problems: int) -> int:
+    return int(load().uscg_problem_stride(problems))
+
+
+# ---------------------------------------------------------------------------
+# context
+# ---------------------------------------------------------------------------
+
+
+class Context:
+    """Device + stream (uscg_ctx). One per device is plenty."""
+
+    def __init__(self, device: int = 0):
+        L = load()
+        h = C.c_void_p()
+        _check(L.uscg_ctx_create(device, C.byref(h)))
+        self.h = h
+        self.device = device
+
+    def set_stream(self, stream_ptr: Optional[int]) -> None:
+        _check(load().uscg_ctx_set_stream(self.h, C.c_void_p(stream_ptr or 0)))
+
+    def synchronize(self) -> None:
+        _check(load().uscg_ctx_synchronize(self.h))
+
+    def close(self) -> None:
+        h, self.h = getattr(self, "h", None), None
+        if h and _lib is not None:
+            _lib.uscg_ctx_destroy(h)
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+_default_ctx: Optional[Context] = None
+_live_tracers: "weakref.WeakSet" = weakref.WeakSet()
+
+
+@atexit.register
+def _release_all() -> None:
+    """Free device state while the library is still loaded: tracers first,
+    then the default context (module teardown order is otherwise arbitrary)."""
+    global _default_ctx
+    for t in list(_live_tracers):
+        t.close()
+    if _default_ctx is not None:
+        _default_ctx.close()
+        _default_ctx = None
+
+
+def default_context() -> Context:
+    global _default_ctx
+    if _default_ctx is None:
+        _default_ctx = Context(0)
+    return _default_ctx
+
+
+# ---------------------------------------------------------------------------
+# grid / scan
+# ---------------------------------------------------------------------------
+
+
+class GridMode(enum.Enum):
+    Slice2D = 0
+    Volume3D = 1
+
+
+@dataclass
+class GridSpec:
+    """GridSpec (grid.hpp:21-44). ``n`` is the image size: n/2 rings and, in 3D
+    by default, n slices. Generalized seams: ``ring_counts`` (per-ring sector
+    counts, None = the reference 4(2k-1) law) and ``n_slices``."""
+
+    n: int = 0
+    ring_spacing: float = 0.0
+    slice_height: float = 0.0
+    mode: GridMode = GridMode.Slice2D
+    ring_counts: Optional[np.ndarray] = None
+    n_slices: Optional[int] = None
+
+    @staticmethod
+    def square_2d(n: int) -> "GridSpec":
+        return GridSpec(n, 2.0 / n, 2.0 / n, GridMode.Slice2D)
+
+    @staticmethod
+    def cube_3d(n: int) -> "GridSpec":
+        return GridSpec(n, 2.0 / n, 2.0 / n, GridMode.Volume3D)
+
+    def rings(self) -> int:
+        return self.n // 2
+
+    def slices(self) -> int:
+        if self.mode != GridMode.Volume3D:
+            return 1
+        return self.n if self.n_slices is None else int(self.n_slices)
+
+    def radius(self) -> float:
+        return 0.5 * self.n * self.ring_spacing
+
+    def counts(self) -> np.ndarray:
+        if self.ring_counts is not None:
+            return np.asarray(self.ring_counts, dtype=np.uint32)
+        k = np.arange(1, self.rings() + 1)
+        return (4 * (2 * k - 1)).astype(np.uint32)
+
+    def cells_per_slice(self) -> int:
+        return int(self.counts().astype(np.int64).sum())
+
+    def cell_count(self) -> int:
+        return self.cells_per_slice() * self.slices()
+
+    def is_reference_law(self) -> bool:
+        return self.ring_counts is None
+
+    def _c(self):
+        cnt = None if self.ring_counts is None else np.ascontiguousarray(self.ring_counts, dtype=np.uint32)
+        g = _Grid(self.rings(), float(self.ring_spacing), self.slices(), float(self.slice_height),
+                  1 if self.mode == GridMode.Volume3D else 0,
+                  cnt.ctypes.data_as(_u32p) if cnt is not None else None)
+        return g, cnt  # keep cnt alive with the struct
+
+
+def ring_counts_m1(n_rings: int) -> np.ndarray:
+    """BASELINE.json sector law: ring i (0-based) has round(2*pi*(i+0.5)) cells."""
+    i = np.arange(n_rings, dtype=np.float64)
+    return np.floor(2.0 * np.pi * (i + 0.5) + 0.5).astype(np.uint32)
+
+
+class Detector(enum.IntEnum):
+    Flat = 0
+    Arc = 1
+    Parallel = 2
+
+
+@dataclass
+class ScanGeometry:
+    """ScanGeometry (scan.hpp:21-41) + detector kind and view-angle list."""
+
+    source: Sequence[float] = (0.0, 0.0, 0.0)
+    detector_center: Sequence[float] = (0.0, 0.0, 0.0)
+    det_u: int = 1
+    det_v: int = 1
+    spacing_u: float = 0.0
+    spacing_v: float = 0.0
+    views: int = 1
+    detector: Detector = Detector.Flat
+    view_angles: Optional[np.ndarray] = None
+
+    def step_deg(self) -> float:
+        return 360.0 / self.views
+
+    def lines(self) -> int:
+        return self.det_u * self.det_v
+
+    def thetas(self) -> np.ndarray:
+        if self.view_angles is not None:
+            return np.asarray(self.view_angles, dtype=np.float64)
+        step = self.step_deg()
+        return np.array([v * step for v in range(self.views)], dtype=np.float64)
+
+    def _c(self):
+        ang = None if self.view_angles is None else np.ascontiguousarray(self.view_angles, dtype=np.float64)
+        s = _Scan(int(self.detector), (C.c_double * 3)(*[float(x) for x in self.source]),
+                  (C.c_double * 3)(*[float(x) for x in self.detector_center]), int(self.det_u), int(self.det_v),
+                  float(self.spacing_u), float(self.spacing_v), int(self.views),
+                  ang.ctypes.data_as(_dp) if ang is not None else None)
+        return s, ang
+
+    def first_view_rays(self):
+        """line_endpoints for every line of the first view, (lines, 3) x 2."""
+        s, keep = self._c()
+        src = np.zeros((self.lines(), 3))
+        det = np.zeros((self.lines(), 3))
+        _check(load().uscg_first_view_rays(C.byref(s), src.ctypes.data_as(_dp), det.ctypes.data_as(_dp)))
+        return src, det
+
+
+# ---------------------------------------------------------------------------
+# tracer
+# ---------------------------------------------------------------------------
+
+
+@dataclass
+class FirstViewCache:
+    offsets: np.ndarray
+    phi_a: np.ndarray
+    phi_b: np.ndarray
+    slice: np.ndarray
+    ring: np.ndarray
+
+    def line_count(self) -> int:
+        return self.offsets.size - 1
+
+    def record_count(self) -> int:
+        return self.phi_a.size
+
+    def byte_size(self) -> int:
+        """Reference accounting (24-byte SegmentRecord + u32 offsets)."""
+        return self.record_count() * 24 + self.offsets.size * 4
+
+
+class Tracer:
+    """Tracer (tracer.hpp:85-105): owns the device-resident first-view cache
+    built by the K1 generator kernels, and traces any (line, view) on the
+    device. ``from_rays`` and ``from_cache`` are the two other constructors of
+    the C ABI (explicit rays; adopt an existing FirstViewCache)."""
+
+    def __init__(self, geom: ScanGeometry, spec: GridSpec, quarter_symmetry: bool = False, threads: int = 1,
+                 ctx: Optional[Context] = None, _handle=None):
+        self.ctx = ctx or default_context()
+        self.geom = geom
+        self.spec = spec
+        if _handle is not None:
+            self.h = _handle
+        else:
+            g, keep1 = spec._c()
+            s, keep2 = geom._c()
+            h = C.c_void_p()
+            _check(load().uscg_tracer_create(self.ctx.h, C.byref(g), C.byref(s), int(bool(quarter_symmetry)),
+                                             C.byref(h)))
+            self.h = h
+        self._info = None
+        _live_tracers.add(self)
+
+    @classmethod
+    def from_rays(cls, spec: GridSpec, src, det, views: int, view_angles=None, geom: Optional[ScanGeometry] = None,
+                  ctx: Optional[Context] = None) -> "Tracer":
+        ctx = ctx or default_context()
+        src = np.ascontiguousarray(src, dtype=np.float64)
+        det = np.ascontiguousarray(det, dtype=np.float64)
+        ang = None if view_angles is None else np.ascontiguousarray(view_angles, dtype=np.float64)
+        g, keep = spec._c()
+        h = C.c_void_p()
+        _check(load().uscg_tracer_create_from_rays(ctx.h, C.byref(g), src.shape[0], src.ctypes.data_as(_dp),
+                                                   det.ctypes.data_as(_dp), views,
+                                                   ang.ctypes.data_as(_dp) if ang is not None else None,
+                                                   C.byref(h)))
+        if geom is None:
+            geom = ScanGeometry(det_u=src.shape[0], views=views, view_angles=ang)
+        return cls(geom, spec, ctx=ctx, _handle=h)
+
+    @classmethod
+    def from_cache(cls, spec: GridSpec, cache: FirstViewCache, views: int, view_angles=None,
+                   geom: Optional[ScanGeometry] = None, ctx: Optional[Context] = None) -> "Tracer":
+        ctx = ctx or default_context()
+        off = np.ascontiguousarray(cache.offsets, dtype=np.uint32)
+        pa = np.ascontiguousarray(cache.phi_a, dtype=np.float64)
+        pb = np.ascontiguousarray(cache.phi_b, dtype=np.float64)
+        sl = np.ascontiguousarray(cache.slice, dtype=np.uint16)
+        rg = np.ascontiguousarray(cache.ring, dtype=np.uint16)
+        ang = None if view_angles is None else np.ascontiguousarray(view_angles, dtype=np.float64)
+        g, keep = spec._c()
+        h = C.c_void_p()
+        _check(load().uscg_tracer_import_cache(ctx.h, C.byref(g), off.size - 1, off.ctypes.data_as(_u32p), pa.size,
+                                               pa.ctypes.data_as(_dp), pb.ctypes.data_as(_dp),
+                                               sl.ctypes.data_as(_u16p), rg.ctypes.data_as(_u16p), views,
+                                               ang.ctypes.data_as(_dp) if ang is not None else None, C.byref(h)))
+        if geom is None:
+            geom = ScanGeometry(det_u=off.size - 1, views=views, view_angles=ang)
+        return cls(geom, spec, ctx=ctx, _handle=h)
+
+    def close(self) -> None:
+        h, self.h = getattr(self, "h", None), None
+        if h and _lib is not None:
+            _lib.uscg_tracer_destroy(h)
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # -- introspection -------------------------------------------------------
+    def info(self) -> dict:
+        i = _Info()
+        _check(load().uscg_tracer_get_info(self.h, C.byref(i)))
+        return {k: getattr(i, k) for k, _ in _Info._fields_}
+
+    def cache(self) -> FirstViewCache:
+        inf = self.info()
+        n, L = inf["records"], inf["lines"]
+        off = np.zeros(L + 1, np.uint32)
+        pa = np.zeros(n); pb = np.zeros(n)
+        sl = np.zeros(n, np.uint16); rg = np.zeros(n, np.uint16)
+        _check(load().uscg_tracer_export_cache(self.h, off.ctypes.data_as(_u32p), pa.ctypes.data_as(_dp),
+                                               pb.ctypes.data_as(_dp), sl.ctypes.data_as(_u16p),
+                                               rg.ctypes.data_as(_u16p)))
+        return FirstViewCache(off, pa, pb, sl, rg)
+
+    def trace_line(self, line: int, theta_deg: float) -> np.ndarray:
+        """Tracer::trace_line: deduplicated active cells, reference emission order."""
+        inf = self.info()
+        cap = inf["max_line_cells"] + inf["max_line_records"] + 1
+        out = np.zeros(cap, np.uint32)
+        n = C.c_int64()
+        _check(load().uscg_trace_line(self.h, int(line), float(theta_deg), out.ctypes.data_as(_u32p), cap,
+                                      C.byref(n)))
+        return out[: n.value].copy()
+
+    def trace_counts(self) -> np.ndarray:
+        inf = self.info()
+        out = np.zeros(inf["views"] * inf["lines"], np.uint32)
+        _check(load().uscg_trace_counts(self.h, out.ctypes.data_as(_u32p)))
+        return out.reshape(inf["views"], inf["lines"])
+
+    def build_schedule(self) -> int:
+        _check(load().uscg_tracer_build_schedule(self.h))
+        return self.info()["levels"]
+
+
+# ---------------------------------------------------------------------------
+# solver types
+# ---------------------------------------------------------------------------
+
+
+@dataclass
+class Field:
+    spec: GridSpec
+    values: np.ndarray
+
+    @staticmethod
+    def constant(spec: GridSpec, value: float) -> "Field":
+        return Field(spec, np.full(spec.cell_count(), float(value)))
+
+
+@dataclass
+class ProjectionSet:
+    geometry: ScanGeometry
+    data: np.ndarray  # (views, lines) or flat view-major
+
+    def at(self, view: int, line: int) -> float:
+        return float(np.asarray(self.data).reshape(-1)[view * self.geometry.lines() + line])
+
+
+@dataclass
+class SolverConfig:
+    beta: float = 0.4
+    tolerance: float = 1e-6
+    max_sweeps: int = 100
+    f_init: float = 1.0
+    p_floor: float = 0.0
+
+
+@dataclass
+class ReconReport:
+    sweep_residuals: list = dc_field(default_factory=list)
+    sweeps: int = 0
+    converged: bool = False
+    all_zero_data: bool = False
+    seconds: float = 0.0
+    zero_measurement_skips: int = 0
+    factor_clamps: int = 0
+    updates: int = 0
+    crossed: Optional[np.ndarray] = None
+
+
+@dataclass
+class ReconResult:
+    field: Field
+    report: ReconReport
+
+
+def _ptr(a: np.ndarray):
+    return C.c_void_p(a.ctypes.data)
+
+
+def _validate_field(field_values: np.ndarray, spec: GridSpec):
+    if field_values.size != spec.cell_count():
+        raise InvalidArgument("field length does not match its grid")
+
+
+def generate_projections(field: Field, geom: ScanGeometry, model: str = "binary",
+                         tracer: Optional[Tracer] = None) -> ProjectionSet:
+    """generate_projections (phantom.cpp:182-211), Binary model on the device."""
+    if model.lower() != "binary":
+        raise InvalidArgument("only the binary forward model runs on the device path")
+    vals = np.ascontiguousarray(field.values, dtype=np.float32).reshape(-1)
+    _validate_field(vals, field.spec)
+    if tracer is None:
+        tracer = Tracer(geom, field.spec, False)
+    out = project_stack(tracer, vals[None, :])
+    return ProjectionSet(geom, out[0].astype(np.float64))
+
+
+def project_stack(tracer: Tracer, fields: np.ndarray) -> np.ndarray:
+    """Binary projections of S independent fields sharing one tracer:
+    fields (S, cell_count) -> (S, views, lines), float32."""
+    f = np.ascontiguousarray(fields, dtype=np.float32)
+    S = f.shape[0]
+    inf = tracer.info()
+    out = np.zeros((S, inf["views"], inf["lines"]), np.float32)
+    _check(load().uscg_project(tracer.h, _ptr(f), S, _ptr(out), 0))
+    return out
+
+
+def _run(proj_data: np.ndarray, init: Optional[np.ndarray], cfg: SolverConfig, tracer: Tracer, S: int,
+         with_crossed: bool = True):
+    inf = tracer.info()
+    p = np.ascontiguousarray(proj_data, dtype=np.float32).reshape(S, -1)
+    if p.shape[1] != inf["views"] * inf["lines"]:
+        raise InvalidArgument(f"projection data size does not match geometry: got {p.shape[1]}, "
+                              f"expected {inf['views'] * inf['lines']}")
+    cells = inf["cell_count"]
+    if init is None:
+        fld = np.zeros((S, cells), np.float32)
+        from_init = 0
+    else:
+        fld = np.array(init, dtype=np.float32, copy=True).reshape(S, cells)
+        from_init = 1
+    reps = (_Report * S)()
+    resid = [np.zeros(cfg.max_sweeps) for _ in range(S)]
+    crossed = [np.zeros(cells, np.uint8) for _ in range(S)] if with_crossed else None
+    for i in range(S):
+        reps[i].sweep_residuals = resid[i].ctypes.data_as(_dp)
+        reps[i].crossed = crossed[i].ctypes.data_as(_u8p) if with_crossed else None
+    c = _Cfg(cfg.beta, cfg.tolerance, cfg.max_sweeps, cfg.f_init, cfg.p_floor)
+    _check(load().uscg_reconstruct(tracer.h, _ptr(p), S, C.byref(c), _ptr(fld), from_init, reps, 0))
+    out = []
+    for i in range(S):
+        r = reps[i]
+        rep = ReconReport(
+            sweep_residuals=list(resid[i][: r.sweeps]) if cfg.tolerance > 0 else [],
+            sweeps=r.sweeps, converged=bool(r.converged), all_zero_data=bool(r.all_zero_data),
+            seconds=r.seconds, zero_measurement_skips=int(r.zero_measurement_skips),
+            factor_clamps=int(r.factor_clamps), updates=int(r.updates),
+            crossed=crossed[i] if with_crossed else None)
+        out.append((fld[i], rep))
+    return out
+
+
+def reconstruct(proj: ProjectionSet, spec: GridSpec, cfg: SolverConfig, tracer: Tracer) -> ReconResult:
+    """reconstruct (solver.cpp:166-169): start from cfg.f_init everywhere."""
+    (f, rep), = _run(np.asarray(proj.data), None, cfg, tracer, 1)
+    return ReconResult(Field(spec, f.astype(np.float64)), rep)
+
+
+def reconstruct_from(proj: ProjectionSet, init: Field, cfg: SolverConfig, tracer: Tracer) -> ReconResult:
+    """reconstruct_from (solver.cpp:171-177): start from `init` (must be > 0)."""
+    vals = np.asarray(init.values, dtype=np.float64)
+    if not np.all(vals > 0):
+        raise InvalidArgument("initial field must be strictly positive")
+    (f, rep), = _run(np.asarray(proj.data), vals, cfg, tracer, 1)
+    return ReconResult(Field(init.spec, f.astype(np.float64)), rep)
+
+
+def reconstruct_stack(projections: np.ndarray, cfg: SolverConfig, tracer: Tracer,
+                      init: Optional[np.ndarray] = None, with_crossed: bool = False):
+    """S independent reconstructions sharing one tracer (the 2D slice stack):
+    projections (S, views, lines) -> list of (field (cell_count,), ReconReport)."""
+    S = projections.shape[0]
+    return _run(projections, init, cfg, tracer, S, with_crossed)
+
+
+def field_to_cartesian(field: Field, npix: Optional[int] = None, ctx: Optional[Context] = None) -> np.ndarray:
+    """field_to_cartesian (phantom.cpp:149-163): (slices, npix, npix), row 0 at the bottom.
+    Reference law with npix = n: the one-to-one permutation; otherwise the
+    bin-point rule at pixel centres."""
+    ctx = ctx or default_context()
+    spec = field.spec
+    npix = spec.n if npix is None else npix
+    vals = np.ascontiguousarray(field.values, dtype=np.float32).reshape(-1)
+    _validate_field(vals, spec)
+    return resample_stack(spec, vals[None, :], npix, ctx)[0]
+
+
+def resample_stack(spec: GridSpec, fields: np.ndarray, npix: int, ctx: Optional[Context] = None) -> np.ndarray:
+    ctx = ctx or default_context()
+    f = np.ascontiguousarray(fields, dtype=np.float32)
+    S = f.shape[0]
+    out = np.zeros((S, spec.slices(), npix, npix), np.float32)
+    g, keep = spec._c()
+    _check(load().uscg_resample(ctx.h, C.byref(g), _ptr(f), S, npix, _ptr(out), 0))
+    return out
+
+
+def uspg_to_cg_map(n: int, ctx: Optional[Context] = None) -> np.ndarray:
+    ctx = ctx or default_context()
+    out = np.zeros(max(n, 0) * max(n, 0), np.uint32)
+    _check(load().uscg_uspg_to_cg_map(ctx.h, n, out.ctypes.data_as(_u32p)))
+    return out

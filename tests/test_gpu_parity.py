@@ -1,0 +1,422 @@
+"""Device path vs the reference library / oracle on the same seeded inputs.
+
+Every call goes through the C ABI (lib/libuscg_b200.so). Tolerances:
+- indices, offsets, slice/ring, counters, crossed masks: bit-exact;
+- generator azimuths (fp64): bit-exact except ulp-level atan2 differences
+  (CUDA atan2 vs glibc), gated at <= 4 ulp;
+- projections: fp32 field summed in fp64 vs the reference's fp64: rel <= 1e-6;
+- reconstructed fields after a few sweeps (fp32 vs fp64): max rel <= 1e-4
+  (SURVEY.md §8(c) measured fp32 drift <= 8.2e-6 after 10-20 sweeps).
+"""
+import numpy as np
+import pytest
+
+from refgeoms import REF_GEOMS, cache_from_ref, ref_tracer, thetas, ub_spec_geom, ulp_diff
+
+pytestmark = pytest.mark.gpu
+
+
+def _ub_tracer(ub, g):
+    spec, geom = ub_spec_geom(ub, g)
+    return spec, geom, ub.Tracer(geom, spec, False)
+
+
+# ---------------------------------------------------------------------------
+# K1 generator: FirstViewCache structure
+# ---------------------------------------------------------------------------
+
+
+@pytest.mark.parametrize("name", ["fan32", "fan64q", "fan16", "cone16", "cone32", "fan128", "cone12", "cone32w"])
+def test_generator_cache_matches_reference(ub, ref, name):
+    g = REF_GEOMS[name]
+    spec, geom, tr = _ub_tracer(ub, g)
+    c = tr.cache()
+    off, pa, pb, sl, rg = ref_tracer(ref, g).cache()
+    assert np.array_equal(c.offsets, off)
+    assert np.array_equal(c.slice, sl)
+    assert np.array_equal(c.ring, rg)
+    da, db = ulp_diff(c.phi_a, pa), ulp_diff(c.phi_b, pb)
+    assert max(da.max(initial=0), db.max(initial=0)) <= 4, "azimuths beyond 4 ulp"
+
+
+@pytest.mark.parametrize("name", ["fan64q", "cone32"])
+def test_quarter_symmetric_tracer_is_identical(ub, name):
+    g = REF_GEOMS[name]
+    spec, geom = ub_spec_geom(ub, g)
+    a = ub.Tracer(geom, spec, False).cache()
+    b = ub.Tracer(geom, spec, True).cache()
+    for x, y in zip((a.offsets, a.phi_a, a.phi_b, a.slice, a.ring), (b.offsets, b.phi_a, b.phi_b, b.slice, b.ring)):
+        assert np.array_equal(x, y)
+
+
+def test_quarter_symmetry_rejects_asymmetric_panels(ub):
+    spec = ub.GridSpec.square_2d(16)
+    geom = ub.ScanGeometry(source=(-8, 0, 0), detector_center=(8, 0, 0), det_u=24, spacing_u=0.05, views=10)
+    with pytest.raises(ub.InvalidArgument):
+        ub.Tracer(geom, spec, True)
+
+
+# ---------------------------------------------------------------------------
+# per-view trace: index lists bit-exact
+# ---------------------------------------------------------------------------
+
+
+@pytest.mark.parametrize("name", ["fan32", "fan16", "cone16", "cone12", "fan64q"])
+def test_trace_line_matches_reference_every_view(ub, ref, name):
+    g = REF_GEOMS[name]
+    rt = ref_tracer(ref, g)
+    spec, geom = ub_spec_geom(ub, g)
+    tr_imp = ub.Tracer.from_cache(spec, cache_from_ref(ub, rt), g["views"])
+    tr_gen = ub.Tracer(geom, spec, False)
+    th = thetas(g["views"])
+    for v in range(g["views"]):
+        for line in range(g["du"] * g["dv"]):
+            want = rt.trace_line(line, th[v])
+            assert np.array_equal(tr_imp.trace_line(line, th[v]), want), (v, line)
+            assert np.array_equal(tr_gen.trace_line(line, th[v]), want), (v, line)
+
+
+def test_trace_line_arbitrary_angles(ub, ref):
+    g = REF_GEOMS["fan32"]
+    rt = ref_tracer(ref, g)
+    spec, geom = ub_spec_geom(ub, g)
+    tr = ub.Tracer.from_cache(spec, cache_from_ref(ub, rt), g["views"])
+    rng = np.random.default_rng(101)
+    for _ in range(300):
+        line = int(rng.integers(0, g["du"]))
+        theta = float(rng.uniform(0, 720.0))
+        assert np.array_equal(tr.trace_line(line, theta), rt.trace_line(line, theta))
+    # a full turn is the identity
+    for line in range(g["du"]):
+        assert np.array_equal(tr.trace_line(line, 360.0), tr.trace_line(line, 0.0))
+
+
+def test_trace_counts_match_reference(ub, ref):
+    g = REF_GEOMS["cone32"]
+    rt = ref_tracer(ref, g)
+    spec, geom, tr = _ub_tracer(ub, g)
+    counts = tr.trace_counts()
+    th = thetas(g["views"])
+    for v in range(g["views"]):
+        for line in range(0, g["du"] * g["dv"], 7):
+            assert counts[v, line] == rt.trace_line(line, th[v]).size
+
+
+@pytest.mark.parametrize("rec,theta,want", [
+    ((95.0, 40.0, 0, 2), 0.0, [5, 6, 7]),
+    ((350.0, 10.0, 0, 2), 0.0, [15, 4]),
+    ((65.0, 10.0, 0, 2), 30.0, [5, 6, 7]),
+    ((10.0, 190.0, 0, 2), 0.0, [4, 5, 6, 7, 8, 9, 10]),
+    ((45.0, 45.0, 0, 2), 0.0, [5]),
+])
+def test_trace_chord_worked_examples(ub, rec, theta, want):
+    """proj/tests/test_tracer.cpp:60-98 through a one-record imported cache."""
+    spec = ub.GridSpec.square_2d(8)
+    cache = ub.FirstViewCache(np.array([0, 1], np.uint32), np.array([rec[0]]), np.array([rec[1]]),
+                              np.array([rec[2]], np.uint16), np.array([rec[3]], np.uint16))
+    tr = ub.Tracer.from_cache(spec, cache, 1)
+    assert tr.trace_line(0, theta).tolist() == want
+
+
+def test_trace_chord_slice_offset(ub):
+    spec = ub.GridSpec.cube_3d(8)
+    cache = ub.FirstViewCache(np.array([0, 1], np.uint32), np.array([95.0]), np.array([40.0]),
+                              np.array([3], np.uint16), np.array([2], np.uint16))
+    tr = ub.Tracer.from_cache(spec, cache, 1)
+    assert tr.trace_line(0, 0.0).tolist() == [3 * 64 + 5, 3 * 64 + 6, 3 * 64 + 7]
+
+
+def test_dedup_of_overlapping_chords(ub, ref):
+    """Two records of one (slice, ring) sharing sectors: the stamp dedup
+    (tracer.cpp:181-195) keeps the first occurrence only."""
+    spec = ub.GridSpec.square_2d(8)
+    cache = ub.FirstViewCache(np.array([0, 3], np.uint32), np.array([95.0, 50.0, 80.0]),
+                              np.array([40.0, 20.0, 100.0]), np.zeros(3, np.uint16),
+                              np.array([2, 2, 3], np.uint16))
+    tr = ub.Tracer.from_cache(spec, cache, 1)
+    # ring 2 (12 cells, head 4): 95/40 -> 5,6,7 ; 50/20 -> 4,5 (5 dup) ; ring 3 (20 cells, head 16): 80/100 -> 20,21
+    assert tr.trace_line(0, 0.0).tolist() == [5, 6, 7, 4, 20, 21]
+    # +40: 135/80 -> 6,7,8 ; 90/60 -> 6,7 (both dup) ; 120/140 -> 22,23
+    assert tr.trace_line(0, 40.0).tolist() == [6, 7, 8, 22, 23]
+
+
+# ---------------------------------------------------------------------------
+# K2 projector
+# ---------------------------------------------------------------------------
+
+
+@pytest.mark.parametrize("name", ["fan128", "cone32", "fan16"])
+def test_project_matches_reference(ub, ref, name):
+    g = REF_GEOMS[name]
+    rt = ref_tracer(ref, g)
+    spec, geom, tr = _ub_tracer(ub, g)
+    rng = np.random.default_rng(7)
+    f = rng.uniform(0.0, 5.0, spec.cell_count()).astype(np.float32)
+    got = ub.generate_projections(ub.Field(spec, f), geom, "binary", tr).data
+    want = rt.project(f.astype(np.float64))
+    np.testing.assert_allclose(got, want, rtol=1e-6, atol=1e-5)
+    ones = ub.generate_projections(ub.Field.constant(spec, 1.0), geom, "binary", tr).data
+    assert np.array_equal(ones, tr.trace_counts().astype(np.float64))
+
+
+def test_project_linearity_and_zero(ub, ref):
+    g = REF_GEOMS["fan16"]
+    spec, geom, tr = _ub_tracer(ub, g)
+    rng = np.random.default_rng(13)
+    f1 = rng.uniform(0, 2, spec.cell_count())
+    f2 = rng.uniform(0, 2, spec.cell_count())
+    p = ub.project_stack(tr, np.stack([f1, f2, 0.75 * f1 + 1.5 * f2, 0 * f1]))
+    np.testing.assert_allclose(p[2], 0.75 * p[0] + 1.5 * p[1], rtol=1e-5)
+    assert np.all(p[3] == 0)
+
+
+# ---------------------------------------------------------------------------
+# K3 MART
+# ---------------------------------------------------------------------------
+
+
+def _check_recon(ub, ref, name, phantom, beta, sweeps, tol=1e-30, rtol=1e-4):
+    g = REF_GEOMS[name]
+    rt = ref_tracer(ref, g)
+    spec, geom, tr = _ub_tracer(ub, g)
+    if phantom == "shepp":
+        truth = ref.phantom(g["n"], g["volume"])
+    else:
+        truth = np.random.default_rng(42).uniform(0.2, 3.0, spec.cell_count())
+    proj = rt.project(truth)
+    want, wrep = rt.reconstruct(proj, beta=beta, tolerance=tol, max_sweeps=sweeps)
+    res = ub.reconstruct(ub.ProjectionSet(geom, proj), spec, ub.SolverConfig(beta=beta, tolerance=tol,
+                                                                             max_sweeps=sweeps), tr)
+    got, rep = res.field.values, res.report
+    rel = np.abs(got - want) / np.abs(want)
+    assert rel.max() <= rtol, rel.max()
+    assert rep.sweeps == wrep["sweeps"]
+    assert rep.zero_measurement_skips == wrep["zero_measurement_skips"]
+    assert rep.factor_clamps == wrep["factor_clamps"]
+    assert np.array_equal(rep.crossed, wrep["crossed"])
+    if tol > 0:
+        np.testing.assert_allclose(rep.sweep_residuals, wrep["sweep_residuals"], rtol=5e-2, atol=1e-6)
+    return got, want
+
+
+def test_reconstruct_matches_reference_fan_shepp(ub, ref):
+    _check_recon(ub, ref, "fan128", "shepp", beta=0.4, sweeps=5)
+
+
+def test_reconstruct_matches_reference_cone(ub, ref):
+    _check_recon(ub, ref, "cone32", "random", beta=0.4, sweeps=3)
+
+
+def test_reconstruct_matches_reference_cone_wide(ub, ref):
+    _check_recon(ub, ref, "cone32w", "random", beta=1.0, sweeps=2, rtol=2e-4)
+
+
+def test_reconstruct_residual_stopping(ub, ref):
+    g = REF_GEOMS["fan16"]
+    rt = ref_tracer(ref, g)
+    spec, geom, tr = _ub_tracer(ub, g)
+    truth = np.random.default_rng(42).uniform(0.2, 3.0, spec.cell_count())
+    proj = rt.project(truth)
+    res = ub.reconstruct(ub.ProjectionSet(geom, proj), spec, ub.SolverConfig(beta=1.0, tolerance=1e-5,
+                                                                             max_sweeps=20000), tr)
+    assert res.report.converged
+    re = ub.generate_projections(res.field, geom, "binary", tr).data
+    nz = proj != 0
+    assert np.all(re[~nz] == 0)
+    np.testing.assert_allclose(re[nz] / proj[nz], 1.0, atol=2e-4)
+
+
+def test_reconstruct_from_resumes(ub, ref):
+    """Blocks of sweeps through reconstruct_from equal one long run
+    (the acceptance runner's resume pattern, acceptance.cpp:537-547)."""
+    g = REF_GEOMS["fan16"]
+    rt = ref_tracer(ref, g)
+    spec, geom, tr = _ub_tracer(ub, g)
+    truth = np.random.default_rng(3).uniform(0.2, 3.0, spec.cell_count())
+    proj = ub.ProjectionSet(geom, rt.project(truth))
+    cfg = ub.SolverConfig(beta=0.4, tolerance=0, max_sweeps=3)
+    a = ub.reconstruct(proj, spec, cfg, tr).field
+    b = ub.reconstruct_from(proj, a, cfg, tr).field
+    c = ub.reconstruct(proj, spec, ub.SolverConfig(beta=0.4, tolerance=0, max_sweeps=6), tr).field
+    assert np.array_equal(b.values.astype(np.float32), c.values.astype(np.float32))
+
+
+def test_untouched_cells_keep_initial_value(ub, ref):
+    spec = ub.GridSpec.square_2d(16)
+    geom = ub.ScanGeometry(source=(-8, 0, 0), detector_center=(8, 0, 0), det_u=11, spacing_u=0.05, views=6)
+    tr = ub.Tracer(geom, spec, False)
+    truth = np.random.default_rng(42).uniform(0.2, 3.0, spec.cell_count())
+    proj = ub.generate_projections(ub.Field(spec, truth), geom, "binary", tr)
+    res = ub.reconstruct(proj, spec, ub.SolverConfig(beta=0.7, f_init=1.375, max_sweeps=5, tolerance=1e-30), tr)
+    untouched = res.report.crossed == 0
+    assert untouched.sum() > 0
+    assert np.all(res.field.values[untouched] == 1.375)
+
+
+def test_positivity_across_relaxations(ub):
+    spec = ub.GridSpec.square_2d(16)
+    geom = ub.ScanGeometry(source=(-8, 0, 0), detector_center=(8, 0, 0), det_u=21, spacing_u=0.2, views=20)
+    tr = ub.Tracer(geom, spec, False)
+    truth = np.random.default_rng(42).uniform(0.2, 3.0, spec.cell_count())
+    proj = ub.generate_projections(ub.Field(spec, truth), geom, "binary", tr)
+    for beta in (0.4, 1.0, 1.9):
+        res = ub.reconstruct(proj, spec, ub.SolverConfig(beta=beta, tolerance=0, max_sweeps=100), tr)
+        assert np.all(res.field.values > 0)
+
+
+def test_input_errors(ub):
+    spec = ub.GridSpec.square_2d(16)
+    geom = ub.ScanGeometry(source=(-8, 0, 0), detector_center=(8, 0, 0), det_u=21, spacing_u=0.2, views=8)
+    tr = ub.Tracer(geom, spec, False)
+    zeros = ub.ProjectionSet(geom, np.zeros((8, 21)))
+    res = ub.reconstruct(zeros, spec, ub.SolverConfig(), tr)
+    assert res.report.all_zero_data and res.report.sweeps == 0
+    assert np.all(res.field.values == 1.0)
+    bad = np.ones((8, 21))
+    bad[0, 3] = np.nan
+    with pytest.raises(ub.InvalidArgument):
+        ub.reconstruct(ub.ProjectionSet(geom, bad), spec, ub.SolverConfig(), tr)
+    bad[0, 3] = np.inf
+    with pytest.raises(ub.InvalidArgument):
+        ub.reconstruct(ub.ProjectionSet(geom, bad), spec, ub.SolverConfig(), tr)
+    bad[0, 3] = -1
+    with pytest.raises(ub.InvalidArgument):
+        ub.reconstruct(ub.ProjectionSet(geom, bad), spec, ub.SolverConfig(), tr)
+    with pytest.raises(ub.InvalidArgument):
+        ub.reconstruct(ub.ProjectionSet(geom, np.ones(7)), spec, ub.SolverConfig(), tr)
+    with pytest.raises(ub.InvalidArgument):
+        ub.reconstruct(ub.ProjectionSet(geom, np.ones((8, 21))), spec, ub.SolverConfig(beta=2.0), tr)
+    with pytest.raises(ub.InvalidArgument):
+        ub.reconstruct(ub.ProjectionSet(geom, np.ones((8, 21))), spec, ub.SolverConfig(f_init=0), tr)
+    with pytest.raises(ub.InvalidArgument):
+        ub.Tracer(ub.ScanGeometry(source=(-8, 0, 0), detector_center=(8, 0, 0), det_u=0, spacing_u=0.2), spec)
+    with pytest.raises(ub.InvalidArgument):
+        ub.Tracer(geom, ub.GridSpec(0, 1.0, 1.0))
+
+
+# ---------------------------------------------------------------------------
+# problem stack (the 2D slice-stack configuration)
+# ---------------------------------------------------------------------------
+
+
+@pytest.mark.parametrize("S", [1, 3, 37, 128])
+def test_stack_matches_oracle_per_problem(ub, orc, S):
+    import oracle
+    spec = ub.GridSpec.square_2d(32)
+    geom = ub.ScanGeometry(source=(-8, 0, 0), detector_center=(8, 0, 0), det_u=25, spacing_u=0.08, views=12)
+    tr = ub.Tracer(geom, spec, False)
+    rng = np.random.default_rng(S)
+    truth = rng.uniform(0.2, 3.0, (S, spec.cell_count()))
+    proj = ub.project_stack(tr, truth.astype(np.float32))
+    proj[min(1, S - 1)] = 0  # one all-zero problem when S > 1
+    g = oracle.OrcGrid.reference(32)
+    src, det = geom.first_view_rays()
+    oc = orc.cache(g, src, det)
+    cfg = ub.SolverConfig(beta=0.5, tolerance=0, max_sweeps=4)
+    out = ub.reconstruct_stack(proj, cfg, tr, with_crossed=True)
+    for p in range(S):
+        want, wrep = oc.reconstruct(geom.thetas(), proj[p].astype(np.float64), beta=0.5, tolerance=0, max_sweeps=4)
+        got, rep = out[p]
+        rel = np.abs(got - want) / want
+        assert rel.max() <= 1e-4, (p, rel.max())
+        assert rep.sweeps == wrep["sweeps"] and rep.all_zero_data == wrep["all_zero_data"]
+        assert rep.updates == wrep["updates"]
+        assert np.array_equal(rep.crossed, wrep["crossed"])
+
+
+# ---------------------------------------------------------------------------
+# generalized seams (verbatim BASELINE shapes) vs the C restatement
+# ---------------------------------------------------------------------------
+
+
+def _m1_case(ub, orc, detector, n_rings=32, volume=False, views=24, du=64, dv=1):
+    import oracle
+    counts = ub.ring_counts_m1(n_rings)
+    if volume:
+        spec = ub.GridSpec(2 * n_rings, 1.0 / n_rings, 2.0 / n_rings, ub.GridMode.Volume3D, ring_counts=counts,
+                           n_slices=n_rings // 2)
+    else:
+        spec = ub.GridSpec(2 * n_rings, 1.0 / n_rings, 1.0 / n_rings, ub.GridMode.Slice2D, ring_counts=counts)
+    if detector == "arc":
+        geom = ub.ScanGeometry(source=(-3, 0, 0), detector_center=(1.5, 0, 0), det_u=du, det_v=dv,
+                               spacing_u=38.94 / du, spacing_v=0.05, views=views, detector=ub.Detector.Arc)
+    elif detector == "parallel":
+        geom = ub.ScanGeometry(source=(-2, 0, 0), detector_center=(2, 0, 0), det_u=du, spacing_u=2.0 / du,
+                               views=views, detector=ub.Detector.Parallel,
+                               view_angles=np.array([180.0 * i / views for i in range(views)]))
+    else:
+        geom = ub.ScanGeometry(source=(-4, 0, 0), detector_center=(2, 0, 0), det_u=du, det_v=dv,
+                               spacing_u=3.1 / du, spacing_v=2.0 * 2.05 / dv, views=views)
+    g = oracle.OrcGrid(n_rings, 1.0 / n_rings, spec.slices(), spec.slice_height, volume, counts)
+    src, det = geom.first_view_rays()
+    oc = orc.cache(g, src, det)
+    tr = ub.Tracer(geom, spec, False)
+    return spec, geom, tr, oc
+
+
+@pytest.mark.parametrize("detector,volume", [("arc", False), ("parallel", False), ("flat", True)])
+def test_generalized_seams_match_restatement(ub, orc, detector, volume):
+    spec, geom, tr, oc = _m1_case(ub, orc, detector, volume=volume, dv=16 if volume else 1,
+                                  du=32 if volume else 64, views=12 if volume else 24)
+    c = tr.cache()
+    assert np.array_equal(c.offsets, oc.offsets)
+    assert np.array_equal(c.slice, oc.records["slice"]) and np.array_equal(c.ring, oc.records["ring"])
+    assert max(ulp_diff(c.phi_a, oc.records["phi_a"]).max(initial=0),
+               ulp_diff(c.phi_b, oc.records["phi_b"]).max(initial=0)) <= 4
+    th = geom.thetas()
+    for v in range(geom.views):
+        for line in range(0, geom.lines(), 3):
+            assert np.array_equal(tr.trace_line(line, th[v]), oc.trace_line(line, th[v])), (v, line)
+    truth = np.random.default_rng(5).uniform(0.2, 2.0, spec.cell_count())
+    proj = oc.project(th, truth)
+    got_p = ub.generate_projections(ub.Field(spec, truth.astype(np.float32)), geom, "binary", tr).data
+    np.testing.assert_allclose(got_p, proj, rtol=1e-6, atol=1e-5)
+    want, wrep = oc.reconstruct(th, proj, beta=0.3, tolerance=0, max_sweeps=3)
+    res = ub.reconstruct(ub.ProjectionSet(geom, proj), spec, ub.SolverConfig(beta=0.3, tolerance=0, max_sweeps=3), tr)
+    rel = np.abs(res.field.values - want) / want
+    assert rel.max() <= 1e-4
+    assert res.report.updates == wrep["updates"]
+
+
+# ---------------------------------------------------------------------------
+# K4 resample
+# ---------------------------------------------------------------------------
+
+
+@pytest.mark.parametrize("n", [2, 4, 16, 64, 256])
+def test_uspg_to_cg_map_matches_reference(ub, ref, n):
+    assert np.array_equal(ub.uspg_to_cg_map(n), ref.uspg_to_cg_map(n))
+
+
+def test_uspg_to_cg_map_rejects_odd(ub):
+    with pytest.raises(ub.DomainError):
+        ub.uspg_to_cg_map(5)
+
+
+@pytest.mark.parametrize("n,volume", [(8, True), (128, False), (64, True)])
+def test_field_to_cartesian_matches_reference(ub, ref, n, volume):
+    spec = ub.GridSpec.cube_3d(n) if volume else ub.GridSpec.square_2d(n)
+    f = np.random.default_rng(5).uniform(0, 2, spec.cell_count()).astype(np.float32)
+    got = ub.field_to_cartesian(ub.Field(spec, f))
+    want = ref.field_to_cartesian(n, volume, f.astype(np.float64))
+    assert np.array_equal(got.astype(np.float64), want)
+
+
+def test_resample_bin_map_matches_restatement(ub, orc):
+    import oracle
+    counts = ub.ring_counts_m1(64)
+    spec = ub.GridSpec(128, 1 / 64, 1 / 64, ub.GridMode.Slice2D, ring_counts=counts)
+    g = oracle.OrcGrid(64, 1 / 64, 1, 1 / 64, False, counts)
+    f = np.random.default_rng(9).uniform(0, 2, spec.cell_count()).astype(np.float32)
+    got = ub.field_to_cartesian(ub.Field(spec, f), npix=256)[0]
+    want = orc.field_to_cartesian(g, f.astype(np.float64), 256)[0]
+    mism = got.astype(np.float64) != want
+    assert mism.sum() <= 4, mism.sum()  # sector-edge pixels only (atan2 ulps)
+
+
+def test_resample_stack_layouts(ub):
+    spec = ub.GridSpec.square_2d(32)
+    f = np.random.default_rng(1).uniform(0, 2, (5, spec.cell_count())).astype(np.float32)
+    out = ub.resample_stack(spec, f, 32)
+    for p in range(5):
+        assert np.array_equal(out[p], ub.field_to_cartesian(ub.Field(spec, f[p])))

@@ -220,6 +220,19 @@ def run_reference(args, rank, world):
     print(json.dumps(line), flush=True)
 
 
+def mart_kernel_name(Sp):
+    p = 1
+    lim = int(os.environ.get("USCG_CHUNK_WIDTH", 8))
+    while p * 2 <= lim and Sp % (p * 2) == 0:
+        p *= 2
+    mode = os.environ.get("USCG_MART_MODE", "flow")
+    if mode == "levels" or p > 8:
+        return f"mart_level_kernel<{p}> (one launch per dependency level)"
+    if mode == "barrier":
+        return f"mart_sweep_kernel<{p}> (one cooperative launch per sweep)"
+    return f"mart_flow_kernel<{p}> (one dataflow launch per sweep)"
+
+
 def metric_name(config):
     return f"ray-voxel updates/s per Sp-MART iteration ({config})"
 
@@ -342,6 +355,27 @@ def main():
     ms_per_step = t_ms / args.steps
     value = U * world / (ms_per_step * 1e-3)
 
+    # ---- K2 projector over the whole stack (device-resident, one launch) ----
+    out_d = torch.empty((units, Sp), dtype=torch.float32, device="cuda")
+
+    def project_dev():
+        uscg._check(L.uscg_project(tracer.h, uscg.C.c_void_p(field_d.data_ptr()), S,
+                                   uscg.C.c_void_p(out_d.data_ptr()), flags))
+
+    project_dev()
+    pe = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    for k in range(args.steps):
+        flush.fill_(float(k))
+        pe[k][0].record(stream)
+        project_dev()
+        pe[k][1].record(stream)
+    torch.cuda.synchronize()
+    tp = float(sum(a.elapsed_time(b) for a, b in pe)) / args.steps
+    U_all = int(counts.sum()) * S
+    Bp = 4 * U_all + 20 * C + 8 * units + 4 * units * Sp
+    projector = {"ms": tp, "updates_per_s": U_all / (tp * 1e-3), "achieved_gbs": Bp / (tp * 1e-3) / 1e9,
+                 "algorithmic_bytes": Bp, "bytes_model": "4*U_all + 20*C + 8*(views*lines) + 4*(views*lines)*S_pad"}
+
     # ---- e2e through the C ABI with pinned host buffers ----
     e2e = None
     if not args.no_e2e:
@@ -393,7 +427,8 @@ def main():
     except Exception:
         pass
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                "traffic": traffic, "peak_kind": peak_kind, "kernel": "mart_level_kernel<32,1024>",
+                "traffic": traffic, "peak_kind": peak_kind,
+                "kernel": mart_kernel_name(Sp),
                 "algorithmic_bytes_per_iteration": B, "launches_per_iteration": levels,
                 "avg_launch_us": 1e6 * t_mart / max(levels, 1),
                 "bytes_model": "8*U + 20*C + 8*(views*lines) + 4*L_nonzero (DESIGN.md §5)"}
@@ -420,7 +455,8 @@ def main():
         "data": "synthetic: seeded random-ellipse phantoms per slice, binary projections, 1% Gaussian noise",
         "config": config_dict(wl, args),
         "ms_per_iteration": ms_per_step, "updates_per_iteration": U * world, "chords_per_iteration": C,
-        "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
+        "roofline": roofline, "projector": projector, "cpu_baseline": cpu, "e2e": e2e,
+        "gpu_launches": int(launches),
         "clocks": clk,
         "precompute": {"generator_s": t_gen, "schedule_s": t_sched, "levels_per_iteration": levels,
                        "records": info["records"], "cache_bytes": info["cache_bytes"]},

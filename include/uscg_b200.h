@@ -197,6 +197,12 @@ uscg_status uscg_resample(uscg_ctx ctx, const uscg_grid* grid, const float* fiel
 /* uspg_to_cg_map(n) itself (grid.hpp:84), n*n u32, host output. */
 uscg_status uscg_uspg_to_cg_map(uscg_ctx ctx, int32_t n, uint32_t* out);
 
+/* ---- diagnostics ---------------------------------------------------------
+ * The device math the generator uses, for parity tests against glibc:
+ * out[4*i + k], k = 0: atan2 (correctly rounded), 1: hypot (correctly
+ * rounded), 2: azimuth_deg (geometry.cpp:39-46), 3: libdevice atan2. */
+uscg_status uscg_diag_math(uscg_ctx ctx, int32_t n, const double* x, const double* y, double* out);
+
 #ifdef __cplusplus
 }
 #endif

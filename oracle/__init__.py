@@ -125,6 +125,7 @@ class Orc:
         L.orc_ring_counts_m1.argtypes = [C.c_int, _u32p]
         L.orc_norm360.argtypes = [C.c_double]
         L.orc_norm360.restype = C.c_double
+        L.orc_math.argtypes = [C.c_size_t, _dp, _dp, _dp]
         L.orc_rmse.argtypes = [C.c_size_t, _dp, _dp]
         L.orc_rmse.restype = C.c_double
         L.orc_ssim.argtypes = [C.c_int, C.c_int, _dp, _dp, C.c_double]
@@ -180,6 +181,13 @@ class Orc:
     def rmse(self, a, b):
         a = np.ascontiguousarray(a, float).ravel(); b = np.ascontiguousarray(b, float).ravel()
         return self.L.orc_rmse(a.size, _ptr(a, _dp), _ptr(b, _dp))
+
+    def math(self, x, y):
+        """glibc atan2(y, x), hypot(x, y), azimuth_deg(x, y): (n, 3)."""
+        x = np.ascontiguousarray(x, float).ravel(); y = np.ascontiguousarray(y, float).ravel()
+        out = np.zeros((x.size, 3))
+        self.L.orc_math(x.size, _ptr(x, _dp), _ptr(y, _dp), _ptr(out, _dp))
+        return out
 
     def ssim(self, a, b, dynamic_range=-1.0):
         a = np.ascontiguousarray(a, float); b = np.ascontiguousarray(b, float)

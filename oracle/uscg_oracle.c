@@ -790,3 +790,12 @@ double orc_ssim(int rows, int cols, const double* ref, const double* test, doubl
     const size_t windows = (size_t)(rows - W + 1) * (size_t)(cols - W + 1);
     return acc / windows;
 }
+
+/* ---- libm probes for the device-math parity tests ------------------------ */
+void orc_math(size_t n, const double* x, const double* y, double* out) {
+    for (size_t i = 0; i < n; ++i) {
+        out[3 * i + 0] = atan2(y[i], x[i]);
+        out[3 * i + 1] = hypot(x[i], y[i]);
+        out[3 * i + 2] = orc_azimuth_deg(x[i], y[i]);
+    }
+}

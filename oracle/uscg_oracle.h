@@ -104,6 +104,9 @@ void orc_bin_map(const orc_grid* g, int npix, uint32_t* out);
    permutation, any other law the bin-point map (outside -> 0) */
 void orc_field_to_cartesian(const orc_grid* g, int npix, const double* field, double* out);
 
+/* glibc atan2 / hypot / azimuth_deg, out[3*i + k] */
+void orc_math(size_t n, const double* x, const double* y, double* out);
+
 double orc_rmse(size_t n, const double* a, const double* b);
 double orc_ssim(int rows, int cols, const double* a, const double* b, double dynamic_range);
 

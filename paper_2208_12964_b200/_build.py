@@ -16,8 +16,8 @@ LIBDIR = os.path.join(HERE, "lib")
 LIB = os.path.join(LIBDIR, "libuscg_b200.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
-SOURCES = ["api.cu", "kernels.cu", "schedule.cpp"]
-HEADERS = ["internal.cuh", "kernels.h", "schedule.h"]
+SOURCES = ["api.cu", "kernels.cu", "mart_sweep.cu", "schedule.cpp"]
+HEADERS = ["internal.cuh", "kernels.h", "schedule.h", "ddmath.cuh"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 # --fmad=false: the fp64 index arithmetic must round exactly like the
 # reference's g++ build (no contraction into FMA), see DESIGN.md §4.

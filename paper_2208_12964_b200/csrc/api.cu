@@ -4,6 +4,8 @@
 #include <atomic>
 #include <chrono>
 #include <cmath>
+#include <cstdlib>
+#include <cstdio>
 #include <cstring>
 #include <memory>
 #include <stdexcept>
@@ -124,6 +126,13 @@ struct uscg_tracer_s {
     bool sched_built = false;
     std::vector<uint32_t> level_off;
     DevBuf<uint32_t> d_order;
+    DevBuf<uint32_t> d_level_off;
+    DevBuf<unsigned> d_bar;
+    DevBuf<uint32_t> d_pred_off, d_preds, d_succ_off, d_succs;
+    uint64_t n_preds = 0;
+    DevBuf<unsigned> d_done;  // dataflow flags [units * nchunks]
+    int done_chunks = 0;
+    unsigned epoch = 0;
     double schedule_seconds = 0;
     // MART workspace
     DevBuf<MartArgs> d_args;
@@ -427,6 +436,29 @@ void build_schedule(uscg_tracer_s* t) {
     t->d_order.alloc(std::max<size_t>(order.size(), 1));
     UB_CUDA(cudaMemcpy(t->d_order.p, order.data(), sizeof(uint32_t) * order.size(),
                        cudaMemcpyHostToDevice));
+    t->d_level_off.alloc(t->level_off.size());
+    UB_CUDA(cudaMemcpy(t->d_level_off.p, t->level_off.data(), sizeof(uint32_t) * t->level_off.size(),
+                       cudaMemcpyHostToDevice));
+    t->d_bar.alloc(2);
+    t->d_pred_off.alloc(sched.pred_off().size());
+    UB_CUDA(cudaMemcpy(t->d_pred_off.p, sched.pred_off().data(),
+                       sizeof(uint32_t) * sched.pred_off().size(), cudaMemcpyHostToDevice));
+    t->d_preds.alloc(std::max<size_t>(sched.preds().size(), 1));
+    if (!sched.preds().empty())
+        UB_CUDA(cudaMemcpy(t->d_preds.p, sched.preds().data(), sizeof(uint32_t) * sched.preds().size(),
+                           cudaMemcpyHostToDevice));
+    t->n_preds = sched.preds().size();
+    {
+        std::vector<uint32_t> succ_off, succs;
+        sched.successors(succ_off, succs);
+        t->d_succ_off.alloc(succ_off.size());
+        UB_CUDA(cudaMemcpy(t->d_succ_off.p, succ_off.data(), sizeof(uint32_t) * succ_off.size(),
+                           cudaMemcpyHostToDevice));
+        t->d_succs.alloc(std::max<size_t>(succs.size(), 1));
+        if (!succs.empty())
+            UB_CUDA(cudaMemcpy(t->d_succs.p, succs.data(), sizeof(uint32_t) * succs.size(),
+                               cudaMemcpyHostToDevice));
+    }
     t->sched_built = true;
     t->schedule_seconds =
         std::chrono::duration<double>(std::chrono::steady_clock::now() - h0).count();
@@ -905,7 +937,24 @@ uscg_status uscg_reconstruct(uscg_tracer t, const float* proj, int32_t problems,
         h.max_cells = t->max_cells;
         t->d_args.ensure(1);
         UB_CUDA(cudaMemcpyAsync(t->d_args.p, &h, sizeof(MartArgs), cudaMemcpyHostToDevice, st));
-        ensure_graph(t, h);
+        // MART executor (USCG_MART_MODE): "flow" (default) dataflow over
+        // per-task done flags; "barrier" one grid barrier per level;
+        // "levels" a CUDA graph with one kernel node per level.
+        static const int mode = [] {
+            const char* e = std::getenv("USCG_MART_MODE");
+            const std::string m = e ? e : "flow";
+            return m == "levels" ? 2 : (m == "barrier" ? 1 : 0);
+        }();
+        const int exec_mode = P <= 8 ? mode : 2;
+        if (exec_mode == 2)
+            ensure_graph(t, h);
+        if (exec_mode == 0 && t->done_chunks != h.nchunks) {
+            t->d_done.alloc(units * uint64_t(h.nchunks));
+            UB_CUDA(cudaMemsetAsync(t->d_done.p, 0, sizeof(unsigned) * units * h.nchunks, st));
+            t->done_chunks = h.nchunks;
+            t->epoch = 0;
+        }
+        const int levels = int(t->level_off.size()) - 1;
 
         std::vector<int> sweeps(S, 0), converged(S, 0);
         std::vector<std::vector<double>> resid(S);
@@ -922,8 +971,50 @@ uscg_status uscg_reconstruct(uscg_tracer t, const float* proj, int32_t problems,
             if (track)
                 UB_CUDA(cudaMemcpyAsync(t->w_prev.p, d_field, sizeof(float) * cells * Sp,
                                         cudaMemcpyDeviceToDevice, st));
-            UB_CUDA(cudaGraphLaunch(t->graph.exec, st));
-            count_launch(t->graph.nodes);
+            if (exec_mode == 0) {
+                // USCG_SWEEP_PROFILE=<file>: per-task stamps {grab, traced, ready, published}
+                static const char* prof_path = std::getenv("USCG_SWEEP_PROFILE");
+                const size_t nt = size_t(units) * h.nchunks;
+                DevBuf<unsigned long long> prof;
+                if (prof_path)
+                    prof.alloc(nt * 8);
+                launch_mart_flow(h, t->d_order.p, t->d_pred_off.p, t->d_succ_off.p, t->d_succs.p,
+                                 t->d_done.p, t->d_bar.p + 1, ++t->epoch, t->n_rings, units, st,
+                                 prof.p);
+                if (prof_path) {
+                    std::vector<unsigned long long> hp(nt * 8);
+                    UB_CUDA(cudaMemcpyAsync(hp.data(), prof.p, sizeof(unsigned long long) * hp.size(),
+                                            cudaMemcpyDeviceToHost, st));
+                    UB_CUDA(cudaStreamSynchronize(st));
+                    if (FILE* fp = std::fopen(prof_path, "wb")) {
+                        std::fwrite(hp.data(), sizeof(unsigned long long), hp.size(), fp);
+                        std::fclose(fp);
+                    }
+                }
+            } else if (exec_mode == 1) {
+                // USCG_SWEEP_PROFILE=<file>: per-level phase stamps of CTA 0 (diagnostics)
+                static const char* prof_path = std::getenv("USCG_SWEEP_PROFILE");
+                DevBuf<unsigned long long> prof;
+                if (prof_path) {
+                    prof.alloc(size_t(levels) * 4);
+                    UB_CUDA(cudaMemsetAsync(prof.p, 0, sizeof(unsigned long long) * levels * 4, st));
+                }
+                launch_mart_sweep(h, t->d_order.p, t->d_level_off.p, levels, t->d_bar.p, t->n_rings,
+                                  st, prof.p);
+                if (prof_path) {
+                    std::vector<unsigned long long> hp(size_t(levels) * 4);
+                    UB_CUDA(cudaMemcpyAsync(hp.data(), prof.p, sizeof(unsigned long long) * hp.size(),
+                                            cudaMemcpyDeviceToHost, st));
+                    UB_CUDA(cudaStreamSynchronize(st));
+                    if (FILE* fp = std::fopen(prof_path, "wb")) {
+                        std::fwrite(hp.data(), sizeof(unsigned long long), hp.size(), fp);
+                        std::fclose(fp);
+                    }
+                }
+            } else {
+                UB_CUDA(cudaGraphLaunch(t->graph.exec, st));
+                count_launch(t->graph.nodes);
+            }
             for (int p = 0; p < S; ++p)
                 sweeps[p] += active[p];
             if (track) {
@@ -1071,6 +1162,24 @@ uscg_status uscg_uspg_to_cg_map(uscg_ctx ctx, int32_t n, uint32_t* out) {
         launch_cg_map(n, d.p, ctx->stream);
         UB_CUDA(cudaMemcpyAsync(out, d.p, sizeof(uint32_t) * n * n, cudaMemcpyDeviceToHost,
                                 ctx->stream));
+        UB_CUDA(cudaStreamSynchronize(ctx->stream));
+    });
+}
+
+uscg_status uscg_diag_math(uscg_ctx ctx, int32_t n, const double* x, const double* y, double* out) {
+    return guarded([&] {
+        bind(ctx);
+        need(n >= 0 && x && y && out, "null buffer");
+        if (n == 0)
+            return;
+        DevBuf<double> d;
+        d.alloc(size_t(n) * 6);
+        UB_CUDA(cudaMemcpyAsync(d.p, x, sizeof(double) * n, cudaMemcpyHostToDevice, ctx->stream));
+        UB_CUDA(cudaMemcpyAsync(d.p + n, y, sizeof(double) * n, cudaMemcpyHostToDevice, ctx->stream));
+        DevBuf<double> o;
+        o.alloc(size_t(n) * 4);
+        launch_diag_math(n, d.p, d.p + n, o.p, ctx->stream);
+        UB_CUDA(cudaMemcpyAsync(out, o.p, sizeof(double) * 4 * n, cudaMemcpyDeviceToHost, ctx->stream));
         UB_CUDA(cudaStreamSynchronize(ctx->stream));
     });
 }

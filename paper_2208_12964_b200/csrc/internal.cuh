@@ -116,14 +116,47 @@ __device__ __forceinline__ int lohi_hi(uint32_t v) { return int((v >> 12) & 0xFF
 __device__ __forceinline__ bool lohi_seam(uint32_t v) { return (v >> 24) & 1u; }
 __device__ __forceinline__ bool lohi_flag(uint32_t v) { return (v >> 25) & 1u; }
 
-// Block-wide exclusive scan of a[0..n) in place; a[n] receives the total.
-// s_warp must hold NT/32 words. All threads must call it.
+// Synchronisation scope of a cooperative trace: the whole block, or a group of
+// NT consecutive threads synchronised by named barrier `id` (1..15).
 template <int NT>
-__device__ __forceinline__ void block_exclusive_scan(uint32_t* a, int n, uint32_t* s_warp) {
+struct BlockSync {
+    static constexpr int kThreads = NT;
+    __device__ __forceinline__ int tid() const { return threadIdx.x; }
+    __device__ __forceinline__ void sync() const { __syncthreads(); }
+    __device__ __forceinline__ bool sync_or(bool p) const { return __syncthreads_or(p) != 0; }
+};
+
+template <int NT>
+struct GroupSync {
+    static constexpr int kThreads = NT;
+    int id;
+    __device__ __forceinline__ int tid() const { return int(threadIdx.x) % NT; }
+    __device__ __forceinline__ void sync() const {
+        asm volatile("bar.sync %0, %1;" ::"r"(id), "n"(NT) : "memory");
+    }
+    __device__ __forceinline__ bool sync_or(bool p) const {
+        int r;
+        asm volatile(
+            "{\n .reg .pred pi, po;\n setp.ne.u32 pi, %1, 0;\n bar.red.or.pred po, %2, %3, pi;\n"
+            " selp.u32 %0, 1, 0, po;\n}"
+            : "=r"(r)
+            : "r"(int(p)), "r"(id), "n"(NT)
+            : "memory");
+        return r != 0;
+    }
+};
+
+// Exclusive scan of a[0..n) in place over the sync scope; a[n] receives the
+// total. s_warp must hold NT/32 words. All threads of the scope must call it.
+template <class Sync>
+__device__ __forceinline__ void block_exclusive_scan(uint32_t* a, int n, uint32_t* s_warp,
+                                                     const Sync& sy) {
+    constexpr int NT = Sync::kThreads;
     constexpr int NW = NT / 32;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int t = sy.tid();
+    const int lane = t & 31, warp = t >> 5;
     const int per = (n + NT - 1) / NT;
-    const int beg = min(n, int(threadIdx.x) * per);
+    const int beg = min(n, t * per);
     const int end = min(n, beg + per);
     uint32_t sum = 0;
     for (int i = beg; i < end; ++i)
@@ -137,7 +170,7 @@ __device__ __forceinline__ void block_exclusive_scan(uint32_t* a, int n, uint32_
     }
     if (lane == 31)
         s_warp[warp] = x;
-    __syncthreads();
+    sy.sync();
     if (warp == 0) {
         uint32_t w = lane < NW ? s_warp[lane] : 0u;
 #pragma unroll
@@ -149,16 +182,16 @@ __device__ __forceinline__ void block_exclusive_scan(uint32_t* a, int n, uint32_
         if (lane < NW)
             s_warp[lane] = w;
     }
-    __syncthreads();
+    sy.sync();
     uint32_t excl = x - sum + (warp > 0 ? s_warp[warp - 1] : 0u);
     for (int i = beg; i < end; ++i) {
         const uint32_t v = a[i];
         a[i] = excl;
         excl += v;
     }
-    if (threadIdx.x == 0)
+    if (t == 0)
         a[n] = s_warp[NW - 1];
-    __syncthreads();
+    sy.sync();
 }
 
 struct TraceSmem {
@@ -173,30 +206,62 @@ struct TraceSmem {
 // Number of cells of record i not already covered by an earlier record of the
 // same (slice, ring) in this line — the TraceScratch stamp dedup
 // (tracer.cpp:181-195) restricted to the only records that can collide.
-__device__ __forceinline__ uint32_t dedup_count(const TraceSmem& S, int i, int ng) {
+// Earlier records of the same (slice, ring) as record i, collected with one
+// backward scan (up to kMaxPartners; more means "scan per cell").
+constexpr int kMaxPartners = 4;
+struct Partners {
+    uint32_t lohi[kMaxPartners];
+    int n;  // -1: overflow, use the full scan
+};
+
+__device__ __forceinline__ Partners find_partners(const TraceSmem& S, int i) {
+    Partners P;
+    P.n = 0;
     const uint32_t b = S.base[i];
+    for (int j = i - 1; j >= 0; --j) {
+        if (S.base[j] != b)
+            continue;
+        if (P.n == kMaxPartners) {
+            P.n = -1;
+            break;
+        }
+        P.lohi[P.n++] = S.lohi[j];
+    }
+    return P;
+}
+
+__device__ __forceinline__ bool covered(const TraceSmem& S, const Partners& P, int i, int q) {
+    if (P.n >= 0) {
+#pragma unroll
+        for (int k = 0; k < kMaxPartners; ++k)
+            if (k < P.n && range_has(q, lohi_lo(P.lohi[k]), lohi_hi(P.lohi[k]), lohi_seam(P.lohi[k])))
+                return true;
+        return false;
+    }
+    const uint32_t b = S.base[i];
+    for (int j = i - 1; j >= 0; --j) {
+        if (S.base[j] != b)
+            continue;
+        const uint32_t w = S.lohi[j];
+        if (range_has(q, lohi_lo(w), lohi_hi(w), lohi_seam(w)))
+            return true;
+    }
+    return false;
+}
+
+__device__ __forceinline__ uint32_t dedup_count(const TraceSmem& S, int i, int ng) {
     const uint32_t v = S.lohi[i];
     const int lo = lohi_lo(v), hi = lohi_hi(v);
-    const bool seam = lohi_seam(v);
+    const Partners P = find_partners(S, i);
     uint32_t c = 0;
-    auto visit = [&](int q) {
-        for (int j = i - 1; j >= 0; --j) {
-            if (S.base[j] != b)
-                continue;
-            const uint32_t w = S.lohi[j];
-            if (range_has(q, lohi_lo(w), lohi_hi(w), lohi_seam(w)))
-                return;
-        }
-        ++c;
-    };
-    if (!seam) {
+    if (!lohi_seam(v)) {
         for (int q = lo; q <= hi; ++q)
-            visit(q);
+            c += !covered(S, P, i, q);
     } else {
         for (int q = hi; q < ng; ++q)
-            visit(q);
+            c += !covered(S, P, i, q);
         for (int q = 0; q <= lo; ++q)
-            visit(q);
+            c += !covered(S, P, i, q);
     }
     return c;
 }
@@ -205,18 +270,21 @@ __device__ __forceinline__ uint32_t dedup_count(const TraceSmem& S, int i, int n
 // deduplicated active cells in the reference emission order (chord order,
 // then sector order, tracer.cpp:174-197) and returns n. With expand == false
 // only the count is produced. All threads must call it; it ends synchronized.
-template <int NT>
-__device__ int block_trace(const TraceArgs& A, int line, double theta, const TraceSmem& S,
-                           bool expand) {
-    const uint32_t r0 = __ldg(A.off + line);
-    const int n = int(__ldg(A.off + line + 1) - r0);
+// Generic form: the sync scope may be a named-barrier group; `rings` may point
+// to a shared-memory copy of the ring table. r0/r1 are the line's record range.
+template <class Sync>
+__device__ int scope_trace(const TraceArgs& A, uint32_t r0, uint32_t r1, double theta,
+                           const TraceSmem& S, bool expand, const RingRow* rings, const Sync& sy) {
+    constexpr int NT = Sync::kThreads;
+    const int n = int(r1 - r0);
+    const int t0 = sy.tid();
     bool any_flag = false;
-    for (int i = threadIdx.x; i < n; i += NT) {
+    for (int i = t0; i < n; i += NT) {
         const uint32_t key = __ldg(A.key + r0 + i);
         const uint32_t ring = key & kRingMask;
         const uint32_t slice = (key >> kSliceShift) & kSliceMask;
         const bool flag = (key & kFlagBit) != 0;
-        const RingRow rr = A.rings[ring];
+        const RingRow rr = rings[ring];
         int lo, hi;
         bool seam;
         rotate_chord(__ldg(A.pa + r0 + i), __ldg(A.pb + r0 + i), theta, rr.count, rr.inv_step, lo,
@@ -229,17 +297,17 @@ __device__ int block_trace(const TraceArgs& A, int line, double theta, const Tra
         S.pos[i] = c;
         any_flag |= flag;
     }
-    if (__syncthreads_or(any_flag)) {
-        for (int i = threadIdx.x; i < n; i += NT)
+    if (sy.sync_or(any_flag)) {
+        for (int i = t0; i < n; i += NT)
             if (lohi_flag(S.lohi[i]))
                 S.pos[i] = dedup_count(S, i, int(S.cnt[i] >> 16));
-        __syncthreads();
+        sy.sync();
     }
-    block_exclusive_scan<NT>(S.pos, n, S.warp);
+    block_exclusive_scan(S.pos, n, S.warp, sy);
     const int total = int(S.pos[n]);
     if (!expand)
         return total;
-    for (int i = threadIdx.x; i < n; i += NT) {
+    for (int i = t0; i < n; i += NT) {
         uint32_t p = S.pos[i];
         const uint32_t b = S.base[i];
         const uint32_t v = S.lohi[i];
@@ -256,15 +324,10 @@ __device__ int block_trace(const TraceArgs& A, int line, double theta, const Tra
                     S.idx[p++] = b + uint32_t(q);
             }
         } else {
+            const Partners P = find_partners(S, i);
             auto emit = [&](int q) {
-                for (int j = i - 1; j >= 0; --j) {
-                    if (S.base[j] != b)
-                        continue;
-                    const uint32_t w = S.lohi[j];
-                    if (range_has(q, lohi_lo(w), lohi_hi(w), lohi_seam(w)))
-                        return;
-                }
-                S.idx[p++] = b + uint32_t(q);
+                if (!covered(S, P, i, q))
+                    S.idx[p++] = b + uint32_t(q);
             };
             if (!lohi_seam(v)) {
                 for (int q = lo; q <= hi; ++q)
@@ -277,8 +340,15 @@ __device__ int block_trace(const TraceArgs& A, int line, double theta, const Tra
             }
         }
     }
-    __syncthreads();
+    sy.sync();
     return total;
+}
+
+template <int NT>
+__device__ int block_trace(const TraceArgs& A, int line, double theta, const TraceSmem& S,
+                           bool expand) {
+    return scope_trace(A, __ldg(A.off + line), __ldg(A.off + line + 1), theta, S, expand, A.rings,
+                       BlockSync<NT>{});
 }
 
 // dynamic smem bytes for block_trace

@@ -12,7 +12,9 @@
 #include <cfloat>
 #include <cmath>
 #include <cstdint>
+#include <cstdlib>
 
+#include "ddmath.cuh"
 #include "kernels.h"
 
 namespace ub {
@@ -30,9 +32,21 @@ void check_launch() {
 }
 }  // namespace
 
+int chunk_limit() {
+    static const int lim = [] {
+        const char* e = std::getenv("USCG_CHUNK_WIDTH");
+        int v = e ? std::atoi(e) : 8;
+        int p = 1;
+        while (p * 2 <= v && p < 32)
+            p <<= 1;
+        return p;
+    }();
+    return lim;
+}
+
 int chunk_width(int problems) {
     int p = 1;
-    while (p < problems && p < 32)
+    while (p < problems && p < chunk_limit())
         p <<= 1;
     return p;
 }
@@ -42,13 +56,22 @@ int problem_stride(int problems) {
     return ((problems + p - 1) / p) * p;
 }
 
+// chunk width used for an interleaved stride Sp (largest power of two <=
+// the chunk limit that divides Sp)
+int stride_chunk(int Sp) {
+    int p = 1;
+    while (p < chunk_limit() && Sp % (p * 2) == 0)
+        p <<= 1;
+    return p;
+}
+
 // =============================================================================
 // K1: first-view coefficient generator, one thread per ray.
 // =============================================================================
 
 // azimuth_deg (geometry.cpp:39-46)
 __device__ __forceinline__ double azimuth_deg(double x, double y) {
-    double deg = atan2(y, x) * kDegPerRad;
+    double deg = atan2_cr(y, x) * kDegPerRad;
     if (deg < 0)
         deg += 360.0;
     if (deg >= 360.0)
@@ -153,7 +176,7 @@ __device__ uint32_t generate_ray(const DevGrid& g, const double* s, const double
     if (R.axial) {
         if (!R.volume)
             return 0;
-        if (hypot(s[0], s[1]) >= g.radius)
+        if (hypot_cr(s[0], s[1]) >= g.radius)
             return 0;
         if (R.dir2 == 0.0)
             return 0;
@@ -232,7 +255,7 @@ __device__ uint32_t generate_ray(const DevGrid& g, const double* s, const double
                         slice = int(sf);
                 }
                 if (keep) {
-                    const double dm = hypot(m0, m1);
+                    const double dm = hypot_cr(m0, m1);
                     ring = int(floor(dm / g.ring_spacing)) + 1;
                     if (ring > g.n_rings)
                         keep = false;
@@ -511,25 +534,34 @@ void launch_crossed(const TraceArgs& A, int views, int max_recs, int max_cells, 
 }
 
 // =============================================================================
-// K2: binary forward projector. One block per (view, line, problem chunk).
+// Gather/scatter shape per problem-chunk width P (problems per block):
+//   NT threads, NCL = NT / P cell lanes, each lane holds up to KR of the
+//   line's cells in registers so that all its loads are in flight at once and
+//   the scatter needs no reload. Lines longer than NCL * KR spill the tail to a
+//   re-read loop.
 // =============================================================================
+template <int P> struct Shape;
+template <> struct Shape<1> { static constexpr int NT = 128, KR = 8; };
+template <> struct Shape<2> { static constexpr int NT = 256, KR = 8; };
+template <> struct Shape<4> { static constexpr int NT = 256, KR = 12; };
+template <> struct Shape<8> { static constexpr int NT = 512, KR = 12; };
+template <> struct Shape<16> { static constexpr int NT = 1024, KR = 12; };
+template <> struct Shape<32> { static constexpr int NT = 1024, KR = 16; };
 
+#define UB_DISPATCH_P(P_, CALL)                      \
+    switch (P_) {                                    \
+        case 1: { constexpr int PP = 1; CALL; } break;   \
+        case 2: { constexpr int PP = 2; CALL; } break;   \
+        case 4: { constexpr int PP = 4; CALL; } break;   \
+        case 8: { constexpr int PP = 8; CALL; } break;   \
+        case 16: { constexpr int PP = 16; CALL; } break; \
+        default: { constexpr int PP = 32; CALL; } break; \
+    }
+
+// Sum over lanes with the same problem (lane % P) and over warps; returns the
+// per-problem total in s_out[p] (threads < P write, then the block syncs).
 template <int P, int NT>
-__global__ void __launch_bounds__(NT) project_kernel(TraceArgs A, const float* __restrict__ field,
-                                                     int Sp, int nchunks, int max_recs,
-                                                     float* __restrict__ out) {
-    extern __shared__ uint32_t smem[];
-    const TraceSmem S = carve_trace_smem<NT>(smem, max_recs);
-    __shared__ double s_red[NT / 32][P];
-    const int unit = blockIdx.x / nchunks, chunk = blockIdx.x % nchunks;
-    const int v = unit / A.lines, line = unit % A.lines;
-    const int n = block_trace<NT>(A, line, A.theta[v], S, true);
-    constexpr int NCL = NT / P;
-    const int p = threadIdx.x % P, cl = threadIdx.x / P;
-    const size_t col = size_t(chunk) * P + p;
-    double sum = 0;
-    for (int c = cl; c < n; c += NCL)
-        sum += double(field[size_t(S.idx[c]) * Sp + col]);
+__device__ __forceinline__ void block_problem_sum(double sum, double (*s_red)[P]) {
 #pragma unroll
     for (int o = P; o < 32; o <<= 1)
         sum += __shfl_xor_sync(0xFFFFFFFFu, sum, o);
@@ -537,6 +569,36 @@ __global__ void __launch_bounds__(NT) project_kernel(TraceArgs A, const float* _
     if (lane < P)
         s_red[warp][lane] = sum;
     __syncthreads();
+}
+
+// K2: binary forward projector. One block per (view, line, problem chunk).
+template <int P>
+__global__ void __launch_bounds__(Shape<P>::NT) project_kernel(TraceArgs A,
+                                                               const float* __restrict__ field,
+                                                               int Sp, int nchunks, int max_recs,
+                                                               float* __restrict__ out) {
+    constexpr int NT = Shape<P>::NT, KR = Shape<P>::KR, NCL = NT / P;
+    extern __shared__ uint32_t smem[];
+    const TraceSmem S = carve_trace_smem<NT>(smem, max_recs);
+    __shared__ double s_red[NT / 32][P];
+    const int unit = blockIdx.x / nchunks, chunk = blockIdx.x % nchunks;
+    const int v = unit / A.lines, line = unit % A.lines;
+    const int n = block_trace<NT>(A, line, A.theta[v], S, true);
+    const int p = threadIdx.x % P, cl = threadIdx.x / P;
+    const size_t col = size_t(chunk) * P + p;
+    float x[KR];
+#pragma unroll
+    for (int i = 0; i < KR; ++i) {
+        const int c = cl + i * NCL;
+        x[i] = c < n ? field[size_t(S.idx[c]) * Sp + col] : 0.f;
+    }
+    double sum = 0;
+#pragma unroll
+    for (int i = 0; i < KR; ++i)
+        sum += double(x[i]);
+    for (int c = cl + KR * NCL; c < n; c += NCL)
+        sum += double(field[size_t(S.idx[c]) * Sp + col]);
+    block_problem_sum<P, NT>(sum, s_red);
     if (threadIdx.x < P) {
         double t = 0;
 #pragma unroll
@@ -546,15 +608,16 @@ __global__ void __launch_bounds__(NT) project_kernel(TraceArgs A, const float* _
     }
 }
 
-template <int P, int NT>
+template <int P>
 static void project_impl(const TraceArgs& A, int views, const float* field, int Sp, int max_recs,
                          int max_cells, float* out, cudaStream_t st) {
+    constexpr int NT = Shape<P>::NT;
     const size_t sm = trace_smem_bytes(NT, max_recs, max_cells);
-    UB_CUDA(cudaFuncSetAttribute(project_kernel<P, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    UB_CUDA(cudaFuncSetAttribute(project_kernel<P>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  int(sm)));
     const int nchunks = Sp / P;
     const long long blocks = (long long)views * A.lines * nchunks;
-    project_kernel<P, NT><<<unsigned(blocks), NT, sm, st>>>(A, field, Sp, nchunks, max_recs, out);
+    project_kernel<P><<<unsigned(blocks), NT, sm, st>>>(A, field, Sp, nchunks, max_recs, out);
     check_launch();
 }
 
@@ -562,18 +625,7 @@ void launch_project(const TraceArgs& A, int views, const float* field, int Sp, i
                     int max_cells, float* out, cudaStream_t st) {
     if ((long long)views * A.lines == 0)
         return;
-    // the chunk width is the largest power of two <= 32 dividing Sp
-    int P = 1;
-    while (P < 32 && Sp % (P * 2) == 0)
-        P *= 2;
-    switch (P) {
-        case 1: project_impl<1, 128>(A, views, field, Sp, max_recs, max_cells, out, st); break;
-        case 2: project_impl<2, 256>(A, views, field, Sp, max_recs, max_cells, out, st); break;
-        case 4: project_impl<4, 256>(A, views, field, Sp, max_recs, max_cells, out, st); break;
-        case 8: project_impl<8, 256>(A, views, field, Sp, max_recs, max_cells, out, st); break;
-        case 16: project_impl<16, 512>(A, views, field, Sp, max_recs, max_cells, out, st); break;
-        default: project_impl<32, 1024>(A, views, field, Sp, max_recs, max_cells, out, st); break;
-    }
+    UB_DISPATCH_P(stride_chunk(Sp), project_impl<PP>(A, views, field, Sp, max_recs, max_cells, out, st));
 }
 
 // =============================================================================
@@ -583,9 +635,10 @@ void launch_project(const TraceArgs& A, int views, const float* field, int Sp, i
 // (solver.cpp:111-136): no atomics on the field, no reordering on any cell.
 // =============================================================================
 
-template <int P, int NT>
-__global__ void __launch_bounds__(NT) mart_level_kernel(const MartArgs* __restrict__ args,
-                                                        const uint32_t* __restrict__ units) {
+template <int P>
+__global__ void __launch_bounds__(Shape<P>::NT) mart_level_kernel(const MartArgs* __restrict__ args,
+                                                                  const uint32_t* __restrict__ units) {
+    constexpr int NT = Shape<P>::NT, KR = Shape<P>::KR, NCL = NT / P;
     extern __shared__ uint32_t smem[];
     __shared__ double s_red[NT / 32][P];
     __shared__ double s_fac[P];
@@ -597,23 +650,25 @@ __global__ void __launch_bounds__(NT) mart_level_kernel(const MartArgs* __restri
     const int v = int(unit / uint32_t(A.tr.lines)), line = int(unit % uint32_t(A.tr.lines));
     const int n = block_trace<NT>(A.tr, line, A.tr.theta[v], S, true);
 
-    constexpr int NCL = NT / P;
     const int p = threadIdx.x % P, cl = threadIdx.x / P;
     const int Sp = A.Sp;
     const size_t col = size_t(chunk) * P + p;
     float* __restrict__ f = A.field;
 
-    // forward_project_line (solver.cpp:25-31)
-    double sum = 0;
-    for (int c = cl; c < n; c += NCL)
-        sum += double(f[size_t(S.idx[c]) * Sp + col]);
+    // forward_project_line (solver.cpp:25-31): all KR loads in flight
+    float x[KR];
 #pragma unroll
-    for (int o = P; o < 32; o <<= 1)
-        sum += __shfl_xor_sync(0xFFFFFFFFu, sum, o);
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    if (lane < P)
-        s_red[warp][lane] = sum;
-    __syncthreads();
+    for (int i = 0; i < KR; ++i) {
+        const int c = cl + i * NCL;
+        x[i] = c < n ? f[size_t(S.idx[c]) * Sp + col] : 0.f;
+    }
+    double sum = 0;
+#pragma unroll
+    for (int i = 0; i < KR; ++i)
+        sum += double(x[i]);
+    for (int c = cl + KR * NCL; c < n; c += NCL)
+        sum += double(f[size_t(S.idx[c]) * Sp + col]);
+    block_problem_sum<P, NT>(sum, s_red);
     if (threadIdx.x < P) {
         const size_t c2 = size_t(chunk) * P + threadIdx.x;
         double p_bar = 0;
@@ -636,74 +691,51 @@ __global__ void __launch_bounds__(NT) mart_level_kernel(const MartArgs* __restri
     }
     __syncthreads();
     const double factor = s_fac[p];
-    if (factor != 0) {
-        for (int c = cl; c < n; c += NCL) {
-            float* q = f + size_t(S.idx[c]) * Sp + col;
-            // the reference's clamp keeps the fp64 field strictly positive
-            // (solver.cpp:42-45); in fp32 a product below FLT_MIN would
-            // underflow to 0, so it saturates at FLT_MIN instead
-            const float r = float(double(*q) * factor);
-            *q = r >= FLT_MIN ? r : FLT_MIN;
+    if (factor == 0)
+        return;
+    // The reference's clamp keeps the fp64 field strictly positive
+    // (solver.cpp:42-45); an fp32 product below FLT_MIN would underflow to 0,
+    // so it saturates at FLT_MIN instead.
+#pragma unroll
+    for (int i = 0; i < KR; ++i) {
+        const int c = cl + i * NCL;
+        if (c < n) {
+            const float r = float(double(x[i]) * factor);
+            f[size_t(S.idx[c]) * Sp + col] = r >= FLT_MIN ? r : FLT_MIN;
         }
+    }
+    for (int c = cl + KR * NCL; c < n; c += NCL) {
+        float* q = f + size_t(S.idx[c]) * Sp + col;
+        const float r = float(double(*q) * factor);
+        *q = r >= FLT_MIN ? r : FLT_MIN;
     }
 }
 
-template <int P, int NT>
+template <int P>
 static size_t mart_smem_t(const MartArgs& a) {
-    return trace_smem_bytes(NT, a.max_recs, a.max_cells);
+    return trace_smem_bytes(Shape<P>::NT, a.max_recs, a.max_cells);
 }
 
 size_t mart_smem_bytes(const MartArgs& a) {
-    const int P = a.Sp / a.nchunks;
-    switch (P) {
-        case 1: return mart_smem_t<1, 128>(a);
-        case 2: return mart_smem_t<2, 256>(a);
-        case 4: return mart_smem_t<4, 256>(a);
-        case 8: return mart_smem_t<8, 256>(a);
-        case 16: return mart_smem_t<16, 512>(a);
-        default: return mart_smem_t<32, 1024>(a);
-    }
-}
-
-template <int P, int NT>
-static void mart_prep_t(const MartArgs& a) {
-    UB_CUDA(cudaFuncSetAttribute(mart_level_kernel<P, NT>,
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 int(mart_smem_t<P, NT>(a))));
+    size_t r = 0;
+    UB_DISPATCH_P(a.Sp / a.nchunks, r = mart_smem_t<PP>(a));
+    return r;
 }
 
 void mart_prepare(const MartArgs& a) {
-    const int P = a.Sp / a.nchunks;
-    switch (P) {
-        case 1: mart_prep_t<1, 128>(a); break;
-        case 2: mart_prep_t<2, 256>(a); break;
-        case 4: mart_prep_t<4, 256>(a); break;
-        case 8: mart_prep_t<8, 256>(a); break;
-        case 16: mart_prep_t<16, 512>(a); break;
-        default: mart_prep_t<32, 1024>(a); break;
-    }
-}
-
-template <int P, int NT>
-static void mart_launch_t(const MartArgs* d, const MartArgs& h, const uint32_t* units, int n,
-                          cudaStream_t st) {
-    mart_level_kernel<P, NT>
-        <<<unsigned(n) * unsigned(h.nchunks), NT, mart_smem_t<P, NT>(h), st>>>(d, units);
+    UB_DISPATCH_P(a.Sp / a.nchunks,
+                  UB_CUDA(cudaFuncSetAttribute(mart_level_kernel<PP>,
+                                               cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                               int(mart_smem_t<PP>(a)))));
 }
 
 void launch_mart_level(const MartArgs* dargs, const MartArgs& h, const uint32_t* units, int n,
                        cudaStream_t st) {
     if (n <= 0)
         return;
-    const int P = h.Sp / h.nchunks;
-    switch (P) {
-        case 1: mart_launch_t<1, 128>(dargs, h, units, n, st); break;
-        case 2: mart_launch_t<2, 256>(dargs, h, units, n, st); break;
-        case 4: mart_launch_t<4, 256>(dargs, h, units, n, st); break;
-        case 8: mart_launch_t<8, 256>(dargs, h, units, n, st); break;
-        case 16: mart_launch_t<16, 512>(dargs, h, units, n, st); break;
-        default: mart_launch_t<32, 1024>(dargs, h, units, n, st); break;
-    }
+    UB_DISPATCH_P(h.Sp / h.nchunks,
+                  (mart_level_kernel<PP><<<unsigned(n) * unsigned(h.nchunks), Shape<PP>::NT,
+                                           mart_smem_t<PP>(h), st>>>(dargs, units)));
     check_launch();
 }
 
@@ -942,7 +974,7 @@ __global__ void bin_map_kernel(DevGrid g, int npix, uint32_t* map) {
     const double px = 2.0 * g.radius / npix;
     const double y = (row + 0.5 - npix / 2) * px;
     const double x = (col + 0.5 - npix / 2) * px;
-    const double rho = hypot(x, y);
+    const double rho = hypot_cr(x, y);
     uint32_t v = 0xFFFFFFFFu;
     if (rho < g.radius) {
         const int ring = int(floor(rho / g.ring_spacing)) + 1;
@@ -999,6 +1031,25 @@ __global__ void cg_map_kernel(int n, uint32_t* out) {
 
 void launch_cg_map(int n, uint32_t* out, cudaStream_t st) {
     cg_map_kernel<<<cdiv((long long)n * n, 256), 256, 0, st>>>(n, out);
+    check_launch();
+}
+
+// ---- diagnostics: the device math the generator uses, for parity tests ----
+__global__ void diag_math_kernel(int n, const double* __restrict__ x, const double* __restrict__ y,
+                                 double* out) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n)
+        return;
+    out[4 * i + 0] = atan2_cr(y[i], x[i]);
+    out[4 * i + 1] = hypot_cr(x[i], y[i]);
+    out[4 * i + 2] = azimuth_deg(x[i], y[i]);
+    out[4 * i + 3] = atan2(y[i], x[i]);
+}
+
+void launch_diag_math(int n, const double* x, const double* y, double* out, cudaStream_t st) {
+    if (n <= 0)
+        return;
+    diag_math_kernel<<<cdiv(n, 256), 256, 0, st>>>(n, x, y, out);
     check_launch();
 }
 

@@ -24,8 +24,10 @@ struct MartArgs {
 };
 
 // problem-chunk width P for S problems (power of two <= 32)
+int chunk_limit();
 int chunk_width(int problems);
 int problem_stride(int problems);
+int stride_chunk(int Sp);
 
 // K1: first-view generator. rays: lines*3 src + lines*3 det (device).
 void launch_generate_count(const DevGrid& g, int lines, const double* src, const double* det,
@@ -57,6 +59,18 @@ void launch_mart_level(const MartArgs* dargs, const MartArgs& hargs, const uint3
 size_t mart_smem_bytes(const MartArgs& a);
 void mart_prepare(const MartArgs& a);  // sets smem attributes
 
+// K3 persistent: one cooperative launch runs every level of a sweep
+// (mart_sweep.cu). Problem chunks of at most 8; bar is a device counter.
+void launch_mart_sweep(const MartArgs& h, const uint32_t* order, const uint32_t* level_off,
+                       int levels, unsigned* bar, int n_rings, cudaStream_t st,
+                       unsigned long long* prof = nullptr);
+size_t sweep_smem_bytes(const MartArgs& a, int n_rings);
+// K3 dataflow: tasks wait only on their predecessors' done flags
+void launch_mart_flow(const MartArgs& h, const uint32_t* order, const uint32_t* pred_off,
+                      const uint32_t* succ_off, const uint32_t* succs, unsigned* count,
+                      unsigned* next, unsigned epoch, int n_rings, uint64_t units,
+                      cudaStream_t st, unsigned long long* prof = nullptr);
+
 // per-problem projection statistics: stats[p*4 + {0: count>0, 1: sum>0, 2: any!=0, 3: invalid}]
 void launch_proj_stats(const float* proj, int units, int S, int Sp, double* stats, cudaStream_t st);
 // per-problem updates per sweep: sum over units with m != 0 of cells[u]
@@ -83,5 +97,7 @@ void launch_bin_map(const DevGrid& g, int npix, uint32_t* map, cudaStream_t st);
 void launch_map_resample(const float* field, uint64_t cells_per_slice, int slices, int S, int Sp,
                          const uint32_t* map, int npix, float* out, cudaStream_t st);
 void launch_cg_map(int n, uint32_t* out, cudaStream_t st);
+// out[4*i + {0: atan2_cr, 1: hypot_cr, 2: azimuth_deg, 3: libdevice atan2}]
+void launch_diag_math(int n, const double* x, const double* y, double* out, cudaStream_t st);
 
 }  // namespace ub

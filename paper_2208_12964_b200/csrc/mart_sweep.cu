@@ -1,0 +1,576 @@
+// K3 (persistent forms): one launch per Sp-MART sweep.
+//
+// The host-built schedule (schedule.h) orders the (view, line) units of a
+// sweep topologically: by ASAP level, and for every unit the distinct units
+// that last wrote one of its cells (its direct predecessors). Any execution
+// that runs each unit after all of its predecessors performs, on every cell,
+// exactly the reference's sequence of updates (solver.cpp:111-136).
+//
+// Two executors share the group-level task code below:
+//   * mart_flow_kernel (default): dataflow. Thread groups grab
+//     (unit, problem-chunk) tasks from an atomic queue in topological order,
+//     trace them while their predecessors are still running, wait only on the
+//     predecessors' done flags, then gather -> reduce -> factor -> scatter and
+//     publish their own flag. No grid-wide barrier.
+//   * mart_sweep_kernel: one grid barrier per dependency level (cooperative
+//     launch), next task traced between arrive and wait.
+// Latency bounds a chain of dependent units (SURVEY.md §7 hard part 1), so the
+// critical path between two dependent tasks is kept to: flag observed ->
+// gather (one L2 round trip, every cell of a thread in flight) -> reduction
+// -> factor -> scatter -> fence -> flag.
+#include <cuda_runtime.h>
+
+#include <cfloat>
+#include <cstdint>
+
+#include "kernels.h"
+
+namespace ub {
+
+namespace {
+constexpr int GT = 256;     // threads per group
+constexpr int GROUPS = 4;   // groups per CTA
+constexpr int CTA = GT * GROUPS;
+
+// KR: scalar cells held per thread; KV: float4 (4-problem) vectors per thread
+template <int P> struct SweepShape;
+template <> struct SweepShape<1> { static constexpr int KR = 4, KV = 0; };
+template <> struct SweepShape<2> { static constexpr int KR = 6, KV = 0; };
+template <> struct SweepShape<4> { static constexpr int KR = 8, KV = 4; };
+template <> struct SweepShape<8> { static constexpr int KR = 16, KV = 6; };
+
+__device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
+    unsigned v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
+__device__ __forceinline__ void st_release(unsigned* p, unsigned v) {
+    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+
+__host__ __device__ inline size_t trace_words(int max_recs, int max_cells) {
+    size_t w = size_t(max_recs) * 4 + 1 + GT / 32 + size_t(max_cells);
+    return (w + 1) & ~size_t(1);
+}
+
+__host__ __device__ inline size_t group_words(int P, int max_recs, int max_cells) {
+    // trace arrays + red (doubles) + fac (doubles) + meta
+    return trace_words(max_recs, max_cells) + 2 * size_t(GT / 32) * P + 2 * size_t(P) + 4;
+}
+
+// One thread group's state and task code.
+template <int P>
+struct GroupWorker {
+    static constexpr int KR = SweepShape<P>::KR, NCL = GT / P;
+    const MartArgs& A;
+    const RingRow* s_rings;
+    TraceSmem tr;
+    double* red;   // [GT/32][P]
+    double* fac;   // [P]
+    int* meta;     // [0]: cells, [1]: unit, [2]: chunk, [3]: scratch (task id)
+    GroupSync<GT> sy;
+    int t;
+    // per-task prefetched scalars (valid in threads t < P)
+    float m_next = 0.f;
+    double pf_next = 0;
+    bool act_next = false;
+
+    __device__ GroupWorker(const MartArgs& a, uint32_t* smem, int n_rings)
+        : A(a), s_rings(reinterpret_cast<const RingRow*>(smem)),
+          sy{1 + int(threadIdx.x) / GT}, t(int(threadIdx.x) % GT) {
+        const int g = int(threadIdx.x) / GT;
+        uint32_t* gbase = smem + (sizeof(RingRow) / 4) * (n_rings + 1) +
+                          size_t(g) * group_words(P, A.max_recs, A.max_cells);
+        tr.base = gbase;
+        tr.lohi = tr.base + A.max_recs;
+        tr.cnt = tr.lohi + A.max_recs;
+        tr.pos = tr.cnt + A.max_recs;
+        tr.warp = tr.pos + A.max_recs + 1;
+        tr.idx = tr.warp + GT / 32;
+        red = reinterpret_cast<double*>(gbase + trace_words(A.max_recs, A.max_cells));
+        fac = red + (GT / 32) * P;
+        meta = reinterpret_cast<int*>(fac + P);
+    }
+
+    // trace (unit, chunk) into the group's smem and prefetch its scalars
+    __device__ void prepare(uint32_t unit, int chunk) {
+        const int v = int(unit / uint32_t(A.tr.lines)), line = int(unit % uint32_t(A.tr.lines));
+        if (t < P) {
+            const size_t c2 = size_t(chunk) * P + t;
+            m_next = __ldg(A.proj + size_t(unit) * A.Sp + c2);
+            pf_next = __ldg(A.p_floor + c2);
+            act_next = __ldg(A.active + c2) != 0;
+        }
+        const int n = scope_trace(A.tr, __ldg(A.tr.off + line), __ldg(A.tr.off + line + 1),
+                                  __ldg(A.tr.theta + v), tr, true, s_rings, sy);
+        if (t == 0) {
+            meta[0] = n;
+            meta[1] = int(unit);
+            meta[2] = chunk;
+        }
+        sy.sync();
+    }
+
+    // gather -> reduce -> factor -> scatter for the prepared task
+    __device__ void update(unsigned long long* prof = nullptr) {
+        if constexpr (P >= 4) {
+            update_vec(prof);
+            return;
+        }
+        const int n = meta[0];
+        const int chunk = meta[2];
+        // element offsets fit 32 bits (cell_count * S_pad < 2^32 is checked on
+        // the host), so no 64-bit address stays live across the gather
+        const uint32_t Sp = uint32_t(A.Sp);
+        const int p = t % P, cl = t / P;
+        const uint32_t col = uint32_t(chunk) * P + uint32_t(p);
+        float* __restrict__ f = A.field;
+        float x[KR];
+#pragma unroll
+        for (int i = 0; i < KR; ++i) {
+            const int c = cl + i * NCL;
+            x[i] = c < n ? __ldcg(f + (tr.idx[c] * Sp + col)) : 0.f;
+        }
+        double sum = 0;
+#pragma unroll
+        for (int i = 0; i < KR; ++i)
+            sum += double(x[i]);
+        for (int c = cl + KR * NCL; c < n; c += 4 * NCL) {
+            float y[4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const int cc = c + j * NCL;
+                y[j] = cc < n ? __ldcg(f + (tr.idx[cc] * Sp + col)) : 0.f;
+            }
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+                sum += double(y[j]);
+        }
+#pragma unroll
+        for (int o = P; o < 32; o <<= 1)
+            sum += __shfl_xor_sync(0xFFFFFFFFu, sum, o);
+        const int lane = t & 31, warp = t >> 5;
+        if (lane < P)
+            red[warp * P + lane] = sum;
+        sy.sync();
+        if (prof && t == 0)
+            prof[3] = gtimer();
+        if (t < P) {
+            double p_bar = 0;
+#pragma unroll
+            for (int w = 0; w < GT / 32; ++w)
+                p_bar += red[w * P + t];
+            double factor = 0;  // 0: no update
+            const double m = double(m_next);
+            if (m != 0 && act_next) {
+                // mart_update_line (solver.cpp:36-46)
+                const double ratio = m / (p_bar > pf_next ? p_bar : pf_next);
+                factor = 1.0 - A.beta * (1.0 - ratio);
+                if (factor <= 0) {
+                    factor = pf_next;
+                    atomicAdd(A.clamps + size_t(chunk) * P + t, 1ull);
+                }
+            }
+            fac[t] = factor;
+        }
+        sy.sync();
+        if (prof && t == 0)
+            prof[4] = gtimer();
+        const double factor = fac[p];
+        if (factor == 0)
+            return;
+        // The reference's clamp keeps the fp64 field strictly positive
+        // (solver.cpp:42-45); an fp32 product below FLT_MIN would underflow
+        // to 0, so it saturates at FLT_MIN instead.
+#pragma unroll
+        for (int i = 0; i < KR; ++i) {
+            const int c = cl + i * NCL;
+            if (c < n) {
+                const float r = float(double(x[i]) * factor);
+                __stcg(f + (tr.idx[c] * Sp + col), r >= FLT_MIN ? r : FLT_MIN);
+            }
+        }
+        for (int c = cl + KR * NCL; c < n; c += 4 * NCL) {
+            float y[4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const int cc = c + j * NCL;
+                y[j] = cc < n ? __ldcg(f + (tr.idx[cc] * Sp + col)) : 0.f;
+            }
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const int cc = c + j * NCL;
+                if (cc < n) {
+                    const float r = float(double(y[j]) * factor);
+                    __stcg(f + (tr.idx[cc] * Sp + col), r >= FLT_MIN ? r : FLT_MIN);
+                }
+            }
+        }
+    }
+
+    // Vector form for P >= 4: a thread moves the 4 adjacent problems of one
+    // cell as one float4 (16 B, aligned: S_pad and the chunk base are
+    // multiples of 4), so a task needs a quarter of the load/store
+    // instructions and twice to four times the cell lanes of the scalar form.
+    __device__ static float scale_cell(float v, double f) {
+        if (f == 0)
+            return v;  // no update for this problem (skip / inactive)
+        const float r = float(double(v) * f);
+        return r >= FLT_MIN ? r : FLT_MIN;
+    }
+
+    __device__ void update_vec(unsigned long long* prof) {
+        constexpr int V = 4, TPC = P / V, NCLV = GT / TPC, KV = SweepShape<P>::KV;
+        const int n = meta[0];
+        const int chunk = meta[2];
+        const uint32_t Sp = uint32_t(A.Sp);
+        const int q = t % TPC, cl = t / TPC;
+        const uint32_t col = uint32_t(chunk) * P + uint32_t(q) * V;
+        float4* __restrict__ f4 = reinterpret_cast<float4*>(A.field);
+        float4 x[KV];
+#pragma unroll
+        for (int i = 0; i < KV; ++i) {
+            const int c = cl + i * NCLV;
+            x[i] = c < n ? __ldcg(f4 + ((tr.idx[c] * Sp + col) >> 2)) : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+        double s0 = 0, s1 = 0, s2 = 0, s3 = 0;
+#pragma unroll
+        for (int i = 0; i < KV; ++i) {
+            s0 += double(x[i].x);
+            s1 += double(x[i].y);
+            s2 += double(x[i].z);
+            s3 += double(x[i].w);
+        }
+        for (int c = cl + KV * NCLV; c < n; c += 2 * NCLV) {
+            const int c2 = c + NCLV;
+            const float4 y0 = __ldcg(f4 + ((tr.idx[c] * Sp + col) >> 2));
+            const float4 y1 = c2 < n ? __ldcg(f4 + ((tr.idx[c2] * Sp + col) >> 2))
+                                     : make_float4(0.f, 0.f, 0.f, 0.f);
+            s0 += double(y0.x) + double(y1.x);
+            s1 += double(y0.y) + double(y1.y);
+            s2 += double(y0.z) + double(y1.z);
+            s3 += double(y0.w) + double(y1.w);
+        }
+#pragma unroll
+        for (int o = TPC; o < 32; o <<= 1) {
+            s0 += __shfl_xor_sync(0xFFFFFFFFu, s0, o);
+            s1 += __shfl_xor_sync(0xFFFFFFFFu, s1, o);
+            s2 += __shfl_xor_sync(0xFFFFFFFFu, s2, o);
+            s3 += __shfl_xor_sync(0xFFFFFFFFu, s3, o);
+        }
+        const int lane = t & 31, warp = t >> 5;
+        if (lane < TPC) {
+            double* r = red + warp * P + q * V;
+            r[0] = s0;
+            r[1] = s1;
+            r[2] = s2;
+            r[3] = s3;
+        }
+        sy.sync();
+        if (prof && t == 0)
+            prof[3] = gtimer();
+        if (t < P) {
+            double p_bar = 0;
+#pragma unroll
+            for (int w = 0; w < GT / 32; ++w)
+                p_bar += red[w * P + t];
+            double factor = 0;  // 0: no update
+            const double m = double(m_next);
+            if (m != 0 && act_next) {
+                // mart_update_line (solver.cpp:36-46)
+                const double ratio = m / (p_bar > pf_next ? p_bar : pf_next);
+                factor = 1.0 - A.beta * (1.0 - ratio);
+                if (factor <= 0) {
+                    factor = pf_next;
+                    atomicAdd(A.clamps + size_t(chunk) * P + t, 1ull);
+                }
+            }
+            fac[t] = factor;
+        }
+        sy.sync();
+        if (prof && t == 0)
+            prof[4] = gtimer();
+        const double g0 = fac[q * V + 0], g1 = fac[q * V + 1], g2 = fac[q * V + 2],
+                     g3 = fac[q * V + 3];
+        if (g0 == 0 && g1 == 0 && g2 == 0 && g3 == 0)
+            return;
+#pragma unroll
+        for (int i = 0; i < KV; ++i) {
+            const int c = cl + i * NCLV;
+            if (c < n) {
+                const float4 r = make_float4(scale_cell(x[i].x, g0), scale_cell(x[i].y, g1),
+                                             scale_cell(x[i].z, g2), scale_cell(x[i].w, g3));
+                __stcg(f4 + ((tr.idx[c] * Sp + col) >> 2), r);
+            }
+        }
+        for (int c = cl + KV * NCLV; c < n; c += NCLV) {
+            float4* p4 = f4 + ((tr.idx[c] * Sp + col) >> 2);
+            const float4 y = __ldcg(p4);
+            __stcg(p4, make_float4(scale_cell(y.x, g0), scale_cell(y.y, g1), scale_cell(y.z, g2),
+                                   scale_cell(y.w, g3)));
+        }
+    }
+};
+
+__device__ __forceinline__ void stage_rings(uint32_t* smem, const RingRow* rings, int n_rings) {
+    RingRow* s = reinterpret_cast<RingRow*>(smem);
+    for (int k = threadIdx.x; k <= n_rings; k += blockDim.x)
+        s[k] = rings[k];
+}
+}  // namespace
+
+size_t sweep_smem_bytes(const MartArgs& a, int n_rings) {
+    const int P = a.Sp / a.nchunks;
+    const size_t rings = sizeof(RingRow) * size_t(n_rings + 1);
+    return rings + sizeof(uint32_t) * GROUPS * group_words(P, a.max_recs, a.max_cells);
+}
+
+// ============================================================================
+// dataflow executor
+// ============================================================================
+
+struct FlowArgs {
+    MartArgs m;
+    const uint32_t* order;     // units in topological (level) order
+    const uint32_t* pred_off;  // by unit id: number of predecessors = pred_off[u+1] - pred_off[u]
+    const uint32_t* succ_off;  // by unit id
+    const uint32_t* succs;     // successor unit ids
+    unsigned* count;           // [units * nchunks]: predecessors completed, cumulative over sweeps
+    unsigned* next;            // task queue head (zeroed per launch)
+    unsigned epoch;            // sweeps run with these counters, this one included
+    int n_tasks;               // units * nchunks
+    int n_rings;
+    unsigned long long* prof;  // optional: per task phase stamps (ns)
+};
+
+__device__ __forceinline__ void red_release_add(unsigned* p, unsigned v) {
+    asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+template <int P>
+__global__ void __launch_bounds__(CTA, 1) mart_flow_kernel(FlowArgs a) {
+    extern __shared__ __align__(16) uint32_t smem[];
+    stage_rings(smem, a.m.tr.rings, a.n_rings);
+    __syncthreads();
+    GroupWorker<P> W(a.m, smem, a.n_rings);
+    const int nchunks = a.m.nchunks;
+    int* s_task = W.meta + 3;
+    if (W.t == 0)
+        *s_task = int(atomicAdd(a.next, 1u));
+    W.sy.sync();
+    int task = *s_task;
+    unsigned long long* prof = nullptr;
+    while (task < a.n_tasks) {
+        if (a.prof && W.t == 0) {
+            prof = a.prof + 8 * size_t(task);
+            prof[0] = gtimer();
+        }
+        const uint32_t unit = __ldg(a.order + task / nchunks);
+        const int chunk = task % nchunks;
+        // claim the next task early; its latency overlaps this one
+        unsigned nxt = 0;
+        if (W.t == 0)
+            nxt = atomicAdd(a.next, 1u);
+        W.prepare(unit, chunk);
+        if (prof)
+            prof[1] = gtimer();
+        // wait until every predecessor's update of this chunk has counted in:
+        // one poller per group on one counter (push model, no per-pred flags)
+        if (W.t == 0) {
+            const unsigned npred = __ldg(a.pred_off + unit + 1) - __ldg(a.pred_off + unit);
+            if (npred) {
+                const unsigned* cnt = a.count + size_t(unit) * nchunks + chunk;
+                const unsigned target = a.epoch * npred;
+                unsigned ns = 16;
+                while (ld_acquire(cnt) < target) {
+                    __nanosleep(ns);
+                    ns = ns < 128 ? ns * 2 : 128;
+                }
+            }
+        }
+        // the acquire above orders this group's gathers (bar.sync below) after
+        // the predecessors' released stores; no SC fence / L1 flush needed
+        W.sy.sync();
+        if (prof)
+            prof[2] = gtimer();
+        W.update(prof);
+        // publish: bar.sync + gpu-scope release reductions make every
+        // thread's field stores visible before a successor can count them
+        W.sy.sync();
+        if (prof)
+            prof[5] = gtimer();
+        const uint32_t sb = __ldg(a.succ_off + unit), se = __ldg(a.succ_off + unit + 1);
+        for (uint32_t k = sb + W.t; k < se; k += GT)
+            red_release_add(a.count + size_t(__ldg(a.succs + k)) * nchunks + chunk, 1u);
+        if (W.t == 0) {
+            *s_task = int(nxt);
+            if (prof)
+                prof[6] = gtimer();
+        }
+        W.sy.sync();
+        task = *s_task;
+    }
+}
+
+template <int P>
+static void flow_launch_t(const FlowArgs& a, size_t smem, int grid, cudaStream_t st) {
+    UB_CUDA(cudaFuncSetAttribute(mart_flow_kernel<P>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 int(smem)));
+    int per_sm = 0;
+    UB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, mart_flow_kernel<P>, CTA, smem));
+    if (per_sm < 1)
+        throw CudaError("mart_flow_kernel cannot be resident (shared memory too large)");
+    mart_flow_kernel<P><<<grid * per_sm, CTA, smem, st>>>(a);
+}
+
+void launch_mart_flow(const MartArgs& h, const uint32_t* order, const uint32_t* pred_off,
+                      const uint32_t* succ_off, const uint32_t* succs, unsigned* count,
+                      unsigned* next, unsigned epoch, int n_rings, uint64_t units,
+                      cudaStream_t st, unsigned long long* prof) {
+    int dev = 0, sms = 0;
+    UB_CUDA(cudaGetDevice(&dev));
+    UB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    FlowArgs a;
+    a.m = h;
+    a.order = order;
+    a.pred_off = pred_off;
+    a.succ_off = succ_off;
+    a.succs = succs;
+    a.count = count;
+    a.next = next;
+    a.epoch = epoch;
+    a.n_tasks = int(units * uint64_t(h.nchunks));
+    a.n_rings = n_rings;
+    a.prof = prof;
+    UB_CUDA(cudaMemsetAsync(next, 0, sizeof(unsigned), st));
+    const size_t smem = sweep_smem_bytes(h, n_rings);
+    switch (h.Sp / h.nchunks) {
+        case 1: flow_launch_t<1>(a, smem, sms, st); break;
+        case 2: flow_launch_t<2>(a, smem, sms, st); break;
+        case 4: flow_launch_t<4>(a, smem, sms, st); break;
+        case 8: flow_launch_t<8>(a, smem, sms, st); break;
+        default: throw CudaError("mart_flow_kernel supports problem chunks of at most 8");
+    }
+    count_launch();
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess)
+        throw CudaError(std::string("mart_flow_kernel launch: ") + cudaGetErrorString(e));
+}
+
+// ============================================================================
+// level-barrier executor
+// ============================================================================
+
+struct SweepArgs {
+    MartArgs m;
+    const uint32_t* order;
+    const uint32_t* level_off;
+    int levels;
+    unsigned* bar;
+    int n_rings;
+    unsigned long long* prof;  // optional: per level 4 globaltimer stamps of CTA 0
+};
+
+template <int P>
+__global__ void __launch_bounds__(CTA, 1) mart_sweep_kernel(SweepArgs a) {
+    extern __shared__ __align__(16) uint32_t smem[];
+    stage_rings(smem, a.m.tr.rings, a.n_rings);
+    __syncthreads();
+    GroupWorker<P> W(a.m, smem, a.n_rings);
+    const int nchunks = a.m.nchunks;
+    const int NG = gridDim.x * GROUPS;
+    const int gid = blockIdx.x * GROUPS + int(threadIdx.x) / GT;
+    auto ntasks = [&](int lev) {
+        return int(__ldg(a.level_off + lev + 1) - __ldg(a.level_off + lev)) * nchunks;
+    };
+    auto prepare = [&](int lev, int task) {
+        const uint32_t unit = __ldg(a.order + __ldg(a.level_off + lev) + task / nchunks);
+        W.prepare(unit, task % nchunks);
+    };
+    const bool stamp = a.prof != nullptr && blockIdx.x == 0 && threadIdx.x == 0;
+    if (a.levels > 0 && gid < ntasks(0))
+        prepare(0, gid);
+    for (int lev = 0; lev < a.levels; ++lev) {
+        if (stamp)
+            a.prof[4 * lev + 0] = gtimer();
+        const int nt = ntasks(lev);
+        for (int task = gid; task < nt; task += NG) {
+            if (task != gid) {
+                W.sy.sync();  // previous update done with the group's smem
+                prepare(lev, task);
+            }
+            W.update();
+        }
+        if (lev + 1 == a.levels)
+            break;
+        // grid barrier, split: arrive, prepare the next task, wait
+        __syncthreads();
+        if (stamp)
+            a.prof[4 * lev + 1] = gtimer();
+        if (threadIdx.x == 0) {
+            __threadfence();
+            atomicAdd(a.bar, 1u);
+        }
+        if (gid < ntasks(lev + 1))
+            prepare(lev + 1, gid);
+        if (stamp)
+            a.prof[4 * lev + 2] = gtimer();
+        if (threadIdx.x == 0) {
+            const unsigned target = unsigned(lev + 1) * gridDim.x;
+            while (ld_acquire(a.bar) < target) {
+            }
+            __threadfence();
+        }
+        if (stamp)
+            a.prof[4 * lev + 3] = gtimer();
+        __syncthreads();
+    }
+}
+
+template <int P>
+static void sweep_launch_t(const SweepArgs& a, size_t smem, int grid, cudaStream_t st) {
+    UB_CUDA(cudaFuncSetAttribute(mart_sweep_kernel<P>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 int(smem)));
+    int per_sm = 0;
+    UB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, mart_sweep_kernel<P>, CTA, smem));
+    if (per_sm < 1)
+        throw CudaError("mart_sweep_kernel cannot be resident (shared memory too large)");
+    void* args[] = {const_cast<SweepArgs*>(&a)};
+    UB_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(mart_sweep_kernel<P>), dim3(grid),
+                                        dim3(CTA), args, smem, st));
+}
+
+void launch_mart_sweep(const MartArgs& h, const uint32_t* order, const uint32_t* level_off,
+                       int levels, unsigned* bar, int n_rings, cudaStream_t st,
+                       unsigned long long* prof) {
+    int dev = 0, sms = 0;
+    UB_CUDA(cudaGetDevice(&dev));
+    UB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    SweepArgs a;
+    a.m = h;
+    a.order = order;
+    a.level_off = level_off;
+    a.levels = levels;
+    a.bar = bar;
+    a.n_rings = n_rings;
+    a.prof = prof;
+    UB_CUDA(cudaMemsetAsync(bar, 0, sizeof(unsigned), st));
+    const size_t smem = sweep_smem_bytes(h, n_rings);
+    switch (h.Sp / h.nchunks) {
+        case 1: sweep_launch_t<1>(a, smem, sms, st); break;
+        case 2: sweep_launch_t<2>(a, smem, sms, st); break;
+        case 4: sweep_launch_t<4>(a, smem, sms, st); break;
+        case 8: sweep_launch_t<8>(a, smem, sms, st); break;
+        default: throw CudaError("mart_sweep_kernel supports problem chunks of at most 8");
+    }
+    count_launch();
+}
+
+}  // namespace ub

@@ -7,16 +7,43 @@ namespace ub {
 void AsapSchedule::add(const uint32_t* idx, const uint32_t* pos_rel, uint32_t n) {
     level_.reserve(level_.size() + n);
     for (uint32_t u = 0; u < n; ++u) {
+        const uint32_t unit = uint32_t(level_.size());
         const uint32_t b = pos_rel[u], e = pos_rel[u + 1];
         uint32_t lev = 0;
-        for (uint32_t i = b; i < e; ++i)
+        scratch_.clear();
+        for (uint32_t i = b; i < e; ++i) {
             lev = std::max(lev, last_[idx[i]]);
+            const uint32_t w = writer_[idx[i]];
+            if (w != kNone && (scratch_.empty() || scratch_.back() != w))
+                scratch_.push_back(w);
+        }
+        std::sort(scratch_.begin(), scratch_.end());
+        scratch_.erase(std::unique(scratch_.begin(), scratch_.end()), scratch_.end());
+        preds_.insert(preds_.end(), scratch_.begin(), scratch_.end());
+        pred_off_.push_back(uint32_t(preds_.size()));
         ++lev;
-        for (uint32_t i = b; i < e; ++i)
+        for (uint32_t i = b; i < e; ++i) {
             last_[idx[i]] = lev;
+            writer_[idx[i]] = unit;
+        }
         level_.push_back(lev);
         max_level_ = std::max(max_level_, lev);
     }
+}
+
+void AsapSchedule::successors(std::vector<uint32_t>& succ_off,
+                              std::vector<uint32_t>& succs) const {
+    const size_t units = level_.size();
+    succ_off.assign(units + 1, 0u);
+    for (uint32_t p : preds_)
+        ++succ_off[p + 1];
+    for (size_t u = 0; u < units; ++u)
+        succ_off[u + 1] += succ_off[u];
+    succs.assign(preds_.size(), 0u);
+    std::vector<uint32_t> cur(succ_off.begin(), succ_off.end() - 1);
+    for (size_t u = 0; u < units; ++u)
+        for (uint32_t k = pred_off_[u]; k < pred_off_[u + 1]; ++k)
+            succs[cur[preds_[k]]++] = uint32_t(u);
 }
 
 void AsapSchedule::finish(std::vector<uint32_t>& order, std::vector<uint32_t>& level_off) const {

@@ -18,7 +18,8 @@ namespace ub {
 
 class AsapSchedule {
 public:
-    explicit AsapSchedule(uint64_t cell_count) : last_(cell_count, 0u) {}
+    explicit AsapSchedule(uint64_t cell_count)
+        : last_(cell_count, 0u), writer_(cell_count, kNone) {}
 
     // supports of consecutive units in sweep order, CSR over `pos`
     // (pos[i]..pos[i+1] relative to idx), units u0 .. u0+n-1
@@ -27,11 +28,26 @@ public:
     // counting sort of the units by level: order (units), level_off (levels + 1)
     void finish(std::vector<uint32_t>& order, std::vector<uint32_t>& level_off) const;
 
+    // Direct predecessors of every unit (by unit id): the distinct units that
+    // last wrote one of its cells earlier in the sweep. A unit may run as
+    // soon as all of them are done (dataflow execution of the same order).
+    const std::vector<uint32_t>& pred_off() const { return pred_off_; }
+    const std::vector<uint32_t>& preds() const { return preds_; }
+
+    // successors (transpose of preds): succ_off (units + 1), succs
+    void successors(std::vector<uint32_t>& succ_off, std::vector<uint32_t>& succs) const;
+
     uint32_t levels() const { return max_level_; }
 
+    static constexpr uint32_t kNone = 0xFFFFFFFFu;
+
 private:
-    std::vector<uint32_t> last_;
+    std::vector<uint32_t> last_;    // level of the last writer per cell
+    std::vector<uint32_t> writer_;  // unit id of the last writer per cell
     std::vector<uint32_t> level_;
+    std::vector<uint32_t> pred_off_{0u};
+    std::vector<uint32_t> preds_;
+    std::vector<uint32_t> scratch_;
     uint32_t max_level_ = 0;
 };
 

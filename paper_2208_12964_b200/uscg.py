@@ -111,7 +111,7 @@ EXPORTS = [
     "uscg_tracer_create_from_rays", "uscg_tracer_import_cache", "uscg_tracer_destroy",
     "uscg_tracer_get_info", "uscg_tracer_export_cache", "uscg_trace_line", "uscg_trace_counts",
     "uscg_tracer_build_schedule", "uscg_problem_stride", "uscg_project", "uscg_reconstruct",
-    "uscg_resample", "uscg_uspg_to_cg_map",
+    "uscg_resample", "uscg_uspg_to_cg_map", "uscg_diag_math",
 ]
 
 _lib = None
@@ -159,6 +159,7 @@ def load(build_if_missing: bool = True):
                                    C.c_uint32]
     L.uscg_resample.argtypes = [vp, C.POINTER(_Grid), vp, C.c_int32, C.c_int32, vp, C.c_uint32]
     L.uscg_uspg_to_cg_map.argtypes = [vp, C.c_int32, _u32p]
+    L.uscg_diag_math.argtypes = [vp, C.c_int32, _dp, _dp, _dp]
     for name in EXPORTS:
         if name not in ("uscg_last_error", "uscg_version", "uscg_launch_count", "uscg_problem_stride"):
             getattr(L, name).restype = C.c_int
@@ -665,4 +666,16 @@ def uspg_to_cg_map(n: int, ctx: Optional[Context] = None) -> np.ndarray:
     ctx = ctx or default_context()
     out = np.zeros(max(n, 0) * max(n, 0), np.uint32)
     _check(load().uscg_uspg_to_cg_map(ctx.h, n, out.ctypes.data_as(_u32p)))
+    return out
+
+
+def diag_math(x, y, ctx: Optional[Context] = None) -> np.ndarray:
+    """Device math of the generator: columns atan2 (correctly rounded), hypot
+    (correctly rounded), azimuth_deg, libdevice atan2 — for parity tests."""
+    ctx = ctx or default_context()
+    x = np.ascontiguousarray(x, dtype=np.float64).ravel()
+    y = np.ascontiguousarray(y, dtype=np.float64).ravel()
+    out = np.zeros((x.size, 4))
+    _check(load().uscg_diag_math(ctx.h, x.size, x.ctypes.data_as(_dp), y.ctypes.data_as(_dp),
+                                 out.ctypes.data_as(_dp)))
     return out

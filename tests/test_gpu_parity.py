@@ -35,8 +35,53 @@ def test_generator_cache_matches_reference(ub, ref, name):
     assert np.array_equal(c.offsets, off)
     assert np.array_equal(c.slice, sl)
     assert np.array_equal(c.ring, rg)
-    da, db = ulp_diff(c.phi_a, pa), ulp_diff(c.phi_b, pb)
-    assert max(da.max(initial=0), db.max(initial=0)) <= 4, "azimuths beyond 4 ulp"
+    assert_phi_adjudicated(c.phi_a, pa)
+    assert_phi_adjudicated(c.phi_b, pb)
+
+
+def assert_phi_adjudicated(got, want):
+    """Azimuths: the device atan2 is correctly rounded; glibc 2.39's is not in
+    ~0.06% of calls (test_device_math_matches_glibc pins both rates against
+    mpmath-free counts). So: bit-exact except isolated 1-ulp differences."""
+    d = ulp_diff(got, want)
+    assert d.max(initial=0) <= 2, "azimuth beyond 2 ulp (1 ulp of atan2 after the degree scaling)"
+    assert np.count_nonzero(d) <= max(2, 0.005 * d.size), f"{np.count_nonzero(d)} of {d.size} differ"
+
+
+def test_device_math_matches_glibc(ub, orc):
+    """atan2 / hypot / azimuth_deg of the generator vs glibc on the chord
+    endpoint distribution (unit disc) and on adversarial sector-edge points."""
+    rng = np.random.default_rng(2208)
+    n = 200_000
+    r = np.sqrt(rng.uniform(0, 1, n))
+    a = rng.uniform(-np.pi, np.pi, n)
+    x, y = r * np.cos(a), r * np.sin(a)
+    # points on exact sector edges of both ring laws (cos/sin of k*360/ng)
+    ng = np.concatenate([4 * (2 * np.arange(1, 65) - 1), np.floor(2 * np.pi * (np.arange(64) + 0.5) + 0.5)])
+    k = rng.integers(0, 10_000, ng.size)
+    ang = np.radians((k % ng) * (360.0 / ng))
+    rad = rng.uniform(0.01, 1, ng.size)
+    x = np.concatenate([x, rad * np.cos(ang), [0.0, -0.0, 1.0, -1.0, 1e-300, 3.0]])
+    y = np.concatenate([y, rad * np.sin(ang), [0.0, 0.0, 0.0, 0.0, 1e-300, -4.0]])
+    dev = ub.uscg.diag_math(x, y)
+    host = orc.math(x, y)
+    mism_atan = np.count_nonzero(dev[:, 0].view(np.uint64) != host[:, 0].view(np.uint64))
+    mism_hyp = np.count_nonzero(dev[:, 1].view(np.uint64) != host[:, 1].view(np.uint64))
+    mism_az = np.count_nonzero(dev[:, 2].view(np.uint64) != host[:, 2].view(np.uint64))
+    libdevice = np.count_nonzero(dev[:, 3].view(np.uint64) != host[:, 0].view(np.uint64))
+    print(f"mismatches vs glibc: atan2 {mism_atan}, hypot {mism_hyp}, azimuth {mism_az}; "
+          f"libdevice atan2 {libdevice} of {x.size}")
+    # glibc 2.39 atan2/hypot are not correctly rounded in ~0.06% / ~0.6% of
+    # these inputs (measured against mpmath at 200 bits, tests/test_oracle.py);
+    # the device functions are, so they may differ from glibc by 1 ulp there.
+    # (azimuth = atan2 * 180/pi, +360 below zero: a 1-ulp atan2 difference can
+    # round to 2 ulp of the degree value)
+    for k, lim, ulps in ((0, 0.002, 1), (1, 0.01, 1), (2, 0.002, 2)):
+        d = ulp_diff(dev[:, k], host[:, k])
+        assert d.max() <= ulps, (k, d.max())
+        assert np.count_nonzero(d) <= lim * x.size, (k, np.count_nonzero(d))
+    # the libdevice atan2 would miss far more often
+    assert libdevice > 10 * mism_atan
 
 
 @pytest.mark.parametrize("name", ["fan64q", "cone32"])
@@ -361,12 +406,22 @@ def test_generalized_seams_match_restatement(ub, orc, detector, volume):
     c = tr.cache()
     assert np.array_equal(c.offsets, oc.offsets)
     assert np.array_equal(c.slice, oc.records["slice"]) and np.array_equal(c.ring, oc.records["ring"])
-    assert max(ulp_diff(c.phi_a, oc.records["phi_a"]).max(initial=0),
-               ulp_diff(c.phi_b, oc.records["phi_b"]).max(initial=0)) <= 4
+    assert_phi_adjudicated(c.phi_a, oc.records["phi_a"])
+    assert_phi_adjudicated(c.phi_b, oc.records["phi_b"])
+    # index lists: exact through the oracle's own cache; with the device-built
+    # cache any difference must sit on a line holding a 1-ulp azimuth
+    ocache = ub.FirstViewCache(oc.offsets, oc.records["phi_a"].copy(), oc.records["phi_b"].copy(),
+                               oc.records["slice"].copy(), oc.records["ring"].copy())
+    tr_imp = ub.Tracer.from_cache(spec, ocache, geom.views, geom.view_angles, geom=geom)
+    ulp_rec = (ulp_diff(c.phi_a, oc.records["phi_a"]) + ulp_diff(c.phi_b, oc.records["phi_b"])) > 0
     th = geom.thetas()
     for v in range(geom.views):
-        for line in range(0, geom.lines(), 3):
-            assert np.array_equal(tr.trace_line(line, th[v]), oc.trace_line(line, th[v])), (v, line)
+        for line in range(geom.lines()):
+            want = oc.trace_line(line, th[v])
+            assert np.array_equal(tr_imp.trace_line(line, th[v]), want), (v, line)
+            if not np.array_equal(tr.trace_line(line, th[v]), want):
+                assert ulp_rec[oc.offsets[line]:oc.offsets[line + 1]].any(), (v, line)
+    tr = tr_imp
     truth = np.random.default_rng(5).uniform(0.2, 2.0, spec.cell_count())
     proj = oc.project(th, truth)
     got_p = ub.generate_projections(ub.Field(spec, truth.astype(np.float32)), geom, "binary", tr).data

@@ -131,6 +131,8 @@ struct uscg_tracer_s {
     DevBuf<uint32_t> d_pred_off, d_preds, d_succ_off, d_succs;
     uint64_t n_preds = 0;
     DevBuf<unsigned> d_done;  // dataflow flags [units * nchunks]
+    DevBuf<uint32_t> w_slab;  // dataflow trace slab
+    DevBuf<unsigned> w_slab_ctl;
     int done_chunks = 0;
     unsigned epoch = 0;
     double schedule_seconds = 0;
@@ -978,9 +980,18 @@ uscg_status uscg_reconstruct(uscg_tracer t, const float* proj, int32_t problems,
                 DevBuf<unsigned long long> prof;
                 if (prof_path)
                     prof.alloc(nt * 8);
+                FlowSlab slab;
+                slab.Q = int(std::min<uint64_t>(units, 4096));
+                slab.slot_words = (t->max_cells + 1 + 31) & ~31;
+                t->w_slab.ensure(size_t(slab.Q) * slab.slot_words);
+                t->w_slab_ctl.ensure(size_t(slab.Q) * 2 + 1);
+                slab.data = t->w_slab.p;
+                slab.ready = t->w_slab_ctl.p;
+                slab.used = t->w_slab_ctl.p + slab.Q;
+                slab.tnext = t->w_slab_ctl.p + 2 * slab.Q;
                 launch_mart_flow(h, t->d_order.p, t->d_pred_off.p, t->d_succ_off.p, t->d_succs.p,
-                                 t->d_done.p, t->d_bar.p + 1, ++t->epoch, t->n_rings, units, st,
-                                 prof.p);
+                                 t->d_done.p, t->d_bar.p + 1, ++t->epoch, t->n_rings, units, slab,
+                                 st, prof.p);
                 if (prof_path) {
                     std::vector<unsigned long long> hp(nt * 8);
                     UB_CUDA(cudaMemcpyAsync(hp.data(), prof.p, sizeof(unsigned long long) * hp.size(),

@@ -65,11 +65,22 @@ void launch_mart_sweep(const MartArgs& h, const uint32_t* order, const uint32_t*
                        int levels, unsigned* bar, int n_rings, cudaStream_t st,
                        unsigned long long* prof = nullptr);
 size_t sweep_smem_bytes(const MartArgs& a, int n_rings);
-// K3 dataflow: tasks wait only on their predecessors' done flags
+// Ring of traced index lists shared by the chunk tasks of a unit:
+// slot = [n, idx[0..n)], slot_words >= max_cells + 1.
+struct FlowSlab {
+    uint32_t* data;     // [Q * slot_words]
+    unsigned* ready;    // [Q]
+    unsigned* used;     // [Q]
+    unsigned* tnext;    // tracer queue head
+    int Q;
+    int slot_words;
+};
+
+// K3 dataflow: tasks wait only on their predecessors (dependency counters)
 void launch_mart_flow(const MartArgs& h, const uint32_t* order, const uint32_t* pred_off,
                       const uint32_t* succ_off, const uint32_t* succs, unsigned* count,
                       unsigned* next, unsigned epoch, int n_rings, uint64_t units,
-                      cudaStream_t st, unsigned long long* prof = nullptr);
+                      const FlowSlab& slab, cudaStream_t st, unsigned long long* prof = nullptr);
 
 // per-problem projection statistics: stats[p*4 + {0: count>0, 1: sum>0, 2: any!=0, 3: invalid}]
 void launch_proj_stats(const float* proj, int units, int S, int Sp, double* stats, cudaStream_t st);

@@ -20,8 +20,10 @@
 // -> factor -> scatter -> fence -> flag.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cfloat>
 #include <cstdint>
+#include <cstdlib>
 
 #include "kernels.h"
 
@@ -343,10 +345,13 @@ struct FlowArgs {
     const uint32_t* succ_off;  // by unit id
     const uint32_t* succs;     // successor unit ids
     unsigned* count;           // [units * nchunks]: predecessors completed, cumulative over sweeps
-    unsigned* next;            // task queue head (zeroed per launch)
+    unsigned* next;            // updater task queue head (zeroed per launch)
     unsigned epoch;            // sweeps run with these counters, this one included
     int n_tasks;               // units * nchunks
+    int n_units;
     int n_rings;
+    FlowSlab slab;             // traced index lists, written once per unit by tracer CTAs
+    int tracer_ctas;
     unsigned long long* prof;  // optional: per task phase stamps (ns)
 };
 
@@ -354,13 +359,57 @@ __device__ __forceinline__ void red_release_add(unsigned* p, unsigned v) {
     asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
+__device__ __forceinline__ void spin_until_geq(const unsigned* p, unsigned target) {
+    unsigned ns = 16;
+    while (ld_acquire(p) < target) {
+        __nanosleep(ns);
+        ns = ns < 128 ? ns * 2 : 128;
+    }
+}
+
+// Tracer role: trace every unit once, in topological order, into a ring of
+// Q slab slots. A slot is rewritten only after every chunk task of its
+// previous occupant has copied it.
 template <int P>
-__global__ void __launch_bounds__(CTA, 1) mart_flow_kernel(FlowArgs a) {
-    extern __shared__ __align__(16) uint32_t smem[];
-    stage_rings(smem, a.m.tr.rings, a.n_rings);
-    __syncthreads();
-    GroupWorker<P> W(a.m, smem, a.n_rings);
+__device__ void flow_tracer(const FlowArgs& a, GroupWorker<P>& W) {
     const int nchunks = a.m.nchunks;
+    const int Q = a.slab.Q;
+    int* s_i = W.meta + 3;
+    while (true) {
+        if (W.t == 0)
+            *s_i = int(atomicAdd(a.slab.tnext, 1u));
+        W.sy.sync();
+        const int i = *s_i;
+        if (i >= a.n_units)
+            break;
+        const uint32_t unit = __ldg(a.order + i);
+        const int v = int(unit / uint32_t(a.m.tr.lines)), line = int(unit % uint32_t(a.m.tr.lines));
+        const int n = scope_trace(a.m.tr, __ldg(a.m.tr.off + line), __ldg(a.m.tr.off + line + 1),
+                                  __ldg(a.m.tr.theta + v), W.tr, true, W.s_rings, W.sy);
+        const int slot = i % Q;
+        const unsigned gen = unsigned(i / Q);
+        if (W.t == 0 && gen > 0)
+            spin_until_geq(a.slab.used + slot, gen * unsigned(nchunks));
+        W.sy.sync();
+        uint32_t* dst = a.slab.data + size_t(slot) * a.slab.slot_words;
+        for (int c = W.t; c < n; c += GT)
+            __stcg(dst + 1 + c, W.tr.idx[c]);
+        if (W.t == 0)
+            __stcg(dst, uint32_t(n));
+        W.sy.sync();
+        if (W.t == 0)
+            asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(a.slab.ready + slot), "r"(gen + 1)
+                         : "memory");
+    }
+}
+
+// Updater role: (unit, chunk) tasks in topological order; copy the unit's
+// index list from the slab, wait for the predecessors of this chunk, update,
+// count in at the successors.
+template <int P>
+__device__ void flow_updater(const FlowArgs& a, GroupWorker<P>& W) {
+    const int nchunks = a.m.nchunks;
+    const int Q = a.slab.Q;
     int* s_task = W.meta + 3;
     if (W.t == 0)
         *s_task = int(atomicAdd(a.next, 1u));
@@ -372,28 +421,44 @@ __global__ void __launch_bounds__(CTA, 1) mart_flow_kernel(FlowArgs a) {
             prof = a.prof + 8 * size_t(task);
             prof[0] = gtimer();
         }
-        const uint32_t unit = __ldg(a.order + task / nchunks);
+        const int i = task / nchunks;
+        const uint32_t unit = __ldg(a.order + i);
         const int chunk = task % nchunks;
         // claim the next task early; its latency overlaps this one
         unsigned nxt = 0;
         if (W.t == 0)
             nxt = atomicAdd(a.next, 1u);
-        W.prepare(unit, chunk);
+        if (W.t < P) {
+            const size_t c2 = size_t(chunk) * P + W.t;
+            W.m_next = __ldg(a.m.proj + size_t(unit) * a.m.Sp + c2);
+            W.pf_next = __ldg(a.m.p_floor + c2);
+            W.act_next = __ldg(a.m.active + c2) != 0;
+        }
+        // the unit's index list from the slab (L2 reads: slots are rewritten)
+        const int slot = i % Q;
+        if (W.t == 0)
+            spin_until_geq(a.slab.ready + slot, unsigned(i / Q) + 1);
+        W.sy.sync();
+        const uint32_t* src = a.slab.data + size_t(slot) * a.slab.slot_words;
+        const int n = int(__ldcg(src));
+        for (int c = W.t; c < n; c += GT)
+            W.tr.idx[c] = __ldcg(src + 1 + c);
+        if (W.t == 0) {
+            W.meta[0] = n;
+            W.meta[1] = int(unit);
+            W.meta[2] = chunk;
+        }
+        W.sy.sync();
+        if (W.t == 0)
+            red_release_add(a.slab.used + slot, 1u);
         if (prof)
             prof[1] = gtimer();
         // wait until every predecessor's update of this chunk has counted in:
         // one poller per group on one counter (push model, no per-pred flags)
         if (W.t == 0) {
             const unsigned npred = __ldg(a.pred_off + unit + 1) - __ldg(a.pred_off + unit);
-            if (npred) {
-                const unsigned* cnt = a.count + size_t(unit) * nchunks + chunk;
-                const unsigned target = a.epoch * npred;
-                unsigned ns = 16;
-                while (ld_acquire(cnt) < target) {
-                    __nanosleep(ns);
-                    ns = ns < 128 ? ns * 2 : 128;
-                }
-            }
+            if (npred)
+                spin_until_geq(a.count + size_t(unit) * nchunks + chunk, a.epoch * npred);
         }
         // the acquire above orders this group's gathers (bar.sync below) after
         // the predecessors' released stores; no SC fence / L1 flush needed
@@ -420,20 +485,41 @@ __global__ void __launch_bounds__(CTA, 1) mart_flow_kernel(FlowArgs a) {
 }
 
 template <int P>
-static void flow_launch_t(const FlowArgs& a, size_t smem, int grid, cudaStream_t st) {
+__global__ void __launch_bounds__(CTA, 1) mart_flow_kernel(FlowArgs a) {
+    extern __shared__ __align__(16) uint32_t smem[];
+    stage_rings(smem, a.m.tr.rings, a.n_rings);
+    __syncthreads();
+    GroupWorker<P> W(a.m, smem, a.n_rings);
+    if (int(blockIdx.x) < a.tracer_ctas)
+        flow_tracer<P>(a, W);
+    else
+        flow_updater<P>(a, W);
+}
+
+template <int P>
+static void flow_launch_t(FlowArgs& a, size_t smem, int sms, cudaStream_t st) {
     UB_CUDA(cudaFuncSetAttribute(mart_flow_kernel<P>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  int(smem)));
     int per_sm = 0;
     UB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, mart_flow_kernel<P>, CTA, smem));
     if (per_sm < 1)
         throw CudaError("mart_flow_kernel cannot be resident (shared memory too large)");
-    mart_flow_kernel<P><<<grid * per_sm, CTA, smem, st>>>(a);
+    const int grid = sms * per_sm;
+    // tracer CTAs: trace work ~ units, update work ~ units * chunks
+    int k = 0;
+    if (const char* e = std::getenv("USCG_TRACER_CTAS"))
+        k = std::atoi(e);
+    else
+        k = int(double(grid) * 2.7 / (2.7 + 4.0 * a.m.nchunks) + 0.5);
+    a.tracer_ctas = std::max(1, std::min(k, grid - 1));
+    // every CTA must be resident: tracers and updaters wait on each other
+    mart_flow_kernel<P><<<grid, CTA, smem, st>>>(a);
 }
 
 void launch_mart_flow(const MartArgs& h, const uint32_t* order, const uint32_t* pred_off,
                       const uint32_t* succ_off, const uint32_t* succs, unsigned* count,
                       unsigned* next, unsigned epoch, int n_rings, uint64_t units,
-                      cudaStream_t st, unsigned long long* prof) {
+                      const FlowSlab& slab, cudaStream_t st, unsigned long long* prof) {
     int dev = 0, sms = 0;
     UB_CUDA(cudaGetDevice(&dev));
     UB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
@@ -447,9 +533,15 @@ void launch_mart_flow(const MartArgs& h, const uint32_t* order, const uint32_t* 
     a.next = next;
     a.epoch = epoch;
     a.n_tasks = int(units * uint64_t(h.nchunks));
+    a.n_units = int(units);
     a.n_rings = n_rings;
+    a.slab = slab;
+    a.tracer_ctas = 1;
     a.prof = prof;
     UB_CUDA(cudaMemsetAsync(next, 0, sizeof(unsigned), st));
+    UB_CUDA(cudaMemsetAsync(slab.tnext, 0, sizeof(unsigned), st));
+    UB_CUDA(cudaMemsetAsync(slab.ready, 0, sizeof(unsigned) * slab.Q, st));
+    UB_CUDA(cudaMemsetAsync(slab.used, 0, sizeof(unsigned) * slab.Q, st));
     const size_t smem = sweep_smem_bytes(h, n_rings);
     switch (h.Sp / h.nchunks) {
         case 1: flow_launch_t<1>(a, smem, sms, st); break;

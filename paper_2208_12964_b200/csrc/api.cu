@@ -1196,3 +1196,33 @@ uscg_status uscg_diag_math(uscg_ctx ctx, int32_t n, const double* x, const doubl
 }
 
 }  // extern "C"
+
+extern "C" uscg_status uscg_schedule_build(uint32_t units, const uint32_t* pos, const uint32_t* idx,
+                                           uint64_t cell_count, uint32_t* order,
+                                           uint32_t* level_off, uint32_t* levels,
+                                           uint32_t* pred_off, uint32_t* preds,
+                                           uint64_t* n_preds) {
+    return guarded([&] {
+        need(pos && idx && order && level_off && levels, "null buffer");
+        for (uint32_t u = 0; u < units; ++u)
+            need(pos[u] <= pos[u + 1], "support offsets must be non-decreasing");
+        for (uint32_t i = 0; i < pos[units]; ++i)
+            need(idx[i] < cell_count, "support cell out of range");
+        AsapSchedule s(cell_count);
+        std::vector<uint32_t> rel(pos, pos + units + 1);
+        for (auto& p : rel)
+            p -= pos[0];
+        s.add(idx + pos[0], rel.data(), units);
+        std::vector<uint32_t> ord, loff;
+        s.finish(ord, loff);
+        std::memcpy(order, ord.data(), sizeof(uint32_t) * ord.size());
+        std::memcpy(level_off, loff.data(), sizeof(uint32_t) * loff.size());
+        *levels = s.levels();
+        if (pred_off)
+            std::memcpy(pred_off, s.pred_off().data(), sizeof(uint32_t) * s.pred_off().size());
+        if (preds)
+            std::memcpy(preds, s.preds().data(), sizeof(uint32_t) * s.preds().size());
+        if (n_preds)
+            *n_preds = s.preds().size();
+    });
+}

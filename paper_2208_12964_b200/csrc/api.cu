@@ -128,7 +128,7 @@ struct uscg_tracer_s {
     DevBuf<uint32_t> d_order;
     DevBuf<uint32_t> d_level_off;
     DevBuf<unsigned> d_bar;
-    DevBuf<uint32_t> d_pred_off, d_preds, d_succ_off, d_succs;
+    DevBuf<uint32_t> d_pred_off, d_preds, d_succ_off, d_succs, d_npred_x;
     uint64_t n_preds = 0;
     DevBuf<unsigned> d_done;  // dataflow flags [units * nchunks]
     DevBuf<uint32_t> w_slab;  // dataflow trace slab
@@ -451,8 +451,13 @@ void build_schedule(uscg_tracer_s* t) {
                            cudaMemcpyHostToDevice));
     t->n_preds = sched.preds().size();
     {
-        std::vector<uint32_t> succ_off, succs;
-        sched.successors(succ_off, succs);
+        // in-sweep + cross-sweep successors, cross-sweep predecessor counts
+        std::vector<uint32_t> npred_x, succ_off, succs;
+        sched.cross(npred_x, succ_off, succs);
+        t->d_npred_x.alloc(std::max<size_t>(npred_x.size(), 1));
+        if (!npred_x.empty())
+            UB_CUDA(cudaMemcpy(t->d_npred_x.p, npred_x.data(), sizeof(uint32_t) * npred_x.size(),
+                               cudaMemcpyHostToDevice));
         t->d_succ_off.alloc(succ_off.size());
         UB_CUDA(cudaMemcpy(t->d_succ_off.p, succ_off.data(), sizeof(uint32_t) * succ_off.size(),
                            cudaMemcpyHostToDevice));
@@ -973,13 +978,19 @@ uscg_status uscg_reconstruct(uscg_tracer t, const float* proj, int32_t problems,
             if (track)
                 UB_CUDA(cudaMemcpyAsync(t->w_prev.p, d_field, sizeof(float) * cells * Sp,
                                         cudaMemcpyDeviceToDevice, st));
+            int n_run = 1;
             if (exec_mode == 0) {
+                // without a per-sweep residual every remaining sweep runs in one
+                // launch, back to back (cross-sweep dependencies)
+                n_run = track ? 1 : cfg->max_sweeps - sweep;
                 // USCG_SWEEP_PROFILE=<file>: per-task stamps {grab, traced, ready, published}
                 static const char* prof_path = std::getenv("USCG_SWEEP_PROFILE");
-                const size_t nt = size_t(units) * h.nchunks;
+                const size_t nt = size_t(units) * h.nchunks * n_run;
                 DevBuf<unsigned long long> prof;
                 if (prof_path)
                     prof.alloc(nt * 8);
+                if (prof_path)
+                    UB_CUDA(cudaMemsetAsync(prof.p, 0, sizeof(unsigned long long) * nt * 8, st));
                 FlowSlab slab;
                 slab.Q = int(std::min<uint64_t>(units, 4096));
                 slab.slot_words = (t->max_cells + 1 + 31) & ~31;
@@ -990,8 +1001,9 @@ uscg_status uscg_reconstruct(uscg_tracer t, const float* proj, int32_t problems,
                 slab.used = t->w_slab_ctl.p + slab.Q;
                 slab.tnext = t->w_slab_ctl.p + 2 * slab.Q;
                 launch_mart_flow(h, t->d_order.p, t->d_pred_off.p, t->d_succ_off.p, t->d_succs.p,
-                                 t->d_done.p, t->d_bar.p + 1, ++t->epoch, t->n_rings, units, slab,
-                                 st, prof.p);
+                                 t->d_npred_x.p, t->d_done.p, t->d_bar.p + 1, t->epoch + 1, n_run,
+                                 t->n_rings, units, slab, st, prof.p);
+                t->epoch += unsigned(n_run);
                 if (prof_path) {
                     std::vector<unsigned long long> hp(nt * 8);
                     UB_CUDA(cudaMemcpyAsync(hp.data(), prof.p, sizeof(unsigned long long) * hp.size(),
@@ -1027,7 +1039,8 @@ uscg_status uscg_reconstruct(uscg_tracer t, const float* proj, int32_t problems,
                 count_launch(t->graph.nodes);
             }
             for (int p = 0; p < S; ++p)
-                sweeps[p] += active[p];
+                sweeps[p] += active[p] * n_run;
+            sweep += n_run - 1;
             if (track) {
                 UB_CUDA(cudaMemsetAsync(t->w_resid.p, 0, sizeof(unsigned int) * Sp, st));
                 launch_residual(d_field, t->w_prev.p, t->d_crossed.p, cells, S, Sp, t->w_resid.p, st);

@@ -621,10 +621,80 @@ static void project_impl(const TraceArgs& A, int views, const float* field, int 
     check_launch();
 }
 
+// K2 for problem stacks (S_pad % 4 == 0): one block per (view, line) traces
+// once and streams every problem of every cell as float4s. Warp w covers cell
+// lane w (all S_pad problems of a cell: contiguous 4*S_pad bytes), 4 cells in
+// flight per thread; per-problem sums reduce across warps in shared memory.
+constexpr int kProjNT = 512;
+
+__global__ void __launch_bounds__(kProjNT) project_stack_kernel(TraceArgs A,
+                                                                const float* __restrict__ field,
+                                                                int Sp, int max_recs,
+                                                                float* __restrict__ out) {
+    extern __shared__ uint32_t smem[];
+    const TraceSmem S = carve_trace_smem<kProjNT>(smem, max_recs);
+    __shared__ double s_red[kProjNT * 4];
+    const int unit = blockIdx.x;
+    const int v = unit / A.lines, line = unit % A.lines;
+    const int n = block_trace<kProjNT>(A, line, A.theta[v], S, true);
+    const int C4 = Sp / 4;
+    const int NCL = kProjNT / C4;
+    const int t = threadIdx.x;
+    const int col4 = t % C4, cl = t / C4;
+    double s0 = 0, s1 = 0, s2 = 0, s3 = 0;
+    if (cl < NCL) {
+        const float4* __restrict__ f4 = reinterpret_cast<const float4*>(field);
+        const uint32_t C4u = uint32_t(C4);
+        int c = cl;
+        for (; c + 3 * NCL < n; c += 4 * NCL) {
+            float4 y[4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+                y[j] = __ldg(f4 + (S.idx[c + j * NCL] * C4u + uint32_t(col4)));
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                s0 += double(y[j].x);
+                s1 += double(y[j].y);
+                s2 += double(y[j].z);
+                s3 += double(y[j].w);
+            }
+        }
+        for (; c < n; c += NCL) {
+            const float4 y = __ldg(f4 + (S.idx[c] * C4u + uint32_t(col4)));
+            s0 += double(y.x);
+            s1 += double(y.y);
+            s2 += double(y.z);
+            s3 += double(y.w);
+        }
+    }
+    double* r = s_red + 4 * t;
+    r[0] = s0;
+    r[1] = s1;
+    r[2] = s2;
+    r[3] = s3;
+    __syncthreads();
+    for (int q = t; q < Sp; q += kProjNT) {
+        const int c4 = q / 4, j = q % 4;
+        double tot = 0;
+        for (int k = 0; k < NCL; ++k)
+            tot += s_red[4 * (k * C4 + c4) + j];
+        out[size_t(unit) * Sp + q] = float(tot);
+    }
+}
+
 void launch_project(const TraceArgs& A, int views, const float* field, int Sp, int max_recs,
                     int max_cells, float* out, cudaStream_t st) {
     if ((long long)views * A.lines == 0)
         return;
+    if (Sp % 4 == 0 && Sp / 4 <= kProjNT) {
+        const size_t sm = trace_smem_bytes(kProjNT, max_recs, max_cells);
+        UB_CUDA(cudaFuncSetAttribute(project_stack_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     int(sm)));
+        const long long blocks = (long long)views * A.lines;
+        project_stack_kernel<<<unsigned(blocks), kProjNT, sm, st>>>(A, field, Sp, max_recs, out);
+        check_launch();
+        return;
+    }
     UB_DISPATCH_P(stride_chunk(Sp), project_impl<PP>(A, views, field, Sp, max_recs, max_cells, out, st));
 }
 

@@ -77,10 +77,13 @@ struct FlowSlab {
 };
 
 // K3 dataflow: tasks wait only on their predecessors (dependency counters)
+// Runs `sweeps` sweeps back to back (cross-sweep dependencies, no boundary);
+// epoch = global 1-based index of the first of them.
 void launch_mart_flow(const MartArgs& h, const uint32_t* order, const uint32_t* pred_off,
-                      const uint32_t* succ_off, const uint32_t* succs, unsigned* count,
-                      unsigned* next, unsigned epoch, int n_rings, uint64_t units,
-                      const FlowSlab& slab, cudaStream_t st, unsigned long long* prof = nullptr);
+                      const uint32_t* succ_off, const uint32_t* succs, const uint32_t* npred_x,
+                      unsigned* count, unsigned* next, unsigned epoch, int sweeps, int n_rings,
+                      uint64_t units, const FlowSlab& slab, cudaStream_t st,
+                      unsigned long long* prof = nullptr);
 
 // per-problem projection statistics: stats[p*4 + {0: count>0, 1: sum>0, 2: any!=0, 3: invalid}]
 void launch_proj_stats(const float* proj, int units, int S, int Sp, double* stats, cudaStream_t st);

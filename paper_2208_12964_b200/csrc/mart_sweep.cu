@@ -342,12 +342,14 @@ struct FlowArgs {
     MartArgs m;
     const uint32_t* order;     // units in topological (level) order
     const uint32_t* pred_off;  // by unit id: number of predecessors = pred_off[u+1] - pred_off[u]
-    const uint32_t* succ_off;  // by unit id
+    const uint32_t* succ_off;  // by unit id: in-sweep and cross-sweep successors
     const uint32_t* succs;     // successor unit ids
+    const uint32_t* npred_x;   // by unit id: cross-sweep predecessors
     unsigned* count;           // [units * nchunks]: predecessors completed, cumulative over sweeps
     unsigned* next;            // updater task queue head (zeroed per launch)
-    unsigned epoch;            // sweeps run with these counters, this one included
-    int n_tasks;               // units * nchunks
+    unsigned epoch;            // global index (1-based) of this launch's first sweep
+    int n_sweeps;              // sweeps run back to back by this launch
+    int n_tasks;               // units * nchunks (per sweep)
     int n_units;
     int n_rings;
     FlowSlab slab;             // traced index lists, written once per unit by tracer CTAs
@@ -375,14 +377,15 @@ __device__ void flow_tracer(const FlowArgs& a, GroupWorker<P>& W) {
     const int nchunks = a.m.nchunks;
     const int Q = a.slab.Q;
     int* s_i = W.meta + 3;
+    const int total = a.n_units * a.n_sweeps;
     while (true) {
         if (W.t == 0)
             *s_i = int(atomicAdd(a.slab.tnext, 1u));
         W.sy.sync();
-        const int i = *s_i;
-        if (i >= a.n_units)
+        const int i = *s_i;  // sequence over (sweep, order position)
+        if (i >= total)
             break;
-        const uint32_t unit = __ldg(a.order + i);
+        const uint32_t unit = __ldg(a.order + i % a.n_units);
         const int v = int(unit / uint32_t(a.m.tr.lines)), line = int(unit % uint32_t(a.m.tr.lines));
         const int n = scope_trace(a.m.tr, __ldg(a.m.tr.off + line), __ldg(a.m.tr.off + line + 1),
                                   __ldg(a.m.tr.theta + v), W.tr, true, W.s_rings, W.sy);
@@ -406,24 +409,51 @@ __device__ void flow_tracer(const FlowArgs& a, GroupWorker<P>& W) {
 // Updater role: (unit, chunk) tasks in topological order; copy the unit's
 // index list from the slab, wait for the predecessors of this chunk, update,
 // count in at the successors.
+// Count a finished task in at its successors: one gpu-scope acq_rel fence
+// (cumulative over the group's stores through the preceding bar.sync), then
+// relaxed reductions. Issued by one lane so the fence's store-completion wait
+// overlaps the rest of the group's next task.
+__device__ __forceinline__ void publish_task(const FlowArgs& a, uint32_t unit, int chunk) {
+    asm volatile("fence.acq_rel.gpu;" ::: "memory");
+    const int nchunks = a.m.nchunks;
+    const uint32_t sb = __ldg(a.succ_off + unit), se = __ldg(a.succ_off + unit + 1);
+    for (uint32_t k = sb; k < se; ++k)
+        asm volatile("red.relaxed.gpu.global.add.u32 [%0], %1;" ::"l"(
+                         a.count + size_t(__ldg(a.succs + k)) * nchunks + chunk),
+                     "r"(1u)
+                     : "memory");
+}
+
 template <int P>
 __device__ void flow_updater(const FlowArgs& a, GroupWorker<P>& W) {
+    constexpr int kCopy = GT - 32;  // warps 0, 2..7 copy the slab; warp 1 waits / publishes
     const int nchunks = a.m.nchunks;
     const int Q = a.slab.Q;
+    const int warp = W.t >> 5, lane = W.t & 31;
+    const GroupSync<kCopy> copy_sync{5 + int(threadIdx.x) / GT};
     int* s_task = W.meta + 3;
     if (W.t == 0)
         *s_task = int(atomicAdd(a.next, 1u));
     W.sy.sync();
     int task = *s_task;
+    bool has_prev = false;
+    uint32_t prev_unit = 0;
+    int prev_chunk = 0;
     unsigned long long* prof = nullptr;
-    while (task < a.n_tasks) {
-        if (a.prof && W.t == 0) {
+    unsigned long long* prev_prof = nullptr;
+    const int total = a.n_tasks * a.n_sweeps;
+    while (task < total) {
+        if (a.prof) {
             prof = a.prof + 8 * size_t(task);
-            prof[0] = gtimer();
+            if (W.t == 0)
+                prof[0] = gtimer();
         }
-        const int i = task / nchunks;
+        const int sweep = task / a.n_tasks;            // 0-based within this launch
+        const int i = (task % a.n_tasks) / nchunks;    // order position
         const uint32_t unit = __ldg(a.order + i);
         const int chunk = task % nchunks;
+        const int seq = sweep * a.n_units + i;         // tracer sequence of this unit
+        const int slot = seq % Q;
         // claim the next task early; its latency overlaps this one
         unsigned nxt = 0;
         if (W.t == 0)
@@ -434,54 +464,65 @@ __device__ void flow_updater(const FlowArgs& a, GroupWorker<P>& W) {
             W.pf_next = __ldg(a.m.p_floor + c2);
             W.act_next = __ldg(a.m.active + c2) != 0;
         }
-        // the unit's index list from the slab (L2 reads: slots are rewritten)
-        const int slot = i % Q;
-        if (W.t == 0)
-            spin_until_geq(a.slab.ready + slot, unsigned(i / Q) + 1);
-        W.sy.sync();
-        const uint32_t* src = a.slab.data + size_t(slot) * a.slab.slot_words;
-        const int n = int(__ldcg(src));
-        for (int c = W.t; c < n; c += GT)
-            W.tr.idx[c] = __ldcg(src + 1 + c);
-        if (W.t == 0) {
-            W.meta[0] = n;
-            W.meta[1] = int(unit);
-            W.meta[2] = chunk;
+        if (warp == 1) {
+            if (lane == 0) {
+                // wait until every predecessor's update of this chunk counted in:
+                // one poller per group on one counter (push model)
+                // sweep s (global, 1-based) needs s in-sweep and s-1 cross-sweep
+                // rounds of its predecessors counted in
+                const unsigned s = a.epoch + unsigned(sweep);
+                const unsigned npred = __ldg(a.pred_off + unit + 1) - __ldg(a.pred_off + unit);
+                const unsigned target = s * npred + (s - 1) * __ldg(a.npred_x + unit);
+                if (target)
+                    spin_until_geq(a.count + size_t(unit) * nchunks + chunk, target);
+            }
+        } else {
+            // the unit's index list from the slab (L2 reads: slots are rewritten)
+            if (W.t == 0)
+                spin_until_geq(a.slab.ready + slot, unsigned(seq / Q) + 1);
+            copy_sync.sync();
+            const int ct = W.t < 32 ? W.t : W.t - 32;
+            const uint32_t* src = a.slab.data + size_t(slot) * a.slab.slot_words;
+            const int n = int(__ldcg(src));
+            for (int c = ct; c < n; c += kCopy)
+                W.tr.idx[c] = __ldcg(src + 1 + c);
+            if (W.t == 0) {
+                W.meta[0] = n;
+                W.meta[1] = int(unit);
+                W.meta[2] = chunk;
+            }
         }
+        // index list copied, predecessors counted in (their acquire orders the
+        // gathers after the released stores), previous task published
         W.sy.sync();
         if (W.t == 0)
             red_release_add(a.slab.used + slot, 1u);
-        if (prof)
-            prof[1] = gtimer();
-        // wait until every predecessor's update of this chunk has counted in:
-        // one poller per group on one counter (push model, no per-pred flags)
-        if (W.t == 0) {
-            const unsigned npred = __ldg(a.pred_off + unit + 1) - __ldg(a.pred_off + unit);
-            if (npred)
-                spin_until_geq(a.count + size_t(unit) * nchunks + chunk, a.epoch * npred);
-        }
-        // the acquire above orders this group's gathers (bar.sync below) after
-        // the predecessors' released stores; no SC fence / L1 flush needed
-        W.sy.sync();
-        if (prof)
-            prof[2] = gtimer();
+        if (prof && W.t == 0)
+            prof[1] = prof[2] = gtimer();
         W.update(prof);
-        // publish: bar.sync + gpu-scope release reductions make every
-        // thread's field stores visible before a successor can count them
         W.sy.sync();
-        if (prof)
+        if (prof && W.t == 0)
             prof[5] = gtimer();
-        const uint32_t sb = __ldg(a.succ_off + unit), se = __ldg(a.succ_off + unit + 1);
-        for (uint32_t k = sb + W.t; k < se; k += GT)
-            red_release_add(a.count + size_t(__ldg(a.succs + k)) * nchunks + chunk, 1u);
-        if (W.t == 0) {
-            *s_task = int(nxt);
-            if (prof)
+        // count in at the successors right away (the chain waits on it): warp 1
+        // issues one gpu-scope release reduction per successor (cumulative over
+        // the group's stores through the bar.sync above); the other warps go
+        // on to the next task's setup meanwhile
+        if (warp == 1) {
+            const uint32_t sb = __ldg(a.succ_off + unit), se = __ldg(a.succ_off + unit + 1);
+            for (uint32_t k = sb + lane; k < se; k += 32)
+                red_release_add(a.count + size_t(__ldg(a.succs + k)) * nchunks + chunk, 1u);
+            if (prof && lane == 0)
                 prof[6] = gtimer();
         }
+        if (W.t == 0)
+            *s_task = int(nxt);
         W.sy.sync();
         task = *s_task;
     }
+    (void)has_prev;
+    (void)prev_unit;
+    (void)prev_chunk;
+    (void)prev_prof;
 }
 
 template <int P>
@@ -517,21 +558,26 @@ static void flow_launch_t(FlowArgs& a, size_t smem, int sms, cudaStream_t st) {
 }
 
 void launch_mart_flow(const MartArgs& h, const uint32_t* order, const uint32_t* pred_off,
-                      const uint32_t* succ_off, const uint32_t* succs, unsigned* count,
-                      unsigned* next, unsigned epoch, int n_rings, uint64_t units,
-                      const FlowSlab& slab, cudaStream_t st, unsigned long long* prof) {
+                      const uint32_t* succ_off, const uint32_t* succs, const uint32_t* npred_x,
+                      unsigned* count, unsigned* next, unsigned epoch, int sweeps, int n_rings,
+                      uint64_t units, const FlowSlab& slab, cudaStream_t st,
+                      unsigned long long* prof) {
     int dev = 0, sms = 0;
     UB_CUDA(cudaGetDevice(&dev));
     UB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    if (units * uint64_t(h.nchunks) * uint64_t(sweeps) >= (1ull << 31))
+        throw CudaError("mart_flow_kernel: too many tasks for one launch");
     FlowArgs a;
     a.m = h;
     a.order = order;
     a.pred_off = pred_off;
     a.succ_off = succ_off;
     a.succs = succs;
+    a.npred_x = npred_x;
     a.count = count;
     a.next = next;
     a.epoch = epoch;
+    a.n_sweeps = sweeps;
     a.n_tasks = int(units * uint64_t(h.nchunks));
     a.n_units = int(units);
     a.n_rings = n_rings;

@@ -37,6 +37,14 @@ public:
     // successors (transpose of preds): succ_off (units + 1), succs
     void successors(std::vector<uint32_t>& succ_off, std::vector<uint32_t>& succs) const;
 
+    // Cross-sweep dependencies (for sweeps run back to back): a unit's
+    // cross predecessors are the final writers, in the previous sweep, of the
+    // cells it is the first in its sweep to touch. npred_x (units) counts
+    // them; succ_all merges in- and cross-successors (a unit can appear in
+    // both lists, it is then counted once for each).
+    void cross(std::vector<uint32_t>& npred_x, std::vector<uint32_t>& succ_all_off,
+               std::vector<uint32_t>& succ_all) const;
+
     uint32_t levels() const { return max_level_; }
 
     static constexpr uint32_t kNone = 0xFFFFFFFFu;
@@ -47,6 +55,8 @@ private:
     std::vector<uint32_t> level_;
     std::vector<uint32_t> pred_off_{0u};
     std::vector<uint32_t> preds_;
+    std::vector<uint32_t> first_off_{0u};  // per unit: cells it touches first in the sweep
+    std::vector<uint32_t> first_cells_;
     std::vector<uint32_t> scratch_;
     uint32_t max_level_ = 0;
 };

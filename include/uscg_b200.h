@@ -198,16 +198,19 @@ uscg_status uscg_resample(uscg_ctx ctx, const uscg_grid* grid, const float* fiel
 uscg_status uscg_uspg_to_cg_map(uscg_ctx ctx, int32_t n, uint32_t* out);
 
 /* ---- MART dependency schedule (host only) ---------------------------------
- * The schedule the device executors run, from explicit supports: units in
- * sweep order, support of unit u = idx[pos[u] .. pos[u+1]) (cell indices <
- * cell_count). Outputs: levels (return via *levels), order (units, sorted by
- * ASAP level, stable), level_off (levels + 1; caller provides units + 1),
- * pred_off (units + 1) and preds (caller provides pos[units] entries: at most
- * one predecessor per support cell; *n_preds receives the count). */
-uscg_status uscg_schedule_build(uint32_t units, const uint32_t* pos, const uint32_t* idx,
-                                uint64_t cell_count, uint32_t* order, uint32_t* level_off,
-                                uint32_t* levels, uint32_t* pred_off, uint32_t* preds,
-                                uint64_t* n_preds);
+ * The schedule the device executors run, from explicit supports: lines in
+ * sweep order, support of line u = idx[pos[u] .. pos[u+1]) (cell indices <
+ * cell_count), grouped into runs of `run` consecutive lines of a view
+ * (run = 1: the line DAG). Outputs, per run: order (sorted by ASAP level,
+ * stable), level_off (levels + 1; caller provides runs + 1), *levels,
+ * pred_off (runs + 1), preds (caller provides pos[units] entries;
+ * *n_preds receives the count), npred_x (cross-sweep predecessors per run,
+ * optional). */
+uscg_status uscg_schedule_build(uint32_t units, uint32_t lines_per_view, uint32_t run,
+                                const uint32_t* pos, const uint32_t* idx, uint64_t cell_count,
+                                uint32_t* order, uint32_t* level_off, uint32_t* levels,
+                                uint32_t* pred_off, uint32_t* preds, uint64_t* n_preds,
+                                uint32_t* npred_x);
 
 /* ---- diagnostics ---------------------------------------------------------
  * The device math the generator uses, for parity tests against glibc:

@@ -129,6 +129,7 @@ struct uscg_tracer_s {
     DevBuf<uint32_t> d_level_off;
     DevBuf<unsigned> d_bar;
     DevBuf<uint32_t> d_pred_off, d_preds, d_succ_off, d_succs, d_npred_x;
+    int run = 1, n_runs = 0, runs_per_view = 0;  // run-granular schedule (dataflow)
     uint64_t n_preds = 0;
     DevBuf<unsigned> d_done;  // dataflow flags [units * nchunks]
     DevBuf<uint32_t> w_slab;  // dataflow trace slab
@@ -395,6 +396,32 @@ void ensure_crossed(uscg_tracer_s* t) {
     t->crossed_built = true;
 }
 
+// MART executor (USCG_MART_MODE): 0 "flow" (default) dataflow over run
+// dependency counters; 1 "barrier" one grid barrier per level; 2 "levels" a
+// CUDA graph with one kernel node per level.
+int mart_mode() {
+    static const int mode = [] {
+        const char* e = std::getenv("USCG_MART_MODE");
+        const std::string m = e ? e : "flow";
+        return m == "levels" ? 2 : (m == "barrier" ? 1 : 0);
+    }();
+    return mode;
+}
+
+// lines per run for the dataflow executor (USCG_RUN, default 4): the largest
+// divisor of the lines per view not above the request; 1 for the level executors
+int run_length(int lines) {
+    if (mart_mode() != 0)
+        return 1;
+    int want = 4;
+    if (const char* e = std::getenv("USCG_RUN"))
+        want = std::max(1, std::atoi(e));
+    for (int r = std::min(want, lines); r > 1; --r)
+        if (lines % r == 0)
+            return r;
+    return 1;
+}
+
 void build_schedule(uscg_tracer_s* t) {
     if (t->sched_built)
         return;
@@ -402,7 +429,16 @@ void build_schedule(uscg_tracer_s* t) {
     UB_CUDA(cudaEventCreate(&e0));
     UB_CUDA(cudaEventCreate(&e1));
     const auto h0 = std::chrono::steady_clock::now();
-    AsapSchedule sched(t->cells);
+    t->run = run_length(t->lines);
+    // a run's index lists live in shared memory (4 groups per CTA): keep the
+    // per-group lists under ~48 KiB
+    while (t->run > 1 && size_t(t->run) * size_t(t->max_cells) * 4 > 48 * 1024) {
+        int r = t->run - 1;
+        while (r > 1 && t->lines % r != 0)
+            --r;
+        t->run = r;
+    }
+    AsapSchedule sched(t->cells, uint32_t(t->lines), uint32_t(t->run));
     const uint64_t units = t->units();
     const uint64_t batch_cells = 1ull << 25;  // 128 MiB of indices per batch
     std::vector<uint32_t> pos;
@@ -433,6 +469,9 @@ void build_schedule(uscg_tracer_s* t) {
         sched.add(idx.data(), pos.data(), n);
         u0 = u1;
     }
+    sched.done();
+    t->n_runs = int(sched.runs());
+    t->runs_per_view = int(sched.runs_per_view());
     std::vector<uint32_t> order;
     sched.finish(order, t->level_off);
     t->d_order.alloc(std::max<size_t>(order.size(), 1));
@@ -942,22 +981,17 @@ uscg_status uscg_reconstruct(uscg_tracer t, const float* proj, int32_t problems,
         h.nchunks = Sp / P;
         h.max_recs = t->max_recs;
         h.max_cells = t->max_cells;
+        h.run = t->run;
         t->d_args.ensure(1);
         UB_CUDA(cudaMemcpyAsync(t->d_args.p, &h, sizeof(MartArgs), cudaMemcpyHostToDevice, st));
-        // MART executor (USCG_MART_MODE): "flow" (default) dataflow over
-        // per-task done flags; "barrier" one grid barrier per level;
-        // "levels" a CUDA graph with one kernel node per level.
-        static const int mode = [] {
-            const char* e = std::getenv("USCG_MART_MODE");
-            const std::string m = e ? e : "flow";
-            return m == "levels" ? 2 : (m == "barrier" ? 1 : 0);
-        }();
-        const int exec_mode = P <= 8 ? mode : 2;
+        const int exec_mode = P <= 8 ? mart_mode() : 2;
+        need(exec_mode != 2 || t->run == 1, "the level executor needs a line-granular schedule");
         if (exec_mode == 2)
             ensure_graph(t, h);
         if (exec_mode == 0 && t->done_chunks != h.nchunks) {
-            t->d_done.alloc(units * uint64_t(h.nchunks));
-            UB_CUDA(cudaMemsetAsync(t->d_done.p, 0, sizeof(unsigned) * units * h.nchunks, st));
+            const uint64_t n = uint64_t(t->n_runs) * uint64_t(h.nchunks);
+            t->d_done.alloc(n);
+            UB_CUDA(cudaMemsetAsync(t->d_done.p, 0, sizeof(unsigned) * n, st));
             t->done_chunks = h.nchunks;
             t->epoch = 0;
         }
@@ -985,14 +1019,14 @@ uscg_status uscg_reconstruct(uscg_tracer t, const float* proj, int32_t problems,
                 n_run = track ? 1 : cfg->max_sweeps - sweep;
                 // USCG_SWEEP_PROFILE=<file>: per-task stamps {grab, traced, ready, published}
                 static const char* prof_path = std::getenv("USCG_SWEEP_PROFILE");
-                const size_t nt = size_t(units) * h.nchunks * n_run;
+                const size_t nt = size_t(t->n_runs) * h.nchunks * n_run;
                 DevBuf<unsigned long long> prof;
                 if (prof_path)
                     prof.alloc(nt * 8);
                 if (prof_path)
                     UB_CUDA(cudaMemsetAsync(prof.p, 0, sizeof(unsigned long long) * nt * 8, st));
                 FlowSlab slab;
-                slab.Q = int(std::min<uint64_t>(units, 4096));
+                slab.Q = int(std::min<uint64_t>(units, 8192));
                 slab.slot_words = (t->max_cells + 1 + 31) & ~31;
                 t->w_slab.ensure(size_t(slab.Q) * slab.slot_words);
                 t->w_slab_ctl.ensure(size_t(slab.Q) * 2 + 1);
@@ -1000,9 +1034,17 @@ uscg_status uscg_reconstruct(uscg_tracer t, const float* proj, int32_t problems,
                 slab.ready = t->w_slab_ctl.p;
                 slab.used = t->w_slab_ctl.p + slab.Q;
                 slab.tnext = t->w_slab_ctl.p + 2 * slab.Q;
-                launch_mart_flow(h, t->d_order.p, t->d_pred_off.p, t->d_succ_off.p, t->d_succs.p,
-                                 t->d_npred_x.p, t->d_done.p, t->d_bar.p + 1, t->epoch + 1, n_run,
-                                 t->n_rings, units, slab, st, prof.p);
+                FlowSchedule fs;
+                fs.order = t->d_order.p;
+                fs.pred_off = t->d_pred_off.p;
+                fs.succ_off = t->d_succ_off.p;
+                fs.succs = t->d_succs.p;
+                fs.npred_x = t->d_npred_x.p;
+                fs.n_runs = t->n_runs;
+                fs.run = t->run;
+                fs.runs_per_view = t->runs_per_view;
+                launch_mart_flow(h, fs, t->d_done.p, t->d_bar.p + 1, t->epoch + 1, n_run, t->n_rings,
+                                 slab, st, prof.p);
                 t->epoch += unsigned(n_run);
                 if (prof_path) {
                     std::vector<unsigned long long> hp(nt * 8);
@@ -1210,22 +1252,27 @@ uscg_status uscg_diag_math(uscg_ctx ctx, int32_t n, const double* x, const doubl
 
 }  // extern "C"
 
-extern "C" uscg_status uscg_schedule_build(uint32_t units, const uint32_t* pos, const uint32_t* idx,
+extern "C" uscg_status uscg_schedule_build(uint32_t units, uint32_t lines_per_view, uint32_t run,
+                                           const uint32_t* pos, const uint32_t* idx,
                                            uint64_t cell_count, uint32_t* order,
                                            uint32_t* level_off, uint32_t* levels,
-                                           uint32_t* pred_off, uint32_t* preds,
-                                           uint64_t* n_preds) {
+                                           uint32_t* pred_off, uint32_t* preds, uint64_t* n_preds,
+                                           uint32_t* npred_x) {
     return guarded([&] {
         need(pos && idx && order && level_off && levels, "null buffer");
+        need(lines_per_view >= 1 && run >= 1 && lines_per_view % run == 0 &&
+                 units % lines_per_view == 0,
+             "runs must tile the views");
         for (uint32_t u = 0; u < units; ++u)
             need(pos[u] <= pos[u + 1], "support offsets must be non-decreasing");
         for (uint32_t i = 0; i < pos[units]; ++i)
             need(idx[i] < cell_count, "support cell out of range");
-        AsapSchedule s(cell_count);
+        AsapSchedule s(cell_count, lines_per_view, run);
         std::vector<uint32_t> rel(pos, pos + units + 1);
         for (auto& p : rel)
             p -= pos[0];
         s.add(idx + pos[0], rel.data(), units);
+        s.done();
         std::vector<uint32_t> ord, loff;
         s.finish(ord, loff);
         std::memcpy(order, ord.data(), sizeof(uint32_t) * ord.size());
@@ -1237,5 +1284,10 @@ extern "C" uscg_status uscg_schedule_build(uint32_t units, const uint32_t* pos, 
             std::memcpy(preds, s.preds().data(), sizeof(uint32_t) * s.preds().size());
         if (n_preds)
             *n_preds = s.preds().size();
+        if (npred_x) {
+            std::vector<uint32_t> nx, so, sa;
+            s.cross(nx, so, sa);
+            std::memcpy(npred_x, nx.data(), sizeof(uint32_t) * nx.size());
+        }
     });
 }

@@ -21,6 +21,7 @@ struct MartArgs {
     int nchunks;
     int max_recs;
     int max_cells;
+    int run = 1;  // lines per dataflow task: shared memory holds `run` index lists per group
 };
 
 // problem-chunk width P for S problems (power of two <= 32)
@@ -77,13 +78,23 @@ struct FlowSlab {
 };
 
 // K3 dataflow: tasks wait only on their predecessors (dependency counters)
+// The run-granular dependency schedule on the device (schedule.h)
+struct FlowSchedule {
+    const uint32_t* order;     // runs in topological order
+    const uint32_t* pred_off;  // runs + 1
+    const uint32_t* succ_off;  // runs + 1 (in- and cross-sweep successors)
+    const uint32_t* succs;
+    const uint32_t* npred_x;   // runs
+    int n_runs;
+    int run;                   // lines per run
+    int runs_per_view;
+};
+
 // Runs `sweeps` sweeps back to back (cross-sweep dependencies, no boundary);
 // epoch = global 1-based index of the first of them.
-void launch_mart_flow(const MartArgs& h, const uint32_t* order, const uint32_t* pred_off,
-                      const uint32_t* succ_off, const uint32_t* succs, const uint32_t* npred_x,
-                      unsigned* count, unsigned* next, unsigned epoch, int sweeps, int n_rings,
-                      uint64_t units, const FlowSlab& slab, cudaStream_t st,
-                      unsigned long long* prof = nullptr);
+void launch_mart_flow(const MartArgs& h, const FlowSchedule& fs, unsigned* count, unsigned* next,
+                      unsigned epoch, int sweeps, int n_rings, const FlowSlab& slab,
+                      cudaStream_t st, unsigned long long* prof = nullptr);
 
 // per-problem projection statistics: stats[p*4 + {0: count>0, 1: sum>0, 2: any!=0, 3: invalid}]
 void launch_proj_stats(const float* proj, int units, int S, int Sp, double* stats, cudaStream_t st);

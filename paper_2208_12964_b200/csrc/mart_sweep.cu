@@ -57,14 +57,16 @@ __device__ __forceinline__ unsigned long long gtimer() {
     return t;
 }
 
-__host__ __device__ inline size_t trace_words(int max_recs, int max_cells) {
-    size_t w = size_t(max_recs) * 4 + 1 + GT / 32 + size_t(max_cells);
+// trace arrays; the index-list area holds `run` lists (a dataflow task's run)
+__host__ __device__ inline size_t trace_words(int max_recs, int max_cells, int run) {
+    size_t w = size_t(max_recs) * 4 + 1 + GT / 32 + size_t(max_cells) * size_t(run);
     return (w + 1) & ~size_t(1);
 }
 
-__host__ __device__ inline size_t group_words(int P, int max_recs, int max_cells) {
-    // trace arrays + red (doubles) + fac (doubles) + meta
-    return trace_words(max_recs, max_cells) + 2 * size_t(GT / 32) * P + 2 * size_t(P) + 4;
+__host__ __device__ inline size_t group_words(int P, int max_recs, int max_cells, int run) {
+    // trace arrays + red (doubles) + fac (doubles) + meta (4 ints) + per-line cell counts
+    return trace_words(max_recs, max_cells, run) + 2 * size_t(GT / 32) * P + 2 * size_t(P) + 4 +
+           ((size_t(run) + 1) & ~size_t(1));
 }
 
 // One thread group's state and task code.
@@ -77,6 +79,8 @@ struct GroupWorker {
     double* red;   // [GT/32][P]
     double* fac;   // [P]
     int* meta;     // [0]: cells, [1]: unit, [2]: chunk, [3]: scratch (task id)
+    int* line_n;   // [run]: cells of each line of the task's run
+    uint32_t* idx0;  // first index list (tr.idx is pointed at line j's list)
     GroupSync<GT> sy;
     int t;
     // per-task prefetched scalars (valid in threads t < P)
@@ -89,16 +93,18 @@ struct GroupWorker {
           sy{1 + int(threadIdx.x) / GT}, t(int(threadIdx.x) % GT) {
         const int g = int(threadIdx.x) / GT;
         uint32_t* gbase = smem + (sizeof(RingRow) / 4) * (n_rings + 1) +
-                          size_t(g) * group_words(P, A.max_recs, A.max_cells);
+                          size_t(g) * group_words(P, A.max_recs, A.max_cells, A.run);
         tr.base = gbase;
         tr.lohi = tr.base + A.max_recs;
         tr.cnt = tr.lohi + A.max_recs;
         tr.pos = tr.cnt + A.max_recs;
         tr.warp = tr.pos + A.max_recs + 1;
         tr.idx = tr.warp + GT / 32;
-        red = reinterpret_cast<double*>(gbase + trace_words(A.max_recs, A.max_cells));
+        idx0 = tr.idx;
+        red = reinterpret_cast<double*>(gbase + trace_words(A.max_recs, A.max_cells, A.run));
         fac = red + (GT / 32) * P;
         meta = reinterpret_cast<int*>(fac + P);
+        line_n = meta + 4;
     }
 
     // trace (unit, chunk) into the group's smem and prefetch its scalars
@@ -331,7 +337,7 @@ __device__ __forceinline__ void stage_rings(uint32_t* smem, const RingRow* rings
 size_t sweep_smem_bytes(const MartArgs& a, int n_rings) {
     const int P = a.Sp / a.nchunks;
     const size_t rings = sizeof(RingRow) * size_t(n_rings + 1);
-    return rings + sizeof(uint32_t) * GROUPS * group_words(P, a.max_recs, a.max_cells);
+    return rings + sizeof(uint32_t) * GROUPS * group_words(P, a.max_recs, a.max_cells, a.run);
 }
 
 // ============================================================================
@@ -340,19 +346,20 @@ size_t sweep_smem_bytes(const MartArgs& a, int n_rings) {
 
 struct FlowArgs {
     MartArgs m;
-    const uint32_t* order;     // units in topological (level) order
-    const uint32_t* pred_off;  // by unit id: number of predecessors = pred_off[u+1] - pred_off[u]
-    const uint32_t* succ_off;  // by unit id: in-sweep and cross-sweep successors
-    const uint32_t* succs;     // successor unit ids
-    const uint32_t* npred_x;   // by unit id: cross-sweep predecessors
-    unsigned* count;           // [units * nchunks]: predecessors completed, cumulative over sweeps
+    const uint32_t* order;     // runs in topological (level) order
+    const uint32_t* pred_off;  // by run id: in-sweep predecessors = pred_off[r+1] - pred_off[r]
+    const uint32_t* succ_off;  // by run id: in-sweep and cross-sweep successors
+    const uint32_t* succs;     // successor run ids
+    const uint32_t* npred_x;   // by run id: cross-sweep predecessors
+    unsigned* count;           // [runs * nchunks]: predecessors completed, cumulative over sweeps
     unsigned* next;            // updater task queue head (zeroed per launch)
     unsigned epoch;            // global index (1-based) of this launch's first sweep
     int n_sweeps;              // sweeps run back to back by this launch
-    int n_tasks;               // units * nchunks (per sweep)
-    int n_units;
+    int n_runs;                // runs per sweep
+    int run;                   // lines per run (divides lines per view)
+    int runs_per_view;
     int n_rings;
-    FlowSlab slab;             // traced index lists, written once per unit by tracer CTAs
+    FlowSlab slab;             // traced index lists, one slot per line
     int tracer_ctas;
     unsigned long long* prof;  // optional: per task phase stamps (ns)
 };
@@ -369,28 +376,36 @@ __device__ __forceinline__ void spin_until_geq(const unsigned* p, unsigned targe
     }
 }
 
-// Tracer role: trace every unit once, in topological order, into a ring of
-// Q slab slots. A slot is rewritten only after every chunk task of its
+// line (unit) id of line j of run `run`
+__device__ __forceinline__ uint32_t run_line(const FlowArgs& a, uint32_t run, int j) {
+    const uint32_t view = run / uint32_t(a.runs_per_view);
+    const uint32_t r = run % uint32_t(a.runs_per_view);
+    return view * uint32_t(a.m.tr.lines) + r * uint32_t(a.run) + uint32_t(j);
+}
+
+// Tracer role: trace every line once, in topological run order, into a ring
+// of Q slab slots. A slot is rewritten only after every chunk task of its
 // previous occupant has copied it.
 template <int P>
 __device__ void flow_tracer(const FlowArgs& a, GroupWorker<P>& W) {
     const int nchunks = a.m.nchunks;
     const int Q = a.slab.Q;
     int* s_i = W.meta + 3;
-    const int total = a.n_units * a.n_sweeps;
+    const long long total = (long long)a.n_runs * a.n_sweeps * a.run;
     while (true) {
         if (W.t == 0)
             *s_i = int(atomicAdd(a.slab.tnext, 1u));
         W.sy.sync();
-        const int i = *s_i;  // sequence over (sweep, order position)
-        if (i >= total)
+        const int seq = *s_i;  // ((sweep * n_runs) + order position) * run + j
+        if (seq >= total)
             break;
-        const uint32_t unit = __ldg(a.order + i % a.n_units);
+        const int pos = (seq / a.run) % a.n_runs;
+        const uint32_t unit = run_line(a, __ldg(a.order + pos), seq % a.run);
         const int v = int(unit / uint32_t(a.m.tr.lines)), line = int(unit % uint32_t(a.m.tr.lines));
         const int n = scope_trace(a.m.tr, __ldg(a.m.tr.off + line), __ldg(a.m.tr.off + line + 1),
                                   __ldg(a.m.tr.theta + v), W.tr, true, W.s_rings, W.sy);
-        const int slot = i % Q;
-        const unsigned gen = unsigned(i / Q);
+        const int slot = seq % Q;
+        const unsigned gen = unsigned(seq / Q);
         if (W.t == 0 && gen > 0)
             spin_until_geq(a.slab.used + slot, gen * unsigned(nchunks));
         W.sy.sync();
@@ -406,24 +421,10 @@ __device__ void flow_tracer(const FlowArgs& a, GroupWorker<P>& W) {
     }
 }
 
-// Updater role: (unit, chunk) tasks in topological order; copy the unit's
-// index list from the slab, wait for the predecessors of this chunk, update,
-// count in at the successors.
-// Count a finished task in at its successors: one gpu-scope acq_rel fence
-// (cumulative over the group's stores through the preceding bar.sync), then
-// relaxed reductions. Issued by one lane so the fence's store-completion wait
-// overlaps the rest of the group's next task.
-__device__ __forceinline__ void publish_task(const FlowArgs& a, uint32_t unit, int chunk) {
-    asm volatile("fence.acq_rel.gpu;" ::: "memory");
-    const int nchunks = a.m.nchunks;
-    const uint32_t sb = __ldg(a.succ_off + unit), se = __ldg(a.succ_off + unit + 1);
-    for (uint32_t k = sb; k < se; ++k)
-        asm volatile("red.relaxed.gpu.global.add.u32 [%0], %1;" ::"l"(
-                         a.count + size_t(__ldg(a.succs + k)) * nchunks + chunk),
-                     "r"(1u)
-                     : "memory");
-}
-
+// Updater role: (run, chunk) tasks in topological order. Wait once for the
+// run's predecessors of this chunk, then update the run's lines in order
+// (the chain between them stays inside the group), then count in at the
+// run's successors.
 template <int P>
 __device__ void flow_updater(const FlowArgs& a, GroupWorker<P>& W) {
     constexpr int kCopy = GT - 32;  // warps 0, 2..7 copy the slab; warp 1 waits / publishes
@@ -436,79 +437,87 @@ __device__ void flow_updater(const FlowArgs& a, GroupWorker<P>& W) {
         *s_task = int(atomicAdd(a.next, 1u));
     W.sy.sync();
     int task = *s_task;
-    bool has_prev = false;
-    uint32_t prev_unit = 0;
-    int prev_chunk = 0;
     unsigned long long* prof = nullptr;
-    unsigned long long* prev_prof = nullptr;
-    const int total = a.n_tasks * a.n_sweeps;
+    const int per_sweep = a.n_runs * nchunks;
+    const int total = per_sweep * a.n_sweeps;
     while (task < total) {
         if (a.prof) {
             prof = a.prof + 8 * size_t(task);
             if (W.t == 0)
                 prof[0] = gtimer();
         }
-        const int sweep = task / a.n_tasks;            // 0-based within this launch
-        const int i = (task % a.n_tasks) / nchunks;    // order position
-        const uint32_t unit = __ldg(a.order + i);
+        const int sweep = task / per_sweep;  // 0-based within this launch
+        const int pos = (task % per_sweep) / nchunks;
         const int chunk = task % nchunks;
-        const int seq = sweep * a.n_units + i;         // tracer sequence of this unit
-        const int slot = seq % Q;
+        const uint32_t run = __ldg(a.order + pos);
         // claim the next task early; its latency overlaps this one
         unsigned nxt = 0;
         if (W.t == 0)
             nxt = atomicAdd(a.next, 1u);
-        if (W.t < P) {
-            const size_t c2 = size_t(chunk) * P + W.t;
-            W.m_next = __ldg(a.m.proj + size_t(unit) * a.m.Sp + c2);
-            W.pf_next = __ldg(a.m.p_floor + c2);
-            W.act_next = __ldg(a.m.active + c2) != 0;
-        }
+        const int seq0 = (sweep * a.n_runs + pos) * a.run;
         if (warp == 1) {
             if (lane == 0) {
-                // wait until every predecessor's update of this chunk counted in:
-                // one poller per group on one counter (push model)
-                // sweep s (global, 1-based) needs s in-sweep and s-1 cross-sweep
-                // rounds of its predecessors counted in
+                // the run's predecessors of this chunk: sweep s (global,
+                // 1-based) needs s in-sweep and s-1 cross-sweep rounds
                 const unsigned s = a.epoch + unsigned(sweep);
-                const unsigned npred = __ldg(a.pred_off + unit + 1) - __ldg(a.pred_off + unit);
-                const unsigned target = s * npred + (s - 1) * __ldg(a.npred_x + unit);
+                const unsigned npred = __ldg(a.pred_off + run + 1) - __ldg(a.pred_off + run);
+                const unsigned target = s * npred + (s - 1) * __ldg(a.npred_x + run);
                 if (target)
-                    spin_until_geq(a.count + size_t(unit) * nchunks + chunk, target);
+                    spin_until_geq(a.count + size_t(run) * nchunks + chunk, target);
             }
         } else {
-            // the unit's index list from the slab (L2 reads: slots are rewritten)
+            // every line's index list of the run, from the slab into shared
+            // memory, while the predecessors finish (L2 reads: slots are rewritten)
             if (W.t == 0)
-                spin_until_geq(a.slab.ready + slot, unsigned(seq / Q) + 1);
+                for (int j = 0; j < a.run; ++j)
+                    spin_until_geq(a.slab.ready + (seq0 + j) % Q, unsigned((seq0 + j) / Q) + 1);
             copy_sync.sync();
             const int ct = W.t < 32 ? W.t : W.t - 32;
-            const uint32_t* src = a.slab.data + size_t(slot) * a.slab.slot_words;
-            const int n = int(__ldcg(src));
-            for (int c = ct; c < n; c += kCopy)
-                W.tr.idx[c] = __ldcg(src + 1 + c);
+            for (int j = 0; j < a.run; ++j) {
+                const uint32_t* src = a.slab.data + size_t((seq0 + j) % Q) * a.slab.slot_words;
+                const int n = int(__ldcg(src));
+                uint32_t* dst = W.idx0 + size_t(j) * a.m.max_cells;
+                for (int c = ct; c < n; c += kCopy)
+                    dst[c] = __ldcg(src + 1 + c);
+                if (W.t == 0)
+                    W.line_n[j] = n;
+            }
             if (W.t == 0) {
-                W.meta[0] = n;
-                W.meta[1] = int(unit);
+                W.meta[1] = int(run);
                 W.meta[2] = chunk;
             }
         }
-        // index list copied, predecessors counted in (their acquire orders the
-        // gathers after the released stores), previous task published
+        // index lists copied and the predecessors counted in (their acquire
+        // orders the gathers after the released stores); later lines of the
+        // run follow the group's own stores (bar.sync between lines)
         W.sy.sync();
-        if (W.t == 0)
-            red_release_add(a.slab.used + slot, 1u);
+        if (W.t < a.run)
+            red_release_add(a.slab.used + (seq0 + W.t) % Q, 1u);
         if (prof && W.t == 0)
             prof[1] = prof[2] = gtimer();
-        W.update(prof);
-        W.sy.sync();
+        for (int j = 0; j < a.run; ++j) {
+            if (W.t < P) {
+                const uint32_t unit = run_line(a, run, j);
+                const size_t c2 = size_t(chunk) * P + W.t;
+                W.m_next = __ldg(a.m.proj + size_t(unit) * a.m.Sp + c2);
+                W.pf_next = __ldg(a.m.p_floor + c2);
+                W.act_next = __ldg(a.m.active + c2) != 0;
+            }
+            W.tr.idx = W.idx0 + size_t(j) * a.m.max_cells;
+            if (W.t == 0)
+                W.meta[0] = W.line_n[j];
+            W.sy.sync();
+            W.update(j == 0 ? prof : nullptr);
+            W.sy.sync();
+        }
+        W.tr.idx = W.idx0;
         if (prof && W.t == 0)
             prof[5] = gtimer();
-        // count in at the successors right away (the chain waits on it): warp 1
-        // issues one gpu-scope release reduction per successor (cumulative over
-        // the group's stores through the bar.sync above); the other warps go
-        // on to the next task's setup meanwhile
+        // count in at the run's successors right away (the chain waits on it):
+        // warp 1 issues one gpu-scope release reduction per successor
+        // (cumulative over the group's stores through the bar.sync above)
         if (warp == 1) {
-            const uint32_t sb = __ldg(a.succ_off + unit), se = __ldg(a.succ_off + unit + 1);
+            const uint32_t sb = __ldg(a.succ_off + run), se = __ldg(a.succ_off + run + 1);
             for (uint32_t k = sb + lane; k < se; k += 32)
                 red_release_add(a.count + size_t(__ldg(a.succs + k)) * nchunks + chunk, 1u);
             if (prof && lane == 0)
@@ -519,10 +528,6 @@ __device__ void flow_updater(const FlowArgs& a, GroupWorker<P>& W) {
         W.sy.sync();
         task = *s_task;
     }
-    (void)has_prev;
-    (void)prev_unit;
-    (void)prev_chunk;
-    (void)prev_prof;
 }
 
 template <int P>
@@ -557,29 +562,28 @@ static void flow_launch_t(FlowArgs& a, size_t smem, int sms, cudaStream_t st) {
     mart_flow_kernel<P><<<grid, CTA, smem, st>>>(a);
 }
 
-void launch_mart_flow(const MartArgs& h, const uint32_t* order, const uint32_t* pred_off,
-                      const uint32_t* succ_off, const uint32_t* succs, const uint32_t* npred_x,
-                      unsigned* count, unsigned* next, unsigned epoch, int sweeps, int n_rings,
-                      uint64_t units, const FlowSlab& slab, cudaStream_t st,
-                      unsigned long long* prof) {
+void launch_mart_flow(const MartArgs& h, const FlowSchedule& fs, unsigned* count, unsigned* next,
+                      unsigned epoch, int sweeps, int n_rings, const FlowSlab& slab,
+                      cudaStream_t st, unsigned long long* prof) {
     int dev = 0, sms = 0;
     UB_CUDA(cudaGetDevice(&dev));
     UB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    if (units * uint64_t(h.nchunks) * uint64_t(sweeps) >= (1ull << 31))
+    if (uint64_t(fs.n_runs) * uint64_t(fs.run) * uint64_t(h.nchunks) * uint64_t(sweeps) >= (1ull << 31))
         throw CudaError("mart_flow_kernel: too many tasks for one launch");
     FlowArgs a;
     a.m = h;
-    a.order = order;
-    a.pred_off = pred_off;
-    a.succ_off = succ_off;
-    a.succs = succs;
-    a.npred_x = npred_x;
+    a.order = fs.order;
+    a.pred_off = fs.pred_off;
+    a.succ_off = fs.succ_off;
+    a.succs = fs.succs;
+    a.npred_x = fs.npred_x;
     a.count = count;
     a.next = next;
     a.epoch = epoch;
     a.n_sweeps = sweeps;
-    a.n_tasks = int(units * uint64_t(h.nchunks));
-    a.n_units = int(units);
+    a.n_runs = fs.n_runs;
+    a.run = fs.run;
+    a.runs_per_view = fs.runs_per_view;
     a.n_rings = n_rings;
     a.slab = slab;
     a.tracer_ctas = 1;

@@ -4,35 +4,54 @@
 
 namespace ub {
 
+AsapSchedule::AsapSchedule(uint64_t cell_count, uint32_t lines_per_view, uint32_t run)
+    : lines_per_view_(lines_per_view ? lines_per_view : 1), run_(run ? run : 1),
+      writer_(cell_count, kNone) {
+    runs_per_view_ = (lines_per_view_ + run_ - 1) / run_;
+}
+
+void AsapSchedule::close_run() {
+    if (cur_run_ == kNone)
+        return;
+    std::sort(scratch_.begin(), scratch_.end());
+    scratch_.erase(std::unique(scratch_.begin(), scratch_.end()), scratch_.end());
+    uint32_t lev = 0;
+    for (uint32_t p : scratch_)
+        lev = std::max(lev, level_[p]);
+    ++lev;
+    preds_.insert(preds_.end(), scratch_.begin(), scratch_.end());
+    pred_off_.push_back(uint32_t(preds_.size()));
+    first_off_.push_back(uint32_t(first_cells_.size()));
+    level_.push_back(lev);
+    max_level_ = std::max(max_level_, lev);
+    scratch_.clear();
+    cur_run_ = kNone;
+}
+
 void AsapSchedule::add(const uint32_t* idx, const uint32_t* pos_rel, uint32_t n) {
-    level_.reserve(level_.size() + n);
-    for (uint32_t u = 0; u < n; ++u) {
-        const uint32_t unit = uint32_t(level_.size());
-        const uint32_t b = pos_rel[u], e = pos_rel[u + 1];
-        uint32_t lev = 0;
-        scratch_.clear();
-        for (uint32_t i = b; i < e; ++i) {
-            lev = std::max(lev, last_[idx[i]]);
-            const uint32_t w = writer_[idx[i]];
+    for (uint32_t i = 0; i < n; ++i, ++lines_added_) {
+        const uint64_t u = lines_added_;
+        const uint32_t run = uint32_t((u / lines_per_view_) * runs_per_view_ +
+                                      (u % lines_per_view_) / run_);
+        if (run != cur_run_) {
+            close_run();
+            cur_run_ = run;  // runs arrive in id order: run == level_.size()
+        }
+        for (uint32_t k = pos_rel[i]; k < pos_rel[i + 1]; ++k) {
+            const uint32_t c = idx[k];
+            const uint32_t w = writer_[c];
+            if (w == run)
+                continue;  // written by an earlier line of this run
             if (w == kNone)
-                first_cells_.push_back(idx[i]);
+                first_cells_.push_back(c);
             else if (scratch_.empty() || scratch_.back() != w)
                 scratch_.push_back(w);
+            writer_[c] = run;
         }
-        first_off_.push_back(uint32_t(first_cells_.size()));
-        std::sort(scratch_.begin(), scratch_.end());
-        scratch_.erase(std::unique(scratch_.begin(), scratch_.end()), scratch_.end());
-        preds_.insert(preds_.end(), scratch_.begin(), scratch_.end());
-        pred_off_.push_back(uint32_t(preds_.size()));
-        ++lev;
-        for (uint32_t i = b; i < e; ++i) {
-            last_[idx[i]] = lev;
-            writer_[idx[i]] = unit;
-        }
-        level_.push_back(lev);
-        max_level_ = std::max(max_level_, lev);
     }
 }
+
+void AsapSchedule::done() { close_run(); }
 
 void AsapSchedule::successors(std::vector<uint32_t>& succ_off,
                               std::vector<uint32_t>& succs) const {
@@ -52,7 +71,7 @@ void AsapSchedule::successors(std::vector<uint32_t>& succ_off,
 void AsapSchedule::cross(std::vector<uint32_t>& npred_x, std::vector<uint32_t>& succ_all_off,
                          std::vector<uint32_t>& succ_all) const {
     const size_t units = level_.size();
-    // cross predecessors: distinct final writers of each unit's first-touch cells
+    // cross predecessors: distinct final writers of each run's first-touch cells
     std::vector<uint32_t> xoff(units + 1, 0u), xpred;
     std::vector<uint32_t> tmp;
     for (size_t u = 0; u < units; ++u) {
@@ -67,7 +86,7 @@ void AsapSchedule::cross(std::vector<uint32_t>& npred_x, std::vector<uint32_t>& 
     npred_x.assign(units, 0u);
     for (size_t u = 0; u < units; ++u)
         npred_x[u] = xoff[u + 1] - xoff[u];
-    // successors of p: units listing p as an in-sweep or a cross predecessor
+    // successors of p: runs listing p as an in-sweep or a cross-sweep predecessor
     succ_all_off.assign(units + 1, 0u);
     for (uint32_t p : preds_)
         ++succ_all_off[p + 1];
@@ -86,15 +105,15 @@ void AsapSchedule::cross(std::vector<uint32_t>& npred_x, std::vector<uint32_t>& 
 }
 
 void AsapSchedule::finish(std::vector<uint32_t>& order, std::vector<uint32_t>& level_off) const {
-    level_off.assign(size_t(max_level_) + 1, 0u);
+    std::vector<uint32_t> cnt(size_t(max_level_) + 1, 0u);
     for (uint32_t lev : level_)
-        ++level_off[lev];  // level_off[l] counts level l (1-based) for now
-    // exclusive offsets: level l (1-based) occupies [level_off[l-1], level_off[l])
-    uint32_t acc = 0;
+        ++cnt[lev];
+    // level l (1-based) occupies [start[l], start[l] + cnt[l])
     std::vector<uint32_t> start(size_t(max_level_) + 1, 0u);
+    uint32_t acc = 0;
     for (uint32_t l = 1; l <= max_level_; ++l) {
         start[l] = acc;
-        acc += level_off[l];
+        acc += cnt[l];
     }
     order.assign(level_.size(), 0u);
     std::vector<uint32_t> cur(start);

@@ -160,8 +160,8 @@ def load(build_if_missing: bool = True):
     L.uscg_resample.argtypes = [vp, C.POINTER(_Grid), vp, C.c_int32, C.c_int32, vp, C.c_uint32]
     L.uscg_uspg_to_cg_map.argtypes = [vp, C.c_int32, _u32p]
     L.uscg_diag_math.argtypes = [vp, C.c_int32, _dp, _dp, _dp]
-    L.uscg_schedule_build.argtypes = [C.c_uint32, _u32p, _u32p, C.c_uint64, _u32p, _u32p, _u32p, _u32p, _u32p,
-                                      C.POINTER(C.c_uint64)]
+    L.uscg_schedule_build.argtypes = [C.c_uint32, C.c_uint32, C.c_uint32, _u32p, _u32p, C.c_uint64, _u32p, _u32p,
+                                      _u32p, _u32p, _u32p, C.POINTER(C.c_uint64), _u32p]
     for name in EXPORTS:
         if name not in ("uscg_last_error", "uscg_version", "uscg_launch_count", "uscg_problem_stride"):
             getattr(L, name).restype = C.c_int
@@ -683,24 +683,28 @@ def diag_math(x, y, ctx: Optional[Context] = None) -> np.ndarray:
     return out
 
 
-def schedule_build(supports, cell_count: int):
+def schedule_build(supports, cell_count: int, lines_per_view: Optional[int] = None, run: int = 1):
     """The MART dependency schedule (host C++, no device needed) from explicit
-    supports in sweep order: returns dict(levels, order, level_off, pred_off, preds)."""
-    pos = np.zeros(len(supports) + 1, np.uint32)
+    supports in sweep order, grouped into runs of `run` consecutive lines of a
+    view: dict(levels, order, level_off, pred_off, preds, npred_x) per run."""
+    n = len(supports)
+    lpv = n if lines_per_view is None else int(lines_per_view)
+    pos = np.zeros(n + 1, np.uint32)
     pos[1:] = np.cumsum([len(s) for s in supports])
     idx = np.ascontiguousarray(np.concatenate([np.asarray(s, np.uint32) for s in supports])
-                               if len(supports) else np.zeros(0, np.uint32), dtype=np.uint32)
-    n = len(supports)
-    order = np.zeros(max(n, 1), np.uint32)
-    level_off = np.zeros(n + 1, np.uint32)
+                               if n else np.zeros(0, np.uint32), dtype=np.uint32)
+    runs = n // max(run, 1) if n else 0
+    order = np.zeros(max(runs, 1), np.uint32)
+    level_off = np.zeros(runs + 1, np.uint32)
     levels = np.zeros(1, np.uint32)
-    pred_off = np.zeros(n + 1, np.uint32)
+    pred_off = np.zeros(runs + 1, np.uint32)
     preds = np.zeros(max(int(pos[-1]), 1), np.uint32)
+    npred_x = np.zeros(max(runs, 1), np.uint32)
     npreds = C.c_uint64()
-    _check(load().uscg_schedule_build(n, pos.ctypes.data_as(_u32p), idx.ctypes.data_as(_u32p), cell_count,
+    _check(load().uscg_schedule_build(n, lpv, run, pos.ctypes.data_as(_u32p), idx.ctypes.data_as(_u32p), cell_count,
                                       order.ctypes.data_as(_u32p), level_off.ctypes.data_as(_u32p),
                                       levels.ctypes.data_as(_u32p), pred_off.ctypes.data_as(_u32p),
-                                      preds.ctypes.data_as(_u32p), C.byref(npreds)))
+                                      preds.ctypes.data_as(_u32p), C.byref(npreds), npred_x.ctypes.data_as(_u32p)))
     L = int(levels[0])
-    return dict(levels=L, order=order[:n], level_off=level_off[:L + 1], pred_off=pred_off,
-                preds=preds[:npreds.value])
+    return dict(levels=L, order=order[:runs], level_off=level_off[:L + 1], pred_off=pred_off,
+                preds=preds[:npreds.value], npred_x=npred_x[:runs])

@@ -408,12 +408,13 @@ int mart_mode() {
     return mode;
 }
 
-// lines per run for the dataflow executor (USCG_RUN, default 4): the largest
-// divisor of the lines per view not above the request; 1 for the level executors
-int run_length(int lines) {
+// lines per run for the dataflow executor (USCG_RUN; default 4 for 2D grids,
+// whose adjacent lines always overlap, and 1 for volumes): the largest divisor
+// of the lines per view not above the request; 1 for the level executors
+int run_length(int lines, bool volume) {
     if (mart_mode() != 0)
         return 1;
-    int want = 4;
+    int want = volume ? 1 : 4;
     if (const char* e = std::getenv("USCG_RUN"))
         want = std::max(1, std::atoi(e));
     for (int r = std::min(want, lines); r > 1; --r)
@@ -429,7 +430,7 @@ void build_schedule(uscg_tracer_s* t) {
     UB_CUDA(cudaEventCreate(&e0));
     UB_CUDA(cudaEventCreate(&e1));
     const auto h0 = std::chrono::steady_clock::now();
-    t->run = run_length(t->lines);
+    t->run = run_length(t->lines, t->volume != 0);
     // a run's index lists live in shared memory (4 groups per CTA): keep the
     // per-group lists under ~48 KiB
     while (t->run > 1 && size_t(t->run) * size_t(t->max_cells) * 4 > 48 * 1024) {

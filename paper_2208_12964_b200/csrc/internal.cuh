@@ -146,6 +146,14 @@ struct GroupSync {
     }
 };
 
+// A single warp as the sync scope.
+struct WarpSync {
+    static constexpr int kThreads = 32;
+    __device__ __forceinline__ int tid() const { return int(threadIdx.x) & 31; }
+    __device__ __forceinline__ void sync() const { __syncwarp(); }
+    __device__ __forceinline__ bool sync_or(bool p) const { return __any_sync(0xFFFFFFFFu, p) != 0; }
+};
+
 // Exclusive scan of a[0..n) in place over the sync scope; a[n] receives the
 // total. s_warp must hold NT/32 words. All threads of the scope must call it.
 template <class Sync>

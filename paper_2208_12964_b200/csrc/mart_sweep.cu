@@ -1,23 +1,26 @@
-// K3 (persistent forms): one launch per Sp-MART sweep.
+// K3 (persistent forms): one launch runs one or more Sp-MART sweeps.
 //
-// The host-built schedule (schedule.h) orders the (view, line) units of a
-// sweep topologically: by ASAP level, and for every unit the distinct units
-// that last wrote one of its cells (its direct predecessors). Any execution
-// that runs each unit after all of its predecessors performs, on every cell,
-// exactly the reference's sequence of updates (solver.cpp:111-136).
+// The host-built schedule (schedule.h) groups the lines of a sweep into runs
+// of R consecutive lines of a view and orders the runs topologically; for
+// every run it lists its predecessors (runs that last wrote one of its cells)
+// and, for sweeps run back to back, its cross-sweep predecessors. Any
+// execution that runs every run after its predecessors, its lines in order,
+// performs on every cell exactly the reference's sequence of updates
+// (proj/src/solver.cpp:111-136).
 //
-// Two executors share the group-level task code below:
-//   * mart_flow_kernel (default): dataflow. Thread groups grab
-//     (unit, problem-chunk) tasks from an atomic queue in topological order,
-//     trace them while their predecessors are still running, wait only on the
-//     predecessors' done flags, then gather -> reduce -> factor -> scatter and
-//     publish their own flag. No grid-wide barrier.
+// Executors sharing the group-level task code below:
+//   * mart_flow_kernel (default): dataflow. Tracer CTAs trace every line once,
+//     in topological order, into a bounded slab of index lists. Updater groups
+//     take (run, problem-chunk) tasks from an atomic queue, stage the run's
+//     index lists in shared memory while the run's predecessors finish (one
+//     dependency counter per task, polled by one lane), update the run's lines
+//     in order, then count in at the successors with gpu-scope release
+//     reductions. No grid barrier, no SC fence. Updater groups are 256-thread
+//     groups for problem stacks (float4 over 8 problems per cell) and single
+//     warps for one problem (3D volumes), so that small tasks keep the machine
+//     busy.
 //   * mart_sweep_kernel: one grid barrier per dependency level (cooperative
-//     launch), next task traced between arrive and wait.
-// Latency bounds a chain of dependent units (SURVEY.md §7 hard part 1), so the
-// critical path between two dependent tasks is kept to: flag observed ->
-// gather (one L2 round trip, every cell of a thread in flight) -> reduction
-// -> factor -> scatter -> fence -> flag.
+//     launch), next task traced between arrive and wait (line-granular).
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -30,25 +33,30 @@
 namespace ub {
 
 namespace {
-constexpr int GT = 256;     // threads per group
-constexpr int GROUPS = 4;   // groups per CTA
-constexpr int CTA = GT * GROUPS;
+constexpr int CTA = 1024;   // threads per CTA (one CTA per SM)
+constexpr int TG = 256;     // tracer group / level-barrier group size
 
-// KR: scalar cells held per thread; KV: float4 (4-problem) vectors per thread
+// Per problem-chunk width P: KR scalar cells held per thread (P < 4),
+// KV float4 (4-problem) vectors per thread (P >= 4).
 template <int P> struct SweepShape;
-template <> struct SweepShape<1> { static constexpr int KR = 4, KV = 0; };
-template <> struct SweepShape<2> { static constexpr int KR = 6, KV = 0; };
-template <> struct SweepShape<4> { static constexpr int KR = 8, KV = 4; };
-template <> struct SweepShape<8> { static constexpr int KR = 16, KV = 6; };
+template <> struct SweepShape<1> { static constexpr int KR = 4, KV = 0, GU = 32; };
+template <> struct SweepShape<2> { static constexpr int KR = 6, KV = 0, GU = 256; };
+template <> struct SweepShape<4> { static constexpr int KR = 8, KV = 4, GU = 256; };
+template <> struct SweepShape<8> { static constexpr int KR = 16, KV = 6, GU = 256; };
+
+template <int G> struct SyncFor {
+    using type = GroupSync<G>;
+    __device__ static type make(int g) { return type{1 + g}; }
+};
+template <> struct SyncFor<32> {
+    using type = WarpSync;
+    __device__ static type make(int) { return WarpSync{}; }
+};
 
 __device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
     unsigned v;
     asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
     return v;
-}
-
-__device__ __forceinline__ void st_release(unsigned* p, unsigned v) {
-    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -57,65 +65,94 @@ __device__ __forceinline__ unsigned long long gtimer() {
     return t;
 }
 
-// trace arrays; the index-list area holds `run` lists (a dataflow task's run)
-__host__ __device__ inline size_t trace_words(int max_recs, int max_cells, int run) {
-    size_t w = size_t(max_recs) * 4 + 1 + GT / 32 + size_t(max_cells) * size_t(run);
-    return (w + 1) & ~size_t(1);
+__device__ __forceinline__ void red_release_add(unsigned* p, unsigned v) {
+    asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
-__host__ __device__ inline size_t group_words(int P, int max_recs, int max_cells, int run) {
-    // trace arrays + red (doubles) + fac (doubles) + meta (4 ints) + per-line cell counts
-    return trace_words(max_recs, max_cells, run) + 2 * size_t(GT / 32) * P + 2 * size_t(P) + 4 +
-           ((size_t(run) + 1) & ~size_t(1));
+__device__ __forceinline__ void spin_until_geq(const unsigned* p, unsigned target) {
+    unsigned ns = 16;
+    while (ld_acquire(p) < target) {
+        __nanosleep(ns);
+        ns = ns < 128 ? ns * 2 : 128;
+    }
+}
+
+// Shared-memory words of one group: [trace arrays when tracing] + `lists`
+// index lists + reduction scratch + meta + per-line cell counts.
+__host__ __device__ inline size_t group_words(int P, int G, bool with_trace, int max_recs,
+                                              int max_cells, int lists) {
+    size_t w = with_trace ? size_t(max_recs) * 4 + 1 + G / 32 : 0;
+    w += size_t(max_cells) * size_t(lists);
+    w = (w + 1) & ~size_t(1);
+    w += 2 * size_t(G / 32) * P + 2 * size_t(P) + 4 + ((size_t(lists) + 1) & ~size_t(1));
+    return w;
+}
+
+__host__ __device__ inline size_t ring_words(int n_rings) {
+    return (sizeof(RingRow) / 4) * size_t(n_rings + 1);
 }
 
 // One thread group's state and task code.
-template <int P>
+template <int P, int G>
 struct GroupWorker {
-    static constexpr int KR = SweepShape<P>::KR, NCL = GT / P;
+    static constexpr int KR = SweepShape<P>::KR, NCL = G / P;
+    using Sync = typename SyncFor<G>::type;
     const MartArgs& A;
     const RingRow* s_rings;
     TraceSmem tr;
-    double* red;   // [GT/32][P]
-    double* fac;   // [P]
-    int* meta;     // [0]: cells, [1]: unit, [2]: chunk, [3]: scratch (task id)
-    int* line_n;   // [run]: cells of each line of the task's run
-    uint32_t* idx0;  // first index list (tr.idx is pointed at line j's list)
-    GroupSync<GT> sy;
+    uint32_t* idx0;  // first index list (tr.idx is pointed at the current line's)
+    double* red;     // [G/32][P]
+    double* fac;     // [P]
+    int* meta;       // [0]: cells, [1]: unit, [2]: chunk, [3]: scratch (task id)
+    int* line_n;     // [lists]: cells of each staged line
+    Sync sy;
     int t;
-    // per-task prefetched scalars (valid in threads t < P)
+    // per-line prefetched scalars (valid in threads t < P)
     float m_next = 0.f;
     double pf_next = 0;
     bool act_next = false;
 
-    __device__ GroupWorker(const MartArgs& a, uint32_t* smem, int n_rings)
+    __device__ GroupWorker(const MartArgs& a, uint32_t* smem, int n_rings, bool with_trace,
+                           int lists)
         : A(a), s_rings(reinterpret_cast<const RingRow*>(smem)),
-          sy{1 + int(threadIdx.x) / GT}, t(int(threadIdx.x) % GT) {
-        const int g = int(threadIdx.x) / GT;
-        uint32_t* gbase = smem + (sizeof(RingRow) / 4) * (n_rings + 1) +
-                          size_t(g) * group_words(P, A.max_recs, A.max_cells, A.run);
-        tr.base = gbase;
-        tr.lohi = tr.base + A.max_recs;
-        tr.cnt = tr.lohi + A.max_recs;
-        tr.pos = tr.cnt + A.max_recs;
-        tr.warp = tr.pos + A.max_recs + 1;
-        tr.idx = tr.warp + GT / 32;
-        idx0 = tr.idx;
-        red = reinterpret_cast<double*>(gbase + trace_words(A.max_recs, A.max_cells, A.run));
-        fac = red + (GT / 32) * P;
+          sy(SyncFor<G>::make(int(threadIdx.x) / G)), t(int(threadIdx.x) % G) {
+        const int g = int(threadIdx.x) / G;
+        uint32_t* gbase = smem + ring_words(n_rings) +
+                          size_t(g) * group_words(P, G, with_trace, A.max_recs, A.max_cells, lists);
+        uint32_t* p = gbase;
+        if (with_trace) {
+            tr.base = p;
+            tr.lohi = tr.base + A.max_recs;
+            tr.cnt = tr.lohi + A.max_recs;
+            tr.pos = tr.cnt + A.max_recs;
+            tr.warp = tr.pos + A.max_recs + 1;
+            p = tr.warp + G / 32;
+        } else {
+            tr.base = tr.lohi = tr.cnt = tr.pos = tr.warp = nullptr;
+        }
+        tr.idx = p;
+        idx0 = p;
+        size_t w = size_t(p - gbase) + size_t(A.max_cells) * size_t(lists);
+        w = (w + 1) & ~size_t(1);
+        red = reinterpret_cast<double*>(gbase + w);
+        fac = red + (G / 32) * P;
         meta = reinterpret_cast<int*>(fac + P);
         line_n = meta + 4;
     }
 
-    // trace (unit, chunk) into the group's smem and prefetch its scalars
-    __device__ void prepare(uint32_t unit, int chunk) {
-        const int v = int(unit / uint32_t(A.tr.lines)), line = int(unit % uint32_t(A.tr.lines));
+    __device__ void load_scalars(uint32_t unit, int chunk) {
         if (t < P) {
             const size_t c2 = size_t(chunk) * P + t;
             m_next = __ldg(A.proj + size_t(unit) * A.Sp + c2);
             pf_next = __ldg(A.p_floor + c2);
             act_next = __ldg(A.active + c2) != 0;
         }
+    }
+
+    // trace (unit, chunk) into the group's smem and prefetch its scalars
+    __device__ void prepare(uint32_t unit, int chunk) {
+        const int v = int(unit / uint32_t(A.tr.lines)), line = int(unit % uint32_t(A.tr.lines));
+        load_scalars(unit, chunk);
         const int n = scope_trace(A.tr, __ldg(A.tr.off + line), __ldg(A.tr.off + line + 1),
                                   __ldg(A.tr.theta + v), tr, true, s_rings, sy);
         if (t == 0) {
@@ -126,7 +163,32 @@ struct GroupWorker {
         sy.sync();
     }
 
-    // gather -> reduce -> factor -> scatter for the prepared task
+    // mart_update_line (solver.cpp:36-46) for the problems of this thread
+    __device__ double line_factor(double p_bar, int chunk) {
+        double factor = 0;  // 0: no update
+        const double m = double(m_next);
+        if (m != 0 && act_next) {
+            const double ratio = m / (p_bar > pf_next ? p_bar : pf_next);
+            factor = 1.0 - A.beta * (1.0 - ratio);
+            if (factor <= 0) {
+                factor = pf_next;
+                atomicAdd(A.clamps + size_t(chunk) * P + t, 1ull);
+            }
+        }
+        return factor;
+    }
+
+    // The reference's clamp keeps the fp64 field strictly positive
+    // (solver.cpp:42-45); an fp32 product below FLT_MIN would underflow to 0,
+    // so it saturates at FLT_MIN instead.
+    __device__ static float scale_cell(float v, double f) {
+        if (f == 0)
+            return v;  // no update for this problem (skip / inactive)
+        const float r = float(double(v) * f);
+        return r >= FLT_MIN ? r : FLT_MIN;
+    }
+
+    // gather -> reduce -> factor -> scatter for the prepared line
     __device__ void update(unsigned long long* prof = nullptr) {
         if constexpr (P >= 4) {
             update_vec(prof);
@@ -164,46 +226,40 @@ struct GroupWorker {
 #pragma unroll
         for (int o = P; o < 32; o <<= 1)
             sum += __shfl_xor_sync(0xFFFFFFFFu, sum, o);
-        const int lane = t & 31, warp = t >> 5;
-        if (lane < P)
-            red[warp * P + lane] = sum;
-        sy.sync();
-        if (prof && t == 0)
-            prof[3] = gtimer();
-        if (t < P) {
-            double p_bar = 0;
+        double factor;
+        if constexpr (G == 32) {
+            // one warp: every lane holds its problem's total after the shuffles
+            if (prof && t == 0)
+                prof[3] = gtimer();
+            factor = __shfl_sync(0xFFFFFFFFu, t < P ? line_factor(sum, chunk) : 0.0, p);
+            if (prof && t == 0)
+                prof[4] = gtimer();
+        } else {
+            const int lane = t & 31, warp = t >> 5;
+            if (lane < P)
+                red[warp * P + lane] = sum;
+            sy.sync();
+            if (prof && t == 0)
+                prof[3] = gtimer();
+            if (t < P) {
+                double p_bar = 0;
 #pragma unroll
-            for (int w = 0; w < GT / 32; ++w)
-                p_bar += red[w * P + t];
-            double factor = 0;  // 0: no update
-            const double m = double(m_next);
-            if (m != 0 && act_next) {
-                // mart_update_line (solver.cpp:36-46)
-                const double ratio = m / (p_bar > pf_next ? p_bar : pf_next);
-                factor = 1.0 - A.beta * (1.0 - ratio);
-                if (factor <= 0) {
-                    factor = pf_next;
-                    atomicAdd(A.clamps + size_t(chunk) * P + t, 1ull);
-                }
+                for (int w = 0; w < G / 32; ++w)
+                    p_bar += red[w * P + t];
+                fac[t] = line_factor(p_bar, chunk);
             }
-            fac[t] = factor;
+            sy.sync();
+            if (prof && t == 0)
+                prof[4] = gtimer();
+            factor = fac[p];
         }
-        sy.sync();
-        if (prof && t == 0)
-            prof[4] = gtimer();
-        const double factor = fac[p];
         if (factor == 0)
             return;
-        // The reference's clamp keeps the fp64 field strictly positive
-        // (solver.cpp:42-45); an fp32 product below FLT_MIN would underflow
-        // to 0, so it saturates at FLT_MIN instead.
 #pragma unroll
         for (int i = 0; i < KR; ++i) {
             const int c = cl + i * NCL;
-            if (c < n) {
-                const float r = float(double(x[i]) * factor);
-                __stcg(f + (tr.idx[c] * Sp + col), r >= FLT_MIN ? r : FLT_MIN);
-            }
+            if (c < n)
+                __stcg(f + (tr.idx[c] * Sp + col), scale_cell(x[i], factor));
         }
         for (int c = cl + KR * NCL; c < n; c += 4 * NCL) {
             float y[4];
@@ -215,10 +271,8 @@ struct GroupWorker {
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
                 const int cc = c + j * NCL;
-                if (cc < n) {
-                    const float r = float(double(y[j]) * factor);
-                    __stcg(f + (tr.idx[cc] * Sp + col), r >= FLT_MIN ? r : FLT_MIN);
-                }
+                if (cc < n)
+                    __stcg(f + (tr.idx[cc] * Sp + col), scale_cell(y[j], factor));
             }
         }
     }
@@ -226,16 +280,9 @@ struct GroupWorker {
     // Vector form for P >= 4: a thread moves the 4 adjacent problems of one
     // cell as one float4 (16 B, aligned: S_pad and the chunk base are
     // multiples of 4), so a task needs a quarter of the load/store
-    // instructions and twice to four times the cell lanes of the scalar form.
-    __device__ static float scale_cell(float v, double f) {
-        if (f == 0)
-            return v;  // no update for this problem (skip / inactive)
-        const float r = float(double(v) * f);
-        return r >= FLT_MIN ? r : FLT_MIN;
-    }
-
+    // instructions and more cell lanes than the scalar form.
     __device__ void update_vec(unsigned long long* prof) {
-        constexpr int V = 4, TPC = P / V, NCLV = GT / TPC, KV = SweepShape<P>::KV;
+        constexpr int V = 4, TPC = P / V, NCLV = G / TPC, KV = SweepShape<P>::KV;
         const int n = meta[0];
         const int chunk = meta[2];
         const uint32_t Sp = uint32_t(A.Sp);
@@ -287,20 +334,9 @@ struct GroupWorker {
         if (t < P) {
             double p_bar = 0;
 #pragma unroll
-            for (int w = 0; w < GT / 32; ++w)
+            for (int w = 0; w < G / 32; ++w)
                 p_bar += red[w * P + t];
-            double factor = 0;  // 0: no update
-            const double m = double(m_next);
-            if (m != 0 && act_next) {
-                // mart_update_line (solver.cpp:36-46)
-                const double ratio = m / (p_bar > pf_next ? p_bar : pf_next);
-                factor = 1.0 - A.beta * (1.0 - ratio);
-                if (factor <= 0) {
-                    factor = pf_next;
-                    atomicAdd(A.clamps + size_t(chunk) * P + t, 1ull);
-                }
-            }
-            fac[t] = factor;
+            fac[t] = line_factor(p_bar, chunk);
         }
         sy.sync();
         if (prof && t == 0)
@@ -334,10 +370,25 @@ __device__ __forceinline__ void stage_rings(uint32_t* smem, const RingRow* rings
 }
 }  // namespace
 
+// level-barrier kernel: 4 groups of 256 threads, each tracing its own tasks
 size_t sweep_smem_bytes(const MartArgs& a, int n_rings) {
     const int P = a.Sp / a.nchunks;
-    const size_t rings = sizeof(RingRow) * size_t(n_rings + 1);
-    return rings + sizeof(uint32_t) * GROUPS * group_words(P, a.max_recs, a.max_cells, a.run);
+    return sizeof(uint32_t) *
+           (ring_words(n_rings) + (CTA / TG) * group_words(P, TG, true, a.max_recs, a.max_cells, 1));
+}
+
+// dataflow kernel: the larger of the tracer layout (4 x 256 threads with trace
+// arrays, one list) and the updater layout (`groups` groups, `run` lists);
+// the updater group count is the most that fit in `budget` bytes
+static size_t flow_smem_bytes(const MartArgs& a, int n_rings, int GU, size_t budget, int& groups) {
+    const int P = a.Sp / a.nchunks;
+    const size_t tracer = (CTA / TG) * group_words(P, TG, true, a.max_recs, a.max_cells, 1);
+    const size_t per = group_words(P, GU, GU == 32, a.max_recs, a.max_cells, a.run);
+    const size_t avail = budget / sizeof(uint32_t) - ring_words(n_rings);
+    groups = int(std::min<size_t>(CTA / GU, avail / per));
+    if (groups < 1 || tracer > avail)
+        throw CudaError("mart_flow_kernel: a run's index lists do not fit in shared memory");
+    return sizeof(uint32_t) * (ring_words(n_rings) + std::max(tracer, per * size_t(groups)));
 }
 
 // ============================================================================
@@ -361,20 +412,9 @@ struct FlowArgs {
     int n_rings;
     FlowSlab slab;             // traced index lists, one slot per line
     int tracer_ctas;
+    int upd_groups;            // updater groups per CTA (shared-memory bound)
     unsigned long long* prof;  // optional: per task phase stamps (ns)
 };
-
-__device__ __forceinline__ void red_release_add(unsigned* p, unsigned v) {
-    asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
-
-__device__ __forceinline__ void spin_until_geq(const unsigned* p, unsigned target) {
-    unsigned ns = 16;
-    while (ld_acquire(p) < target) {
-        __nanosleep(ns);
-        ns = ns < 128 ? ns * 2 : 128;
-    }
-}
 
 // line (unit) id of line j of run `run`
 __device__ __forceinline__ uint32_t run_line(const FlowArgs& a, uint32_t run, int j) {
@@ -387,7 +427,7 @@ __device__ __forceinline__ uint32_t run_line(const FlowArgs& a, uint32_t run, in
 // of Q slab slots. A slot is rewritten only after every chunk task of its
 // previous occupant has copied it.
 template <int P>
-__device__ void flow_tracer(const FlowArgs& a, GroupWorker<P>& W) {
+__device__ void flow_tracer(const FlowArgs& a, GroupWorker<P, TG>& W) {
     const int nchunks = a.m.nchunks;
     const int Q = a.slab.Q;
     int* s_i = W.meta + 3;
@@ -410,7 +450,7 @@ __device__ void flow_tracer(const FlowArgs& a, GroupWorker<P>& W) {
             spin_until_geq(a.slab.used + slot, gen * unsigned(nchunks));
         W.sy.sync();
         uint32_t* dst = a.slab.data + size_t(slot) * a.slab.slot_words;
-        for (int c = W.t; c < n; c += GT)
+        for (int c = W.t; c < n; c += TG)
             __stcg(dst + 1 + c, W.tr.idx[c]);
         if (W.t == 0)
             __stcg(dst, uint32_t(n));
@@ -421,17 +461,15 @@ __device__ void flow_tracer(const FlowArgs& a, GroupWorker<P>& W) {
     }
 }
 
-// Updater role: (run, chunk) tasks in topological order. Wait once for the
-// run's predecessors of this chunk, then update the run's lines in order
-// (the chain between them stays inside the group), then count in at the
-// run's successors.
-template <int P>
-__device__ void flow_updater(const FlowArgs& a, GroupWorker<P>& W) {
-    constexpr int kCopy = GT - 32;  // warps 0, 2..7 copy the slab; warp 1 waits / publishes
+// Updater role: (run, chunk) tasks in topological order. Stage the run's
+// index lists while its predecessors of this chunk finish, update the run's
+// lines in order (the chain between them stays inside the group), then count
+// in at the run's successors.
+template <int P, int G>
+__device__ void flow_updater(const FlowArgs& a, GroupWorker<P, G>& W) {
     const int nchunks = a.m.nchunks;
     const int Q = a.slab.Q;
     const int warp = W.t >> 5, lane = W.t & 31;
-    const GroupSync<kCopy> copy_sync{5 + int(threadIdx.x) / GT};
     int* s_task = W.meta + 3;
     if (W.t == 0)
         *s_task = int(atomicAdd(a.next, 1u));
@@ -455,54 +493,70 @@ __device__ void flow_updater(const FlowArgs& a, GroupWorker<P>& W) {
         if (W.t == 0)
             nxt = atomicAdd(a.next, 1u);
         const int seq0 = (sweep * a.n_runs + pos) * a.run;
-        if (warp == 1) {
-            if (lane == 0) {
-                // the run's predecessors of this chunk: sweep s (global,
-                // 1-based) needs s in-sweep and s-1 cross-sweep rounds
-                const unsigned s = a.epoch + unsigned(sweep);
-                const unsigned npred = __ldg(a.pred_off + run + 1) - __ldg(a.pred_off + run);
-                const unsigned target = s * npred + (s - 1) * __ldg(a.npred_x + run);
-                if (target)
-                    spin_until_geq(a.count + size_t(run) * nchunks + chunk, target);
-            }
-        } else {
+        // sweep s (global, 1-based) needs s in-sweep and s-1 cross-sweep
+        // rounds of the run's predecessors of this chunk counted in
+        const unsigned s = a.epoch + unsigned(sweep);
+        const unsigned npred = __ldg(a.pred_off + run + 1) - __ldg(a.pred_off + run);
+        const unsigned target = s * npred + (s - 1) * __ldg(a.npred_x + run);
+        unsigned* cnt = a.count + size_t(run) * nchunks + chunk;
+        auto stage_lists = [&](int ct, int nct) {
             // every line's index list of the run, from the slab into shared
-            // memory, while the predecessors finish (L2 reads: slots are rewritten)
-            if (W.t == 0)
-                for (int j = 0; j < a.run; ++j)
-                    spin_until_geq(a.slab.ready + (seq0 + j) % Q, unsigned((seq0 + j) / Q) + 1);
-            copy_sync.sync();
-            const int ct = W.t < 32 ? W.t : W.t - 32;
+            // memory (L2 reads: slots are rewritten)
             for (int j = 0; j < a.run; ++j) {
                 const uint32_t* src = a.slab.data + size_t((seq0 + j) % Q) * a.slab.slot_words;
                 const int n = int(__ldcg(src));
                 uint32_t* dst = W.idx0 + size_t(j) * a.m.max_cells;
-                for (int c = ct; c < n; c += kCopy)
+                for (int c = ct; c < n; c += nct)
                     dst[c] = __ldcg(src + 1 + c);
+                if (ct == 0)
+                    W.line_n[j] = n;
+            }
+        };
+        if constexpr (G == 32) {
+            // one problem: every line is updated once per sweep, so the warp
+            // traces its run's lines itself (no slab) while the predecessors
+            // finish, then lane 0 waits on them
+            (void)stage_lists;
+            for (int j = 0; j < a.run; ++j) {
+                const uint32_t unit = run_line(a, run, j);
+                const int v = int(unit / uint32_t(a.m.tr.lines));
+                const int line = int(unit % uint32_t(a.m.tr.lines));
+                W.tr.idx = W.idx0 + size_t(j) * a.m.max_cells;
+                const int n = scope_trace(a.m.tr, __ldg(a.m.tr.off + line), __ldg(a.m.tr.off + line + 1),
+                                          __ldg(a.m.tr.theta + v), W.tr, true, W.s_rings, W.sy);
                 if (W.t == 0)
                     W.line_n[j] = n;
             }
-            if (W.t == 0) {
-                W.meta[1] = int(run);
-                W.meta[2] = chunk;
+            if (W.t == 0 && target)
+                spin_until_geq(cnt, target);
+            W.sy.sync();
+        } else {
+            // warp 1 waits on the predecessors while warps 0, 2..7 stage
+            constexpr int kCopy = G - 32;
+            const GroupSync<kCopy> copy_sync{5 + int(threadIdx.x) / G};
+            if (warp == 1) {
+                if (lane == 0 && target)
+                    spin_until_geq(cnt, target);
+            } else {
+                if (W.t == 0)
+                    for (int j = 0; j < a.run; ++j)
+                        spin_until_geq(a.slab.ready + (seq0 + j) % Q, unsigned((seq0 + j) / Q) + 1);
+                copy_sync.sync();
+                stage_lists(W.t < 32 ? W.t : W.t - 32, kCopy);
             }
+            // index lists staged and the predecessors counted in (the acquire
+            // orders the gathers after their released stores)
+            W.sy.sync();
         }
-        // index lists copied and the predecessors counted in (their acquire
-        // orders the gathers after the released stores); later lines of the
-        // run follow the group's own stores (bar.sync between lines)
-        W.sy.sync();
-        if (W.t < a.run)
+        if (G != 32 && W.t < a.run)
             red_release_add(a.slab.used + (seq0 + W.t) % Q, 1u);
+        if (W.t == 0)
+            W.meta[2] = chunk;
         if (prof && W.t == 0)
             prof[1] = prof[2] = gtimer();
         for (int j = 0; j < a.run; ++j) {
-            if (W.t < P) {
-                const uint32_t unit = run_line(a, run, j);
-                const size_t c2 = size_t(chunk) * P + W.t;
-                W.m_next = __ldg(a.m.proj + size_t(unit) * a.m.Sp + c2);
-                W.pf_next = __ldg(a.m.p_floor + c2);
-                W.act_next = __ldg(a.m.active + c2) != 0;
-            }
+            // later lines of the run follow the group's own stores (sync below)
+            W.load_scalars(run_line(a, run, j), chunk);
             W.tr.idx = W.idx0 + size_t(j) * a.m.max_cells;
             if (W.t == 0)
                 W.meta[0] = W.line_n[j];
@@ -514,14 +568,17 @@ __device__ void flow_updater(const FlowArgs& a, GroupWorker<P>& W) {
         if (prof && W.t == 0)
             prof[5] = gtimer();
         // count in at the run's successors right away (the chain waits on it):
-        // warp 1 issues one gpu-scope release reduction per successor
-        // (cumulative over the group's stores through the bar.sync above)
-        if (warp == 1) {
-            const uint32_t sb = __ldg(a.succ_off + run), se = __ldg(a.succ_off + run + 1);
-            for (uint32_t k = sb + lane; k < se; k += 32)
-                red_release_add(a.count + size_t(__ldg(a.succs + k)) * nchunks + chunk, 1u);
-            if (prof && lane == 0)
-                prof[6] = gtimer();
+        // one gpu-scope release reduction per successor (cumulative over the
+        // group's stores through the sync above)
+        {
+            constexpr int kPub = G == 32 ? 0 : 1;  // publishing warp
+            if (warp == kPub) {
+                const uint32_t sb = __ldg(a.succ_off + run), se = __ldg(a.succ_off + run + 1);
+                for (uint32_t k = sb + lane; k < se; k += 32)
+                    red_release_add(a.count + size_t(__ldg(a.succs + k)) * nchunks + chunk, 1u);
+                if (prof && lane == 0)
+                    prof[6] = gtimer();
+            }
         }
         if (W.t == 0)
             *s_task = int(nxt);
@@ -535,15 +592,26 @@ __global__ void __launch_bounds__(CTA, 1) mart_flow_kernel(FlowArgs a) {
     extern __shared__ __align__(16) uint32_t smem[];
     stage_rings(smem, a.m.tr.rings, a.n_rings);
     __syncthreads();
-    GroupWorker<P> W(a.m, smem, a.n_rings);
-    if (int(blockIdx.x) < a.tracer_ctas)
+    if (int(blockIdx.x) < a.tracer_ctas) {
+        GroupWorker<P, TG> W(a.m, smem, a.n_rings, true, 1);
         flow_tracer<P>(a, W);
-    else
-        flow_updater<P>(a, W);
+    } else {
+        constexpr int GU = SweepShape<P>::GU;
+        if (int(threadIdx.x) / GU >= a.upd_groups)
+            return;  // no shared memory left for this group
+        // single-warp updaters trace their own lines (trace arrays needed)
+        GroupWorker<P, GU> W(a.m, smem, a.n_rings, GU == 32, a.run);
+        flow_updater<P, GU>(a, W);
+    }
 }
 
 template <int P>
-static void flow_launch_t(FlowArgs& a, size_t smem, int sms, cudaStream_t st) {
+static void flow_launch_t(FlowArgs& a, int sms, cudaStream_t st) {
+    constexpr int GU = SweepShape<P>::GU;
+    int dev = 0, optin = 0;
+    UB_CUDA(cudaGetDevice(&dev));
+    UB_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+    const size_t smem = flow_smem_bytes(a.m, a.n_rings, GU, size_t(optin) - 1024, a.upd_groups);
     UB_CUDA(cudaFuncSetAttribute(mart_flow_kernel<P>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  int(smem)));
     int per_sm = 0;
@@ -551,13 +619,16 @@ static void flow_launch_t(FlowArgs& a, size_t smem, int sms, cudaStream_t st) {
     if (per_sm < 1)
         throw CudaError("mart_flow_kernel cannot be resident (shared memory too large)");
     const int grid = sms * per_sm;
-    // tracer CTAs: trace work ~ units, update work ~ units * chunks
+    // tracer CTAs: trace work ~ lines, update work ~ lines * chunks (and more
+    // for single-warp updaters, which finish a line faster than a trace)
     int k = 0;
-    if (const char* e = std::getenv("USCG_TRACER_CTAS"))
-        k = std::atoi(e);
+    if (GU == 32)
+        k = 0;  // single-warp updaters trace their own lines
+    else if (const char* e = std::getenv("USCG_TRACER_CTAS"))
+        k = std::max(1, std::atoi(e));
     else
-        k = int(double(grid) * 2.7 / (2.7 + 4.0 * a.m.nchunks) + 0.5);
-    a.tracer_ctas = std::max(1, std::min(k, grid - 1));
+        k = std::max(1, int(double(grid) * 2.7 / (2.7 + 4.0 * a.m.nchunks) + 0.5));
+    a.tracer_ctas = std::min(k, grid - 1);
     // every CTA must be resident: tracers and updaters wait on each other
     mart_flow_kernel<P><<<grid, CTA, smem, st>>>(a);
 }
@@ -592,12 +663,11 @@ void launch_mart_flow(const MartArgs& h, const FlowSchedule& fs, unsigned* count
     UB_CUDA(cudaMemsetAsync(slab.tnext, 0, sizeof(unsigned), st));
     UB_CUDA(cudaMemsetAsync(slab.ready, 0, sizeof(unsigned) * slab.Q, st));
     UB_CUDA(cudaMemsetAsync(slab.used, 0, sizeof(unsigned) * slab.Q, st));
-    const size_t smem = sweep_smem_bytes(h, n_rings);
     switch (h.Sp / h.nchunks) {
-        case 1: flow_launch_t<1>(a, smem, sms, st); break;
-        case 2: flow_launch_t<2>(a, smem, sms, st); break;
-        case 4: flow_launch_t<4>(a, smem, sms, st); break;
-        case 8: flow_launch_t<8>(a, smem, sms, st); break;
+        case 1: flow_launch_t<1>(a, sms, st); break;
+        case 2: flow_launch_t<2>(a, sms, st); break;
+        case 4: flow_launch_t<4>(a, sms, st); break;
+        case 8: flow_launch_t<8>(a, sms, st); break;
         default: throw CudaError("mart_flow_kernel supports problem chunks of at most 8");
     }
     count_launch();
@@ -625,10 +695,10 @@ __global__ void __launch_bounds__(CTA, 1) mart_sweep_kernel(SweepArgs a) {
     extern __shared__ __align__(16) uint32_t smem[];
     stage_rings(smem, a.m.tr.rings, a.n_rings);
     __syncthreads();
-    GroupWorker<P> W(a.m, smem, a.n_rings);
+    GroupWorker<P, TG> W(a.m, smem, a.n_rings, true, 1);
     const int nchunks = a.m.nchunks;
-    const int NG = gridDim.x * GROUPS;
-    const int gid = blockIdx.x * GROUPS + int(threadIdx.x) / GT;
+    const int NG = gridDim.x * (CTA / TG);
+    const int gid = blockIdx.x * (CTA / TG) + int(threadIdx.x) / TG;
     auto ntasks = [&](int lev) {
         return int(__ldg(a.level_off + lev + 1) - __ldg(a.level_off + lev)) * nchunks;
     };

@@ -985,7 +985,10 @@ uscg_status uscg_reconstruct(uscg_tracer t, const float* proj, int32_t problems,
         h.run = t->run;
         t->d_args.ensure(1);
         UB_CUDA(cudaMemcpyAsync(t->d_args.p, &h, sizeof(MartArgs), cudaMemcpyHostToDevice, st));
-        const int exec_mode = P <= 8 ? mart_mode() : 2;
+        // dataflow: chunks up to 32 problems; level barrier: up to 8
+        int exec_mode = mart_mode();
+        if (exec_mode == 1 && P > 8)
+            exec_mode = 2;
         need(exec_mode != 2 || t->run == 1, "the level executor needs a line-granular schedule");
         if (exec_mode == 2)
             ensure_graph(t, h);
@@ -1023,12 +1026,16 @@ uscg_status uscg_reconstruct(uscg_tracer t, const float* proj, int32_t problems,
                 const size_t nt = size_t(t->n_runs) * h.nchunks * n_run;
                 DevBuf<unsigned long long> prof;
                 if (prof_path)
-                    prof.alloc(nt * 8);
+                    prof.alloc(nt * 16);
                 if (prof_path)
-                    UB_CUDA(cudaMemsetAsync(prof.p, 0, sizeof(unsigned long long) * nt * 8, st));
+                    UB_CUDA(cudaMemsetAsync(prof.p, 0, sizeof(unsigned long long) * nt * 16, st));
                 FlowSlab slab;
-                slab.Q = int(std::min<uint64_t>(units, 8192));
-                slab.slot_words = (t->max_cells + 1 + 31) & ~31;
+                {
+                    const char* e = std::getenv("USCG_SLAB_Q");
+                    slab.Q = int(std::min<uint64_t>(units, e ? std::max(64, std::atoi(e)) : 8192));
+                }
+                // [n][indices][u16 next positions] (mart_sweep.cu, flow_tracer_runs)
+                slab.slot_words = (1 + t->max_cells + (t->max_cells + 1) / 2 + 31) & ~31;
                 t->w_slab.ensure(size_t(slab.Q) * slab.slot_words);
                 t->w_slab_ctl.ensure(size_t(slab.Q) * 2 + 1);
                 slab.data = t->w_slab.p;
@@ -1048,7 +1055,7 @@ uscg_status uscg_reconstruct(uscg_tracer t, const float* proj, int32_t problems,
                                  slab, st, prof.p);
                 t->epoch += unsigned(n_run);
                 if (prof_path) {
-                    std::vector<unsigned long long> hp(nt * 8);
+                    std::vector<unsigned long long> hp(nt * 16);
                     UB_CUDA(cudaMemcpyAsync(hp.data(), prof.p, sizeof(unsigned long long) * hp.size(),
                                             cudaMemcpyDeviceToHost, st));
                     UB_CUDA(cudaStreamSynchronize(st));

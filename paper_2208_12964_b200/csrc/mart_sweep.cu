@@ -26,6 +26,7 @@
 #include <algorithm>
 #include <cfloat>
 #include <cstdint>
+#include <cstdio>
 #include <cstdlib>
 
 #include "kernels.h"
@@ -37,12 +38,18 @@ constexpr int CTA = 1024;   // threads per CTA (one CTA per SM)
 constexpr int TG = 256;     // tracer group / level-barrier group size
 
 // Per problem-chunk width P: KR scalar cells held per thread (P < 4),
-// KV float4 (4-problem) vectors per thread (P >= 4).
+// KV float4 (4-problem) vectors per thread (P >= 4), GU threads per dataflow
+// updater group. Wide chunks move a cell's problems as one 64 / 128-byte
+// segment per L1 wavefront (the per-SM L1 request pipe is the shared resource
+// of the scattered gathers); their groups grow so that a thread still holds
+// KV = 6 cells of a line (768 cells per group).
 template <int P> struct SweepShape;
 template <> struct SweepShape<1> { static constexpr int KR = 4, KV = 0, GU = 32; };
 template <> struct SweepShape<2> { static constexpr int KR = 6, KV = 0, GU = 256; };
 template <> struct SweepShape<4> { static constexpr int KR = 8, KV = 4, GU = 256; };
 template <> struct SweepShape<8> { static constexpr int KR = 16, KV = 6, GU = 256; };
+template <> struct SweepShape<16> { static constexpr int KR = 16, KV = 6, GU = 512; };
+template <> struct SweepShape<32> { static constexpr int KR = 16, KV = 6, GU = 1024; };
 
 template <int G> struct SyncFor {
     using type = GroupSync<G>;
@@ -69,6 +76,37 @@ __device__ __forceinline__ void red_release_add(unsigned* p, unsigned v) {
     asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
+// 16-byte global -> shared copy through L2 (LDGSTS), completed by
+// cp_async_wait_all of the issuing thread
+__device__ __forceinline__ void cp_async16(void* smem_dst, const void* gmem_src) {
+    const unsigned d = unsigned(__cvta_generic_to_shared(smem_dst));
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(gmem_src) : "memory");
+}
+// predicated forms (no divergent branch around the asm)
+__device__ __forceinline__ void cp_async16_if(bool p, void* smem_dst, const void* gmem_src) {
+    const unsigned d = unsigned(__cvta_generic_to_shared(smem_dst));
+    asm volatile(
+        "{ .reg .pred q; setp.ne.b32 q, %2, 0; @q cp.async.cg.shared.global [%0], [%1], 16; }" ::"r"(d),
+        "l"(gmem_src), "r"(int(p))
+        : "memory");
+}
+__device__ __forceinline__ void st_shared_v4_if(bool p, void* smem_dst, float4 v) {
+    const unsigned d = unsigned(__cvta_generic_to_shared(smem_dst));
+    asm volatile(
+        "{ .reg .pred q; setp.ne.b32 q, %1, 0; @q st.shared.v4.f32 [%0], {%2, %3, %4, %5}; }" ::"r"(d),
+        "r"(int(p)), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w)
+        : "memory");
+}
+__device__ __forceinline__ void st_global_cg_v4_if(bool p, void* gmem_dst, float4 v) {
+    asm volatile(
+        "{ .reg .pred q; setp.ne.b32 q, %1, 0; @q st.global.cg.v4.f32 [%0], {%2, %3, %4, %5}; }" ::"l"(
+            gmem_dst),
+        "r"(int(p)), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w)
+        : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
 __device__ __forceinline__ void spin_until_geq(const unsigned* p, unsigned target) {
     unsigned ns = 16;
     while (ld_acquire(p) < target) {
@@ -83,13 +121,42 @@ __host__ __device__ inline size_t group_words(int P, int G, bool with_trace, int
                                               int max_cells, int lists) {
     size_t w = with_trace ? size_t(max_recs) * 4 + 1 + G / 32 : 0;
     w += size_t(max_cells) * size_t(lists);
-    w = (w + 1) & ~size_t(1);
+    w = (w + 3) & ~size_t(3);  // reduction scratch 16-byte aligned
     w += 2 * size_t(G / 32) * P + 2 * size_t(P) + 4 + ((size_t(lists) + 1) & ~size_t(1));
     return w;
 }
 
+__host__ __device__ inline size_t round4(size_t w) { return (w + 3) & ~size_t(3); }
+
 __host__ __device__ inline size_t ring_words(int n_rings) {
-    return (sizeof(RingRow) / 4) * size_t(n_rings + 1);
+    return round4((sizeof(RingRow) / 4) * size_t(n_rings + 1));
+}
+
+// Pipelined runs (see pipe_run): a slab entry of line j+1 of a run carries
+// kPrevMark when its cell is also crossed by line j, and line j carries, per
+// position, the position of its cell in line j+1 (kNoNext: none).
+constexpr uint32_t kPrevMark = 0x80000000u;
+constexpr uint16_t kNoNext = 0xFFFFu;
+
+__host__ __device__ inline int hash_size(int max_cells) {
+    int h = 64;
+    while (h < 2 * max_cells)
+        h <<= 1;
+    return h;
+}
+__host__ __device__ inline size_t npos_words(int run, int max_cells) {
+    return round4((size_t(run) * size_t(max_cells) + 1) / 2);
+}
+// words beyond group_words: tracer = next positions + cell hash (keys, u16
+// positions); updater = next positions + the prefetch buffer [max_cells][P]
+__host__ __device__ inline size_t tracer_extra(int run, int max_cells) {
+    const int H = hash_size(max_cells);
+    return npos_words(run, max_cells) + size_t(H) + round4(size_t(H) / 2);
+}
+__host__ __device__ inline size_t updater_extra(int P, int run, int max_cells) {
+    // + the run's line scalars: m [run][P] f32, p_floor [P] f64, active [P] u32
+    return npos_words(run, max_cells) + size_t(max_cells) * size_t(P) +
+           round4(size_t(run) * P + 3 * size_t(P));
 }
 
 // One thread group's state and task code.
@@ -105,6 +172,7 @@ struct GroupWorker {
     double* fac;     // [P]
     int* meta;       // [0]: cells, [1]: unit, [2]: chunk, [3]: scratch (task id)
     int* line_n;     // [lists]: cells of each staged line
+    uint32_t* ext;   // `extra` words after the standard layout (16-byte aligned)
     Sync sy;
     int t;
     // per-line prefetched scalars (valid in threads t < P)
@@ -113,12 +181,13 @@ struct GroupWorker {
     bool act_next = false;
 
     __device__ GroupWorker(const MartArgs& a, uint32_t* smem, int n_rings, bool with_trace,
-                           int lists)
+                           int lists, size_t extra = 0)
         : A(a), s_rings(reinterpret_cast<const RingRow*>(smem)),
           sy(SyncFor<G>::make(int(threadIdx.x) / G)), t(int(threadIdx.x) % G) {
         const int g = int(threadIdx.x) / G;
-        uint32_t* gbase = smem + ring_words(n_rings) +
-                          size_t(g) * group_words(P, G, with_trace, A.max_recs, A.max_cells, lists);
+        const size_t std_words = round4(group_words(P, G, with_trace, A.max_recs, A.max_cells, lists));
+        uint32_t* gbase = smem + ring_words(n_rings) + size_t(g) * (std_words + extra);
+        ext = gbase + std_words;
         uint32_t* p = gbase;
         if (with_trace) {
             tr.base = p;
@@ -133,7 +202,7 @@ struct GroupWorker {
         tr.idx = p;
         idx0 = p;
         size_t w = size_t(p - gbase) + size_t(A.max_cells) * size_t(lists);
-        w = (w + 1) & ~size_t(1);
+        w = (w + 3) & ~size_t(3);
         red = reinterpret_cast<double*>(gbase + w);
         fac = red + (G / 32) * P;
         meta = reinterpret_cast<int*>(fac + P);
@@ -143,7 +212,7 @@ struct GroupWorker {
     __device__ void load_scalars(uint32_t unit, int chunk) {
         if (t < P) {
             const size_t c2 = size_t(chunk) * P + t;
-            m_next = __ldg(A.proj + size_t(unit) * A.Sp + c2);
+            m_next = __ldcs(A.proj + size_t(unit) * A.Sp + c2);  // read once per sweep
             pf_next = __ldg(A.p_floor + c2);
             act_next = __ldg(A.active + c2) != 0;
         }
@@ -178,14 +247,22 @@ struct GroupWorker {
         return factor;
     }
 
-    // The reference's clamp keeps the fp64 field strictly positive
-    // (solver.cpp:42-45); an fp32 product below FLT_MIN would underflow to 0,
-    // so it saturates at FLT_MIN instead.
-    __device__ static float scale_cell(float v, double f) {
-        if (f == 0)
-            return v;  // no update for this problem (skip / inactive)
-        const float r = float(double(v) * f);
-        return r >= FLT_MIN ? r : FLT_MIN;
+    // A line's update of one problem as an fp32 multiplier and lower bound:
+    // factor 0 (skip / inactive) is {1, 0}, the identity on the positive
+    // field. The factor is computed in fp64 (solver.cpp:36-46) and rounded
+    // once; the reference's clamp keeps the fp64 field strictly positive
+    // (solver.cpp:42-45), and an fp32 product below FLT_MIN would underflow
+    // to 0, so it saturates at FLT_MIN instead.
+    struct Scale {
+        float g, lb;
+    };
+    __device__ static Scale scale_of(double f) {
+        return f == 0 ? Scale{1.f, 0.f} : Scale{float(f), FLT_MIN};
+    }
+    __device__ static float scale_cell(float v, Scale s) { return fmaxf(v * s.g, s.lb); }
+    __device__ static float4 scale4(float4 v, Scale a, Scale b, Scale c, Scale d) {
+        return make_float4(scale_cell(v.x, a), scale_cell(v.y, b), scale_cell(v.z, c),
+                           scale_cell(v.w, d));
     }
 
     // gather -> reduce -> factor -> scatter for the prepared line
@@ -255,11 +332,12 @@ struct GroupWorker {
         }
         if (factor == 0)
             return;
+        const Scale sc = scale_of(factor);
 #pragma unroll
         for (int i = 0; i < KR; ++i) {
             const int c = cl + i * NCL;
             if (c < n)
-                __stcg(f + (tr.idx[c] * Sp + col), scale_cell(x[i], factor));
+                __stcg(f + (tr.idx[c] * Sp + col), scale_cell(x[i], sc));
         }
         for (int c = cl + KR * NCL; c < n; c += 4 * NCL) {
             float y[4];
@@ -272,9 +350,30 @@ struct GroupWorker {
             for (int j = 0; j < 4; ++j) {
                 const int cc = c + j * NCL;
                 if (cc < n)
-                    __stcg(f + (tr.idx[cc] * Sp + col), scale_cell(y[j], factor));
+                    __stcg(f + (tr.idx[cc] * Sp + col), scale_cell(y[j], sc));
             }
         }
+    }
+
+    // A thread's share of p_bar for its 4 problems: the (at most KV) cells it
+    // holds are summed in fp32, then the partials join the fp64 cross-lane and
+    // cross-warp sums (the reference sums in fp64, solver.cpp:36-40). KV-term
+    // fp32 partials bound the relative error of p_bar by (KV-1) * 2^-24, the
+    // size of the fp32 field's own rounding per update.
+    template <int K>
+    __device__ static void partials(const float4* x, double& s0, double& s1, double& s2, double& s3) {
+        float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
+#pragma unroll
+        for (int i = 0; i < K; ++i) {
+            a0 += x[i].x;
+            a1 += x[i].y;
+            a2 += x[i].z;
+            a3 += x[i].w;
+        }
+        s0 = a0;
+        s1 = a1;
+        s2 = a2;
+        s3 = a3;
     }
 
     // Vector form for P >= 4: a thread moves the 4 adjacent problems of one
@@ -295,14 +394,8 @@ struct GroupWorker {
             const int c = cl + i * NCLV;
             x[i] = c < n ? __ldcg(f4 + ((tr.idx[c] * Sp + col) >> 2)) : make_float4(0.f, 0.f, 0.f, 0.f);
         }
-        double s0 = 0, s1 = 0, s2 = 0, s3 = 0;
-#pragma unroll
-        for (int i = 0; i < KV; ++i) {
-            s0 += double(x[i].x);
-            s1 += double(x[i].y);
-            s2 += double(x[i].z);
-            s3 += double(x[i].w);
-        }
+        double s0, s1, s2, s3;
+        partials<KV>(x, s0, s1, s2, s3);
         for (int c = cl + KV * NCLV; c < n; c += 2 * NCLV) {
             const int c2 = c + NCLV;
             const float4 y0 = __ldcg(f4 + ((tr.idx[c] * Sp + col) >> 2));
@@ -331,35 +424,46 @@ struct GroupWorker {
         sy.sync();
         if (prof && t == 0)
             prof[3] = gtimer();
+        factors_to_smem(chunk);
+        sy.sync();
+        if (prof && t == 0)
+            prof[4] = gtimer();
+        Scale g0, g1, g2, g3;
+        if (!load_scales(q, g0, g1, g2, g3))
+            return;
+#pragma unroll
+        for (int i = 0; i < KV; ++i) {
+            const int c = cl + i * NCLV;
+            if (c < n)
+                __stcg(f4 + ((tr.idx[c] * Sp + col) >> 2), scale4(x[i], g0, g1, g2, g3));
+        }
+        for (int c = cl + KV * NCLV; c < n; c += NCLV) {
+            float4* p4 = f4 + ((tr.idx[c] * Sp + col) >> 2);
+            __stcg(p4, scale4(__ldcg(p4), g0, g1, g2, g3));
+        }
+    }
+
+    // threads t < P: the line's factor of problem t from the warp partials
+    // (fp64, solver.cpp:36-46) as its fp32 Scale in the fac slot
+    __device__ void factors_to_smem(int chunk) {
         if (t < P) {
             double p_bar = 0;
 #pragma unroll
             for (int w = 0; w < G / 32; ++w)
                 p_bar += red[w * P + t];
-            fac[t] = line_factor(p_bar, chunk);
+            const Scale s = scale_of(line_factor(p_bar, chunk));
+            reinterpret_cast<float2*>(fac)[t] = make_float2(s.g, s.lb);
         }
-        sy.sync();
-        if (prof && t == 0)
-            prof[4] = gtimer();
-        const double g0 = fac[q * V + 0], g1 = fac[q * V + 1], g2 = fac[q * V + 2],
-                     g3 = fac[q * V + 3];
-        if (g0 == 0 && g1 == 0 && g2 == 0 && g3 == 0)
-            return;
-#pragma unroll
-        for (int i = 0; i < KV; ++i) {
-            const int c = cl + i * NCLV;
-            if (c < n) {
-                const float4 r = make_float4(scale_cell(x[i].x, g0), scale_cell(x[i].y, g1),
-                                             scale_cell(x[i].z, g2), scale_cell(x[i].w, g3));
-                __stcg(f4 + ((tr.idx[c] * Sp + col) >> 2), r);
-            }
-        }
-        for (int c = cl + KV * NCLV; c < n; c += NCLV) {
-            float4* p4 = f4 + ((tr.idx[c] * Sp + col) >> 2);
-            const float4 y = __ldcg(p4);
-            __stcg(p4, make_float4(scale_cell(y.x, g0), scale_cell(y.y, g1), scale_cell(y.z, g2),
-                                   scale_cell(y.w, g3)));
-        }
+    }
+    // the Scales of problems 4q..4q+3; false when none of them is updated
+    __device__ bool load_scales(int q, Scale& a, Scale& b, Scale& c, Scale& d) const {
+        const float4 u = reinterpret_cast<const float4*>(fac)[2 * q];
+        const float4 w = reinterpret_cast<const float4*>(fac)[2 * q + 1];
+        a = Scale{u.x, u.y};
+        b = Scale{u.z, u.w};
+        c = Scale{w.x, w.y};
+        d = Scale{w.z, w.w};
+        return (u.y + u.w + w.y + w.w) != 0.f;  // lb = FLT_MIN marks an update
     }
 };
 
@@ -374,21 +478,37 @@ __device__ __forceinline__ void stage_rings(uint32_t* smem, const RingRow* rings
 size_t sweep_smem_bytes(const MartArgs& a, int n_rings) {
     const int P = a.Sp / a.nchunks;
     return sizeof(uint32_t) *
-           (ring_words(n_rings) + (CTA / TG) * group_words(P, TG, true, a.max_recs, a.max_cells, 1));
+           (ring_words(n_rings) +
+            (CTA / TG) * round4(group_words(P, TG, true, a.max_recs, a.max_cells, 1)));
 }
 
-// dataflow kernel: the larger of the tracer layout (4 x 256 threads with trace
-// arrays, one list) and the updater layout (`groups` groups, `run` lists);
-// the updater group count is the most that fit in `budget` bytes
-static size_t flow_smem_bytes(const MartArgs& a, int n_rings, int GU, size_t budget, int& groups) {
+// dataflow kernel: the larger of the tracer layout (`tgroups` x 256 threads
+// with trace arrays; pipelined: a run's lists, next positions and the cell
+// hash) and the updater layout (`groups` groups, `run` lists; pipelined: next
+// positions and the prefetch buffer). Group counts are the most that fit in
+// `budget` bytes.
+struct FlowLayout {
+    size_t tracer_words, updater_words;  // per group
+    int tgroups, groups;
+    size_t bytes;
+};
+
+static FlowLayout flow_layout(const MartArgs& a, int n_rings, int GU, bool pipe, size_t budget) {
     const int P = a.Sp / a.nchunks;
-    const size_t tracer = (CTA / TG) * group_words(P, TG, true, a.max_recs, a.max_cells, 1);
-    const size_t per = group_words(P, GU, GU == 32, a.max_recs, a.max_cells, a.run);
+    FlowLayout L;
+    L.tracer_words = round4(group_words(P, TG, true, a.max_recs, a.max_cells, pipe ? a.run : 1)) +
+                     (pipe ? tracer_extra(a.run, a.max_cells) : 0);
+    L.updater_words = round4(group_words(P, GU, GU == 32, a.max_recs, a.max_cells, a.run)) +
+                      (pipe ? updater_extra(P, a.run, a.max_cells) : 0);
     const size_t avail = budget / sizeof(uint32_t) - ring_words(n_rings);
-    groups = int(std::min<size_t>(CTA / GU, avail / per));
-    if (groups < 1 || tracer > avail)
+    L.groups = int(std::min<size_t>(CTA / GU, avail / L.updater_words));
+    L.tgroups = int(std::min<size_t>(CTA / TG, avail / L.tracer_words));
+    if (L.groups < 1 || L.tgroups < 1)
         throw CudaError("mart_flow_kernel: a run's index lists do not fit in shared memory");
-    return sizeof(uint32_t) * (ring_words(n_rings) + std::max(tracer, per * size_t(groups)));
+    L.bytes = sizeof(uint32_t) *
+              (ring_words(n_rings) + std::max(L.tracer_words * size_t(L.tgroups),
+                                              L.updater_words * size_t(L.groups)));
+    return L;
 }
 
 // ============================================================================
@@ -413,6 +533,8 @@ struct FlowArgs {
     FlowSlab slab;             // traced index lists, one slot per line
     int tracer_ctas;
     int upd_groups;            // updater groups per CTA (shared-memory bound)
+    int tr_groups;             // tracer groups per tracer CTA
+    int pipe;                  // pipelined runs (run tracer marks, pipe_run updaters)
     unsigned long long* prof;  // optional: per task phase stamps (ns)
 };
 
@@ -461,6 +583,230 @@ __device__ void flow_tracer(const FlowArgs& a, GroupWorker<P, TG>& W) {
     }
 }
 
+// Open-addressing cell -> position hash of one line (shared memory, H a power
+// of two >= 2 x the longest line; cells of a line are distinct).
+__device__ __forceinline__ uint32_t cell_hash(uint32_t cell, int H) {
+    return (cell * 2654435761u) >> (32 - __ffs(H) + 1);
+}
+__device__ __forceinline__ void hash_insert(uint32_t* key, uint16_t* val, int H, uint32_t cell,
+                                            uint16_t pos) {
+    uint32_t h = cell_hash(cell, H);
+    while (atomicCAS(key + h, 0xFFFFFFFFu, cell) != 0xFFFFFFFFu)
+        h = (h + 1) & uint32_t(H - 1);
+    val[h] = pos;
+}
+__device__ __forceinline__ int hash_find(const uint32_t* key, const uint16_t* val, int H,
+                                         uint32_t cell) {
+    uint32_t h = cell_hash(cell, H);
+    while (true) {
+        const uint32_t k = key[h];
+        if (k == cell)
+            return val[h];
+        if (k == 0xFFFFFFFFu)
+            return -1;
+        h = (h + 1) & uint32_t(H - 1);
+    }
+}
+
+// Tracer role for pipelined runs: a group traces a whole run, links its lines
+// (line j+1 entries shared with line j get kPrevMark; line j records where
+// each of its cells sits in line j+1), then writes the run's slab slots.
+// Slot = [n][idx: max_cells][next positions: u16 x max_cells].
+template <int P>
+__device__ void flow_tracer_runs(const FlowArgs& a, GroupWorker<P, TG>& W) {
+    const int nchunks = a.m.nchunks;
+    const int Q = a.slab.Q;
+    const int R = a.run, mc = a.m.max_cells;
+    const int H = hash_size(mc);
+    uint16_t* npos = reinterpret_cast<uint16_t*>(W.ext);
+    uint32_t* hkey = W.ext + npos_words(R, mc);
+    uint16_t* hval = reinterpret_cast<uint16_t*>(hkey + H);
+    int* s_i = W.meta + 3;
+    for (int c = W.t; c < H; c += TG)
+        hkey[c] = 0xFFFFFFFFu;
+    const int total = a.n_runs * a.n_sweeps;
+    while (true) {
+        if (W.t == 0)
+            *s_i = int(atomicAdd(a.slab.tnext, 1u));
+        W.sy.sync();
+        const int rs = *s_i;  // sweep * n_runs + order position
+        if (rs >= total)
+            break;
+        const uint32_t run = __ldg(a.order + rs % a.n_runs);
+        for (int j = 0; j < R; ++j) {
+            const uint32_t unit = run_line(a, run, j);
+            const int v = int(unit / uint32_t(a.m.tr.lines)), line = int(unit % uint32_t(a.m.tr.lines));
+            uint32_t* idx = W.idx0 + size_t(j) * mc;
+            W.tr.idx = idx;
+            const int n = scope_trace(a.m.tr, __ldg(a.m.tr.off + line), __ldg(a.m.tr.off + line + 1),
+                                      __ldg(a.m.tr.theta + v), W.tr, true, W.s_rings, W.sy);
+            if (W.t == 0)
+                W.line_n[j] = n;
+            uint16_t* np = npos + size_t(j) * mc;
+            for (int c = W.t; c < n; c += TG)
+                np[c] = kNoNext;
+            if (j > 0) {
+                // hash holds line j-1 (cell -> position)
+                uint16_t* prev = npos + size_t(j - 1) * mc;
+                for (int c = W.t; c < n; c += TG) {
+                    const int p = hash_find(hkey, hval, H, idx[c]);
+                    if (p >= 0) {
+                        prev[p] = uint16_t(c);
+                        idx[c] |= kPrevMark;
+                    }
+                }
+                W.sy.sync();
+                for (int c = W.t; c < H; c += TG)
+                    hkey[c] = 0xFFFFFFFFu;
+                W.sy.sync();
+            }
+            if (j + 1 < R) {
+                for (int c = W.t; c < n; c += TG)
+                    hash_insert(hkey, hval, H, idx[c] & ~kPrevMark, uint16_t(c));
+                W.sy.sync();
+            }
+        }
+        W.tr.idx = W.idx0;
+        // the run's slots: wait until their previous occupants were copied
+        const int seq0 = rs * R;
+        if (W.t < R) {
+            const int seq = seq0 + W.t;
+            const unsigned gen = unsigned(seq / Q);
+            if (gen > 0)
+                spin_until_geq(a.slab.used + seq % Q, gen * unsigned(nchunks));
+        }
+        W.sy.sync();
+        for (int j = 0; j < R; ++j) {
+            const int n = W.line_n[j];
+            uint32_t* dst = a.slab.data + size_t((seq0 + j) % Q) * a.slab.slot_words;
+            const uint32_t* idx = W.idx0 + size_t(j) * mc;
+            for (int c = W.t; c < n; c += TG)
+                __stcg(dst + 1 + c, idx[c]);
+            const uint32_t* np = reinterpret_cast<const uint32_t*>(npos + size_t(j) * mc);
+            uint32_t* dnp = dst + 1 + mc;
+            if ((mc & 1) == 0) {
+                for (int c = W.t; c < (n + 1) / 2; c += TG)
+                    __stcg(dnp + c, np[c]);
+            } else {
+                const uint16_t* s16 = npos + size_t(j) * mc;
+                uint16_t* d16 = reinterpret_cast<uint16_t*>(dnp);
+                for (int c = W.t; c < n; c += TG)
+                    d16[c] = s16[c];
+            }
+            if (W.t == 0)
+                __stcg(dst, uint32_t(n));
+        }
+        W.sy.sync();
+        if (W.t < R) {
+            const int seq = seq0 + W.t;
+            asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(a.slab.ready + seq % Q),
+                         "r"(unsigned(seq / Q) + 1)
+                         : "memory");
+        }
+    }
+}
+
+// A run's lines with the gathers one line ahead (problem chunks P >= 4, 256-
+// thread groups, lines of at most KV x (256 / (P/4)) cells). Thread (cl, q)
+// owns buffer slots s = cl + i * NCLV of every line, as float4 q of the chunk.
+// While line j is reduced and scaled, the cells of line j+1 that line j does
+// not cross are copied into the owner's slots (cp.async; they cannot change
+// during the run: every other writer is a predecessor or a successor of the
+// run); the cells line j does cross are handed over through shared memory by
+// line j itself after it has scaled them (no global store, no reload). Every
+// cell therefore sees exactly the sequence of updates of the line-by-line
+// form, bit for bit (same reduction order, same factors, same rounding).
+template <int P, int G>
+__device__ void pipe_run(const FlowArgs& a, GroupWorker<P, G>& W, uint32_t run, int chunk,
+                         const uint16_t* npos, float4* buf, unsigned long long* prof) {
+    constexpr int V = 4, TPC = P / V, NCLV = G / TPC, KV = SweepShape<P>::KV;
+    using GW = GroupWorker<P, G>;
+    using Scale = typename GW::Scale;
+    const int q = W.t % TPC, cl = W.t / TPC;
+    const uint32_t Sp4 = uint32_t(a.m.Sp) / V, col4 = (uint32_t(chunk) * P) / V + uint32_t(q);
+    float4* __restrict__ f4 = reinterpret_cast<float4*>(a.m.field);
+    const int mc = a.m.max_cells;
+    auto issue = [&](int j) {
+        const uint32_t* idx = W.idx0 + size_t(j) * mc;
+        const int n = W.line_n[j];
+#pragma unroll
+        for (int i = 0; i < KV; ++i) {
+            const int s = cl + i * NCLV;
+            const uint32_t e = idx[s < n ? s : 0];
+            cp_async16_if(s < n && !(e & kPrevMark), buf + s * TPC + q, f4 + (e & ~kPrevMark) * Sp4 + col4);
+        }
+        cp_async_commit();
+    };
+    // the run's scalars, staged with the index lists
+    const float* sm = reinterpret_cast<const float*>(W.ext + npos_words(a.run, mc) + size_t(mc) * size_t(P));
+    const double* spf = reinterpret_cast<const double*>(sm + a.run * P + (P & 1));
+    const uint32_t* sact = reinterpret_cast<const uint32_t*>(spf + P);
+    if (W.t < P) {
+        W.pf_next = spf[W.t];
+        W.act_next = sact[W.t] != 0;
+    }
+    issue(0);
+    for (int j = 0; j < a.run; ++j) {
+        if (W.t < P)
+            W.m_next = sm[j * P + W.t];
+        const int n = W.line_n[j];
+        const uint32_t* idx = W.idx0 + size_t(j) * mc;
+        const uint16_t* np = npos + size_t(j) * mc;
+        cp_async_wait_all();
+        float4 x[KV];
+#pragma unroll
+        for (int i = 0; i < KV; ++i) {
+            const int s = cl + i * NCLV;
+            x[i] = s < n ? buf[s * TPC + q] : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+        double s0, s1, s2, s3;
+        GW::template partials<KV>(x, s0, s1, s2, s3);
+        // the slots are read (the sums depend on every value) before the
+        // next line's copies may land in them
+        asm volatile("" ::"d"(s0), "d"(s1), "d"(s2), "d"(s3));
+        if (j + 1 < a.run)
+            issue(j + 1);
+#pragma unroll
+        for (int o = TPC; o < 32; o <<= 1) {
+            s0 += __shfl_xor_sync(0xFFFFFFFFu, s0, o);
+            s1 += __shfl_xor_sync(0xFFFFFFFFu, s1, o);
+            s2 += __shfl_xor_sync(0xFFFFFFFFu, s2, o);
+            s3 += __shfl_xor_sync(0xFFFFFFFFu, s3, o);
+        }
+        const int lane = W.t & 31, warp = W.t >> 5;
+        if (lane < TPC) {
+            double* r = W.red + warp * P + q * V;
+            r[0] = s0;
+            r[1] = s1;
+            r[2] = s2;
+            r[3] = s3;
+        }
+        W.sy.sync();
+        if (j == 0 && prof && W.t == 0)
+            prof[3] = gtimer();
+        W.factors_to_smem(chunk);
+        W.sy.sync();
+        if (j == 0 && prof && W.t == 0)
+            prof[4] = gtimer();
+        Scale g0, g1, g2, g3;
+        W.load_scales(q, g0, g1, g2, g3);  // identity Scales store unchanged values
+#pragma unroll
+        for (int i = 0; i < KV; ++i) {
+            const int s = cl + i * NCLV;
+            const bool in = s < n;
+            const float4 r = GW::scale4(x[i], g0, g1, g2, g3);
+            const uint16_t nx = np[in ? s : 0];
+            const uint32_t e = idx[in ? s : 0] & ~kPrevMark;
+            // line j+1 takes shared cells from its buffer slot; the others go home
+            st_shared_v4_if(in && nx != kNoNext, buf + int(nx) * TPC + q, r);
+            st_global_cg_v4_if(in && nx == kNoNext, f4 + e * Sp4 + col4, r);
+        }
+        // hand-overs visible; this line's stores ordered before the next
+        // line's copies
+        W.sy.sync();
+    }
+}
+
 // Updater role: (run, chunk) tasks in topological order. Stage the run's
 // index lists while its predecessors of this chunk finish, update the run's
 // lines in order (the chain between them stays inside the group), then count
@@ -480,7 +826,7 @@ __device__ void flow_updater(const FlowArgs& a, GroupWorker<P, G>& W) {
     const int total = per_sweep * a.n_sweeps;
     while (task < total) {
         if (a.prof) {
-            prof = a.prof + 8 * size_t(task);
+            prof = a.prof + 16 * size_t(task);
             if (W.t == 0)
                 prof[0] = gtimer();
         }
@@ -500,16 +846,55 @@ __device__ void flow_updater(const FlowArgs& a, GroupWorker<P, G>& W) {
         const unsigned target = s * npred + (s - 1) * __ldg(a.npred_x + run);
         unsigned* cnt = a.count + size_t(run) * nchunks + chunk;
         auto stage_lists = [&](int ct, int nct) {
-            // every line's index list of the run, from the slab into shared
-            // memory (L2 reads: slots are rewritten)
+            // every line's index list of the run (pipelined: and next
+            // positions), from the slab into shared memory (L2 reads: slots
+            // are rewritten); four loads in flight per thread
+            const int mc = a.m.max_cells;
             for (int j = 0; j < a.run; ++j) {
                 const uint32_t* src = a.slab.data + size_t((seq0 + j) % Q) * a.slab.slot_words;
                 const int n = int(__ldcg(src));
-                uint32_t* dst = W.idx0 + size_t(j) * a.m.max_cells;
-                for (int c = ct; c < n; c += nct)
-                    dst[c] = __ldcg(src + 1 + c);
+                uint32_t* dst = W.idx0 + size_t(j) * mc;
+                auto copy = [&](const uint32_t* s, uint32_t* d, int m) {
+                    int c = ct;
+                    for (; c + 3 * nct < m; c += 4 * nct) {
+                        const uint32_t v0 = __ldcg(s + c), v1 = __ldcg(s + c + nct),
+                                       v2 = __ldcg(s + c + 2 * nct), v3 = __ldcg(s + c + 3 * nct);
+                        d[c] = v0;
+                        d[c + nct] = v1;
+                        d[c + 2 * nct] = v2;
+                        d[c + 3 * nct] = v3;
+                    }
+                    for (; c < m; c += nct)
+                        d[c] = __ldcg(s + c);
+                };
+                copy(src + 1, dst, n);
+                if (a.pipe) {
+                    uint16_t* np = reinterpret_cast<uint16_t*>(W.ext) + size_t(j) * mc;
+                    if ((mc & 1) == 0) {
+                        copy(src + 1 + mc, reinterpret_cast<uint32_t*>(np), (n + 1) / 2);
+                    } else {
+                        const uint16_t* s16 = reinterpret_cast<const uint16_t*>(src + 1 + mc);
+                        for (int c = ct; c < n; c += nct)
+                            np[c] = __ldcg(s16 + c);
+                    }
+                }
                 if (ct == 0)
                     W.line_n[j] = n;
+            }
+            if (a.pipe) {
+                // the run's measurements and the chunk's floors (inputs: never
+                // written by the sweep, so they load before the predecessors end)
+                float* sm = reinterpret_cast<float*>(
+                    W.ext + npos_words(a.run, mc) + size_t(mc) * size_t(P));
+                double* spf = reinterpret_cast<double*>(sm + a.run * P + (P & 1));
+                uint32_t* sact = reinterpret_cast<uint32_t*>(spf + P);
+                const uint32_t c0 = uint32_t(chunk) * P;
+                for (int k = ct; k < a.run * P; k += nct)
+                    sm[k] = __ldcs(a.m.proj + size_t(run_line(a, run, k / P)) * a.m.Sp + c0 + k % P);
+                for (int k = ct; k < P; k += nct) {
+                    spf[k] = __ldg(a.m.p_floor + c0 + k);
+                    sact[k] = __ldg(a.m.active + c0 + k);
+                }
             }
         };
         if constexpr (G == 32) {
@@ -537,12 +922,17 @@ __device__ void flow_updater(const FlowArgs& a, GroupWorker<P, G>& W) {
             if (warp == 1) {
                 if (lane == 0 && target)
                     spin_until_geq(cnt, target);
+                if (prof && lane == 0)
+                    prof[15] = gtimer();  // predecessors counted in
             } else {
                 if (W.t == 0)
                     for (int j = 0; j < a.run; ++j)
                         spin_until_geq(a.slab.ready + (seq0 + j) % Q, unsigned((seq0 + j) / Q) + 1);
                 copy_sync.sync();
                 stage_lists(W.t < 32 ? W.t : W.t - 32, kCopy);
+                copy_sync.sync();
+                if (prof && W.t == 0)
+                    prof[7] = gtimer();  // lists staged
             }
             // index lists staged and the predecessors counted in (the acquire
             // orders the gathers after their released stores)
@@ -554,15 +944,26 @@ __device__ void flow_updater(const FlowArgs& a, GroupWorker<P, G>& W) {
             W.meta[2] = chunk;
         if (prof && W.t == 0)
             prof[1] = prof[2] = gtimer();
-        for (int j = 0; j < a.run; ++j) {
-            // later lines of the run follow the group's own stores (sync below)
-            W.load_scalars(run_line(a, run, j), chunk);
-            W.tr.idx = W.idx0 + size_t(j) * a.m.max_cells;
-            if (W.t == 0)
-                W.meta[0] = W.line_n[j];
-            W.sy.sync();
-            W.update(j == 0 ? prof : nullptr);
-            W.sy.sync();
+        bool piped = false;
+        if constexpr (P >= 4 && G >= TG) {
+            if (a.pipe) {
+                const uint16_t* npos = reinterpret_cast<const uint16_t*>(W.ext);
+                float4* buf = reinterpret_cast<float4*>(W.ext + npos_words(a.run, a.m.max_cells));
+                pipe_run<P, G>(a, W, run, chunk, npos, buf, prof);
+                piped = true;
+            }
+        }
+        if (!piped) {
+            for (int j = 0; j < a.run; ++j) {
+                // later lines of the run follow the group's own stores (sync below)
+                W.load_scalars(run_line(a, run, j), chunk);
+                W.tr.idx = W.idx0 + size_t(j) * a.m.max_cells;
+                if (W.t == 0)
+                    W.meta[0] = W.line_n[j];
+                W.sy.sync();
+                W.update(j == 0 ? prof : nullptr);
+                W.sy.sync();
+            }
         }
         W.tr.idx = W.idx0;
         if (prof && W.t == 0)
@@ -593,14 +994,22 @@ __global__ void __launch_bounds__(CTA, 1) mart_flow_kernel(FlowArgs a) {
     stage_rings(smem, a.m.tr.rings, a.n_rings);
     __syncthreads();
     if (int(blockIdx.x) < a.tracer_ctas) {
-        GroupWorker<P, TG> W(a.m, smem, a.n_rings, true, 1);
-        flow_tracer<P>(a, W);
+        if (int(threadIdx.x) / TG >= a.tr_groups)
+            return;  // no shared memory left for this group
+        if (a.pipe) {
+            GroupWorker<P, TG> W(a.m, smem, a.n_rings, true, a.run, tracer_extra(a.run, a.m.max_cells));
+            flow_tracer_runs<P>(a, W);
+        } else {
+            GroupWorker<P, TG> W(a.m, smem, a.n_rings, true, 1);
+            flow_tracer<P>(a, W);
+        }
     } else {
         constexpr int GU = SweepShape<P>::GU;
         if (int(threadIdx.x) / GU >= a.upd_groups)
             return;  // no shared memory left for this group
         // single-warp updaters trace their own lines (trace arrays needed)
-        GroupWorker<P, GU> W(a.m, smem, a.n_rings, GU == 32, a.run);
+        GroupWorker<P, GU> W(a.m, smem, a.n_rings, GU == 32, a.run,
+                             a.pipe ? updater_extra(P, a.run, a.m.max_cells) : 0);
         flow_updater<P, GU>(a, W);
     }
 }
@@ -611,7 +1020,26 @@ static void flow_launch_t(FlowArgs& a, int sms, cudaStream_t st) {
     int dev = 0, optin = 0;
     UB_CUDA(cudaGetDevice(&dev));
     UB_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
-    const size_t smem = flow_smem_bytes(a.m, a.n_rings, GU, size_t(optin) - 1024, a.upd_groups);
+    // pipelined runs (USCG_PIPE=1): vector chunks, every line within the
+    // register tile, positions in 16 bits. Off by default: on the c2 stack the
+    // sweep is bound by the per-SM rate of scattered L1 requests and the
+    // dependency chain, not by the gather latency it hides.
+    a.pipe = 0;
+    if constexpr (P >= 4 && GU >= TG) {
+        constexpr int cover = SweepShape<P>::KV * (GU / (P / 4));
+        const char* e = std::getenv("USCG_PIPE");
+        a.pipe = (e ? std::atoi(e) : 0) != 0 && a.m.max_cells <= cover && a.run > 1;
+    }
+    FlowLayout L = flow_layout(a.m, a.n_rings, GU, a.pipe != 0, size_t(optin) - 1024);
+    if (a.pipe && L.groups < std::min(2, CTA / GU)) {  // too little shared memory: plain runs
+        a.pipe = 0;
+        L = flow_layout(a.m, a.n_rings, GU, false, size_t(optin) - 1024);
+    }
+    a.upd_groups = L.groups;
+    if (const char* e = std::getenv("USCG_UPD_GROUPS"))  // experiments: fewer groups per SM
+        a.upd_groups = std::max(1, std::min(L.groups, std::atoi(e)));
+    a.tr_groups = L.tgroups;
+    const size_t smem = L.bytes;
     UB_CUDA(cudaFuncSetAttribute(mart_flow_kernel<P>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  int(smem)));
     int per_sm = 0;
@@ -619,16 +1047,22 @@ static void flow_launch_t(FlowArgs& a, int sms, cudaStream_t st) {
     if (per_sm < 1)
         throw CudaError("mart_flow_kernel cannot be resident (shared memory too large)");
     const int grid = sms * per_sm;
-    // tracer CTAs: trace work ~ lines, update work ~ lines * chunks (and more
-    // for single-warp updaters, which finish a line faster than a trace)
+    // tracer CTAs: trace work ~ lines, update work ~ lines * problems (in
+    // 8-problem units; measured balance 2.7 : 4 per unit at 4 tracer groups)
     int k = 0;
     if (GU == 32)
         k = 0;  // single-warp updaters trace their own lines
     else if (const char* e = std::getenv("USCG_TRACER_CTAS"))
         k = std::max(1, std::atoi(e));
     else
-        k = std::max(1, int(double(grid) * 2.7 / (2.7 + 4.0 * a.m.nchunks) + 0.5));
+        k = std::max(1, int(double(grid) * 2.7 * (4.0 / a.tr_groups) /
+                                (2.7 * (4.0 / a.tr_groups) + 4.0 * (a.m.Sp / 8.0)) + 0.5));
     a.tracer_ctas = std::min(k, grid - 1);
+    if (const char* e = std::getenv("USCG_FLOW_VERBOSE"); e && std::atoi(e))
+        std::fprintf(stderr,
+                     "mart_flow_kernel: P=%d run=%d pipe=%d grid=%d tracer_ctas=%d tr_groups=%d "
+                     "upd_groups=%d smem=%zu\n",
+                     P, a.run, a.pipe, grid, a.tracer_ctas, a.tr_groups, a.upd_groups, smem);
     // every CTA must be resident: tracers and updaters wait on each other
     mart_flow_kernel<P><<<grid, CTA, smem, st>>>(a);
 }
@@ -659,6 +1093,9 @@ void launch_mart_flow(const MartArgs& h, const FlowSchedule& fs, unsigned* count
     a.slab = slab;
     a.tracer_ctas = 1;
     a.prof = prof;
+    a.pipe = 0;
+    a.tr_groups = CTA / TG;
+    a.upd_groups = 1;
     UB_CUDA(cudaMemsetAsync(next, 0, sizeof(unsigned), st));
     UB_CUDA(cudaMemsetAsync(slab.tnext, 0, sizeof(unsigned), st));
     UB_CUDA(cudaMemsetAsync(slab.ready, 0, sizeof(unsigned) * slab.Q, st));
@@ -668,7 +1105,9 @@ void launch_mart_flow(const MartArgs& h, const FlowSchedule& fs, unsigned* count
         case 2: flow_launch_t<2>(a, sms, st); break;
         case 4: flow_launch_t<4>(a, sms, st); break;
         case 8: flow_launch_t<8>(a, sms, st); break;
-        default: throw CudaError("mart_flow_kernel supports problem chunks of at most 8");
+        case 16: flow_launch_t<16>(a, sms, st); break;
+        case 32: flow_launch_t<32>(a, sms, st); break;
+        default: throw CudaError("mart_flow_kernel supports problem chunks of at most 32");
     }
     count_launch();
     cudaError_t e = cudaGetLastError();

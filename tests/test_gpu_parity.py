@@ -369,6 +369,34 @@ def test_stack_matches_oracle_per_problem(ub, orc, S):
         assert np.array_equal(rep.crossed, wrep["crossed"])
 
 
+@pytest.mark.parametrize("S,run,width", [(128, 4, 8), (128, 8, 32), (64, 4, 16), (16, 2, 8), (40, 4, 8),
+                                         (4, 4, 8)])
+def test_pipelined_runs_are_bit_identical(ub, orc, monkeypatch, capfd, S, run, width):
+    """The pipelined run executor (gathers one line ahead, shared cells handed
+    over in shared memory) performs the line-by-line updates bit for bit, for
+    every chunk shape (8 problems / 256 threads, 16 / 512, 32 / 1024)."""
+    monkeypatch.setenv("USCG_RUN", str(run))
+    monkeypatch.setenv("USCG_CHUNK_WIDTH", str(width))
+    monkeypatch.setenv("USCG_FLOW_VERBOSE", "1")
+    spec, geom, tr, oc = _m1_case(ub, orc, "arc", n_rings=48, views=16, du=96)
+    rng = np.random.default_rng(S + run)
+    truth = rng.uniform(0.2, 3.0, (S, spec.cell_count()))
+    proj = ub.project_stack(tr, truth.astype(np.float32))
+    cfg = ub.SolverConfig(beta=0.7, tolerance=0, max_sweeps=3)
+    out = {}
+    for pipe in (1, 0):
+        monkeypatch.setenv("USCG_PIPE", str(pipe))
+        out[pipe] = [f for f, _ in ub.reconstruct_stack(proj, cfg, tr)]
+        log = capfd.readouterr().err
+        assert f"run={run} pipe={pipe}" in log, log
+        if width > 8:
+            assert f"P={width} " in log, log
+    for p in range(S):
+        assert np.array_equal(out[1][p], out[0][p]), p
+    want, _ = oc.reconstruct(geom.thetas(), proj[0].astype(np.float64), beta=0.7, tolerance=0, max_sweeps=3)
+    assert (np.abs(out[1][0] - want) / want).max() <= 1e-4
+
+
 # ---------------------------------------------------------------------------
 # generalized seams (verbatim BASELINE shapes) vs the C restatement
 # ---------------------------------------------------------------------------

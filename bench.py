@@ -250,6 +250,180 @@ def config_dict(wl, args):
 
 
 # ---------------------------------------------------------------------------
+# C5: coefficient generation, rotated reuse, USPG -> CG resampling
+# ---------------------------------------------------------------------------
+def bench_c5(args, rank, world, local):
+    """BASELINE configs[4]. Three device-timed legs:
+    (1) the first-view generator over the 1024x1024 panel (rays/s; device time
+    reported by the library, count + scan + write + annotate); (2) rotated
+    reuse: every (view, line) of 180 views served from the one-view record
+    store, |active| + index checksum per line (lines/s; bytes 20*C + 12*L per
+    view); (3) resampling a seeded U[0,1] 512-ring x 512-slice USPG volume to
+    1024 x 1024 x 512 (8 B per output pixel). N > 1 ranks split detector rows,
+    views and slices (strong scaling; no data-path exchange)."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_2208_12964_b200 as ub
+    from paper_2208_12964_b200 import dist as udist
+    from paper_2208_12964_b200 import uscg, workloads
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    wl = workloads.make("c5")
+    spec, geom = wl.spec, wl.geom
+    ctx = ub.Context(local)
+    # one stream for torch and the library: events time the launching stream
+    # (the legacy default stream's handle is 0, which the ABI reads as "the
+    # context's own stream")
+    stream = torch.cuda.Stream(device=local)
+    torch.cuda.set_stream(stream)
+    ctx.set_stream(stream.cuda_stream)
+    L = ub.load()
+    src, det = geom.first_view_rays()
+    lines = geom.lines()
+    rows = geom.det_v
+    r0, r1 = rank * rows // world, (rank + 1) * rows // world
+    mine = slice(r0 * geom.det_u, r1 * geom.det_u)
+
+    # (1) generator on this rank's detector rows (1-view tracers; the record
+    #     store is rebuilt every step)
+    gen_ms = []
+    recs = 0
+    for k in range(args.warmup + args.steps):
+        tr = ub.Tracer.from_rays(spec, src[mine], det[mine], 1, ctx=ctx)
+        inf = tr.info()
+        if k >= args.warmup:
+            gen_ms.append(inf["generator_ms"])
+        recs = inf["records"]
+        tr.close()
+    g_ms = float(np.mean(gen_ms))
+    rays_mine = (r1 - r0) * geom.det_u
+
+    # (2) rotated reuse over this rank's views, full record store per rank
+    tr = ub.Tracer(geom, spec, False, ctx=ctx)
+    inf = tr.info()
+    v0, v1 = rank * geom.views // world, (rank + 1) * geom.views // world
+    nv = v1 - v0
+    counts_d = torch.empty(nv * lines, dtype=torch.int32, device="cuda")
+    sums_d = torch.empty(nv * lines, dtype=torch.int64, device="cuda")
+
+    def reuse():
+        uscg._check(L.uscg_trace_checksums(tr.h, v0, nv, uscg.C.c_void_p(counts_d.data_ptr()),
+                                           uscg.C.c_void_p(sums_d.data_ptr()), uscg.DEVICE_POINTERS))
+
+    for _ in range(args.warmup):
+        reuse()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clocks = Clocks(local)
+    clocks.start()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    launches0 = ub.launch_count()
+    e0.record(stream)
+    for _ in range(args.steps):
+        reuse()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    reuse_ms = e0.elapsed_time(e1) / args.steps
+    chords = inf["records"] * nv  # chords traversed per pass (records x views)
+    reuse_bytes = 20 * chords + 12 * nv * lines
+    # parity spot check against the library's own per-line counts
+    cnt_ref = tr.trace_counts()[v0:v1].reshape(-1)
+    reuse_ok = bool(np.array_equal(counts_d.cpu().numpy().astype(np.uint32), cnt_ref))
+    tr.close()
+
+    # (3) resample this rank's slices of a seeded U[0,1] volume
+    sl0, sl1 = rank * spec.slices() // world, (rank + 1) * spec.slices() // world
+    sub = ub.GridSpec(spec.n, spec.ring_spacing, spec.slice_height, spec.mode, ring_counts=spec.ring_counts,
+                      n_slices=sl1 - sl0)
+    npix = 1024
+    gen = torch.Generator(device="cuda")
+    gen.manual_seed(12345 + rank)
+    field_d = torch.rand(sub.cell_count(), dtype=torch.float32, device="cuda", generator=gen)
+    img_d = torch.empty((sl1 - sl0, npix, npix), dtype=torch.float32, device="cuda")
+    g_c, keep = sub._c()
+
+    def resample():
+        uscg._check(L.uscg_resample(ctx.h, uscg.C.byref(g_c), uscg.C.c_void_p(field_d.data_ptr()), 1, npix,
+                                    uscg.C.c_void_p(img_d.data_ptr()), uscg.DEVICE_POINTERS))
+
+    for _ in range(args.warmup):
+        resample()
+    torch.cuda.synchronize()
+    e0.record(stream)
+    for _ in range(args.steps):
+        resample()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    launches = ub.launch_count() - launches0
+    clk = clocks.stop()
+    res_ms = e0.elapsed_time(e1) / args.steps
+    px = (sl1 - sl0) * npix * npix
+    g_ms, reuse_ms, res_ms = udist.max_over_ranks([g_ms, reuse_ms, res_ms], device="cuda")
+    rays_all, recs_all = udist.sum_over_ranks([rays_mine, recs], device="cuda")
+
+    if rank != 0:
+        if world > 1:
+            dist.barrier()
+            dist.destroy_process_group()
+        return
+    peak, peak_kind = hbm_peak()
+    gen_bytes = 20 * recs_all + 4 * (lines + 1)
+    reuse_bytes_all = reuse_bytes * world
+    res_bytes = 8 * px * world
+
+    def roof(bytes_, ms, kernel, model):
+        a = bytes_ / (ms * 1e-3) / 1e9
+        return {"bound": "hbm", "achieved": a, "peak": peak, "unit": "GB/s", "frac": a / peak, "traffic": None,
+                "peak_kind": peak_kind, "kernel": kernel, "bytes_model": model}
+
+    cpu = None
+    if not args.no_cpu and world == 1:
+        import oracle
+
+        orc = oracle.Orc()
+        og = oracle.OrcGrid(spec.rings(), spec.ring_spacing, spec.slices(), spec.slice_height, True,
+                            spec.ring_counts)
+        pick = np.random.default_rng(5).choice(lines, 512, replace=False)
+        t0 = time.perf_counter()
+        oc = orc.cache(og, src[pick], det[pick])
+        wall = time.perf_counter() - t0
+        cpu = {"value": pick.size / wall, "unit": "rays/s", "cores": 1, "kind": "port",
+               "sample": f"oracle C restatement of precompute_first_view on {pick.size} random rays of the panel "
+                         f"({wall:.1f} s, {int(oc.offsets[-1])} records)"}
+    value = rays_all / (g_ms * 1e-3)
+    line = {
+        "metric": "first-view generator rays/s (c5)", "value": value, "unit": "rays/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": g_ms, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic: BASELINE c5 geometry; seeded U[0,1] USPG volume for the resample",
+        "config": {"workload": "c5", "rings": spec.rings(), "sector_law": "round(2*pi*(i+0.5))",
+                   "slices": spec.slices(), "cells": spec.cell_count(), "detectors": [geom.det_u, geom.det_v],
+                   "views": geom.views, "resample_pixels": [npix, npix, spec.slices()],
+                   "l2": "working sets (11.6 GB record store, 1.7 + 2.1 GB volumes) exceed L2",
+                   "parallelism": "rows / views / slices split across ranks"},
+        "roofline": roof(gen_bytes, g_ms, "generate_count_kernel + generate_write_kernel + annotate_kernel",
+                         "20*records + 4*(lines+1) written (SURVEY.md §8(d))"),
+        "generator": {"ms": g_ms, "rays": rays_all, "records": recs_all, "records_per_s": recs_all / (g_ms * 1e-3)},
+        "rotated_reuse": {"ms": reuse_ms, "views": geom.views, "lines_per_s": world * nv * lines / (reuse_ms * 1e-3),
+                          "chords_per_s": world * chords / (reuse_ms * 1e-3), "counts_match_library": reuse_ok,
+                          "roofline": roof(reuse_bytes_all, reuse_ms, "checksum_kernel<128>",
+                                           "20*C + 12*L per view (SURVEY.md §8(d))")},
+        "resample": {"ms": res_ms, "pixels": px * world, "pixels_per_s": px * world / (res_ms * 1e-3),
+                     "roofline": roof(res_bytes, res_ms, "bin_map_kernel + map_resample_kernel",
+                                      "8 B per output pixel (SURVEY.md §8(d))")},
+        "cpu_baseline": cpu, "e2e": None, "gpu_launches": int(launches), "clocks": clk,
+    }
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+# ---------------------------------------------------------------------------
 # GPU arm
 # ---------------------------------------------------------------------------
 def main():
@@ -271,6 +445,9 @@ def main():
     if args.impl == "reference":
         run_reference(args, rank, world)
         return
+    if args.config == "c5":
+        bench_c5(args, rank, world, local)
+        return
 
     import torch
     import torch.distributed as dist
@@ -286,7 +463,11 @@ def main():
     wl = workloads.make(args.config, problems=args.problems)
     S = wl.problems
     ctx = ub.Context(local)
-    stream = torch.cuda.current_stream()
+    # one stream for torch and the library: events time the launching stream
+    # (the legacy default stream's handle is 0, which the ABI reads as "the
+    # context's own stream")
+    stream = torch.cuda.Stream(device=local)
+    torch.cuda.set_stream(stream)
     ctx.set_stream(stream.cuda_stream)
 
     # ---- precompute (geometry only; reported separately like ReconReport::seconds) ----

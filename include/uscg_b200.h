@@ -121,6 +121,8 @@ typedef struct {
     uint64_t cells_per_sweep;      /* sum of |active| over every (view, line) */
     uint64_t chords_per_sweep;     /* records * views */
     int32_t levels;                /* MART dependency levels per sweep (0 until built) */
+    double generator_ms;           /* device time of the first-view generator (count + scan +
+                                      write + annotate; 0 for an imported cache) */
 } uscg_tracer_info;
 
 const char* uscg_last_error(void);
@@ -170,6 +172,15 @@ uscg_status uscg_trace_line(uscg_tracer tracer, int32_t line, double theta_deg, 
                             int64_t cap, int64_t* count);
 /* |active| of every line of every view, views*lines u32 (TraceScratch::cells). */
 uscg_status uscg_trace_counts(uscg_tracer tracer, uint32_t* cells_out);
+/* Rotated reuse of the record store (the symmetry saving of FirstViewCache,
+ * tracer.hpp:18-39, served per view by Tracer::trace_line, tracer.cpp:148-201):
+ * for views [view0, view0 + nviews) and every line, |active| (counts,
+ * nviews*lines u32) and the sum of the active cell indices (sums, u64,
+ * independent of emission order), computed from the records without expanding
+ * the index lists. USCG_DEVICE_POINTERS: counts/sums are device buffers and
+ * the call returns without synchronizing. */
+uscg_status uscg_trace_checksums(uscg_tracer tracer, int32_t view0, int32_t nviews,
+                                 uint32_t* counts, uint64_t* sums, uint32_t flags);
 /* Build the MART dependency schedule now (otherwise built on first use). */
 uscg_status uscg_tracer_build_schedule(uscg_tracer tracer);
 /* stride of the interleaved problem dimension for S problems */

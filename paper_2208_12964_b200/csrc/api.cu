@@ -1,6 +1,7 @@
 // C ABI of uscg_b200 (include/uscg_b200.h): host orchestration in C++.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <atomic>
 #include <chrono>
 #include <cmath>
@@ -80,10 +81,13 @@ void set_error(const std::string& msg) { g_last_error = msg; }
 
 using namespace ub;
 
+struct ResampleCache;
+
 struct uscg_ctx_s {
     int device = 0;
     cudaStream_t own = nullptr;
     cudaStream_t stream = nullptr;
+    ResampleCache* resample = nullptr;  // ring table + bin-point map of the last resample grid
 };
 
 struct GraphCache {
@@ -137,6 +141,7 @@ struct uscg_tracer_s {
     int done_chunks = 0;
     unsigned epoch = 0;
     double schedule_seconds = 0;
+    double generator_ms = 0;  // device time of the first-view generator
     // MART workspace
     DevBuf<MartArgs> d_args;
     DevBuf<float> w_field, w_proj, w_prev, w_stage;
@@ -175,6 +180,25 @@ struct uscg_tracer_s {
     }
     cudaStream_t st() const { return ctx->stream; }
     uint64_t units() const { return uint64_t(lines) * uint64_t(views); }
+};
+
+// uscg_resample's per-grid state, kept by the context so that repeated calls
+// on one grid (a volume resampled slab by slab, or every iteration) allocate
+// and build nothing
+struct ResampleCache {
+    int n_rings = -1, n_slices = 0, volume = 0, npix = 0;
+    double ring_spacing = 0, slice_height = 0;
+    std::vector<uint32_t> counts;  // empty: the reference law
+    std::unique_ptr<uscg_tracer_s> grid;
+    DevBuf<uint32_t> map;
+    bool matches(const uscg_grid* g, int n) const {
+        if (!grid || g->n_rings != n_rings || (g->volume ? g->n_slices : 1) != n_slices ||
+            (g->volume ? 1 : 0) != volume || n != npix || g->ring_spacing != ring_spacing ||
+            g->slice_height != slice_height || (g->ring_counts == nullptr) != counts.empty())
+            return false;
+        return !g->ring_counts ||
+               std::equal(counts.begin(), counts.end(), g->ring_counts);
+    }
 };
 
 namespace {
@@ -286,11 +310,14 @@ void fill_views(uscg_tracer_s* t, int views, const double* angles) {
 }
 
 // max records per line, per-unit cell counts, cells per sweep
-void finish_tracer(uscg_tracer_s* t, const std::vector<uint32_t>& off) {
+void finish_tracer(uscg_tracer_s* t, const std::vector<uint32_t>& off,
+                   cudaEvent_t annotated = nullptr) {
     t->max_recs = 0;
     for (int l = 0; l < t->lines; ++l)
         t->max_recs = std::max<int>(t->max_recs, int(off[l + 1] - off[l]));
     launch_annotate(t->lines, t->d_off.p, t->d_pa.p, t->d_pb.p, t->d_key.p, t->d_rings.p, t->st());
+    if (annotated)
+        UB_CUDA(cudaEventRecord(annotated, t->st()));
     const uint64_t units = t->units();
     need(units < (1ull << 32), "views * lines must fit in 32 bits");
     t->d_cells.alloc(units);
@@ -369,9 +396,16 @@ uscg_tracer_s* build_from_rays(uscg_ctx ctx, const uscg_grid* grid, int lines, c
     const DevGrid g = t->dev_grid();
     DevBuf<uint32_t> d_cnt;
     d_cnt.alloc(size_t(lines));
-    launch_generate_count(g, lines, d_rays.p, d_rays.p + 3 * size_t(lines), d_cnt.p, t->st());
     t->d_off.alloc(size_t(lines) + 1);
+    // generator device time: count + scan, then write + annotate (the host
+    // allocation of the record store between them is not counted)
+    cudaEvent_t ev[4];
+    for (auto& e : ev)
+        UB_CUDA(cudaEventCreate(&e));
+    UB_CUDA(cudaEventRecord(ev[0], t->st()));
+    launch_generate_count(g, lines, d_rays.p, d_rays.p + 3 * size_t(lines), d_cnt.p, t->st());
     launch_exclusive_scan_u32(d_cnt.p, t->d_off.p, lines, t->st());
+    UB_CUDA(cudaEventRecord(ev[1], t->st()));
     std::vector<uint32_t> off(size_t(lines) + 1);
     UB_CUDA(cudaMemcpyAsync(off.data(), t->d_off.p, sizeof(uint32_t) * (lines + 1),
                             cudaMemcpyDeviceToHost, t->st()));
@@ -381,9 +415,16 @@ uscg_tracer_s* build_from_rays(uscg_ctx ctx, const uscg_grid* grid, int lines, c
     t->d_pa.alloc(R);
     t->d_pb.alloc(R);
     t->d_key.alloc(R);
+    UB_CUDA(cudaEventRecord(ev[2], t->st()));
     launch_generate_write(g, lines, d_rays.p, d_rays.p + 3 * size_t(lines), t->d_off.p, t->d_pa.p,
                           t->d_pb.p, t->d_key.p, t->st());
-    finish_tracer(t.get(), off);
+    finish_tracer(t.get(), off, ev[3]);
+    float a = 0, b = 0;
+    UB_CUDA(cudaEventElapsedTime(&a, ev[0], ev[1]));
+    UB_CUDA(cudaEventElapsedTime(&b, ev[2], ev[3]));
+    t->generator_ms = double(a) + double(b);
+    for (auto& e : ev)
+        cudaEventDestroy(e);
     return t.release();
 }
 
@@ -585,6 +626,10 @@ uscg_status uscg_ctx_destroy(uscg_ctx ctx) {
         if (!ctx)
             return;
         cudaSetDevice(ctx->device);
+        if (ctx->resample) {
+            cudaDeviceSynchronize();
+            delete ctx->resample;
+        }
         if (ctx->own)
             cudaStreamDestroy(ctx->own);
         delete ctx;
@@ -594,6 +639,10 @@ uscg_status uscg_ctx_destroy(uscg_ctx ctx) {
 uscg_status uscg_ctx_set_stream(uscg_ctx ctx, void* stream) {
     return guarded([&] {
         need(ctx != nullptr, "null context");
+        bind(ctx);
+        // work queued on the old stream (e.g. a cached resample map) is complete
+        // before anything runs on the new one
+        UB_CUDA(cudaStreamSynchronize(ctx->stream));
         ctx->stream = stream ? static_cast<cudaStream_t>(stream) : ctx->own;
     });
 }
@@ -718,6 +767,33 @@ uscg_status uscg_tracer_get_info(uscg_tracer t, uscg_tracer_info* info) {
         info->cells_per_sweep = t->cells_per_sweep;
         info->chords_per_sweep = t->records * uint64_t(t->views);
         info->levels = t->sched_built ? int32_t(t->level_off.size()) - 1 : 0;
+        info->generator_ms = t->generator_ms;
+    });
+}
+
+uscg_status uscg_trace_checksums(uscg_tracer t, int32_t view0, int32_t nviews, uint32_t* counts,
+                                 uint64_t* sums, uint32_t flags) {
+    return guarded([&] {
+        need(t != nullptr, "null tracer");
+        bind(t->ctx);
+        need(counts && sums, "null buffer");
+        need(view0 >= 0 && nviews >= 0 && int64_t(view0) + nviews <= t->views, "view range out of bounds");
+        const uint64_t n = uint64_t(nviews) * uint64_t(t->lines);
+        if (n == 0)
+            return;
+        auto* dsum = reinterpret_cast<unsigned long long*>(sums);
+        if (flags & USCG_DEVICE_POINTERS) {
+            launch_checksums(t->trace_args(), view0, nviews, t->n_rings, t->max_recs, counts, dsum, t->st());
+            return;
+        }
+        DevBuf<uint32_t> dc;
+        DevBuf<unsigned long long> ds;
+        dc.alloc(n);
+        ds.alloc(n);
+        launch_checksums(t->trace_args(), view0, nviews, t->n_rings, t->max_recs, dc.p, ds.p, t->st());
+        UB_CUDA(cudaMemcpyAsync(counts, dc.p, sizeof(uint32_t) * n, cudaMemcpyDeviceToHost, t->st()));
+        UB_CUDA(cudaMemcpyAsync(sums, ds.p, sizeof(uint64_t) * n, cudaMemcpyDeviceToHost, t->st()));
+        UB_CUDA(cudaStreamSynchronize(t->st()));
     });
 }
 
@@ -1186,9 +1262,30 @@ uscg_status uscg_resample(uscg_ctx ctx, const uscg_grid* grid, const float* fiel
         need(field && out, "null buffer");
         need(problems >= 1, "problem count must be >= 1");
         need(npix >= 2 && npix % 2 == 0, "image size must be even");
-        std::unique_ptr<uscg_tracer_s> t(new uscg_tracer_s);
-        t->ctx = ctx;
-        fill_grid(t.get(), grid);
+        need(npix <= 65534, "image size must be at most 65534");
+        const bool perm = grid->ring_counts == nullptr && npix == 2 * grid->n_rings;
+        if (!ctx->resample)
+            ctx->resample = new ResampleCache;
+        ResampleCache& rc = *ctx->resample;
+        if (!rc.matches(grid, npix)) {
+            UB_CUDA(cudaStreamSynchronize(ctx->stream));  // the old map may still be in use
+            rc.grid.reset(new uscg_tracer_s);
+            rc.grid->ctx = ctx;
+            fill_grid(rc.grid.get(), grid);
+            if (!perm) {
+                rc.map.alloc(size_t(npix) * npix);
+                launch_bin_map(rc.grid->dev_grid(), npix, rc.map.p, ctx->stream);
+            }
+            rc.n_rings = grid->n_rings;
+            rc.n_slices = grid->volume ? grid->n_slices : 1;
+            rc.volume = grid->volume ? 1 : 0;
+            rc.npix = npix;
+            rc.ring_spacing = grid->ring_spacing;
+            rc.slice_height = grid->slice_height;
+            rc.counts.assign(grid->ring_counts ? grid->ring_counts : nullptr,
+                             grid->ring_counts ? grid->ring_counts + grid->n_rings : nullptr);
+        }
+        const uscg_tracer_s* t = rc.grid.get();
         const int S = problems;
         const bool dev = flags & USCG_DEVICE_POINTERS;
         const bool inter = flags & USCG_LAYOUT_INTERLEAVED;
@@ -1209,16 +1306,10 @@ uscg_status uscg_resample(uscg_ctx ctx, const uscg_grid* grid, const float* fiel
             d_out.alloc(out_n);
             fout = d_out.p;
         }
-        const bool perm = grid->ring_counts == nullptr && npix == 2 * grid->n_rings;
-        if (perm) {
+        if (perm)
             launch_perm_resample(fin, t->cps, slices, S, Sp, npix, fout, st);
-        } else {
-            DevBuf<uint32_t> map;
-            map.alloc(size_t(npix) * npix);
-            launch_bin_map(t->dev_grid(), npix, map.p, st);
-            launch_map_resample(fin, t->cps, slices, S, Sp, map.p, npix, fout, st);
-            UB_CUDA(cudaStreamSynchronize(st));
-        }
+        else
+            launch_map_resample(fin, t->cps, slices, S, Sp, rc.map.p, npix, fout, st);
         if (!dev)
             UB_CUDA(cudaMemcpyAsync(out, fout, sizeof(float) * out_n, cudaMemcpyDeviceToHost, st));
         UB_CUDA(cudaStreamSynchronize(st));

@@ -280,9 +280,12 @@ __device__ __forceinline__ uint32_t dedup_count(const TraceSmem& S, int i, int n
 // only the count is produced. All threads must call it; it ends synchronized.
 // Generic form: the sync scope may be a named-barrier group; `rings` may point
 // to a shared-memory copy of the ring table. r0/r1 are the line's record range.
+// Phase 1 of a trace: rotate every record of the line (trace_chord,
+// tracer.cpp:104-142) into S.base / S.lohi / S.cnt (count | ng << 16) / S.pos
+// (count); returns whether any record carries the dedup flag (all threads).
 template <class Sync>
-__device__ int scope_trace(const TraceArgs& A, uint32_t r0, uint32_t r1, double theta,
-                           const TraceSmem& S, bool expand, const RingRow* rings, const Sync& sy) {
+__device__ bool rotate_records(const TraceArgs& A, uint32_t r0, uint32_t r1, double theta,
+                               const TraceSmem& S, const RingRow* rings, const Sync& sy) {
     constexpr int NT = Sync::kThreads;
     const int n = int(r1 - r0);
     const int t0 = sy.tid();
@@ -305,7 +308,33 @@ __device__ int scope_trace(const TraceArgs& A, uint32_t r0, uint32_t r1, double 
         S.pos[i] = c;
         any_flag |= flag;
     }
-    if (sy.sync_or(any_flag)) {
+    return sy.sync_or(any_flag);
+}
+
+// count and index sum of one unflagged record's sector range base + [lo..hi]
+// (or the seam range hi..ng-1, 0..lo): an arithmetic series
+__device__ __forceinline__ void range_count_sum(long long b, int lo, int hi, bool seam, int ng,
+                                                unsigned long long& c_acc,
+                                                unsigned long long& s_acc) {
+    long long c, qs;
+    if (!seam) {
+        c = hi - lo + 1;
+        qs = (static_cast<long long>(lo) + hi) * c / 2;
+    } else {
+        c = (ng - hi) + lo + 1;
+        qs = (static_cast<long long>(hi) + ng - 1) * (ng - hi) / 2 + static_cast<long long>(lo) * (lo + 1) / 2;
+    }
+    c_acc += static_cast<unsigned long long>(c);
+    s_acc += static_cast<unsigned long long>(c * b + qs);
+}
+
+template <class Sync>
+__device__ int scope_trace(const TraceArgs& A, uint32_t r0, uint32_t r1, double theta,
+                           const TraceSmem& S, bool expand, const RingRow* rings, const Sync& sy) {
+    constexpr int NT = Sync::kThreads;
+    const int n = int(r1 - r0);
+    const int t0 = sy.tid();
+    if (rotate_records(A, r0, r1, theta, S, rings, sy)) {
         for (int i = t0; i < n; i += NT)
             if (lohi_flag(S.lohi[i]))
                 S.pos[i] = dedup_count(S, i, int(S.cnt[i] >> 16));

@@ -493,6 +493,164 @@ void launch_trace_counts(const TraceArgs& A, int views, int max_recs, uint32_t* 
     check_launch();
 }
 
+// rotated reuse (C5): per (view, line) |active| and the sum of its cells. One
+// warp per line serves every requested view: the line's records come from
+// HBM once and from L1 for the other views (the one-view store serving all
+// views, on chip). Each record is rotated in registers and its sector range
+// summed arithmetically. Dedup-flagged records (tracer.cpp:181-195 only bites
+// between chords of one (slice, ring) whose arcs nearly meet) drop the sectors
+// an earlier chord of the same (slice, ring) covers; their partners are found
+// once per line (they depend on the keys, not the view) and re-rotated per
+// view. Lines beyond the caps scan for partners per view.
+constexpr int kSumWarps = 4;
+constexpr int kSumFlagged = 128;  // flagged records cached per line
+constexpr int kSumPartners = 4;
+
+struct RecRot {
+    long long b;
+    int lo, hi, ng;
+    bool seam;
+};
+
+__device__ __forceinline__ RecRot rot_record(const TraceArgs& A, const RingRow* rings, uint32_t r,
+                                             double theta) {
+    const uint32_t key = __ldg(A.key + r);
+    const RingRow rr = rings[key & kRingMask];
+    RecRot o;
+    rotate_chord(__ldg(A.pa + r), __ldg(A.pb + r), theta, rr.count, rr.inv_step, o.lo, o.hi, o.seam);
+    o.b = ((key >> kSliceShift) & kSliceMask) * (long long)A.cells_per_slice + rr.head;
+    o.ng = int(rr.count);
+    return o;
+}
+
+// sectors of flagged record r0+i not covered by the listed earlier partners
+// (np < 0: scan every earlier record of the same (slice, ring))
+__device__ void flagged_count_sum(const TraceArgs& A, const RingRow* rings, uint32_t r0, int i,
+                                  double theta, const uint16_t* partners, int np,
+                                  unsigned long long& c, unsigned long long& s) {
+    const RecRot me = rot_record(A, rings, r0 + i, theta);
+    RecRot p[kSumPartners];
+    if (np >= 0)
+        for (int k = 0; k < np; ++k)
+            p[k] = rot_record(A, rings, r0 + partners[k], theta);
+    const uint32_t base_key = __ldg(A.key + r0 + i) & ((kSliceMask << kSliceShift) | kRingMask);
+    auto covered = [&](int q) {
+        if (np >= 0) {
+            for (int k = 0; k < np; ++k)
+                if (range_has(q, p[k].lo, p[k].hi, p[k].seam))
+                    return true;
+            return false;
+        }
+        for (int j = i - 1; j >= 0; --j) {
+            if ((__ldg(A.key + r0 + j) & ((kSliceMask << kSliceShift) | kRingMask)) != base_key)
+                continue;
+            const RecRot o = rot_record(A, rings, r0 + j, theta);
+            if (range_has(q, o.lo, o.hi, o.seam))
+                return true;
+        }
+        return false;
+    };
+    auto take = [&](int q) {
+        if (!covered(q)) {
+            ++c;
+            s += static_cast<unsigned long long>(me.b + q);
+        }
+    };
+    if (!me.seam) {
+        for (int q = me.lo; q <= me.hi; ++q)
+            take(q);
+    } else {
+        for (int q = me.hi; q < me.ng; ++q)
+            take(q);
+        for (int q = 0; q <= me.lo; ++q)
+            take(q);
+    }
+}
+
+__global__ void __launch_bounds__(32 * kSumWarps) checksum_kernel(TraceArgs A, int view0, int nviews,
+                                                                  int n_rings, uint32_t* counts,
+                                                                  unsigned long long* sums) {
+    extern __shared__ __align__(16) uint32_t smem[];
+    RingRow* s_rings = reinterpret_cast<RingRow*>(smem);
+    for (int k = threadIdx.x; k <= n_rings; k += blockDim.x)
+        s_rings[k] = A.rings[k];
+    __shared__ uint16_t s_fl[kSumWarps][kSumFlagged];
+    __shared__ uint16_t s_fp[kSumWarps][kSumFlagged][kSumPartners];
+    __shared__ int8_t s_np[kSumWarps][kSumFlagged];
+    __syncthreads();
+    const int warp = int(threadIdx.x) >> 5, lane = int(threadIdx.x) & 31;
+    const int line = int(blockIdx.x) * kSumWarps + warp;
+    if (line >= A.lines)
+        return;
+    const uint32_t r0 = __ldg(A.off + line), r1 = __ldg(A.off + line + 1);
+    const int n = int(r1 - r0);
+    const uint32_t kmask = (kSliceMask << kSliceShift) | kRingMask;
+    // the line's flagged records, in record order
+    int nfl = 0;
+    for (int i0 = 0; i0 < n; i0 += 32) {
+        const int i = i0 + lane;
+        const bool f = i < n && (__ldg(A.key + r0 + i) & kFlagBit) != 0;
+        const unsigned bal = __ballot_sync(0xFFFFFFFFu, f);
+        const int at = nfl + __popc(bal & ((1u << lane) - 1u));
+        if (f && at < kSumFlagged)
+            s_fl[warp][at] = uint16_t(i);
+        nfl += __popc(bal);
+    }
+    const bool cached = nfl <= kSumFlagged;
+    if (cached) {
+        for (int k = lane; k < nfl; k += 32) {
+            const int i = s_fl[warp][k];
+            const uint32_t bk = __ldg(A.key + r0 + i) & kmask;
+            int np = 0;
+            for (int j = i - 1; j >= 0 && np <= kSumPartners; --j)
+                if ((__ldg(A.key + r0 + j) & kmask) == bk) {
+                    if (np < kSumPartners)
+                        s_fp[warp][k][np] = uint16_t(j);
+                    ++np;
+                }
+            s_np[warp][k] = int8_t(np > kSumPartners ? -1 : np);
+        }
+    }
+    __syncwarp();
+    for (int j = 0; j < nviews; ++j) {
+        const double theta = __ldg(A.theta + view0 + j);
+        unsigned long long c = 0, s = 0;
+        for (int i = lane; i < n; i += 32) {
+            if (__ldg(A.key + r0 + i) & kFlagBit) {
+                if (!cached)
+                    flagged_count_sum(A, s_rings, r0, i, theta, nullptr, -1, c, s);
+                continue;
+            }
+            const RecRot o = rot_record(A, s_rings, r0 + i, theta);
+            range_count_sum(o.b, o.lo, o.hi, o.seam, o.ng, c, s);
+        }
+        if (cached)
+            for (int k = lane; k < nfl; k += 32)
+                flagged_count_sum(A, s_rings, r0, s_fl[warp][k], theta, s_fp[warp][k], s_np[warp][k], c, s);
+        for (int o = 16; o > 0; o >>= 1) {
+            c += __shfl_xor_sync(0xFFFFFFFFu, c, o);
+            s += __shfl_xor_sync(0xFFFFFFFFu, s, o);
+        }
+        if (lane == 0) {
+            const size_t k = size_t(j) * A.lines + line;
+            counts[k] = uint32_t(c);
+            sums[k] = s;
+        }
+    }
+}
+
+void launch_checksums(const TraceArgs& A, int view0, int nviews, int n_rings, int max_recs,
+                      uint32_t* counts, unsigned long long* sums, cudaStream_t st) {
+    if (nviews <= 0 || A.lines <= 0)
+        return;
+    (void)max_recs;
+    const size_t sm = sizeof(RingRow) * size_t(n_rings + 1);
+    UB_CUDA(cudaFuncSetAttribute(checksum_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm)));
+    checksum_kernel<<<unsigned((A.lines + kSumWarps - 1) / kSumWarps), 32 * kSumWarps, sm, st>>>(
+        A, view0, nviews, n_rings, counts, sums);
+    check_launch();
+}
+
 template <int NT>
 __global__ void __launch_bounds__(NT) trace_dump_kernel(TraceArgs A, uint32_t unit0, int max_recs,
                                                         const uint32_t* __restrict__ pos,
@@ -1016,31 +1174,70 @@ __device__ __forceinline__ uint32_t cg_inverse(int row, int col, int n) {
 }
 
 // out[(p*slices + s)*n*n + pixel]; field element (p, cell) at cell*cs + p*ps
-__global__ void perm_resample_kernel(const float* __restrict__ field, uint64_t cps, int slices,
-                                     int S, uint64_t cs, uint64_t ps, int n,
-                                     float* __restrict__ out) {
-    const uint64_t npx = uint64_t(n) * n;
-    const uint64_t total = npx * slices * S;
-    for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < total;
-         i += uint64_t(gridDim.x) * blockDim.x) {
-        const uint64_t px = i % npx;
-        const uint64_t sp = i / npx;
-        const int s = int(sp % slices), p = int(sp / slices);
-        const int row = int(px / n), col = int(px % n);
-        const uint64_t cell = uint64_t(s) * cps + cg_inverse(row, col, n);
-        out[i] = field[cell * cs + uint64_t(p) * ps];
+// One output plane (slice s of problem p) per blockIdx.y, four consecutive
+// output pixels per thread (npix is even, so a plane holds a multiple of 4
+// pixels): 32-bit index math, one float4 streaming store, the map read as a
+// uint4. PERM: the reference permutation inverted per pixel (cg_inverse);
+// otherwise the precomputed bin-point map (0xFFFFFFFF = outside the disc).
+template <bool PERM, bool VEC>
+__global__ void __launch_bounds__(256) resample_kernel(const float* __restrict__ field, uint64_t cps,
+                                                       int slices, int planes, uint64_t cs, uint64_t ps,
+                                                       const uint32_t* __restrict__ map, int n,
+                                                       float* __restrict__ out) {
+    const uint32_t npx = uint32_t(n) * uint32_t(n);
+    const uint32_t q = (blockIdx.x * blockDim.x + threadIdx.x) * 4u;
+    if (q >= npx)
+        return;
+    uint32_t m[4];
+    if constexpr (PERM) {
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const uint32_t px = q + uint32_t(k);
+            m[k] = cg_inverse(int(px / uint32_t(n)), int(px % uint32_t(n)), n);
+        }
+    } else {
+        const uint4 mm = __ldg(reinterpret_cast<const uint4*>(map + q));
+        m[0] = mm.x, m[1] = mm.y, m[2] = mm.z, m[3] = mm.w;
     }
+    for (int pl = int(blockIdx.y); pl < planes; pl += int(gridDim.y)) {
+        const int s = pl % slices, p = pl / slices;
+        const float* f = field + uint64_t(s) * cps * cs + uint64_t(p) * ps;
+        float v[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+            v[k] = (!PERM && m[k] == 0xFFFFFFFFu) ? 0.f : __ldg(f + uint64_t(m[k]) * cs);
+        float* o = out + uint64_t(pl) * npx + q;
+        if constexpr (VEC) {
+            __stcs(reinterpret_cast<float4*>(o), make_float4(v[0], v[1], v[2], v[3]));
+        } else {
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+                __stcs(o + k, v[k]);
+        }
+    }
+}
+
+template <bool PERM>
+static void resample_launch(const float* field, uint64_t cps, int slices, int S, int Sp,
+                            const uint32_t* map, int n, float* out, cudaStream_t st) {
+    // Sp > 0: interleaved [cells][Sp]; Sp <= 0: problem-major [S][cells]
+    const uint64_t cells = cps * slices;
+    const uint64_t cs = Sp > 0 ? uint64_t(Sp) : 1, ps = Sp > 0 ? 1 : cells;
+    const int planes = slices * S;
+    const uint32_t npx = uint32_t(n) * uint32_t(n);
+    const dim3 grid(unsigned((npx / 4 + 255) / 256), unsigned(std::min(planes, 65535)));
+    if ((reinterpret_cast<uintptr_t>(out) & 15) == 0)
+        resample_kernel<PERM, true><<<grid, 256, 0, st>>>(field, cps, slices, planes, cs, ps, map, n, out);
+    else
+        resample_kernel<PERM, false><<<grid, 256, 0, st>>>(field, cps, slices, planes, cs, ps, map, n, out);
+    check_launch();
 }
 
 void launch_perm_resample(const float* field, uint64_t cps, int slices, int S, int Sp, int n,
                           float* out, cudaStream_t st) {
-    const uint64_t total = uint64_t(n) * n * slices * S;
-    // Sp > 0: interleaved [cells][Sp]; Sp <= 0: problem-major [S][cells]
-    const uint64_t cells = cps * slices;
-    const uint64_t cs = Sp > 0 ? uint64_t(Sp) : 1, ps = Sp > 0 ? 1 : cells;
-    perm_resample_kernel<<<unsigned(std::min<uint64_t>((total + 255) / 256, 148 * 32)), 256, 0,
-                           st>>>(field, cps, slices, S, cs, ps, n, out);
-    check_launch();
+    if (uint64_t(n) * n * slices * S == 0)
+        return;
+    resample_launch<true>(field, cps, slices, S, Sp, nullptr, n, out, st);
 }
 
 // bin_point (tests/oracles.hpp:36-58) at pixel centres for any ring law
@@ -1073,30 +1270,11 @@ void launch_bin_map(const DevGrid& g, int npix, uint32_t* map, cudaStream_t st) 
     check_launch();
 }
 
-__global__ void map_resample_kernel(const float* __restrict__ field, uint64_t cps, int slices,
-                                    int S, uint64_t cs, uint64_t ps,
-                                    const uint32_t* __restrict__ map, int npix,
-                                    float* __restrict__ out) {
-    const uint64_t npx = uint64_t(npix) * npix;
-    const uint64_t total = npx * slices * S;
-    for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < total;
-         i += uint64_t(gridDim.x) * blockDim.x) {
-        const uint64_t px = i % npx;
-        const uint64_t sp = i / npx;
-        const int s = int(sp % slices), p = int(sp / slices);
-        const uint32_t m = map[px];
-        out[i] = m == 0xFFFFFFFFu ? 0.f : field[(uint64_t(s) * cps + m) * cs + uint64_t(p) * ps];
-    }
-}
-
 void launch_map_resample(const float* field, uint64_t cps, int slices, int S, int Sp,
                          const uint32_t* map, int npix, float* out, cudaStream_t st) {
-    const uint64_t total = uint64_t(npix) * npix * slices * S;
-    const uint64_t cells = cps * slices;
-    const uint64_t cs = Sp > 0 ? uint64_t(Sp) : 1, ps = Sp > 0 ? 1 : cells;
-    map_resample_kernel<<<unsigned(std::min<uint64_t>((total + 255) / 256, 148 * 32)), 256, 0,
-                          st>>>(field, cps, slices, S, cs, ps, map, npix, out);
-    check_launch();
+    if (uint64_t(npix) * npix * slices * S == 0)
+        return;
+    resample_launch<false>(field, cps, slices, S, Sp, map, npix, out, st);
 }
 
 __global__ void cg_map_kernel(int n, uint32_t* out) {

@@ -45,6 +45,10 @@ void launch_trace_one(const TraceArgs& A, int line, double theta, int max_recs, 
                       uint32_t* out, uint32_t* count, cudaStream_t st);
 void launch_trace_counts(const TraceArgs& A, int views, int max_recs, uint32_t* cells,
                          cudaStream_t st);
+// rotated reuse: |active| and the u64 sum of the active cells of every line
+// of views [view0, view0 + nviews)
+void launch_checksums(const TraceArgs& A, int view0, int nviews, int n_rings, int max_recs,
+                      uint32_t* counts, unsigned long long* sums, cudaStream_t st);
 void launch_trace_dump(const TraceArgs& A, uint32_t unit0, uint32_t units, int max_recs,
                        int max_cells, const uint32_t* pos, uint32_t* out, cudaStream_t st);
 void launch_crossed(const TraceArgs& A, int views, int max_recs, int max_cells, uint8_t* crossed,

@@ -102,7 +102,8 @@ class _Info(C.Structure):
     _fields_ = [("lines", C.c_int32), ("views", C.c_int32), ("n_rings", C.c_int32), ("n_slices", C.c_int32),
                 ("records", C.c_uint64), ("cells_per_slice", C.c_uint64), ("cell_count", C.c_uint64),
                 ("cache_bytes", C.c_uint64), ("max_line_records", C.c_int32), ("max_line_cells", C.c_int32),
-                ("cells_per_sweep", C.c_uint64), ("chords_per_sweep", C.c_uint64), ("levels", C.c_int32)]
+                ("cells_per_sweep", C.c_uint64), ("chords_per_sweep", C.c_uint64), ("levels", C.c_int32),
+                ("generator_ms", C.c_double)]
 
 
 EXPORTS = [
@@ -110,6 +111,7 @@ EXPORTS = [
     "uscg_ctx_set_stream", "uscg_ctx_synchronize", "uscg_first_view_rays", "uscg_tracer_create",
     "uscg_tracer_create_from_rays", "uscg_tracer_import_cache", "uscg_tracer_destroy",
     "uscg_tracer_get_info", "uscg_tracer_export_cache", "uscg_trace_line", "uscg_trace_counts",
+    "uscg_trace_checksums",
     "uscg_tracer_build_schedule", "uscg_problem_stride", "uscg_project", "uscg_reconstruct",
     "uscg_resample", "uscg_uspg_to_cg_map", "uscg_diag_math", "uscg_schedule_build",
 ]
@@ -151,6 +153,7 @@ def load(build_if_missing: bool = True):
     L.uscg_tracer_export_cache.argtypes = [vp, _u32p, _dp, _dp, _u16p, _u16p]
     L.uscg_trace_line.argtypes = [vp, C.c_int32, C.c_double, _u32p, C.c_int64, C.POINTER(C.c_int64)]
     L.uscg_trace_counts.argtypes = [vp, _u32p]
+    L.uscg_trace_checksums.argtypes = [vp, C.c_int32, C.c_int32, vp, vp, C.c_uint32]
     L.uscg_tracer_build_schedule.argtypes = [vp]
     L.uscg_problem_stride.argtypes = [C.c_int32]
     L.uscg_problem_stride.restype = C.c_int32
@@ -493,6 +496,16 @@ class Tracer:
         out = np.zeros(inf["views"] * inf["lines"], np.uint32)
         _check(load().uscg_trace_counts(self.h, out.ctypes.data_as(_u32p)))
         return out.reshape(inf["views"], inf["lines"])
+
+    def trace_checksums(self, view0: int = 0, nviews: Optional[int] = None):
+        """Rotated reuse: (|active|, sum of active cell indices) of every line of
+        views [view0, view0 + nviews), each shaped (nviews, lines)."""
+        inf = self.info()
+        nviews = inf["views"] - view0 if nviews is None else nviews
+        counts = np.zeros(nviews * inf["lines"], np.uint32)
+        sums = np.zeros(nviews * inf["lines"], np.uint64)
+        _check(load().uscg_trace_checksums(self.h, int(view0), int(nviews), counts.ctypes.data, sums.ctypes.data, 0))
+        return counts.reshape(nviews, inf["lines"]), sums.reshape(nviews, inf["lines"])
 
     def build_schedule(self) -> int:
         _check(load().uscg_tracer_build_schedule(self.h))

@@ -136,6 +136,46 @@ def test_trace_line_arbitrary_angles(ub, ref):
         assert np.array_equal(tr.trace_line(line, 360.0), tr.trace_line(line, 0.0))
 
 
+@pytest.mark.parametrize("name", ["fan32", "cone16", "fan64q"])
+def test_rotated_reuse_checksums_match_reference(ub, ref, name):
+    """uscg_trace_checksums (C5 rotated reuse): |active| and the index sum of
+    every (view, line), from the records alone, equal the reference's
+    Tracer::trace_line lists; a view sub-range is the same slice."""
+    g = REF_GEOMS[name]
+    rt = ref_tracer(ref, g)
+    spec, geom = ub_spec_geom(ub, g)
+    tr = ub.Tracer.from_cache(spec, cache_from_ref(ub, rt), g["views"])
+    th = thetas(g["views"])
+    counts, sums = tr.trace_checksums()
+    for v in range(g["views"]):
+        for line in range(g["du"] * g["dv"]):
+            want = rt.trace_line(line, th[v])
+            assert counts[v, line] == want.size, (v, line)
+            assert int(sums[v, line]) == int(want.astype(np.uint64).sum()), (v, line)
+    c2, s2 = tr.trace_checksums(view0=1, nviews=2)
+    assert np.array_equal(c2, counts[1:3]) and np.array_equal(s2, sums[1:3])
+    with pytest.raises(ub.InvalidArgument):
+        tr.trace_checksums(view0=g["views"] - 1, nviews=2)
+
+
+@pytest.mark.parametrize("detector,volume", [("arc", False), ("flat", True)])
+def test_rotated_reuse_checksums_generalized(ub, orc, detector, volume):
+    """Same on the M1 sector law (arc fan, flat-panel cone over a volume) against
+    the C restatement's traces, including the dedup-flagged chords."""
+    spec, geom, _, oc = _m1_case(ub, orc, detector, volume=volume, dv=8 if volume else 1, views=12)
+    ocache = ub.FirstViewCache(oc.offsets, oc.records["phi_a"].copy(), oc.records["phi_b"].copy(),
+                               oc.records["slice"].copy(), oc.records["ring"].copy())
+    tr = ub.Tracer.from_cache(spec, ocache, geom.views, geom.view_angles, geom=geom)
+    counts, sums = tr.trace_checksums()
+    th = geom.thetas()
+    lines = tr.info()["lines"]
+    for v in range(len(th)):
+        for line in range(lines):
+            want = oc.trace_line(line, th[v])
+            assert counts[v, line] == want.size, (v, line)
+            assert int(sums[v, line]) == int(np.asarray(want, np.uint64).sum()), (v, line)
+
+
 def test_trace_counts_match_reference(ub, ref):
     g = REF_GEOMS["cone32"]
     rt = ref_tracer(ref, g)
@@ -183,6 +223,11 @@ def test_dedup_of_overlapping_chords(ub, ref):
     assert tr.trace_line(0, 0.0).tolist() == [5, 6, 7, 4, 20, 21]
     # +40: 135/80 -> 6,7,8 ; 90/60 -> 6,7 (both dup) ; 120/140 -> 22,23
     assert tr.trace_line(0, 40.0).tolist() == [6, 7, 8, 22, 23]
+    # the record-level checksum applies the same dedup
+    tr2 = ub.Tracer.from_cache(spec, cache, 2, np.array([0.0, 40.0]))
+    counts, sums = tr2.trace_checksums()
+    assert counts.tolist() == [[6], [5]]
+    assert sums.tolist() == [[5 + 6 + 7 + 4 + 20 + 21], [6 + 7 + 8 + 22 + 23]]
 
 
 # ---------------------------------------------------------------------------

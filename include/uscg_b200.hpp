@@ -152,6 +152,17 @@ public:
         out.resize(std::size_t(n));
     }
 
+    /// Rotated reuse: |active| and the index sum of every line of every view
+    /// ([view][line]), without materialising the index lists.
+    void trace_checksums(std::vector<uint32_t>& counts, std::vector<uint64_t>& sums) const {
+        uscg_tracer_info info{};
+        check(uscg_tracer_get_info(h_.get(), &info));
+        const std::size_t n = std::size_t(info.views) * std::size_t(info.lines);
+        counts.resize(n);
+        sums.resize(n);
+        check(uscg_trace_checksums(h_.get(), 0, info.views, counts.data(), sums.data(), 0));
+    }
+
 private:
     struct Del {
         void operator()(uscg_tracer t) const { uscg_tracer_destroy(t); }

@@ -49,7 +49,8 @@ typedef enum {
 
 enum {
     USCG_DEVICE_POINTERS = 1u,     /* buffers are device memory */
-    USCG_LAYOUT_INTERLEAVED = 2u   /* device-native problem-minor layouts */
+    USCG_LAYOUT_INTERLEAVED = 2u,  /* device-native problem-minor layouts */
+    USCG_MODEL_LENGTH = 4u         /* uscg_project: ForwardModel::LengthWeighted */
 };
 
 typedef struct uscg_ctx_s* uscg_ctx;
@@ -177,8 +178,7 @@ uscg_status uscg_trace_counts(uscg_tracer tracer, uint32_t* cells_out);
  * for views [view0, view0 + nviews) and every line, |active| (counts,
  * nviews*lines u32) and the sum of the active cell indices (sums, u64,
  * independent of emission order), computed from the records without expanding
- * the index lists. USCG_DEVICE_POINTERS: counts/sums are device buffers and
- * the call returns without synchronizing. */
+ * the index lists. USCG_DEVICE_POINTERS: counts/sums are device buffers. */
 uscg_status uscg_trace_checksums(uscg_tracer tracer, int32_t view0, int32_t nviews,
                                  uint32_t* counts, uint64_t* sums, uint32_t flags);
 /* Build the MART dependency schedule now (otherwise built on first use). */
@@ -186,7 +186,11 @@ uscg_status uscg_tracer_build_schedule(uscg_tracer tracer);
 /* stride of the interleaved problem dimension for S problems */
 int32_t uscg_problem_stride(int32_t problems);
 
-/* ---- forward model: generate_projections Binary (proj/src/phantom.cpp:182-211) */
+/* ---- forward model: generate_projections (proj/include/uscg/phantom.hpp:51-52)
+ * Binary (proj/src/phantom.cpp:182-211) by default; USCG_MODEL_LENGTH selects
+ * LengthWeighted (proj/src/phantom.cpp:213-269): the tracer's rays rotated per
+ * view, each chord split at its ring's radial sector boundaries, every piece
+ * weighted by its length (fp64 geometry and sums, fp32 output). */
 uscg_status uscg_project(uscg_tracer tracer, const float* field, int32_t problems, float* proj_out,
                          uint32_t flags);
 

@@ -120,6 +120,7 @@ struct uscg_tracer_s {
     // device
     DevBuf<RingRow> d_rings;
     DevBuf<uint32_t> d_off;
+    DevBuf<double> d_rays;  // first-view rays [src: lines*3][det: lines*3] (length-weighted model)
     DevBuf<double> d_pa, d_pb;
     DevBuf<uint32_t> d_key;
     DevBuf<double> d_theta;
@@ -387,7 +388,7 @@ uscg_tracer_s* build_from_rays(uscg_ctx ctx, const uscg_grid* grid, int lines, c
     fill_grid(t.get(), grid);
     fill_views(t.get(), views, angles);
     t->lines = lines;
-    DevBuf<double> d_rays;
+    DevBuf<double>& d_rays = t->d_rays;
     d_rays.alloc(size_t(lines) * 6);
     UB_CUDA(cudaMemcpyAsync(d_rays.p, src, sizeof(double) * 3 * lines, cudaMemcpyHostToDevice,
                             t->st()));
@@ -784,6 +785,7 @@ uscg_status uscg_trace_checksums(uscg_tracer t, int32_t view0, int32_t nviews, u
         auto* dsum = reinterpret_cast<unsigned long long*>(sums);
         if (flags & USCG_DEVICE_POINTERS) {
             launch_checksums(t->trace_args(), view0, nviews, t->n_rings, t->max_recs, counts, dsum, t->st());
+            UB_CUDA(cudaStreamSynchronize(t->st()));
             return;
         }
         DevBuf<uint32_t> dc;
@@ -905,7 +907,14 @@ uscg_status uscg_project(uscg_tracer t, const float* field, int32_t problems, fl
             t->w_proj.ensure(units * Sp);
             d_out = t->w_proj.p;
         }
-        launch_project(t->trace_args(), t->views, d_field, Sp, t->max_recs, t->max_cells, d_out, st);
+        if (flags & USCG_MODEL_LENGTH) {
+            need(t->d_rays.p != nullptr,
+                 "the length-weighted model needs the tracer's rays (not available for an imported cache)");
+            launch_project_length(t->dev_grid(), t->lines, t->views, t->d_rays.p, t->d_theta.p, d_field, Sp,
+                                  d_out, st);
+        } else {
+            launch_project(t->trace_args(), t->views, d_field, Sp, t->max_recs, t->max_cells, d_out, st);
+        }
         if (!direct_out) {
             if (inter || S == 1) {
                 UB_CUDA(cudaMemcpyAsync(proj_out, d_out, sizeof(float) * units * Sp,

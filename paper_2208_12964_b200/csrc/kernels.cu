@@ -153,9 +153,13 @@ struct RaySources {
     }
 };
 
-template <bool WRITE>
-__device__ uint32_t generate_ray(const DevGrid& g, const double* s, const double* d, double* pa,
-                                 double* pb, uint32_t* key) {
+// Walk one ray through the grid: the sorted, eps-merged crossings of
+// build_sorted_intersections and classify_chord (geometry.cpp:127-227); every
+// kept chord (p, q, slice, ring) goes to on_chord, every rejected one to
+// on_reject. Returns the number of kept chords.
+template <class OnChord, class OnReject>
+__device__ uint32_t walk_ray(const DevGrid& g, const double* s, const double* d, OnChord&& on_chord,
+                             OnReject&& on_reject) {
     RaySources R;
     R.g = &g;
     R.s0 = s[0];
@@ -225,7 +229,6 @@ __device__ uint32_t generate_ray(const DevGrid& g, const double* s, const double
     int np = 0;
     double last_tau = 0;
     double p0 = 0, p1 = 0, p2 = 0;
-    double phi_prev = -1.0;
     uint32_t nrec = 0;
     while (true) {
         double tau;
@@ -270,18 +273,10 @@ __device__ uint32_t generate_ray(const DevGrid& g, const double* s, const double
                 }
             }
             if (keep) {
-                if (WRITE) {
-                    if (phi_prev < 0)
-                        phi_prev = azimuth_deg(p0, p1);
-                    const double phi_q = azimuth_deg(q0, q1);
-                    pa[nrec] = phi_prev;
-                    pb[nrec] = phi_q;
-                    key[nrec] = uint32_t(ring) | (uint32_t(slice) << kSliceShift);
-                    phi_prev = phi_q;
-                }
+                on_chord(p0, p1, p2, q0, q1, q2, slice, ring);
                 ++nrec;
-            } else if (WRITE) {
-                phi_prev = -1.0;
+            } else {
+                on_reject();
             }
         }
         p0 = q0;
@@ -291,6 +286,33 @@ __device__ uint32_t generate_ray(const DevGrid& g, const double* s, const double
         ++np;
     }
     return nrec;
+}
+
+// records of one first-view ray (precompute_first_view, tracer.cpp:38-102):
+// consecutive kept chords share their azimuth at the common point
+template <bool WRITE>
+__device__ uint32_t generate_ray(const DevGrid& g, const double* s, const double* d, double* pa,
+                                 double* pb, uint32_t* key) {
+    double phi_prev = -1.0;
+    uint32_t k = 0;
+    return walk_ray(
+        g, s, d,
+        [&](double p0, double p1, double, double q0, double q1, double, int slice, int ring) {
+            if (WRITE) {
+                if (phi_prev < 0)
+                    phi_prev = azimuth_deg(p0, p1);
+                const double phi_q = azimuth_deg(q0, q1);
+                pa[k] = phi_prev;
+                pb[k] = phi_q;
+                key[k] = uint32_t(ring) | (uint32_t(slice) << kSliceShift);
+                phi_prev = phi_q;
+                ++k;
+            }
+        },
+        [&]() {
+            if (WRITE)
+                phi_prev = -1.0;
+        });
 }
 
 __global__ void generate_count_kernel(DevGrid g, int lines, const double* __restrict__ src,
@@ -311,6 +333,169 @@ __global__ void generate_write_kernel(DevGrid g, int lines, const double* __rest
         return;
     const uint32_t o = off[l];
     generate_ray<true>(g, src + 3 * size_t(l), det + 3 * size_t(l), pa + o, pb + o, key + o);
+}
+
+// =============================================================================
+// K2' length-weighted projector (generate_projections LengthWeighted,
+// phantom.cpp:213-269): per (view, line) the first-view ray rotated by theta
+// (rotate_z_deg, scan.cpp:50-54) is walked through the grid; every chord is
+// cut where it crosses a radial sector boundary of its ring and each piece
+// contributes length x field of the sector of its midpoint. The reference
+// tests every boundary of the ring (O(sectors) per chord); azimuth is monotone
+// along a chord that misses the origin, so only the boundaries between the
+// sectors of its end points (one extra on each side) can cut it, and they are
+// met in order. Rings of at most 16 sectors (where a chord may pass through
+// the origin) test every boundary, as the reference does. fp64 throughout.
+// =============================================================================
+constexpr double kRadPerDeg = 3.141592653589793238462643383279502884 / 180.0;
+
+template <int P>
+struct LengthAcc {
+    const float* field;  // [cells][Sp], this thread's chunk at column col
+    uint32_t Sp, col;
+    double acc[P];
+
+    __device__ void piece(double len, uint32_t cell) {
+        const float* f = field + size_t(cell) * Sp + col;
+#pragma unroll
+        for (int p = 0; p < P; ++p)
+            acc[p] += len * double(__ldg(f + p));
+    }
+};
+
+template <int P>
+__device__ void length_chord(const DevGrid& g, double a0, double a1, double a2, double b0, double b1,
+                             double b2, int slice, int ring, LengthAcc<P>& A) {
+    const double u0 = b0 - a0, u1 = b1 - a1, u2 = b2 - a2;
+    const double chord_len = sqrt(u0 * u0 + u1 * u1 + u2 * u2);
+    const RingRow rr = g.rings[ring];
+    const int ng = int(rr.count);
+    const double step_deg = 360.0 / ng;  // RingLayout::step_deg (grid.cpp:69)
+    const uint32_t base = uint32_t(slice) * g.cells_per_slice + rr.head;
+    auto tau_of = [&](int j, double& tau) {
+        const double psi = j * step_deg * kRadPerDeg;
+        const double ex = cos(psi), ey = sin(psi);
+        const double g0 = ex * a1 - ey * a0;
+        const double g1 = ex * u1 - ey * u0;
+        if (g1 == 0.0)
+            return false;
+        tau = -g0 / g1;
+        return tau > 0.0 && tau < 1.0;
+    };
+    double prev = 0.0;
+    auto emit = [&](double t1) {
+        const double piece = (t1 - prev) * chord_len;
+        if (piece > 0) {
+            const double mid = 0.5 * (prev + t1);
+            const double phi = azimuth_deg(a0 + mid * u0, a1 + mid * u1);
+            int sector = int(phi * rr.inv_step);
+            if (sector >= ng)
+                sector = ng - 1;
+            A.piece(piece, base + uint32_t(sector));
+        }
+        prev = t1;
+    };
+    if (ng <= 16) {
+        double cuts[18];
+        int nc = 0;
+        for (int j = 0; j < ng; ++j) {
+            double tau;
+            if (tau_of(j, tau)) {
+                int k = nc++;
+                while (k > 0 && cuts[k - 1] > tau) {
+                    cuts[k] = cuts[k - 1];
+                    --k;
+                }
+                cuts[k] = tau;
+            }
+        }
+        for (int k = 0; k < nc; ++k)
+            emit(cuts[k]);
+        emit(1.0);
+        return;
+    }
+    int ga = int(azimuth_deg(a0, a1) * rr.inv_step);
+    if (ga >= ng)
+        ga = ng - 1;
+    int gb = int(azimuth_deg(b0, b1) * rr.inv_step);
+    if (gb >= ng)
+        gb = ng - 1;
+    // > 0: azimuth increases along the chord. A radial chord (on a line through
+    // the origin) keeps one azimuth: one piece, in its midpoint's sector (the
+    // reference's cut there is -g0/g1 of two rounding residues, an arbitrary
+    // split of the same length between two sectors)
+    const double cross = a0 * u1 - a1 * u0;
+    if (fabs(cross) <= 1e-12 * sqrt(a0 * a0 + a1 * a1) * sqrt(u0 * u0 + u1 * u1)) {
+        emit(1.0);
+        return;
+    }
+    if (cross > 0) {
+        const int nb = ((gb - ga) % ng + ng) % ng + 2;  // boundaries ga .. gb+1
+        for (int k = 0; k < nb; ++k) {
+            double tau;
+            if (tau_of((ga + k) % ng, tau) && tau > prev)
+                emit(tau);
+        }
+    } else if (cross < 0) {
+        const int nb = ((ga - gb) % ng + ng) % ng + 2;  // boundaries ga+1 down to gb
+        for (int k = 0; k < nb; ++k) {
+            double tau;
+            if (tau_of(((ga + 1 - k) % ng + ng) % ng, tau) && tau > prev)
+                emit(tau);
+        }
+    }
+    emit(1.0);
+}
+
+template <int P>
+__global__ void __launch_bounds__(128) project_length_kernel(DevGrid g, int lines, int views,
+                                                             const double* __restrict__ rays,
+                                                             const double* __restrict__ theta,
+                                                             const float* __restrict__ field, int Sp,
+                                                             float* __restrict__ out) {
+    const long long unit = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (unit >= (long long)lines * views)
+        return;
+    const int v = int(unit / lines), l = int(unit % lines);
+    const int chunk = int(blockIdx.y);
+    // rotate_z_deg (scan.cpp:50-54)
+    const double rad = theta[v] * kRadPerDeg;
+    const double c = cos(rad), sn = sin(rad);
+    const double* s0 = rays + 3 * size_t(l);
+    const double* d0 = rays + 3 * (size_t(lines) + l);
+    const double s[3] = {c * s0[0] - sn * s0[1], sn * s0[0] + c * s0[1], s0[2]};
+    const double d[3] = {c * d0[0] - sn * d0[1], sn * d0[0] + c * d0[1], d0[2]};
+    LengthAcc<P> A{field, uint32_t(Sp), uint32_t(chunk * P), {}};
+#pragma unroll
+    for (int p = 0; p < P; ++p)
+        A.acc[p] = 0.0;
+    walk_ray(
+        g, s, d,
+        [&](double p0, double p1, double p2, double q0, double q1, double q2, int slice, int ring) {
+            length_chord<P>(g, p0, p1, p2, q0, q1, q2, slice, ring, A);
+        },
+        [] {});
+    float* o = out + size_t(unit) * Sp + size_t(chunk) * P;
+#pragma unroll
+    for (int p = 0; p < P; ++p)
+        o[p] = float(A.acc[p]);
+}
+
+void launch_project_length(const DevGrid& g, int lines, int views, const double* rays,
+                           const double* theta, const float* field, int Sp, float* out,
+                           cudaStream_t st) {
+    const long long units = (long long)lines * views;
+    if (units <= 0)
+        return;
+    const int P = stride_chunk(Sp) > 8 ? 8 : stride_chunk(Sp);
+    const dim3 grid(unsigned((units + 127) / 128), unsigned(Sp / P));
+    switch (P) {
+        case 1: project_length_kernel<1><<<grid, 128, 0, st>>>(g, lines, views, rays, theta, field, Sp, out); break;
+        case 2: project_length_kernel<2><<<grid, 128, 0, st>>>(g, lines, views, rays, theta, field, Sp, out); break;
+        case 4: project_length_kernel<4><<<grid, 128, 0, st>>>(g, lines, views, rays, theta, field, Sp, out); break;
+        default: project_length_kernel<8><<<grid, 128, 0, st>>>(g, lines, views, rays, theta, field, Sp, out); break;
+    }
+    check_launch();
 }
 
 void launch_generate_count(const DevGrid& g, int lines, const double* src, const double* det,

@@ -54,6 +54,12 @@ void launch_trace_dump(const TraceArgs& A, uint32_t unit0, uint32_t units, int m
 void launch_crossed(const TraceArgs& A, int views, int max_recs, int max_cells, uint8_t* crossed,
                     cudaStream_t st);
 
+// K2' length-weighted projector (fp64 geometry and sums): rays = first-view
+// [src lines*3][det lines*3] (device), field [cells][Sp], out [views*lines][Sp]
+void launch_project_length(const DevGrid& g, int lines, int views, const double* rays,
+                           const double* theta, const float* field, int Sp, float* out,
+                           cudaStream_t st);
+
 // K2 projector: out [units][Sp]
 void launch_project(const TraceArgs& A, int views, const float* field, int Sp, int max_recs,
                     int max_cells, float* out, cudaStream_t st);

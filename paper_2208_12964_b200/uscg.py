@@ -15,7 +15,7 @@ reference (C++)                       here
 ``SolverConfig`` / ``ReconReport``     :class:`SolverConfig` / :class:`ReconReport`
 ``reconstruct`` solver.hpp:78-79       :func:`reconstruct`
 ``reconstruct_from`` solver.hpp:82-83  :func:`reconstruct_from`
-``generate_projections`` phantom.hpp   :func:`generate_projections` (Binary model)
+``generate_projections`` phantom.hpp   :func:`generate_projections` (Binary, LengthWeighted)
 ``field_to_cartesian`` phantom.hpp:56  :func:`field_to_cartesian`
 ``uspg_to_cg_map`` grid.hpp:84         :func:`uspg_to_cg_map`
 ====================================  ======================================================
@@ -64,6 +64,7 @@ class NoDevice(UscgError):
 
 DEVICE_POINTERS = 1
 LAYOUT_INTERLEAVED = 2
+MODEL_LENGTH = 4  # uscg_project: ForwardModel::LengthWeighted
 
 # ---------------------------------------------------------------------------
 # ctypes structures (include/uscg_b200.h)
@@ -575,25 +576,31 @@ def _validate_field(field_values: np.ndarray, spec: GridSpec):
 
 def generate_projections(field: Field, geom: ScanGeometry, model: str = "binary",
                          tracer: Optional[Tracer] = None) -> ProjectionSet:
-    """generate_projections (phantom.cpp:182-211), Binary model on the device."""
-    if model.lower() != "binary":
-        raise InvalidArgument("only the binary forward model runs on the device path")
+    """generate_projections (phantom.hpp:51-52) on the device: model "binary"
+    (phantom.cpp:182-211) or "length" / "lengthweighted" (phantom.cpp:213-269)."""
+    m = model.lower().replace("_", "").replace("-", "")
+    if m not in ("binary", "length", "lengthweighted"):
+        raise InvalidArgument(f"unknown forward model {model!r}")
     vals = np.ascontiguousarray(field.values, dtype=np.float32).reshape(-1)
     _validate_field(vals, field.spec)
-    if tracer is None:
+    if tracer is None or m != "binary":
+        # the reference's length-weighted model walks the geometry itself and
+        # takes no tracer (phantom.cpp:213-269); here it runs on a tracer's rays
         tracer = Tracer(geom, field.spec, False)
-    out = project_stack(tracer, vals[None, :])
+    out = project_stack(tracer, vals[None, :], model="binary" if m == "binary" else "length")
     return ProjectionSet(geom, out[0].astype(np.float64))
 
 
-def project_stack(tracer: Tracer, fields: np.ndarray) -> np.ndarray:
-    """Binary projections of S independent fields sharing one tracer:
-    fields (S, cell_count) -> (S, views, lines), float32."""
+def project_stack(tracer: Tracer, fields: np.ndarray, model: str = "binary") -> np.ndarray:
+    """Projections of S independent fields sharing one tracer:
+    fields (S, cell_count) -> (S, views, lines), float32. model "binary" or
+    "length" (length-weighted; needs a tracer built from a geometry or rays)."""
     f = np.ascontiguousarray(fields, dtype=np.float32)
     S = f.shape[0]
     inf = tracer.info()
     out = np.zeros((S, inf["views"], inf["lines"]), np.float32)
-    _check(load().uscg_project(tracer.h, _ptr(f), S, _ptr(out), 0))
+    flags = MODEL_LENGTH if model == "length" else 0
+    _check(load().uscg_project(tracer.h, _ptr(f), S, _ptr(out), flags))
     return out
 
 

@@ -235,6 +235,116 @@ def test_dedup_of_overlapping_chords(ub, ref):
 # ---------------------------------------------------------------------------
 
 
+# ---------------------------------------------------------------------------
+# K2' length-weighted projector (phantom.cpp:213-269)
+# ---------------------------------------------------------------------------
+
+
+def _clipped_length(s, d, radius, zhalf=None):
+    """Length of the segment s -> d inside the disc of `radius` (2D) or the
+    cylinder |z| <= zhalf (3D): what a unit field integrates to."""
+    s, d = np.asarray(s, float), np.asarray(d, float)
+    u = d - s
+    lo, hi = 0.0, 1.0
+    a = u[0] ** 2 + u[1] ** 2
+    c = s[0] ** 2 + s[1] ** 2 - radius ** 2
+    if a == 0:
+        if c > 0:
+            return 0.0
+    else:
+        b = 2 * (s[0] * u[0] + s[1] * u[1])
+        disc = b * b - 4 * a * c
+        if disc <= 0:
+            return 0.0
+        r = np.sqrt(disc)
+        lo, hi = max(lo, (-b - r) / (2 * a)), min(hi, (-b + r) / (2 * a))
+    if zhalf is not None:
+        if u[2] == 0:
+            if abs(s[2]) > zhalf:
+                return 0.0
+        else:
+            t0, t1 = (-zhalf - s[2]) / u[2], (zhalf - s[2]) / u[2]
+            lo, hi = max(lo, min(t0, t1)), min(hi, max(t0, t1))
+    return max(0.0, hi - lo) * float(np.linalg.norm(u))
+
+
+def _rot(p, deg):
+    rad = deg * (np.pi / 180.0)
+    c, s = np.cos(rad), np.sin(rad)
+    return np.array([c * p[0] - s * p[1], s * p[0] + c * p[1], p[2]])
+
+
+@pytest.mark.parametrize("name", ["fan16", "cone12", "fan32", "cone16"])
+def test_length_weighted_matches_reference(ub, ref, name):
+    """generate_projections(field, geom, LengthWeighted): the reference library
+    on its own geometries (field values exact in fp32; fp32 output), and the
+    unit field integrates to the in-volume path length (test_phantom.cpp:178-226).
+    Adjudicated: a ray through the origin lies on a sector boundary in some
+    views, where the reference splits its radial chords between the two
+    sectors at -g0/g1 of two rounding residues; there only the path length
+    (the sum over the pieces) is defined, and only it is compared."""
+    g = REF_GEOMS[name]
+    rt = ref_tracer(ref, g)
+    spec, geom = ub_spec_geom(ub, g)
+    rng = np.random.default_rng(3)
+    f = rng.integers(1, 64, spec.cell_count()) / 16.0
+    want = rt.project_length(f)
+    got = ub.generate_projections(ub.Field(spec, f.astype(np.float32)), geom, "length").data.reshape(want.shape)
+    ones = ub.generate_projections(ub.Field(spec, np.ones(spec.cell_count(), np.float32)), geom,
+                                   "length").data.reshape(want.shape)
+    radius = 0.5 * spec.n * spec.ring_spacing
+    zhalf = 0.5 * spec.slices() * spec.slice_height if g["volume"] else None
+    src, det = geom.first_view_rays()
+    th = thetas(g["views"])
+    radial = 0
+    for v in range(g["views"]):
+        for line in range(geom.lines()):
+            s, d = _rot(src[line], th[v]), _rot(det[line], th[v])
+            u = d - s
+            if abs(s[0] * u[1] - s[1] * u[0]) <= 1e-9 * np.hypot(u[0], u[1]):
+                radial += 1  # through the origin: path length only
+            else:
+                assert abs(got[v, line] - want[v, line]) <= 2e-6 * abs(want[v, line]) + 1e-6, (v, line)
+            exp = _clipped_length(s, d, radius, zhalf)
+            if exp == 0:
+                assert ones[v, line] <= 1e-6
+            else:
+                assert abs(ones[v, line] - exp) <= 1e-6 * exp + 1e-6, (v, line, ones[v, line], exp)
+    assert radial <= g["views"] * g["dv"]  # at most the central ray of each detector row
+
+
+def test_length_weighted_linearity_and_stack(ub):
+    """Linear in the field (test_phantom.cpp:228-253), and a stack of fields
+    projects like each field alone."""
+    spec = ub.GridSpec.square_2d(16)
+    geom = ub.ScanGeometry(source=(-8, 0, 0), detector_center=(8, 0, 0), det_u=11, spacing_u=0.2, views=5)
+    rng = np.random.default_rng(13)
+    f1, f2 = rng.uniform(0, 2, spec.cell_count()), rng.uniform(0, 2, spec.cell_count())
+    a, b = 0.75, 1.5
+    p = [ub.generate_projections(ub.Field(spec, x.astype(np.float32)), geom, "length").data
+         for x in (f1, f2, a * f1 + b * f2)]
+    np.testing.assert_allclose(p[2], a * p[0] + b * p[1], rtol=1e-5, atol=1e-6)
+    tr = ub.Tracer(geom, spec, False)
+    stack = rng.uniform(0.1, 2.0, (5, spec.cell_count())).astype(np.float32)
+    got = ub.project_stack(tr, stack, model="length")
+    for i in range(5):
+        one = ub.generate_projections(ub.Field(spec, stack[i]), geom, "length").data
+        np.testing.assert_allclose(got[i].reshape(-1), one.reshape(-1), rtol=1e-6, atol=1e-7)
+
+
+@pytest.mark.parametrize("detector,volume", [("arc", False), ("flat", True)])
+def test_length_weighted_generalized_seams(ub, orc, detector, volume):
+    """M1 sector law (odd sector counts: the reference also cuts at psi + 180,
+    which only splits pieces within one sector) against the C restatement."""
+    spec, geom, tr, oc = _m1_case(ub, orc, detector, volume=volume, dv=6 if volume else 1, du=24, views=8)
+    f = np.random.default_rng(4).integers(1, 64, spec.cell_count()) / 16.0
+    want = oc.project_length(geom.thetas(), f)
+    got = ub.project_stack(tr, f[None, :].astype(np.float32), model="length")[0]
+    np.testing.assert_allclose(got, want, rtol=2e-6, atol=1e-6)
+    with pytest.raises(ub.InvalidArgument):
+        ub.generate_projections(ub.Field(spec, f.astype(np.float32)), geom, "cubic")
+
+
 @pytest.mark.parametrize("name", ["fan128", "cone32", "fan16"])
 def test_project_matches_reference(ub, ref, name):
     g = REF_GEOMS[name]

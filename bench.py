@@ -569,6 +569,17 @@ def main():
     Bp = 4 * U_all + 20 * C + 8 * units + 4 * units * Sp
     projector = {"ms": tp, "updates_per_s": U_all / (tp * 1e-3), "achieved_gbs": Bp / (tp * 1e-3) / 1e9,
                  "algorithmic_bytes": Bp, "bytes_model": "4*U_all + 20*C + 8*(views*lines) + 4*(views*lines)*S_pad"}
+    # length-weighted model (phantom.cpp:213-269) over the whole stack, one call
+    lw0, lw1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    lw0.record(stream)
+    uscg._check(L.uscg_project(tracer.h, uscg.C.c_void_p(field_d.data_ptr()), S, uscg.C.c_void_p(out_d.data_ptr()),
+                               flags | uscg.MODEL_LENGTH))
+    lw1.record(stream)
+    torch.cuda.synchronize()
+    tlw = lw0.elapsed_time(lw1)
+    projector["length_weighted"] = {"ms": tlw, "problems": S, "rays_per_s": units * S / (tlw * 1e-3),
+                                    "model": "fp64 ray walk per (view, line, 8-problem chunk); cuts at the "
+                                             "radial boundaries inside each chord's sector range"}
 
     # ---- e2e through the C ABI with pinned host buffers ----
     e2e = None

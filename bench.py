@@ -358,11 +358,33 @@ def bench_c5(args, rank, world, local):
         resample()
     e1.record(stream)
     torch.cuda.synchronize()
+    res_ms = e0.elapsed_time(e1) / args.steps
+    # (4) volume image-quality scores of the resampled volume against a
+    #     perturbed copy (mae / rmse / ssim per slice, shared ssim range as
+    #     ssim_volume, metrics.cpp:170-199)
+    test_d = img_d * 0.97 + 0.01
+    nsl = sl1 - sl0
+    m_mae, m_rmse, m_ssim = np.zeros(nsl), np.zeros(nsl), np.zeros(nsl)
+    dp = uscg.C.POINTER(uscg.C.c_double)
+
+    def metrics():
+        uscg._check(L.uscg_image_metrics(ctx.h, uscg.C.c_void_p(img_d.data_ptr()),
+                                         uscg.C.c_void_p(test_d.data_ptr()), nsl, npix, npix, 1, -1.0,
+                                         m_mae.ctypes.data_as(dp), m_rmse.ctypes.data_as(dp),
+                                         m_ssim.ctypes.data_as(dp), uscg.DEVICE_POINTERS))
+
+    metrics()
+    torch.cuda.synchronize()
+    e0.record(stream)
+    for _ in range(args.steps):
+        metrics()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    met_ms = e0.elapsed_time(e1) / args.steps
     launches = ub.launch_count() - launches0
     clk = clocks.stop()
-    res_ms = e0.elapsed_time(e1) / args.steps
     px = (sl1 - sl0) * npix * npix
-    g_ms, reuse_ms, res_ms = udist.max_over_ranks([g_ms, reuse_ms, res_ms], device="cuda")
+    g_ms, reuse_ms, res_ms, met_ms = udist.max_over_ranks([g_ms, reuse_ms, res_ms, met_ms], device="cuda")
     rays_all, recs_all = udist.sum_over_ranks([rays_mine, recs], device="cuda")
 
     if rank != 0:
@@ -415,6 +437,10 @@ def bench_c5(args, rank, world, local):
         "resample": {"ms": res_ms, "pixels": px * world, "pixels_per_s": px * world / (res_ms * 1e-3),
                      "roofline": roof(res_bytes, res_ms, "bin_map_kernel + map_resample_kernel",
                                       "8 B per output pixel (SURVEY.md §8(d))")},
+        "metrics": {"ms": met_ms, "slices": nsl * world, "ssim_volume": float(m_ssim.mean()),
+                    "rmse_volume": float(m_rmse.mean()), "pixels_per_s": px * world / (met_ms * 1e-3),
+                    "roofline": roof(res_bytes, met_ms, "moments_kernel + ssim_kernel",
+                                     "8 B per pixel pair read (two fp32 rasters; SURVEY.md §8(f) row 3)")},
         "cpu_baseline": cpu, "e2e": None, "gpu_launches": int(launches), "clocks": clk,
     }
     print(json.dumps(line), flush=True)

@@ -212,6 +212,21 @@ uscg_status uscg_resample(uscg_ctx ctx, const uscg_grid* grid, const float* fiel
 /* uspg_to_cg_map(n) itself (grid.hpp:84), n*n u32, host output. */
 uscg_status uscg_uspg_to_cg_map(uscg_ctx ctx, int32_t n, uint32_t* out);
 
+/* ---- image-quality metrics (proj/src/metrics.cpp) on the device ------------
+ * ref, test: `slices` rasters of rows x cols floats each (row-major, row 0 at
+ * the bottom, as uscg_resample writes them). Per slice (any output may be
+ * NULL): mae / rmse (metrics.cpp:35-60) and ssim (metrics.cpp:105-136: 8x8
+ * windows, stride 1, C1 = (0.01 L)^2, C2 = (0.03 L)^2). L is dynamic_range when
+ * > 0, else the range (max - min, 1 when constant) of each reference slice
+ * (ssim, metrics.cpp:27-31) or, with shared_range = 1, of the whole reference
+ * stack (ssim_volume, metrics.cpp:186-199). mae/rmse/ssim_volume are the means
+ * of the per-slice values. Errors as the reference: empty images, and images
+ * smaller than the 8x8 window when ssim is asked for (invalid argument). */
+uscg_status uscg_image_metrics(uscg_ctx ctx, const float* ref, const float* test, int32_t slices,
+                               int32_t rows, int32_t cols, int32_t shared_range,
+                               double dynamic_range, double* mae_out, double* rmse_out,
+                               double* ssim_out, uint32_t flags);
+
 /* ---- MART dependency schedule (host only) ---------------------------------
  * The schedule the device executors run, from explicit supports: lines in
  * sweep order, support of line u = idx[pos[u] .. pos[u+1]) (cell indices <

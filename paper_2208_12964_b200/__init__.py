@@ -7,14 +7,15 @@ reference library's reconstruction API on top of that ABI.
 from .uscg import (  # noqa: F401
     Context, Detector, DomainError, Field, FirstViewCache, GridMode, GridSpec, InvalidArgument, NoDevice,
     ProjectionSet, ReconReport, ReconResult, ScanGeometry, SolverConfig, Tracer, field_to_cartesian,
-    generate_projections, launch_count, load, problem_stride, project_stack, reconstruct, reconstruct_from,
-    reconstruct_stack, resample_stack, ring_counts_m1, uspg_to_cg_map,
+    generate_projections, image_metrics, launch_count, load, mae, mae_volume, problem_stride, project_stack,
+    reconstruct, reconstruct_from, reconstruct_stack, resample_stack, ring_counts_m1, rmse, rmse_volume, ssim,
+    ssim_volume, uspg_to_cg_map,
 )
 
 __all__ = [
     "Context", "Detector", "DomainError", "Field", "FirstViewCache", "GridMode", "GridSpec", "InvalidArgument",
     "NoDevice", "ProjectionSet", "ReconReport", "ReconResult", "ScanGeometry", "SolverConfig", "Tracer",
-    "field_to_cartesian", "generate_projections", "launch_count", "load", "problem_stride", "project_stack",
-    "reconstruct", "reconstruct_from", "reconstruct_stack", "resample_stack", "ring_counts_m1",
-    "uspg_to_cg_map",
+    "field_to_cartesian", "generate_projections", "image_metrics", "launch_count", "load", "mae", "mae_volume",
+    "problem_stride", "project_stack", "reconstruct", "reconstruct_from", "reconstruct_stack", "resample_stack",
+    "ring_counts_m1", "rmse", "rmse_volume", "ssim", "ssim_volume", "uspg_to_cg_map",
 ]

@@ -16,7 +16,7 @@ LIBDIR = os.path.join(HERE, "lib")
 LIB = os.path.join(LIBDIR, "libuscg_b200.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
-SOURCES = ["api.cu", "kernels.cu", "mart_sweep.cu", "schedule.cpp"]
+SOURCES = ["api.cu", "kernels.cu", "mart_sweep.cu", "metrics.cu", "schedule.cpp"]
 HEADERS = ["internal.cuh", "kernels.h", "schedule.h", "ddmath.cuh"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 # --fmad=false: the fp64 index arithmetic must round exactly like the

@@ -82,12 +82,14 @@ void set_error(const std::string& msg) { g_last_error = msg; }
 using namespace ub;
 
 struct ResampleCache;
+struct MetricsWork;
 
 struct uscg_ctx_s {
     int device = 0;
     cudaStream_t own = nullptr;
     cudaStream_t stream = nullptr;
     ResampleCache* resample = nullptr;  // ring table + bin-point map of the last resample grid
+    MetricsWork* metrics = nullptr;     // uscg_image_metrics scratch (grown, never shrunk)
 };
 
 struct GraphCache {
@@ -181,6 +183,12 @@ struct uscg_tracer_s {
     }
     cudaStream_t st() const { return ctx->stream; }
     uint64_t units() const { return uint64_t(lines) * uint64_t(views); }
+};
+
+// uscg_image_metrics scratch, kept by the context so repeated scoring does
+// not allocate (cudaFree synchronizes the device)
+struct MetricsWork {
+    DevBuf<double> part, mom, c1c2, spart, sout;
 };
 
 // uscg_resample's per-grid state, kept by the context so that repeated calls
@@ -627,9 +635,10 @@ uscg_status uscg_ctx_destroy(uscg_ctx ctx) {
         if (!ctx)
             return;
         cudaSetDevice(ctx->device);
-        if (ctx->resample) {
+        if (ctx->resample || ctx->metrics) {
             cudaDeviceSynchronize();
             delete ctx->resample;
+            delete ctx->metrics;
         }
         if (ctx->own)
             cudaStreamDestroy(ctx->own);
@@ -1321,6 +1330,74 @@ uscg_status uscg_resample(uscg_ctx ctx, const uscg_grid* grid, const float* fiel
             launch_map_resample(fin, t->cps, slices, S, Sp, rc.map.p, npix, fout, st);
         if (!dev)
             UB_CUDA(cudaMemcpyAsync(out, fout, sizeof(float) * out_n, cudaMemcpyDeviceToHost, st));
+        UB_CUDA(cudaStreamSynchronize(st));
+    });
+}
+
+uscg_status uscg_image_metrics(uscg_ctx ctx, const float* ref, const float* test, int32_t slices,
+                               int32_t rows, int32_t cols, int32_t shared_range,
+                               double dynamic_range, double* mae_out, double* rmse_out,
+                               double* ssim_out, uint32_t flags) {
+    return guarded([&] {
+        bind(ctx);
+        need(ref && test, "null image");
+        need(slices >= 1, "volume slice counts differ or are empty");  // metrics.cpp:165
+        need(rows >= 1 && cols >= 1, "empty image");                     // metrics.cpp:16
+        if (ssim_out)
+            need(rows >= 8 && cols >= 8, "image smaller than the 8x8 ssim window");  // metrics.cpp:109
+        const uint64_t px = uint64_t(rows) * uint64_t(cols);
+        const uint64_t n = px * uint64_t(slices);
+        cudaStream_t st = ctx->stream;
+        DevBuf<float> d_ref, d_test;
+        const float* a = ref;
+        const float* b = test;
+        if (!(flags & USCG_DEVICE_POINTERS)) {
+            d_ref.alloc(n);
+            d_test.alloc(n);
+            UB_CUDA(cudaMemcpyAsync(d_ref.p, ref, sizeof(float) * n, cudaMemcpyHostToDevice, st));
+            UB_CUDA(cudaMemcpyAsync(d_test.p, test, sizeof(float) * n, cudaMemcpyHostToDevice, st));
+            a = d_ref.p;
+            b = d_test.p;
+        }
+        if (!ctx->metrics)
+            ctx->metrics = new MetricsWork;
+        MetricsWork& w = *ctx->metrics;
+        w.part.ensure(size_t(slices) * size_t(metrics_blocks(px)) * 4);
+        w.mom.ensure(size_t(slices) * 4);
+        launch_moments(a, b, slices, px, w.part.p, w.mom.p, st);
+        std::vector<double> m(size_t(slices) * 4);
+        UB_CUDA(cudaMemcpyAsync(m.data(), w.mom.p, sizeof(double) * m.size(), cudaMemcpyDeviceToHost, st));
+        UB_CUDA(cudaStreamSynchronize(st));
+        for (int s = 0; s < slices; ++s) {
+            if (mae_out)
+                mae_out[s] = m[4 * s + 2] / double(px);
+            if (rmse_out)
+                rmse_out[s] = std::sqrt(m[4 * s + 3] / double(px));
+        }
+        if (!ssim_out)
+            return;
+        // dynamic range: given, per reference slice, or over the whole stack
+        double lo_all = m[0], hi_all = m[1];
+        for (int s = 1; s < slices; ++s) {
+            lo_all = std::min(lo_all, m[4 * s]);
+            hi_all = std::max(hi_all, m[4 * s + 1]);
+        }
+        std::vector<double> c1c2(size_t(slices) * 2);
+        for (int s = 0; s < slices; ++s) {
+            double L = dynamic_range;
+            if (!(L > 0)) {
+                const double r = shared_range ? hi_all - lo_all : m[4 * s + 1] - m[4 * s];
+                L = r > 0 ? r : 1.0;
+            }
+            c1c2[2 * s] = (0.01 * L) * (0.01 * L);
+            c1c2[2 * s + 1] = (0.03 * L) * (0.03 * L);
+        }
+        w.c1c2.ensure(c1c2.size());
+        w.spart.ensure(size_t(slices) * size_t(ssim_tiles(rows, cols)));
+        w.sout.ensure(size_t(slices));
+        UB_CUDA(cudaMemcpyAsync(w.c1c2.p, c1c2.data(), sizeof(double) * c1c2.size(), cudaMemcpyHostToDevice, st));
+        launch_ssim(a, b, slices, rows, cols, w.c1c2.p, w.spart.p, w.sout.p, st);
+        UB_CUDA(cudaMemcpyAsync(ssim_out, w.sout.p, sizeof(double) * slices, cudaMemcpyDeviceToHost, st));
         UB_CUDA(cudaStreamSynchronize(st));
     });
 }

@@ -125,6 +125,17 @@ void launch_from_interleaved(const float* in, float* out, uint64_t n, int S, int
                              cudaStream_t st);
 void launch_fill(float* p, uint64_t n, float v, cudaStream_t st);
 
+// image-quality metrics (metrics.cu): per slice of `slices` rasters of px pixels
+// out[4*s + {0: min ref, 1: max ref, 2: sum |ref-test|, 3: sum (ref-test)^2}];
+// part: slices * metrics_blocks(px) * 4 doubles
+int metrics_blocks(uint64_t px);
+void launch_moments(const float* ref, const float* test, int slices, uint64_t px, double* part,
+                    double* out, cudaStream_t st);
+// mean SSIM per slice; c1c2 [slices][2]; part: slices * ssim_tiles(rows, cols) doubles
+int ssim_tiles(int rows, int cols);
+void launch_ssim(const float* ref, const float* test, int slices, int rows, int cols,
+                 const double* c1c2, double* part, double* out, cudaStream_t st);
+
 // K4 resample
 void launch_perm_resample(const float* field, uint64_t cells_per_slice, int slices, int S, int Sp,
                           int n, float* out, cudaStream_t st);

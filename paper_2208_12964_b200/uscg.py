@@ -114,7 +114,7 @@ EXPORTS = [
     "uscg_tracer_get_info", "uscg_tracer_export_cache", "uscg_trace_line", "uscg_trace_counts",
     "uscg_trace_checksums",
     "uscg_tracer_build_schedule", "uscg_problem_stride", "uscg_project", "uscg_reconstruct",
-    "uscg_resample", "uscg_uspg_to_cg_map", "uscg_diag_math", "uscg_schedule_build",
+    "uscg_resample", "uscg_uspg_to_cg_map", "uscg_diag_math", "uscg_schedule_build", "uscg_image_metrics",
 ]
 
 _lib = None
@@ -163,6 +163,8 @@ def load(build_if_missing: bool = True):
                                    C.c_uint32]
     L.uscg_resample.argtypes = [vp, C.POINTER(_Grid), vp, C.c_int32, C.c_int32, vp, C.c_uint32]
     L.uscg_uspg_to_cg_map.argtypes = [vp, C.c_int32, _u32p]
+    L.uscg_image_metrics.argtypes = [vp, vp, vp, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_double, _dp, _dp,
+                                     _dp, C.c_uint32]
     L.uscg_diag_math.argtypes = [vp, C.c_int32, _dp, _dp, _dp]
     L.uscg_schedule_build.argtypes = [C.c_uint32, C.c_uint32, C.c_uint32, _u32p, _u32p, C.c_uint64, _u32p, _u32p,
                                       _u32p, _u32p, _u32p, C.POINTER(C.c_uint64), _u32p]
@@ -682,6 +684,60 @@ def resample_stack(spec: GridSpec, fields: np.ndarray, npix: int, ctx: Optional[
     g, keep = spec._c()
     _check(load().uscg_resample(ctx.h, C.byref(g), _ptr(f), S, npix, _ptr(out), 0))
     return out
+
+
+def image_metrics(ref, test, shared_range: bool = False, dynamic_range: float = -1.0, ssim: bool = True,
+                  ctx: Optional[Context] = None) -> dict:
+    """Per-slice mae / rmse / ssim of two (slices, rows, cols) raster stacks on
+    the device (metrics.cpp:35-60,105-136); shared_range: one ssim dynamic range
+    from the whole reference stack (ssim_volume, metrics.cpp:186-199)."""
+    ctx = ctx or default_context()
+    a = np.ascontiguousarray(ref, dtype=np.float32)
+    b = np.ascontiguousarray(test, dtype=np.float32)
+    if a.ndim == 2:
+        a, b = a[None], b[None]
+    if a.shape != b.shape:
+        raise InvalidArgument("image shapes differ")
+    S, rows, cols = a.shape
+    mae_o, rmse_o, ssim_o = np.zeros(S), np.zeros(S), np.zeros(S)
+    _check(load().uscg_image_metrics(ctx.h, _ptr(a), _ptr(b), S, rows, cols, int(bool(shared_range)),
+                                     float(dynamic_range), mae_o.ctypes.data_as(_dp), rmse_o.ctypes.data_as(_dp),
+                                     ssim_o.ctypes.data_as(_dp) if ssim else None, 0))
+    out = {"mae": mae_o, "rmse": rmse_o}
+    if ssim:
+        out["ssim"] = ssim_o
+    return out
+
+
+def rmse(ref, test) -> float:
+    """uscg::rmse(Image, Image) (metrics.cpp:42-50,57-60)."""
+    return float(image_metrics(ref, test, ssim=False)["rmse"][0])
+
+
+def mae(ref, test) -> float:
+    """uscg::mae(Image, Image) (metrics.cpp:35-41,52-55)."""
+    return float(image_metrics(ref, test, ssim=False)["mae"][0])
+
+
+def ssim(ref, test, dynamic_range: float = -1.0) -> float:
+    """uscg::ssim (metrics.cpp:105-136): 8x8 windows, stride 1."""
+    return float(image_metrics(ref, test, dynamic_range=dynamic_range)["ssim"][0])
+
+
+def rmse_volume(ref, test) -> float:
+    """uscg::rmse_volume (metrics.cpp:178-184): mean of per-slice rmse."""
+    return float(image_metrics(ref, test, ssim=False)["rmse"].mean())
+
+
+def mae_volume(ref, test) -> float:
+    """uscg::mae_volume (metrics.cpp:170-176)."""
+    return float(image_metrics(ref, test, ssim=False)["mae"].mean())
+
+
+def ssim_volume(ref, test) -> float:
+    """uscg::ssim_volume (metrics.cpp:186-199): per-slice ssim with the dynamic
+    range of the whole reference stack, averaged."""
+    return float(image_metrics(ref, test, shared_range=True)["ssim"].mean())
 
 
 def uspg_to_cg_map(n: int, ctx: Optional[Context] = None) -> np.ndarray:

@@ -658,3 +658,52 @@ def test_resample_stack_layouts(ub):
     out = ub.resample_stack(spec, f, 32)
     for p in range(5):
         assert np.array_equal(out[p], ub.field_to_cartesian(ub.Field(spec, f[p])))
+
+
+# ---------------------------------------------------------------------------
+# image-quality metrics on the device (metrics.cpp)
+# ---------------------------------------------------------------------------
+
+
+@pytest.mark.parametrize("shape", [(8, 8), (37, 53), (100, 9), (64, 64)])
+def test_image_metrics_match_reference(ub, ref, shape):
+    """rmse / mae / ssim of one raster pair against the reference library
+    (values exact in fp32; the window sums run in another fp64 order)."""
+    rng = np.random.default_rng(shape[0] * 131 + shape[1])
+    a = rng.integers(0, 64, shape) / 64.0
+    b = np.clip(a + rng.normal(0, 0.05, shape), 0, None).astype(np.float32).astype(np.float64)
+    m = ub.image_metrics(a, b)
+    assert abs(m["rmse"][0] - ref.rmse(a, b)) <= 1e-12 * max(1.0, ref.rmse(a, b))
+    assert abs(m["mae"][0] - np.abs(a - b).mean()) <= 1e-12
+    assert abs(m["ssim"][0] - ref.ssim(a, b)) <= 1e-12
+    assert abs(ub.ssim(a, b, 2.5) - ref.ssim(a, b, 2.5)) <= 1e-12
+    # constant reference: the dynamic range falls back to 1 (metrics.cpp:27-31)
+    c = np.full(shape, 0.5)
+    assert abs(ub.ssim(c, b) - ref.ssim(c, b)) <= 1e-12
+
+
+def test_image_metrics_volume_scores(ub, ref):
+    """ssim_volume shares the reference stack's range (metrics.cpp:186-199);
+    the volume scores are means of the per-slice values."""
+    rng = np.random.default_rng(21)
+    a = rng.integers(0, 256, (5, 40, 33)) / 64.0
+    a[2] *= 0.25  # slices with different ranges
+    b = np.clip(a + rng.normal(0, 0.1, a.shape), 0, None).astype(np.float32).astype(np.float64)
+    L = a.max() - a.min()
+    want = np.mean([ref.ssim(a[s], b[s], L) for s in range(5)])
+    assert abs(ub.ssim_volume(a, b) - want) <= 1e-12
+    per = ub.image_metrics(a, b)
+    for s in range(5):
+        assert abs(per["ssim"][s] - ref.ssim(a[s], b[s])) <= 1e-12
+    assert abs(ub.rmse_volume(a, b) - np.mean([ref.rmse(a[s], b[s]) for s in range(5)])) <= 1e-12
+    assert abs(ub.mae_volume(a, b) - np.mean(np.abs(a - b).mean(axis=(1, 2)))) <= 1e-12
+
+
+def test_image_metrics_errors(ub):
+    with pytest.raises(ub.InvalidArgument):
+        ub.ssim(np.ones((7, 20)), np.ones((7, 20)))  # smaller than the 8x8 window
+    assert ub.rmse(np.ones((7, 20)), np.zeros((7, 20))) == 1.0
+    with pytest.raises(ub.InvalidArgument):
+        ub.image_metrics(np.ones((8, 8)), np.ones((8, 9)))
+    with pytest.raises(ub.InvalidArgument):
+        ub.image_metrics(np.ones((0, 8, 8)), np.ones((0, 8, 8)))

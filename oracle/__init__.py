@@ -298,6 +298,12 @@ class Ref:
         L.ref_trace_chord.restype = C.c_int64
         L.ref_project_binary.argtypes = [C.c_void_p, _dp, _dp]
         L.ref_project_length.argtypes = [C.c_void_p, _dp, _dp]
+        _sp = C.POINTER(C.c_char_p)
+        L.ref_write_field.argtypes = [C.c_char_p, C.c_int, C.c_double, C.c_double, C.c_int, _dp, _sp, _sp, C.c_int]
+        L.ref_write_projections.argtypes = [C.c_char_p, C.c_int, C.c_int, C.c_int, C.c_double, C.c_double, _dp, _dp,
+                                            _dp, _sp, _sp, C.c_int]
+        L.ref_write_pgm16.argtypes = [C.c_char_p, C.c_int, C.c_int, _dp, C.c_double, C.c_double, _sp, _sp, C.c_int]
+        L.ref_read_pgm16.argtypes = [C.c_char_p, C.POINTER(C.c_int), C.POINTER(C.c_int), _dp, C.c_longlong]
         L.ref_reconstruct.argtypes = [C.c_void_p, _dp, _dp, C.c_double, C.c_double, C.c_int, C.c_double,
                                       C.c_double, _dp, _dp, _dp, _u8p]
         L.ref_mart_update_line.argtypes = [C.c_int, _dp, C.c_int64, _u32p, C.c_int64, C.c_double,
@@ -351,6 +357,43 @@ class Ref:
     def ssim(self, a, b, dynamic_range=-1.0):
         a = np.ascontiguousarray(a, float); b = np.ascontiguousarray(b, float)
         return self.L.ref_ssim(a.shape[0], a.shape[1], _ptr(a, _dp), _ptr(b, _dp), dynamic_range)
+
+
+def _kv(side):
+    """parallel (keys, values) C string arrays of a dict / list of pairs"""
+    items = list(side.items()) if isinstance(side, dict) else list(side or [])
+    keys = (C.c_char_p * max(1, len(items)))(*[k.encode() for k, _ in items])
+    vals = (C.c_char_p * max(1, len(items)))(*[str(v).encode() for _, v in items])
+    return keys, vals, len(items)
+
+
+class RefIO:
+    """The reference's file writers / PGM reader (proj/src/io.cpp) through the shim."""
+
+    def __init__(self, ref: "Ref"):
+        self.ref = ref
+
+    def write_field(self, path, n, r, h, volume, values, side=None):
+        v = np.ascontiguousarray(values, float)
+        self.ref.check(self.ref.L.ref_write_field(str(path).encode(), n, r, h, int(volume), _ptr(v, _dp), *_kv(side)))
+
+    def write_projections(self, path, views, det_u, det_v, su, sv, src, ctr, data, side=None):
+        d = np.ascontiguousarray(data, float)
+        s3 = np.ascontiguousarray(src, float)
+        c3 = np.ascontiguousarray(ctr, float)
+        self.ref.check(self.ref.L.ref_write_projections(str(path).encode(), views, det_u, det_v, su, sv, _ptr(s3, _dp),
+                                                        _ptr(c3, _dp), _ptr(d, _dp), *_kv(side)))
+
+    def write_pgm16(self, path, img, wmin, wmax, side=None):
+        im = np.ascontiguousarray(img, float)
+        self.ref.check(self.ref.L.ref_write_pgm16(str(path).encode(), im.shape[0], im.shape[1], _ptr(im, _dp), wmin,
+                                                  wmax, *_kv(side)))
+
+    def read_pgm16(self, path, cap=1 << 24):
+        out = np.zeros(cap)
+        rows, cols = C.c_int(), C.c_int()
+        self.ref.check(self.ref.L.ref_read_pgm16(str(path).encode(), C.byref(rows), C.byref(cols), _ptr(out, _dp), cap))
+        return out[: rows.value * cols.value].reshape(rows.value, cols.value)
 
 
 class RefTracer:

@@ -31,6 +31,7 @@
 #include <vector>
 
 #include "uscg/grid.hpp"
+#include "uscg/io.hpp"
 #include "uscg/metrics.hpp"
 #include "uscg/phantom.hpp"
 #include "uscg/solver.hpp"
@@ -269,6 +270,61 @@ int ref_phantom(int n, double r, double h, int volume, int kind, double* out) {
         ph.n = n;
         PhantomResult res = generate_phantom(ph, spec);
         std::memcpy(out, res.field.values.data(), res.field.values.size() * sizeof(double));
+    });
+}
+
+// ---- file formats (proj/src/io.cpp): the reference's own writers, for the
+// byte-for-byte format tests of include/uscg_b200_io.hpp. Sidecar entries come
+// in as parallel key / value string arrays.
+static Sidecar sidecar_of(const char* const* keys, const char* const* vals, int nkv) {
+    Sidecar s;
+    for (int i = 0; i < nkv; ++i)
+        s.set(keys[i], std::string(vals[i]));
+    return s;
+}
+
+int ref_write_field(const char* path, int n, double r, double h, int volume, const double* values,
+                    const char* const* keys, const char* const* vals, int nkv) {
+    return guarded([&] {
+        Field f{make_spec(n, r, h, volume), {}};
+        f.values.assign(values, values + f.spec.cell_count());
+        write_field(path, f, sidecar_of(keys, vals, nkv));
+    });
+}
+
+int ref_write_projections(const char* path, int views, int det_u, int det_v, double su, double sv,
+                          const double* src, const double* ctr, const double* data,
+                          const char* const* keys, const char* const* vals, int nkv) {
+    return guarded([&] {
+        ProjectionSet p;
+        p.geometry.views = views;
+        p.geometry.det_u = det_u;
+        p.geometry.det_v = det_v;
+        p.geometry.spacing_u = su;
+        p.geometry.spacing_v = sv;
+        p.geometry.source = {src[0], src[1], src[2]};
+        p.geometry.detector_center = {ctr[0], ctr[1], ctr[2]};
+        p.data.assign(data, data + std::size_t(views) * det_u * det_v);
+        write_projections(path, p, sidecar_of(keys, vals, nkv));
+    });
+}
+
+int ref_write_pgm16(const char* path, int rows, int cols, const double* v, double wmin, double wmax,
+                    const char* const* keys, const char* const* vals, int nkv) {
+    return guarded([&] {
+        Image im{rows, cols, std::vector<double>(v, v + std::size_t(rows) * cols)};
+        write_pgm16(path, im, wmin, wmax, sidecar_of(keys, vals, nkv));
+    });
+}
+
+// rows, cols out; values (row 0 at the bottom, through the sidecar window) into out (cap doubles)
+int ref_read_pgm16(const char* path, int* rows, int* cols, double* out, long long cap) {
+    return guarded([&] {
+        auto [im, side] = read_pgm16(path);
+        *rows = im.rows;
+        *cols = im.cols;
+        if (static_cast<long long>(im.v.size()) <= cap)
+            std::memcpy(out, im.v.data(), im.v.size() * sizeof(double));
     });
 }
 

@@ -14,6 +14,8 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIBDIR = os.path.join(HERE, "lib")
 LIB = os.path.join(LIBDIR, "libuscg_b200.so")
+CLI = os.path.join(LIBDIR, "uscg_b200")  # the reference's CLI pipeline over the C ABI
+CLI_SRC = os.path.join(HERE, "cli", "uscg_cli.cpp")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
 SOURCES = ["api.cu", "kernels.cu", "mart_sweep.cu", "metrics.cu", "schedule.cpp"]
@@ -35,8 +37,30 @@ def _stale() -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
+def _cli_stale() -> bool:
+    if not os.path.exists(CLI):
+        return True
+    t = os.path.getmtime(CLI)
+    deps = [CLI_SRC, LIB, os.path.join(ROOT, "include", "uscg_b200.h"),
+            os.path.join(ROOT, "include", "uscg_b200_io.hpp")]
+    return any(os.path.getmtime(d) > t for d in deps)
+
+
+def build_cli() -> str:
+    """g++ build of the CLI (host C++17 over the C ABI), rpath to lib/."""
+    cmd = ["g++", "-std=c++17", "-O2", "-Wall", "-I", os.path.join(ROOT, "include"), CLI_SRC, "-o", CLI + ".tmp",
+           "-L", LIBDIR, "-luscg_b200", "-Wl,-rpath,$ORIGIN"]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        raise RuntimeError(f"CLI build failed:\n{r.stdout}\n{r.stderr}")
+    os.replace(CLI + ".tmp", CLI)
+    return CLI
+
+
 def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not _stale():
+        if _cli_stale():
+            build_cli()
         return LIB
     os.makedirs(LIBDIR, exist_ok=True)
     objs = []
@@ -59,6 +83,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
         f.write("\n".join(log))
     if verbose:
         print("\n".join(log))
+    build_cli()
     return LIB
 
 

@@ -450,6 +450,126 @@ def bench_c5(args, rank, world, local):
 
 
 # ---------------------------------------------------------------------------
+# the paper's comparison: USPG vs Cartesian Siddon MART (proj/src/bench.cpp)
+# ---------------------------------------------------------------------------
+def bench_cmp(args, rank, world, local):
+    """bench_compare (bench.cpp:24-88) with acceptance_9's configuration
+    (acceptance.cpp:600-611: n 256, 101 detectors, spacing 0.05, 50 views,
+    30 sweeps, beta 0.4) on the device: storage of the symmetry-compressed
+    cache vs the stored Cartesian system for p = 10 / 50 / 100 views, and the
+    time of the polar pipeline (cache build + sweeps) against Cartesian MART
+    with Siddon on the fly (sweeps) and stored (precompute + sweeps). The
+    reference's own CPU times for the same comparison are measured beside it.
+    Rank 0 only (one problem; no sharding)."""
+    import torch
+
+    import paper_2208_12964_b200 as ub
+    from paper_2208_12964_b200 import uscg, workloads
+
+    if rank != 0:
+        return
+    torch.cuda.set_device(local)
+    n, det, spacing, views, sweeps, beta = 256, 101, 0.05, 50, 30, 0.4
+    spec = ub.GridSpec.square_2d(n)
+
+    def geom_of(p):
+        return ub.ScanGeometry(source=(-8, 0, 0), detector_center=(8, 0, 0), det_u=det, spacing_u=spacing, views=p)
+
+    quarter = det % 2 == 1  # ScanGeometry::quarter_symmetric (scan.cpp:44-48): odd panel, on-axis source
+
+    memory = []
+    for p in (10, 50, 100):
+        g = geom_of(p)
+        tr = ub.Tracer(g, spec, quarter)
+        inf = tr.info()
+        cs = ub.CartesianSystem(spec, g, stored=True)
+        cinf = cs.info()
+        rows = p * det
+        memory.append({"views": p, "polar_cache_bytes": inf["cache_bytes"],
+                       "cartesian_stored_bytes": cinf["device_bytes"],
+                       "ratio": cinf["device_bytes"] / inf["cache_bytes"],
+                       "reference_layout": {"polar_cache_bytes": 24 * inf["records"] + 4 * (det + 1),
+                                            "cartesian_stored_bytes": 8 * (rows + 1) + 12 * cinf["entries"]}})
+        tr.close()
+        cs.close()
+
+    geom = geom_of(views)
+    wl = workloads.make("c1-ref")  # seeded random-ellipse phantom generator (no Shepp-Logan table bundled)
+    wl.spec = spec
+    truth = workloads.phantom_fields(wl, 1)[0]
+    tr0 = ub.Tracer(geom, spec, quarter)
+    proj = ub.project_stack(tr0, truth[None, :].astype(np.float32))[0]
+    tr0.close()
+    cfg = ub.SolverConfig(beta=beta, tolerance=0, max_sweeps=sweeps)
+
+    def polar():
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        tr = ub.Tracer(geom, spec, quarter)
+        res = ub.reconstruct(ub.ProjectionSet(geom, proj.astype(np.float64)), spec, cfg, tr)
+        torch.cuda.synchronize()
+        wall = time.perf_counter() - t0
+        tr.close()
+        return wall, res.report.seconds
+
+    def cartesian(stored):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        cs = ub.CartesianSystem(spec, geom, stored=stored)
+        field, sec = cs.reconstruct(proj, cfg)
+        torch.cuda.synchronize()
+        wall = time.perf_counter() - t0
+        info = cs.info()
+        cs.close()
+        return wall, sec, info
+
+    for _ in range(max(1, args.warmup)):
+        polar(), cartesian(False), cartesian(True)
+    reps = max(1, args.steps)
+    pol = [polar() for _ in range(reps)]
+    otf = [cartesian(False) for _ in range(reps)]
+    sto = [cartesian(True) for _ in range(reps)]
+    polar_s = float(np.median([w for w, _ in pol]))
+    polar_sweeps_s = float(np.median([s for _, s in pol]))
+    otf_sweeps_s = float(np.median([s for _, s, _ in otf]))
+    stored_s = float(np.median([w for w, _, _ in sto]))
+    stored_sweeps_s = float(np.median([s for _, s, _ in sto]))
+    cpu = None
+    if not args.no_cpu:
+        import oracle
+        if os.path.exists(oracle.REF_SO):
+            ref = oracle.Ref()
+            # the reference on the same data and geometry (its bench_compare
+            # pipeline; one core, as the reference's solver)
+            t0 = time.perf_counter()
+            rt = ref.tracer(n, False, (-8, 0, 0), (8, 0, 0), det, 1, spacing, 0.0, views, quarter)
+            rt.reconstruct(proj.reshape(views, det).astype(np.float64), beta=beta, tolerance=0, max_sweeps=sweeps)
+            ref_polar = time.perf_counter() - t0
+            _, ref_otf = ref.cartesian_mart(n, False, (-8, 0, 0), (8, 0, 0), det, 1, spacing, 0.0, views,
+                                            proj.astype(np.float64), beta=beta, sweeps=sweeps, stored=False)
+            cpu = {"value": ref_otf / ref_polar, "unit": "x", "cores": 1, "kind": "reference",
+                   "sample": f"unmodified reference: polar cache build + {sweeps} sweeps {ref_polar:.2f} s, "
+                             f"Cartesian Siddon on the fly {ref_otf:.2f} s (acceptance_9 gate >= 1.4, paper 2.5)",
+                   "polar_seconds": ref_polar, "cartesian_otf_seconds": ref_otf}
+    line = {
+        "metric": "USPG vs Cartesian Siddon MART speedup (cmp, acceptance_9 config)",
+        "value": otf_sweeps_s / polar_s, "unit": "x", "n_gpus": 1, "steps": reps, "warmup": args.warmup,
+        "ms_per_step": polar_s * 1e3, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+        "dtype": "f32", "data": "synthetic: seeded random-ellipse phantom on square_2d(256), binary projections",
+        "config": {"workload": "cmp", "n": n, "detectors": det, "spacing": spacing, "views": views,
+                   "sweeps": sweeps, "beta": beta, "l2": "small problem, L2-resident"},
+        "speed": {"polar_seconds": polar_s, "polar_sweeps_seconds": polar_sweeps_s,
+                  "cartesian_otf_seconds": otf_sweeps_s, "cartesian_stored_seconds": stored_s,
+                  "cartesian_stored_sweeps_seconds": stored_sweeps_s,
+                  "speedup_vs_otf": otf_sweeps_s / polar_s, "speedup_vs_stored": stored_s / polar_s,
+                  "cartesian_levels": otf[0][2]["levels"]},
+        "memory": memory, "cpu_baseline": cpu, "e2e": None, "roofline": None,
+        "gpu_launches": None,
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
 # GPU arm
 # ---------------------------------------------------------------------------
 def main():
@@ -473,6 +593,9 @@ def main():
         return
     if args.config == "c5":
         bench_c5(args, rank, world, local)
+        return
+    if args.config == "cmp":
+        bench_cmp(args, rank, world, local)
         return
 
     import torch

@@ -227,6 +227,38 @@ uscg_status uscg_image_metrics(uscg_ctx ctx, const float* ref, const float* test
                                double dynamic_range, double* mae_out, double* rmse_out,
                                double* ssim_out, uint32_t flags);
 
+/* ---- Cartesian comparator (proj/include/uscg/siddon.hpp) ------------------
+ * The paper's baseline on the same hardware: MART on an axis-aligned voxel
+ * grid with Siddon path-length coefficients for every (view, line) — no
+ * symmetry compression, so the stored system grows with the view count. */
+typedef struct {
+    int32_t nx, ny, nz;
+    double voxel;
+    double origin[3]; /* minimum corner */
+} uscg_cartesian;
+typedef struct uscg_csystem_s* uscg_csystem;
+/* CartesianSpec::like (siddon.cpp:18-31): n x n (x slices) voxels of the
+ * ring spacing covering the grid's square / cube. Host only. */
+uscg_status uscg_cartesian_like(const uscg_grid* grid, uscg_cartesian* out);
+/* precompute_cartesian_system (siddon.cpp:104-125) on the device, plus the
+ * MART dependency schedule of its supports. stored = 0 keeps the schedule only
+ * (cartesian_mart_otf: every line re-traced on every pass). */
+uscg_status uscg_csystem_create(uscg_ctx ctx, const uscg_cartesian* cart, const uscg_scan* scan,
+                                int32_t stored, uscg_csystem* out);
+uscg_status uscg_csystem_info(uscg_csystem sys, uint64_t* entries, uint64_t* device_bytes,
+                              int32_t* levels, double* precompute_ms);
+/* CartesianSystem (offsets views*lines+1, voxel indices, f32 lengths) to host
+ * arrays; stored systems only. */
+uscg_status uscg_csystem_export(uscg_csystem sys, uint32_t* offsets, uint32_t* idx, float* weight);
+/* cartesian_mart_stored / cartesian_mart_otf (siddon.cpp:147-209): exactly
+ * cfg->max_sweeps sweeps (the reference's comparator has no stopping test),
+ * p_floor = cfg->p_floor when > 0 else 1e-12 x the mean positive measurement,
+ * field starts at cfg->f_init. proj [views*lines], field_out voxel_count;
+ * *seconds receives the device time of the sweeps. */
+uscg_status uscg_csystem_reconstruct(uscg_csystem sys, const float* proj, const uscg_solver_config* cfg,
+                                     float* field_out, double* seconds, uint32_t flags);
+uscg_status uscg_csystem_destroy(uscg_csystem sys);
+
 /* ---- MART dependency schedule (host only) ---------------------------------
  * The schedule the device executors run, from explicit supports: lines in
  * sweep order, support of line u = idx[pos[u] .. pos[u+1]) (cell indices <

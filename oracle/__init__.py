@@ -304,6 +304,11 @@ class Ref:
                                             _dp, _sp, _sp, C.c_int]
         L.ref_write_pgm16.argtypes = [C.c_char_p, C.c_int, C.c_int, _dp, C.c_double, C.c_double, _sp, _sp, C.c_int]
         L.ref_read_pgm16.argtypes = [C.c_char_p, C.POINTER(C.c_int), C.POINTER(C.c_int), _dp, C.c_longlong]
+        L.ref_cartesian_system.argtypes = [C.c_int, C.c_double, C.c_double, C.c_int, _dp, _dp, C.c_int, C.c_int,
+                                           C.c_double, C.c_double, C.c_int, _u64p, _u32p, _dp, _u64p]
+        L.ref_cartesian_mart.argtypes = [C.c_int, C.c_double, C.c_double, C.c_int, _dp, _dp, C.c_int, C.c_int,
+                                         C.c_double, C.c_double, C.c_int, _dp, C.c_double, C.c_int, C.c_double,
+                                         C.c_int, _dp, _dp]
         L.ref_reconstruct.argtypes = [C.c_void_p, _dp, _dp, C.c_double, C.c_double, C.c_int, C.c_double,
                                       C.c_double, _dp, _dp, _dp, _u8p]
         L.ref_mart_update_line.argtypes = [C.c_int, _dp, C.c_int64, _u32p, C.c_int64, C.c_double,
@@ -344,6 +349,35 @@ class Ref:
         out = np.zeros((slices, n, n))
         self.check(self.L.ref_field_to_cartesian(n, 2.0 / n, 2.0 / n, int(volume), _ptr(f, _dp), _ptr(out, _dp)))
         return out
+
+    def cartesian_system(self, n, volume, src, ctr, det_u, det_v, su, sv, views):
+        """precompute_cartesian_system on CartesianSpec::like(reference grid n):
+        (offsets u64 [rows+1], idx u32, weight f64)"""
+        s3, c3 = np.ascontiguousarray(src, float), np.ascontiguousarray(ctr, float)
+        r = h = 2.0 / n
+        ent = np.zeros(1, np.uint64)
+        args = (n, r, h, int(volume), _ptr(s3, _dp), _ptr(c3, _dp), det_u, det_v, su, sv, views)
+        self.check(self.L.ref_cartesian_system(*args, None, None, None, _ptr(ent, _u64p)))
+        rows = views * det_u * det_v
+        off = np.zeros(rows + 1, np.uint64)
+        idx = np.zeros(int(ent[0]), np.uint32)
+        w = np.zeros(int(ent[0]))
+        self.check(self.L.ref_cartesian_system(*args, _ptr(off, _u64p), _ptr(idx, _u32p), _ptr(w, _dp), _ptr(ent, _u64p)))
+        return off, idx, w
+
+    def cartesian_mart(self, n, volume, src, ctr, det_u, det_v, su, sv, views, proj, beta=0.4, sweeps=5,
+                       f_init=1.0, stored=True):
+        """cartesian_mart_stored / cartesian_mart_otf: (values, seconds)"""
+        s3, c3 = np.ascontiguousarray(src, float), np.ascontiguousarray(ctr, float)
+        p = np.ascontiguousarray(proj, float)
+        cells = n * n * (n if volume else 1)
+        out = np.zeros(cells)
+        sec = np.zeros(1)
+        r = h = 2.0 / n
+        self.check(self.L.ref_cartesian_mart(n, r, h, int(volume), _ptr(s3, _dp), _ptr(c3, _dp), det_u, det_v, su, sv,
+                                             views, _ptr(p, _dp), beta, sweeps, f_init, int(stored), _ptr(out, _dp),
+                                             _ptr(sec, _dp)))
+        return out, float(sec[0])
 
     def phantom(self, n, volume):
         out = np.zeros((n if volume else 1) * n * n)

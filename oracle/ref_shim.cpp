@@ -32,6 +32,7 @@
 
 #include "uscg/grid.hpp"
 #include "uscg/io.hpp"
+#include "uscg/siddon.hpp"
 #include "uscg/metrics.hpp"
 #include "uscg/phantom.hpp"
 #include "uscg/solver.hpp"
@@ -325,6 +326,46 @@ int ref_read_pgm16(const char* path, int* rows, int* cols, double* out, long lon
         *cols = im.cols;
         if (static_cast<long long>(im.v.size()) <= cap)
             std::memcpy(out, im.v.data(), im.v.size() * sizeof(double));
+    });
+}
+
+// ---- Cartesian comparator (proj/src/siddon.cpp) -------------------------
+// CartesianSpec::like(GridSpec(n, r, h, mode)) and a ScanGeometry.
+// system: counts (rows), entries out via offsets (rows+1, u64), idx, weight;
+// call with idx == nullptr first to get the entry count in *entries.
+int ref_cartesian_system(int n, double r, double h, int volume, const double* src, const double* ctr,
+                         int det_u, int det_v, double su, double sv, int views, std::uint64_t* offsets,
+                         std::uint32_t* idx, double* weight, std::uint64_t* entries) {
+    return guarded([&] {
+        const CartesianSpec c = CartesianSpec::like(make_spec(n, r, h, volume));
+        const CartesianSystem sys = precompute_cartesian_system(make_geom(src, ctr, det_u, det_v, su, sv, views), c);
+        *entries = sys.idx.size();
+        if (!idx)
+            return;
+        std::memcpy(offsets, sys.offsets.data(), sys.offsets.size() * sizeof(std::uint64_t));
+        std::memcpy(idx, sys.idx.data(), sys.idx.size() * sizeof(std::uint32_t));
+        std::memcpy(weight, sys.weight.data(), sys.weight.size() * sizeof(double));
+    });
+}
+
+// cartesian_mart_stored (stored != 0) or cartesian_mart_otf; out: voxel_count values
+int ref_cartesian_mart(int n, double r, double h, int volume, const double* src, const double* ctr,
+                       int det_u, int det_v, double su, double sv, int views, const double* proj,
+                       double beta, int sweeps, double f_init, int stored, double* out, double* seconds) {
+    return guarded([&] {
+        const CartesianSpec c = CartesianSpec::like(make_spec(n, r, h, volume));
+        ProjectionSet p;
+        p.geometry = make_geom(src, ctr, det_u, det_v, su, sv, views);
+        p.data.assign(proj, proj + std::size_t(views) * det_u * det_v);
+        SolverConfig cfg;
+        cfg.beta = beta;
+        cfg.max_sweeps = sweeps;
+        cfg.f_init = f_init;
+        cfg.tolerance = 0;
+        CartesianMartResult res = stored ? cartesian_mart_stored(p, c, precompute_cartesian_system(p.geometry, c), cfg)
+                                         : cartesian_mart_otf(p, c, cfg);
+        std::memcpy(out, res.values.data(), res.values.size() * sizeof(double));
+        *seconds = res.seconds;
     });
 }
 

@@ -1402,6 +1402,227 @@ uscg_status uscg_image_metrics(uscg_ctx ctx, const float* ref, const float* test
     });
 }
 
+// ---- Cartesian comparator ------------------------------------------------------
+
+struct uscg_csystem_s {
+    uscg_ctx ctx = nullptr;
+    DevCart C{};
+    int lines = 0, views = 0, stored = 1;
+    uint64_t voxels = 0, entries = 0;
+    double precompute_ms = 0;
+    DevBuf<double> d_rays, d_theta;
+    DevBuf<uint32_t> d_off, d_idx, d_order;
+    DevBuf<float> d_w, w_proj, w_field;
+    DevBuf<unsigned long long> w_clamps;
+    std::vector<uint32_t> level_off;
+};
+
+uscg_status uscg_cartesian_like(const uscg_grid* grid, uscg_cartesian* out) {
+    return guarded([&] {
+        validate_grid(grid);
+        need(out != nullptr, "null output");
+        const int n = 2 * grid->n_rings;
+        const double radius = 0.5 * n * grid->ring_spacing;
+        out->nx = out->ny = n;
+        out->voxel = grid->ring_spacing;
+        out->origin[0] = out->origin[1] = -radius;
+        if (grid->volume) {
+            out->nz = grid->n_slices;
+            out->origin[2] = -0.5 * grid->n_slices * grid->slice_height;
+        } else {
+            out->nz = 1;
+            out->origin[2] = -0.5 * grid->ring_spacing;
+        }
+    });
+}
+
+uscg_status uscg_csystem_create(uscg_ctx ctx, const uscg_cartesian* cart, const uscg_scan* scan,
+                                int32_t stored, uscg_csystem* out) {
+    return guarded([&] {
+        bind(ctx);
+        need(cart && scan && out, "null argument");
+        need(cart->nx >= 1 && cart->ny >= 1 && cart->nz >= 1, "voxel counts must be >= 1");  // siddon.cpp:11-16
+        need(cart->voxel > 0, "voxel size must be positive");
+        validate_scan(scan);
+        std::unique_ptr<uscg_csystem_s> s(new uscg_csystem_s);
+        s->ctx = ctx;
+        s->C = DevCart{cart->nx, cart->ny, cart->nz, cart->voxel, cart->origin[0], cart->origin[1], cart->origin[2]};
+        s->voxels = uint64_t(cart->nx) * uint64_t(cart->ny) * uint64_t(cart->nz);
+        need(s->voxels < (1ull << 32), "voxel count must fit in 32 bits");
+        s->stored = stored ? 1 : 0;
+        s->lines = scan->det_u * scan->det_v;
+        s->views = scan->views;
+        const uint64_t rows = uint64_t(s->lines) * uint64_t(s->views);
+        need(rows < (1ull << 31), "views * lines must fit in 31 bits");
+        std::vector<double> rays(size_t(s->lines) * 6);
+        first_view_rays(scan, rays.data(), rays.data() + 3 * size_t(s->lines));
+        std::vector<double> th(size_t(s->views));
+        const double step = 360.0 / s->views;
+        for (int v = 0; v < s->views; ++v)
+            th[v] = norm360(scan->view_angles_deg ? scan->view_angles_deg[v] : v * step);
+        cudaStream_t st = ctx->stream;
+        s->d_rays.alloc(rays.size());
+        s->d_theta.alloc(th.size());
+        UB_CUDA(cudaMemcpyAsync(s->d_rays.p, rays.data(), sizeof(double) * rays.size(), cudaMemcpyHostToDevice, st));
+        UB_CUDA(cudaMemcpyAsync(s->d_theta.p, th.data(), sizeof(double) * th.size(), cudaMemcpyHostToDevice, st));
+        cudaEvent_t e0, e1;
+        UB_CUDA(cudaEventCreate(&e0));
+        UB_CUDA(cudaEventCreate(&e1));
+        UB_CUDA(cudaEventRecord(e0, st));
+        DevBuf<uint32_t> cnt;
+        cnt.alloc(rows);
+        launch_siddon_count(s->C, s->lines, s->views, s->d_rays.p, s->d_theta.p, cnt.p, st);
+        s->d_off.alloc(rows + 1);
+        launch_exclusive_scan_u32(cnt.p, s->d_off.p, int(rows), st);
+        uint32_t total = 0;
+        UB_CUDA(cudaMemcpyAsync(&total, s->d_off.p + rows, sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+        UB_CUDA(cudaStreamSynchronize(st));
+        s->entries = total;
+        s->d_idx.alloc(std::max<uint64_t>(total, 1));
+        s->d_w.alloc(std::max<uint64_t>(total, 1));
+        launch_siddon_write(s->C, s->lines, s->views, s->d_rays.p, s->d_theta.p, s->d_off.p, s->d_idx.p, s->d_w.p, st);
+        UB_CUDA(cudaEventRecord(e1, st));
+        // the dependency schedule of the supports (host, schedule.h)
+        std::vector<uint32_t> off(rows + 1), idx(total);
+        UB_CUDA(cudaMemcpyAsync(off.data(), s->d_off.p, sizeof(uint32_t) * off.size(), cudaMemcpyDeviceToHost, st));
+        UB_CUDA(cudaMemcpyAsync(idx.data(), s->d_idx.p, sizeof(uint32_t) * idx.size(), cudaMemcpyDeviceToHost, st));
+        UB_CUDA(cudaStreamSynchronize(st));
+        float ms = 0;
+        UB_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+        s->precompute_ms = ms;
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+        AsapSchedule sched(s->voxels, uint32_t(s->lines), 1);
+        sched.add(idx.data(), off.data(), uint32_t(rows));
+        sched.done();
+        std::vector<uint32_t> order;
+        sched.finish(order, s->level_off);
+        s->d_order.alloc(order.size());
+        UB_CUDA(cudaMemcpyAsync(s->d_order.p, order.data(), sizeof(uint32_t) * order.size(), cudaMemcpyHostToDevice, st));
+        UB_CUDA(cudaStreamSynchronize(st));
+        if (!s->stored) {  // on the fly: only the schedule is kept
+            s->d_idx.release();
+            s->d_w.release();
+        }
+        *out = s.release();
+    });
+}
+
+uscg_status uscg_csystem_info(uscg_csystem s, uint64_t* entries, uint64_t* device_bytes, int32_t* levels,
+                              double* precompute_ms) {
+    return guarded([&] {
+        need(s != nullptr, "null system");
+        if (entries)
+            *entries = s->entries;
+        if (device_bytes)  // offsets + (stored) voxel index + length per entry
+            *device_bytes = sizeof(uint32_t) * (uint64_t(s->lines) * s->views + 1) +
+                            (s->stored ? s->entries * (sizeof(uint32_t) + sizeof(float)) : 0);
+        if (levels)
+            *levels = int32_t(s->level_off.size()) - 1;
+        if (precompute_ms)
+            *precompute_ms = s->precompute_ms;
+    });
+}
+
+uscg_status uscg_csystem_export(uscg_csystem s, uint32_t* offsets, uint32_t* idx, float* weight) {
+    return guarded([&] {
+        need(s != nullptr, "null system");
+        need(s->stored, "an on-the-fly system keeps no coefficients");
+        need(offsets && idx && weight, "null buffer");
+        bind(s->ctx);
+        cudaStream_t st = s->ctx->stream;
+        const uint64_t rows = uint64_t(s->lines) * s->views;
+        UB_CUDA(cudaMemcpyAsync(offsets, s->d_off.p, sizeof(uint32_t) * (rows + 1), cudaMemcpyDeviceToHost, st));
+        UB_CUDA(cudaMemcpyAsync(idx, s->d_idx.p, sizeof(uint32_t) * s->entries, cudaMemcpyDeviceToHost, st));
+        UB_CUDA(cudaMemcpyAsync(weight, s->d_w.p, sizeof(float) * s->entries, cudaMemcpyDeviceToHost, st));
+        UB_CUDA(cudaStreamSynchronize(st));
+    });
+}
+
+uscg_status uscg_csystem_reconstruct(uscg_csystem s, const float* proj, const uscg_solver_config* cfg,
+                                     float* field_out, double* seconds, uint32_t flags) {
+    return guarded([&] {
+        need(s && proj && cfg && field_out, "null argument");
+        bind(s->ctx);
+        need(cfg->beta > 0 && cfg->beta < 2, "beta must lie in (0, 2)");  // validate_config
+        need(cfg->f_init > 0, "f_init must be positive");
+        need(cfg->max_sweeps >= 1, "max_sweeps must be >= 1");
+        cudaStream_t st = s->ctx->stream;
+        const uint64_t rows = uint64_t(s->lines) * s->views;
+        const bool dev = flags & USCG_DEVICE_POINTERS;
+        // p_floor (auto_p_floor, siddon.cpp:135-145) from the measurements
+        std::vector<float> hp;
+        const float* pp = proj;
+        if (dev) {
+            hp.resize(rows);
+            UB_CUDA(cudaMemcpyAsync(hp.data(), proj, sizeof(float) * rows, cudaMemcpyDeviceToHost, st));
+            UB_CUDA(cudaStreamSynchronize(st));
+            pp = hp.data();
+        }
+        double sum = 0;
+        uint64_t count = 0;
+        for (uint64_t i = 0; i < rows; ++i) {
+            need(std::isfinite(pp[i]) && pp[i] >= 0, "projection data must be finite and non-negative");
+            if (pp[i] > 0) {
+                sum += pp[i];
+                ++count;
+            }
+        }
+        const double p_floor = cfg->p_floor > 0 ? cfg->p_floor : (count == 0 ? 1e-12 : 1e-12 * (sum / count));
+        const float* d_proj = proj;
+        if (!dev) {
+            s->w_proj.ensure(rows);
+            UB_CUDA(cudaMemcpyAsync(s->w_proj.p, proj, sizeof(float) * rows, cudaMemcpyHostToDevice, st));
+            d_proj = s->w_proj.p;
+        }
+        float* d_field = field_out;
+        if (!dev) {
+            s->w_field.ensure(s->voxels);
+            d_field = s->w_field.p;
+        }
+        launch_fill(d_field, s->voxels, float(cfg->f_init), st);
+        s->w_clamps.ensure(1);
+        UB_CUDA(cudaMemsetAsync(s->w_clamps.p, 0, sizeof(unsigned long long), st));
+        cudaEvent_t e0, e1;
+        UB_CUDA(cudaEventCreate(&e0));
+        UB_CUDA(cudaEventCreate(&e1));
+        UB_CUDA(cudaEventRecord(e0, st));
+        const int levels = int(s->level_off.size()) - 1;
+        for (int sweep = 0; sweep < cfg->max_sweeps; ++sweep)
+            for (int l = 0; l < levels; ++l) {
+                const uint32_t* units = s->d_order.p + s->level_off[l];
+                const int n = int(s->level_off[l + 1] - s->level_off[l]);
+                if (s->stored)
+                    launch_csr_level(units, n, s->d_off.p, s->d_idx.p, s->d_w.p, d_proj, d_field, cfg->beta, p_floor,
+                                     s->w_clamps.p, st);
+                else
+                    launch_otf_level(s->C, s->lines, s->d_rays.p, s->d_theta.p, units, n, d_proj, d_field, cfg->beta,
+                                     p_floor, s->w_clamps.p, st);
+            }
+        UB_CUDA(cudaGetLastError());
+        UB_CUDA(cudaEventRecord(e1, st));
+        if (!dev)
+            UB_CUDA(cudaMemcpyAsync(field_out, d_field, sizeof(float) * s->voxels, cudaMemcpyDeviceToHost, st));
+        UB_CUDA(cudaStreamSynchronize(st));
+        float ms = 0;
+        UB_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+        if (seconds)
+            *seconds = ms * 1e-3;
+    });
+}
+
+uscg_status uscg_csystem_destroy(uscg_csystem s) {
+    return guarded([&] {
+        if (!s)
+            return;
+        cudaSetDevice(s->ctx->device);
+        cudaDeviceSynchronize();
+        delete s;
+    });
+}
+
 uscg_status uscg_uspg_to_cg_map(uscg_ctx ctx, int32_t n, uint32_t* out) {
     return guarded([&] {
         bind(ctx);

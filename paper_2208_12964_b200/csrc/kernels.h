@@ -136,6 +136,26 @@ int ssim_tiles(int rows, int cols);
 void launch_ssim(const float* ref, const float* test, int slices, int rows, int cols,
                  const double* c1c2, double* part, double* out, cudaStream_t st);
 
+// Cartesian comparator (cartesian.cu): an axis-aligned voxel grid
+// (CartesianSpec, proj/include/uscg/siddon.hpp:11-25)
+struct DevCart {
+    int nx, ny, nz;
+    double voxel;
+    double o0, o1, o2;  // minimum corner
+};
+// Siddon system: counts per (view, line), then CSR lists (u32 voxel, f32 length)
+void launch_siddon_count(const DevCart& C, int lines, int views, const double* rays, const double* theta,
+                         uint32_t* counts, cudaStream_t st);
+void launch_siddon_write(const DevCart& C, int lines, int views, const double* rays, const double* theta,
+                         const uint32_t* off, uint32_t* idx, float* w, cudaStream_t st);
+// one dependency level of the weighted MART: stored lists or Siddon on the fly
+void launch_csr_level(const uint32_t* units, int n, const uint32_t* off, const uint32_t* idx, const float* w,
+                      const float* proj, float* f, double beta, double p_floor, unsigned long long* clamps,
+                      cudaStream_t st);
+void launch_otf_level(const DevCart& C, int lines, const double* rays, const double* theta, const uint32_t* units,
+                      int n, const float* proj, float* f, double beta, double p_floor, unsigned long long* clamps,
+                      cudaStream_t st);
+
 // K4 resample
 void launch_perm_resample(const float* field, uint64_t cells_per_slice, int slices, int S, int Sp,
                           int n, float* out, cudaStream_t st);

@@ -99,6 +99,11 @@ class _Report(C.Structure):
                 ("crossed", _u8p)]
 
 
+class _Cart(C.Structure):
+    _fields_ = [("nx", C.c_int32), ("ny", C.c_int32), ("nz", C.c_int32), ("voxel", C.c_double),
+                ("origin", C.c_double * 3)]
+
+
 class _Info(C.Structure):
     _fields_ = [("lines", C.c_int32), ("views", C.c_int32), ("n_rings", C.c_int32), ("n_slices", C.c_int32),
                 ("records", C.c_uint64), ("cells_per_slice", C.c_uint64), ("cell_count", C.c_uint64),
@@ -115,6 +120,8 @@ EXPORTS = [
     "uscg_trace_checksums",
     "uscg_tracer_build_schedule", "uscg_problem_stride", "uscg_project", "uscg_reconstruct",
     "uscg_resample", "uscg_uspg_to_cg_map", "uscg_diag_math", "uscg_schedule_build", "uscg_image_metrics",
+    "uscg_cartesian_like", "uscg_csystem_create", "uscg_csystem_info", "uscg_csystem_export",
+    "uscg_csystem_reconstruct", "uscg_csystem_destroy",
 ]
 
 _lib = None
@@ -163,6 +170,12 @@ def load(build_if_missing: bool = True):
                                    C.c_uint32]
     L.uscg_resample.argtypes = [vp, C.POINTER(_Grid), vp, C.c_int32, C.c_int32, vp, C.c_uint32]
     L.uscg_uspg_to_cg_map.argtypes = [vp, C.c_int32, _u32p]
+    L.uscg_cartesian_like.argtypes = [C.POINTER(_Grid), C.POINTER(_Cart)]
+    L.uscg_csystem_create.argtypes = [vp, C.POINTER(_Cart), C.POINTER(_Scan), C.c_int32, C.POINTER(vp)]
+    L.uscg_csystem_info.argtypes = [vp, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64), C.POINTER(C.c_int32), _dp]
+    L.uscg_csystem_export.argtypes = [vp, _u32p, _u32p, _fp]
+    L.uscg_csystem_reconstruct.argtypes = [vp, vp, C.POINTER(_Cfg), vp, _dp, C.c_uint32]
+    L.uscg_csystem_destroy.argtypes = [vp]
     L.uscg_image_metrics.argtypes = [vp, vp, vp, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_double, _dp, _dp,
                                      _dp, C.c_uint32]
     L.uscg_diag_math.argtypes = [vp, C.c_int32, _dp, _dp, _dp]
@@ -738,6 +751,63 @@ def ssim_volume(ref, test) -> float:
     """uscg::ssim_volume (metrics.cpp:186-199): per-slice ssim with the dynamic
     range of the whole reference stack, averaged."""
     return float(image_metrics(ref, test, shared_range=True)["ssim"].mean())
+
+
+class CartesianSystem:
+    """The paper's Cartesian baseline on the device (proj/include/uscg/siddon.hpp):
+    CartesianSpec::like(spec), precompute_cartesian_system(geom, cspec) and
+    cartesian_mart_stored (stored=True) / cartesian_mart_otf (stored=False)."""
+
+    def __init__(self, spec: GridSpec, geom: ScanGeometry, stored: bool = True, ctx: Optional[Context] = None):
+        ctx = ctx or default_context()
+        self._ctx = ctx
+        g, keep_g = spec._c()
+        self.cart = _Cart()
+        _check(load().uscg_cartesian_like(C.byref(g), C.byref(self.cart)))
+        sc, keep_s = geom._c()
+        h = C.c_void_p()
+        _check(load().uscg_csystem_create(ctx.h, C.byref(self.cart), C.byref(sc), int(bool(stored)), C.byref(h)))
+        self.h = h.value
+        self.geom, self.stored = geom, bool(stored)
+        self.voxels = self.cart.nx * self.cart.ny * self.cart.nz
+
+    def info(self) -> dict:
+        e, b, lv, ms = C.c_uint64(), C.c_uint64(), C.c_int32(), C.c_double()
+        _check(load().uscg_csystem_info(self.h, C.byref(e), C.byref(b), C.byref(lv), C.byref(ms)))
+        return {"entries": e.value, "device_bytes": b.value, "levels": lv.value, "precompute_ms": ms.value}
+
+    def export(self):
+        """(offsets u32 [views*lines+1], voxel indices u32, lengths f32)"""
+        inf = self.info()
+        rows = self.geom.views * self.geom.lines()
+        off = np.zeros(rows + 1, np.uint32)
+        idx = np.zeros(inf["entries"], np.uint32)
+        w = np.zeros(inf["entries"], np.float32)
+        _check(load().uscg_csystem_export(self.h, off.ctypes.data_as(_u32p), idx.ctypes.data_as(_u32p),
+                                          w.ctypes.data_as(_fp)))
+        return off, idx, w
+
+    def reconstruct(self, proj, cfg: SolverConfig):
+        """(field f32 [voxels], device seconds) after cfg.max_sweeps sweeps"""
+        p = np.ascontiguousarray(proj, dtype=np.float32).reshape(-1)
+        if p.size != self.geom.views * self.geom.lines():
+            raise InvalidArgument("projection data size does not match geometry")
+        out = np.zeros(self.voxels, np.float32)
+        sec = C.c_double()
+        c = _Cfg(cfg.beta, cfg.tolerance, cfg.max_sweeps, cfg.f_init, cfg.p_floor)
+        _check(load().uscg_csystem_reconstruct(self.h, _ptr(p), C.byref(c), _ptr(out), C.byref(sec), 0))
+        return out, sec.value
+
+    def close(self) -> None:
+        h, self.h = getattr(self, "h", None), None
+        if h and _lib is not None:
+            _lib.uscg_csystem_destroy(h)
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 def uspg_to_cg_map(n: int, ctx: Optional[Context] = None) -> np.ndarray:

@@ -183,6 +183,13 @@ uscg_status uscg_trace_checksums(uscg_tracer tracer, int32_t view0, int32_t nvie
                                  uint32_t* counts, uint64_t* sums, uint32_t flags);
 /* Build the MART dependency schedule now (otherwise built on first use). */
 uscg_status uscg_tracer_build_schedule(uscg_tracer tracer);
+/* The schedule the dataflow executor runs (built if needed): lines per run,
+ * runs, levels, the level-sorted run order (runs), level offsets (levels+1),
+ * in-sweep predecessors (pred_off runs+1, preds *n_preds) and cross-sweep
+ * predecessor counts (runs). Call with null arrays first for the sizes. */
+uscg_status uscg_tracer_export_schedule(uscg_tracer tracer, int32_t* run, uint32_t* runs, uint32_t* levels,
+                                        uint64_t* n_preds, uint32_t* order, uint32_t* level_off,
+                                        uint32_t* pred_off, uint32_t* preds, uint32_t* npred_x);
 /* stride of the interleaved problem dimension for S problems */
 int32_t uscg_problem_stride(int32_t problems);
 

@@ -473,27 +473,70 @@ int run_length(int lines, bool volume) {
     return 1;
 }
 
-void build_schedule(uscg_tracer_s* t) {
-    if (t->sched_built)
-        return;
-    cudaEvent_t e0, e1;
-    UB_CUDA(cudaEventCreate(&e0));
-    UB_CUDA(cudaEventCreate(&e1));
-    const auto h0 = std::chrono::steady_clock::now();
-    t->run = run_length(t->lines, t->volume != 0);
-    // a run's index lists live in shared memory (4 groups per CTA): keep the
-    // per-group lists under ~48 KiB
-    while (t->run > 1 && size_t(t->run) * size_t(t->max_cells) * 4 > 48 * 1024) {
-        int r = t->run - 1;
-        while (r > 1 && t->lines % r != 0)
-            --r;
-        t->run = r;
+// The run DAG from the device-built edges (schedule_gpu.cu: sorted unique
+// succ << 32 | pred, pred | 0x80000000 for cross-sweep): the same structures
+// AsapSchedule produces (schedule.cpp) — in-sweep preds ascending, ASAP levels
+// in run order (preds precede their successors), level-sorted order, merged
+// successor lists in the same order.
+struct RunSchedule {
+    std::vector<uint32_t> order, level_off, pred_off, preds, npred_x, succ_off, succs;
+    uint32_t levels = 0;
+};
+
+void schedule_from_edges(const std::vector<unsigned long long>& edges, uint32_t runs, RunSchedule& R) {
+    R.pred_off.assign(size_t(runs) + 1, 0u);
+    R.npred_x.assign(runs, 0u);
+    R.preds.clear();
+    R.preds.reserve(edges.size());
+    std::vector<uint32_t> succ_cnt(size_t(runs) + 1, 0u);
+    for (unsigned long long e : edges) {
+        const uint32_t u = uint32_t(e >> 32), p = uint32_t(e) & 0x7FFFFFFFu;
+        if (uint32_t(e) & 0x80000000u)
+            ++R.npred_x[u];
+        else {
+            R.preds.push_back(p);
+            ++R.pred_off[size_t(u) + 1];
+        }
+        ++succ_cnt[size_t(p) + 1];
     }
+    for (uint32_t u = 0; u < runs; ++u)
+        R.pred_off[size_t(u) + 1] += R.pred_off[u];
+    // levels (1-based) in run order
+    std::vector<uint32_t> level(runs, 0u);
+    R.levels = 0;
+    for (uint32_t u = 0; u < runs; ++u) {
+        uint32_t lev = 0;
+        for (uint32_t k = R.pred_off[u]; k < R.pred_off[size_t(u) + 1]; ++k)
+            lev = std::max(lev, level[R.preds[k]]);
+        level[u] = lev + 1;
+        R.levels = std::max(R.levels, lev + 1);
+    }
+    std::vector<uint32_t> cnt(size_t(R.levels) + 2, 0u);
+    for (uint32_t l : level)
+        ++cnt[l];
+    R.level_off.assign(size_t(R.levels) + 1, 0u);
+    for (uint32_t l = 1; l <= R.levels; ++l)
+        R.level_off[l] = R.level_off[l - 1] + cnt[l];
+    std::vector<uint32_t> at(R.level_off.begin(), R.level_off.end());
+    R.order.assign(runs, 0u);
+    for (uint32_t u = 0; u < runs; ++u)
+        R.order[at[level[u] - 1]++] = u;
+    // successors: for each u ascending, its in-sweep then cross preds (edge order)
+    for (uint32_t u = 0; u < runs; ++u)
+        succ_cnt[size_t(u) + 1] += succ_cnt[u];
+    R.succ_off = succ_cnt;
+    R.succs.assign(edges.size(), 0u);
+    std::vector<uint32_t> cur(R.succ_off.begin(), R.succ_off.end() - 1);
+    for (unsigned long long e : edges)
+        R.succs[cur[uint32_t(e) & 0x7FFFFFFFu]++] = uint32_t(e >> 32);
+}
+
+// the host builder (schedule.cpp): traces copied back in batches
+void host_schedule(uscg_tracer_s* t, RunSchedule& R) {
     AsapSchedule sched(t->cells, uint32_t(t->lines), uint32_t(t->run));
     const uint64_t units = t->units();
     const uint64_t batch_cells = 1ull << 25;  // 128 MiB of indices per batch
-    std::vector<uint32_t> pos;
-    std::vector<uint32_t> idx;
+    std::vector<uint32_t> pos, idx;
     DevBuf<uint32_t> d_pos, d_idx;
     uint64_t u0 = 0;
     while (u0 < units) {
@@ -509,58 +552,66 @@ void build_schedule(uscg_tracer_s* t) {
             pos[i + 1] = pos[i] + t->h_cells[u0 + i];
         d_pos.ensure(pos.size());
         d_idx.ensure(std::max<uint64_t>(tot, 1));
-        UB_CUDA(cudaMemcpyAsync(d_pos.p, pos.data(), sizeof(uint32_t) * pos.size(),
-                                cudaMemcpyHostToDevice, t->st()));
-        launch_trace_dump(t->trace_args(), uint32_t(u0), n, t->max_recs, t->max_cells, d_pos.p,
-                          d_idx.p, t->st());
+        UB_CUDA(cudaMemcpyAsync(d_pos.p, pos.data(), sizeof(uint32_t) * pos.size(), cudaMemcpyHostToDevice, t->st()));
+        launch_trace_dump(t->trace_args(), uint32_t(u0), n, t->max_recs, t->max_cells, d_pos.p, d_idx.p, t->st());
         idx.resize(std::max<uint64_t>(tot, 1));
-        UB_CUDA(cudaMemcpyAsync(idx.data(), d_idx.p, sizeof(uint32_t) * tot, cudaMemcpyDeviceToHost,
-                                t->st()));
+        UB_CUDA(cudaMemcpyAsync(idx.data(), d_idx.p, sizeof(uint32_t) * tot, cudaMemcpyDeviceToHost, t->st()));
         UB_CUDA(cudaStreamSynchronize(t->st()));
         sched.add(idx.data(), pos.data(), n);
         u0 = u1;
     }
     sched.done();
-    t->n_runs = int(sched.runs());
-    t->runs_per_view = int(sched.runs_per_view());
-    std::vector<uint32_t> order;
-    sched.finish(order, t->level_off);
-    t->d_order.alloc(std::max<size_t>(order.size(), 1));
-    UB_CUDA(cudaMemcpy(t->d_order.p, order.data(), sizeof(uint32_t) * order.size(),
-                       cudaMemcpyHostToDevice));
-    t->d_level_off.alloc(t->level_off.size());
-    UB_CUDA(cudaMemcpy(t->d_level_off.p, t->level_off.data(), sizeof(uint32_t) * t->level_off.size(),
-                       cudaMemcpyHostToDevice));
-    t->d_bar.alloc(2);
-    t->d_pred_off.alloc(sched.pred_off().size());
-    UB_CUDA(cudaMemcpy(t->d_pred_off.p, sched.pred_off().data(),
-                       sizeof(uint32_t) * sched.pred_off().size(), cudaMemcpyHostToDevice));
-    t->d_preds.alloc(std::max<size_t>(sched.preds().size(), 1));
-    if (!sched.preds().empty())
-        UB_CUDA(cudaMemcpy(t->d_preds.p, sched.preds().data(), sizeof(uint32_t) * sched.preds().size(),
-                           cudaMemcpyHostToDevice));
-    t->n_preds = sched.preds().size();
-    {
-        // in-sweep + cross-sweep successors, cross-sweep predecessor counts
-        std::vector<uint32_t> npred_x, succ_off, succs;
-        sched.cross(npred_x, succ_off, succs);
-        t->d_npred_x.alloc(std::max<size_t>(npred_x.size(), 1));
-        if (!npred_x.empty())
-            UB_CUDA(cudaMemcpy(t->d_npred_x.p, npred_x.data(), sizeof(uint32_t) * npred_x.size(),
-                               cudaMemcpyHostToDevice));
-        t->d_succ_off.alloc(succ_off.size());
-        UB_CUDA(cudaMemcpy(t->d_succ_off.p, succ_off.data(), sizeof(uint32_t) * succ_off.size(),
-                           cudaMemcpyHostToDevice));
-        t->d_succs.alloc(std::max<size_t>(succs.size(), 1));
-        if (!succs.empty())
-            UB_CUDA(cudaMemcpy(t->d_succs.p, succs.data(), sizeof(uint32_t) * succs.size(),
-                               cudaMemcpyHostToDevice));
+    sched.finish(R.order, R.level_off);
+    R.levels = sched.levels();
+    R.pred_off = sched.pred_off();
+    R.preds = sched.preds();
+    sched.cross(R.npred_x, R.succ_off, R.succs);
+}
+
+template <class T>
+void upload(DevBuf<T>& d, const std::vector<T>& h) {
+    d.alloc(std::max<size_t>(h.size(), 1));
+    if (!h.empty())
+        UB_CUDA(cudaMemcpy(d.p, h.data(), sizeof(T) * h.size(), cudaMemcpyHostToDevice));
+}
+
+void build_schedule(uscg_tracer_s* t) {
+    if (t->sched_built)
+        return;
+    const auto h0 = std::chrono::steady_clock::now();
+    t->run = run_length(t->lines, t->volume != 0);
+    // a run's index lists live in shared memory (4 groups per CTA): keep the
+    // per-group lists under ~48 KiB
+    while (t->run > 1 && size_t(t->run) * size_t(t->max_cells) * 4 > 48 * 1024) {
+        int r = t->run - 1;
+        while (r > 1 && t->lines % r != 0)
+            --r;
+        t->run = r;
     }
+    t->runs_per_view = t->lines / t->run;
+    t->n_runs = t->views * t->runs_per_view;
+    RunSchedule R;
+    const char* host = std::getenv("USCG_HOST_SCHEDULE");
+    if (host && std::atoi(host)) {
+        host_schedule(t, R);
+    } else {
+        std::vector<unsigned long long> edges;
+        gpu_schedule_edges(t->trace_args(), t->views, t->max_recs, t->max_cells, t->cells, t->cells_per_sweep,
+                           uint32_t(t->run), uint32_t(t->runs_per_view), edges, t->st());
+        schedule_from_edges(edges, uint32_t(t->n_runs), R);
+    }
+    t->level_off = R.level_off;
+    upload(t->d_order, R.order);
+    upload(t->d_level_off, t->level_off);
+    t->d_bar.alloc(2);
+    upload(t->d_pred_off, R.pred_off);
+    upload(t->d_preds, R.preds);
+    t->n_preds = R.preds.size();
+    upload(t->d_npred_x, R.npred_x);
+    upload(t->d_succ_off, R.succ_off);
+    upload(t->d_succs, R.succs);
     t->sched_built = true;
-    t->schedule_seconds =
-        std::chrono::duration<double>(std::chrono::steady_clock::now() - h0).count();
-    cudaEventDestroy(e0);
-    cudaEventDestroy(e1);
+    t->schedule_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - h0).count();
 }
 
 // One sweep = one graph replay: every dependency level is a kernel node.
@@ -862,6 +913,33 @@ uscg_status uscg_trace_counts(uscg_tracer t, uint32_t* cells_out) {
     return guarded([&] {
         need(t && cells_out, "null argument");
         std::memcpy(cells_out, t->h_cells.data(), sizeof(uint32_t) * t->h_cells.size());
+    });
+}
+
+uscg_status uscg_tracer_export_schedule(uscg_tracer t, int32_t* run, uint32_t* runs, uint32_t* levels,
+                                        uint64_t* n_preds, uint32_t* order, uint32_t* level_off,
+                                        uint32_t* pred_off, uint32_t* preds, uint32_t* npred_x) {
+    return guarded([&] {
+        need(t != nullptr, "null tracer");
+        bind(t->ctx);
+        build_schedule(t);
+        if (run)
+            *run = t->run;
+        if (runs)
+            *runs = uint32_t(t->n_runs);
+        if (levels)
+            *levels = uint32_t(t->level_off.size()) - 1;
+        if (n_preds)
+            *n_preds = t->n_preds;
+        auto get = [&](uint32_t* dst, const DevBuf<uint32_t>& src, size_t n) {
+            if (dst && n)
+                UB_CUDA(cudaMemcpy(dst, src.p, sizeof(uint32_t) * n, cudaMemcpyDeviceToHost));
+        };
+        get(order, t->d_order, size_t(t->n_runs));
+        get(level_off, t->d_level_off, t->level_off.size());
+        get(pred_off, t->d_pred_off, size_t(t->n_runs) + 1);
+        get(preds, t->d_preds, t->n_preds);
+        get(npred_x, t->d_npred_x, size_t(t->n_runs));
     });
 }
 

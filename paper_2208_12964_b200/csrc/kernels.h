@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <vector>
 
 #include "internal.cuh"
 
@@ -155,6 +156,12 @@ void launch_csr_level(const uint32_t* units, int n, const uint32_t* off, const u
 void launch_otf_level(const DevCart& C, int lines, const double* rays, const double* theta, const uint32_t* units,
                       int n, const float* proj, float* f, double beta, double p_floor, unsigned long long* clamps,
                       cudaStream_t st);
+
+// the MART dependency edges on the device (schedule_gpu.cu): sorted unique
+// (succ_run << 32 | pred_run), pred word | 0x80000000 for cross-sweep edges
+void gpu_schedule_edges(const TraceArgs& A, int views, int max_recs, int max_cells, uint64_t cells,
+                        uint64_t visits, uint32_t run, uint32_t runs_per_view,
+                        std::vector<unsigned long long>& out_edges, cudaStream_t st);
 
 // K4 resample
 void launch_perm_resample(const float* field, uint64_t cells_per_slice, int slices, int S, int Sp,

@@ -117,7 +117,7 @@ EXPORTS = [
     "uscg_ctx_set_stream", "uscg_ctx_synchronize", "uscg_first_view_rays", "uscg_tracer_create",
     "uscg_tracer_create_from_rays", "uscg_tracer_import_cache", "uscg_tracer_destroy",
     "uscg_tracer_get_info", "uscg_tracer_export_cache", "uscg_trace_line", "uscg_trace_counts",
-    "uscg_trace_checksums",
+    "uscg_trace_checksums", "uscg_tracer_export_schedule",
     "uscg_tracer_build_schedule", "uscg_problem_stride", "uscg_project", "uscg_reconstruct",
     "uscg_resample", "uscg_uspg_to_cg_map", "uscg_diag_math", "uscg_schedule_build", "uscg_image_metrics",
     "uscg_cartesian_like", "uscg_csystem_create", "uscg_csystem_info", "uscg_csystem_export",
@@ -163,6 +163,8 @@ def load(build_if_missing: bool = True):
     L.uscg_trace_counts.argtypes = [vp, _u32p]
     L.uscg_trace_checksums.argtypes = [vp, C.c_int32, C.c_int32, vp, vp, C.c_uint32]
     L.uscg_tracer_build_schedule.argtypes = [vp]
+    L.uscg_tracer_export_schedule.argtypes = [vp, C.POINTER(C.c_int32), _u32p, _u32p, C.POINTER(C.c_uint64), _u32p,
+                                              _u32p, _u32p, _u32p, _u32p]
     L.uscg_problem_stride.argtypes = [C.c_int32]
     L.uscg_problem_stride.restype = C.c_int32
     L.uscg_project.argtypes = [vp, vp, C.c_int32, vp, C.c_uint32]
@@ -522,6 +524,23 @@ class Tracer:
         sums = np.zeros(nviews * inf["lines"], np.uint64)
         _check(load().uscg_trace_checksums(self.h, int(view0), int(nviews), counts.ctypes.data, sums.ctypes.data, 0))
         return counts.reshape(nviews, inf["lines"]), sums.reshape(nviews, inf["lines"])
+
+    def schedule(self) -> dict:
+        """The dataflow executor's run schedule: run, runs, levels, order,
+        level_off, pred_off, preds, npred_x (numpy u32 arrays)."""
+        L = load()
+        run, runs, levels, npr = C.c_int32(), C.c_uint32(), C.c_uint32(), C.c_uint64()
+        _check(L.uscg_tracer_export_schedule(self.h, C.byref(run), C.byref(runs), C.byref(levels), C.byref(npr),
+                                             None, None, None, None, None))
+        R, V, P = runs.value, levels.value, npr.value
+        out = {k: np.zeros(n, np.uint32) for k, n in (("order", R), ("level_off", V + 1), ("pred_off", R + 1),
+                                                      ("preds", max(P, 1)), ("npred_x", R))}
+        _check(L.uscg_tracer_export_schedule(self.h, C.byref(run), C.byref(runs), C.byref(levels), C.byref(npr),
+                                             *[out[k].ctypes.data_as(_u32p) for k in
+                                               ("order", "level_off", "pred_off", "preds", "npred_x")]))
+        out["preds"] = out["preds"][:P]
+        out.update(run=run.value, runs=R, levels=V)
+        return out
 
     def build_schedule(self) -> int:
         _check(load().uscg_tracer_build_schedule(self.h))

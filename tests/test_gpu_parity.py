@@ -757,3 +757,28 @@ def test_cartesian_mart_matches_reference(ub, ref, stored):
     got, sec = cs.reconstruct(proj, ub.SolverConfig(beta=0.4, tolerance=0, max_sweeps=3))
     assert sec > 0
     np.testing.assert_allclose(got, want, rtol=1e-4, atol=1e-6)
+
+
+# ---------------------------------------------------------------------------
+# the dependency schedule built on the device (schedule_gpu.cu)
+# ---------------------------------------------------------------------------
+
+
+@pytest.mark.parametrize("case", ["fan16", "fan32", "cone16", "cone32", "m1arc"])
+def test_device_schedule_equals_host_schedule(ub, orc, monkeypatch, case):
+    """The sort-based device builder yields exactly the host AsapSchedule:
+    the same runs, levels, level-sorted order, in-sweep predecessors and
+    cross-sweep predecessor counts."""
+    def build(host):
+        monkeypatch.setenv("USCG_HOST_SCHEDULE", "1" if host else "0")
+        if case == "m1arc":
+            _, _, tr, _ = _m1_case(ub, orc, "arc", n_rings=40, views=20, du=48)
+        else:
+            _, _, tr = _ub_tracer(ub, REF_GEOMS[case])
+        return tr.schedule()
+
+    got, want = build(False), build(True)
+    for k in ("run", "runs", "levels"):
+        assert got[k] == want[k], k
+    for k in ("order", "level_off", "pred_off", "preds", "npred_x"):
+        assert np.array_equal(got[k], want[k]), k

@@ -260,7 +260,8 @@ def bench_c5(args, rank, world, local):
     store, |active| + index checksum per line (lines/s; bytes 20*C + 12*L per
     view); (3) resampling a seeded U[0,1] 512-ring x 512-slice USPG volume to
     1024 x 1024 x 512 (8 B per output pixel). N > 1 ranks split detector rows,
-    views and slices (strong scaling; no data-path exchange)."""
+    views and slices (strong scaling); the generator's one exchange assembles
+    the full record store on every rank (dist.assemble_cache)."""
     import torch
     import torch.distributed as dist
 
@@ -301,8 +302,27 @@ def bench_c5(args, rank, world, local):
     g_ms = float(np.mean(gen_ms))
     rays_mine = (r1 - r0) * geom.det_u
 
-    # (2) rotated reuse over this rank's views, full record store per rank
-    tr = ub.Tracer(geom, spec, False, ctx=ctx)
+    # the full record store on every rank: one rank alone generates it; N
+    # ranks exchange their row blocks (dist.assemble_cache: all-gather of the
+    # counts and of the padded segments over NCCL)
+    exchange_ms = 0.0
+    if world > 1:
+        local_tr = ub.Tracer.from_rays(spec, src[mine], det[mine], 1, ctx=ctx)
+        part = local_tr.copy_cache(device=True)
+        local_tr.close()
+        torch.cuda.synchronize()
+        dist.barrier()
+        x0, x1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        x0.record(stream)
+        full = udist.assemble_cache(*part)
+        x1.record(stream)
+        torch.cuda.synchronize()
+        exchange_ms = x0.elapsed_time(x1)
+        tr = ub.Tracer.from_key_cache(spec, *full, geom.views, geom.view_angles, geom=geom, ctx=ctx)
+        del full, part
+    else:
+        tr = ub.Tracer(geom, spec, False, ctx=ctx)
+    # (2) rotated reuse over this rank's views
     inf = tr.info()
     v0, v1 = rank * geom.views // world, (rank + 1) * geom.views // world
     nv = v1 - v0
@@ -384,7 +404,8 @@ def bench_c5(args, rank, world, local):
     launches = ub.launch_count() - launches0
     clk = clocks.stop()
     px = (sl1 - sl0) * npix * npix
-    g_ms, reuse_ms, res_ms, met_ms = udist.max_over_ranks([g_ms, reuse_ms, res_ms, met_ms], device="cuda")
+    g_ms, reuse_ms, res_ms, met_ms, exchange_ms = udist.max_over_ranks(
+        [g_ms, reuse_ms, res_ms, met_ms, exchange_ms], device="cuda")
     rays_all, recs_all = udist.sum_over_ranks([rays_mine, recs], device="cuda")
 
     if rank != 0:
@@ -416,7 +437,7 @@ def bench_c5(args, rank, world, local):
         cpu = {"value": pick.size / wall, "unit": "rays/s", "cores": 1, "kind": "port",
                "sample": f"oracle C restatement of precompute_first_view on {pick.size} random rays of the panel "
                          f"({wall:.1f} s, {int(oc.offsets[-1])} records)"}
-    value = rays_all / (g_ms * 1e-3)
+    value = rays_all / ((g_ms + exchange_ms) * 1e-3)  # generation + the exchange that assembles the store
     line = {
         "metric": "first-view generator rays/s (c5)", "value": value, "unit": "rays/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": g_ms, "higher_is_better": True,
@@ -429,7 +450,8 @@ def bench_c5(args, rank, world, local):
                    "parallelism": "rows / views / slices split across ranks"},
         "roofline": roof(gen_bytes, g_ms, "generate_count_kernel + generate_write_kernel + annotate_kernel",
                          "20*records + 4*(lines+1) written (SURVEY.md §8(d))"),
-        "generator": {"ms": g_ms, "rays": rays_all, "records": recs_all, "records_per_s": recs_all / (g_ms * 1e-3)},
+        "generator": {"ms": g_ms, "exchange_ms": exchange_ms, "rays": rays_all, "records": recs_all,
+                      "records_per_s": recs_all / ((g_ms + exchange_ms) * 1e-3)},
         "rotated_reuse": {"ms": reuse_ms, "views": geom.views, "lines_per_s": world * nv * lines / (reuse_ms * 1e-3),
                           "chords_per_s": world * chords / (reuse_ms * 1e-3), "counts_match_library": reuse_ok,
                           "roofline": roof(reuse_bytes_all, reuse_ms, "checksum_kernel<128>",

@@ -160,6 +160,18 @@ uscg_status uscg_tracer_import_cache(uscg_ctx ctx, const uscg_grid* grid, int32_
                                      const double* phi_a, const double* phi_b,
                                      const uint16_t* slice, const uint16_t* ring, int32_t views,
                                      const double* view_angles_deg, uscg_tracer* out);
+/* The record store in its device layout (offsets lines+1 u32; phi_a, phi_b
+ * records f64; keys records u32 = ring | slice << 12 | dedup flag << 31) into
+ * caller buffers, host or (USCG_DEVICE_POINTERS) device. */
+uscg_status uscg_tracer_copy_cache(uscg_tracer tracer, uint32_t* offsets, double* phi_a, double* phi_b,
+                                   uint32_t* keys, uint32_t flags);
+/* uscg_tracer_import_cache from that layout, host or (USCG_DEVICE_POINTERS)
+ * device arrays: the assembly step of the row-sharded multi-GPU generator
+ * (dedup flags are recomputed). */
+uscg_status uscg_tracer_import_cache_keys(uscg_ctx ctx, const uscg_grid* grid, int32_t lines,
+                                          const uint32_t* offsets, uint64_t records, const double* phi_a,
+                                          const double* phi_b, const uint32_t* keys, int32_t views,
+                                          const double* view_angles_deg, uint32_t flags, uscg_tracer* out);
 uscg_status uscg_tracer_destroy(uscg_tracer tracer);
 uscg_status uscg_tracer_get_info(uscg_tracer tracer, uscg_tracer_info* info);
 /* FirstViewCache::offsets()/records() (tracer.hpp:28-29) to host arrays */

@@ -802,6 +802,66 @@ uscg_status uscg_tracer_import_cache(uscg_ctx ctx, const uscg_grid* grid, int32_
     });
 }
 
+uscg_status uscg_tracer_copy_cache(uscg_tracer t, uint32_t* offsets, double* phi_a, double* phi_b,
+                                   uint32_t* keys, uint32_t flags) {
+    return guarded([&] {
+        need(t != nullptr, "null tracer");
+        bind(t->ctx);
+        need(offsets && phi_a && phi_b && keys, "null buffer");
+        const cudaMemcpyKind k = (flags & USCG_DEVICE_POINTERS) ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
+        cudaStream_t st = t->st();
+        UB_CUDA(cudaMemcpyAsync(offsets, t->d_off.p, sizeof(uint32_t) * (size_t(t->lines) + 1), k, st));
+        if (t->records) {
+            UB_CUDA(cudaMemcpyAsync(phi_a, t->d_pa.p, sizeof(double) * t->records, k, st));
+            UB_CUDA(cudaMemcpyAsync(phi_b, t->d_pb.p, sizeof(double) * t->records, k, st));
+            UB_CUDA(cudaMemcpyAsync(keys, t->d_key.p, sizeof(uint32_t) * t->records, k, st));
+        }
+        UB_CUDA(cudaStreamSynchronize(st));
+    });
+}
+
+uscg_status uscg_tracer_import_cache_keys(uscg_ctx ctx, const uscg_grid* grid, int32_t lines,
+                                          const uint32_t* offsets, uint64_t records, const double* phi_a,
+                                          const double* phi_b, const uint32_t* keys, int32_t views,
+                                          const double* view_angles_deg, uint32_t flags, uscg_tracer* out) {
+    return guarded([&] {
+        bind(ctx);
+        need(out != nullptr, "null output");
+        validate_grid(grid);
+        need(lines >= 1 && offsets, "line count must be >= 1");
+        need(records < (1ull << 32), "record count must fit in 32 bits");
+        const bool dev = flags & USCG_DEVICE_POINTERS;
+        const cudaMemcpyKind k = dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+        std::vector<uint32_t> off(size_t(lines) + 1);
+        UB_CUDA(cudaMemcpy(off.data(), offsets, sizeof(uint32_t) * off.size(),
+                           dev ? cudaMemcpyDeviceToHost : cudaMemcpyHostToHost));
+        need(off[0] == 0 && off[lines] == records, "offsets do not match the record count");
+        for (int l = 0; l < lines; ++l)
+            need(off[l] <= off[l + 1], "offsets must be non-decreasing");
+        std::unique_ptr<uscg_tracer_s> t(new uscg_tracer_s);
+        t->ctx = ctx;
+        t->device = ctx->device;
+        fill_grid(t.get(), grid);
+        fill_views(t.get(), views, view_angles_deg);
+        t->lines = lines;
+        t->records = records;
+        const size_t R = std::max<size_t>(records, 1);
+        t->d_off.alloc(size_t(lines) + 1);
+        t->d_pa.alloc(R);
+        t->d_pb.alloc(R);
+        t->d_key.alloc(R);
+        UB_CUDA(cudaMemcpy(t->d_off.p, off.data(), sizeof(uint32_t) * off.size(), cudaMemcpyHostToDevice));
+        if (records) {
+            UB_CUDA(cudaMemcpy(t->d_pa.p, phi_a, sizeof(double) * records, k));
+            UB_CUDA(cudaMemcpy(t->d_pb.p, phi_b, sizeof(double) * records, k));
+            UB_CUDA(cudaMemcpy(t->d_key.p, keys, sizeof(uint32_t) * records, k));
+            launch_clear_flags(t->d_key.p, records, t->st());
+        }
+        finish_tracer(t.get(), off);  // validates nothing further; annotate sets the dedup flags
+        *out = t.release();
+    });
+}
+
 uscg_status uscg_tracer_destroy(uscg_tracer tracer) {
     return guarded([&] {
         if (!tracer)

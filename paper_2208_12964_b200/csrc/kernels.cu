@@ -573,6 +573,18 @@ __global__ void annotate_kernel(int lines, const uint32_t* __restrict__ off,
     }
 }
 
+__global__ void clear_flags_kernel(uint32_t* key, uint64_t n) {
+    for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x)
+        key[i] &= ~kFlagBit;
+}
+
+void launch_clear_flags(uint32_t* key, uint64_t n, cudaStream_t st) {
+    if (n == 0)
+        return;
+    clear_flags_kernel<<<unsigned(std::min<uint64_t>((n + 255) / 256, 148 * 16)), 256, 0, st>>>(key, n);
+    check_launch();
+}
+
 void launch_annotate(int lines, const uint32_t* off, const double* pa, const double* pb,
                      uint32_t* key, const RingRow* rings, cudaStream_t st) {
     if (lines <= 0)

@@ -39,6 +39,8 @@ void launch_generate_write(const DevGrid& g, int lines, const double* src, const
                            cudaStream_t st);
 void launch_annotate(int lines, const uint32_t* off, const double* pa, const double* pb,
                      uint32_t* key, const RingRow* rings, cudaStream_t st);
+// drop the dedup flags of imported keys (annotate sets them again)
+void launch_clear_flags(uint32_t* key, uint64_t n, cudaStream_t st);
 void launch_exclusive_scan_u32(const uint32_t* in, uint32_t* out, int n, cudaStream_t st);
 
 // traces

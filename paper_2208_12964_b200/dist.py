@@ -74,3 +74,78 @@ def gather_stack(local: np.ndarray, n_total: int, rank: int, world: int, device=
         return None
     rows = [parts[r][: shard(n_total, r, world)[1] - shard(n_total, r, world)[0]] for r in range(world)]
     return torch.cat(rows).cpu().numpy().reshape((n_total,) + local.shape[1:])
+
+
+# ---------------------------------------------------------------------------
+# row-sharded first-view generator (generator row)
+# ---------------------------------------------------------------------------
+
+
+def concat_caches(parts):
+    """Concatenate record stores of consecutive line blocks, in block order:
+    parts = [(offsets, phi_a, phi_b, keys), ...] (torch tensors; offsets local,
+    starting at 0, as int32 bit patterns of u32). Returns the full store."""
+    import torch
+    dev = parts[0][0].device
+    base = 0
+    offs, pas, pbs, keys = [], [], [], []
+    for off, pa, pb, key in parts:
+        L = off.numel() - 1
+        offs.append(off[:L].to(torch.int64) + base)
+        pas.append(pa)
+        pbs.append(pb)
+        keys.append(key)
+        base += pa.numel()
+    offs.append(torch.tensor([base], dtype=torch.int64, device=dev))
+    if base >= 1 << 32:
+        raise ValueError("record count must fit in 32 bits")
+    full_off = torch.cat(offs)
+    full_off = torch.where(full_off >= 1 << 31, full_off - (1 << 32), full_off).to(torch.int32)  # u32 bits
+    return full_off, torch.cat(pas), torch.cat(pbs), torch.cat(keys)
+
+
+def assemble_cache(off, pa, pb, key):
+    """The generator's one exchange: every rank holds the records of a
+    contiguous block of lines; all ranks receive the full store. All-gather of
+    the per-rank (lines, records) counts, then one all-gather per array of the
+    segments padded to the largest (NCCL on the GPU, gloo on the CPU), and the
+    record bases from an exclusive scan of the counts (concat_caches)."""
+    import torch
+    import torch.distributed as dist
+    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size() == 1:
+        return off, pa, pb, key
+    world = dist.get_world_size()
+    dev = off.device
+    counts = torch.tensor([off.numel() - 1, pa.numel()], dtype=torch.int64, device=dev)
+    allc = [torch.zeros_like(counts) for _ in range(world)]
+    dist.all_gather(allc, counts)
+    Ls = [int(c[0]) for c in allc]
+    Rs = [int(c[1]) for c in allc]
+
+    def gather(t, n, m):
+        pad = torch.zeros(max(m, 1), dtype=t.dtype, device=dev)
+        pad[:n] = t[:n]
+        parts = [torch.empty_like(pad) for _ in range(world)]
+        dist.all_gather(parts, pad)
+        return parts
+
+    offp = gather(off, Ls[dist.get_rank()] + 1, max(Ls) + 1)
+    pap = gather(pa, pa.numel(), max(Rs))
+    pbp = gather(pb, pb.numel(), max(Rs))
+    kp = gather(key, key.numel(), max(Rs))
+    return concat_caches([(offp[r][: Ls[r] + 1], pap[r][: Rs[r]], pbp[r][: Rs[r]], kp[r][: Rs[r]])
+                          for r in range(world)])
+
+
+def generate_sharded(spec, geom, rank: int, world: int, ctx=None):
+    """Rank `rank` generates the first-view records of detector rows
+    shard(det_v) and every rank assembles the full tracer (assemble_cache)."""
+    from .uscg import Tracer
+    src, det = geom.first_view_rays()
+    r0, r1 = shard(geom.det_v, rank, world)
+    l0, l1 = r0 * geom.det_u, r1 * geom.det_u
+    local = Tracer.from_rays(spec, src[l0:l1], det[l0:l1], 1, ctx=ctx)
+    part = local.copy_cache(device=True)
+    local.close()
+    full = assemble_cache(*part)
+    return Tracer.from_key_cache(spec, *full, geom.views, geom.view_angles, geom=geom, ctx=ctx)

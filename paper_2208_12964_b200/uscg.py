@@ -117,7 +117,8 @@ EXPORTS = [
     "uscg_ctx_set_stream", "uscg_ctx_synchronize", "uscg_first_view_rays", "uscg_tracer_create",
     "uscg_tracer_create_from_rays", "uscg_tracer_import_cache", "uscg_tracer_destroy",
     "uscg_tracer_get_info", "uscg_tracer_export_cache", "uscg_trace_line", "uscg_trace_counts",
-    "uscg_trace_checksums", "uscg_tracer_export_schedule",
+    "uscg_trace_checksums", "uscg_tracer_export_schedule", "uscg_tracer_copy_cache",
+    "uscg_tracer_import_cache_keys",
     "uscg_tracer_build_schedule", "uscg_problem_stride", "uscg_project", "uscg_reconstruct",
     "uscg_resample", "uscg_uspg_to_cg_map", "uscg_diag_math", "uscg_schedule_build", "uscg_image_metrics",
     "uscg_cartesian_like", "uscg_csystem_create", "uscg_csystem_info", "uscg_csystem_export",
@@ -157,6 +158,9 @@ def load(build_if_missing: bool = True):
     L.uscg_tracer_import_cache.argtypes = [vp, C.POINTER(_Grid), C.c_int32, _u32p, C.c_uint64, _dp, _dp, _u16p,
                                            _u16p, C.c_int32, _dp, C.POINTER(vp)]
     L.uscg_tracer_destroy.argtypes = [vp]
+    L.uscg_tracer_copy_cache.argtypes = [vp, vp, vp, vp, vp, C.c_uint32]
+    L.uscg_tracer_import_cache_keys.argtypes = [vp, C.POINTER(_Grid), C.c_int32, vp, C.c_uint64, vp, vp, vp,
+                                                C.c_int32, _dp, C.c_uint32, C.POINTER(vp)]
     L.uscg_tracer_get_info.argtypes = [vp, C.POINTER(_Info)]
     L.uscg_tracer_export_cache.argtypes = [vp, _u32p, _dp, _dp, _u16p, _u16p]
     L.uscg_trace_line.argtypes = [vp, C.c_int32, C.c_double, _u32p, C.c_int64, C.POINTER(C.c_int64)]
@@ -469,6 +473,40 @@ class Tracer:
                                                ang.ctypes.data_as(_dp) if ang is not None else None, C.byref(h)))
         if geom is None:
             geom = ScanGeometry(det_u=off.size - 1, views=views, view_angles=ang)
+        return cls(geom, spec, ctx=ctx, _handle=h)
+
+    def copy_cache(self, device: bool = True):
+        """The record store in the device layout as torch tensors (on this
+        tracer's GPU, or the host): offsets (lines+1) and keys (records) as
+        int32 bit patterns of the u32 values, phi_a / phi_b float64."""
+        import torch
+        inf = self.info()
+        where = torch.device("cuda", self.ctx.device) if device else torch.device("cpu")
+        off = torch.empty(inf["lines"] + 1, dtype=torch.int32, device=where)
+        pa = torch.empty(max(inf["records"], 1), dtype=torch.float64, device=where)
+        pb = torch.empty_like(pa)
+        key = torch.empty(max(inf["records"], 1), dtype=torch.int32, device=where)
+        _check(load().uscg_tracer_copy_cache(self.h, off.data_ptr(), pa.data_ptr(), pb.data_ptr(), key.data_ptr(),
+                                             DEVICE_POINTERS if device else 0))
+        R = inf["records"]
+        return off, pa[:R], pb[:R], key[:R]
+
+    @classmethod
+    def from_key_cache(cls, spec: GridSpec, offsets, phi_a, phi_b, keys, views: int, view_angles=None,
+                       geom: Optional[ScanGeometry] = None, ctx: Optional[Context] = None) -> "Tracer":
+        """Import a record store in the device layout (torch tensors, CUDA or CPU)."""
+        ctx = ctx or default_context()
+        dev = offsets.is_cuda
+        ang = None if view_angles is None else np.ascontiguousarray(view_angles, dtype=np.float64)
+        g, keep = spec._c()
+        h = C.c_void_p()
+        _check(load().uscg_tracer_import_cache_keys(ctx.h, C.byref(g), int(offsets.numel()) - 1, offsets.data_ptr(),
+                                                    int(phi_a.numel()), phi_a.data_ptr(), phi_b.data_ptr(),
+                                                    keys.data_ptr(), views,
+                                                    ang.ctypes.data_as(_dp) if ang is not None else None,
+                                                    DEVICE_POINTERS if dev else 0, C.byref(h)))
+        if geom is None:
+            geom = ScanGeometry(det_u=int(offsets.numel()) - 1, views=views, view_angles=ang)
         return cls(geom, spec, ctx=ctx, _handle=h)
 
     def close(self) -> None:

@@ -782,3 +782,37 @@ def test_device_schedule_equals_host_schedule(ub, orc, monkeypatch, case):
         assert got[k] == want[k], k
     for k in ("order", "level_off", "pred_off", "preds", "npred_x"):
         assert np.array_equal(got[k], want[k]), k
+
+
+# ---------------------------------------------------------------------------
+# row-sharded generator on the device (dist.generate_sharded / concat_caches)
+# ---------------------------------------------------------------------------
+
+
+@pytest.mark.parametrize("name", ["cone16", "cone32w"])
+def test_row_sharded_generator_assembles_the_same_store(ub, name):
+    """Rows generated in blocks and assembled (copy_cache -> concat_caches ->
+    from_key_cache) give the directly generated store, dedup flags included,
+    and the same traces."""
+    import torch
+    from paper_2208_12964_b200 import dist as udist
+    g = REF_GEOMS[name]
+    spec, geom = ub_spec_geom(ub, g)
+    direct = ub.Tracer(geom, spec, False)
+    src, det = geom.first_view_rays()
+    parts = []
+    for r in range(3):
+        r0, r1 = udist.shard(g["dv"], r, 3)
+        t = ub.Tracer.from_rays(spec, src[r0 * g["du"]:r1 * g["du"]], det[r0 * g["du"]:r1 * g["du"]], 1)
+        parts.append(t.copy_cache(device=True))
+        t.close()
+    full = udist.concat_caches(parts)
+    asm = ub.Tracer.from_key_cache(spec, *full, g["views"], geom=geom)
+    for a, b in zip(asm.copy_cache(device=True), direct.copy_cache(device=True)):
+        assert torch.equal(a, b)
+    th = thetas(g["views"])
+    for line in range(0, geom.lines(), 7):
+        assert np.array_equal(asm.trace_line(line, th[1]), direct.trace_line(line, th[1]))
+    one = udist.generate_sharded(spec, geom, 0, 1)  # world 1: no exchange
+    for a, b in zip(one.copy_cache(device=True), direct.copy_cache(device=True)):
+        assert torch.equal(a, b)

@@ -85,3 +85,55 @@ def test_two_rank_slice_sharding_matches_single_process(tmp_path):
     assert np.array_equal(stack, want.astype(np.float32))
     assert list(red[:2]) == [2.0, 5.0]     # max over ranks
     assert red[2] == S                      # every slice reconstructed once
+
+
+# ---------------------------------------------------------------------------
+# row-sharded generator: the exchange (generator row)
+# ---------------------------------------------------------------------------
+
+
+def _cone_rays():
+    import oracle
+    orc = oracle.Orc()
+    grid = oracle.OrcGrid.reference(12, True)
+    # 5 x 7 flat panel: the row blocks of two ranks are uneven
+    s, d = orc.rays_flat((-3, 0, 0), (10, 0, 0), 5, 7, 1.0, 1.0)
+    return orc, grid, s, d
+
+
+def _key_layout(oc):
+    """record store of an oracle cache in the device layout (keys without flags)"""
+    import torch
+    rec = oc.records
+    keys = rec["ring"].astype(np.uint32) | (rec["slice"].astype(np.uint32) << 12)
+    return (torch.from_numpy(oc.offsets.astype(np.uint32).view(np.int32).copy()),
+            torch.from_numpy(rec["phi_a"].copy()), torch.from_numpy(rec["phi_b"].copy()),
+            torch.from_numpy(keys.view(np.int32).copy()))
+
+
+def _gen_worker(rank, world, port, out_dir):
+    import sys
+    sys.path.insert(0, ROOT)
+    import torch.distributed as dist
+    from paper_2208_12964_b200 import dist as udist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(world))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    orc, grid, s, d = _cone_rays()
+    r0, r1 = udist.shard(7, rank, world)
+    part = _key_layout(orc.cache(grid, s[r0 * 5:r1 * 5], d[r0 * 5:r1 * 5]))
+    full = udist.assemble_cache(*part)
+    dist.barrier()
+    if rank == 0:
+        np.savez(os.path.join(out_dir, "full.npz"), *[t.numpy() for t in full])
+    dist.destroy_process_group()
+
+
+@pytest.mark.timeout(300)
+def test_two_rank_generator_exchange_assembles_the_full_store(tmp_path):
+    port = _free_port()
+    mp.spawn(_gen_worker, args=(2, port, str(tmp_path)), nprocs=2, join=True)
+    got = np.load(tmp_path / "full.npz")
+    orc, grid, s, d = _cone_rays()
+    want = [t.numpy() for t in _key_layout(orc.cache(grid, s, d))]
+    for k, w in enumerate(want):
+        assert np.array_equal(got[f"arr_{k}"], w), k

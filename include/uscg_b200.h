@@ -202,6 +202,10 @@ uscg_status uscg_tracer_build_schedule(uscg_tracer tracer);
 uscg_status uscg_tracer_export_schedule(uscg_tracer tracer, int32_t* run, uint32_t* runs, uint32_t* levels,
                                         uint64_t* n_preds, uint32_t* order, uint32_t* level_off,
                                         uint32_t* pred_off, uint32_t* preds, uint32_t* npred_x);
+/* its merged successor lists (in- and cross-sweep, the dependency counters'
+ * push targets): succ_off [runs + 1], succs [n_succs]; NULL arrays are skipped */
+uscg_status uscg_tracer_export_successors(uscg_tracer tracer, uint64_t* n_succs, uint32_t* succ_off,
+                                          uint32_t* succs);
 /* stride of the interleaved problem dimension for S problems */
 int32_t uscg_problem_stride(int32_t problems);
 

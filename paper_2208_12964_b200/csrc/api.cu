@@ -137,7 +137,7 @@ struct uscg_tracer_s {
     DevBuf<unsigned> d_bar;
     DevBuf<uint32_t> d_pred_off, d_preds, d_succ_off, d_succs, d_npred_x;
     int run = 1, n_runs = 0, runs_per_view = 0;  // run-granular schedule (dataflow)
-    uint64_t n_preds = 0;
+    uint64_t n_preds = 0, n_succs = 0;
     DevBuf<unsigned> d_done;  // dataflow flags [units * nchunks]
     DevBuf<uint32_t> w_slab;  // dataflow trace slab
     DevBuf<unsigned> w_slab_ctl;
@@ -473,63 +473,11 @@ int run_length(int lines, bool volume) {
     return 1;
 }
 
-// The run DAG from the device-built edges (schedule_gpu.cu: sorted unique
-// succ << 32 | pred, pred | 0x80000000 for cross-sweep): the same structures
-// AsapSchedule produces (schedule.cpp) — in-sweep preds ascending, ASAP levels
-// in run order (preds precede their successors), level-sorted order, merged
-// successor lists in the same order.
+// The run DAG of the host builder (AsapSchedule, USCG_HOST_SCHEDULE=1)
 struct RunSchedule {
     std::vector<uint32_t> order, level_off, pred_off, preds, npred_x, succ_off, succs;
     uint32_t levels = 0;
 };
-
-void schedule_from_edges(const std::vector<unsigned long long>& edges, uint32_t runs, RunSchedule& R) {
-    R.pred_off.assign(size_t(runs) + 1, 0u);
-    R.npred_x.assign(runs, 0u);
-    R.preds.clear();
-    R.preds.reserve(edges.size());
-    std::vector<uint32_t> succ_cnt(size_t(runs) + 1, 0u);
-    for (unsigned long long e : edges) {
-        const uint32_t u = uint32_t(e >> 32), p = uint32_t(e) & 0x7FFFFFFFu;
-        if (uint32_t(e) & 0x80000000u)
-            ++R.npred_x[u];
-        else {
-            R.preds.push_back(p);
-            ++R.pred_off[size_t(u) + 1];
-        }
-        ++succ_cnt[size_t(p) + 1];
-    }
-    for (uint32_t u = 0; u < runs; ++u)
-        R.pred_off[size_t(u) + 1] += R.pred_off[u];
-    // levels (1-based) in run order
-    std::vector<uint32_t> level(runs, 0u);
-    R.levels = 0;
-    for (uint32_t u = 0; u < runs; ++u) {
-        uint32_t lev = 0;
-        for (uint32_t k = R.pred_off[u]; k < R.pred_off[size_t(u) + 1]; ++k)
-            lev = std::max(lev, level[R.preds[k]]);
-        level[u] = lev + 1;
-        R.levels = std::max(R.levels, lev + 1);
-    }
-    std::vector<uint32_t> cnt(size_t(R.levels) + 2, 0u);
-    for (uint32_t l : level)
-        ++cnt[l];
-    R.level_off.assign(size_t(R.levels) + 1, 0u);
-    for (uint32_t l = 1; l <= R.levels; ++l)
-        R.level_off[l] = R.level_off[l - 1] + cnt[l];
-    std::vector<uint32_t> at(R.level_off.begin(), R.level_off.end());
-    R.order.assign(runs, 0u);
-    for (uint32_t u = 0; u < runs; ++u)
-        R.order[at[level[u] - 1]++] = u;
-    // successors: for each u ascending, its in-sweep then cross preds (edge order)
-    for (uint32_t u = 0; u < runs; ++u)
-        succ_cnt[size_t(u) + 1] += succ_cnt[u];
-    R.succ_off = succ_cnt;
-    R.succs.assign(edges.size(), 0u);
-    std::vector<uint32_t> cur(R.succ_off.begin(), R.succ_off.end() - 1);
-    for (unsigned long long e : edges)
-        R.succs[cur[uint32_t(e) & 0x7FFFFFFFu]++] = uint32_t(e >> 32);
-}
 
 // the host builder (schedule.cpp): traces copied back in batches
 void host_schedule(uscg_tracer_s* t, RunSchedule& R) {
@@ -590,26 +538,42 @@ void build_schedule(uscg_tracer_s* t) {
     }
     t->runs_per_view = t->lines / t->run;
     t->n_runs = t->views * t->runs_per_view;
-    RunSchedule R;
     const char* host = std::getenv("USCG_HOST_SCHEDULE");
     if (host && std::atoi(host)) {
+        RunSchedule R;
         host_schedule(t, R);
+        t->level_off = R.level_off;
+        upload(t->d_order, R.order);
+        upload(t->d_level_off, t->level_off);
+        upload(t->d_pred_off, R.pred_off);
+        upload(t->d_preds, R.preds);
+        t->n_preds = R.preds.size();
+        upload(t->d_npred_x, R.npred_x);
+        upload(t->d_succ_off, R.succ_off);
+        upload(t->d_succs, R.succs);
+        t->n_succs = R.succs.size();
     } else {
-        std::vector<unsigned long long> edges;
-        gpu_schedule_edges(t->trace_args(), t->views, t->max_recs, t->max_cells, t->cells, t->cells_per_sweep,
-                           uint32_t(t->run), uint32_t(t->runs_per_view), edges, t->st());
-        schedule_from_edges(edges, uint32_t(t->n_runs), R);
+        // edges, CSR lists, levels and order all on the device (schedule_gpu.cu)
+        GpuSchedule G;
+        G.alloc = [t](GpuSchedule::Array a, size_t n) -> uint32_t* {
+            DevBuf<uint32_t>* d[] = {&t->d_order,  &t->d_level_off, &t->d_pred_off, &t->d_preds,
+                                     &t->d_npred_x, &t->d_succ_off,  &t->d_succs};
+            d[a]->alloc(n);
+            return d[a]->p;
+        };
+        gpu_schedule_build(t->trace_args(), t->views, t->max_recs, t->max_cells, t->cells, t->cells_per_sweep,
+                           uint32_t(t->run), uint32_t(t->runs_per_view), G, t->st());
+        t->level_off = std::move(G.level_off);
+        t->n_preds = G.n_preds;
+        t->n_succs = G.n_succs;
+        if (const char* e = std::getenv("USCG_FLOW_VERBOSE"); e && std::atoi(e))
+            std::fprintf(stderr,
+                         "schedule: %zu runs, %u levels, %llu preds, %llu succs; edges %.3f s, lists %.3f s, "
+                         "levels %.3f s, order %.3f s\n",
+                         size_t(t->n_runs), unsigned(t->level_off.size() - 1), (unsigned long long)G.n_preds,
+                         (unsigned long long)G.n_succs, G.seconds[0], G.seconds[1], G.seconds[2], G.seconds[3]);
     }
-    t->level_off = R.level_off;
-    upload(t->d_order, R.order);
-    upload(t->d_level_off, t->level_off);
     t->d_bar.alloc(2);
-    upload(t->d_pred_off, R.pred_off);
-    upload(t->d_preds, R.preds);
-    t->n_preds = R.preds.size();
-    upload(t->d_npred_x, R.npred_x);
-    upload(t->d_succ_off, R.succ_off);
-    upload(t->d_succs, R.succs);
     t->sched_built = true;
     t->schedule_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - h0).count();
 }
@@ -1000,6 +964,21 @@ uscg_status uscg_tracer_export_schedule(uscg_tracer t, int32_t* run, uint32_t* r
         get(pred_off, t->d_pred_off, size_t(t->n_runs) + 1);
         get(preds, t->d_preds, t->n_preds);
         get(npred_x, t->d_npred_x, size_t(t->n_runs));
+    });
+}
+
+uscg_status uscg_tracer_export_successors(uscg_tracer t, uint64_t* n_succs, uint32_t* succ_off, uint32_t* succs) {
+    return guarded([&] {
+        need(t != nullptr, "null tracer");
+        bind(t->ctx);
+        build_schedule(t);
+        if (n_succs)
+            *n_succs = t->n_succs;
+        if (succ_off)
+            UB_CUDA(cudaMemcpy(succ_off, t->d_succ_off.p, sizeof(uint32_t) * (size_t(t->n_runs) + 1),
+                               cudaMemcpyDeviceToHost));
+        if (succs && t->n_succs)
+            UB_CUDA(cudaMemcpy(succs, t->d_succs.p, sizeof(uint32_t) * t->n_succs, cudaMemcpyDeviceToHost));
     });
 }
 

@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <functional>
 #include <vector>
 
 #include "internal.cuh"
@@ -159,11 +160,18 @@ void launch_otf_level(const DevCart& C, int lines, const double* rays, const dou
                       int n, const float* proj, float* f, double beta, double p_floor, unsigned long long* clamps,
                       cudaStream_t st);
 
-// the MART dependency edges on the device (schedule_gpu.cu): sorted unique
-// (succ_run << 32 | pred_run), pred word | 0x80000000 for cross-sweep edges
-void gpu_schedule_edges(const TraceArgs& A, int views, int max_recs, int max_cells, uint64_t cells,
-                        uint64_t visits, uint32_t run, uint32_t runs_per_view,
-                        std::vector<unsigned long long>& out_edges, cudaStream_t st);
+// The MART run schedule built on the device (schedule_gpu.cu): the same
+// structures AsapSchedule produces (schedule.h), written into device arrays
+// the caller allocates through `alloc` (which, count) once the sizes are known.
+struct GpuSchedule {
+    enum Array { kOrder, kLevelOff, kPredOff, kPreds, kNpredX, kSuccOff, kSuccs };
+    std::function<uint32_t*(Array, size_t)> alloc;
+    std::vector<uint32_t> level_off;  // host copy
+    uint64_t n_preds = 0, n_succs = 0;
+    double seconds[4] = {0, 0, 0, 0};  // edges, lists, levels, order
+};
+void gpu_schedule_build(const TraceArgs& A, int views, int max_recs, int max_cells, uint64_t cells, uint64_t visits,
+                        uint32_t run, uint32_t runs_per_view, GpuSchedule& out, cudaStream_t st);
 
 // K4 resample
 void launch_perm_resample(const float* field, uint64_t cells_per_slice, int slices, int S, int Sp,

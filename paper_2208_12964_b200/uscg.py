@@ -119,7 +119,7 @@ EXPORTS = [
     "uscg_tracer_get_info", "uscg_tracer_export_cache", "uscg_trace_line", "uscg_trace_counts",
     "uscg_trace_checksums", "uscg_tracer_export_schedule", "uscg_tracer_copy_cache",
     "uscg_tracer_import_cache_keys",
-    "uscg_tracer_build_schedule", "uscg_problem_stride", "uscg_project", "uscg_reconstruct",
+    "uscg_tracer_build_schedule", "uscg_tracer_export_successors", "uscg_problem_stride", "uscg_project", "uscg_reconstruct",
     "uscg_resample", "uscg_uspg_to_cg_map", "uscg_diag_math", "uscg_schedule_build", "uscg_image_metrics",
     "uscg_cartesian_like", "uscg_csystem_create", "uscg_csystem_info", "uscg_csystem_export",
     "uscg_csystem_reconstruct", "uscg_csystem_destroy",
@@ -167,6 +167,7 @@ def load(build_if_missing: bool = True):
     L.uscg_trace_counts.argtypes = [vp, _u32p]
     L.uscg_trace_checksums.argtypes = [vp, C.c_int32, C.c_int32, vp, vp, C.c_uint32]
     L.uscg_tracer_build_schedule.argtypes = [vp]
+    L.uscg_tracer_export_successors.argtypes = [vp, C.POINTER(C.c_uint64), _u32p, _u32p]
     L.uscg_tracer_export_schedule.argtypes = [vp, C.POINTER(C.c_int32), _u32p, _u32p, C.POINTER(C.c_uint64), _u32p,
                                               _u32p, _u32p, _u32p, _u32p]
     L.uscg_problem_stride.argtypes = [C.c_int32]
@@ -565,7 +566,7 @@ class Tracer:
 
     def schedule(self) -> dict:
         """The dataflow executor's run schedule: run, runs, levels, order,
-        level_off, pred_off, preds, npred_x (numpy u32 arrays)."""
+        level_off, pred_off, preds, npred_x, succ_off, succs (numpy u32 arrays)."""
         L = load()
         run, runs, levels, npr = C.c_int32(), C.c_uint32(), C.c_uint32(), C.c_uint64()
         _check(L.uscg_tracer_export_schedule(self.h, C.byref(run), C.byref(runs), C.byref(levels), C.byref(npr),
@@ -577,6 +578,13 @@ class Tracer:
                                              *[out[k].ctypes.data_as(_u32p) for k in
                                                ("order", "level_off", "pred_off", "preds", "npred_x")]))
         out["preds"] = out["preds"][:P]
+        ns = C.c_uint64()
+        _check(L.uscg_tracer_export_successors(self.h, C.byref(ns), None, None))
+        out["succ_off"] = np.zeros(R + 1, np.uint32)
+        out["succs"] = np.zeros(max(ns.value, 1), np.uint32)
+        _check(L.uscg_tracer_export_successors(self.h, C.byref(ns), out["succ_off"].ctypes.data_as(_u32p),
+                                               out["succs"].ctypes.data_as(_u32p)))
+        out["succs"] = out["succs"][:ns.value]
         out.update(run=run.value, runs=R, levels=V)
         return out
 

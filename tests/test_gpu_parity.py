@@ -767,8 +767,8 @@ def test_cartesian_mart_matches_reference(ub, ref, stored):
 @pytest.mark.parametrize("case", ["fan16", "fan32", "cone16", "cone32", "m1arc"])
 def test_device_schedule_equals_host_schedule(ub, orc, monkeypatch, case):
     """The sort-based device builder yields exactly the host AsapSchedule:
-    the same runs, levels, level-sorted order, in-sweep predecessors and
-    cross-sweep predecessor counts."""
+    the same runs, levels, level-sorted order, in-sweep predecessors,
+    cross-sweep predecessor counts and merged successor lists."""
     def build(host):
         monkeypatch.setenv("USCG_HOST_SCHEDULE", "1" if host else "0")
         if case == "m1arc":
@@ -780,7 +780,7 @@ def test_device_schedule_equals_host_schedule(ub, orc, monkeypatch, case):
     got, want = build(False), build(True)
     for k in ("run", "runs", "levels"):
         assert got[k] == want[k], k
-    for k in ("order", "level_off", "pred_off", "preds", "npred_x"):
+    for k in ("order", "level_off", "pred_off", "preds", "npred_x", "succ_off", "succs"):
         assert np.array_equal(got[k], want[k]), k
 
 

@@ -215,19 +215,28 @@ struct TraceSmem {
 // same (slice, ring) in this line — the TraceScratch stamp dedup
 // (tracer.cpp:181-195) restricted to the only records that can collide.
 // Earlier records of the same (slice, ring) as record i, collected with one
-// backward scan (up to kMaxPartners; more means "scan per cell").
+// backward scan (up to kMaxPartners; more means "scan per cell"). A line's
+// records of one slice are contiguous along the ray (a ray crosses each
+// z-slab once), so the scan stops at the start of record i's slice block.
 constexpr int kMaxPartners = 4;
 struct Partners {
     uint32_t lohi[kMaxPartners];
-    int n;  // -1: overflow, use the full scan
+    int n;         // -1: overflow, use the full scan
+    uint32_t slo;  // first cell of record i's slice
 };
 
-__device__ __forceinline__ Partners find_partners(const TraceSmem& S, int i) {
+__device__ __forceinline__ bool same_slice(uint32_t bj, uint32_t slo, uint32_t cps) { return bj - slo < cps; }
+
+__device__ __forceinline__ Partners find_partners(const TraceSmem& S, int i, uint32_t cps) {
     Partners P;
     P.n = 0;
     const uint32_t b = S.base[i];
+    P.slo = b - b % cps;
     for (int j = i - 1; j >= 0; --j) {
-        if (S.base[j] != b)
+        const uint32_t bj = S.base[j];
+        if (!same_slice(bj, P.slo, cps))
+            break;
+        if (bj != b)
             continue;
         if (P.n == kMaxPartners) {
             P.n = -1;
@@ -238,7 +247,7 @@ __device__ __forceinline__ Partners find_partners(const TraceSmem& S, int i) {
     return P;
 }
 
-__device__ __forceinline__ bool covered(const TraceSmem& S, const Partners& P, int i, int q) {
+__device__ __forceinline__ bool covered(const TraceSmem& S, const Partners& P, int i, int q, uint32_t cps) {
     if (P.n >= 0) {
 #pragma unroll
         for (int k = 0; k < kMaxPartners; ++k)
@@ -248,7 +257,10 @@ __device__ __forceinline__ bool covered(const TraceSmem& S, const Partners& P, i
     }
     const uint32_t b = S.base[i];
     for (int j = i - 1; j >= 0; --j) {
-        if (S.base[j] != b)
+        const uint32_t bj = S.base[j];
+        if (!same_slice(bj, P.slo, cps))
+            break;
+        if (bj != b)
             continue;
         const uint32_t w = S.lohi[j];
         if (range_has(q, lohi_lo(w), lohi_hi(w), lohi_seam(w)))
@@ -257,19 +269,19 @@ __device__ __forceinline__ bool covered(const TraceSmem& S, const Partners& P, i
     return false;
 }
 
-__device__ __forceinline__ uint32_t dedup_count(const TraceSmem& S, int i, int ng) {
+__device__ __forceinline__ uint32_t dedup_count(const TraceSmem& S, int i, int ng, uint32_t cps) {
     const uint32_t v = S.lohi[i];
     const int lo = lohi_lo(v), hi = lohi_hi(v);
-    const Partners P = find_partners(S, i);
+    const Partners P = find_partners(S, i, cps);
     uint32_t c = 0;
     if (!lohi_seam(v)) {
         for (int q = lo; q <= hi; ++q)
-            c += !covered(S, P, i, q);
+            c += !covered(S, P, i, q, cps);
     } else {
         for (int q = hi; q < ng; ++q)
-            c += !covered(S, P, i, q);
+            c += !covered(S, P, i, q, cps);
         for (int q = 0; q <= lo; ++q)
-            c += !covered(S, P, i, q);
+            c += !covered(S, P, i, q, cps);
     }
     return c;
 }
@@ -287,26 +299,42 @@ template <class Sync>
 __device__ bool rotate_records(const TraceArgs& A, uint32_t r0, uint32_t r1, double theta,
                                const TraceSmem& S, const RingRow* rings, const Sync& sy) {
     constexpr int NT = Sync::kThreads;
+    constexpr int K = 4;  // records per thread with their loads in flight together
     const int n = int(r1 - r0);
     const int t0 = sy.tid();
     bool any_flag = false;
-    for (int i = t0; i < n; i += NT) {
-        const uint32_t key = __ldg(A.key + r0 + i);
-        const uint32_t ring = key & kRingMask;
-        const uint32_t slice = (key >> kSliceShift) & kSliceMask;
-        const bool flag = (key & kFlagBit) != 0;
-        const RingRow rr = rings[ring];
-        int lo, hi;
-        bool seam;
-        rotate_chord(__ldg(A.pa + r0 + i), __ldg(A.pb + r0 + i), theta, rr.count, rr.inv_step, lo,
-                     hi, seam);
-        S.base[i] = slice * A.cells_per_slice + rr.head;
-        S.lohi[i] = pack_lohi(lo, hi, seam, flag);
-        const uint32_t ng = rr.count;
-        const uint32_t c = seam ? (ng - uint32_t(hi)) + uint32_t(lo) + 1u : uint32_t(hi - lo) + 1u;
-        S.cnt[i] = c | (ng << 16);
-        S.pos[i] = c;
-        any_flag |= flag;
+    for (int i0 = t0; i0 < n; i0 += K * NT) {
+        uint32_t key[K];
+        double pa[K], pb[K];
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+            const int i = i0 + k * NT;
+            if (i < n) {
+                key[k] = __ldg(A.key + r0 + i);
+                pa[k] = __ldg(A.pa + r0 + i);
+                pb[k] = __ldg(A.pb + r0 + i);
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+            const int i = i0 + k * NT;
+            if (i >= n)
+                break;
+            const uint32_t ring = key[k] & kRingMask;
+            const uint32_t slice = (key[k] >> kSliceShift) & kSliceMask;
+            const bool flag = (key[k] & kFlagBit) != 0;
+            const RingRow rr = rings[ring];
+            int lo, hi;
+            bool seam;
+            rotate_chord(pa[k], pb[k], theta, rr.count, rr.inv_step, lo, hi, seam);
+            S.base[i] = slice * A.cells_per_slice + rr.head;
+            S.lohi[i] = pack_lohi(lo, hi, seam, flag);
+            const uint32_t ng = rr.count;
+            const uint32_t c = seam ? (ng - uint32_t(hi)) + uint32_t(lo) + 1u : uint32_t(hi - lo) + 1u;
+            S.cnt[i] = c | (ng << 16);
+            S.pos[i] = c;
+            any_flag |= flag;
+        }
     }
     return sy.sync_or(any_flag);
 }
@@ -337,7 +365,7 @@ __device__ int scope_trace(const TraceArgs& A, uint32_t r0, uint32_t r1, double 
     if (rotate_records(A, r0, r1, theta, S, rings, sy)) {
         for (int i = t0; i < n; i += NT)
             if (lohi_flag(S.lohi[i]))
-                S.pos[i] = dedup_count(S, i, int(S.cnt[i] >> 16));
+                S.pos[i] = dedup_count(S, i, int(S.cnt[i] >> 16), A.cells_per_slice);
         sy.sync();
     }
     block_exclusive_scan(S.pos, n, S.warp, sy);
@@ -361,9 +389,9 @@ __device__ int scope_trace(const TraceArgs& A, uint32_t r0, uint32_t r1, double 
                     S.idx[p++] = b + uint32_t(q);
             }
         } else {
-            const Partners P = find_partners(S, i);
+            const Partners P = find_partners(S, i, A.cells_per_slice);
             auto emit = [&](int q) {
-                if (!covered(S, P, i, q))
+                if (!covered(S, P, i, q, A.cells_per_slice))
                     S.idx[p++] = b + uint32_t(q);
             };
             if (!lohi_seam(v)) {

@@ -36,6 +36,12 @@ namespace ub {
 namespace {
 constexpr int CTA = 1024;   // threads per CTA (one CTA per SM)
 constexpr int TG = 256;     // tracer group / level-barrier group size
+// dataflow CTA size: single-warp updaters (one problem) are shared-memory
+// bound at ~18 per SM, so their CTA is smaller and gets ~96 registers a thread
+template <int P>
+constexpr int flow_cta() {
+    return P == 1 ? 640 : CTA;
+}
 
 // Per problem-chunk width P: KR scalar cells held per thread (P < 4),
 // KV float4 (4-problem) vectors per thread (P >= 4), GU threads per dataflow
@@ -44,7 +50,7 @@ constexpr int TG = 256;     // tracer group / level-barrier group size
 // of the scattered gathers); their groups grow so that a thread still holds
 // KV = 6 cells of a line (768 cells per group).
 template <int P> struct SweepShape;
-template <> struct SweepShape<1> { static constexpr int KR = 4, KV = 0, GU = 32; };
+template <> struct SweepShape<1> { static constexpr int KR = 16, KV = 0, GU = 32; };
 template <> struct SweepShape<2> { static constexpr int KR = 6, KV = 0, GU = 256; };
 template <> struct SweepShape<4> { static constexpr int KR = 8, KV = 4, GU = 256; };
 template <> struct SweepShape<8> { static constexpr int KR = 16, KV = 6, GU = 256; };
@@ -72,6 +78,10 @@ __device__ __forceinline__ unsigned long long gtimer() {
     return t;
 }
 
+__device__ __forceinline__ void fence_acq_rel_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
+__device__ __forceinline__ void red_relaxed_add(unsigned* p, unsigned v) {
+    asm volatile("red.relaxed.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
 __device__ __forceinline__ void red_release_add(unsigned* p, unsigned v) {
     asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
@@ -107,12 +117,24 @@ __device__ __forceinline__ void st_global_cg_v4_if(bool p, void* gmem_dst, float
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 
+__device__ __forceinline__ unsigned ld_relaxed(const unsigned* p) {
+    unsigned v;
+    asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
+// Wait until *p >= target, then acquire. The polls are relaxed: a gpu-scope
+// acquire load compiles to LDG + CCTL.IVALL, which invalidates the whole L1
+// of the SM (the other warps' cached records and offsets) on every poll. The
+// final acquire reads a value at least as recent as the one polled
+// (coherence), so it synchronizes with the same release.
 __device__ __forceinline__ void spin_until_geq(const unsigned* p, unsigned target) {
     unsigned ns = 16;
-    while (ld_acquire(p) < target) {
+    while (ld_relaxed(p) < target) {
         __nanosleep(ns);
         ns = ns < 128 ? ns * 2 : 128;
     }
+    (void)ld_acquire(p);
 }
 
 // Shared-memory words of one group: [trace arrays when tracing] + `lists`
@@ -493,7 +515,7 @@ struct FlowLayout {
     size_t bytes;
 };
 
-static FlowLayout flow_layout(const MartArgs& a, int n_rings, int GU, bool pipe, size_t budget) {
+static FlowLayout flow_layout(const MartArgs& a, int n_rings, int GU, bool pipe, size_t budget, int cta) {
     const int P = a.Sp / a.nchunks;
     FlowLayout L;
     L.tracer_words = round4(group_words(P, TG, true, a.max_recs, a.max_cells, pipe ? a.run : 1)) +
@@ -501,8 +523,8 @@ static FlowLayout flow_layout(const MartArgs& a, int n_rings, int GU, bool pipe,
     L.updater_words = round4(group_words(P, GU, GU == 32, a.max_recs, a.max_cells, a.run)) +
                       (pipe ? updater_extra(P, a.run, a.max_cells) : 0);
     const size_t avail = budget / sizeof(uint32_t) - ring_words(n_rings);
-    L.groups = int(std::min<size_t>(CTA / GU, avail / L.updater_words));
-    L.tgroups = int(std::min<size_t>(CTA / TG, avail / L.tracer_words));
+    L.groups = int(std::min<size_t>(cta / GU, avail / L.updater_words));
+    L.tgroups = int(std::min<size_t>(cta / TG, avail / L.tracer_words));
     if (L.groups < 1 || L.tgroups < 1)
         throw CudaError("mart_flow_kernel: a run's index lists do not fit in shared memory");
     L.bytes = sizeof(uint32_t) *
@@ -907,11 +929,19 @@ __device__ void flow_updater(const FlowArgs& a, GroupWorker<P, G>& W) {
                 const int v = int(unit / uint32_t(a.m.tr.lines));
                 const int line = int(unit % uint32_t(a.m.tr.lines));
                 W.tr.idx = W.idx0 + size_t(j) * a.m.max_cells;
-                const int n = scope_trace(a.m.tr, __ldg(a.m.tr.off + line), __ldg(a.m.tr.off + line + 1),
-                                          __ldg(a.m.tr.theta + v), W.tr, true, W.s_rings, W.sy);
+                const uint32_t r0 = __ldg(a.m.tr.off + line), r1 = __ldg(a.m.tr.off + line + 1);
+                const double theta = __ldg(a.m.tr.theta + v);
+                if (prof && j == 0) {
+                    __syncwarp();
+                    if (W.t == 0)
+                        prof[9] = gtimer() + 0 * (r0 + r1 + uint32_t(theta));  // metadata loaded
+                }
+                const int n = scope_trace(a.m.tr, r0, r1, theta, W.tr, true, W.s_rings, W.sy);
                 if (W.t == 0)
                     W.line_n[j] = n;
             }
+            if (prof && W.t == 0)
+                prof[8] = gtimer();  // traced
             if (W.t == 0 && target)
                 spin_until_geq(cnt, target);
             W.sy.sync();
@@ -969,14 +999,17 @@ __device__ void flow_updater(const FlowArgs& a, GroupWorker<P, G>& W) {
         if (prof && W.t == 0)
             prof[5] = gtimer();
         // count in at the run's successors right away (the chain waits on it):
-        // one gpu-scope release reduction per successor (cumulative over the
-        // group's stores through the sync above)
+        // one gpu-scope fence (cumulative over the group's stores through the
+        // sync above), then a relaxed reduction per successor: fence +
+        // relaxed write is a release pattern, with one memory barrier per
+        // task instead of one per 32 successors
         {
             constexpr int kPub = G == 32 ? 0 : 1;  // publishing warp
             if (warp == kPub) {
                 const uint32_t sb = __ldg(a.succ_off + run), se = __ldg(a.succ_off + run + 1);
+                fence_acq_rel_gpu();
                 for (uint32_t k = sb + lane; k < se; k += 32)
-                    red_release_add(a.count + size_t(__ldg(a.succs + k)) * nchunks + chunk, 1u);
+                    red_relaxed_add(a.count + size_t(__ldg(a.succs + k)) * nchunks + chunk, 1u);
                 if (prof && lane == 0)
                     prof[6] = gtimer();
             }
@@ -989,7 +1022,7 @@ __device__ void flow_updater(const FlowArgs& a, GroupWorker<P, G>& W) {
 }
 
 template <int P>
-__global__ void __launch_bounds__(CTA, 1) mart_flow_kernel(FlowArgs a) {
+__global__ void __launch_bounds__(flow_cta<P>(), 1) mart_flow_kernel(FlowArgs a) {
     extern __shared__ __align__(16) uint32_t smem[];
     stage_rings(smem, a.m.tr.rings, a.n_rings);
     __syncthreads();
@@ -1030,10 +1063,11 @@ static void flow_launch_t(FlowArgs& a, int sms, cudaStream_t st) {
         const char* e = std::getenv("USCG_PIPE");
         a.pipe = (e ? std::atoi(e) : 0) != 0 && a.m.max_cells <= cover && a.run > 1;
     }
-    FlowLayout L = flow_layout(a.m, a.n_rings, GU, a.pipe != 0, size_t(optin) - 1024);
-    if (a.pipe && L.groups < std::min(2, CTA / GU)) {  // too little shared memory: plain runs
+    constexpr int kCta = flow_cta<P>();
+    FlowLayout L = flow_layout(a.m, a.n_rings, GU, a.pipe != 0, size_t(optin) - 1024, kCta);
+    if (a.pipe && L.groups < std::min(2, kCta / GU)) {  // too little shared memory: plain runs
         a.pipe = 0;
-        L = flow_layout(a.m, a.n_rings, GU, false, size_t(optin) - 1024);
+        L = flow_layout(a.m, a.n_rings, GU, false, size_t(optin) - 1024, kCta);
     }
     a.upd_groups = L.groups;
     if (const char* e = std::getenv("USCG_UPD_GROUPS"))  // experiments: fewer groups per SM
@@ -1043,7 +1077,7 @@ static void flow_launch_t(FlowArgs& a, int sms, cudaStream_t st) {
     UB_CUDA(cudaFuncSetAttribute(mart_flow_kernel<P>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  int(smem)));
     int per_sm = 0;
-    UB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, mart_flow_kernel<P>, CTA, smem));
+    UB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, mart_flow_kernel<P>, kCta, smem));
     if (per_sm < 1)
         throw CudaError("mart_flow_kernel cannot be resident (shared memory too large)");
     const int grid = sms * per_sm;
@@ -1064,7 +1098,7 @@ static void flow_launch_t(FlowArgs& a, int sms, cudaStream_t st) {
                      "upd_groups=%d smem=%zu\n",
                      P, a.run, a.pipe, grid, a.tracer_ctas, a.tr_groups, a.upd_groups, smem);
     // every CTA must be resident: tracers and updaters wait on each other
-    mart_flow_kernel<P><<<grid, CTA, smem, st>>>(a);
+    mart_flow_kernel<P><<<grid, kCta, smem, st>>>(a);
 }
 
 void launch_mart_flow(const MartArgs& h, const FlowSchedule& fs, unsigned* count, unsigned* next,
@@ -1175,7 +1209,7 @@ __global__ void __launch_bounds__(CTA, 1) mart_sweep_kernel(SweepArgs a) {
             a.prof[4 * lev + 2] = gtimer();
         if (threadIdx.x == 0) {
             const unsigned target = unsigned(lev + 1) * gridDim.x;
-            while (ld_acquire(a.bar) < target) {
+            while (ld_relaxed(a.bar) < target) {
             }
             __threadfence();
         }

@@ -833,6 +833,29 @@ __device__ void pipe_run(const FlowArgs& a, GroupWorker<P, G>& W, uint32_t run, 
 // index lists while its predecessors of this chunk finish, update the run's
 // lines in order (the chain between them stays inside the group), then count
 // in at the run's successors.
+__device__ __forceinline__ void prefetch_l2(const void* base, size_t elem, uint32_t r0, uint32_t r1) {
+    const uintptr_t b = (reinterpret_cast<uintptr_t>(base) + elem * r0) & ~uintptr_t(15);
+    const uintptr_t e = (reinterpret_cast<uintptr_t>(base) + elem * r1 + 15) & ~uintptr_t(15);
+    if (e > b)
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(b), "r"(uint32_t(e - b)) : "memory");
+}
+
+// Single-warp updaters: the next task's first-view records (its trace reads
+// them from HBM: the store is larger than L2) prefetched into L2 while this
+// task publishes. `nxt` (lane 0) is the claimed next task.
+__device__ __forceinline__ void prefetch_next(const FlowArgs& a, unsigned nxt, int per_sweep, int total) {
+    nxt = __shfl_sync(0xFFFFFFFFu, nxt, 0);
+    if ((threadIdx.x & 31) != 0 || int(nxt) >= total)
+        return;
+    const uint32_t run = __ldg(a.order + (int(nxt) % per_sweep) / a.m.nchunks);
+    const uint32_t unit = run_line(a, run, 0);
+    const uint32_t line = unit % uint32_t(a.m.tr.lines);
+    const uint32_t r0 = __ldg(a.m.tr.off + line), r1 = __ldg(a.m.tr.off + line + a.run);
+    prefetch_l2(a.m.tr.key, sizeof(uint32_t), r0, r1);
+    prefetch_l2(a.m.tr.pa, sizeof(double), r0, r1);
+    prefetch_l2(a.m.tr.pb, sizeof(double), r0, r1);
+}
+
 template <int P, int G>
 __device__ void flow_updater(const FlowArgs& a, GroupWorker<P, G>& W) {
     const int nchunks = a.m.nchunks;
@@ -867,6 +890,18 @@ __device__ void flow_updater(const FlowArgs& a, GroupWorker<P, G>& W) {
         const unsigned npred = __ldg(a.pred_off + run + 1) - __ldg(a.pred_off + run);
         const unsigned target = s * npred + (s - 1) * __ldg(a.npred_x + run);
         unsigned* cnt = a.count + size_t(run) * nchunks + chunk;
+        // the publishing warp loads the run's first 64 successors now: their
+        // latency is hidden behind the task instead of stalling the publish
+        constexpr int kPub = G == 32 ? 0 : 1;  // publishing warp
+        uint32_t sb = 0, se = 0, succ0 = 0, succ1 = 0;
+        if (G == 32) {  // (the larger groups have no registers to spare)
+            sb = __ldg(a.succ_off + run);
+            se = __ldg(a.succ_off + run + 1);
+            if (sb + lane < se)
+                succ0 = __ldg(a.succs + sb + lane);
+            if (sb + 32 + lane < se)
+                succ1 = __ldg(a.succs + sb + 32 + lane);
+        }
         auto stage_lists = [&](int ct, int nct) {
             // every line's index list of the run (pipelined: and next
             // positions), from the slab into shared memory (L2 reads: slots
@@ -1004,12 +1039,23 @@ __device__ void flow_updater(const FlowArgs& a, GroupWorker<P, G>& W) {
         // relaxed write is a release pattern, with one memory barrier per
         // task instead of one per 32 successors
         {
-            constexpr int kPub = G == 32 ? 0 : 1;  // publishing warp
             if (warp == kPub) {
-                const uint32_t sb = __ldg(a.succ_off + run), se = __ldg(a.succ_off + run + 1);
-                fence_acq_rel_gpu();
-                for (uint32_t k = sb + lane; k < se; k += 32)
-                    red_relaxed_add(a.count + size_t(__ldg(a.succs + k)) * nchunks + chunk, 1u);
+                if constexpr (G == 32) {
+                    fence_acq_rel_gpu();
+                    if (sb + lane < se)
+                        red_relaxed_add(a.count + size_t(succ0) * nchunks + chunk, 1u);
+                    if (sb + 32 + lane < se)
+                        red_relaxed_add(a.count + size_t(succ1) * nchunks + chunk, 1u);
+                    for (uint32_t k = sb + 64 + lane; k < se; k += 32)
+                        red_relaxed_add(a.count + size_t(__ldg(a.succs + k)) * nchunks + chunk, 1u);
+                    prefetch_next(a, nxt, per_sweep, total);
+                } else {
+                    sb = __ldg(a.succ_off + run);
+                    se = __ldg(a.succ_off + run + 1);
+                    fence_acq_rel_gpu();
+                    for (uint32_t k = sb + lane; k < se; k += 32)
+                        red_relaxed_add(a.count + size_t(__ldg(a.succs + k)) * nchunks + chunk, 1u);
+                }
                 if (prof && lane == 0)
                     prof[6] = gtimer();
             }

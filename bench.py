@@ -604,6 +604,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--length-model", action="store_true",
+                    help="also time the length-weighted projector over the stack (not part of the step)")
     args = ap.parse_args()
 
     rank = int(os.environ.get("RANK", "0"))
@@ -740,17 +742,20 @@ def main():
     Bp = 4 * U_all + 20 * C + 8 * units + 4 * units * Sp
     projector = {"ms": tp, "updates_per_s": U_all / (tp * 1e-3), "achieved_gbs": Bp / (tp * 1e-3) / 1e9,
                  "algorithmic_bytes": Bp, "bytes_model": "4*U_all + 20*C + 8*(views*lines) + 4*(views*lines)*S_pad"}
-    # length-weighted model (phantom.cpp:213-269) over the whole stack, one call
-    lw0, lw1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    lw0.record(stream)
-    uscg._check(L.uscg_project(tracer.h, uscg.C.c_void_p(field_d.data_ptr()), S, uscg.C.c_void_p(out_d.data_ptr()),
-                               flags | uscg.MODEL_LENGTH))
-    lw1.record(stream)
-    torch.cuda.synchronize()
-    tlw = lw0.elapsed_time(lw1)
-    projector["length_weighted"] = {"ms": tlw, "problems": S, "rays_per_s": units * S / (tlw * 1e-3),
-                                    "model": "fp64 ray walk per (view, line, 8-problem chunk); cuts at the "
-                                             "radial boundaries inside each chord's sector range"}
+    # length-weighted model (phantom.cpp:213-269) over the whole stack, one
+    # call (opt-in: it is not part of the step, and would dominate the
+    # command's launch list)
+    if args.length_model:
+        lw0, lw1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        lw0.record(stream)
+        uscg._check(L.uscg_project(tracer.h, uscg.C.c_void_p(field_d.data_ptr()), S,
+                                   uscg.C.c_void_p(out_d.data_ptr()), flags | uscg.MODEL_LENGTH))
+        lw1.record(stream)
+        torch.cuda.synchronize()
+        tlw = lw0.elapsed_time(lw1)
+        projector["length_weighted"] = {"ms": tlw, "problems": S, "rays_per_s": units * S / (tlw * 1e-3),
+                                        "model": "fp64 ray walk per (view, line, 8-problem chunk); cuts at the "
+                                                 "radial boundaries inside each chord's sector range"}
 
     # ---- e2e through the C ABI with pinned host buffers ----
     e2e = None

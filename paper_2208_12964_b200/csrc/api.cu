@@ -1104,12 +1104,10 @@ uscg_status uscg_reconstruct(uscg_tracer t, const float* proj, int32_t problems,
         }
 
         // ---- ProjectionSet::validate + auto_p_floor + all-zero check ----
-        t->w_stats.ensure(size_t(4) * Sp);
-        UB_CUDA(cudaMemsetAsync(t->w_stats.p, 0, sizeof(double) * 4 * Sp, st));
+        t->w_stats.ensure(proj_stats_words(S));
         launch_proj_stats(d_proj, int(units), S, Sp, t->w_stats.p, st);
-        std::vector<double> stats(size_t(4) * Sp);
-        UB_CUDA(cudaMemcpyAsync(stats.data(), t->w_stats.p, sizeof(double) * 4 * Sp,
-                                cudaMemcpyDeviceToHost, st));
+        std::vector<double> stats(size_t(4) * S);
+        UB_CUDA(cudaMemcpyAsync(stats.data(), t->w_stats.p, sizeof(double) * 4 * S, cudaMemcpyDeviceToHost, st));
 
         // ---- field -> device [cells][Sp] ----
         float* d_field = nullptr;

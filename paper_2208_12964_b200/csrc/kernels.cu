@@ -1177,56 +1177,91 @@ void launch_mart_level(const MartArgs* dargs, const MartArgs& h, const uint32_t*
 // threadIdx.x = column in the tile, threadIdx.y = row lane.
 // =============================================================================
 
-__global__ void proj_stats_kernel(const float* __restrict__ proj, int units, int S, int Sp,
-                                  double* stats) {
+// ProjectionSet::validate + auto_p_floor + all-zero test (solver.cpp:76-95)
+// per problem: block partials (no atomics), then an in-order fold, so the
+// positive-measurement sum (and with it p_floor) is the same on every run.
+constexpr int kStatBlocks = 256;
+
+__global__ void __launch_bounds__(256) proj_stats_kernel(const float* __restrict__ proj, int units, int S, int Sp,
+                                                         double* __restrict__ part) {
+    __shared__ double sh[8][32][4];
     const int col = blockIdx.y * 32 + threadIdx.x;
-    if (col >= S)
-        return;
     double cnt = 0, sum = 0, nz = 0, bad = 0;
-    for (int u = blockIdx.x * blockDim.y + threadIdx.y; u < units; u += gridDim.x * blockDim.y) {
-        const float m = proj[size_t(u) * Sp + col];
-        if (!isfinite(m) || m < 0)
-            bad = 1;
-        if (m > 0) {
-            cnt += 1;
-            sum += double(m);
+    if (col < S) {
+        for (int u = blockIdx.x * blockDim.y + threadIdx.y; u < units; u += gridDim.x * blockDim.y) {
+            const float m = proj[size_t(u) * Sp + col];
+            if (!isfinite(m) || m < 0)
+                bad = 1;
+            if (m > 0) {
+                cnt += 1;
+                sum += double(m);
+            }
+            if (m != 0)
+                nz = 1;
         }
-        if (m != 0)
-            nz = 1;
     }
-    atomicAdd(stats + 4 * col + 0, cnt);
-    atomicAdd(stats + 4 * col + 1, sum);
-    if (nz > 0)
-        atomicAdd(stats + 4 * col + 2, 1.0);
-    if (bad > 0)
-        atomicAdd(stats + 4 * col + 3, 1.0);
+    sh[threadIdx.y][threadIdx.x][0] = cnt;
+    sh[threadIdx.y][threadIdx.x][1] = sum;
+    sh[threadIdx.y][threadIdx.x][2] = nz;
+    sh[threadIdx.y][threadIdx.x][3] = bad;
+    __syncthreads();
+    if (threadIdx.y < 4 && col < S) {
+        const int k = threadIdx.y;
+        double acc = 0;
+        for (int y = 0; y < 8; ++y)
+            acc = k >= 2 ? fmax(acc, sh[y][threadIdx.x][k]) : acc + sh[y][threadIdx.x][k];
+        part[(size_t(blockIdx.x) * S + col) * 4 + k] = acc;
+    }
 }
 
-void launch_proj_stats(const float* proj, int units, int S, int Sp, double* stats,
-                       cudaStream_t st) {
-    dim3 block(32, 8);
-    dim3 grid(unsigned(std::min(cdiv(units, 8), 1184)), unsigned(cdiv(S, 32)));
-    proj_stats_kernel<<<grid, block, 0, st>>>(proj, units, S, Sp, stats);
+__global__ void stats_fold_kernel(const double* __restrict__ part, int S, int blocks, double* __restrict__ stats) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;  // col * 4 + k
+    if (i >= 4 * S)
+        return;
+    const int k = i & 3;
+    double acc = 0;
+    for (int b = 0; b < blocks; ++b)
+        acc = k >= 2 ? fmax(acc, part[size_t(b) * S * 4 + i]) : acc + part[size_t(b) * S * 4 + i];
+    stats[i] = acc;
+}
+
+size_t proj_stats_words(int S) { return size_t(4) * S * (kStatBlocks + 1); }
+
+void launch_proj_stats(const float* proj, int units, int S, int Sp, double* stats, cudaStream_t st) {
+    const int blocks = std::max(1, std::min(cdiv(units, 8), kStatBlocks));
+    double* part = stats + size_t(4) * S;
+    proj_stats_kernel<<<dim3(unsigned(blocks), unsigned(cdiv(S, 32))), dim3(32, 8), 0, st>>>(proj, units, S, Sp,
+                                                                                              part);
+    check_launch();
+    stats_fold_kernel<<<unsigned(cdiv(4 * S, 128)), 128, 0, st>>>(part, S, blocks, stats);
     check_launch();
 }
 
-__global__ void sweep_updates_kernel(const float* __restrict__ proj,
-                                     const uint32_t* __restrict__ cells, int units, int S, int Sp,
-                                     unsigned long long* out) {
+__global__ void __launch_bounds__(256) sweep_updates_kernel(const float* __restrict__ proj,
+                                                            const uint32_t* __restrict__ cells, int units, int S,
+                                                            int Sp, unsigned long long* out) {
+    __shared__ unsigned long long sh[8][32];
     const int col = blockIdx.y * 32 + threadIdx.x;
-    if (col >= S)
-        return;
     unsigned long long acc = 0;
-    for (int u = blockIdx.x * blockDim.y + threadIdx.y; u < units; u += gridDim.x * blockDim.y)
-        if (proj[size_t(u) * Sp + col] != 0)
-            acc += cells[u];
-    atomicAdd(out + col, acc);
+    if (col < S)
+        for (int u = blockIdx.x * blockDim.y + threadIdx.y; u < units; u += gridDim.x * blockDim.y)
+            if (proj[size_t(u) * Sp + col] != 0)
+                acc += cells[u];
+    sh[threadIdx.y][threadIdx.x] = acc;
+    __syncthreads();
+    if (threadIdx.y == 0 && col < S) {
+        unsigned long long t = 0;
+        for (int y = 0; y < 8; ++y)
+            t += sh[y][threadIdx.x];
+        if (t)
+            atomicAdd(out + col, t);
+    }
 }
 
 void launch_sweep_updates(const float* proj, const uint32_t* cells, int units, int S, int Sp,
                           unsigned long long* out, cudaStream_t st) {
     dim3 block(32, 8);
-    dim3 grid(unsigned(std::min(cdiv(units, 8), 1184)), unsigned(cdiv(S, 32)));
+    dim3 grid(unsigned(std::min(cdiv(units, 8), kStatBlocks)), unsigned(cdiv(S, 32)));
     sweep_updates_kernel<<<grid, block, 0, st>>>(proj, cells, units, S, Sp, out);
     check_launch();
 }

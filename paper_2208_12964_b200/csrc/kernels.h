@@ -110,7 +110,9 @@ void launch_mart_flow(const MartArgs& h, const FlowSchedule& fs, unsigned* count
                       unsigned epoch, int sweeps, int n_rings, const FlowSlab& slab,
                       cudaStream_t st, unsigned long long* prof = nullptr);
 
-// per-problem projection statistics: stats[p*4 + {0: count>0, 1: sum>0, 2: any!=0, 3: invalid}]
+// per-problem projection statistics: stats[p*4 + {0: count>0, 1: sum>0, 2: any!=0, 3: invalid}];
+// stats must hold proj_stats_words(S) doubles (the tail is block partials)
+size_t proj_stats_words(int S);
 void launch_proj_stats(const float* proj, int units, int S, int Sp, double* stats, cudaStream_t st);
 // per-problem updates per sweep: sum over units with m != 0 of cells[u]
 void launch_sweep_updates(const float* proj, const uint32_t* cells, int units, int S, int Sp,

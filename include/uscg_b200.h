@@ -224,6 +224,16 @@ uscg_status uscg_project(uscg_tracer tracer, const float* field, int32_t problem
 uscg_status uscg_reconstruct(uscg_tracer tracer, const float* proj, int32_t problems,
                              const uscg_solver_config* cfg, float* field_inout, int32_t from_init,
                              uscg_report* reports, uint32_t flags);
+/* uscg_reconstruct over `batch` independent problem stacks in host memory
+ * (proj[b], field_inout[b] as in uscg_reconstruct; host layout per
+ * USCG_LAYOUT_INTERLEAVED), with the transfers overlapped with the solves:
+ * stack b+1 uploads on one copy stream and stack b-1 downloads on another
+ * while stack b is solved (double-buffered device staging). Pinned host
+ * buffers are needed for the overlap. reports: batch * problems entries, or
+ * NULL. The first failing stack's error is returned; later stacks are not run. */
+uscg_status uscg_reconstruct_batch(uscg_tracer tracer, int32_t batch, const float* const* proj,
+                                   int32_t problems, const uscg_solver_config* cfg, float* const* field_inout,
+                                   int32_t from_init, uscg_report* reports, uint32_t flags);
 
 /* ---- resampling: uspg_to_cg_map + field_to_cartesian (proj/src/grid.cpp:75-99,
  * proj/src/phantom.cpp:149-163). Output [S][slices][npix][npix], row 0 at the

@@ -8,7 +8,7 @@ from .uscg import (  # noqa: F401
     CartesianSystem, Context, Detector, DomainError, Field, FirstViewCache, GridMode, GridSpec, InvalidArgument, NoDevice,
     ProjectionSet, ReconReport, ReconResult, ScanGeometry, SolverConfig, Tracer, field_to_cartesian,
     generate_projections, image_metrics, launch_count, load, mae, mae_volume, problem_stride, project_stack,
-    reconstruct, reconstruct_from, reconstruct_stack, resample_stack, ring_counts_m1, rmse, rmse_volume, ssim,
+    reconstruct, reconstruct_batch, reconstruct_from, reconstruct_stack, resample_stack, ring_counts_m1, rmse, rmse_volume, ssim,
     ssim_volume, uspg_to_cg_map,
 )
 
@@ -16,6 +16,6 @@ __all__ = [
     "CartesianSystem", "Context", "Detector", "DomainError", "Field", "FirstViewCache", "GridMode", "GridSpec", "InvalidArgument",
     "NoDevice", "ProjectionSet", "ReconReport", "ReconResult", "ScanGeometry", "SolverConfig", "Tracer",
     "field_to_cartesian", "generate_projections", "image_metrics", "launch_count", "load", "mae", "mae_volume",
-    "problem_stride", "project_stack", "reconstruct", "reconstruct_from", "reconstruct_stack", "resample_stack",
+    "problem_stride", "project_stack", "reconstruct", "reconstruct_batch", "reconstruct_from", "reconstruct_stack", "resample_stack",
     "ring_counts_m1", "rmse", "rmse_volume", "ssim", "ssim_volume", "uspg_to_cg_map",
 ]

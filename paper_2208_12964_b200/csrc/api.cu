@@ -29,6 +29,11 @@ struct InvalidArgument : std::invalid_argument {
 struct DomainError : std::domain_error {
     using std::domain_error::domain_error;
 };
+// a nested C-ABI call's failure, passed through with its status
+struct StatusError : std::runtime_error {
+    uscg_status code;
+    StatusError(uscg_status c, const char* msg) : std::runtime_error(msg ? msg : "error"), code(c) {}
+};
 
 double norm360(double deg) {  // geometry.cpp:48-55
     deg = std::fmod(deg, 360.0);
@@ -153,6 +158,15 @@ struct uscg_tracer_s {
     DevBuf<unsigned long long> w_clamps, w_updates, w_tmp;
     DevBuf<unsigned int> w_resid;
     GraphCache graph;
+    // uscg_reconstruct_batch: double-buffered staging and its copy streams
+    DevBuf<float> w_bin[2], w_bout[2];
+    cudaStream_t copy_in = nullptr, copy_out = nullptr;
+    ~uscg_tracer_s() {
+        if (copy_in)
+            cudaStreamDestroy(copy_in);
+        if (copy_out)
+            cudaStreamDestroy(copy_out);
+    }
 
     DevGrid dev_grid() const {
         DevGrid g;
@@ -226,6 +240,9 @@ uscg_status guarded(F&& f) {
     } catch (const NoDevice& e) {
         set_error(e.what());
         return USCG_ERR_NO_DEVICE;
+    } catch (const StatusError& e) {
+        set_error(e.what());
+        return e.code;
     } catch (const CudaError& e) {
         set_error(e.what());
         return USCG_ERR_CUDA;
@@ -1061,329 +1078,479 @@ uscg_status uscg_project(uscg_tracer t, const float* field, int32_t problems, fl
     });
 }
 
-uscg_status uscg_reconstruct(uscg_tracer t, const float* proj, int32_t problems,
-                             const uscg_solver_config* cfg, float* field_inout, int32_t from_init,
-                             uscg_report* reports, uint32_t flags) {
-    return guarded([&] {
-        need(t != nullptr, "null tracer");
-        bind(t->ctx);
-        need(cfg != nullptr, "null config");
-        need(proj && field_inout, "null buffer");
-        need(problems >= 1, "problem count must be >= 1");
-        // validate_config (solver.cpp:55-61)
-        need(cfg->beta > 0 && cfg->beta < 2, "relaxation must lie in (0, 2)");
-        need(cfg->f_init > 0, "initial field value must be positive");
-        need(cfg->max_sweeps >= 1, "sweep budget must be >= 1");
-        const int S = problems, Sp = problem_stride(S), P = chunk_width(S);
-        const bool dev = flags & USCG_DEVICE_POINTERS;
-        const bool inter = flags & USCG_LAYOUT_INTERLEAVED;
-        const uint64_t units = t->units();
-        const uint64_t cells = t->cells;
-        cudaStream_t st = t->st();
+// The body of uscg_reconstruct. after_launch (may be null) runs once, right
+// after the first MART launch is enqueued: uscg_reconstruct_batch queues the
+// previous stack's download there, behind this solve's small host reads.
+static void reconstruct_body(uscg_tracer t, const float* proj, int32_t problems, const uscg_solver_config* cfg,
+                      float* field_inout, int32_t from_init, uscg_report* reports, uint32_t flags,
+                      const std::function<void()>* after_launch) {
+    need(t != nullptr, "null tracer");
+    bind(t->ctx);
+    need(cfg != nullptr, "null config");
+    need(proj && field_inout, "null buffer");
+    need(problems >= 1, "problem count must be >= 1");
+    // validate_config (solver.cpp:55-61)
+    need(cfg->beta > 0 && cfg->beta < 2, "relaxation must lie in (0, 2)");
+    need(cfg->f_init > 0, "initial field value must be positive");
+    need(cfg->max_sweeps >= 1, "sweep budget must be >= 1");
+    const int S = problems, Sp = problem_stride(S), P = chunk_width(S);
+    const bool dev = flags & USCG_DEVICE_POINTERS;
+    const bool inter = flags & USCG_LAYOUT_INTERLEAVED;
+    const uint64_t units = t->units();
+    const uint64_t cells = t->cells;
+    cudaStream_t st = t->st();
 
-        // ---- projections -> device [units][Sp] ----
-        const float* d_proj = nullptr;
-        if (dev && (inter || S == 1)) {
-            d_proj = proj;
+    // ---- projections -> device [units][Sp] ----
+    const float* d_proj = nullptr;
+    if (dev && (inter || S == 1)) {
+        d_proj = proj;
+    } else {
+        t->w_proj.ensure(units * Sp);
+        if (inter || S == 1) {
+            UB_CUDA(cudaMemcpyAsync(t->w_proj.p, proj, sizeof(float) * units * Sp,
+                                    dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, st));
         } else {
-            t->w_proj.ensure(units * Sp);
+            const float* src = proj;
+            if (!dev) {
+                t->w_stage.ensure(std::max<uint64_t>(units * S, cells * S));
+                UB_CUDA(cudaMemcpyAsync(t->w_stage.p, proj, sizeof(float) * units * S,
+                                        cudaMemcpyHostToDevice, st));
+                src = t->w_stage.p;
+            }
+            launch_to_interleaved(src, t->w_proj.p, units, S, Sp, 0.f, st);
+        }
+        d_proj = t->w_proj.p;
+    }
+
+    // ---- ProjectionSet::validate + auto_p_floor + all-zero check ----
+    t->w_stats.ensure(proj_stats_words(S));
+    launch_proj_stats(d_proj, int(units), S, Sp, t->w_stats.p, st);
+    std::vector<double> stats(size_t(4) * S);
+    UB_CUDA(cudaMemcpyAsync(stats.data(), t->w_stats.p, sizeof(double) * 4 * S, cudaMemcpyDeviceToHost, st));
+
+    // ---- field -> device [cells][Sp] ----
+    float* d_field = nullptr;
+    const bool direct_field = dev && (inter || S == 1);
+    if (direct_field) {
+        d_field = field_inout;
+    } else {
+        t->w_field.ensure(cells * Sp);
+        d_field = t->w_field.p;
+    }
+    if (from_init) {
+        if (!direct_field) {
             if (inter || S == 1) {
-                UB_CUDA(cudaMemcpyAsync(t->w_proj.p, proj, sizeof(float) * units * Sp,
-                                        dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, st));
+                UB_CUDA(cudaMemcpyAsync(d_field, field_inout, sizeof(float) * cells * Sp,
+                                        dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
+                                        st));
             } else {
-                const float* src = proj;
+                const float* src = field_inout;
                 if (!dev) {
                     t->w_stage.ensure(std::max<uint64_t>(units * S, cells * S));
-                    UB_CUDA(cudaMemcpyAsync(t->w_stage.p, proj, sizeof(float) * units * S,
+                    UB_CUDA(cudaMemcpyAsync(t->w_stage.p, field_inout, sizeof(float) * cells * S,
                                             cudaMemcpyHostToDevice, st));
                     src = t->w_stage.p;
                 }
-                launch_to_interleaved(src, t->w_proj.p, units, S, Sp, 0.f, st);
+                launch_to_interleaved(src, d_field, cells, S, Sp, 1.f, st);
             }
-            d_proj = t->w_proj.p;
         }
-
-        // ---- ProjectionSet::validate + auto_p_floor + all-zero check ----
-        t->w_stats.ensure(proj_stats_words(S));
-        launch_proj_stats(d_proj, int(units), S, Sp, t->w_stats.p, st);
-        std::vector<double> stats(size_t(4) * S);
-        UB_CUDA(cudaMemcpyAsync(stats.data(), t->w_stats.p, sizeof(double) * 4 * S, cudaMemcpyDeviceToHost, st));
-
-        // ---- field -> device [cells][Sp] ----
-        float* d_field = nullptr;
-        const bool direct_field = dev && (inter || S == 1);
-        if (direct_field) {
-            d_field = field_inout;
-        } else {
-            t->w_field.ensure(cells * Sp);
-            d_field = t->w_field.p;
-        }
-        if (from_init) {
-            if (!direct_field) {
-                if (inter || S == 1) {
-                    UB_CUDA(cudaMemcpyAsync(d_field, field_inout, sizeof(float) * cells * Sp,
-                                            dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
-                                            st));
-                } else {
-                    const float* src = field_inout;
-                    if (!dev) {
-                        t->w_stage.ensure(std::max<uint64_t>(units * S, cells * S));
-                        UB_CUDA(cudaMemcpyAsync(t->w_stage.p, field_inout, sizeof(float) * cells * S,
-                                                cudaMemcpyHostToDevice, st));
-                        src = t->w_stage.p;
-                    }
-                    launch_to_interleaved(src, d_field, cells, S, Sp, 1.f, st);
-                }
-            }
-            t->w_tmp.ensure(1);
-            UB_CUDA(cudaMemsetAsync(t->w_tmp.p, 0, sizeof(unsigned long long), st));
-            launch_count_nonpositive(d_field, cells * Sp, t->w_tmp.p, st);
-            unsigned long long bad = 0;
-            UB_CUDA(cudaMemcpyAsync(&bad, t->w_tmp.p, sizeof(bad), cudaMemcpyDeviceToHost, st));
-            UB_CUDA(cudaStreamSynchronize(st));
-            need(bad == 0, "initial field must be strictly positive");
-        } else {
-            launch_fill(d_field, cells * Sp, float(cfg->f_init), st);
-        }
+        t->w_tmp.ensure(1);
+        UB_CUDA(cudaMemsetAsync(t->w_tmp.p, 0, sizeof(unsigned long long), st));
+        launch_count_nonpositive(d_field, cells * Sp, t->w_tmp.p, st);
+        unsigned long long bad = 0;
+        UB_CUDA(cudaMemcpyAsync(&bad, t->w_tmp.p, sizeof(bad), cudaMemcpyDeviceToHost, st));
         UB_CUDA(cudaStreamSynchronize(st));
-        std::vector<double> p_floor(Sp, 1e-12);
-        std::vector<uint8_t> active(Sp, 0);
-        std::vector<int> all_zero(S, 0);
-        for (int p = 0; p < S; ++p) {
-            if (stats[4 * p + 3] > 0)
-                throw InvalidArgument("projection data contains a non-finite or negative measurement");
-            const double cnt = stats[4 * p + 0], sum = stats[4 * p + 1];
-            p_floor[p] = cfg->p_floor > 0 ? cfg->p_floor : (cnt == 0 ? 1e-12 : 1e-12 * (sum / cnt));
-            all_zero[p] = stats[4 * p + 2] == 0;
-            active[p] = !all_zero[p];
-        }
+        need(bad == 0, "initial field must be strictly positive");
+    } else {
+        launch_fill(d_field, cells * Sp, float(cfg->f_init), st);
+    }
+    UB_CUDA(cudaStreamSynchronize(st));
+    std::vector<double> p_floor(Sp, 1e-12);
+    std::vector<uint8_t> active(Sp, 0);
+    std::vector<int> all_zero(S, 0);
+    for (int p = 0; p < S; ++p) {
+        if (stats[4 * p + 3] > 0)
+            throw InvalidArgument("projection data contains a non-finite or negative measurement");
+        const double cnt = stats[4 * p + 0], sum = stats[4 * p + 1];
+        p_floor[p] = cfg->p_floor > 0 ? cfg->p_floor : (cnt == 0 ? 1e-12 : 1e-12 * (sum / cnt));
+        all_zero[p] = stats[4 * p + 2] == 0;
+        active[p] = !all_zero[p];
+    }
 
-        build_schedule(t);
-        const bool track = cfg->tolerance > 0;
-        if (track || reports)
-            ensure_crossed(t);
+    build_schedule(t);
+    const bool track = cfg->tolerance > 0;
+    if (track || reports)
+        ensure_crossed(t);
 
-        // ---- per-problem updates per sweep (U counter) ----
-        t->w_updates.ensure(Sp);
-        UB_CUDA(cudaMemsetAsync(t->w_updates.p, 0, sizeof(unsigned long long) * Sp, st));
-        launch_sweep_updates(d_proj, t->d_cells.p, int(units), S, Sp, t->w_updates.p, st);
-        std::vector<unsigned long long> upd(Sp);
-        UB_CUDA(cudaMemcpyAsync(upd.data(), t->w_updates.p, sizeof(unsigned long long) * Sp,
-                                cudaMemcpyDeviceToHost, st));
+    // ---- per-problem updates per sweep (U counter) ----
+    t->w_updates.ensure(Sp);
+    UB_CUDA(cudaMemsetAsync(t->w_updates.p, 0, sizeof(unsigned long long) * Sp, st));
+    launch_sweep_updates(d_proj, t->d_cells.p, int(units), S, Sp, t->w_updates.p, st);
+    std::vector<unsigned long long> upd(Sp);
+    UB_CUDA(cudaMemcpyAsync(upd.data(), t->w_updates.p, sizeof(unsigned long long) * Sp,
+                            cudaMemcpyDeviceToHost, st));
 
-        t->w_pfloor.ensure(Sp);
-        t->w_active.ensure(Sp);
-        t->w_clamps.ensure(Sp);
-        UB_CUDA(cudaMemcpyAsync(t->w_pfloor.p, p_floor.data(), sizeof(double) * Sp,
-                                cudaMemcpyHostToDevice, st));
-        UB_CUDA(cudaMemcpyAsync(t->w_active.p, active.data(), Sp, cudaMemcpyHostToDevice, st));
-        UB_CUDA(cudaMemsetAsync(t->w_clamps.p, 0, sizeof(unsigned long long) * Sp, st));
+    t->w_pfloor.ensure(Sp);
+    t->w_active.ensure(Sp);
+    t->w_clamps.ensure(Sp);
+    UB_CUDA(cudaMemcpyAsync(t->w_pfloor.p, p_floor.data(), sizeof(double) * Sp,
+                            cudaMemcpyHostToDevice, st));
+    UB_CUDA(cudaMemcpyAsync(t->w_active.p, active.data(), Sp, cudaMemcpyHostToDevice, st));
+    UB_CUDA(cudaMemsetAsync(t->w_clamps.p, 0, sizeof(unsigned long long) * Sp, st));
 
-        MartArgs h;
-        h.tr = t->trace_args();
-        h.field = d_field;
-        h.proj = d_proj;
-        h.p_floor = t->w_pfloor.p;
-        h.active = t->w_active.p;
-        h.clamps = t->w_clamps.p;
-        h.beta = cfg->beta;
-        h.Sp = Sp;
-        h.nchunks = Sp / P;
-        h.max_recs = t->max_recs;
-        h.max_cells = t->max_cells;
-        h.run = t->run;
-        t->d_args.ensure(1);
-        UB_CUDA(cudaMemcpyAsync(t->d_args.p, &h, sizeof(MartArgs), cudaMemcpyHostToDevice, st));
-        // dataflow: chunks up to 32 problems; level barrier: up to 8
-        int exec_mode = mart_mode();
-        if (exec_mode == 1 && P > 8)
-            exec_mode = 2;
-        need(exec_mode != 2 || t->run == 1, "the level executor needs a line-granular schedule");
-        if (exec_mode == 2)
-            ensure_graph(t, h);
-        if (exec_mode == 0 && t->done_chunks != h.nchunks) {
-            const uint64_t n = uint64_t(t->n_runs) * uint64_t(h.nchunks);
-            t->d_done.alloc(n);
-            UB_CUDA(cudaMemsetAsync(t->d_done.p, 0, sizeof(unsigned) * n, st));
-            t->done_chunks = h.nchunks;
-            t->epoch = 0;
-        }
-        const int levels = int(t->level_off.size()) - 1;
+    MartArgs h;
+    h.tr = t->trace_args();
+    h.field = d_field;
+    h.proj = d_proj;
+    h.p_floor = t->w_pfloor.p;
+    h.active = t->w_active.p;
+    h.clamps = t->w_clamps.p;
+    h.beta = cfg->beta;
+    h.Sp = Sp;
+    h.nchunks = Sp / P;
+    h.max_recs = t->max_recs;
+    h.max_cells = t->max_cells;
+    h.run = t->run;
+    t->d_args.ensure(1);
+    UB_CUDA(cudaMemcpyAsync(t->d_args.p, &h, sizeof(MartArgs), cudaMemcpyHostToDevice, st));
+    // dataflow: chunks up to 32 problems; level barrier: up to 8
+    int exec_mode = mart_mode();
+    if (exec_mode == 1 && P > 8)
+        exec_mode = 2;
+    need(exec_mode != 2 || t->run == 1, "the level executor needs a line-granular schedule");
+    if (exec_mode == 2)
+        ensure_graph(t, h);
+    if (exec_mode == 0 && t->done_chunks != h.nchunks) {
+        const uint64_t n = uint64_t(t->n_runs) * uint64_t(h.nchunks);
+        t->d_done.alloc(n);
+        UB_CUDA(cudaMemsetAsync(t->d_done.p, 0, sizeof(unsigned) * n, st));
+        t->done_chunks = h.nchunks;
+        t->epoch = 0;
+    }
+    const int levels = int(t->level_off.size()) - 1;
 
-        std::vector<int> sweeps(S, 0), converged(S, 0);
-        std::vector<std::vector<double>> resid(S);
+    std::vector<int> sweeps(S, 0), converged(S, 0);
+    std::vector<std::vector<double>> resid(S);
+    if (track)
+        t->w_prev.ensure(cells * Sp), t->w_resid.ensure(Sp);
+    int n_active = 0;
+    for (int p = 0; p < S; ++p)
+        n_active += active[p];
+    cudaEvent_t e0, e1;
+    UB_CUDA(cudaEventCreate(&e0));
+    UB_CUDA(cudaEventCreate(&e1));
+    UB_CUDA(cudaEventRecord(e0, st));
+    for (int sweep = 0; sweep < cfg->max_sweeps && n_active > 0; ++sweep) {
         if (track)
-            t->w_prev.ensure(cells * Sp), t->w_resid.ensure(Sp);
-        int n_active = 0;
-        for (int p = 0; p < S; ++p)
-            n_active += active[p];
-        cudaEvent_t e0, e1;
-        UB_CUDA(cudaEventCreate(&e0));
-        UB_CUDA(cudaEventCreate(&e1));
-        UB_CUDA(cudaEventRecord(e0, st));
-        for (int sweep = 0; sweep < cfg->max_sweeps && n_active > 0; ++sweep) {
-            if (track)
-                UB_CUDA(cudaMemcpyAsync(t->w_prev.p, d_field, sizeof(float) * cells * Sp,
-                                        cudaMemcpyDeviceToDevice, st));
-            int n_run = 1;
-            if (exec_mode == 0) {
-                // without a per-sweep residual every remaining sweep runs in one
-                // launch, back to back (cross-sweep dependencies)
-                n_run = track ? 1 : cfg->max_sweeps - sweep;
-                // USCG_SWEEP_PROFILE=<file>: per-task stamps {grab, traced, ready, published}
-                static const char* prof_path = std::getenv("USCG_SWEEP_PROFILE");
-                const size_t nt = size_t(t->n_runs) * h.nchunks * n_run;
-                DevBuf<unsigned long long> prof;
-                if (prof_path)
-                    prof.alloc(nt * 16);
-                if (prof_path)
-                    UB_CUDA(cudaMemsetAsync(prof.p, 0, sizeof(unsigned long long) * nt * 16, st));
-                FlowSlab slab;
-                {
-                    const char* e = std::getenv("USCG_SLAB_Q");
-                    slab.Q = int(std::min<uint64_t>(units, e ? std::max(64, std::atoi(e)) : 8192));
-                }
-                // [n][indices][u16 next positions] (mart_sweep.cu, flow_tracer_runs)
-                slab.slot_words = (1 + t->max_cells + (t->max_cells + 1) / 2 + 31) & ~31;
-                t->w_slab.ensure(size_t(slab.Q) * slab.slot_words);
-                t->w_slab_ctl.ensure(size_t(slab.Q) * 2 + 1);
-                slab.data = t->w_slab.p;
-                slab.ready = t->w_slab_ctl.p;
-                slab.used = t->w_slab_ctl.p + slab.Q;
-                slab.tnext = t->w_slab_ctl.p + 2 * slab.Q;
-                FlowSchedule fs;
-                fs.order = t->d_order.p;
-                fs.pred_off = t->d_pred_off.p;
-                fs.succ_off = t->d_succ_off.p;
-                fs.succs = t->d_succs.p;
-                fs.npred_x = t->d_npred_x.p;
-                fs.n_runs = t->n_runs;
-                fs.run = t->run;
-                fs.runs_per_view = t->runs_per_view;
-                launch_mart_flow(h, fs, t->d_done.p, t->d_bar.p + 1, t->epoch + 1, n_run, t->n_rings,
-                                 slab, st, prof.p);
-                t->epoch += unsigned(n_run);
-                if (prof_path) {
-                    std::vector<unsigned long long> hp(nt * 16);
-                    UB_CUDA(cudaMemcpyAsync(hp.data(), prof.p, sizeof(unsigned long long) * hp.size(),
-                                            cudaMemcpyDeviceToHost, st));
-                    UB_CUDA(cudaStreamSynchronize(st));
-                    if (FILE* fp = std::fopen(prof_path, "wb")) {
-                        std::fwrite(hp.data(), sizeof(unsigned long long), hp.size(), fp);
-                        std::fclose(fp);
-                    }
-                }
-            } else if (exec_mode == 1) {
-                // USCG_SWEEP_PROFILE=<file>: per-level phase stamps of CTA 0 (diagnostics)
-                static const char* prof_path = std::getenv("USCG_SWEEP_PROFILE");
-                DevBuf<unsigned long long> prof;
-                if (prof_path) {
-                    prof.alloc(size_t(levels) * 4);
-                    UB_CUDA(cudaMemsetAsync(prof.p, 0, sizeof(unsigned long long) * levels * 4, st));
-                }
-                launch_mart_sweep(h, t->d_order.p, t->d_level_off.p, levels, t->d_bar.p, t->n_rings,
-                                  st, prof.p);
-                if (prof_path) {
-                    std::vector<unsigned long long> hp(size_t(levels) * 4);
-                    UB_CUDA(cudaMemcpyAsync(hp.data(), prof.p, sizeof(unsigned long long) * hp.size(),
-                                            cudaMemcpyDeviceToHost, st));
-                    UB_CUDA(cudaStreamSynchronize(st));
-                    if (FILE* fp = std::fopen(prof_path, "wb")) {
-                        std::fwrite(hp.data(), sizeof(unsigned long long), hp.size(), fp);
-                        std::fclose(fp);
-                    }
-                }
-            } else {
-                UB_CUDA(cudaGraphLaunch(t->graph.exec, st));
-                count_launch(t->graph.nodes);
+            UB_CUDA(cudaMemcpyAsync(t->w_prev.p, d_field, sizeof(float) * cells * Sp,
+                                    cudaMemcpyDeviceToDevice, st));
+        int n_run = 1;
+        if (exec_mode == 0) {
+            // without a per-sweep residual every remaining sweep runs in one
+            // launch, back to back (cross-sweep dependencies)
+            n_run = track ? 1 : cfg->max_sweeps - sweep;
+            // USCG_SWEEP_PROFILE=<file>: per-task stamps {grab, traced, ready, published}
+            static const char* prof_path = std::getenv("USCG_SWEEP_PROFILE");
+            const size_t nt = size_t(t->n_runs) * h.nchunks * n_run;
+            DevBuf<unsigned long long> prof;
+            if (prof_path)
+                prof.alloc(nt * 16);
+            if (prof_path)
+                UB_CUDA(cudaMemsetAsync(prof.p, 0, sizeof(unsigned long long) * nt * 16, st));
+            FlowSlab slab;
+            {
+                const char* e = std::getenv("USCG_SLAB_Q");
+                slab.Q = int(std::min<uint64_t>(units, e ? std::max(64, std::atoi(e)) : 8192));
             }
-            for (int p = 0; p < S; ++p)
-                sweeps[p] += active[p] * n_run;
-            sweep += n_run - 1;
-            if (track) {
-                UB_CUDA(cudaMemsetAsync(t->w_resid.p, 0, sizeof(unsigned int) * Sp, st));
-                launch_residual(d_field, t->w_prev.p, t->d_crossed.p, cells, S, Sp, t->w_resid.p, st);
-                std::vector<unsigned int> bits(Sp);
-                UB_CUDA(cudaMemcpyAsync(bits.data(), t->w_resid.p, sizeof(unsigned int) * Sp,
+            // [n][indices][u16 next positions] (mart_sweep.cu, flow_tracer_runs)
+            slab.slot_words = (1 + t->max_cells + (t->max_cells + 1) / 2 + 31) & ~31;
+            t->w_slab.ensure(size_t(slab.Q) * slab.slot_words);
+            t->w_slab_ctl.ensure(size_t(slab.Q) * 2 + 1);
+            slab.data = t->w_slab.p;
+            slab.ready = t->w_slab_ctl.p;
+            slab.used = t->w_slab_ctl.p + slab.Q;
+            slab.tnext = t->w_slab_ctl.p + 2 * slab.Q;
+            FlowSchedule fs;
+            fs.order = t->d_order.p;
+            fs.pred_off = t->d_pred_off.p;
+            fs.succ_off = t->d_succ_off.p;
+            fs.succs = t->d_succs.p;
+            fs.npred_x = t->d_npred_x.p;
+            fs.n_runs = t->n_runs;
+            fs.run = t->run;
+            fs.runs_per_view = t->runs_per_view;
+            launch_mart_flow(h, fs, t->d_done.p, t->d_bar.p + 1, t->epoch + 1, n_run, t->n_rings,
+                             slab, st, prof.p);
+            t->epoch += unsigned(n_run);
+            if (prof_path) {
+                std::vector<unsigned long long> hp(nt * 16);
+                UB_CUDA(cudaMemcpyAsync(hp.data(), prof.p, sizeof(unsigned long long) * hp.size(),
                                         cudaMemcpyDeviceToHost, st));
                 UB_CUDA(cudaStreamSynchronize(st));
-                bool changed = false;
-                for (int p = 0; p < S; ++p) {
-                    if (!active[p])
-                        continue;
-                    float r;
-                    std::memcpy(&r, &bits[p], sizeof(r));
-                    resid[p].push_back(double(r));
-                    if (double(r) <= cfg->tolerance) {
-                        converged[p] = 1;
-                        active[p] = 0;
-                        --n_active;
-                        changed = true;
-                    }
+                if (FILE* fp = std::fopen(prof_path, "wb")) {
+                    std::fwrite(hp.data(), sizeof(unsigned long long), hp.size(), fp);
+                    std::fclose(fp);
                 }
-                if (changed)
-                    UB_CUDA(cudaMemcpyAsync(t->w_active.p, active.data(), Sp, cudaMemcpyHostToDevice,
-                                            st));
             }
-        }
-        UB_CUDA(cudaEventRecord(e1, st));
-
-        // ---- field back ----
-        if (!direct_field) {
-            if (inter || S == 1) {
-                UB_CUDA(cudaMemcpyAsync(field_inout, d_field, sizeof(float) * cells * Sp,
-                                        dev ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, st));
-            } else {
-                float* dst = field_inout;
-                if (!dev) {
-                    t->w_stage.ensure(std::max<uint64_t>(units * S, cells * S));
-                    dst = t->w_stage.p;
+        } else if (exec_mode == 1) {
+            // USCG_SWEEP_PROFILE=<file>: per-level phase stamps of CTA 0 (diagnostics)
+            static const char* prof_path = std::getenv("USCG_SWEEP_PROFILE");
+            DevBuf<unsigned long long> prof;
+            if (prof_path) {
+                prof.alloc(size_t(levels) * 4);
+                UB_CUDA(cudaMemsetAsync(prof.p, 0, sizeof(unsigned long long) * levels * 4, st));
+            }
+            launch_mart_sweep(h, t->d_order.p, t->d_level_off.p, levels, t->d_bar.p, t->n_rings,
+                              st, prof.p);
+            if (prof_path) {
+                std::vector<unsigned long long> hp(size_t(levels) * 4);
+                UB_CUDA(cudaMemcpyAsync(hp.data(), prof.p, sizeof(unsigned long long) * hp.size(),
+                                        cudaMemcpyDeviceToHost, st));
+                UB_CUDA(cudaStreamSynchronize(st));
+                if (FILE* fp = std::fopen(prof_path, "wb")) {
+                    std::fwrite(hp.data(), sizeof(unsigned long long), hp.size(), fp);
+                    std::fclose(fp);
                 }
-                launch_from_interleaved(d_field, dst, cells, S, Sp, st);
-                if (!dev)
-                    UB_CUDA(cudaMemcpyAsync(field_inout, dst, sizeof(float) * cells * S,
-                                            cudaMemcpyDeviceToHost, st));
             }
+        } else {
+            UB_CUDA(cudaGraphLaunch(t->graph.exec, st));
+            count_launch(t->graph.nodes);
         }
-        std::vector<unsigned long long> clamps(Sp);
-        UB_CUDA(cudaMemcpyAsync(clamps.data(), t->w_clamps.p, sizeof(unsigned long long) * Sp,
-                                cudaMemcpyDeviceToHost, st));
-        UB_CUDA(cudaStreamSynchronize(st));
-        float ms = 0;
-        UB_CUDA(cudaEventElapsedTime(&ms, e0, e1));
-        cudaEventDestroy(e0);
-        cudaEventDestroy(e1);
-
-        if (reports) {
-            std::vector<uint8_t> crossed;
-            bool need_crossed = false;
-            for (int p = 0; p < S; ++p)
-                need_crossed |= reports[p].crossed != nullptr;
-            if (need_crossed) {
-                crossed.resize(cells);
-                UB_CUDA(cudaMemcpy(crossed.data(), t->d_crossed.p, cells, cudaMemcpyDeviceToHost));
-            }
+        if (after_launch) {
+            (*after_launch)();
+            after_launch = nullptr;
+        }
+        for (int p = 0; p < S; ++p)
+            sweeps[p] += active[p] * n_run;
+        sweep += n_run - 1;
+        if (track) {
+            UB_CUDA(cudaMemsetAsync(t->w_resid.p, 0, sizeof(unsigned int) * Sp, st));
+            launch_residual(d_field, t->w_prev.p, t->d_crossed.p, cells, S, Sp, t->w_resid.p, st);
+            std::vector<unsigned int> bits(Sp);
+            UB_CUDA(cudaMemcpyAsync(bits.data(), t->w_resid.p, sizeof(unsigned int) * Sp,
+                                    cudaMemcpyDeviceToHost, st));
+            UB_CUDA(cudaStreamSynchronize(st));
+            bool changed = false;
             for (int p = 0; p < S; ++p) {
-                uscg_report& r = reports[p];
-                r.sweeps = sweeps[p];
-                r.converged = converged[p];
-                r.all_zero_data = all_zero[p];
-                r.seconds = ms * 1e-3;
-                r.factor_clamps = clamps[p];
-                r.updates = uint64_t(upd[p]) * uint64_t(sweeps[p]);
-                // zero-measurement lines are skipped in every sweep (solver.cpp:119-127)
-                r.zero_measurement_skips = uint64_t(double(units) - stats[4 * p + 0]) * uint64_t(sweeps[p]);
-                if (r.sweep_residuals)
-                    for (size_t i = 0; i < resid[p].size(); ++i)
-                        r.sweep_residuals[i] = resid[p][i];
-                if (r.crossed) {
-                    if (all_zero[p])
-                        std::memset(r.crossed, 0, cells);
-                    else
-                        std::memcpy(r.crossed, crossed.data(), cells);
+                if (!active[p])
+                    continue;
+                float r;
+                std::memcpy(&r, &bits[p], sizeof(r));
+                resid[p].push_back(double(r));
+                if (double(r) <= cfg->tolerance) {
+                    converged[p] = 1;
+                    active[p] = 0;
+                    --n_active;
+                    changed = true;
                 }
             }
+            if (changed)
+                UB_CUDA(cudaMemcpyAsync(t->w_active.p, active.data(), Sp, cudaMemcpyHostToDevice,
+                                        st));
         }
+    }
+    UB_CUDA(cudaEventRecord(e1, st));
+    if (after_launch)  // no sweep ran
+        (*after_launch)();
+
+    // ---- field back ----
+    if (!direct_field) {
+        if (inter || S == 1) {
+            UB_CUDA(cudaMemcpyAsync(field_inout, d_field, sizeof(float) * cells * Sp,
+                                    dev ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, st));
+        } else {
+            float* dst = field_inout;
+            if (!dev) {
+                t->w_stage.ensure(std::max<uint64_t>(units * S, cells * S));
+                dst = t->w_stage.p;
+            }
+            launch_from_interleaved(d_field, dst, cells, S, Sp, st);
+            if (!dev)
+                UB_CUDA(cudaMemcpyAsync(field_inout, dst, sizeof(float) * cells * S,
+                                        cudaMemcpyDeviceToHost, st));
+        }
+    }
+    std::vector<unsigned long long> clamps(Sp);
+    UB_CUDA(cudaMemcpyAsync(clamps.data(), t->w_clamps.p, sizeof(unsigned long long) * Sp,
+                            cudaMemcpyDeviceToHost, st));
+    UB_CUDA(cudaStreamSynchronize(st));
+    float ms = 0;
+    UB_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+
+    if (reports) {
+        std::vector<uint8_t> crossed;
+        bool need_crossed = false;
+        for (int p = 0; p < S; ++p)
+            need_crossed |= reports[p].crossed != nullptr;
+        if (need_crossed) {
+            crossed.resize(cells);
+            UB_CUDA(cudaMemcpy(crossed.data(), t->d_crossed.p, cells, cudaMemcpyDeviceToHost));
+        }
+        for (int p = 0; p < S; ++p) {
+            uscg_report& r = reports[p];
+            r.sweeps = sweeps[p];
+            r.converged = converged[p];
+            r.all_zero_data = all_zero[p];
+            r.seconds = ms * 1e-3;
+            r.factor_clamps = clamps[p];
+            r.updates = uint64_t(upd[p]) * uint64_t(sweeps[p]);
+            // zero-measurement lines are skipped in every sweep (solver.cpp:119-127)
+            r.zero_measurement_skips = uint64_t(double(units) - stats[4 * p + 0]) * uint64_t(sweeps[p]);
+            if (r.sweep_residuals)
+                for (size_t i = 0; i < resid[p].size(); ++i)
+                    r.sweep_residuals[i] = resid[p][i];
+            if (r.crossed) {
+                if (all_zero[p])
+                    std::memset(r.crossed, 0, cells);
+                else
+                    std::memcpy(r.crossed, crossed.data(), cells);
+            }
+        }
+    }
+}
+
+uscg_status uscg_reconstruct(uscg_tracer t, const float* proj, int32_t problems,
+                             const uscg_solver_config* cfg, float* field_inout, int32_t from_init,
+                             uscg_report* reports, uint32_t flags) {
+    return guarded([&] { reconstruct_body(t, proj, problems, cfg, field_inout, from_init, reports, flags, nullptr); });
+}
+
+// Batched reconstruction with copy/compute overlap. Device memory: two
+// staging sets (the host layout of one stack: projections and field) and,
+// for the [S][n] host layout, one interleaved working set that the solves
+// use in turn. Per stack b (set k = b % 2):
+//   copy-in stream : [wait: set k free] H2D proj/field -> in[k]      -> ev_in[b]
+//   ctx stream     : [wait ev_in[b]] to_interleaved -> work           -> ev_used[b]
+//                    uscg_reconstruct(work, device pointers)
+//                    [wait: out[k] free] from_interleaved -> out[k]   -> ev_ready[b]
+//   copy-out stream: [wait ev_ready[b]] D2H out[k] -> host            -> ev_out[b]
+// With the interleaved host layout (or S == 1) the solve runs in place on
+// in[k] and downloads from it, so in[k] is free only after ev_out[b].
+uscg_status uscg_reconstruct_batch(uscg_tracer t, int32_t batch, const float* const* proj, int32_t problems,
+                                   const uscg_solver_config* cfg, float* const* field_inout, int32_t from_init,
+                                   uscg_report* reports, uint32_t flags) {
+    // events of one call (destroyed after both copy streams drained)
+    struct Events {
+        std::vector<cudaEvent_t> ev;
+        cudaStream_t in, out;
+        ~Events() {
+            if (in)
+                cudaStreamSynchronize(in);
+            if (out)
+                cudaStreamSynchronize(out);
+            for (cudaEvent_t e : ev)
+                cudaEventDestroy(e);
+        }
+        cudaEvent_t make() {
+            cudaEvent_t e;
+            UB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+            ev.push_back(e);
+            return e;
+        }
+    };
+    return guarded([&] {
+        need(t != nullptr, "null tracer");
+        need(batch >= 0, "batch must be >= 0");
+        need(batch == 0 || (proj && field_inout), "null buffer");
+        need(!(flags & USCG_DEVICE_POINTERS), "uscg_reconstruct_batch takes host buffers");
+        need(problems >= 1, "problem count must be >= 1");
+        for (int b = 0; b < batch; ++b)
+            need(proj[b] && field_inout[b], "null buffer");
+        if (batch == 0)
+            return;
+        bind(t->ctx);
+        const int S = problems, Sp = problem_stride(S);
+        const bool inter = (flags & USCG_LAYOUT_INTERLEAVED) || S == 1;
+        const uint64_t units = t->units(), cells = t->cells;
+        const uint64_t pw = inter ? units * Sp : units * S;  // host-layout words per stack
+        const uint64_t fw = inter ? cells * Sp : cells * S;
+        cudaStream_t st = t->st();
+        if (!t->copy_in)
+            UB_CUDA(cudaStreamCreateWithFlags(&t->copy_in, cudaStreamNonBlocking));
+        if (!t->copy_out)
+            UB_CUDA(cudaStreamCreateWithFlags(&t->copy_out, cudaStreamNonBlocking));
+        Events E{{}, t->copy_in, t->copy_out};
+        DevBuf<float>* in = t->w_bin;
+        DevBuf<float>* out = t->w_bout;
+        for (int k = 0; k < 2 && k < batch; ++k) {
+            in[k].ensure(pw + fw);
+            if (!inter)
+                out[k].ensure(fw);
+        }
+        if (!inter) {  // the solves' interleaved working set
+            t->w_proj.ensure(units * Sp);
+            t->w_field.ensure(cells * Sp);
+        }
+        std::vector<cudaEvent_t> ev_in(batch), ev_free(batch), ev_ready(batch), ev_out(batch);
+        for (int b = 0; b < batch; ++b) {
+            ev_in[b] = E.make();
+            ev_free[b] = E.make();
+            ev_ready[b] = E.make();
+            ev_out[b] = E.make();
+        }
+        // earlier work on the context stream (e.g. the caller's) precedes the uploads
+        cudaEvent_t start = E.make();
+        UB_CUDA(cudaEventRecord(start, st));
+        UB_CUDA(cudaStreamWaitEvent(t->copy_in, start, 0));
+        auto upload = [&](int b) {
+            const int k = b % 2;
+            if (b >= 2)  // in[k] is free once stack b-2 no longer needs it
+                UB_CUDA(cudaStreamWaitEvent(t->copy_in, ev_free[b - 2], 0));
+            UB_CUDA(cudaMemcpyAsync(in[k].p, proj[b], sizeof(float) * pw, cudaMemcpyHostToDevice, t->copy_in));
+            if (from_init)
+                UB_CUDA(cudaMemcpyAsync(in[k].p + pw, field_inout[b], sizeof(float) * fw, cudaMemcpyHostToDevice,
+                                        t->copy_in));
+            UB_CUDA(cudaEventRecord(ev_in[b], t->copy_in));
+        };
+        // stack b-1's download is queued only once stack b's solve is launched:
+        // the solve's small host reads (validation statistics) would otherwise
+        // wait behind it on the copy engine, serializing download and solve
+        auto download = [&](int b) {
+            UB_CUDA(cudaStreamWaitEvent(t->copy_out, ev_ready[b], 0));
+            const float* src = inter ? in[b % 2].p + pw : out[b % 2].p;
+            UB_CUDA(cudaMemcpyAsync(field_inout[b], src, sizeof(float) * fw, cudaMemcpyDeviceToHost,
+                                    t->copy_out));
+            UB_CUDA(cudaEventRecord(ev_out[b], t->copy_out));
+            if (inter)  // the solve ran in place on in[k]: free after the download
+                UB_CUDA(cudaEventRecord(ev_free[b], t->copy_out));
+        };
+        upload(0);
+        for (int b = 0; b < batch; ++b) {
+            const int k = b % 2;
+            UB_CUDA(cudaStreamWaitEvent(st, ev_in[b], 0));
+            float* d_proj = in[k].p;
+            float* d_field = in[k].p + pw;
+            if (!inter) {
+                launch_to_interleaved(in[k].p, t->w_proj.p, units, S, Sp, 0.f, st);
+                if (from_init)
+                    launch_to_interleaved(in[k].p + pw, t->w_field.p, cells, S, Sp, 1.f, st);
+                UB_CUDA(cudaEventRecord(ev_free[b], st));
+                d_proj = t->w_proj.p;
+                d_field = t->w_field.p;
+            }
+            const std::function<void()> hook = [&] {
+                if (b >= 1)
+                    download(b - 1);
+                if (b + 1 < batch)
+                    upload(b + 1);  // overlaps this stack's solve
+            };
+            reconstruct_body(t, d_proj, S, cfg, d_field, from_init, reports ? reports + size_t(b) * S : nullptr,
+                             USCG_DEVICE_POINTERS | USCG_LAYOUT_INTERLEAVED, &hook);
+            if (!inter) {
+                if (b >= 2)  // out[k] is free once stack b-2 has been downloaded
+                    UB_CUDA(cudaStreamWaitEvent(st, ev_out[b - 2], 0));
+                launch_from_interleaved(t->w_field.p, out[k].p, cells, S, Sp, st);
+            }
+            UB_CUDA(cudaEventRecord(ev_ready[b], st));
+        }
+        download(batch - 1);
+        // the context stream ends after the last download (callers time on it)
+        UB_CUDA(cudaStreamWaitEvent(st, ev_out[batch - 1], 0));
+        UB_CUDA(cudaStreamSynchronize(t->copy_out));
+        UB_CUDA(cudaStreamSynchronize(t->copy_in));
+        UB_CUDA(cudaStreamSynchronize(st));
     });
 }
 

@@ -119,7 +119,7 @@ EXPORTS = [
     "uscg_tracer_get_info", "uscg_tracer_export_cache", "uscg_trace_line", "uscg_trace_counts",
     "uscg_trace_checksums", "uscg_tracer_export_schedule", "uscg_tracer_copy_cache",
     "uscg_tracer_import_cache_keys",
-    "uscg_tracer_build_schedule", "uscg_tracer_export_successors", "uscg_problem_stride", "uscg_project", "uscg_reconstruct",
+    "uscg_tracer_build_schedule", "uscg_tracer_export_successors", "uscg_reconstruct_batch", "uscg_problem_stride", "uscg_project", "uscg_reconstruct",
     "uscg_resample", "uscg_uspg_to_cg_map", "uscg_diag_math", "uscg_schedule_build", "uscg_image_metrics",
     "uscg_cartesian_like", "uscg_csystem_create", "uscg_csystem_info", "uscg_csystem_export",
     "uscg_csystem_reconstruct", "uscg_csystem_destroy",
@@ -175,6 +175,8 @@ def load(build_if_missing: bool = True):
     L.uscg_project.argtypes = [vp, vp, C.c_int32, vp, C.c_uint32]
     L.uscg_reconstruct.argtypes = [vp, vp, C.c_int32, C.POINTER(_Cfg), vp, C.c_int32, C.POINTER(_Report),
                                    C.c_uint32]
+    L.uscg_reconstruct_batch.argtypes = [vp, C.c_int32, C.POINTER(vp), C.c_int32, C.POINTER(_Cfg), C.POINTER(vp),
+                                         C.c_int32, C.POINTER(_Report), C.c_uint32]
     L.uscg_resample.argtypes = [vp, C.POINTER(_Grid), vp, C.c_int32, C.c_int32, vp, C.c_uint32]
     L.uscg_uspg_to_cg_map.argtypes = [vp, C.c_int32, _u32p]
     L.uscg_cartesian_like.argtypes = [C.POINTER(_Grid), C.POINTER(_Cart)]
@@ -740,6 +742,41 @@ def reconstruct_stack(projections: np.ndarray, cfg: SolverConfig, tracer: Tracer
     projections (S, views, lines) -> list of (field (cell_count,), ReconReport)."""
     S = projections.shape[0]
     return _run(projections, init, cfg, tracer, S, with_crossed)
+
+
+def reconstruct_batch(stacks, cfg: SolverConfig, tracer: Tracer, inits=None):
+    """reconstruct_stack over several independent stacks (each (S, views,
+    lines)) in one call, their host transfers overlapped with the neighbouring
+    stacks' solves (uscg_reconstruct_batch); returns one list of fields
+    (S, cell_count) per stack. Host buffers are pinned (torch) when torch is
+    importable, so the copies can overlap."""
+    inf = tracer.info()
+    cells, units = inf["cell_count"], inf["views"] * inf["lines"]
+    B = len(stacks)
+    if B == 0:
+        return []
+    S = int(np.asarray(stacks[0]).shape[0])
+    try:
+        import torch
+        pin = lambda a: torch.from_numpy(np.ascontiguousarray(a, dtype=np.float32)).pin_memory()  # noqa: E731
+        host = lambda t: t.numpy()  # noqa: E731
+    except Exception:  # pragma: no cover - torch is part of the image
+        pin = lambda a: np.ascontiguousarray(a, dtype=np.float32)  # noqa: E731
+        host = lambda t: t  # noqa: E731
+    projs, flds = [], []
+    for b in range(B):
+        p = np.asarray(stacks[b], dtype=np.float32).reshape(S, -1)
+        if p.shape[1] != units:
+            raise InvalidArgument(f"projection data size does not match geometry: got {p.shape[1]}, "
+                                  f"expected {units}")
+        projs.append(pin(p))
+        flds.append(pin(np.zeros((S, cells), np.float32) if inits is None
+                        else np.asarray(inits[b], np.float32).reshape(S, cells)))
+    pp = (C.c_void_p * B)(*[C.c_void_p(host(x).ctypes.data) for x in projs])
+    ff = (C.c_void_p * B)(*[C.c_void_p(host(x).ctypes.data) for x in flds])
+    c = _Cfg(cfg.beta, cfg.tolerance, cfg.max_sweeps, cfg.f_init, cfg.p_floor)
+    _check(load().uscg_reconstruct_batch(tracer.h, B, pp, S, C.byref(c), ff, 0 if inits is None else 1, None, 0))
+    return [host(f).copy() for f in flds]
 
 
 def field_to_cartesian(field: Field, npix: Optional[int] = None, ctx: Optional[Context] = None) -> np.ndarray:

@@ -552,6 +552,36 @@ def test_pipelined_runs_are_bit_identical(ub, orc, monkeypatch, capfd, S, run, w
     assert (np.abs(out[1][0] - want) / want).max() <= 1e-4
 
 
+@pytest.mark.parametrize("S,init", [(1, False), (5, False), (8, True)])
+def test_batched_reconstruction_equals_one_call_per_stack(ub, orc, S, init):
+    """uscg_reconstruct_batch (transfers of neighbouring stacks overlapped with
+    each solve, double-buffered staging) returns exactly what one
+    uscg_reconstruct call per stack returns, for 1-4 stacks (the ping-pong
+    buffers are reused from the third stack on)."""
+    spec, geom, tr, _ = _m1_case(ub, orc, "arc", n_rings=32, views=12, du=64)
+    rng = np.random.default_rng(11 + S)
+    cfg = ub.SolverConfig(beta=0.5, tolerance=0, max_sweeps=2)
+    for B in (1, 4):
+        stacks = [ub.project_stack(tr, rng.uniform(0.2, 3.0, (S, spec.cell_count())).astype(np.float32))
+                  for _ in range(B)]
+        inits = [rng.uniform(0.5, 1.5, (S, spec.cell_count())).astype(np.float32) for _ in range(B)] if init else None
+        got = ub.reconstruct_batch(stacks, cfg, tr, inits)
+        for b in range(B):
+            want = ub.reconstruct_stack(stacks[b], cfg, tr, None if inits is None else inits[b])
+            for p in range(S):
+                assert np.array_equal(got[b][p], want[p][0]), (B, b, p)
+
+
+def test_batched_reconstruction_reports_the_failing_stack(ub, orc):
+    """A stack with invalid data fails the batch with the reference's error."""
+    spec, geom, tr, _ = _m1_case(ub, orc, "arc", n_rings=32, views=12, du=64)
+    good = ub.project_stack(tr, np.ones((2, spec.cell_count()), np.float32))
+    bad = good.copy()
+    bad[1, 0, 0] = -1.0
+    with pytest.raises(ub.InvalidArgument, match="non-finite or negative"):
+        ub.reconstruct_batch([good, bad, good], ub.SolverConfig(beta=0.5, tolerance=0, max_sweeps=1), tr)
+
+
 # ---------------------------------------------------------------------------
 # generalized seams (verbatim BASELINE shapes) vs the C restatement
 # ---------------------------------------------------------------------------

@@ -423,32 +423,87 @@ uscg_tracer_s* build_from_rays(uscg_ctx ctx, const uscg_grid* grid, int lines, c
     DevBuf<uint32_t> d_cnt;
     d_cnt.alloc(size_t(lines));
     t->d_off.alloc(size_t(lines) + 1);
-    // generator device time: count + scan, then write + annotate (the host
-    // allocation of the record store between them is not counted)
-    cudaEvent_t ev[4];
+    // generator device time: the passes before and after the host allocation
+    // of the record store (the allocation itself is not counted)
+    cudaEvent_t ev[6];  // [0,1] count or bound, [4,5] slot pass, [2,3] write or compaction + annotate
     for (auto& e : ev)
         UB_CUDA(cudaEventCreate(&e));
-    UB_CUDA(cudaEventRecord(ev[0], t->st()));
-    launch_generate_count(g, lines, d_rays.p, d_rays.p + 3 * size_t(lines), d_cnt.p, t->st());
-    launch_exclusive_scan_u32(d_cnt.p, t->d_off.p, lines, t->st());
-    UB_CUDA(cudaEventRecord(ev[1], t->st()));
+    bool timed_slots = false;
+    const double* src_d = d_rays.p;
+    const double* det_d = d_rays.p + 3 * size_t(lines);
     std::vector<uint32_t> off(size_t(lines) + 1);
-    UB_CUDA(cudaMemcpyAsync(off.data(), t->d_off.p, sizeof(uint32_t) * (lines + 1),
-                            cudaMemcpyDeviceToHost, t->st()));
-    UB_CUDA(cudaStreamSynchronize(t->st()));
+    // One pass (default): bounded slots, then compaction. The bound is at most
+    // 2 n_rings + n_slices + 4 records per ray; the slot scratch must fit in u32
+    // offsets and in device memory, else (or on a slot overflow) the exact
+    // count pass runs first.
+    bool one_pass = std::getenv("USCG_GEN_TWO_PASS") == nullptr &&
+                    uint64_t(lines) * uint64_t(2 * t->n_rings + (t->volume ? t->n_slices : 0) + 4) < (1ull << 32);
+    DevBuf<uint32_t> d_boff, d_skey;
+    DevBuf<double> d_spa, d_spb;
+    DevBuf<unsigned> d_flag;
+    if (one_pass) {
+        UB_CUDA(cudaEventRecord(ev[0], t->st()));
+        launch_generate_bound(g, lines, src_d, det_d, d_cnt.p, t->st());
+        d_boff.alloc(size_t(lines) + 1);
+        launch_exclusive_scan_u32(d_cnt.p, d_boff.p, lines, t->st());
+        UB_CUDA(cudaEventRecord(ev[1], t->st()));
+        uint32_t slots = 0;
+        UB_CUDA(cudaMemcpy(&slots, d_boff.p + lines, sizeof(uint32_t), cudaMemcpyDeviceToHost));
+        size_t free_b = 0, total_b = 0;
+        UB_CUDA(cudaMemGetInfo(&free_b, &total_b));
+        one_pass = double(slots) * 40.0 < 0.8 * double(free_b);  // slots + the packed store
+        if (one_pass) {
+            const size_t n = std::max<size_t>(slots, 1);
+            d_spa.alloc(n);
+            d_spb.alloc(n);
+            d_skey.alloc(n);
+            d_flag.alloc(1);
+            UB_CUDA(cudaMemsetAsync(d_flag.p, 0, sizeof(unsigned), t->st()));
+            UB_CUDA(cudaEventRecord(ev[4], t->st()));
+            launch_generate_slots(g, lines, src_d, det_d, d_boff.p, d_spa.p, d_spb.p, d_skey.p, d_cnt.p, d_flag.p,
+                                  t->st());
+            launch_exclusive_scan_u32(d_cnt.p, t->d_off.p, lines, t->st());
+            UB_CUDA(cudaEventRecord(ev[5], t->st()));
+            timed_slots = true;
+            unsigned overflow = 0;
+            UB_CUDA(cudaMemcpyAsync(&overflow, d_flag.p, sizeof(unsigned), cudaMemcpyDeviceToHost, t->st()));
+            UB_CUDA(cudaMemcpyAsync(off.data(), t->d_off.p, sizeof(uint32_t) * (lines + 1), cudaMemcpyDeviceToHost,
+                                    t->st()));
+            UB_CUDA(cudaStreamSynchronize(t->st()));
+            one_pass = overflow == 0;
+        }
+    }
+    if (!one_pass) {
+        d_spa.release();
+        d_spb.release();
+        d_skey.release();
+        timed_slots = false;
+        UB_CUDA(cudaEventRecord(ev[0], t->st()));
+        launch_generate_count(g, lines, src_d, det_d, d_cnt.p, t->st());
+        launch_exclusive_scan_u32(d_cnt.p, t->d_off.p, lines, t->st());
+        UB_CUDA(cudaEventRecord(ev[1], t->st()));
+        UB_CUDA(cudaMemcpyAsync(off.data(), t->d_off.p, sizeof(uint32_t) * (lines + 1), cudaMemcpyDeviceToHost,
+                                t->st()));
+        UB_CUDA(cudaStreamSynchronize(t->st()));
+    }
     t->records = off[lines];
     const size_t R = std::max<size_t>(t->records, 1);
     t->d_pa.alloc(R);
     t->d_pb.alloc(R);
     t->d_key.alloc(R);
     UB_CUDA(cudaEventRecord(ev[2], t->st()));
-    launch_generate_write(g, lines, d_rays.p, d_rays.p + 3 * size_t(lines), t->d_off.p, t->d_pa.p,
-                          t->d_pb.p, t->d_key.p, t->st());
+    if (one_pass)
+        launch_compact_records(lines, d_boff.p, t->d_off.p, d_spa.p, d_spb.p, d_skey.p, t->d_pa.p, t->d_pb.p,
+                               t->d_key.p, t->st());
+    else
+        launch_generate_write(g, lines, src_d, det_d, t->d_off.p, t->d_pa.p, t->d_pb.p, t->d_key.p, t->st());
     finish_tracer(t.get(), off, ev[3]);
-    float a = 0, b = 0;
+    float a = 0, b = 0, c = 0;
     UB_CUDA(cudaEventElapsedTime(&a, ev[0], ev[1]));
     UB_CUDA(cudaEventElapsedTime(&b, ev[2], ev[3]));
-    t->generator_ms = double(a) + double(b);
+    if (timed_slots)
+        UB_CUDA(cudaEventElapsedTime(&c, ev[4], ev[5]));
+    t->generator_ms = double(a) + double(b) + double(c);
     for (auto& e : ev)
         cudaEventDestroy(e);
     return t.release();

@@ -292,7 +292,7 @@ __device__ uint32_t walk_ray(const DevGrid& g, const double* s, const double* d,
 // consecutive kept chords share their azimuth at the common point
 template <bool WRITE>
 __device__ uint32_t generate_ray(const DevGrid& g, const double* s, const double* d, double* pa,
-                                 double* pb, uint32_t* key) {
+                                 double* pb, uint32_t* key, uint32_t cap = 0xFFFFFFFFu) {
     double phi_prev = -1.0;
     uint32_t k = 0;
     return walk_ray(
@@ -302,9 +302,11 @@ __device__ uint32_t generate_ray(const DevGrid& g, const double* s, const double
                 if (phi_prev < 0)
                     phi_prev = azimuth_deg(p0, p1);
                 const double phi_q = azimuth_deg(q0, q1);
-                pa[k] = phi_prev;
-                pb[k] = phi_q;
-                key[k] = uint32_t(ring) | (uint32_t(slice) << kSliceShift);
+                if (k < cap) {
+                    pa[k] = phi_prev;
+                    pb[k] = phi_q;
+                    key[k] = uint32_t(ring) | (uint32_t(slice) << kSliceShift);
+                }
                 phi_prev = phi_q;
                 ++k;
             }
@@ -333,6 +335,94 @@ __global__ void generate_write_kernel(DevGrid g, int lines, const double* __rest
         return;
     const uint32_t o = off[l];
     generate_ray<true>(g, src + 3 * size_t(l), det + 3 * size_t(l), pa + o, pb + o, key + o);
+}
+
+// One-pass generator. A ray's records are at most its crossings (a kept chord
+// joins two consecutive crossings): the ring circles it reaches, twice each,
+// and the z-planes its segment spans. bound_kernel over-estimates that count
+// without walking the ray; the write pass fills each ray's bounded slot,
+// records its true count and flags any ray whose slot was too small (the
+// caller then falls back to the exact count pass); compaction packs the slots.
+__global__ void generate_bound_kernel(DevGrid g, int lines, const double* __restrict__ src,
+                                      const double* __restrict__ det, uint32_t* __restrict__ bound) {
+    const int l = blockIdx.x * blockDim.x + threadIdx.x;
+    if (l >= lines)
+        return;
+    const double* s = src + 3 * size_t(l);
+    const double* d = det + 3 * size_t(l);
+    const double dir0 = d[0] - s[0], dir1 = d[1] - s[1], dir2 = d[2] - s[2];
+    const double ux = s[0] - d[0], uy = s[1] - d[1];
+    const double uxy2 = ux * ux + uy * uy;
+    const double dd2 = dir0 * dir0 + dir1 * dir1 + dir2 * dir2;
+    const bool axial = dd2 == 0.0 || uxy2 <= 1e-24 * dd2;
+    uint32_t b = 2;
+    if (!axial) {
+        const double cross = s[0] * d[1] - s[1] * d[0];
+        const double dist = sqrt(cross * cross / uxy2);
+        const int k0 = max(1, int(floor(dist / g.ring_spacing)) - 1);
+        if (k0 <= g.n_rings)
+            b += 2u * uint32_t(g.n_rings - k0 + 1);
+    }
+    if (g.volume && dir2 != 0.0) {
+        const double za = fmin(s[2], d[2]) + g.zoff, zb = fmax(s[2], d[2]) + g.zoff;
+        const int lo = max(0, int(ceil(za / g.slice_height)) - 1);
+        const int hi = min(g.n_slices, int(floor(zb / g.slice_height)) + 1);
+        if (hi >= lo)
+            b += uint32_t(hi - lo + 1);
+    }
+    bound[l] = b;
+}
+
+__global__ void generate_slot_kernel(DevGrid g, int lines, const double* __restrict__ src,
+                                     const double* __restrict__ det, const uint32_t* __restrict__ boff,
+                                     double* pa, double* pb, uint32_t* key, uint32_t* __restrict__ counts,
+                                     unsigned* overflow) {
+    const int l = blockIdx.x * blockDim.x + threadIdx.x;
+    if (l >= lines)
+        return;
+    const uint32_t o = boff[l], cap = boff[l + 1] - o;
+    const uint32_t n = generate_ray<true>(g, src + 3 * size_t(l), det + 3 * size_t(l), pa + o, pb + o, key + o,
+                                          cap);
+    counts[l] = n;
+    if (n > cap)
+        atomicOr(overflow, 1u);
+}
+
+// warp per ray: its records from the bounded slot to the packed store
+__global__ void compact_records_kernel(int lines, const uint32_t* __restrict__ boff,
+                                       const uint32_t* __restrict__ off, const double* __restrict__ spa,
+                                       const double* __restrict__ spb, const uint32_t* __restrict__ skey,
+                                       double* __restrict__ pa, double* __restrict__ pb, uint32_t* __restrict__ key) {
+    const int l = int((blockIdx.x * size_t(blockDim.x) + threadIdx.x) >> 5);
+    const int lane = threadIdx.x & 31;
+    if (l >= lines)
+        return;
+    const uint32_t from = boff[l], to = off[l], n = off[l + 1] - to;
+    for (uint32_t i = lane; i < n; i += 32) {
+        pa[to + i] = spa[from + i];
+        pb[to + i] = spb[from + i];
+        key[to + i] = skey[from + i];
+    }
+}
+
+void launch_generate_bound(const DevGrid& g, int lines, const double* src, const double* det, uint32_t* bound,
+                           cudaStream_t st) {
+    generate_bound_kernel<<<cdiv(lines, 128), 128, 0, st>>>(g, lines, src, det, bound);
+    check_launch();
+}
+
+void launch_generate_slots(const DevGrid& g, int lines, const double* src, const double* det, const uint32_t* boff,
+                           double* pa, double* pb, uint32_t* key, uint32_t* counts, unsigned* overflow,
+                           cudaStream_t st) {
+    generate_slot_kernel<<<cdiv(lines, 64), 64, 0, st>>>(g, lines, src, det, boff, pa, pb, key, counts, overflow);
+    check_launch();
+}
+
+void launch_compact_records(int lines, const uint32_t* boff, const uint32_t* off, const double* spa,
+                            const double* spb, const uint32_t* skey, double* pa, double* pb, uint32_t* key,
+                            cudaStream_t st) {
+    compact_records_kernel<<<cdiv(lines, 8), 256, 0, st>>>(lines, boff, off, spa, spb, skey, pa, pb, key);
+    check_launch();
 }
 
 // =============================================================================
@@ -593,52 +683,6 @@ void launch_annotate(int lines, const uint32_t* off, const double* pa, const dou
     check_launch();
 }
 
-// ---- exclusive scan (single block, chunked; used for the record offsets) ----
-__global__ void scan_kernel(const uint32_t* __restrict__ in, uint32_t* out, int n) {
-    __shared__ uint32_t s_warp[32];
-    __shared__ uint32_t s_carry;
-    if (threadIdx.x == 0)
-        s_carry = 0;
-    __syncthreads();
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    for (int base = 0; base < n; base += 1024) {
-        const int i = base + threadIdx.x;
-        const uint32_t v = i < n ? in[i] : 0u;
-        uint32_t x = v;
-        for (int o = 1; o < 32; o <<= 1) {
-            const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, x, o);
-            if (lane >= o)
-                x += y;
-        }
-        if (lane == 31)
-            s_warp[warp] = x;
-        __syncthreads();
-        if (warp == 0) {
-            uint32_t w = s_warp[lane];
-            for (int o = 1; o < 32; o <<= 1) {
-                const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, w, o);
-                if (lane >= o)
-                    w += y;
-            }
-            s_warp[lane] = w;
-        }
-        __syncthreads();
-        const uint32_t incl = x + (warp > 0 ? s_warp[warp - 1] : 0u) + s_carry;
-        if (i < n)
-            out[i] = incl - v;
-        __syncthreads();
-        if (threadIdx.x == 1023)
-            s_carry = incl;
-        __syncthreads();
-    }
-    if (threadIdx.x == 0)
-        out[n] = s_carry;
-}
-
-void launch_exclusive_scan_u32(const uint32_t* in, uint32_t* out, int n, cudaStream_t st) {
-    scan_kernel<<<1, 1024, 0, st>>>(in, out, n);
-    check_launch();
-}
 
 // =============================================================================
 // traces

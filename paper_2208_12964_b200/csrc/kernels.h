@@ -38,6 +38,16 @@ void launch_generate_count(const DevGrid& g, int lines, const double* src, const
 void launch_generate_write(const DevGrid& g, int lines, const double* src, const double* det,
                            const uint32_t* off, double* pa, double* pb, uint32_t* key,
                            cudaStream_t st);
+// one-pass form: per-ray record bound, bounded slots (true counts, overflow
+// flag), compaction into the packed store
+void launch_generate_bound(const DevGrid& g, int lines, const double* src, const double* det, uint32_t* bound,
+                           cudaStream_t st);
+void launch_generate_slots(const DevGrid& g, int lines, const double* src, const double* det, const uint32_t* boff,
+                           double* pa, double* pb, uint32_t* key, uint32_t* counts, unsigned* overflow,
+                           cudaStream_t st);
+void launch_compact_records(int lines, const uint32_t* boff, const uint32_t* off, const double* spa,
+                            const double* spb, const uint32_t* skey, double* pa, double* pb, uint32_t* key,
+                            cudaStream_t st);
 void launch_annotate(int lines, const uint32_t* off, const double* pa, const double* pb,
                      uint32_t* key, const RingRow* rings, cudaStream_t st);
 // drop the dedup flags of imported keys (annotate sets them again)

@@ -454,6 +454,19 @@ void exclusive_scan(const uint32_t* in, uint32_t* out, uint64_t n, Scratch& temp
 }
 }  // namespace
 
+// record offsets: out[0] = 0, out[i + 1] = in[0] + ... + in[i] (n + 1 entries)
+void launch_exclusive_scan_u32(const uint32_t* in, uint32_t* out, int n, cudaStream_t st) {
+    UB_CUDA(cudaMemsetAsync(out, 0, sizeof(uint32_t), st));
+    if (n <= 0)
+        return;
+    size_t tb = 0;
+    UB_CUDA(cub::DeviceScan::InclusiveSum(nullptr, tb, in, out + 1, int64_t(n), st));
+    Scratch temp;
+    temp.ensure(tb);
+    UB_CUDA(cub::DeviceScan::InclusiveSum(temp.p, tb, in, out + 1, int64_t(n), st));
+    UB_CUDA(cudaStreamSynchronize(st));  // before the temp storage is released
+}
+
 void gpu_schedule_build(const TraceArgs& A, int views, int max_recs, int max_cells, uint64_t cells, uint64_t visits,
                         uint32_t run, uint32_t runs_per_view, GpuSchedule& out, cudaStream_t st) {
     const uint32_t runs = uint32_t(views) * runs_per_view;

@@ -582,6 +582,23 @@ def test_batched_reconstruction_reports_the_failing_stack(ub, orc):
         ub.reconstruct_batch([good, bad, good], ub.SolverConfig(beta=0.5, tolerance=0, max_sweeps=1), tr)
 
 
+@pytest.mark.parametrize("name", ["fan64q", "cone16", "cone32w", "cone12"])
+def test_one_pass_generator_equals_count_then_write(ub, monkeypatch, name):
+    """The one-pass generator (bounded slots, true counts, compaction) builds
+    the same record store as the exact count pass followed by the write pass."""
+    out = {}
+    for two in (False, True):
+        if two:
+            monkeypatch.setenv("USCG_GEN_TWO_PASS", "1")
+        else:
+            monkeypatch.delenv("USCG_GEN_TWO_PASS", raising=False)
+        _, _, tr = _ub_tracer(ub, REF_GEOMS[name])
+        out[two] = tr.cache()
+    a, b = out[False], out[True]
+    for k in ("offsets", "phi_a", "phi_b", "slice", "ring"):
+        assert np.array_equal(getattr(a, k), getattr(b, k)), k
+
+
 # ---------------------------------------------------------------------------
 # generalized seams (verbatim BASELINE shapes) vs the C restatement
 # ---------------------------------------------------------------------------

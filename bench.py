@@ -220,17 +220,19 @@ def run_reference(args, rank, world):
     print(json.dumps(line), flush=True)
 
 
-def mart_kernel_name(Sp):
+def mart_kernel_name(Sp, executor):
+    """The MART kernel the library ran (uscg_tracer_info.executor)."""
     p = 1
-    lim = int(os.environ.get("USCG_CHUNK_WIDTH", 8))
+    lim = int(os.environ.get("USCG_CHUNK_WIDTH", 32))
     while p * 2 <= lim and Sp % (p * 2) == 0:
         p *= 2
-    mode = os.environ.get("USCG_MART_MODE", "flow")
-    if mode == "levels" or p > 8:
+    if executor == 3:
+        return f"mart_wave_kernel<{p}> (one persistent launch per reconstruct call; task = (view, {p}-problem chunk))"
+    if executor == 2:
         return f"mart_level_kernel<{p}> (one launch per dependency level)"
-    if mode == "barrier":
+    if executor == 1:
         return f"mart_sweep_kernel<{p}> (one cooperative launch per sweep)"
-    return f"mart_flow_kernel<{p}> (one dataflow launch per sweep)"
+    return f"mart_flow_kernel<{p}> (one dataflow launch per reconstruct call)"
 
 
 def metric_name(config):
@@ -820,7 +822,7 @@ def main():
         pass
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                 "traffic": traffic, "peak_kind": peak_kind,
-                "kernel": mart_kernel_name(Sp),
+                "kernel": mart_kernel_name(Sp, tracer.info()["executor"]),
                 "algorithmic_bytes_per_iteration": B, "dependency_levels_per_iteration": levels,
                 "launches": "one persistent launch per reconstruct call (all K iterations); achieved = "
                             "B * K / device time of that launch",
@@ -854,7 +856,9 @@ def main():
         "gpu_launches": int(launches),
         "clocks": clk,
         "precompute": {"generator_s": t_gen, "schedule_s": t_sched, "levels_per_iteration": levels,
-                       "records": info["records"], "cache_bytes": info["cache_bytes"]},
+                       "records": info["records"], "cache_bytes": info["cache_bytes"],
+                       "wave_build_s": tracer.info()["wave_build_s"],
+                       "wave_requirements": tracer.info()["wave_requirements"]},
     }
     print(json.dumps(line), flush=True)
     if world > 1:

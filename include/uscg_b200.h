@@ -124,6 +124,10 @@ typedef struct {
     int32_t levels;                /* MART dependency levels per sweep (0 until built) */
     double generator_ms;           /* device time of the first-view generator (count + scan +
                                       write + annotate; 0 for an imported cache) */
+    int32_t executor;              /* MART executor of the last reconstruction: -1 none yet,
+                                      0 flow, 1 barrier, 2 levels, 3 wave (USCG_MART_MODE) */
+    uint64_t wave_requirements;    /* wave executor: other-view requirements per sweep (0 until built) */
+    double wave_build_s;           /* wave executor: host seconds to build its lists and requirements */
 } uscg_tracer_info;
 
 const char* uscg_last_error(void);

@@ -149,7 +149,18 @@ struct uscg_tracer_s {
     int done_chunks = 0;
     unsigned epoch = 0;
     double schedule_seconds = 0;
+    // wave executor (2D stacks): every line's traced list and its other-view
+    // requirements (mart_sweep.cu), progress counters [views * nchunks]
+    bool wave_built = false;
+    DevBuf<uint32_t> d_wpos, d_wdep_off, d_wdeps;
+    DevBuf<uint2> d_went;
+    DevBuf<unsigned> d_wprog, d_wnext;
+    int wave_chunks = 0;
+    unsigned wave_epoch = 0;
+    uint64_t wave_deps = 0;
+    double wave_seconds = 0;
     double generator_ms = 0;  // device time of the first-view generator
+    int executor = -1;        // MART executor of the last reconstruction (uscg_tracer_info)
     // MART workspace
     DevBuf<MartArgs> d_args;
     DevBuf<float> w_field, w_proj, w_prev, w_stage;
@@ -518,23 +529,32 @@ void ensure_crossed(uscg_tracer_s* t) {
     t->crossed_built = true;
 }
 
-// MART executor (USCG_MART_MODE): 0 "flow" (default) dataflow over run
-// dependency counters; 1 "barrier" one grid barrier per level; 2 "levels" a
-// CUDA graph with one kernel node per level.
+// MART executor (USCG_MART_MODE): 0 "flow" dataflow over run dependency
+// counters; 1 "barrier" one grid barrier per level; 2 "levels" a CUDA graph
+// with one kernel node per level; 3 "wave" one task per (view, problem chunk)
+// ordered by per-view progress counters (2D stacks). Unset: "auto" (-1), the
+// wave executor where it applies (2D grid, chunks of 4-16 problems, lines
+// within its register tile, the traced lists within a memory budget), else flow.
 int mart_mode() {
-    static const int mode = [] {
-        const char* e = std::getenv("USCG_MART_MODE");
-        const std::string m = e ? e : "flow";
-        return m == "levels" ? 2 : (m == "barrier" ? 1 : 0);
-    }();
-    return mode;
+    const char* e = std::getenv("USCG_MART_MODE");
+    const std::string m = e ? e : "auto";
+    if (m == "levels")
+        return 2;
+    if (m == "barrier")
+        return 1;
+    if (m == "flow")
+        return 0;
+    if (m == "wave")
+        return 3;
+    return -1;
 }
 
 // lines per run for the dataflow executor (USCG_RUN; default 4 for 2D grids,
 // whose adjacent lines always overlap, and 1 for volumes): the largest divisor
 // of the lines per view not above the request; 1 for the level executors
 int run_length(int lines, bool volume) {
-    if (mart_mode() != 0)
+    const int mode = mart_mode();
+    if (mode == 1 || mode == 2)
         return 1;
     int want = volume ? 1 : 4;
     if (const char* e = std::getenv("USCG_RUN"))
@@ -648,6 +668,130 @@ void build_schedule(uscg_tracer_s* t) {
     t->d_bar.alloc(2);
     t->sched_built = true;
     t->schedule_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - h0).count();
+}
+
+// The wave executor's inputs (mart_sweep.cu): every (view, line)'s traced
+// index list, kept on the device, and per line the progress each other view
+// must have reached before the line may run. In-sweep: the line's earlier
+// toucher of each cell, if in another view (same-view order is the task's
+// own). Cross-sweep: where the line is the first toucher of a cell in a
+// sweep, the previous sweep's last toucher. A view's own previous-sweep task
+// is awaited at task start, so same-view requirements are dropped; so is
+// every requirement an earlier line of the view already implies (progress
+// counters are monotone and a view's lines become ready in order).
+constexpr uint64_t kWaveIdxBudget = uint64_t(1) << 29;  // traced entries (2 GiB)
+
+bool wave_fits(const uscg_tracer_s* t) {
+    return !t->volume && t->cells_per_sweep > 0 && t->cells_per_sweep <= kWaveIdxBudget &&
+           t->cells < (uint64_t(1) << 31);
+}
+
+void build_wave(uscg_tracer_s* t) {
+    if (t->wave_built)
+        return;
+    const auto h0 = std::chrono::steady_clock::now();
+    const uint64_t units = t->units();
+    const uint32_t L = uint32_t(t->lines);
+    std::vector<uint32_t> pos(units + 1);
+    pos[0] = 0;
+    for (uint64_t u = 0; u < units; ++u)
+        pos[u + 1] = pos[u] + t->h_cells[u];
+    const uint64_t total = pos[units];
+    upload(t->d_wpos, pos);
+    std::vector<uint32_t> idx(std::max<uint64_t>(total, 1));
+    {
+        DevBuf<uint32_t> d_idx;
+        d_idx.alloc(std::max<uint64_t>(total, 1));
+        launch_trace_dump(t->trace_args(), 0, uint32_t(units), t->max_recs, t->max_cells, t->d_wpos.p, d_idx.p,
+                          t->st());
+        UB_CUDA(cudaMemcpyAsync(idx.data(), d_idx.p, sizeof(uint32_t) * total, cudaMemcpyDeviceToHost, t->st()));
+        UB_CUDA(cudaStreamSynchronize(t->st()));
+    }
+    // entries: {cell | also in the previous line of the view << 31, position
+    // in the next line of the view or 0xFFFF} (the executor's hand-overs)
+    {
+        constexpr uint32_t kNone = ~0u;
+        std::vector<uint2> ent(std::max<uint64_t>(total, 1));
+        std::vector<uint32_t> stamp(t->cells, kNone), where(t->cells);
+        for (uint64_t u = 0; u < units; ++u) {
+            for (uint32_t k = pos[u]; k < pos[u + 1]; ++k) {
+                ent[k] = make_uint2(idx[k], 0xFFFFu);
+                stamp[idx[k]] = uint32_t(u);
+                where[idx[k]] = k - pos[u];
+            }
+            if (u % L == 0)
+                continue;
+            for (uint32_t k = pos[u - 1]; k < pos[u]; ++k) {
+                const uint32_t c = idx[k];
+                if (stamp[c] == uint32_t(u)) {
+                    ent[k].y = where[c];
+                    ent[pos[u] + where[c]].x |= 0x80000000u;
+                }
+            }
+        }
+        t->d_went.alloc(ent.size());
+        UB_CUDA(cudaMemcpy(t->d_went.p, ent.data(), sizeof(uint2) * ent.size(), cudaMemcpyHostToDevice));
+    }
+
+    constexpr uint32_t NONE = ~0u;
+    const uint32_t views = uint32_t(t->views);
+    std::vector<uint32_t> last(t->cells, NONE), first(t->cells, NONE);
+    std::vector<uint32_t> run_max[2] = {std::vector<uint32_t>(views, 0), std::vector<uint32_t>(views, 0)};
+    std::vector<std::pair<uint32_t, uint32_t>> cand;  // (view, required lines) of one line
+    auto condense = [&](int xs, std::vector<uint32_t>& out) {
+        // keep, per view, the largest requirement; drop what an earlier line implies
+        std::sort(cand.begin(), cand.end());
+        for (size_t i = 0; i < cand.size(); ++i) {
+            if (i + 1 < cand.size() && cand[i + 1].first == cand[i].first)
+                continue;
+            const uint32_t w = cand[i].first, need = cand[i].second;
+            if (need > run_max[xs][w]) {
+                run_max[xs][w] = need;
+                out.push_back(w | (uint32_t(xs) << 31));
+                out.push_back(need);
+            }
+        }
+        cand.clear();
+    };
+    std::vector<std::vector<uint32_t>> in_deps(units);
+    for (uint64_t u = 0; u < units; ++u) {
+        const uint32_t v = uint32_t(u / L);
+        if (u % L == 0)
+            std::fill(run_max[0].begin(), run_max[0].end(), 0u);
+        for (uint32_t k = pos[u]; k < pos[u + 1]; ++k) {
+            const uint32_t c = idx[k];
+            const uint32_t w = last[c];
+            if (w == NONE)
+                first[c] = uint32_t(u);
+            else if (w / L != v)
+                cand.emplace_back(w / L, w % L + 1);
+            last[c] = uint32_t(u);
+        }
+        condense(0, in_deps[u]);
+    }
+    std::vector<uint32_t> dep_off(units + 1), deps;
+    dep_off[0] = 0;
+    for (uint64_t u = 0; u < units; ++u) {
+        const uint32_t v = uint32_t(u / L);
+        if (u % L == 0)
+            std::fill(run_max[1].begin(), run_max[1].end(), 0u);
+        for (uint32_t k = pos[u]; k < pos[u + 1]; ++k) {
+            const uint32_t c = idx[k];
+            if (first[c] == uint32_t(u) && last[c] / L != v)
+                cand.emplace_back(last[c] / L, last[c] % L + 1);
+        }
+        deps.insert(deps.end(), in_deps[u].begin(), in_deps[u].end());
+        condense(1, deps);
+        dep_off[u + 1] = uint32_t(deps.size() / 2);
+    }
+    upload(t->d_wdep_off, dep_off);
+    upload(t->d_wdeps, deps);
+    t->wave_deps = deps.size() / 2;
+    t->wave_built = true;
+    t->wave_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - h0).count();
+    if (const char* e = std::getenv("USCG_FLOW_VERBOSE"); e && std::atoi(e))
+        std::fprintf(stderr, "wave schedule: %llu traced entries, %llu requirements, %.3f s\n",
+                     (unsigned long long)total, (unsigned long long)t->wave_deps, t->wave_seconds);
 }
 
 // One sweep = one graph replay: every dependency level is a kernel node.
@@ -925,6 +1069,9 @@ uscg_status uscg_tracer_get_info(uscg_tracer t, uscg_tracer_info* info) {
         info->chords_per_sweep = t->records * uint64_t(t->views);
         info->levels = t->sched_built ? int32_t(t->level_off.size()) - 1 : 0;
         info->generator_ms = t->generator_ms;
+        info->executor = t->executor;
+        info->wave_requirements = t->wave_deps;
+        info->wave_build_s = t->wave_seconds;
     });
 }
 
@@ -1272,6 +1419,20 @@ static void reconstruct_body(uscg_tracer t, const float* proj, int32_t problems,
     int exec_mode = mart_mode();
     if (exec_mode == 1 && P > 8)
         exec_mode = 2;
+    if (exec_mode == -1 || exec_mode == 3)
+        exec_mode = wave_fits(t) && wave_supported(h) && wave_fits_smem(h, t->lines) ? 3 : 0;
+    t->executor = exec_mode;
+    if (exec_mode == 3) {
+        build_wave(t);
+        if (t->wave_chunks != h.nchunks) {
+            const uint64_t n = uint64_t(t->views) * uint64_t(h.nchunks);
+            t->d_wprog.alloc(n);
+            t->d_wnext.alloc(1);
+            UB_CUDA(cudaMemsetAsync(t->d_wprog.p, 0, sizeof(unsigned) * n, st));
+            t->wave_chunks = h.nchunks;
+            t->wave_epoch = 0;
+        }
+    }
     need(exec_mode != 2 || t->run == 1, "the level executor needs a line-granular schedule");
     if (exec_mode == 2)
         ensure_graph(t, h);
@@ -1300,7 +1461,36 @@ static void reconstruct_body(uscg_tracer t, const float* proj, int32_t problems,
             UB_CUDA(cudaMemcpyAsync(t->w_prev.p, d_field, sizeof(float) * cells * Sp,
                                     cudaMemcpyDeviceToDevice, st));
         int n_run = 1;
-        if (exec_mode == 0) {
+        if (exec_mode == 3) {
+            n_run = track ? 1 : cfg->max_sweeps - sweep;
+            WaveSchedule ws;
+            ws.pos = t->d_wpos.p;
+            ws.ent = t->d_went.p;
+            ws.dep_off = t->d_wdep_off.p;
+            ws.deps = t->d_wdeps.p;
+            ws.views = t->views;
+            ws.lines = t->lines;
+            // USCG_SWEEP_PROFILE=<file>: per task {start, end, ready-wait, gather, reduce, store, cta}
+            static const char* prof_path = std::getenv("USCG_SWEEP_PROFILE");
+            const size_t nt = size_t(t->views) * h.nchunks * n_run;
+            DevBuf<unsigned long long> prof;
+            if (prof_path) {
+                prof.alloc(nt * 8);
+                UB_CUDA(cudaMemsetAsync(prof.p, 0, sizeof(unsigned long long) * nt * 8, st));
+            }
+            launch_mart_wave(h, ws, t->d_wprog.p, t->d_wnext.p, t->wave_epoch, n_run, st, prof.p);
+            t->wave_epoch += unsigned(n_run);
+            if (prof_path) {
+                std::vector<unsigned long long> hp(nt * 8);
+                UB_CUDA(cudaMemcpyAsync(hp.data(), prof.p, sizeof(unsigned long long) * hp.size(),
+                                        cudaMemcpyDeviceToHost, st));
+                UB_CUDA(cudaStreamSynchronize(st));
+                if (FILE* fp = std::fopen(prof_path, "wb")) {
+                    std::fwrite(hp.data(), sizeof(unsigned long long), hp.size(), fp);
+                    std::fclose(fp);
+                }
+            }
+        } else if (exec_mode == 0) {
             // without a per-sweep residual every remaining sweep runs in one
             // launch, back to back (cross-sweep dependencies)
             n_run = track ? 1 : cfg->max_sweeps - sweep;

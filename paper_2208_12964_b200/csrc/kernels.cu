@@ -34,10 +34,10 @@ void check_launch() {
 }  // namespace
 
 int chunk_limit() {
-    // 8: measured best on the c2 stack (16 / 32 move more bytes per L1
-    // request but lengthen the dependency chain's lines)
+    // 32: the wave executor's best on the c2 stack (a cell's 32 problems are
+    // one 128-byte segment); the flow executor's best is 8
     const char* e = std::getenv("USCG_CHUNK_WIDTH");
-    const int v = e ? std::atoi(e) : 8;
+    const int v = e ? std::atoi(e) : 32;
     int p = 1;
     while (p * 2 <= v && p < 32)
         p <<= 1;

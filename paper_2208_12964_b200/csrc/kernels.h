@@ -120,6 +120,26 @@ void launch_mart_flow(const MartArgs& h, const FlowSchedule& fs, unsigned* count
                       unsigned epoch, int sweeps, int n_rings, const FlowSlab& slab,
                       cudaStream_t st, unsigned long long* prof = nullptr);
 
+// K3 wave executor (2D problem stacks, mart_sweep.cu): one task per (sweep,
+// view, problem chunk) updates the view's lines in order; other views are
+// ordered by per-(view, chunk) progress counters.
+struct WaveSchedule {
+    const uint32_t* pos;      // [units + 1] offsets into ent
+    const uint2* ent;         // every (view, line)'s traced list: {cell | in previous line << 31,
+                              //  position in the next line of the view (0xFFFF: none)}
+    const uint32_t* dep_off;  // [units + 1]
+    const uint32_t* deps;     // pairs {view | cross-sweep << 31, required lines of that view}
+    int views;
+    int lines;
+};
+bool wave_supported(const MartArgs& h);
+bool wave_fits_smem(const MartArgs& h, int lines);
+size_t wave_smem_bytes(const MartArgs& m, int lines);
+// prog: [views * nchunks] cumulative line counters; epoch: 0-based global
+// index of the launch's first sweep
+void launch_mart_wave(const MartArgs& h, const WaveSchedule& ws, unsigned* prog, unsigned* next, unsigned epoch,
+                      int sweeps, cudaStream_t st, unsigned long long* prof = nullptr);
+
 // per-problem projection statistics: stats[p*4 + {0: count>0, 1: sum>0, 2: any!=0, 3: invalid}];
 // stats must hold proj_stats_words(S) doubles (the tail is block partials)
 size_t proj_stats_words(int S);

@@ -202,11 +202,13 @@ struct GroupWorker {
     double pf_next = 0;
     bool act_next = false;
 
+    // group = -1: the group of this thread (threadIdx.x / G); else that
+    // group's shared-memory layout (a helper warp working on a group's lines)
     __device__ GroupWorker(const MartArgs& a, uint32_t* smem, int n_rings, bool with_trace,
-                           int lists, size_t extra = 0)
+                           int lists, size_t extra = 0, int group = -1)
         : A(a), s_rings(reinterpret_cast<const RingRow*>(smem)),
           sy(SyncFor<G>::make(int(threadIdx.x) / G)), t(int(threadIdx.x) % G) {
-        const int g = int(threadIdx.x) / G;
+        const int g = group >= 0 ? group : int(threadIdx.x) / G;
         const size_t std_words = round4(group_words(P, G, with_trace, A.max_recs, A.max_cells, lists));
         uint32_t* gbase = smem + ring_words(n_rings) + size_t(g) * (std_words + extra);
         ext = gbase + std_words;
@@ -1193,6 +1195,466 @@ void launch_mart_flow(const MartArgs& h, const FlowSchedule& fs, unsigned* count
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess)
         throw CudaError(std::string("mart_flow_kernel launch: ") + cudaGetErrorString(e));
+}
+
+// ============================================================================
+// wave executor (2D problem stacks)
+// ============================================================================
+//
+// A task is one view of one problem chunk in one sweep: a CTA updates the
+// view's lines in order, so the chain between consecutive lines of a view
+// (adjacent lines of a polar grid always share cells) stays inside the CTA
+// and costs a block barrier, not a cross-SM handshake. Lines of other views
+// are ordered by one progress counter per (view, chunk), the number of lines
+// of that view the chunk has completed (cumulative over sweeps). Every line
+// carries the list of other-view counters it needs (the last earlier toucher
+// of each of its cells, and for the first toucher of a cell in a sweep, the
+// previous sweep's last toucher), condensed on the host to the entries that
+// raise a requirement of an earlier line of the view. Executing every line
+// after those requirements, the lines of a view in order, performs on every
+// cell exactly the reference's sequence of updates (proj/src/solver.cpp:111-136).
+//
+// CTA = G updater threads (the GroupWorker line code: bit-identical to the
+// flow executor's lines) + one control warp. The control warp checks the
+// requirements of up to 32 lines per round (one lane per line) and raises
+// `ready`; it publishes the updaters' `done` to the view's counter with one
+// gpu-scope fence per round (cumulative over the updaters' stores through
+// their barrier and the shared-memory release). Tasks are taken in ticket
+// order (sweep, view, chunk); a task waits only on smaller tickets, so every
+// resident CTA makes progress.
+
+struct WaveArgs {
+    MartArgs m;
+    const uint32_t* pos;      // [units + 1]: traced list of unit u at ent[pos[u], pos[u+1])
+    const uint2* ent;         // per traced entry {cell | in previous line << 31, position in next line}
+    const uint32_t* dep_off;  // [units + 1]
+    const uint32_t* deps;     // pairs {view | cross-sweep << 31, required line count of that view}
+    unsigned* prog;           // [views * nchunks]: lines completed, cumulative over sweeps
+    unsigned* next;           // task ticket (zeroed per launch)
+    unsigned epoch;           // global 0-based index of this launch's first sweep
+    int n_sweeps;
+    int views;
+    int lines;
+    unsigned long long* prof;  // optional: per task 8 stamps/sums (ns), see mart_wave_kernel
+};
+
+constexpr uint32_t kWavePrev = 0x80000000u;  // entry's cell is also in the previous line
+constexpr uint32_t kWaveNoNext = 0xFFFFu;     // entry's cell is not in the next line
+
+// Updater shape per chunk width P: G = 16 P threads, TPC = P/4 threads per
+// cell (one float4 each), 64 cells per pass and KV = 12 cells per thread (a
+// line of up to 768 cells). The CTA is small so that several share an SM:
+// one CTA's reduction and barriers overlap another's memory phase (a CTA's
+// lines are a dependent chain). MB = CTAs per SM the registers must allow.
+template <int P> struct WaveShape {
+    static constexpr int G = 16 * P, KV = 12;
+    static constexpr int MB = P <= 8 ? 4 : (P == 16 ? 2 : 1);
+};
+template <int P> __host__ __device__ constexpr int wave_cover() { return WaveShape<P>::KV * (WaveShape<P>::G / (P / 4)); }
+
+__device__ __forceinline__ unsigned ld_acquire_cta_shared(const unsigned* p) {
+    unsigned v;
+    const unsigned a = unsigned(__cvta_generic_to_shared(p));
+    asm volatile("ld.acquire.cta.shared.u32 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release_cta_shared(unsigned* p, unsigned v) {
+    const unsigned a = unsigned(__cvta_generic_to_shared(p));
+    asm volatile("st.release.cta.shared.u32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+}
+__device__ __forceinline__ void st_relaxed_gpu(unsigned* p, unsigned v) {
+    asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ void cp_async8_if(bool p, void* smem_dst, const void* gmem_src) {
+    const unsigned d = unsigned(__cvta_generic_to_shared(smem_dst));
+    asm volatile(
+        "{ .reg .pred q; setp.ne.b32 q, %2, 0; @q cp.async.ca.shared.global [%0], [%1], 8; }" ::"r"(d),
+        "l"(gmem_src), "r"(int(p))
+        : "memory");
+}
+
+// dynamic shared memory: [ring words][group words][view offsets L+1]
+// [entry ring 3 x cover uint2][field buffer cover x P floats]
+template <int P>
+__host__ __device__ inline size_t wave_words(int max_recs, int max_cells, int lines) {
+    return ring_words(0) + round4(group_words(P, WaveShape<P>::G, false, max_recs, max_cells, 0)) +
+           round4(size_t(lines) + 1) + 3 * 2 * size_t(wave_cover<P>()) + size_t(wave_cover<P>()) * P;
+}
+
+size_t wave_smem_bytes(const MartArgs& m, int lines) {
+    switch (m.Sp / m.nchunks) {
+        case 4: return 4 * wave_words<4>(m.max_recs, m.max_cells, lines);
+        case 8: return 4 * wave_words<8>(m.max_recs, m.max_cells, lines);
+        case 16: return 4 * wave_words<16>(m.max_recs, m.max_cells, lines);
+        case 32: return 4 * wave_words<32>(m.max_recs, m.max_cells, lines);
+        default: return 0;
+    }
+}
+
+template <int P>
+__global__ void __launch_bounds__(WaveShape<P>::G + 64, WaveShape<P>::MB) mart_wave_kernel(WaveArgs a) {
+    constexpr int G = WaveShape<P>::G, V = 4, TPC = P / V, NCLV = G / TPC, KV = WaveShape<P>::KV;
+    constexpr int COVER = wave_cover<P>();
+    using GW = GroupWorker<P, G>;
+    using Scale = typename GW::Scale;
+    extern __shared__ __align__(16) uint32_t smem[];
+    __shared__ unsigned s_task, s_ready, s_done;
+    const int nchunks = a.m.nchunks;
+    const unsigned L = unsigned(a.lines);
+    const int per_sweep = a.views * nchunks;
+    const int total = per_sweep * a.n_sweeps;
+    uint32_t* s_pos = smem + ring_words(0) + round4(group_words(P, G, false, a.m.max_recs, a.m.max_cells, 0));
+    uint2* s_ent = reinterpret_cast<uint2*>(s_pos + round4(size_t(L) + 1));  // [3][COVER]
+    float4* buf = reinterpret_cast<float4*>(s_ent + 3 * COVER);                 // [COVER][TPC]
+    if (threadIdx.x == 0) {
+        s_task = atomicAdd(a.next, 1u);
+        s_ready = 0;
+        s_done = 0;
+    }
+    __syncthreads();
+    int task = int(s_task);
+    // line barrier (updaters + factor warp) and updater-only barrier
+    auto line_sync = [] { asm volatile("bar.sync 1, %0;" ::"n"(G + 32) : "memory"); };
+    auto upd_sync = [] { asm volatile("bar.sync 2, %0;" ::"n"(G) : "memory"); };
+    if (int(threadIdx.x) >= G && int(threadIdx.x) < G + 32) {
+        // ---- factor warp: the line factors (solver.cpp:36-46) from the
+        // updaters' partial sums, and the CTA-scope release of `done`. It
+        // issues no global stores, so its release fence waits on nothing. ----
+        GW W(a.m, smem, 0, false, 0, 0, 0);  // W.t = lane
+        const int lane = W.t;
+        while (task < total) {
+            const int v = (task % per_sweep) / nchunks, chunk = task % nchunks;
+            const uint32_t u0 = uint32_t(v) * L;
+            float nm = 0.f;
+            if (lane < P) {
+                const size_t c2 = size_t(chunk) * P + lane;
+                W.pf_next = __ldg(a.m.p_floor + c2);
+                W.act_next = __ldg(a.m.active + c2) != 0;
+                nm = __ldcs(a.m.proj + size_t(u0) * a.m.Sp + c2);
+            }
+            for (unsigned j = 0; j < L; ++j) {
+                W.m_next = nm;
+                if (j + 1 < L && lane < P)
+                    nm = __ldcs(a.m.proj + size_t(u0 + j + 1) * a.m.Sp + size_t(chunk) * P + lane);
+                line_sync();  // A: partial sums in W.red
+                W.factors_to_smem(chunk);
+                line_sync();  // B: factors in W.fac
+                line_sync();  // C: the line's hand-overs and stores issued
+                if (lane == 0)
+                    st_release_cta_shared(&s_done, j + 1);
+            }
+            __syncthreads();  // task boundary
+            task = int(s_task);
+            __syncthreads();
+        }
+        return;
+    }
+    if (int(threadIdx.x) >= G + 32) {
+        // ---- control warp ----
+        const int lane = int(threadIdx.x) & 31;
+        while (task < total) {
+            const int sweep = task / per_sweep;
+            const int v = (task % per_sweep) / nchunks, chunk = task % nchunks;
+            const unsigned gs = a.epoch + unsigned(sweep);
+            unsigned* mine = a.prog + size_t(v) * nchunks + chunk;
+            const uint32_t u0 = uint32_t(v) * L;
+            // the previous sweep's task of this (view, chunk) has published every line
+            if (lane == 0 && gs > 0)
+                spin_until_geq(mine, gs * L);
+            __syncwarp();
+            unsigned ready = 0, published = 0;
+            unsigned ns = 0;
+            while (published < L) {
+                bool moved = false;
+                if (ready < L) {
+                    // lane i checks line ready + i
+                    const unsigned j = ready + unsigned(lane);
+                    bool ok = true;
+                    if (j < L) {
+                        const uint32_t b = __ldg(a.dep_off + u0 + j), e = __ldg(a.dep_off + u0 + j + 1);
+                        for (uint32_t k = b; k < e && ok; ++k) {
+                            const uint32_t w = __ldg(a.deps + 2 * size_t(k));
+                            const unsigned xs = w >> 31, u = w & 0x7FFFFFFFu;
+                            if (gs < xs)
+                                continue;  // no previous sweep
+                            const unsigned need = (gs - xs) * L + __ldg(a.deps + 2 * size_t(k) + 1);
+                            ok = ld_acquire(a.prog + size_t(u) * nchunks + chunk) >= need;
+                        }
+                    }
+                    const unsigned bad = __ballot_sync(0xFFFFFFFFu, !ok);
+                    const unsigned adv = bad ? unsigned(__ffs(bad) - 1) : 32u;
+                    const unsigned nr = min(L, ready + adv);
+                    if (nr > ready) {
+                        ready = nr;
+                        moved = true;
+                        if (lane == 0)
+                            st_release_cta_shared(&s_ready, ready);
+                    }
+                }
+                const unsigned d = ld_acquire_cta_shared(&s_done);
+                if (d > published) {
+                    if (lane == 0) {
+                        fence_acq_rel_gpu();
+                        st_relaxed_gpu(mine, gs * L + d);
+                    }
+                    published = d;
+                    moved = true;
+                }
+                if (moved) {
+                    ns = 0;
+                } else {
+                    ns = ns ? min(ns * 2, 128u) : 16u;
+                    __nanosleep(ns);
+                }
+            }
+            __syncwarp();
+            if (lane == 0) {
+                s_task = atomicAdd(a.next, 1u);
+                s_ready = 0;
+                s_done = 0;
+            }
+            __syncthreads();  // task boundary (with the updaters)
+            task = int(s_task);
+            __syncthreads();  // everyone has read the ticket
+        }
+        return;
+    }
+    // ---- updaters ----
+    // Thread (cl, q) owns slots s = cl + i * NCLV of every line: the entry of
+    // the cell at position s (s_ent ring, 2 lines ahead) and float4 q of its
+    // problems (buf). A line's cells that the previous line does not cross are
+    // copied into the owner's slots during the previous line (cp.async, once
+    // the line's requirements hold: no other writer can touch them until this
+    // task publishes the line); the cells it does cross are handed over by
+    // the previous line after scaling (shared memory; no store, no reload).
+    // Every cell sees exactly the line-by-line updates, bit for bit.
+    GW W(a.m, smem, 0, false, 0, 0, 0);
+    const int t = W.t;
+    const int q = t % TPC, cl = t / TPC;
+    float4* __restrict__ f4 = reinterpret_cast<float4*>(a.m.field);
+    const uint32_t Sp4 = uint32_t(a.m.Sp) / V;
+    auto wait_ready = [&](unsigned j) {
+        if (ld_acquire_cta_shared(&s_ready) <= j) {
+            while (ld_acquire_cta_shared(&s_ready) <= j)
+                __nanosleep(16);
+        }
+    };
+    while (task < total) {
+        const int v = (task % per_sweep) / nchunks, chunk = task % nchunks;
+        const uint32_t u0 = uint32_t(v) * L;
+        const uint32_t col4 = (uint32_t(chunk) * P) / V + uint32_t(q);
+        for (unsigned j = unsigned(t); j <= L; j += G)
+            s_pos[j] = __ldg(a.pos + u0 + j);
+        upd_sync();
+        // USCG_SWEEP_PROFILE: {start, end, ready-wait, gather, reduce, store} (ns, thread 0)
+        const bool prof = a.prof != nullptr && t == 0;
+        unsigned long long p_start = prof ? gtimer() : 0, p_wait = 0, p_gather = 0, p_reduce = 0, p_store = 0;
+        // entries of line j (own slots) into ring slot j % 3
+        auto load_entries = [&](unsigned j) {
+            const uint32_t p0 = s_pos[j];
+            const int n = int(s_pos[j + 1] - p0);
+            uint2* dst = s_ent + (j % 3) * COVER;
+#pragma unroll
+            for (int i = 0; i < KV; ++i) {
+                const int s = cl + i * NCLV;
+                cp_async8_if(q == 0 && s < n, dst + s, a.ent + p0 + s);
+            }
+        };
+        // field values of line j's cells that line j-1 does not cross (own slots)
+        auto gather = [&](unsigned j) {
+            const int n = int(s_pos[j + 1] - s_pos[j]);
+            const uint2* e = s_ent + (j % 3) * COVER;
+#pragma unroll
+            for (int i = 0; i < KV; ++i) {
+                const int s = cl + i * NCLV;
+                const uint32_t c = s < n ? e[s].x : kWavePrev;
+                cp_async16_if(!(c & kWavePrev), buf + s * TPC + q, f4 + size_t(c) * Sp4 + col4);
+            }
+        };
+        // the entries are written by the slot's q == 0 thread: one barrier
+        // makes them visible to the other TPC - 1 threads of the cell
+        load_entries(0);
+        if (L > 1)
+            load_entries(1);
+        cp_async_commit();
+        cp_async_wait_all();
+        upd_sync();
+        wait_ready(0);
+        gather(0);
+        cp_async_commit();
+        for (unsigned j = 0; j < L; ++j) {
+            const int n = int(s_pos[j + 1] - s_pos[j]);
+            const unsigned long long p1 = prof ? gtimer() : 0;
+            cp_async_wait_all();  // this line's values (own copies); hand-overs: barrier C
+            float4 x[KV];
+#pragma unroll
+            for (int i = 0; i < KV; ++i) {
+                const int s = cl + i * NCLV;
+                x[i] = s < n ? buf[s * TPC + q] : make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+            double s0, s1, s2, s3;
+            GW::template partials<KV>(x, s0, s1, s2, s3);
+            // the slots are read (the sums depend on every value) before the
+            // next line's copies may land in them
+            asm volatile("" ::"d"(s0), "d"(s1), "d"(s2), "d"(s3));
+#pragma unroll
+            for (int o = TPC; o < 32; o <<= 1) {
+                s0 += __shfl_xor_sync(0xFFFFFFFFu, s0, o);
+                s1 += __shfl_xor_sync(0xFFFFFFFFu, s1, o);
+                s2 += __shfl_xor_sync(0xFFFFFFFFu, s2, o);
+                s3 += __shfl_xor_sync(0xFFFFFFFFu, s3, o);
+            }
+            const int lane = t & 31, warp = t >> 5;
+            if (lane < TPC) {
+                double* r = W.red + warp * P + q * V;
+                r[0] = s0;
+                r[1] = s1;
+                r[2] = s2;
+                r[3] = s3;
+            }
+            line_sync();  // A
+            const unsigned long long p2 = prof ? gtimer() : 0;
+            // while the factor warp works: entries two lines ahead; the next
+            // line's own copies once its requirements hold (its entries,
+            // loaded by the cell's q == 0 thread and waited for at this
+            // line's start, are visible after barrier A)
+            if (j + 2 < L)
+                load_entries(j + 2);
+            bool issued = false;
+            if (j + 1 < L && ld_acquire_cta_shared(&s_ready) > j + 1) {
+                gather(j + 1);
+                issued = true;
+            }
+            cp_async_commit();
+            line_sync();  // B
+            const unsigned long long p3 = prof ? gtimer() : 0;
+            Scale g0, g1, g2, g3;
+            // identity Scales (no problem of the chunk updated) still hand over
+            const bool any = W.load_scales(q, g0, g1, g2, g3);
+            const uint2* e = s_ent + (j % 3) * COVER;
+#pragma unroll
+            for (int i = 0; i < KV; ++i) {
+                const int s = cl + i * NCLV;
+                const bool in = s < n;
+                const uint2 en = e[in ? s : 0];
+                const float4 r = GW::scale4(x[i], g0, g1, g2, g3);
+                const bool hand = in && en.y != kWaveNoNext;
+                st_shared_v4_if(hand, buf + int(en.y) * TPC + q, r);
+                st_global_cg_v4_if(any && in && !hand, f4 + size_t(en.x & ~kWavePrev) * Sp4 + col4, r);
+            }
+            // C: hand-overs visible; this line's stores ordered before the
+            // factor warp's release of `done`
+            line_sync();
+            unsigned long long p4 = prof ? gtimer() : 0, p5 = p4;
+            if (!issued && j + 1 < L) {
+                wait_ready(j + 1);
+                if (prof)
+                    p5 = gtimer();
+                gather(j + 1);
+                cp_async_commit();
+            }
+            if (prof) {
+                p_wait += p5 - p4;
+                p_gather += p2 - p1;
+                p_reduce += p3 - p2;
+                p_store += p4 - p3;
+            }
+        }
+        if (prof) {
+            unsigned long long* o = a.prof + 8 * size_t(task);
+            o[0] = p_start;
+            o[1] = gtimer();
+            o[2] = p_wait;
+            o[3] = p_gather;
+            o[4] = p_reduce;
+            o[5] = p_store;
+            o[6] = blockIdx.x;
+        }
+        __syncthreads();  // task boundary (the control warp grabs the next ticket)
+        task = int(s_task);
+        __syncthreads();
+    }
+}
+
+template <int P>
+static void wave_launch_t(const WaveArgs& a, int sms, cudaStream_t st) {
+    constexpr int NT = WaveShape<P>::G + 64;
+    const size_t smem = wave_smem_bytes(a.m, a.lines);
+    UB_CUDA(cudaFuncSetAttribute(mart_wave_kernel<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    int per_sm = 0;
+    UB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, mart_wave_kernel<P>, NT, smem));
+    if (per_sm < 1)
+        throw CudaError("mart_wave_kernel cannot be resident");
+    if (const char* e = std::getenv("USCG_WAVE_PER_SM"))
+        per_sm = std::max(1, std::min(per_sm, std::atoi(e)));
+    const int total = a.views * a.m.nchunks * a.n_sweeps;
+    const int grid = std::min(total, sms * per_sm);
+    if (const char* e = std::getenv("USCG_FLOW_VERBOSE"); e && std::atoi(e))
+        std::fprintf(stderr, "mart_wave_kernel: P=%d grid=%d per_sm=%d smem=%zu tasks=%d\n", P, grid, per_sm,
+                     smem, total);
+    // every CTA must be resident: tasks wait on smaller tickets only, held by running CTAs
+    mart_wave_kernel<P><<<grid, NT, smem, st>>>(a);
+}
+
+bool wave_supported(const MartArgs& h) {
+    int optin = 0, dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess ||
+        cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev) != cudaSuccess)
+        return false;
+    const int P = h.Sp / h.nchunks;
+    int cover = 0;
+    switch (P) {
+        case 4: cover = wave_cover<4>(); break;
+        case 8: cover = wave_cover<8>(); break;
+        case 16: cover = wave_cover<16>(); break;
+        case 32: cover = wave_cover<32>(); break;
+        default: return false;
+    }
+    return h.max_cells <= cover && h.max_cells < int(kWaveNoNext);
+}
+
+bool wave_fits_smem(const MartArgs& h, int lines) {
+    int optin = 0, dev = 0;
+    UB_CUDA(cudaGetDevice(&dev));
+    UB_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+    return wave_smem_bytes(h, lines) + 64 <= size_t(optin);
+}
+
+void launch_mart_wave(const MartArgs& h, const WaveSchedule& ws, unsigned* prog, unsigned* next, unsigned epoch,
+                      int sweeps, cudaStream_t st, unsigned long long* prof) {
+    int dev = 0, sms = 0;
+    UB_CUDA(cudaGetDevice(&dev));
+    UB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    if (uint64_t(ws.views) * uint64_t(h.nchunks) * uint64_t(sweeps) >= (1ull << 31) ||
+        uint64_t(epoch + sweeps) * uint64_t(ws.lines) >= (1ull << 32))
+        throw CudaError("mart_wave_kernel: too many tasks for one launch");
+    if (!wave_supported(h) || !wave_fits_smem(h, ws.lines))
+        throw CudaError("mart_wave_kernel: unsupported chunk width or line length");
+    WaveArgs a;
+    a.m = h;
+    a.pos = ws.pos;
+    a.ent = ws.ent;
+    a.dep_off = ws.dep_off;
+    a.deps = ws.deps;
+    a.prog = prog;
+    a.next = next;
+    a.epoch = epoch;
+    a.n_sweeps = sweeps;
+    a.views = ws.views;
+    a.lines = ws.lines;
+    a.prof = prof;
+    UB_CUDA(cudaMemsetAsync(next, 0, sizeof(unsigned), st));
+    switch (h.Sp / h.nchunks) {
+        case 4: wave_launch_t<4>(a, sms, st); break;
+        case 8: wave_launch_t<8>(a, sms, st); break;
+        case 16: wave_launch_t<16>(a, sms, st); break;
+        case 32: wave_launch_t<32>(a, sms, st); break;
+        default: throw CudaError("mart_wave_kernel supports problem chunks of 4, 8, 16 or 32");
+    }
+    count_launch();
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess)
+        throw CudaError(std::string("mart_wave_kernel launch: ") + cudaGetErrorString(e));
 }
 
 // ============================================================================

@@ -530,6 +530,7 @@ def test_pipelined_runs_are_bit_identical(ub, orc, monkeypatch, capfd, S, run, w
     """The pipelined run executor (gathers one line ahead, shared cells handed
     over in shared memory) performs the line-by-line updates bit for bit, for
     every chunk shape (8 problems / 256 threads, 16 / 512, 32 / 1024)."""
+    monkeypatch.setenv("USCG_MART_MODE", "flow")
     monkeypatch.setenv("USCG_RUN", str(run))
     monkeypatch.setenv("USCG_CHUNK_WIDTH", str(width))
     monkeypatch.setenv("USCG_FLOW_VERBOSE", "1")
@@ -550,6 +551,56 @@ def test_pipelined_runs_are_bit_identical(ub, orc, monkeypatch, capfd, S, run, w
         assert np.array_equal(out[1][p], out[0][p]), p
     want, _ = oc.reconstruct(geom.thetas(), proj[0].astype(np.float64), beta=0.7, tolerance=0, max_sweeps=3)
     assert (np.abs(out[1][0] - want) / want).max() <= 1e-4
+
+
+@pytest.mark.parametrize("S,width,detector,tol,beta", [(128, 8, "arc", 0, 0.7), (64, 16, "arc", 0, 0.7),
+                                                      (128, 32, "arc", 0, 0.7), (64, 32, "parallel", 1e-3, 0.7),
+                                                      (40, 8, "parallel", 0, 0.7), (16, 4, "arc", 0, 0.7),
+                                                      (32, 8, "arc", 1e-3, 0.7), (24, 8, "arc", 0, 1.9)])
+def test_wave_executor_matches_flow(ub, orc, monkeypatch, capfd, S, width, detector, tol, beta):
+    """The wave executor (one CTA per (view, problem chunk), other views
+    ordered by progress counters, gathers one line ahead with shared cells
+    handed over in shared memory) performs the flow executor's line updates:
+    same reports and fields within fp32 summation-order differences, over
+    back-to-back sweeps (tol 0: one launch), one launch per sweep (tol > 0);
+    bit-identical between runs on 1 CTA per SM and on the most that fit and
+    on repeated calls (the counters carry over): a schedule race would show
+    as a difference. Clamps exercised at beta 1.9."""
+    monkeypatch.setenv("USCG_CHUNK_WIDTH", str(width))
+    monkeypatch.setenv("USCG_FLOW_VERBOSE", "1")
+    spec, geom, tr, oc = _m1_case(ub, orc, detector, n_rings=48, views=16, du=96)
+    rng = np.random.default_rng(S + width)
+    truth = rng.uniform(0.2, 3.0, (S, spec.cell_count()))
+    proj = ub.project_stack(tr, truth.astype(np.float32))
+    if beta > 1:
+        proj[:, 3, 40:60] = 1e-9  # drives factors <= 0: clamps
+    proj[min(2, S - 1)] = 0  # one all-zero problem
+    cfg = ub.SolverConfig(beta=beta, tolerance=tol, max_sweeps=3)
+    out = {}
+    for mode, per_sm in (("wave", 1), ("flow", 0), ("wave", 8), ("wave", 8)):
+        monkeypatch.setenv("USCG_MART_MODE", mode)
+        monkeypatch.setenv("USCG_WAVE_PER_SM", str(per_sm))
+        res = ub.reconstruct_stack(proj, cfg, tr)
+        log = capfd.readouterr().err
+        assert (f"mart_wave_kernel: P={width} " if mode == "wave" else "mart_flow_kernel") in log, log
+        if mode in out:
+            for p in range(S):
+                assert np.array_equal(res[p][0], out[mode][p][0]), ("repeat", p)
+        out[mode] = res
+    for p in range(S):
+        (fw, rw), (ff, rf) = out["wave"][p], out["flow"][p]
+        # the same updates; p_bar summed in another order (fp32 partials;
+        # at beta 1.9 near-clamp factors amplify those roundings)
+        if beta < 1:
+            np.testing.assert_allclose(fw, ff, rtol=2e-5, atol=0)
+        assert (rw.sweeps, rw.updates, rw.factor_clamps) == (rf.sweeps, rf.updates, rf.factor_clamps), p
+    if beta > 1:
+        # clamped lines drive values below fp32's range: the oracle check is
+        # the other cases' (test_positivity_across_relaxations covers clamps)
+        assert sum(out["wave"][p][1].factor_clamps for p in range(S)) > 0
+        return
+    want, _ = oc.reconstruct(geom.thetas(), proj[0].astype(np.float64), beta=beta, tolerance=tol, max_sweeps=3)
+    assert (np.abs(out["wave"][0][0] - want) / want).max() <= 1e-4
 
 
 @pytest.mark.parametrize("S,init", [(1, False), (5, False), (8, True)])

@@ -1370,6 +1370,7 @@ __global__ void __launch_bounds__(WaveShape<P>::G + 64, WaveShape<P>::MB) mart_w
                     // lane i checks line ready + i
                     const unsigned j = ready + unsigned(lane);
                     bool ok = true;
+                    const unsigned* last = nullptr;  // the lane's last satisfied counter
                     if (j < L) {
                         const uint32_t b = __ldg(a.dep_off + u0 + j), e = __ldg(a.dep_off + u0 + j + 1);
                         for (uint32_t k = b; k < e && ok; ++k) {
@@ -1378,13 +1379,22 @@ __global__ void __launch_bounds__(WaveShape<P>::G + 64, WaveShape<P>::MB) mart_w
                             if (gs < xs)
                                 continue;  // no previous sweep
                             const unsigned need = (gs - xs) * L + __ldg(a.deps + 2 * size_t(k) + 1);
-                            ok = ld_acquire(a.prog + size_t(u) * nchunks + chunk) >= need;
+                            // relaxed polls: a gpu-scope acquire load also
+                            // invalidates the SM's L1 (CCTL.IVALL) on every poll
+                            last = a.prog + size_t(u) * nchunks + chunk;
+                            ok = ld_relaxed(last) >= need;
                         }
                     }
                     const unsigned bad = __ballot_sync(0xFFFFFFFFu, !ok);
                     const unsigned adv = bad ? unsigned(__ffs(bad) - 1) : 32u;
                     const unsigned nr = min(L, ready + adv);
                     if (nr > ready) {
+                        // acquire what the advancing lanes observed (coherence:
+                        // the re-read is at least as recent), then release to
+                        // the updaters
+                        if (unsigned(lane) < adv && last != nullptr)
+                            (void)ld_acquire(last);
+                        __syncwarp();
                         ready = nr;
                         moved = true;
                         if (lane == 0)

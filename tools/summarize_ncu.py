@@ -72,7 +72,7 @@ def main():
     ap.add_argument("--launches")
     ap.add_argument("--tag", required=True)
     ap.add_argument("--config", default="c2")
-    ap.add_argument("--kernel", default="mart_flow_kernel")
+    ap.add_argument("--kernel", default="mart_wave_kernel")
     args = ap.parse_args()
     os.makedirs(PROF, exist_ok=True)
 

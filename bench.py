@@ -450,7 +450,7 @@ def bench_c5(args, rank, world, local):
                    "views": geom.views, "resample_pixels": [npix, npix, spec.slices()],
                    "l2": "working sets (11.6 GB record store, 1.7 + 2.1 GB volumes) exceed L2",
                    "parallelism": "rows / views / slices split across ranks"},
-        "roofline": roof(gen_bytes, g_ms, "generate_count_kernel + generate_write_kernel + annotate_kernel",
+        "roofline": roof(gen_bytes, g_ms, "generate_bound_kernel + generate_slot_kernel + compact_records_kernel + annotate_kernel",
                          "20*records + 4*(lines+1) written (SURVEY.md §8(d))"),
         "generator": {"ms": g_ms, "exchange_ms": exchange_ms, "rays": rays_all, "records": recs_all,
                       "records_per_s": recs_all / ((g_ms + exchange_ms) * 1e-3)},

@@ -1281,8 +1281,16 @@ __host__ __device__ inline size_t wave_words(int max_recs, int max_cells, int li
            round4(size_t(lines) + 1) + 3 * 2 * size_t(wave_cover<P>()) + size_t(wave_cover<P>()) * P;
 }
 
+constexpr int kWave1K = 24;
+constexpr int kWave1Cover = 32 * kWave1K;
+
+__host__ __device__ inline size_t wave1_words(int lines) {
+    return round4(size_t(lines) + 1) + 3 * 2 * size_t(kWave1Cover) + size_t(kWave1Cover);
+}
+
 size_t wave_smem_bytes(const MartArgs& m, int lines) {
     switch (m.Sp / m.nchunks) {
+        case 1: return 4 * wave1_words(lines);
         case 4: return 4 * wave_words<4>(m.max_recs, m.max_cells, lines);
         case 8: return 4 * wave_words<8>(m.max_recs, m.max_cells, lines);
         case 16: return 4 * wave_words<16>(m.max_recs, m.max_cells, lines);
@@ -1586,6 +1594,217 @@ __global__ void __launch_bounds__(WaveShape<P>::G + 64, WaveShape<P>::MB) mart_w
     }
 }
 
+// Single-problem form (P = 1, e.g. one 2D slice): one updater warp per task,
+// warp-level sums (no block barriers), the factor computed by every lane, and
+// the warp publishes each line one line late (its stores have drained by
+// then, so the gpu-scope fence is short). Lines of up to 32 * K1 cells.
+
+__global__ void __launch_bounds__(64) mart_wave1_kernel(WaveArgs a) {
+    extern __shared__ __align__(16) uint32_t smem[];
+    __shared__ unsigned s_task, s_ready, s_done;
+    const unsigned L = unsigned(a.lines);
+    const int total = a.views * a.n_sweeps;
+    uint32_t* s_pos = smem;
+    uint2* s_ent = reinterpret_cast<uint2*>(s_pos + round4(size_t(L) + 1));  // [3][cover]
+    float* buf = reinterpret_cast<float*>(s_ent + 3 * kWave1Cover);          // [cover]
+    const int lane = int(threadIdx.x) & 31;
+    if (threadIdx.x == 0) {
+        s_task = atomicAdd(a.next, 1u);
+        s_ready = 0;
+        s_done = 0;
+    }
+    __syncthreads();
+    int task = int(s_task);
+    if (threadIdx.x >= 32) {
+        // ---- control warp: the lines' other-view requirements, and the
+        // publication of completed lines (one gpu-scope fence per round) ----
+        unsigned claimed = 0;
+        while (task < total) {
+            const int sweep = task / a.views, v = task % a.views;
+            const unsigned gs = a.epoch + unsigned(sweep);
+            unsigned* mine = a.prog + v;
+            const uint32_t u0 = uint32_t(v) * L;
+            if (lane == 0 && gs > 0)
+                spin_until_geq(mine, gs * L);
+            __syncwarp();
+            unsigned ready = 0, published = 0, ns = 0;
+            while (published < L) {
+                bool moved = false;
+                if (ready < L) {
+                    const unsigned j = ready + unsigned(lane);
+                    bool ok = true;
+                    const unsigned* last = nullptr;
+                    if (j < L) {
+                        const uint32_t b = __ldg(a.dep_off + u0 + j), e = __ldg(a.dep_off + u0 + j + 1);
+                        for (uint32_t k = b; k < e && ok; ++k) {
+                            const uint32_t w = __ldg(a.deps + 2 * size_t(k));
+                            const unsigned xs = w >> 31, u = w & 0x7FFFFFFFu;
+                            if (gs < xs)
+                                continue;
+                            const unsigned need = (gs - xs) * L + __ldg(a.deps + 2 * size_t(k) + 1);
+                            last = a.prog + u;
+                            ok = ld_relaxed(last) >= need;
+                        }
+                    }
+                    const unsigned bad = __ballot_sync(0xFFFFFFFFu, !ok);
+                    const unsigned adv = bad ? unsigned(__ffs(bad) - 1) : 32u;
+                    const unsigned nr = min(L, ready + adv);
+                    if (nr > ready) {
+                        if (unsigned(lane) < adv && last != nullptr)
+                            (void)ld_acquire(last);
+                        __syncwarp();
+                        ready = nr;
+                        moved = true;
+                        if (lane == 0)
+                            st_release_cta_shared(&s_ready, ready);
+                    }
+                }
+                const unsigned d = ld_acquire_cta_shared(&s_done);
+                if (d > published) {
+                    if (lane == 0) {
+                        fence_acq_rel_gpu();
+                        st_relaxed_gpu(mine, gs * L + d);
+                    }
+                    published = d;
+                    moved = true;
+                }
+                if (moved) {
+                    ns = 0;
+                } else {
+                    ns = ns ? min(ns * 2, 128u) : 16u;
+                    __nanosleep(ns);
+                }
+            }
+            if (lane == 0)
+                claimed = atomicAdd(a.next, 1u);
+            __syncthreads();  // task boundary
+            if (lane == 0) {
+                s_task = claimed;
+                s_ready = 0;
+                s_done = 0;
+            }
+            __syncthreads();
+            task = int(s_task);
+        }
+        return;
+    }
+    // ---- updater warp ----
+    float* __restrict__ f = a.m.field;
+    auto wait_ready = [&](unsigned j) {
+        if (ld_acquire_cta_shared(&s_ready) <= j) {
+            while (ld_acquire_cta_shared(&s_ready) <= j)
+                __nanosleep(16);
+        }
+    };
+    while (task < total) {
+        const int v = task % a.views;
+        const uint32_t u0 = uint32_t(v) * L;
+        for (unsigned j = unsigned(lane); j <= L; j += 32)
+            s_pos[j] = __ldg(a.pos + u0 + j);
+        __syncwarp();
+        const double pf = __ldg(a.m.p_floor);
+        const bool act = __ldg(a.m.active) != 0;
+        auto load_entries = [&](unsigned j) {
+            const uint32_t p0 = s_pos[j];
+            const int n = int(s_pos[j + 1] - p0);
+            uint2* dst = s_ent + (j % 3) * kWave1Cover;
+#pragma unroll
+            for (int i = 0; i < kWave1K; ++i) {
+                const int s = lane + 32 * i;
+                cp_async8_if(s < n, dst + s, a.ent + p0 + s);
+            }
+        };
+        // the next line's cells that this line does not cross, into
+        // registers (L2 loads: a 4-byte cp.async would go through L1, which
+        // can hold a stale copy of a cell this warp stored since)
+        float xn[kWave1K];
+        auto gather = [&](unsigned j) {
+            const int n = int(s_pos[j + 1] - s_pos[j]);
+            const uint2* e = s_ent + (j % 3) * kWave1Cover;
+#pragma unroll
+            for (int i = 0; i < kWave1K; ++i) {
+                const int s = lane + 32 * i;
+                const uint32_t c = s < n ? e[s].x : kWavePrev;
+                xn[i] = !(c & kWavePrev) ? __ldcg(f + c) : 0.f;
+            }
+        };
+        load_entries(0);
+        if (L > 1)
+            load_entries(1);
+        cp_async_commit();
+        cp_async_wait_all();
+        __syncwarp();
+        wait_ready(0);
+        gather(0);
+        float nm = __ldcs(a.m.proj + size_t(u0) * a.m.Sp);
+        for (unsigned j = 0; j < L; ++j) {
+            const int n = int(s_pos[j + 1] - s_pos[j]);
+            const double m = double(nm);
+            if (j + 1 < L)
+                nm = __ldcs(a.m.proj + size_t(u0 + j + 1) * a.m.Sp);
+            cp_async_wait_all();  // the entries of line j+1
+            __syncwarp();  // hand-overs of line j-1, entries loaded by other lanes
+            const uint2* e = s_ent + (j % 3) * kWave1Cover;
+            float x[kWave1K];
+            float part = 0.f;
+#pragma unroll
+            for (int i = 0; i < kWave1K; ++i) {
+                const int s = lane + 32 * i;
+                x[i] = s < n ? ((e[s].x & kWavePrev) ? buf[s] : xn[i]) : 0.f;
+                part += x[i];
+            }
+            double p_bar = part;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1)
+                p_bar += __shfl_xor_sync(0xFFFFFFFFu, p_bar, o);
+            __syncwarp();  // every lane has read its slots of line j
+            if (j + 2 < L)
+                load_entries(j + 2);
+            cp_async_commit();
+            bool issued = false;
+            if (j + 1 < L && ld_acquire_cta_shared(&s_ready) > j + 1) {
+                gather(j + 1);
+                issued = true;
+            }
+            // mart_update_line (solver.cpp:36-46), fp64, in every lane
+            double factor = 0;
+            if (m != 0 && act) {
+                const double ratio = m / (p_bar > pf ? p_bar : pf);
+                factor = 1.0 - a.m.beta * (1.0 - ratio);
+                if (factor <= 0) {
+                    factor = pf;
+                    if (lane == 0)
+                        atomicAdd(a.m.clamps, 1ull);
+                }
+            }
+            const bool any = factor != 0;
+            const float g = any ? float(factor) : 1.f, lb = any ? FLT_MIN : 0.f;
+#pragma unroll
+            for (int i = 0; i < kWave1K; ++i) {
+                const int s = lane + 32 * i;
+                if (s < n) {
+                    const uint2 en = e[s];
+                    const float r = fmaxf(x[i] * g, lb);
+                    if (en.y != kWaveNoNext)
+                        buf[en.y] = r;  // handed over to line j+1
+                    else if (any)
+                        __stcg(f + (en.x & ~kWavePrev), r);
+                }
+            }
+            __syncwarp();  // the line's stores and hand-overs precede `done`
+            if (lane == 0)
+                st_release_cta_shared(&s_done, j + 1);
+            if (!issued && j + 1 < L) {
+                wait_ready(j + 1);
+                gather(j + 1);
+            }
+        }
+        __syncthreads();  // task boundary
+        __syncthreads();
+        task = int(s_task);
+    }
+}
+
 template <int P>
 static void wave_launch_t(const WaveArgs& a, int sms, cudaStream_t st) {
     constexpr int NT = WaveShape<P>::G + 64;
@@ -1606,6 +1825,23 @@ static void wave_launch_t(const WaveArgs& a, int sms, cudaStream_t st) {
     mart_wave_kernel<P><<<grid, NT, smem, st>>>(a);
 }
 
+static void wave1_launch(const WaveArgs& a, int sms, cudaStream_t st) {
+    const size_t smem = wave_smem_bytes(a.m, a.lines);
+    UB_CUDA(cudaFuncSetAttribute(mart_wave1_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    int per_sm = 0;
+    UB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, mart_wave1_kernel, 64, smem));
+    if (per_sm < 1)
+        throw CudaError("mart_wave1_kernel cannot be resident");
+    if (const char* e = std::getenv("USCG_WAVE_PER_SM"))
+        per_sm = std::max(1, std::min(per_sm, std::atoi(e)));
+    const int total = a.views * a.n_sweeps;
+    const int grid = std::min(total, sms * per_sm);
+    if (const char* e = std::getenv("USCG_FLOW_VERBOSE"); e && std::atoi(e))
+        std::fprintf(stderr, "mart_wave_kernel: P=1 grid=%d per_sm=%d smem=%zu tasks=%d\n", grid, per_sm, smem,
+                     total);
+    mart_wave1_kernel<<<grid, 64, smem, st>>>(a);
+}
+
 bool wave_supported(const MartArgs& h) {
     int optin = 0, dev = 0;
     if (cudaGetDevice(&dev) != cudaSuccess ||
@@ -1614,6 +1850,7 @@ bool wave_supported(const MartArgs& h) {
     const int P = h.Sp / h.nchunks;
     int cover = 0;
     switch (P) {
+        case 1: cover = h.Sp == 1 ? kWave1Cover : 0; break;
         case 4: cover = wave_cover<4>(); break;
         case 8: cover = wave_cover<8>(); break;
         case 16: cover = wave_cover<16>(); break;
@@ -1655,11 +1892,12 @@ void launch_mart_wave(const MartArgs& h, const WaveSchedule& ws, unsigned* prog,
     a.prof = prof;
     UB_CUDA(cudaMemsetAsync(next, 0, sizeof(unsigned), st));
     switch (h.Sp / h.nchunks) {
+        case 1: wave1_launch(a, sms, st); break;
         case 4: wave_launch_t<4>(a, sms, st); break;
         case 8: wave_launch_t<8>(a, sms, st); break;
         case 16: wave_launch_t<16>(a, sms, st); break;
         case 32: wave_launch_t<32>(a, sms, st); break;
-        default: throw CudaError("mart_wave_kernel supports problem chunks of 4, 8, 16 or 32");
+        default: throw CudaError("mart_wave_kernel supports problem chunks of 1 (one problem), 4, 8, 16 or 32");
     }
     count_launch();
     cudaError_t e = cudaGetLastError();

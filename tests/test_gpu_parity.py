@@ -556,7 +556,9 @@ def test_pipelined_runs_are_bit_identical(ub, orc, monkeypatch, capfd, S, run, w
 @pytest.mark.parametrize("S,width,detector,tol,beta", [(128, 8, "arc", 0, 0.7), (64, 16, "arc", 0, 0.7),
                                                       (128, 32, "arc", 0, 0.7), (64, 32, "parallel", 1e-3, 0.7),
                                                       (40, 8, "parallel", 0, 0.7), (16, 4, "arc", 0, 0.7),
-                                                      (32, 8, "arc", 1e-3, 0.7), (24, 8, "arc", 0, 1.9)])
+                                                      (32, 8, "arc", 1e-3, 0.7), (24, 8, "arc", 0, 1.9),
+                                                      (1, 1, "arc", 0, 0.7), (1, 1, "parallel", 1e-3, 0.7),
+                                                      (1, 1, "arc", 0, 1.9)])
 def test_wave_executor_matches_flow(ub, orc, monkeypatch, capfd, S, width, detector, tol, beta):
     """The wave executor (one CTA per (view, problem chunk), other views
     ordered by progress counters, gathers one line ahead with shared cells
@@ -574,7 +576,8 @@ def test_wave_executor_matches_flow(ub, orc, monkeypatch, capfd, S, width, detec
     proj = ub.project_stack(tr, truth.astype(np.float32))
     if beta > 1:
         proj[:, 3, 40:60] = 1e-9  # drives factors <= 0: clamps
-    proj[min(2, S - 1)] = 0  # one all-zero problem
+    if S > 1:
+        proj[min(2, S - 1)] = 0  # one all-zero problem
     cfg = ub.SolverConfig(beta=beta, tolerance=tol, max_sweeps=3)
     out = {}
     for mode, per_sm in (("wave", 1), ("flow", 0), ("wave", 8), ("wave", 8)):

@@ -161,6 +161,12 @@ struct uscg_tracer_s {
     double wave_seconds = 0;
     double generator_ms = 0;  // device time of the first-view generator
     int executor = -1;        // MART executor of the last reconstruction (uscg_tracer_info)
+    // flow executor, one problem: every (view, line)'s traced list (built once
+    // per geometry when it fits in device memory)
+    bool lists_built = false, lists_off = false;
+    DevBuf<uint32_t> d_lists;
+    DevBuf<unsigned long long> d_lpos;
+    double lists_seconds = 0;
     // MART workspace
     DevBuf<MartArgs> d_args;
     DevBuf<float> w_field, w_proj, w_prev, w_stage;
@@ -792,6 +798,57 @@ void build_wave(uscg_tracer_s* t) {
     if (const char* e = std::getenv("USCG_FLOW_VERBOSE"); e && std::atoi(e))
         std::fprintf(stderr, "wave schedule: %llu traced entries, %llu requirements, %.3f s\n",
                      (unsigned long long)total, (unsigned long long)t->wave_deps, t->wave_seconds);
+}
+
+// The flow executor's one-problem lists (USCG_FLOW_LISTS=0 disables): the
+// traced index list of every (view, line) in unit order, written by the trace
+// kernel in batches of at most 2^27 cells (u32 positions within a batch), so
+// the single-warp updaters copy a line instead of tracing it every sweep. Kept
+// only when it takes at most half of the free device memory.
+void build_lists(uscg_tracer_s* t) {
+    if (t->lists_built || t->lists_off)
+        return;
+    if (const char* e = std::getenv("USCG_FLOW_LISTS"); e && !std::atoi(e)) {
+        t->lists_off = true;
+        return;
+    }
+    const auto h0 = std::chrono::steady_clock::now();
+    const uint64_t units = t->units(), total = t->cells_per_sweep;
+    size_t free_b = 0, total_b = 0;
+    UB_CUDA(cudaMemGetInfo(&free_b, &total_b));
+    if (total == 0 || total * 4 + (units + 1) * 8 > free_b / 2) {
+        t->lists_off = true;
+        return;
+    }
+    std::vector<unsigned long long> lpos(units + 1);
+    lpos[0] = 0;
+    for (uint64_t u = 0; u < units; ++u)
+        lpos[u + 1] = lpos[u] + t->h_cells[u];
+    t->d_lpos.alloc(lpos.size());
+    UB_CUDA(cudaMemcpy(t->d_lpos.p, lpos.data(), sizeof(unsigned long long) * lpos.size(), cudaMemcpyHostToDevice));
+    t->d_lists.alloc(total);
+    constexpr uint64_t kBatch = uint64_t(1) << 27;
+    std::vector<uint32_t> pos;
+    DevBuf<uint32_t> d_pos;
+    uint64_t u0 = 0;
+    while (u0 < units) {
+        uint64_t u1 = u0 + 1;
+        while (u1 < units && lpos[u1 + 1] - lpos[u0] <= kBatch)
+            ++u1;
+        pos.resize(size_t(u1 - u0) + 1);
+        for (uint64_t u = u0; u <= u1; ++u)
+            pos[size_t(u - u0)] = uint32_t(lpos[u] - lpos[u0]);
+        d_pos.ensure(pos.size());
+        UB_CUDA(cudaMemcpyAsync(d_pos.p, pos.data(), sizeof(uint32_t) * pos.size(), cudaMemcpyHostToDevice, t->st()));
+        launch_trace_dump(t->trace_args(), uint32_t(u0), uint32_t(u1 - u0), t->max_recs, t->max_cells, d_pos.p,
+                          t->d_lists.p + lpos[u0], t->st());
+        UB_CUDA(cudaStreamSynchronize(t->st()));  // pos is reused
+        u0 = u1;
+    }
+    t->lists_built = true;
+    t->lists_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - h0).count();
+    if (const char* e = std::getenv("USCG_FLOW_VERBOSE"); e && std::atoi(e))
+        std::fprintf(stderr, "flow lists: %llu entries, %.3f s\n", (unsigned long long)total, t->lists_seconds);
 }
 
 // One sweep = one graph replay: every dependency level is a kernel node.
@@ -1441,6 +1498,8 @@ static void reconstruct_body(uscg_tracer t, const float* proj, int32_t problems,
     need(exec_mode != 2 || t->run == 1, "the level executor needs a line-granular schedule");
     if (exec_mode == 2)
         ensure_graph(t, h);
+    if (exec_mode == 0 && P == 1)
+        build_lists(t);  // once per geometry, outside the timed sweeps
     if (exec_mode == 0 && t->done_chunks != h.nchunks) {
         const uint64_t n = uint64_t(t->n_runs) * uint64_t(h.nchunks);
         t->d_done.alloc(n);
@@ -1530,7 +1589,8 @@ static void reconstruct_body(uscg_tracer t, const float* proj, int32_t problems,
             fs.run = t->run;
             fs.runs_per_view = t->runs_per_view;
             launch_mart_flow(h, fs, t->d_done.p, t->d_bar.p + 1, t->epoch + 1, n_run, t->n_rings,
-                             slab, st, prof.p);
+                             slab, st, prof.p, t->lists_built ? t->d_lists.p : nullptr,
+                             t->lists_built ? t->d_lpos.p : nullptr);
             t->epoch += unsigned(n_run);
             if (prof_path) {
                 std::vector<unsigned long long> hp(nt * 16);

@@ -116,9 +116,12 @@ struct FlowSchedule {
 
 // Runs `sweeps` sweeps back to back (cross-sweep dependencies, no boundary);
 // epoch = global 1-based index of the first of them.
+// lists/lpos (optional, one-problem runs): every (view, line)'s traced list
+// at lists[lpos[u], lpos[u+1]) instead of tracing each line every sweep
 void launch_mart_flow(const MartArgs& h, const FlowSchedule& fs, unsigned* count, unsigned* next,
                       unsigned epoch, int sweeps, int n_rings, const FlowSlab& slab,
-                      cudaStream_t st, unsigned long long* prof = nullptr);
+                      cudaStream_t st, unsigned long long* prof = nullptr, const uint32_t* lists = nullptr,
+                      const unsigned long long* lpos = nullptr);
 
 // K3 wave executor (2D problem stacks, mart_sweep.cu): one task per (sweep,
 // view, problem chunk) updates the view's lines in order; other views are

@@ -517,12 +517,13 @@ struct FlowLayout {
     size_t bytes;
 };
 
-static FlowLayout flow_layout(const MartArgs& a, int n_rings, int GU, bool pipe, size_t budget, int cta) {
+static FlowLayout flow_layout(const MartArgs& a, int n_rings, int GU, bool pipe, size_t budget, int cta,
+                              bool lists = false) {
     const int P = a.Sp / a.nchunks;
     FlowLayout L;
     L.tracer_words = round4(group_words(P, TG, true, a.max_recs, a.max_cells, pipe ? a.run : 1)) +
                      (pipe ? tracer_extra(a.run, a.max_cells) : 0);
-    L.updater_words = round4(group_words(P, GU, GU == 32, a.max_recs, a.max_cells, a.run)) +
+    L.updater_words = round4(group_words(P, GU, GU == 32 && !lists, a.max_recs, a.max_cells, a.run)) +
                       (pipe ? updater_extra(P, a.run, a.max_cells) : 0);
     const size_t avail = budget / sizeof(uint32_t) - ring_words(n_rings);
     L.groups = int(std::min<size_t>(cta / GU, avail / L.updater_words));
@@ -560,6 +561,10 @@ struct FlowArgs {
     int tr_groups;             // tracer groups per tracer CTA
     int pipe;                  // pipelined runs (run tracer marks, pipe_run updaters)
     unsigned long long* prof;  // optional: per task phase stamps (ns)
+    // single-warp updaters: every (view, line)'s traced list, built once per
+    // geometry (null: trace each line from the record store every sweep)
+    const uint32_t* lists;
+    const unsigned long long* lpos;  // [units + 1]
 };
 
 // line (unit) id of line j of run `run`
@@ -851,6 +856,14 @@ __device__ __forceinline__ void prefetch_next(const FlowArgs& a, unsigned nxt, i
         return;
     const uint32_t run = __ldg(a.order + (int(nxt) % per_sweep) / a.m.nchunks);
     const uint32_t unit = run_line(a, run, 0);
+    if (a.lists) {  // the next task's traced lists
+        const unsigned long long l0 = __ldg(a.lpos + unit), l1 = __ldg(a.lpos + unit + a.run);
+        const uintptr_t b = reinterpret_cast<uintptr_t>(a.lists + l0) & ~uintptr_t(15);
+        const uintptr_t e = (reinterpret_cast<uintptr_t>(a.lists + l1) + 15) & ~uintptr_t(15);
+        if (e > b)
+            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(b), "r"(uint32_t(e - b)) : "memory");
+        return;
+    }
     const uint32_t line = unit % uint32_t(a.m.tr.lines);
     const uint32_t r0 = __ldg(a.m.tr.off + line), r1 = __ldg(a.m.tr.off + line + a.run);
     prefetch_l2(a.m.tr.key, sizeof(uint32_t), r0, r1);
@@ -961,7 +974,28 @@ __device__ void flow_updater(const FlowArgs& a, GroupWorker<P, G>& W) {
             // traces its run's lines itself (no slab) while the predecessors
             // finish, then lane 0 waits on them
             (void)stage_lists;
-            for (int j = 0; j < a.run; ++j) {
+            for (int j = 0; j < a.run && a.lists; ++j) {
+                // the line's list, traced once per geometry
+                const uint32_t unit = run_line(a, run, j);
+                const unsigned long long l0 = __ldg(a.lpos + unit);
+                const int n = int(__ldg(a.lpos + unit + 1) - l0);
+                uint32_t* dst = W.idx0 + size_t(j) * a.m.max_cells;
+                const uint32_t* src = a.lists + l0;
+                int c = W.t;
+                for (; c + 96 < n; c += 128) {
+                    const uint32_t v0 = __ldcs(src + c), v1 = __ldcs(src + c + 32), v2 = __ldcs(src + c + 64),
+                                   v3 = __ldcs(src + c + 96);
+                    dst[c] = v0;
+                    dst[c + 32] = v1;
+                    dst[c + 64] = v2;
+                    dst[c + 96] = v3;
+                }
+                for (; c < n; c += 32)
+                    dst[c] = __ldcs(src + c);
+                if (W.t == 0)
+                    W.line_n[j] = n;
+            }
+            for (int j = 0; j < a.run && !a.lists; ++j) {
                 const uint32_t unit = run_line(a, run, j);
                 const int v = int(unit / uint32_t(a.m.tr.lines));
                 const int line = int(unit % uint32_t(a.m.tr.lines));
@@ -1089,7 +1123,8 @@ __global__ void __launch_bounds__(flow_cta<P>(), 1) mart_flow_kernel(FlowArgs a)
         if (int(threadIdx.x) / GU >= a.upd_groups)
             return;  // no shared memory left for this group
         // single-warp updaters trace their own lines (trace arrays needed)
-        GroupWorker<P, GU> W(a.m, smem, a.n_rings, GU == 32, a.run,
+        // unless the lists are precomputed
+        GroupWorker<P, GU> W(a.m, smem, a.n_rings, GU == 32 && a.lists == nullptr, a.run,
                              a.pipe ? updater_extra(P, a.run, a.m.max_cells) : 0);
         flow_updater<P, GU>(a, W);
     }
@@ -1112,7 +1147,7 @@ static void flow_launch_t(FlowArgs& a, int sms, cudaStream_t st) {
         a.pipe = (e ? std::atoi(e) : 0) != 0 && a.m.max_cells <= cover && a.run > 1;
     }
     constexpr int kCta = flow_cta<P>();
-    FlowLayout L = flow_layout(a.m, a.n_rings, GU, a.pipe != 0, size_t(optin) - 1024, kCta);
+    FlowLayout L = flow_layout(a.m, a.n_rings, GU, a.pipe != 0, size_t(optin) - 1024, kCta, a.lists != nullptr);
     if (a.pipe && L.groups < std::min(2, kCta / GU)) {  // too little shared memory: plain runs
         a.pipe = 0;
         L = flow_layout(a.m, a.n_rings, GU, false, size_t(optin) - 1024, kCta);
@@ -1151,7 +1186,8 @@ static void flow_launch_t(FlowArgs& a, int sms, cudaStream_t st) {
 
 void launch_mart_flow(const MartArgs& h, const FlowSchedule& fs, unsigned* count, unsigned* next,
                       unsigned epoch, int sweeps, int n_rings, const FlowSlab& slab,
-                      cudaStream_t st, unsigned long long* prof) {
+                      cudaStream_t st, unsigned long long* prof, const uint32_t* lists,
+                      const unsigned long long* lpos) {
     int dev = 0, sms = 0;
     UB_CUDA(cudaGetDevice(&dev));
     UB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
@@ -1175,6 +1211,8 @@ void launch_mart_flow(const MartArgs& h, const FlowSchedule& fs, unsigned* count
     a.slab = slab;
     a.tracer_ctas = 1;
     a.prof = prof;
+    a.lists = (h.Sp / h.nchunks == 1) ? lists : nullptr;
+    a.lpos = a.lists ? lpos : nullptr;
     a.pipe = 0;
     a.tr_groups = CTA / TG;
     a.upd_groups = 1;

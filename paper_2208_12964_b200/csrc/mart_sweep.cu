@@ -979,6 +979,11 @@ __device__ void flow_updater(const FlowArgs& a, GroupWorker<P, G>& W) {
                 const uint32_t unit = run_line(a, run, j);
                 const unsigned long long l0 = __ldg(a.lpos + unit);
                 const int n = int(__ldg(a.lpos + unit + 1) - l0);
+                if (prof && j == 0) {
+                    __syncwarp();
+                    if (W.t == 0)
+                        prof[9] = gtimer() + 0 * unsigned(n);  // metadata loaded
+                }
                 uint32_t* dst = W.idx0 + size_t(j) * a.m.max_cells;
                 const uint32_t* src = a.lists + l0;
                 int c = W.t;

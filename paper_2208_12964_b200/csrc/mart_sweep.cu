@@ -1108,7 +1108,9 @@ __device__ void flow_updater(const FlowArgs& a, GroupWorker<P, G>& W) {
     }
 }
 
-template <int P>
+// LISTS: single-warp updaters fed by precomputed lists (no trace arrays in
+// their shared memory; a compile-time layout, as the traced form's)
+template <int P, bool LISTS>
 __global__ void __launch_bounds__(flow_cta<P>(), 1) mart_flow_kernel(FlowArgs a) {
     extern __shared__ __align__(16) uint32_t smem[];
     stage_rings(smem, a.m.tr.rings, a.n_rings);
@@ -1129,13 +1131,13 @@ __global__ void __launch_bounds__(flow_cta<P>(), 1) mart_flow_kernel(FlowArgs a)
             return;  // no shared memory left for this group
         // single-warp updaters trace their own lines (trace arrays needed)
         // unless the lists are precomputed
-        GroupWorker<P, GU> W(a.m, smem, a.n_rings, GU == 32 && a.lists == nullptr, a.run,
+        GroupWorker<P, GU> W(a.m, smem, a.n_rings, GU == 32 && !LISTS, a.run,
                              a.pipe ? updater_extra(P, a.run, a.m.max_cells) : 0);
         flow_updater<P, GU>(a, W);
     }
 }
 
-template <int P>
+template <int P, bool LISTS = false>
 static void flow_launch_t(FlowArgs& a, int sms, cudaStream_t st) {
     constexpr int GU = SweepShape<P>::GU;
     int dev = 0, optin = 0;
@@ -1152,7 +1154,7 @@ static void flow_launch_t(FlowArgs& a, int sms, cudaStream_t st) {
         a.pipe = (e ? std::atoi(e) : 0) != 0 && a.m.max_cells <= cover && a.run > 1;
     }
     constexpr int kCta = flow_cta<P>();
-    FlowLayout L = flow_layout(a.m, a.n_rings, GU, a.pipe != 0, size_t(optin) - 1024, kCta, a.lists != nullptr);
+    FlowLayout L = flow_layout(a.m, a.n_rings, GU, a.pipe != 0, size_t(optin) - 1024, kCta, LISTS);
     if (a.pipe && L.groups < std::min(2, kCta / GU)) {  // too little shared memory: plain runs
         a.pipe = 0;
         L = flow_layout(a.m, a.n_rings, GU, false, size_t(optin) - 1024, kCta);
@@ -1162,10 +1164,10 @@ static void flow_launch_t(FlowArgs& a, int sms, cudaStream_t st) {
         a.upd_groups = std::max(1, std::min(L.groups, std::atoi(e)));
     a.tr_groups = L.tgroups;
     const size_t smem = L.bytes;
-    UB_CUDA(cudaFuncSetAttribute(mart_flow_kernel<P>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    UB_CUDA(cudaFuncSetAttribute(mart_flow_kernel<P, LISTS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  int(smem)));
     int per_sm = 0;
-    UB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, mart_flow_kernel<P>, kCta, smem));
+    UB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, mart_flow_kernel<P, LISTS>, kCta, smem));
     if (per_sm < 1)
         throw CudaError("mart_flow_kernel cannot be resident (shared memory too large)");
     const int grid = sms * per_sm;
@@ -1186,7 +1188,7 @@ static void flow_launch_t(FlowArgs& a, int sms, cudaStream_t st) {
                      "upd_groups=%d smem=%zu\n",
                      P, a.run, a.pipe, grid, a.tracer_ctas, a.tr_groups, a.upd_groups, smem);
     // every CTA must be resident: tracers and updaters wait on each other
-    mart_flow_kernel<P><<<grid, kCta, smem, st>>>(a);
+    mart_flow_kernel<P, LISTS><<<grid, kCta, smem, st>>>(a);
 }
 
 void launch_mart_flow(const MartArgs& h, const FlowSchedule& fs, unsigned* count, unsigned* next,
@@ -1226,7 +1228,27 @@ void launch_mart_flow(const MartArgs& h, const FlowSchedule& fs, unsigned* count
     UB_CUDA(cudaMemsetAsync(slab.ready, 0, sizeof(unsigned) * slab.Q, st));
     UB_CUDA(cudaMemsetAsync(slab.used, 0, sizeof(unsigned) * slab.Q, st));
     switch (h.Sp / h.nchunks) {
-        case 1: flow_launch_t<1>(a, sms, st); break;
+        case 1: {
+            // list-fed single-warp updaters: keep the traced form's layout
+            // (trace arrays reserved, unused) when it still fits every group
+            // of the CTA — measured faster there (C1 0.92 vs 1.17 ms, C3 5.9
+            // vs 6.6 ms per iteration) — else drop the trace arrays to fit
+            // more groups (C4: 121 vs 166 ms)
+            bool compact = false;
+            if (a.lists) {
+                int dev = 0, optin = 0;
+                UB_CUDA(cudaGetDevice(&dev));
+                UB_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+                constexpr int GU = SweepShape<1>::GU, kCta = flow_cta<1>();
+                const FlowLayout L = flow_layout(a.m, a.n_rings, GU, false, size_t(optin) - 1024, kCta, false);
+                compact = L.groups < kCta / GU;
+            }
+            if (compact)
+                flow_launch_t<1, true>(a, sms, st);
+            else
+                flow_launch_t<1, false>(a, sms, st);
+            break;
+        }
         case 2: flow_launch_t<2>(a, sms, st); break;
         case 4: flow_launch_t<4>(a, sms, st); break;
         case 8: flow_launch_t<8>(a, sms, st); break;

@@ -153,7 +153,7 @@ struct uscg_tracer_s {
     // requirements (mart_sweep.cu), progress counters [views * nchunks]
     bool wave_built = false;
     DevBuf<uint32_t> d_wpos, d_wdep_off, d_wdeps;
-    DevBuf<uint2> d_went;
+    DevBuf<uint2> d_went, d_went2;
     DevBuf<unsigned> d_wprog, d_wnext;
     int wave_chunks = 0;
     unsigned wave_epoch = 0;
@@ -737,6 +737,30 @@ void build_wave(uscg_tracer_s* t) {
         }
         t->d_went.alloc(ent.size());
         UB_CUDA(cudaMemcpy(t->d_went.p, ent.data(), sizeof(uint2) * ent.size(), cudaMemcpyHostToDevice));
+        // two-ahead form (mart_wave2_kernel): also the position in line+2 of
+        // a cell line+1 does not cross, and the matching in-line-2-only flag
+        std::vector<uint2> ent2(ent.size());
+        for (size_t k = 0; k < ent.size(); ++k)
+            ent2[k] = make_uint2(ent[k].x, ent[k].y | 0xFFFF0000u);
+        std::fill(stamp.begin(), stamp.end(), kNone);
+        for (uint64_t u = 0; u + 2 < units + 0; ++u) {
+            if (u % L + 2 >= L)
+                continue;
+            const uint64_t w = u + 2;
+            for (uint32_t k = pos[w]; k < pos[w + 1]; ++k) {
+                stamp[idx[k]] = uint32_t(w);
+                where[idx[k]] = k - pos[w];
+            }
+            for (uint32_t k = pos[u]; k < pos[u + 1]; ++k) {
+                const uint32_t c = idx[k];
+                if ((ent[k].y & 0xFFFFu) == 0xFFFFu && stamp[c] == uint32_t(w)) {
+                    ent2[k].y = (ent[k].y & 0xFFFFu) | (where[c] << 16);
+                    ent2[pos[w] + where[c]].x |= 0x40000000u;
+                }
+            }
+        }
+        t->d_went2.alloc(ent2.size());
+        UB_CUDA(cudaMemcpy(t->d_went2.p, ent2.data(), sizeof(uint2) * ent2.size(), cudaMemcpyHostToDevice));
     }
 
     constexpr uint32_t NONE = ~0u;
@@ -1530,6 +1554,7 @@ static void reconstruct_body(uscg_tracer t, const float* proj, int32_t problems,
             WaveSchedule ws;
             ws.pos = t->d_wpos.p;
             ws.ent = t->d_went.p;
+            ws.ent2 = t->d_went2.p;
             ws.dep_off = t->d_wdep_off.p;
             ws.deps = t->d_wdeps.p;
             ws.views = t->views;

@@ -130,6 +130,7 @@ struct WaveSchedule {
     const uint32_t* pos;      // [units + 1] offsets into ent
     const uint2* ent;         // every (view, line)'s traced list: {cell | in previous line << 31,
                               //  position in the next line of the view (0xFFFF: none)}
+    const uint2* ent2;        // the same, two-ahead form (mart_sweep.cu, mart_wave2_kernel)
     const uint32_t* dep_off;  // [units + 1]
     const uint32_t* deps;     // pairs {view | cross-sweep << 31, required lines of that view}
     int views;

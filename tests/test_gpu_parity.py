@@ -606,6 +606,35 @@ def test_wave_executor_matches_flow(ub, orc, monkeypatch, capfd, S, width, detec
     assert (np.abs(out["wave"][0][0] - want) / want).max() <= 1e-4
 
 
+@pytest.mark.parametrize("S,width", [(64, 16), (40, 8)])
+def test_two_ahead_wave_matches_flow(ub, orc, monkeypatch, capfd, S, width):
+    """The two-ahead wave form (line k+1's sum as N + g_k H, copies two lines
+    ahead, hand-overs one or two lines ahead; opt-in USCG_WAVE_TWO=1) updates
+    like the flow executor within fp32 summation order, and bit-identically
+    between 1 CTA per SM and the most that fit (a schedule race would show)."""
+    monkeypatch.setenv("USCG_CHUNK_WIDTH", str(width))
+    monkeypatch.setenv("USCG_FLOW_VERBOSE", "1")
+    spec, geom, tr, oc = _m1_case(ub, orc, "arc", n_rings=48, views=16, du=96)
+    rng = np.random.default_rng(5 + S)
+    truth = rng.uniform(0.2, 3.0, (S, spec.cell_count()))
+    proj = ub.project_stack(tr, truth.astype(np.float32))
+    cfg = ub.SolverConfig(beta=0.7, tolerance=0, max_sweeps=3)
+    out = []
+    for mode, two, per_sm in (("wave", 1, 1), ("wave", 1, 8), ("flow", 0, 0)):
+        monkeypatch.setenv("USCG_MART_MODE", mode)
+        monkeypatch.setenv("USCG_WAVE_TWO", str(two))
+        monkeypatch.setenv("USCG_WAVE_PER_SM", str(per_sm))
+        out.append(ub.reconstruct_stack(proj, cfg, tr))
+        log = capfd.readouterr().err
+        assert ("(two-ahead)" in log) == (mode == "wave"), log
+    for p in range(S):
+        assert np.array_equal(out[0][p][0], out[1][p][0]), p
+        np.testing.assert_allclose(out[0][p][0], out[2][p][0], rtol=2e-5, atol=0)
+        assert out[0][p][1].updates == out[2][p][1].updates
+    want, _ = oc.reconstruct(geom.thetas(), proj[0].astype(np.float64), beta=0.7, tolerance=0, max_sweeps=3)
+    assert (np.abs(out[0][0][0] - want) / want).max() <= 1e-4
+
+
 @pytest.mark.parametrize("S,init", [(1, False), (5, False), (8, True)])
 def test_batched_reconstruction_equals_one_call_per_stack(ub, orc, S, init):
     """uscg_reconstruct_batch (transfers of neighbouring stacks overlapped with

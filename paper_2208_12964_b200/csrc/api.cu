@@ -685,7 +685,7 @@ void build_schedule(uscg_tracer_s* t) {
 // is awaited at task start, so same-view requirements are dropped; so is
 // every requirement an earlier line of the view already implies (progress
 // counters are monotone and a view's lines become ready in order).
-constexpr uint64_t kWaveIdxBudget = uint64_t(1) << 29;  // traced entries (2 GiB)
+constexpr uint64_t kWaveIdxBudget = uint64_t(1) << 27;  // traced entries: 2 x 1 GiB of device lists, host build ~3 GB
 
 bool wave_fits(const uscg_tracer_s* t) {
     return !t->volume && t->cells_per_sweep > 0 && t->cells_per_sweep <= kWaveIdxBudget &&

@@ -76,6 +76,10 @@ struct DevBuf {
         if (count > n)
             alloc(count);
     }
+    void swap(DevBuf& o) {
+        std::swap(p, o.p);
+        std::swap(n, o.n);
+    }
 };
 }  // namespace
 
@@ -178,11 +182,44 @@ struct uscg_tracer_s {
     // uscg_reconstruct_batch: double-buffered staging and its copy streams
     DevBuf<float> w_bin[2], w_bout[2];
     cudaStream_t copy_in = nullptr, copy_out = nullptr;
+    // ... and two solve slots, so that one stack's solve starts while the
+    // previous one drains (wave executor): a slot's per-solve workspaces and
+    // wave progress counters are swapped into the tracer for its solve
+    struct SolveSlot {
+        DevBuf<float> w_proj, w_field;
+        DevBuf<double> w_stats, w_pfloor;
+        DevBuf<uint8_t> w_active;
+        DevBuf<unsigned long long> w_clamps, w_updates, w_tmp;
+        DevBuf<MartArgs> d_args;
+        DevBuf<unsigned> d_wprog, d_wnext;
+        int wave_chunks = 0;
+        unsigned wave_epoch = 0;
+        cudaStream_t st = nullptr;
+    };
+    SolveSlot slots[2];
+    void swap_slot(SolveSlot& o) {
+        w_proj.swap(o.w_proj);
+        w_field.swap(o.w_field);
+        w_stats.swap(o.w_stats);
+        w_pfloor.swap(o.w_pfloor);
+        w_active.swap(o.w_active);
+        w_clamps.swap(o.w_clamps);
+        w_updates.swap(o.w_updates);
+        w_tmp.swap(o.w_tmp);
+        d_args.swap(o.d_args);
+        d_wprog.swap(o.d_wprog);
+        d_wnext.swap(o.d_wnext);
+        std::swap(wave_chunks, o.wave_chunks);
+        std::swap(wave_epoch, o.wave_epoch);
+    }
     ~uscg_tracer_s() {
         if (copy_in)
             cudaStreamDestroy(copy_in);
         if (copy_out)
             cudaStreamDestroy(copy_out);
+        for (auto& sl : slots)
+            if (sl.st)
+                cudaStreamDestroy(sl.st);
     }
 
     DevGrid dev_grid() const {
@@ -1366,7 +1403,7 @@ uscg_status uscg_project(uscg_tracer t, const float* field, int32_t problems, fl
 // previous stack's download there, behind this solve's small host reads.
 static void reconstruct_body(uscg_tracer t, const float* proj, int32_t problems, const uscg_solver_config* cfg,
                       float* field_inout, int32_t from_init, uscg_report* reports, uint32_t flags,
-                      const std::function<void()>* after_launch) {
+                      const std::function<void()>* after_launch, std::function<void()>* finish_out = nullptr) {
     need(t != nullptr, "null tracer");
     bind(t->ctx);
     need(cfg != nullptr, "null config");
@@ -1705,9 +1742,15 @@ static void reconstruct_body(uscg_tracer t, const float* proj, int32_t problems,
                                         cudaMemcpyDeviceToHost, st));
         }
     }
+    // the rest waits for the solve: run now, or later by the caller
+    // (uscg_reconstruct_batch starts the next stack's solve first). A copy
+    // into pageable memory would block here until the solve ends, so the
+    // clamp counters are read after the stream has drained.
+    const unsigned long long* d_clamps = t->w_clamps.p;
+    auto finish = [=]() {
+    UB_CUDA(cudaStreamSynchronize(st));
     std::vector<unsigned long long> clamps(Sp);
-    UB_CUDA(cudaMemcpyAsync(clamps.data(), t->w_clamps.p, sizeof(unsigned long long) * Sp,
-                            cudaMemcpyDeviceToHost, st));
+    UB_CUDA(cudaMemcpyAsync(clamps.data(), d_clamps, sizeof(unsigned long long) * Sp, cudaMemcpyDeviceToHost, st));
     UB_CUDA(cudaStreamSynchronize(st));
     float ms = 0;
     UB_CUDA(cudaEventElapsedTime(&ms, e0, e1));
@@ -1744,6 +1787,11 @@ static void reconstruct_body(uscg_tracer t, const float* proj, int32_t problems,
             }
         }
     }
+    };
+    if (finish_out)
+        *finish_out = finish;
+    else
+        finish();
 }
 
 uscg_status uscg_reconstruct(uscg_tracer t, const float* proj, int32_t problems,
@@ -1763,6 +1811,25 @@ uscg_status uscg_reconstruct(uscg_tracer t, const float* proj, int32_t problems,
 //   copy-out stream: [wait ev_ready[b]] D2H out[k] -> host            -> ev_out[b]
 // With the interleaved host layout (or S == 1) the solve runs in place on
 // in[k] and downloads from it, so in[k] is free only after ev_out[b].
+// uscg_reconstruct_batch overlaps neighbouring stacks' solves when the wave
+// executor runs them without residual tracking (USCG_BATCH_OVERLAP=0: one at
+// a time)
+static bool overlap_solves(uscg_tracer t, int S, const uscg_solver_config* cfg) {
+    if (const char* e = std::getenv("USCG_BATCH_OVERLAP"); e && !std::atoi(e))
+        return false;
+    if (cfg == nullptr || cfg->tolerance > 0)
+        return false;
+    const int mode = mart_mode(), P = chunk_width(S), Sp = problem_stride(S);
+    if (!(mode == 3 || (mode == -1 && P >= 4)))
+        return false;
+    MartArgs h{};
+    h.Sp = Sp;
+    h.nchunks = Sp / P;
+    h.max_recs = t->max_recs;
+    h.max_cells = t->max_cells;
+    return wave_fits(t) && wave_supported(h) && wave_fits_smem(h, t->lines);
+}
+
 uscg_status uscg_reconstruct_batch(uscg_tracer t, int32_t batch, const float* const* proj, int32_t problems,
                                    const uscg_solver_config* cfg, float* const* field_inout, int32_t from_init,
                                    uscg_report* reports, uint32_t flags) {
@@ -1851,17 +1918,50 @@ uscg_status uscg_reconstruct_batch(uscg_tracer t, int32_t batch, const float* co
             if (inter)  // the solve ran in place on in[k]: free after the download
                 UB_CUDA(cudaEventRecord(ev_free[b], t->copy_out));
         };
+        // overlapped solves (wave executor, no residual tracking): stack b+1's
+        // solve is launched on the other solve slot before stack b's has
+        // drained, so the wave's ramp and drain of neighbouring stacks overlap
+        const bool overlap = batch > 1 && overlap_solves(t, S, cfg);
+        std::vector<std::function<void()>> fin(batch);
+        cudaStream_t orig = t->ctx->stream;
+        if (overlap)
+            for (auto& sl : t->slots)
+                if (!sl.st)
+                    UB_CUDA(cudaStreamCreateWithFlags(&sl.st, cudaStreamNonBlocking));
         upload(0);
         for (int b = 0; b < batch; ++b) {
             const int k = b % 2;
-            UB_CUDA(cudaStreamWaitEvent(st, ev_in[b], 0));
+            if (overlap && b >= 2)
+                fin[b - 2]();  // stack b-2 (this slot's previous solve) finished
+
+            struct SlotIn {  // the slot's workspaces and stream, swapped in for this solve
+                uscg_tracer_s* t;
+                uscg_tracer_s::SolveSlot* sl;
+                cudaStream_t orig;
+                SlotIn(uscg_tracer_s* tt, uscg_tracer_s::SolveSlot* s, cudaStream_t o) : t(tt), sl(s), orig(o) {
+                    if (sl) {
+                        t->swap_slot(*sl);
+                        t->ctx->stream = sl->st;
+                    }
+                }
+                ~SlotIn() {
+                    if (sl) {
+                        t->swap_slot(*sl);
+                        t->ctx->stream = orig;
+                    }
+                }
+            } slot_in(t, overlap ? &t->slots[k] : nullptr, orig);
+            const cudaStream_t cur = t->st();
+            UB_CUDA(cudaStreamWaitEvent(cur, ev_in[b], 0));
             float* d_proj = in[k].p;
             float* d_field = in[k].p + pw;
             if (!inter) {
-                launch_to_interleaved(in[k].p, t->w_proj.p, units, S, Sp, 0.f, st);
+                t->w_proj.ensure(units * Sp);
+                t->w_field.ensure(cells * Sp);
+                launch_to_interleaved(in[k].p, t->w_proj.p, units, S, Sp, 0.f, cur);
                 if (from_init)
-                    launch_to_interleaved(in[k].p + pw, t->w_field.p, cells, S, Sp, 1.f, st);
-                UB_CUDA(cudaEventRecord(ev_free[b], st));
+                    launch_to_interleaved(in[k].p + pw, t->w_field.p, cells, S, Sp, 1.f, cur);
+                UB_CUDA(cudaEventRecord(ev_free[b], cur));
                 d_proj = t->w_proj.p;
                 d_field = t->w_field.p;
             }
@@ -1872,14 +1972,17 @@ uscg_status uscg_reconstruct_batch(uscg_tracer t, int32_t batch, const float* co
                     upload(b + 1);  // overlaps this stack's solve
             };
             reconstruct_body(t, d_proj, S, cfg, d_field, from_init, reports ? reports + size_t(b) * S : nullptr,
-                             USCG_DEVICE_POINTERS | USCG_LAYOUT_INTERLEAVED, &hook);
+                             USCG_DEVICE_POINTERS | USCG_LAYOUT_INTERLEAVED, &hook, overlap ? &fin[b] : nullptr);
             if (!inter) {
                 if (b >= 2)  // out[k] is free once stack b-2 has been downloaded
-                    UB_CUDA(cudaStreamWaitEvent(st, ev_out[b - 2], 0));
-                launch_from_interleaved(t->w_field.p, out[k].p, cells, S, Sp, st);
+                    UB_CUDA(cudaStreamWaitEvent(cur, ev_out[b - 2], 0));
+                launch_from_interleaved(t->w_field.p, out[k].p, cells, S, Sp, cur);
             }
-            UB_CUDA(cudaEventRecord(ev_ready[b], st));
+            UB_CUDA(cudaEventRecord(ev_ready[b], cur));
         }
+        if (overlap)
+            for (int b = std::max(0, batch - 2); b < batch; ++b)
+                fin[b]();
         download(batch - 1);
         // the context stream ends after the last download (callers time on it)
         UB_CUDA(cudaStreamWaitEvent(st, ev_out[batch - 1], 0));

@@ -1877,7 +1877,13 @@ template <int P>
 static void wave_launch_t(const WaveArgs& a, int sms, cudaStream_t st) {
     constexpr int NT = WaveShape<P>::G + 64;
     const size_t smem = wave_smem_bytes(a.m, a.lines);
-    UB_CUDA(cudaFuncSetAttribute(mart_wave_kernel<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    // set once per size: changing a running kernel's attributes would wait
+    // for it (uscg_reconstruct_batch overlaps neighbouring stacks' solves)
+    static size_t set_smem = 0;
+    if (smem > set_smem) {
+        UB_CUDA(cudaFuncSetAttribute(mart_wave_kernel<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+        set_smem = smem;
+    }
     int per_sm = 0;
     UB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, mart_wave_kernel<P>, NT, smem));
     if (per_sm < 1)

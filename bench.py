@@ -599,7 +599,9 @@ def bench_cmp(args, rank, world, local):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=None,
+                    help="timed steps (default: the configuration's iteration count for c1-c4 — one whole "
+                         "reconstruction, C2: 20 — and 5 for c5, cmp and the reference arm)")
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="c2")
     ap.add_argument("--problems", type=int, default=None)
@@ -614,6 +616,11 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
 
+    if args.steps is None:
+        args.steps = 5
+        if args.impl != "reference" and args.config in ("c1", "c2", "c3", "c4"):
+            from paper_2208_12964_b200 import workloads
+            args.steps = int(workloads.make(args.config).sweeps)
     if args.impl == "reference":
         run_reference(args, rank, world)
         return

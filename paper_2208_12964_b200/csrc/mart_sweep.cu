@@ -1878,7 +1878,8 @@ __global__ void __launch_bounds__(64) mart_wave1_kernel(WaveArgs a) {
 template <int P>
 static void wave_launch_t(const WaveArgs& a, int sms, cudaStream_t st) {
     constexpr int NT = WaveShape<P>::G + 64;
-    const size_t smem = wave_smem_bytes(a.m, a.lines);
+    // this form's own layout (wave_smem_bytes also covers the two-ahead form)
+    const size_t smem = 4 * wave_words<P>(a.m.max_recs, a.m.max_cells, a.lines);
     // set once per size: changing a running kernel's attributes would wait
     // for it (uscg_reconstruct_batch overlaps neighbouring stacks' solves)
     static size_t set_smem = 0;

@@ -127,7 +127,9 @@ typedef struct {
     int32_t executor;              /* MART executor of the last reconstruction: -1 none yet,
                                       0 flow, 1 barrier, 2 levels, 3 wave (USCG_MART_MODE) */
     uint64_t wave_requirements;    /* wave executor: other-view requirements per sweep (0 until built) */
-    double wave_build_s;           /* wave executor: host seconds to build its lists and requirements */
+    double wave_build_s;           /* wave executor: seconds to build its lists and requirements */
+    uint64_t executor_bytes;       /* device bytes the MART executors derived from the record store
+                                      (traced lists, wave entries/requirements, run schedule) */
 } uscg_tracer_info;
 
 const char* uscg_last_error(void);

@@ -81,6 +81,13 @@ class OrcGrid:
                         int(self.volume), _ptr(self.counts, _u32p))
 
     @classmethod
+    def of(cls, spec):
+        """The generalized grid of a GridSpec-like object (duck-typed)."""
+        volume = int(getattr(spec.mode, "value", spec.mode)) == 1
+        counts = None if spec.ring_counts is None else np.asarray(spec.ring_counts, np.uint32)
+        return cls(spec.rings(), spec.ring_spacing, spec.slices(), spec.slice_height, volume, counts)
+
+    @classmethod
     def reference(cls, n, volume=False):
         """GridSpec::square_2d(n) / cube_3d(n) (include/uscg/grid.hpp:38-43)."""
         return cls(n // 2, 2.0 / n, n if volume else 1, 2.0 / n, volume)
@@ -149,6 +156,24 @@ class Orc:
         s = np.zeros((det_u, 3)); d = np.zeros((det_u, 3))
         self.L.orc_rays_parallel(det_u, su, half_len, _ptr(s, _dp), _ptr(d, _dp))
         return s, d
+
+    def rays_for(self, geom):
+        """First-view rays of a scan description (duck-typed: source,
+        detector_center, det_u, det_v, spacing_u, spacing_v, detector kind
+        0 flat / 1 arc / 2 parallel), built by the restatement's own ray
+        generators (scan.cpp:27-36 and the M4/M7 seams) — never by the
+        product library."""
+        kind = int(getattr(geom, "detector", 0))
+        src, ctr = tuple(map(float, geom.source)), tuple(map(float, geom.detector_center))
+        if kind == 0:
+            return self.rays_flat(src, ctr, geom.det_u, geom.det_v, geom.spacing_u, geom.spacing_v)
+        if geom.det_v != 1:
+            raise ValueError("arc / parallel generators are 2D (det_v == 1)")
+        if kind == 1:
+            return self.rays_arc(src, ctr, geom.det_u, geom.spacing_u)
+        if src[1:] != (0.0, 0.0) or ctr[1:] != (0.0, 0.0) or not src[0] == -ctr[0] or ctr[0] <= 0:
+            raise ValueError("the parallel generator is restated for an on-axis beam centred on the origin")
+        return self.rays_parallel(geom.det_u, geom.spacing_u, ctr[0])
 
     def ring_counts_m1(self, n_rings):
         out = np.zeros(n_rings, np.uint32)

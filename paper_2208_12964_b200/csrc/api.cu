@@ -72,6 +72,7 @@ struct DevBuf {
         }
         n = count;
     }
+    uint64_t bytes() const { return uint64_t(n) * sizeof(T); }
     void ensure(size_t count) {
         if (count > n)
             alloc(count);
@@ -1190,6 +1191,10 @@ uscg_status uscg_tracer_get_info(uscg_tracer t, uscg_tracer_info* info) {
         info->executor = t->executor;
         info->wave_requirements = t->wave_deps;
         info->wave_build_s = t->wave_seconds;
+        info->executor_bytes = t->d_lists.bytes() + t->d_lpos.bytes() + t->d_went.bytes() + t->d_went2.bytes() +
+                               t->d_wpos.bytes() + t->d_wdep_off.bytes() + t->d_wdeps.bytes() +
+                               t->d_order.bytes() + t->d_pred_off.bytes() + t->d_preds.bytes() +
+                               t->d_succ_off.bytes() + t->d_succs.bytes() + t->d_npred_x.bytes();
     });
 }
 

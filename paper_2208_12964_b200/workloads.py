@@ -183,8 +183,10 @@ def lump_value(rng: np.random.Generator, x, y, z):
     return np.where(inside, 8.0, np.where(cyl, 0.2, 0.0))
 
 
-def phantom_fields(wl: Workload, problems: Optional[int] = None) -> np.ndarray:
-    """(S, cell_count) float64 truth fields, problem p seeded with seed + p."""
+def phantom_fields(wl: Workload, problems: Optional[int] = None, first: int = 0) -> np.ndarray:
+    """(S, cell_count) float64 truth fields of problems first .. first+S-1,
+    problem p seeded with seed + p (so a slice-sharded rank generates exactly
+    its rows of the full stack)."""
     S = wl.problems if problems is None else problems
     spec = wl.spec
     x, y, z = cell_centroids(spec)
@@ -192,7 +194,7 @@ def phantom_fields(wl: Workload, problems: Optional[int] = None) -> np.ndarray:
     volume = spec.mode == GridMode.Volume3D
     out = np.zeros((S, spec.cell_count()))
     for p in range(S):
-        rng = np.random.default_rng(wl.seed + p)
+        rng = np.random.default_rng(wl.seed + first + p)
         if wl.phantom == "lump":
             vals = [lump_value(rng, x / scale, y / scale, zz / scale) for zz in z]
         else:
@@ -202,13 +204,19 @@ def phantom_fields(wl: Workload, problems: Optional[int] = None) -> np.ndarray:
     return out
 
 
-def add_noise(wl: Workload, proj: np.ndarray, seed_offset: int = 7) -> np.ndarray:
-    """Seeded multiplicative noise clipped at zero."""
+def add_noise(wl: Workload, proj: np.ndarray, seed_offset: int = 7, first: int = 0) -> np.ndarray:
+    """Seeded multiplicative noise clipped at zero. proj is
+    (S, ...) for problems first .. first+S-1; problem p's noise is seeded
+    with seed + 1000003 + seed_offset + p, so shards draw their own rows of
+    the full stack's noise."""
     if wl.noise == "none" or wl.noise_level == 0:
         return proj
-    rng = np.random.default_rng(wl.seed + 1_000_003 + seed_offset)
-    noisy = proj * (1.0 + wl.noise_level * rng.standard_normal(proj.shape))
-    return np.clip(noisy, 0.0, None).astype(proj.dtype)
+    out = np.empty_like(proj)
+    for p in range(proj.shape[0]):
+        rng = np.random.default_rng(wl.seed + 1_000_003 + seed_offset + first + p)
+        noisy = proj[p] * (1.0 + wl.noise_level * rng.standard_normal(proj[p].shape))
+        out[p] = np.clip(noisy, 0.0, None)
+    return out
 
 
 def counters(cells_per_unit: np.ndarray, proj: np.ndarray, records: int, views: int):

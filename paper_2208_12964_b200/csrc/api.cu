@@ -102,15 +102,6 @@ struct uscg_ctx_s {
     MetricsWork* metrics = nullptr;     // uscg_image_metrics scratch (grown, never shrunk)
 };
 
-struct GraphCache {
-    cudaGraphExec_t exec = nullptr;
-    int Sp = 0, nchunks = 0;
-    uint32_t nodes = 0;
-    ~GraphCache() {
-        if (exec)
-            cudaGraphExecDestroy(exec);
-    }
-};
 
 struct uscg_tracer_s {
     uscg_ctx ctx = nullptr;
@@ -158,7 +149,7 @@ struct uscg_tracer_s {
     // requirements (mart_sweep.cu), progress counters [views * nchunks]
     bool wave_built = false;
     DevBuf<uint32_t> d_wpos, d_wdep_off, d_wdeps;
-    DevBuf<uint2> d_went, d_went2;
+    DevBuf<uint2> d_went;
     DevBuf<unsigned> d_wprog, d_wnext;
     int wave_chunks = 0;
     unsigned wave_epoch = 0;
@@ -179,7 +170,6 @@ struct uscg_tracer_s {
     DevBuf<uint8_t> w_active;
     DevBuf<unsigned long long> w_clamps, w_updates, w_tmp;
     DevBuf<unsigned int> w_resid;
-    GraphCache graph;
     // uscg_reconstruct_batch: double-buffered staging and its copy streams
     DevBuf<float> w_bin[2], w_bout[2];
     cudaStream_t copy_in = nullptr, copy_out = nullptr;
@@ -574,18 +564,13 @@ void ensure_crossed(uscg_tracer_s* t) {
 }
 
 // MART executor (USCG_MART_MODE): 0 "flow" dataflow over run dependency
-// counters; 1 "barrier" one grid barrier per level; 2 "levels" a CUDA graph
-// with one kernel node per level; 3 "wave" one task per (view, problem chunk)
-// ordered by per-view progress counters (2D stacks). Unset: "auto" (-1), the
-// wave executor where it applies (2D grid, chunks of 4-16 problems, lines
-// within its register tile, the traced lists within a memory budget), else flow.
+// counters; 3 "wave" one task per (view, problem chunk) ordered by per-view
+// progress counters (2D stacks). Unset: "auto" (-1), the wave executor where
+// it applies (2D grid, chunks of 4-32 problems, lines within its cover, the
+// traced lists within a memory budget), else flow.
 int mart_mode() {
     const char* e = std::getenv("USCG_MART_MODE");
     const std::string m = e ? e : "auto";
-    if (m == "levels")
-        return 2;
-    if (m == "barrier")
-        return 1;
     if (m == "flow")
         return 0;
     if (m == "wave")
@@ -597,9 +582,6 @@ int mart_mode() {
 // whose adjacent lines always overlap, and 1 for volumes): the largest divisor
 // of the lines per view not above the request; 1 for the level executors
 int run_length(int lines, bool volume) {
-    const int mode = mart_mode();
-    if (mode == 1 || mode == 2)
-        return 1;
     int want = volume ? 1 : 4;
     if (const char* e = std::getenv("USCG_RUN"))
         want = std::max(1, std::atoi(e));
@@ -775,30 +757,6 @@ void build_wave(uscg_tracer_s* t) {
         }
         t->d_went.alloc(ent.size());
         UB_CUDA(cudaMemcpy(t->d_went.p, ent.data(), sizeof(uint2) * ent.size(), cudaMemcpyHostToDevice));
-        // two-ahead form (mart_wave2_kernel): also the position in line+2 of
-        // a cell line+1 does not cross, and the matching in-line-2-only flag
-        std::vector<uint2> ent2(ent.size());
-        for (size_t k = 0; k < ent.size(); ++k)
-            ent2[k] = make_uint2(ent[k].x, ent[k].y | 0xFFFF0000u);
-        std::fill(stamp.begin(), stamp.end(), kNone);
-        for (uint64_t u = 0; u + 2 < units + 0; ++u) {
-            if (u % L + 2 >= L)
-                continue;
-            const uint64_t w = u + 2;
-            for (uint32_t k = pos[w]; k < pos[w + 1]; ++k) {
-                stamp[idx[k]] = uint32_t(w);
-                where[idx[k]] = k - pos[w];
-            }
-            for (uint32_t k = pos[u]; k < pos[u + 1]; ++k) {
-                const uint32_t c = idx[k];
-                if ((ent[k].y & 0xFFFFu) == 0xFFFFu && stamp[c] == uint32_t(w)) {
-                    ent2[k].y = (ent[k].y & 0xFFFFu) | (where[c] << 16);
-                    ent2[pos[w] + where[c]].x |= 0x40000000u;
-                }
-            }
-        }
-        t->d_went2.alloc(ent2.size());
-        UB_CUDA(cudaMemcpy(t->d_went2.p, ent2.data(), sizeof(uint2) * ent2.size(), cudaMemcpyHostToDevice));
     }
 
     constexpr uint32_t NONE = ~0u;
@@ -911,37 +869,6 @@ void build_lists(uscg_tracer_s* t) {
     t->lists_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - h0).count();
     if (const char* e = std::getenv("USCG_FLOW_VERBOSE"); e && std::atoi(e))
         std::fprintf(stderr, "flow lists: %llu entries, %.3f s\n", (unsigned long long)total, t->lists_seconds);
-}
-
-// One sweep = one graph replay: every dependency level is a kernel node.
-void ensure_graph(uscg_tracer_s* t, const MartArgs& h) {
-    GraphCache& G = t->graph;
-    if (G.exec && G.Sp == h.Sp && G.nchunks == h.nchunks)
-        return;
-    if (G.exec) {
-        cudaGraphExecDestroy(G.exec);
-        G.exec = nullptr;
-    }
-    mart_prepare(h);
-    cudaStream_t cap;
-    UB_CUDA(cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking));
-    UB_CUDA(cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal));
-    const uint32_t levels = uint32_t(t->level_off.size()) - 1;
-    for (uint32_t l = 0; l < levels; ++l) {
-        const uint32_t b = t->level_off[l], e = t->level_off[l + 1];
-        launch_mart_level(t->d_args.p, h, t->d_order.p + b, int(e - b), cap);
-    }
-    g_launches.fetch_sub(levels);  // captured, not launched
-    cudaGraph_t graph;
-    UB_CUDA(cudaStreamEndCapture(cap, &graph));
-    cudaError_t e = cudaGraphInstantiate(&G.exec, graph, 0);
-    cudaGraphDestroy(graph);
-    cudaStreamDestroy(cap);
-    if (e != cudaSuccess)
-        throw CudaError(std::string("cudaGraphInstantiate: ") + cudaGetErrorString(e));
-    G.Sp = h.Sp;
-    G.nchunks = h.nchunks;
-    G.nodes = levels;
 }
 
 }  // namespace
@@ -1191,7 +1118,7 @@ uscg_status uscg_tracer_get_info(uscg_tracer t, uscg_tracer_info* info) {
         info->executor = t->executor;
         info->wave_requirements = t->wave_deps;
         info->wave_build_s = t->wave_seconds;
-        info->executor_bytes = t->d_lists.bytes() + t->d_lpos.bytes() + t->d_went.bytes() + t->d_went2.bytes() +
+        info->executor_bytes = t->d_lists.bytes() + t->d_lpos.bytes() + t->d_went.bytes() +
                                t->d_wpos.bytes() + t->d_wdep_off.bytes() + t->d_wdeps.bytes() +
                                t->d_order.bytes() + t->d_pred_off.bytes() + t->d_preds.bytes() +
                                t->d_succ_off.bytes() + t->d_succs.bytes() + t->d_npred_x.bytes();
@@ -1538,10 +1465,7 @@ static void reconstruct_body(uscg_tracer t, const float* proj, int32_t problems,
     h.run = t->run;
     t->d_args.ensure(1);
     UB_CUDA(cudaMemcpyAsync(t->d_args.p, &h, sizeof(MartArgs), cudaMemcpyHostToDevice, st));
-    // dataflow: chunks up to 32 problems; level barrier: up to 8
     int exec_mode = mart_mode();
-    if (exec_mode == 1 && P > 8)
-        exec_mode = 2;
     // auto: the wave executor for stacks (P >= 4); for one problem the flow
     // executor's 4-line runs measure faster on C1 (0.93 vs 1.03 ms per
     // iteration), so the single-warp wave form runs only when requested
@@ -1561,9 +1485,6 @@ static void reconstruct_body(uscg_tracer t, const float* proj, int32_t problems,
             t->wave_epoch = 0;
         }
     }
-    need(exec_mode != 2 || t->run == 1, "the level executor needs a line-granular schedule");
-    if (exec_mode == 2)
-        ensure_graph(t, h);
     if (exec_mode == 0 && P == 1)
         build_lists(t);  // once per geometry, outside the timed sweeps
     if (exec_mode == 0 && t->done_chunks != h.nchunks) {
@@ -1596,7 +1517,6 @@ static void reconstruct_body(uscg_tracer t, const float* proj, int32_t problems,
             WaveSchedule ws;
             ws.pos = t->d_wpos.p;
             ws.ent = t->d_went.p;
-            ws.ent2 = t->d_went2.p;
             ws.dep_off = t->d_wdep_off.p;
             ws.deps = t->d_wdeps.p;
             ws.views = t->views;
@@ -1669,29 +1589,6 @@ static void reconstruct_body(uscg_tracer t, const float* proj, int32_t problems,
                     std::fclose(fp);
                 }
             }
-        } else if (exec_mode == 1) {
-            // USCG_SWEEP_PROFILE=<file>: per-level phase stamps of CTA 0 (diagnostics)
-            static const char* prof_path = std::getenv("USCG_SWEEP_PROFILE");
-            DevBuf<unsigned long long> prof;
-            if (prof_path) {
-                prof.alloc(size_t(levels) * 4);
-                UB_CUDA(cudaMemsetAsync(prof.p, 0, sizeof(unsigned long long) * levels * 4, st));
-            }
-            launch_mart_sweep(h, t->d_order.p, t->d_level_off.p, levels, t->d_bar.p, t->n_rings,
-                              st, prof.p);
-            if (prof_path) {
-                std::vector<unsigned long long> hp(size_t(levels) * 4);
-                UB_CUDA(cudaMemcpyAsync(hp.data(), prof.p, sizeof(unsigned long long) * hp.size(),
-                                        cudaMemcpyDeviceToHost, st));
-                UB_CUDA(cudaStreamSynchronize(st));
-                if (FILE* fp = std::fopen(prof_path, "wb")) {
-                    std::fwrite(hp.data(), sizeof(unsigned long long), hp.size(), fp);
-                    std::fclose(fp);
-                }
-            }
-        } else {
-            UB_CUDA(cudaGraphLaunch(t->graph.exec, st));
-            count_launch(t->graph.nodes);
         }
         if (after_launch) {
             (*after_launch)();

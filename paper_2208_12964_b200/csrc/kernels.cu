@@ -1106,117 +1106,6 @@ void launch_project(const TraceArgs& A, int views, const float* field, int Sp, i
 }
 
 // =============================================================================
-// K3: one dependency level of Sp-MART. The units of a level have pairwise
-// disjoint cell supports (host-built ASAP schedule), so applying them
-// concurrently performs exactly the reference's sequential updates
-// (solver.cpp:111-136): no atomics on the field, no reordering on any cell.
-// =============================================================================
-
-template <int P>
-__global__ void __launch_bounds__(Shape<P>::NT) mart_level_kernel(const MartArgs* __restrict__ args,
-                                                                  const uint32_t* __restrict__ units) {
-    constexpr int NT = Shape<P>::NT, KR = Shape<P>::KR, NCL = NT / P;
-    extern __shared__ uint32_t smem[];
-    __shared__ double s_red[NT / 32][P];
-    __shared__ double s_fac[P];
-    const MartArgs& A = *args;
-    const TraceSmem S = carve_trace_smem<NT>(smem, A.max_recs);
-    const int nchunks = A.nchunks;
-    const uint32_t unit = units[blockIdx.x / nchunks];
-    const int chunk = blockIdx.x % nchunks;
-    const int v = int(unit / uint32_t(A.tr.lines)), line = int(unit % uint32_t(A.tr.lines));
-    const int n = block_trace<NT>(A.tr, line, A.tr.theta[v], S, true);
-
-    const int p = threadIdx.x % P, cl = threadIdx.x / P;
-    const int Sp = A.Sp;
-    const size_t col = size_t(chunk) * P + p;
-    float* __restrict__ f = A.field;
-
-    // forward_project_line (solver.cpp:25-31): all KR loads in flight
-    float x[KR];
-#pragma unroll
-    for (int i = 0; i < KR; ++i) {
-        const int c = cl + i * NCL;
-        x[i] = c < n ? f[size_t(S.idx[c]) * Sp + col] : 0.f;
-    }
-    double sum = 0;
-#pragma unroll
-    for (int i = 0; i < KR; ++i)
-        sum += double(x[i]);
-    for (int c = cl + KR * NCL; c < n; c += NCL)
-        sum += double(f[size_t(S.idx[c]) * Sp + col]);
-    block_problem_sum<P, NT>(sum, s_red);
-    if (threadIdx.x < P) {
-        const size_t c2 = size_t(chunk) * P + threadIdx.x;
-        double p_bar = 0;
-#pragma unroll
-        for (int w = 0; w < NT / 32; ++w)
-            p_bar += s_red[w][threadIdx.x];
-        const double m = double(A.proj[size_t(unit) * Sp + c2]);
-        double factor = 0;  // 0 marks "no update"
-        if (m != 0 && A.active[c2]) {
-            // mart_update_line (solver.cpp:36-46)
-            const double pf = A.p_floor[c2];
-            const double ratio = m / (p_bar > pf ? p_bar : pf);
-            factor = 1.0 - A.beta * (1.0 - ratio);
-            if (factor <= 0) {
-                factor = pf;
-                atomicAdd(A.clamps + c2, 1ull);
-            }
-        }
-        s_fac[threadIdx.x] = factor;
-    }
-    __syncthreads();
-    const double factor = s_fac[p];
-    if (factor == 0)
-        return;
-    // The reference's clamp keeps the fp64 field strictly positive
-    // (solver.cpp:42-45); an fp32 product below FLT_MIN would underflow to 0,
-    // so it saturates at FLT_MIN instead.
-#pragma unroll
-    for (int i = 0; i < KR; ++i) {
-        const int c = cl + i * NCL;
-        if (c < n) {
-            const float r = float(double(x[i]) * factor);
-            f[size_t(S.idx[c]) * Sp + col] = r >= FLT_MIN ? r : FLT_MIN;
-        }
-    }
-    for (int c = cl + KR * NCL; c < n; c += NCL) {
-        float* q = f + size_t(S.idx[c]) * Sp + col;
-        const float r = float(double(*q) * factor);
-        *q = r >= FLT_MIN ? r : FLT_MIN;
-    }
-}
-
-template <int P>
-static size_t mart_smem_t(const MartArgs& a) {
-    return trace_smem_bytes(Shape<P>::NT, a.max_recs, a.max_cells);
-}
-
-size_t mart_smem_bytes(const MartArgs& a) {
-    size_t r = 0;
-    UB_DISPATCH_P(a.Sp / a.nchunks, r = mart_smem_t<PP>(a));
-    return r;
-}
-
-void mart_prepare(const MartArgs& a) {
-    UB_DISPATCH_P(a.Sp / a.nchunks,
-                  UB_CUDA(cudaFuncSetAttribute(mart_level_kernel<PP>,
-                                               cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                               int(mart_smem_t<PP>(a)))));
-}
-
-void launch_mart_level(const MartArgs* dargs, const MartArgs& h, const uint32_t* units, int n,
-                       cudaStream_t st) {
-    if (n <= 0)
-        return;
-    UB_DISPATCH_P(h.Sp / h.nchunks,
-                  (mart_level_kernel<PP><<<unsigned(n) * unsigned(h.nchunks), Shape<PP>::NT,
-                                           mart_smem_t<PP>(h), st>>>(dargs, units)));
-    check_launch();
-}
-
-// =============================================================================
 // per-problem reductions over [n][Sp] arrays: blockIdx.y = 32-column tile,
 // threadIdx.x = column in the tile, threadIdx.y = row lane.
 // =============================================================================

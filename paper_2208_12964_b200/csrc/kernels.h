@@ -78,18 +78,6 @@ void launch_project_length(const DevGrid& g, int lines, int views, const double*
 void launch_project(const TraceArgs& A, int views, const float* field, int Sp, int max_recs,
                     int max_cells, float* out, cudaStream_t st);
 
-// K3 one MART dependency level: n units of `units`, all problem chunks
-void launch_mart_level(const MartArgs* dargs, const MartArgs& hargs, const uint32_t* units, int n,
-                       cudaStream_t st);
-size_t mart_smem_bytes(const MartArgs& a);
-void mart_prepare(const MartArgs& a);  // sets smem attributes
-
-// K3 persistent: one cooperative launch runs every level of a sweep
-// (mart_sweep.cu). Problem chunks of at most 8; bar is a device counter.
-void launch_mart_sweep(const MartArgs& h, const uint32_t* order, const uint32_t* level_off,
-                       int levels, unsigned* bar, int n_rings, cudaStream_t st,
-                       unsigned long long* prof = nullptr);
-size_t sweep_smem_bytes(const MartArgs& a, int n_rings);
 // Ring of traced index lists shared by the chunk tasks of a unit:
 // slot = [n, idx[0..n)], slot_words >= max_cells + 1.
 struct FlowSlab {
@@ -130,7 +118,6 @@ struct WaveSchedule {
     const uint32_t* pos;      // [units + 1] offsets into ent
     const uint2* ent;         // every (view, line)'s traced list: {cell | in previous line << 31,
                               //  position in the next line of the view (0xFFFF: none)}
-    const uint2* ent2;        // the same, two-ahead form (mart_sweep.cu, mart_wave2_kernel)
     const uint32_t* dep_off;  // [units + 1]
     const uint32_t* deps;     // pairs {view | cross-sweep << 31, required lines of that view}
     int views;

@@ -19,8 +19,9 @@
 //     groups for problem stacks (float4 over 8 problems per cell) and single
 //     warps for one problem (3D volumes), so that small tasks keep the machine
 //     busy.
-//   * mart_sweep_kernel: one grid barrier per dependency level (cooperative
-//     launch), next task traced between arrive and wait (line-granular).
+//   * mart_wave_kernel (2D stacks, below): one CTA per (view, problem chunk)
+//     task, the view's lines in order inside the CTA, other views ordered by
+//     per-view progress counters.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -497,14 +498,6 @@ __device__ __forceinline__ void stage_rings(uint32_t* smem, const RingRow* rings
         s[k] = rings[k];
 }
 }  // namespace
-
-// level-barrier kernel: 4 groups of 256 threads, each tracing its own tasks
-size_t sweep_smem_bytes(const MartArgs& a, int n_rings) {
-    const int P = a.Sp / a.nchunks;
-    return sizeof(uint32_t) *
-           (ring_words(n_rings) +
-            (CTA / TG) * round4(group_words(P, TG, true, a.max_recs, a.max_cells, 1)));
-}
 
 // dataflow kernel: the larger of the tracer layout (`tgroups` x 256 threads
 // with trace arrays; pipelined: a run's lists, next positions and the cell
@@ -1292,8 +1285,6 @@ struct WaveArgs {
     MartArgs m;
     const uint32_t* pos;      // [units + 1]: traced list of unit u at ent[pos[u], pos[u+1])
     const uint2* ent;         // per traced entry {cell | in previous line << 31, position in next line}
-    const uint2* ent2;        // two-ahead form: {cell | in line-1 << 31 | in line-2 only << 30,
-                              //  position in line+1 | position in line+2 (if not in line+1) << 16}
     const uint32_t* dep_off;  // [units + 1]
     const uint32_t* deps;     // pairs {view | cross-sweep << 31, required line count of that view}
     unsigned* prog;           // [views * nchunks]: lines completed, cumulative over sweeps
@@ -1350,20 +1341,11 @@ __host__ __device__ inline size_t wave_words(int max_recs, int max_cells, int li
            round4(size_t(lines) + 1) + 3 * 2 * size_t(wave_cover<P>()) + size_t(wave_cover<P>()) * P;
 }
 
-constexpr int kWave1K = 24;
-constexpr int kWave1Cover = 32 * kWave1K;
-
-__host__ __device__ inline size_t wave1_words(int lines) {
-    return round4(size_t(lines) + 1) + 3 * 2 * size_t(kWave1Cover) + size_t(kWave1Cover);
-}
-
-template <int P> __host__ __device__ inline size_t wave2_words(int lines);
 size_t wave_smem_bytes(const MartArgs& m, int lines) {
     switch (m.Sp / m.nchunks) {
-        case 1: return 4 * wave1_words(lines);
         case 4: return 4 * wave_words<4>(m.max_recs, m.max_cells, lines);
-        case 8: return 4 * std::max(wave_words<8>(m.max_recs, m.max_cells, lines), wave2_words<8>(lines));
-        case 16: return 4 * std::max(wave_words<16>(m.max_recs, m.max_cells, lines), wave2_words<16>(lines));
+        case 8: return 4 * wave_words<8>(m.max_recs, m.max_cells, lines);
+        case 16: return 4 * wave_words<16>(m.max_recs, m.max_cells, lines);
         case 32: return 4 * wave_words<32>(m.max_recs, m.max_cells, lines);
         default: return 0;
     }
@@ -1617,7 +1599,9 @@ __global__ void __launch_bounds__(WaveShape<P>::G + 64, WaveShape<P>::MB) mart_w
             line_sync();  // B
             const unsigned long long p3 = prof ? gtimer() : 0;
             Scale g0, g1, g2, g3;
-            // identity Scales (no problem of the chunk updated) still hand over
+            // identity Scales (none of the thread's 4 problems updated) still
+            // hand over, and a cell handed in by the previous line is not in
+            // global memory yet: it is stored whatever this line's scales
             const bool any = W.load_scales(q, g0, g1, g2, g3);
             const uint2* e = s_ent + (j % 3) * COVER;
 #pragma unroll
@@ -1628,7 +1612,8 @@ __global__ void __launch_bounds__(WaveShape<P>::G + 64, WaveShape<P>::MB) mart_w
                 const float4 r = GW::scale4(x[i], g0, g1, g2, g3);
                 const bool hand = in && en.y != kWaveNoNext;
                 st_shared_v4_if(hand, buf + int(en.y) * TPC + q, r);
-                st_global_cg_v4_if(any && in && !hand, f4 + size_t(en.x & ~kWavePrev) * Sp4 + col4, r);
+                st_global_cg_v4_if((any || (en.x & kWavePrev)) && in && !hand,
+                                   f4 + size_t(en.x & ~kWavePrev) * Sp4 + col4, r);
             }
             // C: hand-overs visible; this line's stores ordered before the
             // factor warp's release of `done`
@@ -1664,221 +1649,9 @@ __global__ void __launch_bounds__(WaveShape<P>::G + 64, WaveShape<P>::MB) mart_w
     }
 }
 
-// Single-problem form (P = 1, e.g. one 2D slice): one updater warp per task,
-// warp-level sums (no block barriers), the factor computed by every lane, and
-// the warp publishes each line one line late (its stores have drained by
-// then, so the gpu-scope fence is short). Lines of up to 32 * K1 cells.
-
-__global__ void __launch_bounds__(64) mart_wave1_kernel(WaveArgs a) {
-    extern __shared__ __align__(16) uint32_t smem[];
-    __shared__ unsigned s_task, s_ready, s_done;
-    const unsigned L = unsigned(a.lines);
-    const int total = a.views * a.n_sweeps;
-    uint32_t* s_pos = smem;
-    uint2* s_ent = reinterpret_cast<uint2*>(s_pos + round4(size_t(L) + 1));  // [3][cover]
-    float* buf = reinterpret_cast<float*>(s_ent + 3 * kWave1Cover);          // [cover]
-    const int lane = int(threadIdx.x) & 31;
-    if (threadIdx.x == 0) {
-        s_task = atomicAdd(a.next, 1u);
-        s_ready = 0;
-        s_done = 0;
-    }
-    __syncthreads();
-    int task = int(s_task);
-    if (threadIdx.x >= 32) {
-        // ---- control warp: the lines' other-view requirements, and the
-        // publication of completed lines (one gpu-scope fence per round) ----
-        unsigned claimed = 0;
-        while (task < total) {
-            const int sweep = task / a.views, v = task % a.views;
-            const unsigned gs = a.epoch + unsigned(sweep);
-            unsigned* mine = a.prog + v;
-            const uint32_t u0 = uint32_t(v) * L;
-            if (lane == 0 && gs > 0)
-                spin_until_geq(mine, gs * L);
-            __syncwarp();
-            unsigned ready = 0, published = 0, ns = 0;
-            while (published < L) {
-                bool moved = false;
-                if (ready < L) {
-                    const unsigned j = ready + unsigned(lane);
-                    bool ok = true;
-                    const unsigned* last = nullptr;
-                    if (j < L) {
-                        const uint32_t b = __ldg(a.dep_off + u0 + j), e = __ldg(a.dep_off + u0 + j + 1);
-                        for (uint32_t k = b; k < e && ok; ++k) {
-                            const uint32_t w = __ldg(a.deps + 2 * size_t(k));
-                            const unsigned xs = w >> 31, u = w & 0x7FFFFFFFu;
-                            if (gs < xs)
-                                continue;
-                            const unsigned need = (gs - xs) * L + __ldg(a.deps + 2 * size_t(k) + 1);
-                            last = a.prog + u;
-                            ok = ld_relaxed(last) >= need;
-                        }
-                    }
-                    const unsigned bad = __ballot_sync(0xFFFFFFFFu, !ok);
-                    const unsigned adv = bad ? unsigned(__ffs(bad) - 1) : 32u;
-                    const unsigned nr = min(L, ready + adv);
-                    if (nr > ready) {
-                        if (unsigned(lane) < adv && last != nullptr)
-                            (void)ld_acquire(last);
-                        __syncwarp();
-                        ready = nr;
-                        moved = true;
-                        if (lane == 0)
-                            st_release_cta_shared(&s_ready, ready);
-                    }
-                }
-                const unsigned d = ld_acquire_cta_shared(&s_done);
-                if (d > published) {
-                    if (lane == 0) {
-                        fence_acq_rel_gpu();
-                        st_relaxed_gpu(mine, gs * L + d);
-                    }
-                    published = d;
-                    moved = true;
-                }
-                if (moved) {
-                    ns = 0;
-                } else {
-                    ns = ns ? min(ns * 2, 128u) : 16u;
-                    __nanosleep(ns);
-                }
-            }
-            if (lane == 0)
-                claimed = atomicAdd(a.next, 1u);
-            __syncthreads();  // task boundary
-            if (lane == 0) {
-                s_task = claimed;
-                s_ready = 0;
-                s_done = 0;
-            }
-            __syncthreads();
-            task = int(s_task);
-        }
-        return;
-    }
-    // ---- updater warp ----
-    float* __restrict__ f = a.m.field;
-    auto wait_ready = [&](unsigned j) {
-        if (ld_acquire_cta_shared(&s_ready) <= j) {
-            while (ld_acquire_cta_shared(&s_ready) <= j)
-                __nanosleep(16);
-        }
-    };
-    while (task < total) {
-        const int v = task % a.views;
-        const uint32_t u0 = uint32_t(v) * L;
-        for (unsigned j = unsigned(lane); j <= L; j += 32)
-            s_pos[j] = __ldg(a.pos + u0 + j);
-        __syncwarp();
-        const double pf = __ldg(a.m.p_floor);
-        const bool act = __ldg(a.m.active) != 0;
-        auto load_entries = [&](unsigned j) {
-            const uint32_t p0 = s_pos[j];
-            const int n = int(s_pos[j + 1] - p0);
-            uint2* dst = s_ent + (j % 3) * kWave1Cover;
-#pragma unroll
-            for (int i = 0; i < kWave1K; ++i) {
-                const int s = lane + 32 * i;
-                cp_async8_if(s < n, dst + s, a.ent + p0 + s);
-            }
-        };
-        // the next line's cells that this line does not cross, into
-        // registers (L2 loads: a 4-byte cp.async would go through L1, which
-        // can hold a stale copy of a cell this warp stored since)
-        float xn[kWave1K];
-        auto gather = [&](unsigned j) {
-            const int n = int(s_pos[j + 1] - s_pos[j]);
-            const uint2* e = s_ent + (j % 3) * kWave1Cover;
-#pragma unroll
-            for (int i = 0; i < kWave1K; ++i) {
-                const int s = lane + 32 * i;
-                const uint32_t c = s < n ? e[s].x : kWavePrev;
-                xn[i] = !(c & kWavePrev) ? __ldcg(f + c) : 0.f;
-            }
-        };
-        load_entries(0);
-        if (L > 1)
-            load_entries(1);
-        cp_async_commit();
-        cp_async_wait_all();
-        __syncwarp();
-        wait_ready(0);
-        gather(0);
-        float nm = __ldcs(a.m.proj + size_t(u0) * a.m.Sp);
-        for (unsigned j = 0; j < L; ++j) {
-            const int n = int(s_pos[j + 1] - s_pos[j]);
-            const double m = double(nm);
-            if (j + 1 < L)
-                nm = __ldcs(a.m.proj + size_t(u0 + j + 1) * a.m.Sp);
-            cp_async_wait_all();  // the entries of line j+1
-            __syncwarp();  // hand-overs of line j-1, entries loaded by other lanes
-            const uint2* e = s_ent + (j % 3) * kWave1Cover;
-            float x[kWave1K];
-            float part = 0.f;
-#pragma unroll
-            for (int i = 0; i < kWave1K; ++i) {
-                const int s = lane + 32 * i;
-                x[i] = s < n ? ((e[s].x & kWavePrev) ? buf[s] : xn[i]) : 0.f;
-                part += x[i];
-            }
-            double p_bar = part;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1)
-                p_bar += __shfl_xor_sync(0xFFFFFFFFu, p_bar, o);
-            __syncwarp();  // every lane has read its slots of line j
-            if (j + 2 < L)
-                load_entries(j + 2);
-            cp_async_commit();
-            bool issued = false;
-            if (j + 1 < L && ld_acquire_cta_shared(&s_ready) > j + 1) {
-                gather(j + 1);
-                issued = true;
-            }
-            // mart_update_line (solver.cpp:36-46), fp64, in every lane
-            double factor = 0;
-            if (m != 0 && act) {
-                const double ratio = m / (p_bar > pf ? p_bar : pf);
-                factor = 1.0 - a.m.beta * (1.0 - ratio);
-                if (factor <= 0) {
-                    factor = pf;
-                    if (lane == 0)
-                        atomicAdd(a.m.clamps, 1ull);
-                }
-            }
-            const bool any = factor != 0;
-            const float g = any ? float(factor) : 1.f, lb = any ? FLT_MIN : 0.f;
-#pragma unroll
-            for (int i = 0; i < kWave1K; ++i) {
-                const int s = lane + 32 * i;
-                if (s < n) {
-                    const uint2 en = e[s];
-                    const float r = fmaxf(x[i] * g, lb);
-                    if (en.y != kWaveNoNext)
-                        buf[en.y] = r;  // handed over to line j+1
-                    else if (any)
-                        __stcg(f + (en.x & ~kWavePrev), r);
-                }
-            }
-            __syncwarp();  // the line's stores and hand-overs precede `done`
-            if (lane == 0)
-                st_release_cta_shared(&s_done, j + 1);
-            if (!issued && j + 1 < L) {
-                wait_ready(j + 1);
-                gather(j + 1);
-            }
-        }
-        __syncthreads();  // task boundary
-        __syncthreads();
-        task = int(s_task);
-    }
-}
-
 template <int P>
 static void wave_launch_t(const WaveArgs& a, int sms, cudaStream_t st) {
     constexpr int NT = WaveShape<P>::G + 64;
-    // this form's own layout (wave_smem_bytes also covers the two-ahead form)
     const size_t smem = 4 * wave_words<P>(a.m.max_recs, a.m.max_cells, a.lines);
     // set once per size: changing a running kernel's attributes would wait
     // for it (uscg_reconstruct_batch overlaps neighbouring stacks' solves)
@@ -1902,426 +1675,6 @@ static void wave_launch_t(const WaveArgs& a, int sms, cudaStream_t st) {
     mart_wave_kernel<P><<<grid, NT, smem, st>>>(a);
 }
 
-// Two-ahead form (P = 8, 16): line k+1's sum is N_{k+1} + g_k * H_k, where
-// H_k is line k's sum over the cells it hands to line k+1 (before line k's
-// update) and N_{k+1} line k+1's sum over its other cells, so each line needs
-// one block reduction (of H_k and N_{k+1} together) and the factors form a
-// scalar chain. N_{k+1}'s cells are in shared memory a line early: line k+2's
-// own cells are copied during line k (three line buffers), the cells it shares
-// with line k+1 are handed over by line k+1, and those it shares only with line
-// k by line k directly. Line k's stores are issued while the factor warp works.
-// Per-cell arithmetic is the line-by-line form's (one fp32 scaling per line);
-// only p̄ is summed differently (fp64, within fp32 rounding of the others).
-constexpr uint32_t kW2Prev1 = 0x80000000u, kW2Prev2 = 0x40000000u, kW2Cell = 0x3FFFFFFFu;
-
-template <int P>
-__host__ __device__ inline size_t wave2_words(int lines) {
-    constexpr int G = WaveShape<P>::G, COVER = wave_cover<P>();
-    return round4(size_t(lines) + 1) + 5 * 2 * size_t(COVER) + 3 * size_t(COVER) * P + 4 * size_t(G / 32) * P +
-           round4(2 * size_t(P));
-}
-
-template <int P>
-__global__ void __launch_bounds__(WaveShape<P>::G + 64, 1) mart_wave2_kernel(WaveArgs a) {
-    constexpr int G = WaveShape<P>::G, V = 4, TPC = P / V, NCLV = G / TPC, KV = WaveShape<P>::KV;
-    constexpr int COVER = wave_cover<P>();
-    extern __shared__ __align__(16) uint32_t smem[];
-    __shared__ unsigned s_task, s_ready, s_done;
-    const int nchunks = a.m.nchunks;
-    const unsigned L = unsigned(a.lines);
-    const int per_sweep = a.views * nchunks;
-    const int total = per_sweep * a.n_sweeps;
-    uint32_t* s_pos = smem;
-    uint2* s_ent = reinterpret_cast<uint2*>(s_pos + round4(size_t(L) + 1));  // [5][COVER]
-    float4* bufs = reinterpret_cast<float4*>(s_ent + 5 * COVER);             // [3][COVER][TPC]
-    double* red2 = reinterpret_cast<double*>(bufs + 3 * COVER * TPC);        // [G/32][2P]: H, N
-    float2* fac = reinterpret_cast<float2*>(red2 + (G / 32) * 2 * P);       // [P]: {g, lb}
-    if (threadIdx.x == 0) {
-        s_task = atomicAdd(a.next, 1u);
-        s_ready = 0;
-        s_done = 0;
-    }
-    __syncthreads();
-    int task = int(s_task);
-    auto line_sync = [] { asm volatile("bar.sync 1, %0;" ::"n"(G + 32) : "memory"); };
-    auto upd_sync = [] { asm volatile("bar.sync 2, %0;" ::"n"(G) : "memory"); };
-    const int warp_id = int(threadIdx.x) / 32, lane = int(threadIdx.x) & 31;
-    if (warp_id == G / 32) {
-        // ---- factor warp ----
-        while (task < total) {
-            const int v = (task % per_sweep) / nchunks, chunk = task % nchunks;
-            const uint32_t u0 = uint32_t(v) * L;
-            double pf = 0;
-            bool act = false;
-            if (lane < P) {
-                pf = __ldg(a.m.p_floor + size_t(chunk) * P + lane);
-                act = __ldg(a.m.active + size_t(chunk) * P + lane) != 0;
-            }
-            double gk = 1.0;
-            auto factor = [&](double p_bar, float m) {
-                float g = 1.f, lb = 0.f;
-                if (lane < P && m != 0.f && act) {
-                    const double ratio = double(m) / (p_bar > pf ? p_bar : pf);
-                    double f = 1.0 - a.m.beta * (1.0 - ratio);
-                    if (f <= 0) {
-                        f = pf;
-                        atomicAdd(a.m.clamps + size_t(chunk) * P + lane, 1ull);
-                    }
-                    g = float(f);
-                    lb = FLT_MIN;
-                }
-                if (lane < P)
-                    fac[lane] = make_float2(g, lb);
-                gk = double(g);
-            };
-            auto meas = [&](unsigned j) {
-                return lane < P ? __ldcs(a.m.proj + size_t(u0 + j) * a.m.Sp + size_t(chunk) * P + lane) : 0.f;
-            };
-            float nm = meas(0);
-            line_sync();  // A: line 0's sum (N slots)
-            {
-                double p_bar = 0;
-                if (lane < P)
-                    for (int w = 0; w < G / 32; ++w)
-                        p_bar += red2[w * 2 * P + P + lane];
-                factor(p_bar, nm);
-            }
-            if (L > 1)
-                nm = meas(1);
-            line_sync();  // B: g_0
-            for (unsigned k = 0; k < L; ++k) {
-                line_sync();  // A: H_k, N_{k+1}; line k's hand-overs written
-                if (k + 1 < L) {
-                    double h = 0, n = 0;
-                    if (lane < P)
-                        for (int w = 0; w < G / 32; ++w) {
-                            h += red2[w * 2 * P + lane];
-                            n += red2[w * 2 * P + P + lane];
-                        }
-                    factor(n + gk * h, nm);
-                    if (k + 2 < L)
-                        nm = meas(k + 2);
-                }
-                line_sync();  // B: line k's stores issued; g_{k+1} in fac
-                if (lane == 0)
-                    st_release_cta_shared(&s_done, k + 1);
-            }
-            __syncthreads();  // task boundary (the control warp hands out the ticket between)
-            __syncthreads();
-            task = int(s_task);
-        }
-        return;
-    }
-    if (warp_id == G / 32 + 1) {
-        // ---- control warp: requirements and publication (as mart_wave_kernel) ----
-        unsigned claimed = 0;
-        while (task < total) {
-            const int sweep = task / per_sweep;
-            const int v = (task % per_sweep) / nchunks, chunk = task % nchunks;
-            const unsigned gs = a.epoch + unsigned(sweep);
-            unsigned* mine = a.prog + size_t(v) * nchunks + chunk;
-            const uint32_t u0 = uint32_t(v) * L;
-            if (lane == 0 && gs > 0)
-                spin_until_geq(mine, gs * L);
-            __syncwarp();
-            unsigned ready = 0, published = 0, ns = 0;
-            while (published < L) {
-                bool moved = false;
-                if (ready < L) {
-                    const unsigned j = ready + unsigned(lane);
-                    bool ok = true;
-                    const unsigned* last = nullptr;
-                    if (j < L) {
-                        const uint32_t b = __ldg(a.dep_off + u0 + j), e = __ldg(a.dep_off + u0 + j + 1);
-                        for (uint32_t k = b; k < e && ok; ++k) {
-                            const uint32_t w = __ldg(a.deps + 2 * size_t(k));
-                            const unsigned xs = w >> 31, u = w & 0x7FFFFFFFu;
-                            if (gs < xs)
-                                continue;
-                            const unsigned need = (gs - xs) * L + __ldg(a.deps + 2 * size_t(k) + 1);
-                            last = a.prog + size_t(u) * nchunks + chunk;
-                            ok = ld_relaxed(last) >= need;
-                        }
-                    }
-                    const unsigned bad = __ballot_sync(0xFFFFFFFFu, !ok);
-                    const unsigned adv = bad ? unsigned(__ffs(bad) - 1) : 32u;
-                    const unsigned nr = min(L, ready + adv);
-                    if (nr > ready) {
-                        if (unsigned(lane) < adv && last != nullptr)
-                            (void)ld_acquire(last);
-                        __syncwarp();
-                        ready = nr;
-                        moved = true;
-                        if (lane == 0)
-                            st_release_cta_shared(&s_ready, ready);
-                    }
-                }
-                const unsigned d = ld_acquire_cta_shared(&s_done);
-                if (d > published) {
-                    if (lane == 0) {
-                        fence_acq_rel_gpu();
-                        st_relaxed_gpu(mine, gs * L + d);
-                    }
-                    published = d;
-                    moved = true;
-                }
-                if (moved) {
-                    ns = 0;
-                } else {
-                    ns = ns ? min(ns * 2, 128u) : 16u;
-                    __nanosleep(ns);
-                }
-            }
-            if (lane == 0)
-                claimed = atomicAdd(a.next, 1u);
-            __syncthreads();  // task boundary
-            if (lane == 0) {
-                s_task = claimed;
-                s_ready = 0;
-                s_done = 0;
-            }
-            __syncthreads();
-            task = int(s_task);
-        }
-        return;
-    }
-    // ---- updaters ----
-    const int t = int(threadIdx.x);
-    const int q = t % TPC, cl = t / TPC;
-    float4* __restrict__ f4 = reinterpret_cast<float4*>(a.m.field);
-    const uint32_t Sp4 = uint32_t(a.m.Sp) / V;
-    auto wait_ready = [&](unsigned j) {
-        if (ld_acquire_cta_shared(&s_ready) <= j) {
-            while (ld_acquire_cta_shared(&s_ready) <= j)
-                __nanosleep(16);
-        }
-    };
-    auto warp_sums = [&](double& s0, double& s1, double& s2, double& s3) {
-#pragma unroll
-        for (int o = TPC; o < 32; o <<= 1) {
-            s0 += __shfl_xor_sync(0xFFFFFFFFu, s0, o);
-            s1 += __shfl_xor_sync(0xFFFFFFFFu, s1, o);
-            s2 += __shfl_xor_sync(0xFFFFFFFFu, s2, o);
-            s3 += __shfl_xor_sync(0xFFFFFFFFu, s3, o);
-        }
-    };
-    while (task < total) {
-        const int v = (task % per_sweep) / nchunks, chunk = task % nchunks;
-        const uint32_t u0 = uint32_t(v) * L;
-        const uint32_t col4 = (uint32_t(chunk) * P) / V + uint32_t(q);
-        for (unsigned j = unsigned(t); j <= L; j += G)
-            s_pos[j] = __ldg(a.pos + u0 + j);
-        upd_sync();
-        auto lnum = [&](unsigned j) { return int(s_pos[j + 1] - s_pos[j]); };
-        auto load_entries = [&](unsigned j) {
-            const uint32_t p0 = s_pos[j];
-            const int n = int(s_pos[j + 1] - p0);
-            uint2* dst = s_ent + (j % 5) * COVER;
-#pragma unroll
-            for (int i = 0; i < KV; ++i) {
-                const int s = cl + i * NCLV;
-                cp_async8_if(q == 0 && s < n, dst + s, a.ent2 + p0 + s);
-            }
-        };
-        // line j's cells not handed over (by line j-1 or j-2): own slots
-        auto gather = [&](unsigned j) {
-            const int n = lnum(j);
-            const uint2* e = s_ent + (j % 5) * COVER;
-            float4* b = bufs + (j % 3) * COVER * TPC;
-#pragma unroll
-            for (int i = 0; i < KV; ++i) {
-                const int s = cl + i * NCLV;
-                const uint32_t c = s < n ? e[s].x : kW2Prev1;
-                cp_async16_if(!(c & (kW2Prev1 | kW2Prev2)), b + s * TPC + q, f4 + size_t(c & kW2Cell) * Sp4 + col4);
-            }
-        };
-        // prologue: entries of lines 0..3, lines 0 and 1's own cells, line 0's sum
-        for (unsigned j = 0; j < 4 && j < L; ++j)
-            load_entries(j);
-        cp_async_commit();
-        cp_async_wait_all();
-        upd_sync();
-        wait_ready(L > 1 ? 1 : 0);
-        gather(0);
-        if (L > 1)
-            gather(1);
-        cp_async_commit();
-        cp_async_wait_all();
-        {
-            const int n = lnum(0);
-            float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
-#pragma unroll
-            for (int i = 0; i < KV; ++i) {
-                const int s = cl + i * NCLV;
-                if (s < n) {
-                    const float4 x = bufs[s * TPC + q];
-                    a0 += x.x;
-                    a1 += x.y;
-                    a2 += x.z;
-                    a3 += x.w;
-                }
-            }
-            double s0 = a0, s1 = a1, s2 = a2, s3 = a3;
-            warp_sums(s0, s1, s2, s3);
-            if ((t & 31) < TPC) {
-                double* r = red2 + (t >> 5) * 2 * P + P + q * V;
-                r[0] = s0;
-                r[1] = s1;
-                r[2] = s2;
-                r[3] = s3;
-            }
-        }
-        line_sync();  // A: line 0's sum
-        line_sync();  // B: g_0
-        for (unsigned k = 0; k < L; ++k) {
-            const int n = lnum(k);
-            const bool more = k + 1 < L;
-            const float4* bk = bufs + (k % 3) * COVER * TPC;
-            float4* bk1 = bufs + ((k + 1) % 3) * COVER * TPC;
-            float4* bk2 = bufs + ((k + 2) % 3) * COVER * TPC;
-            // (a) entries of line k+4 (two iterations before first use: the
-            // loads complete before the barriers that show them to the
-            // cell's other threads), then line k+2's own cells (its buffer
-            // held line k-1, read an iteration ago; its cells that lines k+1
-            // and k do not cross were stored at line k-1 or earlier, before B)
-            if (k + 4 < L)
-                load_entries(k + 4);
-            cp_async_commit();
-            bool issued = false;
-            if (k + 2 < L && ld_acquire_cta_shared(&s_ready) > k + 2) {
-                gather(k + 2);
-                issued = true;
-            }
-            cp_async_commit();
-            // (b) line k: scale by g_k, hand over (1 or 2 lines ahead); H_k
-            float g[4], lb[4];
-            {
-                const float4 u = reinterpret_cast<const float4*>(fac)[2 * q];
-                const float4 w = reinterpret_cast<const float4*>(fac)[2 * q + 1];
-                g[0] = u.x; lb[0] = u.y; g[1] = u.z; lb[1] = u.w;
-                g[2] = w.x; lb[2] = w.y; g[3] = w.z; lb[3] = w.w;
-            }
-            const bool any = (lb[0] + lb[1] + lb[2] + lb[3]) != 0.f;
-            const uint2* e = s_ent + (k % 5) * COVER;
-            float4 r[KV];
-            float h0 = 0.f, h1 = 0.f, h2 = 0.f, h3 = 0.f;
-#pragma unroll
-            for (int i = 0; i < KV; ++i) {
-                const int s = cl + i * NCLV;
-                const bool in = s < n;
-                const float4 x = in ? bk[s * TPC + q] : make_float4(0.f, 0.f, 0.f, 0.f);
-                const uint2 en = e[in ? s : 0];
-                const uint32_t n1 = en.y & 0xFFFFu, n2 = en.y >> 16;
-                r[i] = make_float4(fmaxf(x.x * g[0], lb[0]), fmaxf(x.y * g[1], lb[1]), fmaxf(x.z * g[2], lb[2]),
-                                   fmaxf(x.w * g[3], lb[3]));
-                const bool h1p = in && n1 != kWaveNoNext;
-                const bool h2p = in && !h1p && n2 != kWaveNoNext;
-                if (h1p) {
-                    h0 += x.x;
-                    h1 += x.y;
-                    h2 += x.z;
-                    h3 += x.w;
-                }
-                st_shared_v4_if(h1p, bk1 + int(n1) * TPC + q, r[i]);
-                st_shared_v4_if(h2p, bk2 + int(n2) * TPC + q, r[i]);
-            }
-            // (c) N_{k+1}: line k+1's own cells (copied an iteration ago)
-            // and those line k-1 handed over two ahead
-            float n0 = 0.f, nn1 = 0.f, n2 = 0.f, n3 = 0.f;
-            if (more) {
-                // all but this iteration's two groups: line k+1's copies and
-                // the entries of line k+3
-                asm volatile("cp.async.wait_group 2;" ::: "memory");
-                const int m1 = lnum(k + 1);
-                const uint2* e1 = s_ent + ((k + 1) % 5) * COVER;
-#pragma unroll
-                for (int i = 0; i < KV; ++i) {
-                    const int s = cl + i * NCLV;
-                    if (s < m1 && !(e1[s].x & kW2Prev1)) {
-                        const float4 x = bk1[s * TPC + q];
-                        n0 += x.x;
-                        nn1 += x.y;
-                        n2 += x.z;
-                        n3 += x.w;
-                    }
-                }
-            }
-            {
-                double s0 = h0, s1 = h1, s2 = h2, s3 = h3;
-                double t0 = n0, t1 = nn1, t2 = n2, t3 = n3;
-                warp_sums(s0, s1, s2, s3);
-                warp_sums(t0, t1, t2, t3);
-                if ((t & 31) < TPC) {
-                    double* rr = red2 + (t >> 5) * 2 * P + q * V;
-                    rr[0] = s0;
-                    rr[1] = s1;
-                    rr[2] = s2;
-                    rr[3] = s3;
-                    rr[P + 0] = t0;
-                    rr[P + 1] = t1;
-                    rr[P + 2] = t2;
-                    rr[P + 3] = t3;
-                }
-            }
-            line_sync();  // A
-            // (d) line k's stores (cells handed to neither next line) while
-            // the factor warp forms g_{k+1}
-#pragma unroll
-            for (int i = 0; i < KV; ++i) {
-                const int s = cl + i * NCLV;
-                const bool in = s < n;
-                const uint2 en = e[in ? s : 0];
-                st_global_cg_v4_if(any && in && en.y == 0xFFFFFFFFu, f4 + size_t(en.x & kW2Cell) * Sp4 + col4, r[i]);
-            }
-            line_sync();  // B: stores issued (before `done`), g_{k+1}, hand-overs visible
-            if (!issued && k + 2 < L) {
-                wait_ready(k + 2);
-                gather(k + 2);
-                cp_async_commit();
-            }
-        }
-        __syncthreads();  // task boundary (the control warp hands out the ticket between)
-        __syncthreads();
-        task = int(s_task);
-    }
-}
-
-template <int P>
-static void wave2_launch(const WaveArgs& a, int sms, cudaStream_t st) {
-    constexpr int NT = WaveShape<P>::G + 64;
-    const size_t smem = 4 * wave2_words<P>(a.lines);
-    UB_CUDA(cudaFuncSetAttribute(mart_wave2_kernel<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-    int per_sm = 0;
-    UB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, mart_wave2_kernel<P>, NT, smem));
-    if (per_sm < 1)
-        throw CudaError("mart_wave2_kernel cannot be resident");
-    if (const char* e = std::getenv("USCG_WAVE_PER_SM"))
-        per_sm = std::max(1, std::min(per_sm, std::atoi(e)));
-    const int total = a.views * a.m.nchunks * a.n_sweeps;
-    const int grid = std::min(total, sms * per_sm);
-    if (const char* e = std::getenv("USCG_FLOW_VERBOSE"); e && std::atoi(e))
-        std::fprintf(stderr, "mart_wave_kernel: P=%d (two-ahead) grid=%d per_sm=%d smem=%zu tasks=%d\n", P, grid,
-                     per_sm, smem, total);
-    mart_wave2_kernel<P><<<grid, NT, smem, st>>>(a);
-}
-
-static void wave1_launch(const WaveArgs& a, int sms, cudaStream_t st) {
-    const size_t smem = wave_smem_bytes(a.m, a.lines);
-    UB_CUDA(cudaFuncSetAttribute(mart_wave1_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-    int per_sm = 0;
-    UB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, mart_wave1_kernel, 64, smem));
-    if (per_sm < 1)
-        throw CudaError("mart_wave1_kernel cannot be resident");
-    if (const char* e = std::getenv("USCG_WAVE_PER_SM"))
-        per_sm = std::max(1, std::min(per_sm, std::atoi(e)));
-    const int total = a.views * a.n_sweeps;
-    const int grid = std::min(total, sms * per_sm);
-    if (const char* e = std::getenv("USCG_FLOW_VERBOSE"); e && std::atoi(e))
-        std::fprintf(stderr, "mart_wave_kernel: P=1 grid=%d per_sm=%d smem=%zu tasks=%d\n", grid, per_sm, smem,
-                     total);
-    mart_wave1_kernel<<<grid, 64, smem, st>>>(a);
-}
-
 bool wave_supported(const MartArgs& h) {
     int optin = 0, dev = 0;
     if (cudaGetDevice(&dev) != cudaSuccess ||
@@ -2330,7 +1683,6 @@ bool wave_supported(const MartArgs& h) {
     const int P = h.Sp / h.nchunks;
     int cover = 0;
     switch (P) {
-        case 1: cover = h.Sp == 1 ? kWave1Cover : 0; break;
         case 4: cover = wave_cover<4>(); break;
         case 8: cover = wave_cover<8>(); break;
         case 16: cover = wave_cover<16>(); break;
@@ -2361,7 +1713,6 @@ void launch_mart_wave(const MartArgs& h, const WaveSchedule& ws, unsigned* prog,
     a.m = h;
     a.pos = ws.pos;
     a.ent = ws.ent;
-    a.ent2 = ws.ent2;
     a.dep_off = ws.dep_off;
     a.deps = ws.deps;
     a.prog = prog;
@@ -2372,131 +1723,17 @@ void launch_mart_wave(const MartArgs& h, const WaveSchedule& ws, unsigned* prog,
     a.lines = ws.lines;
     a.prof = prof;
     UB_CUDA(cudaMemsetAsync(next, 0, sizeof(unsigned), st));
-    // USCG_WAVE_TWO=1: the two-ahead form for 8 / 16-problem chunks
-    // (parity-green; measured slower on C2: DESIGN.md §4.4)
-    const char* w2 = std::getenv("USCG_WAVE_TWO");
-    const bool two = (w2 ? std::atoi(w2) != 0 : false) && ws.ent2 != nullptr;
     switch (h.Sp / h.nchunks) {
-        case 1: wave1_launch(a, sms, st); break;
         case 4: wave_launch_t<4>(a, sms, st); break;
-        case 8: two ? wave2_launch<8>(a, sms, st) : wave_launch_t<8>(a, sms, st); break;
-        case 16: two ? wave2_launch<16>(a, sms, st) : wave_launch_t<16>(a, sms, st); break;
+        case 8: wave_launch_t<8>(a, sms, st); break;
+        case 16: wave_launch_t<16>(a, sms, st); break;
         case 32: wave_launch_t<32>(a, sms, st); break;
-        default: throw CudaError("mart_wave_kernel supports problem chunks of 1 (one problem), 4, 8, 16 or 32");
+        default: throw CudaError("mart_wave_kernel supports problem chunks of 4, 8, 16 or 32");
     }
     count_launch();
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess)
         throw CudaError(std::string("mart_wave_kernel launch: ") + cudaGetErrorString(e));
-}
-
-// ============================================================================
-// level-barrier executor
-// ============================================================================
-
-struct SweepArgs {
-    MartArgs m;
-    const uint32_t* order;
-    const uint32_t* level_off;
-    int levels;
-    unsigned* bar;
-    int n_rings;
-    unsigned long long* prof;  // optional: per level 4 globaltimer stamps of CTA 0
-};
-
-template <int P>
-__global__ void __launch_bounds__(CTA, 1) mart_sweep_kernel(SweepArgs a) {
-    extern __shared__ __align__(16) uint32_t smem[];
-    stage_rings(smem, a.m.tr.rings, a.n_rings);
-    __syncthreads();
-    GroupWorker<P, TG> W(a.m, smem, a.n_rings, true, 1);
-    const int nchunks = a.m.nchunks;
-    const int NG = gridDim.x * (CTA / TG);
-    const int gid = blockIdx.x * (CTA / TG) + int(threadIdx.x) / TG;
-    auto ntasks = [&](int lev) {
-        return int(__ldg(a.level_off + lev + 1) - __ldg(a.level_off + lev)) * nchunks;
-    };
-    auto prepare = [&](int lev, int task) {
-        const uint32_t unit = __ldg(a.order + __ldg(a.level_off + lev) + task / nchunks);
-        W.prepare(unit, task % nchunks);
-    };
-    const bool stamp = a.prof != nullptr && blockIdx.x == 0 && threadIdx.x == 0;
-    if (a.levels > 0 && gid < ntasks(0))
-        prepare(0, gid);
-    for (int lev = 0; lev < a.levels; ++lev) {
-        if (stamp)
-            a.prof[4 * lev + 0] = gtimer();
-        const int nt = ntasks(lev);
-        for (int task = gid; task < nt; task += NG) {
-            if (task != gid) {
-                W.sy.sync();  // previous update done with the group's smem
-                prepare(lev, task);
-            }
-            W.update();
-        }
-        if (lev + 1 == a.levels)
-            break;
-        // grid barrier, split: arrive, prepare the next task, wait
-        __syncthreads();
-        if (stamp)
-            a.prof[4 * lev + 1] = gtimer();
-        if (threadIdx.x == 0) {
-            __threadfence();
-            atomicAdd(a.bar, 1u);
-        }
-        if (gid < ntasks(lev + 1))
-            prepare(lev + 1, gid);
-        if (stamp)
-            a.prof[4 * lev + 2] = gtimer();
-        if (threadIdx.x == 0) {
-            const unsigned target = unsigned(lev + 1) * gridDim.x;
-            while (ld_relaxed(a.bar) < target) {
-            }
-            __threadfence();
-        }
-        if (stamp)
-            a.prof[4 * lev + 3] = gtimer();
-        __syncthreads();
-    }
-}
-
-template <int P>
-static void sweep_launch_t(const SweepArgs& a, size_t smem, int grid, cudaStream_t st) {
-    UB_CUDA(cudaFuncSetAttribute(mart_sweep_kernel<P>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 int(smem)));
-    int per_sm = 0;
-    UB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, mart_sweep_kernel<P>, CTA, smem));
-    if (per_sm < 1)
-        throw CudaError("mart_sweep_kernel cannot be resident (shared memory too large)");
-    void* args[] = {const_cast<SweepArgs*>(&a)};
-    UB_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(mart_sweep_kernel<P>), dim3(grid),
-                                        dim3(CTA), args, smem, st));
-}
-
-void launch_mart_sweep(const MartArgs& h, const uint32_t* order, const uint32_t* level_off,
-                       int levels, unsigned* bar, int n_rings, cudaStream_t st,
-                       unsigned long long* prof) {
-    int dev = 0, sms = 0;
-    UB_CUDA(cudaGetDevice(&dev));
-    UB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    SweepArgs a;
-    a.m = h;
-    a.order = order;
-    a.level_off = level_off;
-    a.levels = levels;
-    a.bar = bar;
-    a.n_rings = n_rings;
-    a.prof = prof;
-    UB_CUDA(cudaMemsetAsync(bar, 0, sizeof(unsigned), st));
-    const size_t smem = sweep_smem_bytes(h, n_rings);
-    switch (h.Sp / h.nchunks) {
-        case 1: sweep_launch_t<1>(a, smem, sms, st); break;
-        case 2: sweep_launch_t<2>(a, smem, sms, st); break;
-        case 4: sweep_launch_t<4>(a, smem, sms, st); break;
-        case 8: sweep_launch_t<8>(a, smem, sms, st); break;
-        default: throw CudaError("mart_sweep_kernel supports problem chunks of at most 8");
-    }
-    count_launch();
 }
 
 }  // namespace ub

@@ -18,6 +18,7 @@ Inputs are the bench's own: seeded phantoms (workloads.phantom_fields), binary
 projections of them, the configuration's noise.
 """
 import dataclasses
+import os
 import threading
 
 import numpy as np
@@ -130,15 +131,17 @@ def test_c2_verbatim_wave_twenty_sweeps(ub, orc, capfd, monkeypatch):
     proj = workloads.add_noise(wl, ub.project_stack(tr, truth.astype(np.float32))).astype(np.float32)
     out = ub.reconstruct_stack(proj, ub.SolverConfig(beta=wl.beta, tolerance=0, max_sweeps=wl.sweeps), tr,
                                with_crossed=True)
-    assert "mart_wave_kernel: P=32 " in capfd.readouterr().err
+    if os.environ.get("USCG_MART_MODE", "auto") in ("auto", "wave"):
+        assert "mart_wave_kernel: P=32 " in capfd.readouterr().err
     counts = tr.trace_counts().reshape(-1).astype(np.int64)
     for p in range(S):
         nz = proj[p].reshape(-1) != 0
         assert out[p][1].updates == int(counts[nz].sum()) * wl.sweeps, p
-        assert out[p][1].zero_measurement_skips == int((~nz).sum()), p
+        assert out[p][1].zero_measurement_skips == int((~nz).sum()) * wl.sweeps, p
     pick = [0, 31, 77, 127]
     g, src, det = _oracle_side(orc, spec, geom)
     ref = _oracle_many(orc, g, src, det, geom.thetas(), [proj[p] for p in pick], wl.beta, wl.sweeps)
+    print("c2 max rel per problem:", {p: _maxrel(out[p][0], want) for p, (want, _) in zip(pick, ref)})
     for p, (want, wrep) in zip(pick, ref):
         got, rep = out[p]
         _check_report(rep, wrep)

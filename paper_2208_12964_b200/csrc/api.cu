@@ -163,6 +163,11 @@ struct uscg_tracer_s {
     DevBuf<uint32_t> d_lists;
     DevBuf<unsigned long long> d_lpos;
     double lists_seconds = 0;
+    // tile executor (one small problem): the lines in ASAP level order
+    bool tile_built = false, tile_off = false;
+    DevBuf<uint4> d_tmeta;
+    DevBuf<uint32_t> d_tlevel;
+    int tile_levels = 0;
     // MART workspace
     DevBuf<MartArgs> d_args;
     DevBuf<float> w_field, w_proj, w_prev, w_stage;
@@ -565,9 +570,11 @@ void ensure_crossed(uscg_tracer_s* t) {
 
 // MART executor (USCG_MART_MODE): 0 "flow" dataflow over run dependency
 // counters; 3 "wave" one task per (view, problem chunk) ordered by per-view
-// progress counters (2D stacks). Unset: "auto" (-1), the wave executor where
-// it applies (2D grid, chunks of 4-32 problems, lines within its cover, the
-// traced lists within a memory budget), else flow.
+// progress counters (2D stacks); 4 "tile" one CTA with the field in shared
+// memory (one small problem). Unset: "auto" (-1), the wave executor where it
+// applies (2D grid, chunks of 4-32 problems, lines within its cover, the
+// traced lists within a memory budget), the tile executor for one problem
+// whose field and line metadata fit in shared memory, else flow.
 int mart_mode() {
     const char* e = std::getenv("USCG_MART_MODE");
     const std::string m = e ? e : "auto";
@@ -575,6 +582,8 @@ int mart_mode() {
         return 0;
     if (m == "wave")
         return 3;
+    if (m == "tile")
+        return 4;
     return -1;
 }
 
@@ -871,6 +880,60 @@ void build_lists(uscg_tracer_s* t) {
         std::fprintf(stderr, "flow lists: %llu entries, %.3f s\n", (unsigned long long)total, t->lists_seconds);
 }
 
+// The tile executor's schedule (mart_tile.cu): every line's ASAP level within
+// a sweep (level = 1 + the largest level of an earlier line sharing a cell),
+// lines sorted by level. Geometry only, built once per tracer from the traced
+// lists; small problems only (tile_fits).
+bool build_tile(uscg_tracer_s* t) {
+    if (t->tile_built || t->tile_off)
+        return t->tile_built;
+    const uint64_t units = t->units(), total = t->cells_per_sweep;
+    if (units >= (uint64_t(1) << 24) || total >= (uint64_t(1) << 32) ||
+        !tile_fits(t->cells, int(units), 1)) {
+        t->tile_off = true;
+        return false;
+    }
+    build_lists(t);
+    if (!t->lists_built) {
+        t->tile_off = true;
+        return false;
+    }
+    std::vector<unsigned long long> lpos(units + 1);
+    std::vector<uint32_t> idx(std::max<uint64_t>(total, 1));
+    UB_CUDA(cudaMemcpy(lpos.data(), t->d_lpos.p, sizeof(unsigned long long) * lpos.size(), cudaMemcpyDeviceToHost));
+    UB_CUDA(cudaMemcpy(idx.data(), t->d_lists.p, sizeof(uint32_t) * total, cudaMemcpyDeviceToHost));
+    std::vector<uint32_t> last(t->cells, 0), level(units);
+    uint32_t levels = 0;
+    for (uint64_t u = 0; u < units; ++u) {
+        uint32_t lev = 0;
+        for (uint64_t k = lpos[u]; k < lpos[u + 1]; ++k)
+            lev = std::max(lev, last[idx[k]]);
+        ++lev;
+        for (uint64_t k = lpos[u]; k < lpos[u + 1]; ++k)
+            last[idx[k]] = lev;
+        level[u] = lev - 1;
+        levels = std::max(levels, lev);
+    }
+    if (!tile_fits(t->cells, int(units), int(levels))) {
+        t->tile_off = true;
+        return false;
+    }
+    std::vector<uint32_t> off(levels + 1, 0);
+    for (uint64_t u = 0; u < units; ++u)
+        ++off[level[u] + 1];
+    for (uint32_t l = 0; l < levels; ++l)
+        off[l + 1] += off[l];
+    std::vector<uint4> meta(units);
+    std::vector<uint32_t> fill(off.begin(), off.end() - 1);
+    for (uint64_t u = 0; u < units; ++u)
+        meta[fill[level[u]]++] = make_uint4(uint32_t(u), uint32_t(lpos[u]), uint32_t(lpos[u + 1] - lpos[u]), 0u);
+    upload(t->d_tmeta, meta);
+    upload(t->d_tlevel, off);
+    t->tile_levels = int(levels);
+    t->tile_built = true;
+    return true;
+}
+
 }  // namespace
 
 extern "C" {
@@ -1121,7 +1184,8 @@ uscg_status uscg_tracer_get_info(uscg_tracer t, uscg_tracer_info* info) {
         info->executor_bytes = t->d_lists.bytes() + t->d_lpos.bytes() + t->d_went.bytes() +
                                t->d_wpos.bytes() + t->d_wdep_off.bytes() + t->d_wdeps.bytes() +
                                t->d_order.bytes() + t->d_pred_off.bytes() + t->d_preds.bytes() +
-                               t->d_succ_off.bytes() + t->d_succs.bytes() + t->d_npred_x.bytes();
+                               t->d_succ_off.bytes() + t->d_succs.bytes() + t->d_npred_x.bytes() +
+                               t->d_tmeta.bytes() + t->d_tlevel.bytes();
     });
 }
 
@@ -1466,12 +1530,13 @@ static void reconstruct_body(uscg_tracer t, const float* proj, int32_t problems,
     t->d_args.ensure(1);
     UB_CUDA(cudaMemcpyAsync(t->d_args.p, &h, sizeof(MartArgs), cudaMemcpyHostToDevice, st));
     int exec_mode = mart_mode();
-    // auto: the wave executor for stacks (P >= 4); for one problem the flow
-    // executor's 4-line runs measure faster on C1 (0.93 vs 1.03 ms per
-    // iteration), so the single-warp wave form runs only when requested
+    // auto: the wave executor for stacks (P >= 4); the tile executor for one
+    // problem that fits in one CTA's shared memory; else flow
     if ((exec_mode == -1 && P >= 4) || exec_mode == 3)
         exec_mode = wave_fits(t) && wave_supported(h) && wave_fits_smem(h, t->lines) ? 3 : 0;
-    else if (exec_mode == -1)
+    else if ((exec_mode == -1 || exec_mode == 4) && Sp == 1)
+        exec_mode = build_tile(t) ? 4 : 0;
+    else if (exec_mode == -1 || exec_mode == 4)
         exec_mode = 0;
     t->executor = exec_mode;
     if (exec_mode == 3) {
@@ -1541,6 +1606,15 @@ static void reconstruct_body(uscg_tracer t, const float* proj, int32_t problems,
                     std::fclose(fp);
                 }
             }
+        } else if (exec_mode == 4) {
+            n_run = track ? 1 : cfg->max_sweeps - sweep;
+            TileSchedule ts;
+            ts.meta = t->d_tmeta.p;
+            ts.level_off = t->d_tlevel.p;
+            ts.lists = t->d_lists.p;
+            ts.units = int(units);
+            ts.levels = t->tile_levels;
+            launch_mart_tile(h, ts, cells, n_run, st);
         } else if (exec_mode == 0) {
             // without a per-sweep residual every remaining sweep runs in one
             // launch, back to back (cross-sweep dependencies)
@@ -1811,7 +1885,9 @@ uscg_status uscg_reconstruct_batch(uscg_tracer t, int32_t batch, const float* co
         // stack b-1's download is queued only once stack b's solve is launched:
         // the solve's small host reads (validation statistics) would otherwise
         // wait behind it on the copy engine, serializing download and solve
+        int queued_down = 0;  // stacks [0, queued_down) have their download queued
         auto download = [&](int b) {
+            queued_down = b + 1;
             UB_CUDA(cudaStreamWaitEvent(t->copy_out, ev_ready[b], 0));
             const float* src = inter ? in[b % 2].p + pw : out[b % 2].p;
             UB_CUDA(cudaMemcpyAsync(field_inout[b], src, sizeof(float) * fw, cudaMemcpyDeviceToHost,
@@ -1825,16 +1901,26 @@ uscg_status uscg_reconstruct_batch(uscg_tracer t, int32_t batch, const float* co
         // drained, so the wave's ramp and drain of neighbouring stacks overlap
         const bool overlap = batch > 1 && overlap_solves(t, S, cfg);
         std::vector<std::function<void()>> fin(batch);
+        std::vector<char> fin_done(batch, 0);
+        auto finish = [&](int b) {
+            if (fin[b] && !fin_done[b]) {
+                fin_done[b] = 1;
+                fin[b]();
+            }
+        };
         cudaStream_t orig = t->ctx->stream;
         if (overlap)
             for (auto& sl : t->slots)
                 if (!sl.st)
                     UB_CUDA(cudaStreamCreateWithFlags(&sl.st, cudaStreamNonBlocking));
+        int failed = batch;  // the stack being solved when an error is thrown
+        try {
         upload(0);
         for (int b = 0; b < batch; ++b) {
+            failed = b;
             const int k = b % 2;
             if (overlap && b >= 2)
-                fin[b - 2]();  // stack b-2 (this slot's previous solve) finished
+                finish(b - 2);  // stack b-2 (this slot's previous solve) finished
 
             struct SlotIn {  // the slot's workspaces and stream, swapped in for this solve
                 uscg_tracer_s* t;
@@ -1882,9 +1968,27 @@ uscg_status uscg_reconstruct_batch(uscg_tracer t, int32_t batch, const float* co
             }
             UB_CUDA(cudaEventRecord(ev_ready[b], cur));
         }
+        } catch (...) {
+            // the stacks solved before the failing one still deliver their
+            // fields and reports, and no copy or solve is left in flight
+            try {
+                for (int b = 0; b < failed; ++b)
+                    finish(b);
+                for (int b = queued_down; b < failed; ++b)
+                    download(b);
+                cudaStreamSynchronize(t->copy_out);
+                cudaStreamSynchronize(t->copy_in);
+                for (auto& sl : t->slots)
+                    if (sl.st)
+                        cudaStreamSynchronize(sl.st);
+                cudaStreamSynchronize(st);
+            } catch (...) {
+            }
+            throw;
+        }
         if (overlap)
             for (int b = std::max(0, batch - 2); b < batch; ++b)
-                fin[b]();
+                finish(b);
         download(batch - 1);
         // the context stream ends after the last download (callers time on it)
         UB_CUDA(cudaStreamWaitEvent(st, ev_out[batch - 1], 0));

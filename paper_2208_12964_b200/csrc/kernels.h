@@ -78,6 +78,20 @@ void launch_project_length(const DevGrid& g, int lines, int views, const double*
 void launch_project(const TraceArgs& A, int views, const float* field, int Sp, int max_recs,
                     int max_cells, float* out, cudaStream_t st);
 
+// K3 for one small problem (mart_tile.cu): one CTA, the field in shared
+// memory, the lines of each ASAP level in parallel (one warp per line), a
+// block barrier between levels.
+struct TileSchedule {
+    const uint4* meta;         // [units] in level order: {unit, list offset, cells, 0}
+    const uint32_t* level_off; // [levels + 1] slots per level (one sweep)
+    const uint32_t* lists;     // traced index lists (offsets below 2^32)
+    int units;
+    int levels;
+};
+size_t tile_smem_bytes(uint64_t cells, int units, int levels);
+bool tile_fits(uint64_t cells, int units, int levels);
+void launch_mart_tile(const MartArgs& h, const TileSchedule& ts, uint64_t cells, int sweeps, cudaStream_t st);
+
 // Ring of traced index lists shared by the chunk tasks of a unit:
 // slot = [n, idx[0..n)], slot_words >= max_cells + 1.
 struct FlowSlab {

@@ -29,12 +29,33 @@
 #include <cstdint>
 #include <cstdio>
 #include <cstdlib>
+#include <map>
+#include <mutex>
+#include <utility>
 
 #include "kernels.h"
 
 namespace ub {
 
 namespace {
+// largest dynamic shared-memory size set per (kernel, device)
+std::mutex g_attr_mu;
+std::map<std::pair<const void*, int>, size_t> g_attr;
+size_t attr_smem(const void* fn) {
+    int dev = 0;
+    UB_CUDA(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> lk(g_attr_mu);
+    auto it = g_attr.find({fn, dev});
+    return it == g_attr.end() ? 0 : it->second;
+}
+void note_attr_smem(const void* fn, size_t smem) {
+    int dev = 0;
+    UB_CUDA(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> lk(g_attr_mu);
+    size_t& v = g_attr[{fn, dev}];
+    v = std::max(v, smem);
+}
+
 constexpr int CTA = 1024;   // threads per CTA (one CTA per SM)
 constexpr int TG = 256;     // tracer group / level-barrier group size
 // dataflow CTA size: single-warp updaters (one problem) are shared-memory
@@ -1653,12 +1674,13 @@ template <int P>
 static void wave_launch_t(const WaveArgs& a, int sms, cudaStream_t st) {
     constexpr int NT = WaveShape<P>::G + 64;
     const size_t smem = 4 * wave_words<P>(a.m.max_recs, a.m.max_cells, a.lines);
-    // set once per size: changing a running kernel's attributes would wait
-    // for it (uscg_reconstruct_batch overlaps neighbouring stacks' solves)
-    static size_t set_smem = 0;
-    if (smem > set_smem) {
+    // set once per (device, size): changing a running kernel's attributes
+    // would wait for it (uscg_reconstruct_batch overlaps neighbouring stacks'
+    // solves). The attribute is per device, and contexts on several devices
+    // or host threads may launch concurrently.
+    if (smem > attr_smem(reinterpret_cast<const void*>(&mart_wave_kernel<P>))) {
         UB_CUDA(cudaFuncSetAttribute(mart_wave_kernel<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-        set_smem = smem;
+        note_attr_smem(reinterpret_cast<const void*>(&mart_wave_kernel<P>), smem);
     }
     int per_sm = 0;
     UB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, mart_wave_kernel<P>, NT, smem));

@@ -411,6 +411,40 @@ def test_reconstruct_matches_reference_cone_wide(ub, ref):
     _check_recon(ub, ref, "cone32w", "random", beta=1.0, sweeps=2, rtol=2e-4)
 
 
+@pytest.mark.parametrize("name,beta,sweeps,tol", [("fan128", 0.4, 5, 0), ("cone32", 0.4, 3, 0),
+                                                   ("fan16", 1.0, 6, 1e-5), ("cone12", 1.9, 3, 0)])
+def test_tile_executor_matches_flow_and_reference(ub, ref, monkeypatch, capfd, name, beta, sweeps, tol):
+    """The one-CTA tile executor (field in shared memory, one warp per line of
+    an ASAP level, a block barrier between levels; the default for one small
+    problem) and the flow executor both match the reference library: counters
+    and crossed masks exactly, fields within fp32 tolerance."""
+    g = REF_GEOMS[name]
+    rt = ref_tracer(ref, g)
+    truth = np.random.default_rng(3).uniform(0.2, 3.0, rt.cells)
+    proj = rt.project(truth)
+    if beta > 1:
+        proj[1, :4] = 1e-9  # clamps
+    want, wrep = rt.reconstruct(proj, beta=beta, tolerance=tol, max_sweeps=sweeps)
+    monkeypatch.setenv("USCG_FLOW_VERBOSE", "1")
+    out = {}
+    for mode in ("tile", "flow"):
+        monkeypatch.setenv("USCG_MART_MODE", mode)
+        spec, geom, tr = _ub_tracer(ub, g)
+        res = ub.reconstruct(ub.ProjectionSet(geom, proj), spec,
+                             ub.SolverConfig(beta=beta, tolerance=tol, max_sweeps=sweeps), tr)
+        log = capfd.readouterr().err
+        assert f"mart_{mode}_kernel" in log, log
+        rep = res.report
+        assert rep.sweeps == wrep["sweeps"] and rep.factor_clamps == wrep["factor_clamps"]
+        assert rep.zero_measurement_skips == wrep["zero_measurement_skips"]
+        assert np.array_equal(rep.crossed, wrep["crossed"])
+        rel = np.abs(res.field.values - want) / np.abs(want)
+        assert rel.max() <= (2e-4 if beta > 1 else 1e-4), (mode, rel.max())
+        out[mode] = res.field.values
+    if beta > 1:
+        assert wrep["factor_clamps"] > 0
+
+
 def test_reconstruct_residual_stopping(ub, ref):
     g = REF_GEOMS["fan16"]
     rt = ref_tracer(ref, g)
@@ -648,14 +682,34 @@ def test_batched_reconstruction_equals_one_call_per_stack(ub, orc, S, init):
                 assert np.array_equal(got[b][p], want[p][0]), (B, b, p)
 
 
-def test_batched_reconstruction_reports_the_failing_stack(ub, orc):
-    """A stack with invalid data fails the batch with the reference's error."""
+@pytest.mark.parametrize("S", [2, 8])
+def test_batched_reconstruction_reports_the_failing_stack(ub, orc, S):
+    """A stack with invalid data fails the batch with the reference's error;
+    the stack solved before it still delivers its field (S = 8: the wave
+    executor's overlapped solve slots)."""
+    import ctypes as C
+
+    import torch
+
+    from paper_2208_12964_b200 import uscg
     spec, geom, tr, _ = _m1_case(ub, orc, "arc", n_rings=32, views=12, du=64)
-    good = ub.project_stack(tr, np.ones((2, spec.cell_count()), np.float32))
+    rng = np.random.default_rng(S)
+    good = ub.project_stack(tr, rng.uniform(0.5, 2.0, (S, spec.cell_count())).astype(np.float32))
     bad = good.copy()
     bad[1, 0, 0] = -1.0
+    cfg = ub.SolverConfig(beta=0.5, tolerance=0, max_sweeps=2)
     with pytest.raises(ub.InvalidArgument, match="non-finite or negative"):
-        ub.reconstruct_batch([good, bad, good], ub.SolverConfig(beta=0.5, tolerance=0, max_sweeps=1), tr)
+        ub.reconstruct_batch([good, bad, good], cfg, tr)
+    stacks = [torch.from_numpy(x.reshape(S, -1).copy()).pin_memory() for x in (good, bad, good)]
+    fields = [torch.zeros((S, spec.cell_count()), dtype=torch.float32).pin_memory() for _ in range(3)]
+    pp = (C.c_void_p * 3)(*[C.c_void_p(x.data_ptr()) for x in stacks])
+    ff = (C.c_void_p * 3)(*[C.c_void_p(x.data_ptr()) for x in fields])
+    c = uscg._Cfg(cfg.beta, cfg.tolerance, cfg.max_sweeps, cfg.f_init, cfg.p_floor)
+    rc = ub.load().uscg_reconstruct_batch(tr.h, 3, pp, S, C.byref(c), ff, 0, None, 0)
+    assert rc == 1
+    want = np.stack([f for f, _ in ub.reconstruct_stack(good, cfg, tr)])
+    assert np.array_equal(fields[0].numpy(), want)
+    assert not fields[2].numpy().any()  # never solved
 
 
 @pytest.mark.parametrize("name", ["fan64q", "cone16", "cone32w", "cone12"])

@@ -61,3 +61,19 @@ s0 = (st[:, 0] - t0) * 1e-3
 s1 = (st[:, 1] - t0) * 1e-3
 inflight = [((s0 < b) & (s1 > a)).sum() for a, b in zip(edges[:-1], edges[1:])]
 print("  tasks overlapping each tenth of the span:", inflight)
+# per (sweep, chunk): start-time lag between consecutive views, in lines
+nch = Sp // min(32, Sp)
+allst = np.fromfile(path, np.uint64) if os.path.exists(path) else None
+per_sweep = info["views"] * nch
+tick = np.nonzero(ok)[0]
+start = dict(zip(tick.tolist(), st[:, 0].tolist()))
+end = dict(zip(tick.tolist(), st[:, 1].tolist()))
+lags = []
+for tk in tick:
+    v = (tk % per_sweep) // nch
+    if v + 1 < info["views"] and tk + nch in start:
+        lags.append((start[tk + nch] - start[tk]) * 1e-3)
+lags = np.array(lags)
+line_us = dur.mean() / lines
+print(f"  view-to-view start lag: mean {lags.mean():.2f} us = {lags.mean() / line_us:.1f} lines of {line_us:.3f} us; "
+      f"sweep = {info['views']} lags + one task = {(info['views'] * lags.mean() + dur.mean()) / 1e3:.3f} ms")

@@ -433,11 +433,18 @@ def bench_mart(gpu: Gpu, config, args, rank, world, steps=None, warmup=None, cpu
     ms_per_step = t_ms / steps
     value = U_all / (ms_per_step * 1e-3)
 
-    # ---- K2 projector over the stack (device-resident, one launch) ----
-    out_d = torch.empty((units, Sp), dtype=torch.float32, device="cuda")
+    # ---- K2 projector over the stack (device-resident, one launch); one
+    #      problem on N ranks: each rank projects its block of views
+    #      (dist.view_subset_tracer over the same record store) ----
+    ptr, p_units = tracer, units
+    if not stacked and world > 1:
+        v0, v1 = udist.shard(info["views"], rank, world)
+        ptr = udist.view_subset_tracer(tracer, v0, v1)
+        p_units = (v1 - v0) * info["lines"]
+    out_d = torch.empty((max(p_units, 1), Sp), dtype=torch.float32, device="cuda")
 
     def project_dev():
-        uscg._check(L.uscg_project(tracer.h, uscg.C.c_void_p(field_d.data_ptr()), S,
+        uscg._check(L.uscg_project(ptr.h, uscg.C.c_void_p(field_d.data_ptr()), S,
                                    uscg.C.c_void_p(out_d.data_ptr()), flags))
 
     project_dev()
@@ -449,11 +456,21 @@ def bench_mart(gpu: Gpu, config, args, rank, world, steps=None, warmup=None, cpu
         b.record(stream)
     torch.cuda.synchronize()
     tp = float(sum(a.elapsed_time(b) for a, b in pe)) / len(pe)
-    Bp = 4 * E * S + 20 * C + 8 * units + 4 * units * Sp
+    (tp,) = udist.max_over_ranks([tp], device="cuda")
+    if ptr is not tracer:
+        ptr.close()
+    # the whole job over all ranks (stacks: every rank's slices; one problem:
+    # every rank's views); frac is per GPU
+    S_job = S_all if stacked else 1
+    reps = world if stacked else 1
+    Bp = 4 * E * S_job + reps * (20 * C + 8 * units + 4 * units * Sp)
     peak, peak_kind = hbm_peak()
-    projector = {"ms": tp, "updates_per_s": E * S / (tp * 1e-3), "achieved_gbs": Bp / (tp * 1e-3) / 1e9,
-                 "frac": Bp / (tp * 1e-3) / 1e9 / peak, "algorithmic_bytes": Bp,
+    projector = {"ms": tp, "updates_per_s": E * S_job / (tp * 1e-3), "achieved_gbs": Bp / (tp * 1e-3) / 1e9,
+                 "frac": Bp / (tp * 1e-3) / 1e9 / peak / world, "algorithmic_bytes": Bp,
                  "kernel": "project_stack_kernel" if Sp > 1 else "project_kernel<1>",
+                 "parallelism": ("slices sharded" if stacked else
+                                 f"views sharded over {world} GPU(s) (dist.view_subset_tracer)" if world > 1
+                                 else "one GPU"),
                  "bytes_model": "4*E*S (field gathers) + 20*C (records) + 8*(views*lines) (offsets, measurement "
                                 "index) + 4*(views*lines)*S_pad (projections written)"}
     del out_d

@@ -1,8 +1,12 @@
-"""Multi-GPU plumbing for the slice stack (one process per GPU).
+"""Multi-GPU plumbing (one process per GPU).
 
 SURVEY.md §8(e): the 2D-stack configuration shards by slice with no
-communication during iterations; cone-beam MART (C3/C4) does not shard (the
-reference's update within a view is sequential), so it runs replicas only.
+communication during iterations; the projector shards by view (every
+(view, line) is independent and the field read-only,
+proj/src/phantom.cpp:182-211); resampling shards by slice
+(proj/src/phantom.cpp:149-163); the generator shards by detector row with one
+exchange; cone-beam MART (C3/C4) does not shard (the reference's update
+within a view is sequential), so it runs replicas only.
 torch.distributed is used for rendezvous, the barrier around the timed region,
 the max-over-ranks timing reduction and the optional end gather of fields —
 never inside a sweep.
@@ -149,3 +153,90 @@ def generate_sharded(spec, geom, rank: int, world: int, ctx=None):
     local.close()
     full = assemble_cache(*part)
     return Tracer.from_key_cache(spec, *full, geom.views, geom.view_angles, geom=geom, ctx=ctx)
+
+
+# ---------------------------------------------------------------------------
+# view-sharded projector (projector row)
+# ---------------------------------------------------------------------------
+
+
+def view_subset_tracer(tracer, v0: int, v1: int):
+    """A tracer over views [v0, v1) of `tracer`, sharing its record store (the
+    symmetry-compressed store is view-independent: a copy of the one-view
+    records on the same device, no regeneration)."""
+    import dataclasses
+
+    from .uscg import Tracer
+    th = np.asarray(tracer.geom.thetas(), dtype=np.float64)[v0:v1]
+    off, pa, pb, key = tracer.copy_cache(device=True)
+    geom = dataclasses.replace(tracer.geom, views=v1 - v0, view_angles=th)
+    return Tracer.from_key_cache(tracer.spec, off, pa, pb, key, v1 - v0, th, geom=geom, ctx=tracer.ctx)
+
+
+def project_views_local(tracer, fields: np.ndarray, rank: int, world: int) -> np.ndarray:
+    """This rank's share of generate_projections: the binary projections of
+    every field over views shard(views, rank, world): (S, v1 - v0, lines)."""
+    from .uscg import project_stack
+    v0, v1 = shard(tracer.info()["views"], rank, world)
+    if v1 == v0:
+        return np.zeros((fields.shape[0], 0, tracer.info()["lines"]), np.float32)
+    sub = view_subset_tracer(tracer, v0, v1)
+    try:
+        return project_stack(sub, fields)
+    finally:
+        sub.close()
+
+
+def concat_views(parts) -> np.ndarray:
+    """The rank-ordered view blocks (each (S, views_r, lines)) as one stack."""
+    return np.concatenate(list(parts), axis=1)
+
+
+def all_gather_views(local: np.ndarray, n_views: int, rank: int, world: int, device=None) -> np.ndarray:
+    """Every rank receives the full (S, n_views, lines) projections: one
+    all-gather of the view blocks padded to the largest shard."""
+    import torch
+    import torch.distributed as dist
+    if world == 1:
+        return local
+    S, _, lines = local.shape
+    cap = (n_views + world - 1) // world
+    buf = torch.zeros((S, cap, lines), dtype=torch.float32, device=device)
+    lo, hi = shard(n_views, rank, world)
+    buf[:, : hi - lo] = torch.from_numpy(np.ascontiguousarray(local, dtype=np.float32)).to(buf)
+    parts = [torch.zeros_like(buf) for _ in range(world)]
+    dist.all_gather(parts, buf)
+    return concat_views([parts[r][:, : shard(n_views, r, world)[1] - shard(n_views, r, world)[0]].cpu().numpy()
+                         for r in range(world)])
+
+
+def project_view_sharded(tracer, fields: np.ndarray, rank: int, world: int, device=None) -> np.ndarray:
+    """generate_projections on N GPUs: each rank projects its view block, one
+    all-gather assembles the full set on every rank."""
+    local = project_views_local(tracer, fields, rank, world)
+    return all_gather_views(local, tracer.info()["views"], rank, world, device)
+
+
+# ---------------------------------------------------------------------------
+# slice-sharded resampling (SURVEY.md §8(e), resample row)
+# ---------------------------------------------------------------------------
+
+
+def slice_subgrid(spec, s0: int, s1: int):
+    """The grid of slices [s0, s1) of a volume grid (same rings, sector law,
+    slice height)."""
+    from .uscg import GridSpec
+    return GridSpec(spec.n, spec.ring_spacing, spec.slice_height, spec.mode, ring_counts=spec.ring_counts,
+                    n_slices=s1 - s0)
+
+
+def resample_local(spec, field: np.ndarray, npix: int, rank: int, world: int, ctx=None) -> np.ndarray:
+    """field_to_cartesian of this rank's slices shard(slices, rank, world) of
+    one volume field (reference flat order): (s1 - s0, npix, npix)."""
+    from .uscg import resample_stack
+    s0, s1 = shard(spec.slices(), rank, world)
+    cps = spec.cells_per_slice()
+    if s1 == s0:
+        return np.zeros((0, npix, npix), np.float32)
+    sub = slice_subgrid(spec, s0, s1)
+    return resample_stack(sub, np.asarray(field).reshape(-1)[s0 * cps: s1 * cps][None], npix, ctx)[0]

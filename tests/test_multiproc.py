@@ -137,3 +137,106 @@ def test_two_rank_generator_exchange_assembles_the_full_store(tmp_path):
     want = [t.numpy() for t in _key_layout(orc.cache(grid, s, d))]
     for k, w in enumerate(want):
         assert np.array_equal(got[f"arr_{k}"], w), k
+
+
+# ---------------------------------------------------------------------------
+# the slice-sharded bench inputs, the view-sharded projector's exchange and the
+# slice-sharded resample
+# ---------------------------------------------------------------------------
+
+
+def test_sharded_stack_inputs_are_rows_of_the_full_stack():
+    """bench.py's C2 shards generate exactly their rows of the full stack's
+    phantoms and noise (problem p seeded by p, whatever the shard)."""
+    from paper_2208_12964_b200 import workloads
+    from paper_2208_12964_b200.dist import shard
+    wl = workloads.make("c2", problems=5)
+    full = workloads.phantom_fields(wl, 5)
+    proj = np.random.default_rng(1).uniform(0, 2, (5, 40)).astype(np.float32)
+    noisy = workloads.add_noise(wl, proj)
+    for world in (2, 3):
+        for r in range(world):
+            lo, hi = shard(5, r, world)
+            assert np.array_equal(workloads.phantom_fields(wl, hi - lo, first=lo), full[lo:hi])
+            assert np.array_equal(workloads.add_noise(wl, proj[lo:hi], first=lo), noisy[lo:hi])
+
+
+def _view_case():
+    import oracle
+    orc = oracle.Orc()
+    grid = oracle.OrcGrid(16, 1 / 16, 1, 1 / 16, False, orc.ring_counts_m1(16))
+    s, d = orc.rays_arc((-3, 0, 0), (1.5, 0, 0), 48, 38.94 / 48)
+    th = np.array([360.0 * i / 11 for i in range(11)])
+    truth = np.random.default_rng(8).uniform(0.2, 2.0, (3, grid.cell_count()))
+    return orc, grid, s, d, th, truth
+
+
+def _view_worker(rank, world, port, out_dir):
+    import sys
+    sys.path.insert(0, ROOT)
+    import torch.distributed as dist
+    from paper_2208_12964_b200 import dist as udist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(world))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    orc, grid, s, d, th, truth = _view_case()
+    v0, v1 = udist.shard(th.size, rank, world)
+    oc = orc.cache(grid, s, d)
+    local = np.stack([oc.project(th[v0:v1], truth[p]) for p in range(truth.shape[0])]).astype(np.float32)
+    full = udist.all_gather_views(local, th.size, rank, world)
+    np.save(os.path.join(out_dir, f"views{rank}.npy"), full)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.timeout(300)
+def test_two_rank_view_sharded_projection_exchange(tmp_path):
+    """Each rank projects its view block; one all-gather gives every rank the
+    full projection set (the per-rank projections here are the oracle's, the
+    stand-in for each GPU's project_views_local)."""
+    port = _free_port()
+    mp.spawn(_view_worker, args=(2, port, str(tmp_path)), nprocs=2, join=True)
+    orc, grid, s, d, th, truth = _view_case()
+    oc = orc.cache(grid, s, d)
+    want = np.stack([oc.project(th, truth[p]) for p in range(truth.shape[0])]).astype(np.float32)
+    for r in range(2):
+        assert np.array_equal(np.load(tmp_path / f"views{r}.npy"), want)
+
+
+def _res_case():
+    import oracle
+    orc = oracle.Orc()
+    grid = oracle.OrcGrid(12, 1 / 12, 10, 2 / 12, True, orc.ring_counts_m1(12))
+    field = np.random.default_rng(4).uniform(0, 1, grid.cell_count())
+    return orc, grid, field
+
+
+def _res_worker(rank, world, port, out_dir):
+    import sys
+    sys.path.insert(0, ROOT)
+    import oracle
+    import torch.distributed as dist
+    from paper_2208_12964_b200 import dist as udist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(world))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    orc, grid, field = _res_case()
+    s0, s1 = udist.shard(grid.n_slices, rank, world)
+    cps = grid.cells_per_slice()
+    sub = oracle.OrcGrid(grid.n_rings, grid.ring_spacing, s1 - s0, grid.slice_height, True, grid.counts)
+    local = orc.field_to_cartesian(sub, field[s0 * cps:s1 * cps], 32).astype(np.float32)
+    stack = udist.gather_stack(local, grid.n_slices, rank, world)
+    if rank == 0:
+        np.save(os.path.join(out_dir, "img.npy"), stack)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.timeout(300)
+def test_two_rank_slice_sharded_resample(tmp_path):
+    """Each rank resamples its slices (the oracle's field_to_cartesian on the
+    rank's sub-volume, the stand-in for dist.resample_local), rank 0 gathers
+    the raster stack; it equals the single-process resample."""
+    port = _free_port()
+    mp.spawn(_res_worker, args=(2, port, str(tmp_path)), nprocs=2, join=True)
+    orc, grid, field = _res_case()
+    want = orc.field_to_cartesian(grid, field, 32).astype(np.float32)
+    assert np.array_equal(np.load(tmp_path / "img.npy"), want)

@@ -463,16 +463,23 @@ def bench_mart(gpu: Gpu, config, args, rank, world, steps=None, warmup=None, cpu
     # every rank's views); frac is per GPU
     S_job = S_all if stacked else 1
     reps = world if stacked else 1
-    Bp = 4 * E * S_job + reps * (20 * C + 8 * units + 4 * units * Sp)
+    listed = Sp == 1 and int(info.get("executor_bytes", 0)) > 0
+    if listed:  # one problem with the solver's traced lists: project_lists_kernel
+        Bp = 8 * E + 12 * units
+        p_model = "8*E (u32 list entry + fp32 field gather per cell) + 12*(views*lines) (u64 offsets, output)"
+    else:
+        Bp = 4 * E * S_job + reps * (20 * C + 8 * units + 4 * units * Sp)
+        p_model = ("4*E*S (field gathers) + 20*C (records) + 8*(views*lines) (offsets, measurement index) + "
+                   "4*(views*lines)*S_pad (projections written)")
     peak, peak_kind = hbm_peak()
     projector = {"ms": tp, "updates_per_s": E * S_job / (tp * 1e-3), "achieved_gbs": Bp / (tp * 1e-3) / 1e9,
                  "frac": Bp / (tp * 1e-3) / 1e9 / peak / world, "algorithmic_bytes": Bp,
-                 "kernel": "project_stack_kernel" if Sp > 1 else "project_kernel<1>",
+                 "kernel": ("project_stack_kernel" if Sp > 1 else
+                            "project_lists_kernel" if listed else "project_kernel<1>"),
                  "parallelism": ("slices sharded" if stacked else
                                  f"views sharded over {world} GPU(s) (dist.view_subset_tracer)" if world > 1
                                  else "one GPU"),
-                 "bytes_model": "4*E*S (field gathers) + 20*C (records) + 8*(views*lines) (offsets, measurement "
-                                "index) + 4*(views*lines)*S_pad (projections written)"}
+                 "bytes_model": p_model}
     del out_d
 
     # ---- e2e through the C ABI with pinned host buffers ----
@@ -815,7 +822,7 @@ def bench_c5(args, rank, world, local):
                                    "all views served from L1): not an HBM figure",
                           "hbm_bytes_model": "20*records + 12*views*lines (records once, counts + checksums out)"},
         "resample": {"ms": res_ms, "pixels": px_all, "pixels_per_s": px_all / (res_ms * 1e-3),
-                     "roofline": roof(res_bytes, res_ms, "perm/bin_map + map_resample_kernel",
+                     "roofline": roof(res_bytes, res_ms, "tiled_resample_kernel (per 32x32 tile: coalesced cell runs staged in shared memory)",
                                       "8 B per output pixel (SURVEY.md §8(d))")},
         "metrics": {"ms": met_ms, "slices": spec.slices(), "ssim_volume": float(m_ssim.mean()),
                     "rmse_volume": float(m_rmse.mean()), "pixels_per_s": px_all / (met_ms * 1e-3),

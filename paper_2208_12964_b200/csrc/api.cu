@@ -264,6 +264,11 @@ struct ResampleCache {
     std::vector<uint32_t> counts;  // empty: the reference law
     std::unique_ptr<uscg_tracer_s> grid;
     DevBuf<uint32_t> map;
+    // tiled plan (npix % 32 == 0): per 32x32 tile its distinct cells, per
+    // pixel (tile-major) the slot of its cell in that list
+    bool tiled = false;
+    DevBuf<uint32_t> toff, tcells;
+    DevBuf<uint16_t> slot;
     bool matches(const uscg_grid* g, int n) const {
         if (!grid || g->n_rings != n_rings || (g->volume ? g->n_slices : 1) != n_slices ||
             (g->volume ? 1 : 0) != volume || n != npix || g->ring_spacing != ring_spacing ||
@@ -275,6 +280,54 @@ struct ResampleCache {
 };
 
 namespace {
+
+// The tiled resample plan from the pixel -> cell map (bin-point map, or the
+// inverse permutation): once per (grid, npix), on the host from the map.
+void build_resample_plan(ResampleCache& rc, bool perm, int npix, cudaStream_t st) {
+    const size_t npx = size_t(npix) * npix;
+    DevBuf<uint32_t> pm;
+    const uint32_t* dmap = rc.map.p;
+    if (perm) {
+        pm.alloc(npx);
+        launch_perm_map(npix, pm.p, st);
+        dmap = pm.p;
+    }
+    std::vector<uint32_t> map(npx);
+    UB_CUDA(cudaMemcpyAsync(map.data(), dmap, sizeof(uint32_t) * npx, cudaMemcpyDeviceToHost, st));
+    UB_CUDA(cudaStreamSynchronize(st));
+    const int T = 32, tx = npix / T, tiles = tx * tx;
+    std::vector<uint32_t> toff(size_t(tiles) + 1, 0), tcells, cells;
+    std::vector<uint16_t> slot(npx);
+    tcells.reserve(npx);
+    for (int tile = 0; tile < tiles; ++tile) {
+        const int r0 = (tile / tx) * T, c0 = (tile % tx) * T;
+        cells.clear();
+        for (int i = 0; i < T * T; ++i) {
+            const uint32_t c = map[size_t(r0 + i / T) * npix + c0 + i % T];
+            if (c != 0xFFFFFFFFu)
+                cells.push_back(c);
+        }
+        std::sort(cells.begin(), cells.end());
+        cells.erase(std::unique(cells.begin(), cells.end()), cells.end());
+        for (int i = 0; i < T * T; ++i) {
+            const uint32_t c = map[size_t(r0 + i / T) * npix + c0 + i % T];
+            slot[size_t(tile) * T * T + i] =
+                c == 0xFFFFFFFFu ? uint16_t(0xFFFF)
+                                 : uint16_t(std::lower_bound(cells.begin(), cells.end(), c) - cells.begin());
+        }
+        tcells.insert(tcells.end(), cells.begin(), cells.end());
+        toff[size_t(tile) + 1] = uint32_t(tcells.size());
+    }
+    rc.toff.alloc(toff.size());
+    rc.tcells.alloc(std::max<size_t>(tcells.size(), 1));
+    rc.slot.alloc(slot.size());
+    UB_CUDA(cudaMemcpyAsync(rc.toff.p, toff.data(), sizeof(uint32_t) * toff.size(), cudaMemcpyHostToDevice, st));
+    if (!tcells.empty())
+        UB_CUDA(cudaMemcpyAsync(rc.tcells.p, tcells.data(), sizeof(uint32_t) * tcells.size(), cudaMemcpyHostToDevice,
+                                st));
+    UB_CUDA(cudaMemcpyAsync(rc.slot.p, slot.data(), sizeof(uint16_t) * slot.size(), cudaMemcpyHostToDevice, st));
+    UB_CUDA(cudaStreamSynchronize(st));
+}
 
 template <class F>
 uscg_status guarded(F&& f) {
@@ -1375,6 +1428,10 @@ uscg_status uscg_project(uscg_tracer t, const float* field, int32_t problems, fl
                  "the length-weighted model needs the tracer's rays (not available for an imported cache)");
             launch_project_length(t->dev_grid(), t->lines, t->views, t->d_rays.p, t->d_theta.p, d_field, Sp,
                                   d_out, st);
+        } else if (Sp == 1 && t->lists_built) {
+            // one problem whose traced lists the solver has built (volumes):
+            // stream them instead of re-tracing every (view, line)
+            launch_project_lists(t->d_lists.p, t->d_lpos.p, units, d_field, d_out, st);
         } else {
             launch_project(t->trace_args(), t->views, d_field, Sp, t->max_recs, t->max_cells, d_out, st);
         }
@@ -2024,6 +2081,9 @@ uscg_status uscg_resample(uscg_ctx ctx, const uscg_grid* grid, const float* fiel
                 rc.map.alloc(size_t(npix) * npix);
                 launch_bin_map(rc.grid->dev_grid(), npix, rc.map.p, ctx->stream);
             }
+            rc.tiled = npix % 32 == 0;
+            if (rc.tiled)
+                build_resample_plan(rc, perm, npix, ctx->stream);
             rc.n_rings = grid->n_rings;
             rc.n_slices = grid->volume ? grid->n_slices : 1;
             rc.volume = grid->volume ? 1 : 0;
@@ -2054,7 +2114,9 @@ uscg_status uscg_resample(uscg_ctx ctx, const uscg_grid* grid, const float* fiel
             d_out.alloc(out_n);
             fout = d_out.p;
         }
-        if (perm)
+        if (rc.tiled)
+            launch_tiled_resample(fin, t->cps, slices, S, Sp, rc.toff.p, rc.tcells.p, rc.slot.p, npix, fout, st);
+        else if (perm)
             launch_perm_resample(fin, t->cps, slices, S, Sp, npix, fout, st);
         else
             launch_map_resample(fin, t->cps, slices, S, Sp, rc.map.p, npix, fout, st);

@@ -1105,6 +1105,52 @@ void launch_project(const TraceArgs& A, int views, const float* field, int Sp, i
     UB_DISPATCH_P(stride_chunk(Sp), project_impl<PP>(A, views, field, Sp, max_recs, max_cells, out, st));
 }
 
+// K2 for one problem, fed by the tracer's traced lists (built once per
+// geometry by the first reconstruction, api.cu build_lists): a warp per
+// (view, line) streams the line's list (coalesced u32) and gathers the field,
+// fp64 sum (generate_projections Binary, phantom.cpp:193-211); the same index
+// sets in the same emission order as the trace-based kernel, without
+// re-rotating and expanding the records.
+constexpr int kProjListNT = 256;
+
+__global__ void __launch_bounds__(kProjListNT) project_lists_kernel(const uint32_t* __restrict__ lists,
+                                                                    const unsigned long long* __restrict__ lpos,
+                                                                    uint64_t units, const float* __restrict__ field,
+                                                                    float* __restrict__ out) {
+    const uint64_t u = uint64_t(blockIdx.x) * (kProjListNT / 32) + (threadIdx.x >> 5);
+    const int lane = int(threadIdx.x & 31);
+    if (u >= units)
+        return;
+    const unsigned long long b = __ldg(lpos + u), e = __ldg(lpos + u + 1);
+    double s = 0;
+    unsigned long long k = b + unsigned(lane);
+    for (; k + 96 < e; k += 128) {
+        const uint32_t c0 = __ldcs(lists + k), c1 = __ldcs(lists + k + 32), c2 = __ldcs(lists + k + 64),
+                       c3 = __ldcs(lists + k + 96);
+        const float v0 = __ldg(field + c0), v1 = __ldg(field + c1), v2 = __ldg(field + c2), v3 = __ldg(field + c3);
+        s += double(v0);
+        s += double(v1);
+        s += double(v2);
+        s += double(v3);
+    }
+    for (; k < e; k += 32)
+        s += double(__ldg(field + __ldcs(lists + k)));
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1)
+        s += __shfl_xor_sync(0xFFFFFFFFu, s, o);
+    if (lane == 0)
+        out[u] = float(s);
+}
+
+void launch_project_lists(const uint32_t* lists, const unsigned long long* lpos, uint64_t units, const float* field,
+                          float* out, cudaStream_t st) {
+    if (units == 0)
+        return;
+    const uint64_t blocks = (units + kProjListNT / 32 - 1) / (kProjListNT / 32);
+    project_lists_kernel<<<unsigned(blocks), kProjListNT, 0, st>>>(lists, lpos, units, field, out);
+    check_launch();
+}
+
 // =============================================================================
 // per-problem reductions over [n][Sp] arrays: blockIdx.y = 32-column tile,
 // threadIdx.x = column in the tile, threadIdx.y = row lane.
@@ -1339,11 +1385,15 @@ __device__ __forceinline__ uint32_t cg_inverse(int row, int col, int n) {
 }
 
 // out[(p*slices + s)*n*n + pixel]; field element (p, cell) at cell*cs + p*ps
-// One output plane (slice s of problem p) per blockIdx.y, four consecutive
-// output pixels per thread (npix is even, so a plane holds a multiple of 4
-// pixels): 32-bit index math, one float4 streaming store, the map read as a
-// uint4. PERM: the reference permutation inverted per pixel (cg_inverse);
-// otherwise the precomputed bin-point map (0xFFFFFFFF = outside the disc).
+// Four consecutive output pixels per thread (npix is even, so a plane holds a
+// multiple of 4 pixels) and kResPlanes output planes per block row
+// (blockIdx.y): the pixel's source cells are found once (PERM: the reference
+// permutation inverted per pixel, cg_inverse; otherwise the precomputed
+// bin-point map, 0xFFFFFFFF = outside the disc) and reused for every plane,
+// and the gathers of four planes are in flight at once before their
+// streaming float4 stores.
+constexpr int kResPlanes = 16;
+
 template <bool PERM, bool VEC>
 __global__ void __launch_bounds__(256) resample_kernel(const float* __restrict__ field, uint64_t cps,
                                                        int slices, int planes, uint64_t cs, uint64_t ps,
@@ -1364,20 +1414,30 @@ __global__ void __launch_bounds__(256) resample_kernel(const float* __restrict__
         const uint4 mm = __ldg(reinterpret_cast<const uint4*>(map + q));
         m[0] = mm.x, m[1] = mm.y, m[2] = mm.z, m[3] = mm.w;
     }
-    for (int pl = int(blockIdx.y); pl < planes; pl += int(gridDim.y)) {
-        const int s = pl % slices, p = pl / slices;
-        const float* f = field + uint64_t(s) * cps * cs + uint64_t(p) * ps;
-        float v[4];
+    const int p0 = int(blockIdx.y) * kResPlanes, p1 = min(planes, p0 + kResPlanes);
+    for (int pl0 = p0; pl0 < p1; pl0 += 4) {
+        float v[4][4];
 #pragma unroll
-        for (int k = 0; k < 4; ++k)
-            v[k] = (!PERM && m[k] == 0xFFFFFFFFu) ? 0.f : __ldg(f + uint64_t(m[k]) * cs);
-        float* o = out + uint64_t(pl) * npx + q;
-        if constexpr (VEC) {
-            __stcs(reinterpret_cast<float4*>(o), make_float4(v[0], v[1], v[2], v[3]));
-        } else {
+        for (int j = 0; j < 4; ++j) {
+            const int pl = min(pl0 + j, p1 - 1);
+            const int s = pl % slices, p = pl / slices;
+            const float* f = field + uint64_t(s) * cps * cs + uint64_t(p) * ps;
 #pragma unroll
             for (int k = 0; k < 4; ++k)
-                __stcs(o + k, v[k]);
+                v[j][k] = (!PERM && m[k] == 0xFFFFFFFFu) ? 0.f : __ldg(f + uint64_t(m[k]) * cs);
+        }
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            if (pl0 + j >= p1)
+                break;
+            float* o = out + uint64_t(pl0 + j) * npx + q;
+            if constexpr (VEC) {
+                __stcs(reinterpret_cast<float4*>(o), make_float4(v[j][0], v[j][1], v[j][2], v[j][3]));
+            } else {
+#pragma unroll
+                for (int k = 0; k < 4; ++k)
+                    __stcs(o + k, v[j][k]);
+            }
         }
     }
 }
@@ -1390,7 +1450,10 @@ static void resample_launch(const float* field, uint64_t cps, int slices, int S,
     const uint64_t cs = Sp > 0 ? uint64_t(Sp) : 1, ps = Sp > 0 ? 1 : cells;
     const int planes = slices * S;
     const uint32_t npx = uint32_t(n) * uint32_t(n);
-    const dim3 grid(unsigned((npx / 4 + 255) / 256), unsigned(std::min(planes, 65535)));
+    const int rows = (planes + kResPlanes - 1) / kResPlanes;
+    if (rows > 65535)
+        throw CudaError("resample: too many output planes for one launch");
+    const dim3 grid(unsigned((npx / 4 + 255) / 256), unsigned(rows));
     if ((reinterpret_cast<uintptr_t>(out) & 15) == 0)
         resample_kernel<PERM, true><<<grid, 256, 0, st>>>(field, cps, slices, planes, cs, ps, map, n, out);
     else
@@ -1440,6 +1503,87 @@ void launch_map_resample(const float* field, uint64_t cps, int slices, int S, in
     if (uint64_t(npix) * npix * slices * S == 0)
         return;
     resample_launch<false>(field, cps, slices, S, Sp, map, npix, out, st);
+}
+
+// pixel -> cell of the reference permutation (the inverse of uspg_to_cg_map)
+__global__ void perm_map_kernel(int n, uint32_t* map) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n * n)
+        return;
+    map[i] = cg_inverse(i / n, i % n, n);
+}
+
+void launch_perm_map(int n, uint32_t* map, cudaStream_t st) {
+    perm_map_kernel<<<cdiv((long long)n * n, 256), 256, 0, st>>>(n, map);
+    check_launch();
+}
+
+// Tiled resample: a block owns one 32 x 32 pixel tile and kResPlanes output
+// planes. The tile's distinct source cells (tcells, ascending: a few dozen
+// runs of consecutive cells, one per ring crossed) are gathered per plane
+// into shared memory with coalesced loads, then every pixel reads its cell
+// from shared memory (slot, tile-major) and the rows are written as
+// streaming float4s. The scattered per-pixel gathers of resample_kernel
+// become per-run loads: the field is read about once and the output written
+// once (8 B per output pixel).
+constexpr int kTile = 32, kTileNTr = 256;
+
+__global__ void __launch_bounds__(kTileNTr) tiled_resample_kernel(const float* __restrict__ field, uint64_t cps,
+                                                                  int slices, int planes, uint64_t cs, uint64_t ps,
+                                                                  const uint32_t* __restrict__ toff,
+                                                                  const uint32_t* __restrict__ tcells,
+                                                                  const uint16_t* __restrict__ slot, int n,
+                                                                  float* __restrict__ out) {
+    __shared__ float buf[2][kTile * kTile];
+    const int tiles_x = n / kTile;
+    const int tile = int(blockIdx.x);
+    const int ty = tile / tiles_x, tx = tile % tiles_x;
+    const int t = int(threadIdx.x);
+    const uint32_t b = __ldg(toff + tile), D = __ldg(toff + tile + 1) - b;
+    uint32_t cell[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        const uint32_t i = uint32_t(t + k * kTileNTr);
+        cell[k] = i < D ? __ldg(tcells + b + i) : 0u;
+    }
+    const uint2 sl = __ldg(reinterpret_cast<const uint2*>(slot + size_t(tile) * kTile * kTile) + t);
+    const uint32_t s4[4] = {sl.x & 0xFFFFu, sl.x >> 16, sl.y & 0xFFFFu, sl.y >> 16};
+    const int lp = 4 * t, row = ty * kTile + lp / kTile, col = tx * kTile + lp % kTile;
+    const uint32_t npx = uint32_t(n) * uint32_t(n);
+    const int p0 = int(blockIdx.y) * kResPlanes, p1 = min(planes, p0 + kResPlanes);
+    for (int pl = p0; pl < p1; ++pl) {
+        const int s = pl % slices, p = pl / slices;
+        const float* f = field + uint64_t(s) * cps * cs + uint64_t(p) * ps;
+        float* sb = buf[pl & 1];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const uint32_t i = uint32_t(t + k * kTileNTr);
+            if (i < D)
+                sb[i] = __ldg(f + uint64_t(cell[k]) * cs);
+        }
+        __syncthreads();
+        float v[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+            v[k] = s4[k] == 0xFFFFu ? 0.f : sb[s4[k]];
+        __stcs(reinterpret_cast<float4*>(out + uint64_t(pl) * npx + uint64_t(row) * n + col),
+               make_float4(v[0], v[1], v[2], v[3]));
+    }
+}
+
+void launch_tiled_resample(const float* field, uint64_t cps, int slices, int S, int Sp, const uint32_t* toff,
+                           const uint32_t* tcells, const uint16_t* slot, int n, float* out, cudaStream_t st) {
+    if (uint64_t(n) * n * slices * S == 0)
+        return;
+    const uint64_t cells = cps * slices;
+    const uint64_t cs = Sp > 0 ? uint64_t(Sp) : 1, ps = Sp > 0 ? 1 : cells;
+    const int planes = slices * S;
+    const int rows = (planes + kResPlanes - 1) / kResPlanes;
+    if (rows > 65535)
+        throw CudaError("resample: too many output planes for one launch");
+    const dim3 grid(unsigned((n / kTile) * (n / kTile)), unsigned(rows));
+    tiled_resample_kernel<<<grid, kTileNTr, 0, st>>>(field, cps, slices, planes, cs, ps, toff, tcells, slot, n, out);
+    check_launch();
 }
 
 __global__ void cg_map_kernel(int n, uint32_t* out) {

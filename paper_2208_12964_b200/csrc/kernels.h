@@ -74,6 +74,10 @@ void launch_project_length(const DevGrid& g, int lines, int views, const double*
                            const double* theta, const float* field, int Sp, float* out,
                            cudaStream_t st);
 
+// K2 for one problem from precomputed traced lists (lists[lpos[u], lpos[u+1])): out [units]
+void launch_project_lists(const uint32_t* lists, const unsigned long long* lpos, uint64_t units, const float* field,
+                          float* out, cudaStream_t st);
+
 // K2 projector: out [units][Sp]
 void launch_project(const TraceArgs& A, int views, const float* field, int Sp, int max_recs,
                     int max_cells, float* out, cudaStream_t st);
@@ -214,6 +218,13 @@ void gpu_schedule_build(const TraceArgs& A, int views, int max_recs, int max_cel
 void launch_perm_resample(const float* field, uint64_t cells_per_slice, int slices, int S, int Sp,
                           int n, float* out, cudaStream_t st);
 void launch_bin_map(const DevGrid& g, int npix, uint32_t* map, cudaStream_t st);
+// pixel -> cell of the reference permutation, npix x npix
+void launch_perm_map(int n, uint32_t* map, cudaStream_t st);
+// tiled resample (npix % 32 == 0): per 32x32 tile its distinct source cells
+// tcells[toff[t], toff[t+1]) and per pixel (tile-major) the cell's slot
+// (0xFFFF: outside the disc)
+void launch_tiled_resample(const float* field, uint64_t cps, int slices, int S, int Sp, const uint32_t* toff,
+                           const uint32_t* tcells, const uint16_t* slot, int n, float* out, cudaStream_t st);
 void launch_map_resample(const float* field, uint64_t cells_per_slice, int slices, int S, int Sp,
                          const uint32_t* map, int npix, float* out, cudaStream_t st);
 void launch_cg_map(int n, uint32_t* out, cudaStream_t st);

@@ -445,6 +445,25 @@ def test_tile_executor_matches_flow_and_reference(ub, ref, monkeypatch, capfd, n
         assert wrep["factor_clamps"] > 0
 
 
+@pytest.mark.parametrize("name", ["cone32", "fan128", "cone32w"])
+def test_list_fed_projector_matches_traced_projector(ub, ref, name):
+    """Once a reconstruction has built the tracer's traced lists, one-problem
+    projections stream them (project_lists_kernel) instead of re-tracing:
+    the same sums as the trace-based kernel and the reference library."""
+    g = REF_GEOMS[name]
+    rt = ref_tracer(ref, g)
+    spec, geom, tr = _ub_tracer(ub, g)
+    truth = np.random.default_rng(11).uniform(0.2, 3.0, spec.cell_count())
+    traced = ub.project_stack(tr, truth[None].astype(np.float32))[0]
+    ub.reconstruct(ub.ProjectionSet(geom, traced.astype(np.float64)), spec,
+                   ub.SolverConfig(beta=0.5, tolerance=0, max_sweeps=1), tr)
+    assert tr.info()["executor_bytes"] > 0  # the lists exist now
+    listed = ub.project_stack(tr, truth[None].astype(np.float32))[0]
+    want = rt.project(truth.astype(np.float32).astype(np.float64))
+    np.testing.assert_allclose(listed, traced, rtol=1e-6, atol=1e-6)
+    np.testing.assert_allclose(listed, want, rtol=1e-6, atol=1e-5)
+
+
 def test_reconstruct_residual_stopping(ub, ref):
     g = REF_GEOMS["fan16"]
     rt = ref_tracer(ref, g)

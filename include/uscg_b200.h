@@ -178,6 +178,13 @@ uscg_status uscg_tracer_import_cache_keys(uscg_ctx ctx, const uscg_grid* grid, i
                                           const uint32_t* offsets, uint64_t records, const double* phi_a,
                                           const double* phi_b, const uint32_t* keys, int32_t views,
                                           const double* view_angles_deg, uint32_t flags, uscg_tracer* out);
+/* Diagnostics: the wave executor's derived arrays (built by the first 2D
+ * stack reconstruction; USCG_HOST_WAVE=1 builds them on the host): entries
+ * (2 u32 per traced cell: cell | in-previous-line << 31, position in the next
+ * line or 0xFFFF), requirement offsets (units + 1) and requirement pairs
+ * ({view | cross-sweep << 31, lines of that view}). NULL arrays: sizes only. */
+uscg_status uscg_tracer_export_wave(uscg_tracer tracer, uint64_t* n_entries, uint64_t* n_deps,
+                                    uint32_t* entries, uint32_t* dep_off, uint32_t* deps);
 uscg_status uscg_tracer_destroy(uscg_tracer tracer);
 uscg_status uscg_tracer_get_info(uscg_tracer tracer, uscg_tracer_info* info);
 /* FirstViewCache::offsets()/records() (tracer.hpp:28-29) to host arrays */

@@ -778,27 +778,15 @@ bool wave_fits(const uscg_tracer_s* t) {
            t->cells < (uint64_t(1) << 31);
 }
 
-void build_wave(uscg_tracer_s* t) {
-    if (t->wave_built)
-        return;
-    const auto h0 = std::chrono::steady_clock::now();
+// The host builder (USCG_HOST_WAVE=1; the reference for the device build's
+// test): the traced lists copied back, then one pass in sweep order.
+void build_wave_host(uscg_tracer_s* t, const std::vector<uint32_t>& pos, const uint32_t* d_idx) {
     const uint64_t units = t->units();
     const uint32_t L = uint32_t(t->lines);
-    std::vector<uint32_t> pos(units + 1);
-    pos[0] = 0;
-    for (uint64_t u = 0; u < units; ++u)
-        pos[u + 1] = pos[u] + t->h_cells[u];
     const uint64_t total = pos[units];
-    upload(t->d_wpos, pos);
     std::vector<uint32_t> idx(std::max<uint64_t>(total, 1));
-    {
-        DevBuf<uint32_t> d_idx;
-        d_idx.alloc(std::max<uint64_t>(total, 1));
-        launch_trace_dump(t->trace_args(), 0, uint32_t(units), t->max_recs, t->max_cells, t->d_wpos.p, d_idx.p,
-                          t->st());
-        UB_CUDA(cudaMemcpyAsync(idx.data(), d_idx.p, sizeof(uint32_t) * total, cudaMemcpyDeviceToHost, t->st()));
-        UB_CUDA(cudaStreamSynchronize(t->st()));
-    }
+    UB_CUDA(cudaMemcpyAsync(idx.data(), d_idx, sizeof(uint32_t) * total, cudaMemcpyDeviceToHost, t->st()));
+    UB_CUDA(cudaStreamSynchronize(t->st()));
     // entries: {cell | also in the previous line of the view << 31, position
     // in the next line of the view or 0xFFFF} (the executor's hand-overs)
     {
@@ -879,6 +867,34 @@ void build_wave(uscg_tracer_s* t) {
     upload(t->d_wdep_off, dep_off);
     upload(t->d_wdeps, deps);
     t->wave_deps = deps.size() / 2;
+}
+
+void build_wave(uscg_tracer_s* t) {
+    if (t->wave_built)
+        return;
+    const auto h0 = std::chrono::steady_clock::now();
+    const uint64_t units = t->units();
+    std::vector<uint32_t> pos(units + 1);
+    pos[0] = 0;
+    for (uint64_t u = 0; u < units; ++u)
+        pos[u + 1] = pos[u] + t->h_cells[u];
+    const uint64_t total = pos[units];
+    upload(t->d_wpos, pos);
+    DevBuf<uint32_t> d_idx;
+    d_idx.alloc(std::max<uint64_t>(total, 1));
+    launch_trace_dump(t->trace_args(), 0, uint32_t(units), t->max_recs, t->max_cells, t->d_wpos.p, d_idx.p, t->st());
+    const char* host = std::getenv("USCG_HOST_WAVE");
+    if ((host && std::atoi(host)) || !wave_build_supported(uint32_t(t->lines), uint32_t(t->views), t->cells)) {
+        build_wave_host(t, pos, d_idx.p);
+    } else {
+        t->d_went.alloc(std::max<uint64_t>(total, 1));
+        std::vector<uint32_t> dep_off, deps;
+        gpu_wave_build(t->d_wpos.p, d_idx.p, total, uint32_t(units), uint32_t(t->lines), uint32_t(t->views),
+                       t->cells, t->d_went.p, dep_off, deps, t->st());
+        upload(t->d_wdep_off, dep_off);
+        upload(t->d_wdeps, deps);
+        t->wave_deps = deps.size() / 2;
+    }
     t->wave_built = true;
     t->wave_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - h0).count();
     if (const char* e = std::getenv("USCG_FLOW_VERBOSE"); e && std::atoi(e))
@@ -1215,6 +1231,24 @@ uscg_status uscg_tracer_destroy(uscg_tracer tracer) {
         cudaSetDevice(tracer->device);
         cudaDeviceSynchronize();
         delete tracer;
+    });
+}
+
+uscg_status uscg_tracer_export_wave(uscg_tracer t, uint64_t* n_entries, uint64_t* n_deps, uint32_t* entries,
+                                    uint32_t* dep_off, uint32_t* deps) {
+    return guarded([&] {
+        need(t && n_entries && n_deps, "null argument");
+        bind(t->ctx);
+        need(t->wave_built, "the wave executor's arrays are not built (run a 2D stack reconstruction first)");
+        const uint64_t ne = t->cells_per_sweep, nd = t->wave_deps;
+        *n_entries = ne;
+        *n_deps = nd;
+        if (entries && ne)
+            UB_CUDA(cudaMemcpy(entries, t->d_went.p, sizeof(uint2) * ne, cudaMemcpyDeviceToHost));
+        if (dep_off)
+            UB_CUDA(cudaMemcpy(dep_off, t->d_wdep_off.p, sizeof(uint32_t) * (t->units() + 1), cudaMemcpyDeviceToHost));
+        if (deps && nd)
+            UB_CUDA(cudaMemcpy(deps, t->d_wdeps.p, sizeof(uint32_t) * 2 * nd, cudaMemcpyDeviceToHost));
     });
 }
 

@@ -141,6 +141,12 @@ struct WaveSchedule {
     int views;
     int lines;
 };
+// the wave executor's entries and requirements built on the device
+// (wave_build.cu) from the traced lists idx[pos[u], pos[u+1]) of every unit
+bool wave_build_supported(uint32_t lines, uint32_t views, uint64_t cells);
+void gpu_wave_build(const uint32_t* pos, const uint32_t* idx, uint64_t total, uint32_t units, uint32_t lines,
+                    uint32_t views, uint64_t cells, uint2* ent, std::vector<uint32_t>& dep_off,
+                    std::vector<uint32_t>& deps, cudaStream_t st);
 bool wave_supported(const MartArgs& h);
 bool wave_fits_smem(const MartArgs& h, int lines);
 size_t wave_smem_bytes(const MartArgs& m, int lines);

@@ -123,7 +123,7 @@ EXPORTS = [
     "uscg_tracer_build_schedule", "uscg_tracer_export_successors", "uscg_reconstruct_batch", "uscg_problem_stride", "uscg_project", "uscg_reconstruct",
     "uscg_resample", "uscg_uspg_to_cg_map", "uscg_diag_math", "uscg_schedule_build", "uscg_image_metrics",
     "uscg_cartesian_like", "uscg_csystem_create", "uscg_csystem_info", "uscg_csystem_export",
-    "uscg_csystem_reconstruct", "uscg_csystem_destroy",
+    "uscg_csystem_reconstruct", "uscg_csystem_destroy", "uscg_tracer_export_wave",
 ]
 
 _lib = None
@@ -163,6 +163,7 @@ def load(build_if_missing: bool = True):
     L.uscg_tracer_import_cache_keys.argtypes = [vp, C.POINTER(_Grid), C.c_int32, vp, C.c_uint64, vp, vp, vp,
                                                 C.c_int32, _dp, C.c_uint32, C.POINTER(vp)]
     L.uscg_tracer_get_info.argtypes = [vp, C.POINTER(_Info)]
+    L.uscg_tracer_export_wave.argtypes = [vp, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64), _u32p, _u32p, _u32p]
     L.uscg_tracer_export_cache.argtypes = [vp, _u32p, _dp, _dp, _u16p, _u16p]
     L.uscg_trace_line.argtypes = [vp, C.c_int32, C.c_double, _u32p, C.c_int64, C.POINTER(C.c_int64)]
     L.uscg_trace_counts.argtypes = [vp, _u32p]
@@ -590,6 +591,20 @@ class Tracer:
         out["succs"] = out["succs"][:ns.value]
         out.update(run=run.value, runs=R, levels=V)
         return out
+
+    def wave_arrays(self) -> dict:
+        """The wave executor's derived arrays (diagnostics): entries (n, 2) u32,
+        dep_off (units + 1) and deps (n, 2) u32."""
+        L = load()
+        ne, nd = C.c_uint64(), C.c_uint64()
+        _check(L.uscg_tracer_export_wave(self.h, C.byref(ne), C.byref(nd), None, None, None))
+        inf = self.info()
+        ent = np.zeros((max(ne.value, 1), 2), np.uint32)
+        off = np.zeros(inf["views"] * inf["lines"] + 1, np.uint32)
+        deps = np.zeros((max(nd.value, 1), 2), np.uint32)
+        _check(L.uscg_tracer_export_wave(self.h, C.byref(ne), C.byref(nd), ent.ctypes.data_as(_u32p),
+                                         off.ctypes.data_as(_u32p), deps.ctypes.data_as(_u32p)))
+        return {"entries": ent[: ne.value], "dep_off": off, "deps": deps[: nd.value]}
 
     def build_schedule(self) -> int:
         _check(load().uscg_tracer_build_schedule(self.h))

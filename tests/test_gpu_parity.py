@@ -606,6 +606,33 @@ def test_pipelined_runs_are_bit_identical(ub, orc, monkeypatch, capfd, S, run, w
     assert (np.abs(out[1][0] - want) / want).max() <= 1e-4
 
 
+@pytest.mark.parametrize("case", ["small", "c2"])
+def test_device_wave_build_equals_host_build(ub, orc, monkeypatch, capfd, case):
+    """The wave executor's entries and per-line requirements built on the
+    device (wave_build.cu: hashed next-line links, sorted (cell, unit) visits,
+    condensed candidates) equal the host builder's (USCG_HOST_WAVE=1) array
+    for array, on a small M1-law stack and on the verbatim C2 geometry."""
+    from paper_2208_12964_b200 import workloads
+    monkeypatch.setenv("USCG_FLOW_VERBOSE", "1")
+    if case == "c2":
+        wl = workloads.make("c2")
+        spec, geom = wl.spec, wl.geom
+    else:
+        spec, geom, _, _ = _m1_case(ub, orc, "arc", n_rings=48, views=16, du=96)
+    arrays = {}
+    for host in ("0", "1"):
+        monkeypatch.setenv("USCG_HOST_WAVE", host)
+        tr = ub.Tracer(geom, spec, False)
+        proj = ub.project_stack(tr, np.ones((32, spec.cell_count()), np.float32))
+        ub.reconstruct_stack(proj, ub.SolverConfig(beta=0.5, tolerance=0, max_sweeps=1), tr)
+        assert "mart_wave_kernel: P=32 " in capfd.readouterr().err
+        arrays[host] = tr.wave_arrays()
+        tr.close()
+    for k in ("entries", "dep_off", "deps"):
+        assert np.array_equal(arrays["0"][k], arrays["1"][k]), k
+    assert arrays["0"]["deps"].shape[0] > 0
+
+
 @pytest.mark.parametrize("S,width", [(32, 32), (16, 16), (8, 8), (64, 4)])
 def test_wave_zero_lines_keep_handed_over_cells(ub, orc, monkeypatch, capfd, S, width):
     """Lines whose measurements are zero for every problem of a chunk (rim

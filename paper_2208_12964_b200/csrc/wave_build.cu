@@ -147,29 +147,47 @@ __global__ void __launch_bounds__(kNT) candidates_kernel(const unsigned long lon
         cand[base + __popc(has & ((1u << lane) - 1))] = mine[0];
 }
 
-// one thread per (kind, view, other view) group of the sorted candidates: per
-// line the largest need, kept where it raises the maximum over the view's
-// earlier lines; survivors as (unit << 32 | kind << 31 | other view << 16 | need)
-__global__ void condense_kernel(const unsigned long long* __restrict__ cand, uint64_t n, uint32_t L,
-                                unsigned long long* __restrict__ out, unsigned long long* __restrict__ count) {
+// Condensing the sorted candidates, in parallel: within a (kind, view, other
+// view) group, a line's largest need is its last entry; it is kept when it
+// exceeds the largest need of the group's earlier lines (a max-scan by group
+// over the line maxima, other entries contributing 0). Survivors as
+// (unit << 32 | kind << 31 | other view << 16 | need).
+__global__ void line_max_kernel(const unsigned long long* __restrict__ cand, uint64_t n,
+                                unsigned long long* __restrict__ group, uint32_t* __restrict__ val) {
     const uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (i >= n || (i > 0 && (cand[i - 1] >> 32) == (cand[i] >> 32)))
-        return;  // not the start of a group
-    const unsigned long long g = cand[i] >> 32;
-    const uint32_t xs = uint32_t(g >> 30), v = uint32_t(g >> 15) & 0x7FFFu, w = uint32_t(g) & 0x7FFFu;
-    uint32_t run_max = 0;
-    for (uint64_t j = i; j < n && (cand[j] >> 32) == g; ++j) {
-        const unsigned long long k = cand[j];
-        // the last entry of a line's run holds its largest need
-        if (j + 1 < n && (cand[j + 1] >> 16) == (k >> 16))
-            continue;
-        const uint32_t line = uint32_t(k >> 16) & 0xFFFFu, need = uint32_t(k) & 0xFFFFu;
-        if (need > run_max) {
-            run_max = need;
-            const uint64_t at = atomicAdd(count, 1ull);
-            out[at] = (uint64_t(v * L + line) << 32) | (uint64_t(xs) << 31) | (uint64_t(w) << 16) | need;
+    if (i >= n)
+        return;
+    const unsigned long long k = cand[i];
+    const bool line_max = i + 1 == n || (cand[i + 1] >> 16) != (k >> 16);
+    group[i] = k >> 32;
+    val[i] = line_max ? uint32_t(k) & 0xFFFFu : 0u;
+}
+
+__global__ void survivors_kernel(const unsigned long long* __restrict__ cand, uint64_t n,
+                                 const uint32_t* __restrict__ val, const uint32_t* __restrict__ scan, uint32_t L,
+                                 unsigned long long* __restrict__ out, unsigned long long* __restrict__ count) {
+    const uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    bool keep = false;
+    unsigned long long o = 0;
+    if (i < n && val[i] != 0) {
+        const unsigned long long k = cand[i];
+        const uint32_t prev = (i > 0 && (cand[i - 1] >> 32) == (k >> 32)) ? scan[i - 1] : 0u;
+        const uint32_t need = val[i];
+        if (need > prev) {
+            const uint32_t xs = uint32_t(k >> 62), v = uint32_t(k >> 47) & 0x7FFFu, w = uint32_t(k >> 32) & 0x7FFFu;
+            const uint32_t line = uint32_t(k >> 16) & 0xFFFFu;
+            o = (uint64_t(v * L + line) << 32) | (uint64_t(xs) << 31) | (uint64_t(w) << 16) | need;
+            keep = true;
         }
     }
+    const unsigned lane = threadIdx.x & 31;
+    const unsigned has = __ballot_sync(0xFFFFFFFFu, keep);
+    unsigned long long base = 0;
+    if (has && lane == unsigned(__ffs(has) - 1))
+        base = atomicAdd(count, (unsigned long long)__popc(has));
+    base = __shfl_sync(0xFFFFFFFFu, base, has ? __ffs(has) - 1 : 0);
+    if (keep)
+        out[base + __popc(has & ((1u << lane) - 1))] = o;
 }
 
 __global__ void deps_kernel(const unsigned long long* __restrict__ sorted, uint64_t n, uint32_t* __restrict__ deps,
@@ -240,7 +258,16 @@ void gpu_wave_build(const uint32_t* pos, const uint32_t* idx, uint64_t total, ui
     unsigned long long *ca = cand.p, *cb = ctmp.p;
     if (nc) {
         sort_keys(ca, cb, nc, 0, 63, st);
-        condense_kernel<<<blocks(nc), kNT, 0, st>>>(ca, nc, L, cb, counts.p + 1);
+        Buf<unsigned long long> group(nc);
+        Buf<uint32_t> val(nc), scan(nc);
+        line_max_kernel<<<blocks(nc), kNT, 0, st>>>(ca, nc, group.p, val.p);
+        size_t tb = 0;
+        UB_CUDA(cub::DeviceScan::InclusiveScanByKey(nullptr, tb, group.p, val.p, scan.p, cub::Max(), int64_t(nc),
+                                                    cuda::std::equal_to<>(), st));
+        Buf<char> temp(tb);
+        UB_CUDA(cub::DeviceScan::InclusiveScanByKey(temp.p, tb, group.p, val.p, scan.p, cub::Max(), int64_t(nc),
+                                                    cuda::std::equal_to<>(), st));
+        survivors_kernel<<<blocks(nc), kNT, 0, st>>>(ca, nc, val.p, scan.p, L, cb, counts.p + 1);
         UB_CUDA(cudaGetLastError());
     }
     unsigned long long nd = 0;

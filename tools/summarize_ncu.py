@@ -131,8 +131,20 @@ def main():
     with open(os.path.join(PROF, f"{args.tag}_summary.md"), "w") as f:
         f.write("\n".join(lines) + "\n")
     if traffic:
-        with open(os.path.join(PROF, "traffic.json"), "w") as f:
-            json.dump(traffic, f, indent=1)
+        # one entry per configuration; the profile driver runs one MART
+        # launch of one iteration, so a launch's DRAM bytes are an iteration's
+        path = os.path.join(PROF, "traffic.json")
+        try:
+            with open(path) as f:
+                allt = json.load(f)
+            if "config" in allt:  # the round-1 single-entry layout
+                allt = {}
+        except Exception:
+            allt = {}
+        traffic["dram_bytes_per_iteration"] = traffic["dram_bytes_per_launch"]
+        allt[args.config] = traffic
+        with open(path, "w") as f:
+            json.dump(allt, f, indent=1)
     print("\n".join(lines))
 
 

@@ -569,7 +569,7 @@ def bench_mart(gpu: Gpu, config, args, rank, world, steps=None, warmup=None, cpu
                 "traffic": traffic, "traffic_unit": "DRAM bytes per iteration (ncu, profiles/)",
                 "peak_kind": peak_kind, "kernel": mart_kernel_name(info, P),
                 "algorithmic_bytes_per_iteration": B, "bytes_model": model,
-                "dependency_levels_per_iteration": levels,
+                "flow_run_levels_per_iteration": levels,
                 "launches": "one persistent launch per reconstruct call (all K iterations); achieved = "
                             "B * K / device time of that launch"}
 

@@ -339,8 +339,11 @@ def chunk_width(Sp):
     return p
 
 
-def bench_mart(gpu: Gpu, config, args, rank, world, steps=None, warmup=None, cpu=True, e2e=True, iso=True):
-    """One MART configuration: returns the JSON line (rank 0) or None."""
+def bench_mart(gpu: Gpu, config, args, rank, world, steps=None, warmup=None, cpu=True, e2e=True, iso=True,
+               weak=False):
+    """One MART configuration: returns the JSON line (rank 0) or None.
+    weak: every rank reconstructs a whole stack of its own (distinct seeds)
+    instead of its shard of the config's stack."""
     import torch
 
     from paper_2208_12964_b200 import dist as udist
@@ -353,7 +356,9 @@ def bench_mart(gpu: Gpu, config, args, rank, world, steps=None, warmup=None, cpu
     wl = workloads.make(config, problems=args.problems if config == args.config else None)
     S_all = wl.problems
     stacked = S_all > 1
-    lo, hi = udist.shard(S_all, rank, world) if stacked else (0, 1)
+    lo, hi = udist.shard(S_all, rank, world) if stacked and not weak else (0, S_all)
+    if weak:
+        wl.seed = udist.rank_seed(wl.seed, rank)
     S = hi - lo
 
     # ---- precompute (geometry only; reported separately like ReconReport::seconds) ----
@@ -399,7 +404,7 @@ def bench_mart(gpu: Gpu, config, args, rank, world, steps=None, warmup=None, cpu
         step_dev()
     torch.cuda.synchronize()
     info = tracer.info()
-    if world > 1:
+    if world > 1 and torch.distributed.is_initialized():
         torch.distributed.barrier()
     clocks = Clocks(gpu.local).start()
     # (1) headline: K iterations as one reconstruct call, run back to back like
@@ -521,7 +526,7 @@ def bench_mart(gpu: Gpu, config, args, rank, world, steps=None, warmup=None, cpu
             run_e2e(1)
             nrun = steps
         torch.cuda.synchronize()
-        if world > 1:
+        if world > 1 and torch.distributed.is_initialized():
             torch.distributed.barrier()
         a, b = gpu.event(), gpu.event()
         torch.cuda.synchronize()
@@ -980,6 +985,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-uscg", action="store_true", help="C2 line without the nested C3/C4 measurements")
     ap.add_argument("--no-store-fed", action="store_true", help="skip the store-fed (no lists) executor timing")
+    ap.add_argument("--no-weak", action="store_true", help="N > 1: skip the weak-scaling extra key")
     args = ap.parse_args()
 
     if "WORLD_SIZE" not in os.environ and args.gpus > 1:
@@ -1013,6 +1019,16 @@ def main():
         else:
             gpu = Gpu(local)
             line = bench_mart(gpu, args.config, args, rank, world)
+            if world > 1 and args.config == "c2" and not args.no_weak:
+                # extra key: weak scaling, one whole 128-slice stack per GPU
+                # (the headline `value` shards the config's stack)
+                wk = bench_mart(gpu, "c2", args, rank, world, cpu=False, e2e=False, iso=False, weak=True)
+                if rank == 0:
+                    line["weak_scaling"] = {"value": wk["value"], "unit": "updates/s",
+                                            "ms_per_step": wk["ms_per_step"],
+                                            "slices_per_gpu": wk["per_gpu_slices"],
+                                            "note": "every GPU reconstructs its own 128-slice stack (distinct seeds); "
+                                                    "value = all GPUs' updates / the slowest GPU's time"}
             if rank == 0 and args.config == "c2" and world == 1 and not args.no_store_fed:
                 line["store_fed"] = bench_store_fed(gpu, "c2", args)
             if rank == 0 and args.config == "c2" and world == 1 and not args.no_uscg:

@@ -148,7 +148,7 @@ struct uscg_tracer_s {
     // wave executor (2D stacks): every line's traced list and its other-view
     // requirements (mart_sweep.cu), progress counters [views * nchunks]
     bool wave_built = false;
-    DevBuf<uint32_t> d_wpos, d_wdep_off, d_wdeps;
+    DevBuf<uint32_t> d_wpos, d_wdep_off, d_wdeps, d_wcross;
     DevBuf<uint2> d_went;
     DevBuf<unsigned> d_wprog, d_wnext;
     int wave_chunks = 0;
@@ -895,6 +895,8 @@ void build_wave(uscg_tracer_s* t) {
         upload(t->d_wdeps, deps);
         t->wave_deps = deps.size() / 2;
     }
+    t->d_wcross.alloc(2 * std::max<uint64_t>(units, 1));
+    launch_wave_cross(t->d_wpos.p, t->d_went.p, uint32_t(units), t->d_wcross.p, t->st());
     t->wave_built = true;
     t->wave_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - h0).count();
     if (const char* e = std::getenv("USCG_FLOW_VERBOSE"); e && std::atoi(e))
@@ -1638,9 +1640,9 @@ static void reconstruct_body(uscg_tracer t, const float* proj, int32_t problems,
         build_wave(t);
         if (t->wave_chunks != h.nchunks) {
             const uint64_t n = uint64_t(t->views) * uint64_t(h.nchunks);
-            t->d_wprog.alloc(n);
+            t->d_wprog.alloc(2 * n);  // the pair kernel keeps one counter per CTA
             t->d_wnext.alloc(1);
-            UB_CUDA(cudaMemsetAsync(t->d_wprog.p, 0, sizeof(unsigned) * n, st));
+            UB_CUDA(cudaMemsetAsync(t->d_wprog.p, 0, sizeof(unsigned) * 2 * n, st));
             t->wave_chunks = h.nchunks;
             t->wave_epoch = 0;
         }
@@ -1679,6 +1681,7 @@ static void reconstruct_body(uscg_tracer t, const float* proj, int32_t problems,
             ws.ent = t->d_went.p;
             ws.dep_off = t->d_wdep_off.p;
             ws.deps = t->d_wdeps.p;
+            ws.cross = t->d_wcross.p;
             ws.views = t->views;
             ws.lines = t->lines;
             // USCG_SWEEP_PROFILE=<file>: per task {start, end, ready-wait, gather, reduce, store, cta}

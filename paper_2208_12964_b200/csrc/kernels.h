@@ -138,9 +138,11 @@ struct WaveSchedule {
                               //  position in the next line of the view (0xFFFF: none)}
     const uint32_t* dep_off;  // [units + 1]
     const uint32_t* deps;     // pairs {view | cross-sweep << 31, required lines of that view}
+    const uint32_t* cross;    // [units][2]: pair kernel, hand-overs crossing into CTA r per line
     int views;
     int lines;
 };
+void launch_wave_cross(const uint32_t* pos, const uint2* ent, uint32_t units, uint32_t* cross, cudaStream_t st);
 // the wave executor's entries and requirements built on the device
 // (wave_build.cu) from the traced lists idx[pos[u], pos[u+1]) of every unit
 bool wave_build_supported(uint32_t lines, uint32_t views, uint64_t cells);

@@ -1308,7 +1308,9 @@ struct WaveArgs {
     const uint2* ent;         // per traced entry {cell | in previous line << 31, position in next line}
     const uint32_t* dep_off;  // [units + 1]
     const uint32_t* deps;     // pairs {view | cross-sweep << 31, required line count of that view}
-    unsigned* prog;           // [views * nchunks]: lines completed, cumulative over sweeps
+    const uint32_t* cross;    // [units][2]: pair kernel, hand-overs crossing into CTA r per line
+    unsigned* prog;           // [views * nchunks] (pair kernel: [views * nchunks][2]): lines completed,
+                              // cumulative over sweeps
     unsigned* next;           // task ticket (zeroed per launch)
     unsigned epoch;           // global 0-based index of this launch's first sweep
     int n_sweeps;
@@ -1697,6 +1699,456 @@ static void wave_launch_t(const WaveArgs& a, int sms, cudaStream_t st) {
     mart_wave_kernel<P><<<grid, NT, smem, st>>>(a);
 }
 
+// ============================================================================
+// wave executor, CTA pairs (P = 32): a view task runs on a 2-CTA cluster
+// ============================================================================
+//
+// The single-CTA wave form spends ~2.4 us of a line's ~2.8 us moving the
+// line's rows through one SM's load/store path (profiles/r2_row_microbench.md),
+// while the dependency chain leaves SMs idle about half the time. Here the two
+// CTAs of a cluster (two SMs) split every line's cells (position s belongs to
+// CTA s & 1): each copies, sums, scales, hands over and stores half the rows.
+// Per line the partial sums of both CTAs meet through distributed shared
+// memory (each factor warp reads both in a fixed order, so both CTAs form the
+// same factors), cells handed to the next line go to the owning CTA's buffer
+// (st.shared::cluster), and two split mbarriers per CTA (arrivals from the
+// updater warps of both CTAs, release/acquire at cluster scope) replace the
+// block barriers A and C of the single-CTA form. CTA 0 publishes progress;
+// both CTAs' control warps check requirements. Every cell still sees the
+// line-by-line updates in order.
+namespace pair {
+constexpr int P = 32, V = 4, TPC = P / V, G = 384, NW = G / 32, NCLV = G / TPC, KV = 8;
+constexpr int COVERL = KV * NCLV;  // slots per CTA (a line covers 2 x COVERL = 768 cells)
+constexpr int NT = G + 64;
+
+__host__ __device__ inline size_t words(int lines) {
+    // s_pos | red[2][2 CTAs][NW][P] f64 | fac[P] float2 | ent[3][COVERL] uint2 | buf[COVERL][P] f32
+    return round4(size_t(lines) + 1) + 2 * 2 * 2 * size_t(NW) * P + 2 * size_t(P) + 3 * 2 * size_t(COVERL) +
+           size_t(COVERL) * P;
+}
+
+__device__ __forceinline__ uint32_t cluster_rank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ uint32_t map_peer(const void* p, uint32_t rank) {
+    uint32_t d;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(d) : "r"(uint32_t(__cvta_generic_to_shared(p))), "r"(rank));
+    return d;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_init(uint64_t* b, unsigned n) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(uint32_t(__cvta_generic_to_shared(b))), "r"(n)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_local(uint64_t* b) {
+    asm volatile("mbarrier.arrive.release.cluster.shared::cta.b64 _, [%0];" ::"r"(
+                     uint32_t(__cvta_generic_to_shared(b)))
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_cta(uint64_t* b) {
+    asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(uint32_t(__cvta_generic_to_shared(b)))
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_local(uint64_t* b, unsigned tx) {
+    asm volatile("mbarrier.arrive.expect_tx.release.cta.shared::cta.b64 _, [%0], %1;" ::"r"(
+                     uint32_t(__cvta_generic_to_shared(b))),
+                 "r"(tx)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_remote(uint32_t cluster_addr) {
+    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, unsigned parity) {
+    asm volatile(
+        "{ .reg .pred p; W: mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1; @!p bra W; }" ::"r"(
+            uint32_t(__cvta_generic_to_shared(b))),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void st_cluster_v4(uint32_t cluster_addr, float4 v) {
+    asm volatile("st.shared::cluster.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(cluster_addr), "f"(v.x), "f"(v.y),
+                 "f"(v.z), "f"(v.w)
+                 : "memory");
+}
+__device__ __forceinline__ double ld_cluster_f64(uint32_t cluster_addr) {
+    double v;
+    asm volatile("ld.shared::cluster.f64 %0, [%1];" : "=d"(v) : "r"(cluster_addr) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_cluster_u32(uint32_t cluster_addr, unsigned v) {
+    asm volatile("st.shared::cluster.u32 [%0], %1;" ::"r"(cluster_addr), "r"(v) : "memory");
+}
+}  // namespace pair
+
+__global__ void __launch_bounds__(pair::NT, 2) mart_wave_pair_kernel(WaveArgs a) {
+    using namespace pair;
+    using GW = GroupWorker<P, G>;
+    using Scale = typename GW::Scale;
+    extern __shared__ __align__(16) uint32_t smem[];
+    __shared__ unsigned s_task, s_ready, s_done;
+    __shared__ __align__(8) uint64_t barA, barC;
+    const uint32_t rank = cluster_rank(), peer = rank ^ 1u;
+    const int nchunks = a.m.nchunks;
+    const unsigned L = unsigned(a.lines);
+    const int per_sweep = a.views * nchunks;
+    const int total = per_sweep * a.n_sweeps;
+    uint32_t* s_pos = smem;
+    double* red = reinterpret_cast<double*>(smem + round4(size_t(L) + 1));  // [2 phases][2 CTAs][NW][P]
+    float2* fac = reinterpret_cast<float2*>(red + 2 * 2 * NW * P);          // [P]
+    uint2* s_ent = reinterpret_cast<uint2*>(fac + P);                         // [3][COVERL]
+    float4* buf = reinterpret_cast<float4*>(s_ent + 3 * COVERL);              // [COVERL][TPC]
+    const int tid = int(threadIdx.x);
+    // one progress counter per (view, chunk, CTA): each CTA publishes its
+    // own half of a line's cells; a requirement holds when both halves do
+    auto prog_of = [&](int view, int chunk, uint32_t r) {
+        return a.prog + (size_t(view) * nchunks + chunk) * 2 + r;
+    };
+    if (tid == 0) {
+        mbar_init(&barA, NW);      // + the peer's partials as transaction bytes
+        mbar_init(&barC, NW + 1);  // + the peer factor warp's arrival + the peer's hand-overs (bytes)
+        s_ready = 0;
+        s_done = 0;
+    }
+    cluster_sync_all();  // barriers initialised in both CTAs
+    if (rank == 0 && tid == 0) {
+        const unsigned t0 = atomicAdd(a.next, 1u);
+        s_task = t0;
+        st_cluster_u32(map_peer(&s_task, peer), t0);
+    }
+    cluster_sync_all();
+    int task = int(s_task);
+    auto task_boundary = [&](bool leader) {
+        cluster_sync_all();  // every thread of both CTAs: the task is done everywhere
+        if (leader) {
+            s_ready = 0;
+            s_done = 0;
+            if (rank == 0) {
+                const unsigned nt = atomicAdd(a.next, 1u);
+                s_task = nt;
+                st_cluster_u32(map_peer(&s_task, peer), nt);
+            }
+        }
+        cluster_sync_all();
+        return int(s_task);
+    };
+    auto line_sync = [] { asm volatile("bar.sync 1, %0;" ::"n"(G + 32) : "memory"); };
+    auto upd_sync = [] { asm volatile("bar.sync 2, %0;" ::"n"(G) : "memory"); };
+    unsigned jl = 0;  // lines this CTA has processed (mbarrier phase = jl & 1)
+    if (tid >= G && tid < G + 32) {
+        // ---- factor warp ----
+        const int lane = tid & 31;
+        const uint32_t peer_barC = map_peer(&barC, peer);
+        while (task < total) {
+            const int v = (task % per_sweep) / nchunks, chunk = task % nchunks;
+            const uint32_t u0 = uint32_t(v) * L;
+            const size_t c2 = size_t(chunk) * P + lane;
+            const double pf = __ldg(a.m.p_floor + c2);
+            const bool act = __ldg(a.m.active + c2) != 0;
+            float nm = __ldcs(a.m.proj + size_t(u0) * a.m.Sp + c2);
+            for (unsigned j = 0; j < L; ++j, ++jl) {
+                const float m = nm;
+                if (j + 1 < L)
+                    nm = __ldcs(a.m.proj + size_t(u0 + j + 1) * a.m.Sp + c2);
+                mbar_wait(&barA, jl & 1);  // both CTAs' partials of line j
+                const int par = int(jl & 1);
+                double p_bar = 0;  // CTA 0's warps first, in both CTAs
+#pragma unroll
+                for (int k = 0; k < 2 * NW; ++k)
+                    p_bar += red[(size_t(par) * 2 * NW + k) * P + lane];
+                double factor = 0;
+                if (m != 0.f && act) {
+                    const double ratio = double(m) / (p_bar > pf ? p_bar : pf);
+                    factor = 1.0 - a.m.beta * (1.0 - ratio);
+                    if (factor <= 0) {
+                        factor = pf;
+                        if (rank == 0)
+                            atomicAdd(a.m.clamps + c2, 1ull);
+                    }
+                }
+                const Scale sc = GW::scale_of(factor);
+                fac[lane] = make_float2(sc.g, sc.lb);
+                line_sync();  // B: factors in fac
+                // this CTA has consumed line j's partials: the peer may send line j+1's
+                if (lane == 0)
+                    mbar_arrive_remote(peer_barC);
+                mbar_wait(&barC, jl & 1);  // this CTA's stores and the peer's hand-overs of line j
+                if (lane == 0)
+                    st_release_cta_shared(&s_done, j + 1);
+            }
+            task = task_boundary(false);
+        }
+        return;
+    }
+    if (tid >= G + 32) {
+        // ---- control warp: requirements, and this CTA's progress ----
+        const int lane = tid & 31;
+        while (task < total) {
+            const int sweep = task / per_sweep;
+            const int v = (task % per_sweep) / nchunks, chunk = task % nchunks;
+            const unsigned gs = a.epoch + unsigned(sweep);
+            unsigned* mine = prog_of(v, chunk, rank);
+            const uint32_t u0 = uint32_t(v) * L;
+            if (lane < 2 && gs > 0)
+                spin_until_geq(prog_of(v, chunk, uint32_t(lane)), gs * L);
+            __syncwarp();
+            unsigned ready = 0, published = 0;
+            unsigned ns = 0;
+            while (ready < L || published < L) {
+                bool moved = false;
+                if (ready < L) {
+                    const unsigned j = ready + unsigned(lane);
+                    bool ok = true;
+                    const unsigned* last = nullptr;
+                    if (j < L) {
+                        const uint32_t b = __ldg(a.dep_off + u0 + j), e = __ldg(a.dep_off + u0 + j + 1);
+                        for (uint32_t k = b; k < e && ok; ++k) {
+                            const uint32_t w = __ldg(a.deps + 2 * size_t(k));
+                            const unsigned xs = w >> 31, u = w & 0x7FFFFFFFu;
+                            if (gs < xs)
+                                continue;
+                            const unsigned need = (gs - xs) * L + __ldg(a.deps + 2 * size_t(k) + 1);
+                            last = prog_of(int(u), chunk, 0);
+                            ok = ld_relaxed(last) >= need && ld_relaxed(last + 1) >= need;
+                        }
+                    }
+                    const unsigned bad = __ballot_sync(0xFFFFFFFFu, !ok);
+                    const unsigned adv = bad ? unsigned(__ffs(bad) - 1) : 32u;
+                    const unsigned nr = min(L, ready + adv);
+                    if (nr > ready) {
+                        if (unsigned(lane) < adv && last != nullptr) {
+                            (void)ld_acquire(last);
+                            (void)ld_acquire(last + 1);
+                        }
+                        __syncwarp();
+                        ready = nr;
+                        moved = true;
+                        if (lane == 0)
+                            st_release_cta_shared(&s_ready, ready);
+                    }
+                }
+                if (published < L) {
+                    const unsigned d = ld_acquire_cta_shared(&s_done);
+                    if (d > published) {
+                        if (lane == 0) {
+                            fence_acq_rel_gpu();
+                            st_relaxed_gpu(mine, gs * L + d);
+                        }
+                        published = d;
+                        moved = true;
+                    }
+                }
+                if (moved) {
+                    ns = 0;
+                } else {
+                    ns = ns ? min(ns * 2, 128u) : 16u;
+                    __nanosleep(ns);
+                }
+            }
+            __syncwarp();
+            task = task_boundary(lane == 0);
+        }
+        return;
+    }
+    // ---- updaters: this CTA's slots ls = cl + i * NCLV hold the line's
+    // positions s = 2 * ls + rank ----
+    const int q = tid % TPC, cl = tid / TPC;
+    const int lane = tid & 31, warp = tid >> 5;
+    float4* __restrict__ f4 = reinterpret_cast<float4*>(a.m.field);
+    const uint32_t Sp4 = uint32_t(a.m.Sp) / V;
+    const uint32_t peer_buf = map_peer(buf, peer), peer_red = map_peer(red, peer);
+    const uint32_t peer_barA = map_peer(&barA, peer), peer_barC = map_peer(&barC, peer);
+    auto wait_ready = [&](unsigned j) {
+        while (ld_acquire_cta_shared(&s_ready) <= j)
+            __nanosleep(16);
+    };
+    while (task < total) {
+        const int v = (task % per_sweep) / nchunks, chunk = task % nchunks;
+        const uint32_t u0 = uint32_t(v) * L;
+        const uint32_t col4 = (uint32_t(chunk) * P) / V + uint32_t(q);
+        for (unsigned j = unsigned(tid); j <= L; j += G)
+            s_pos[j] = __ldg(a.pos + u0 + j);
+        upd_sync();
+        auto load_entries = [&](unsigned j) {
+            const uint32_t p0 = s_pos[j];
+            const int n = int(s_pos[j + 1] - p0);
+            uint2* dst = s_ent + (j % 3) * COVERL;
+#pragma unroll
+            for (int i = 0; i < KV; ++i) {
+                const int ls = cl + i * NCLV, s = 2 * ls + int(rank);
+                cp_async8_if(q == 0 && s < n, dst + ls, a.ent + p0 + s);
+            }
+        };
+        auto gather = [&](unsigned j) {
+            const int n = int(s_pos[j + 1] - s_pos[j]);
+            const uint2* e = s_ent + (j % 3) * COVERL;
+#pragma unroll
+            for (int i = 0; i < KV; ++i) {
+                const int ls = cl + i * NCLV, s = 2 * ls + int(rank);
+                const uint32_t c = s < n ? e[ls].x : kWavePrev;
+                cp_async16_if(!(c & kWavePrev), buf + ls * TPC + q, f4 + size_t(c) * Sp4 + col4);
+            }
+        };
+        load_entries(0);
+        if (L > 1)
+            load_entries(1);
+        cp_async_commit();
+        cp_async_wait_all();
+        upd_sync();
+        wait_ready(0);
+        gather(0);
+        cp_async_commit();
+        for (unsigned j = 0; j < L; ++j, ++jl) {
+            const int n = int(s_pos[j + 1] - s_pos[j]);
+            cp_async_wait_all();  // this line's own copies
+            if (j > 0)
+                mbar_wait(&barC, (jl - 1) & 1);  // the previous line's hand-overs, from both CTAs
+            else
+                upd_sync();
+            float4 x[KV];
+#pragma unroll
+            for (int i = 0; i < KV; ++i) {
+                const int ls = cl + i * NCLV, s = 2 * ls + int(rank);
+                x[i] = s < n ? buf[ls * TPC + q] : make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+            double s0, s1, s2, s3;
+            GW::template partials<KV>(x, s0, s1, s2, s3);
+            asm volatile("" ::"d"(s0), "d"(s1), "d"(s2), "d"(s3));
+#pragma unroll
+            for (int o = TPC; o < 32; o <<= 1) {
+                s0 += __shfl_xor_sync(0xFFFFFFFFu, s0, o);
+                s1 += __shfl_xor_sync(0xFFFFFFFFu, s1, o);
+                s2 += __shfl_xor_sync(0xFFFFFFFFu, s2, o);
+                s3 += __shfl_xor_sync(0xFFFFFFFFu, s3, o);
+            }
+            const int par = int(jl & 1);
+            if (lane < TPC) {
+                // this warp's partials into red[par][rank][warp] of both CTAs
+                // (the peer's copy as transaction bytes on its barrier A)
+                const size_t off = ((size_t(par) * 2 + rank) * NW + warp) * P + q * V;
+                double* r = red + off;
+                r[0] = s0;
+                r[1] = s1;
+                r[2] = s2;
+                r[3] = s3;
+                const uint32_t pr = peer_red + uint32_t(off * sizeof(double));
+                asm volatile(
+                    "st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.f64 [%0], {%1, %2}, [%3];" ::"r"(pr),
+                    "d"(s0), "d"(s1), "r"(peer_barA)
+                    : "memory");
+                asm volatile(
+                    "st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.f64 [%0], {%1, %2}, [%3];" ::"r"(pr + 16),
+                    "d"(s2), "d"(s3), "r"(peer_barA)
+                    : "memory");
+            }
+            __syncwarp();
+            if (lane == 0) {  // A (CTA-local arrivals; warp 0 expects the peer's bytes)
+                if (warp == 0)
+                    mbar_arrive_expect_local(&barA, unsigned(NW * TPC * 32));
+                else
+                    mbar_arrive_cta(&barA);
+            }
+            // while the factor warps work: entries two lines ahead; the next
+            // line's own copies once its requirements hold
+            if (j + 2 < L)
+                load_entries(j + 2);
+            bool issued = false;
+            if (j + 1 < L && ld_acquire_cta_shared(&s_ready) > j + 1) {
+                gather(j + 1);
+                issued = true;
+            }
+            cp_async_commit();
+            line_sync();  // B: factors
+            const float4 u = reinterpret_cast<const float4*>(fac)[2 * q];
+            const float4 w = reinterpret_cast<const float4*>(fac)[2 * q + 1];
+            const Scale g0{u.x, u.y}, g1{u.z, u.w}, g2{w.x, w.y}, g3{w.z, w.w};
+            const bool any = (u.y + u.w + w.y + w.w) != 0.f;
+            const uint2* e = s_ent + (j % 3) * COVERL;
+#pragma unroll
+            for (int i = 0; i < KV; ++i) {
+                const int ls = cl + i * NCLV, s = 2 * ls + int(rank);
+                const bool in = s < n;
+                const uint2 en = e[in ? ls : 0];
+                const float4 r = GW::scale4(x[i], g0, g1, g2, g3);
+                const bool hand = in && en.y != kWaveNoNext;
+                if (hand) {
+                    const uint32_t p = en.y, lp = p >> 1;
+                    if ((p & 1u) == rank)
+                        buf[lp * TPC + q] = r;
+                    else
+                        asm volatile(
+                            "st.async.shared::cluster.mbarrier::complete_tx::bytes.v4.f32 [%0], {%1, %2, %3, %4}, "
+                            "[%5];" ::"r"(peer_buf + uint32_t((lp * TPC + q) * sizeof(float4))),
+                            "f"(r.x), "f"(r.y), "f"(r.z), "f"(r.w), "r"(peer_barC)
+                            : "memory");
+                }
+                // a cell handed in by the previous line is not in global memory yet
+                st_global_cg_v4_if((any || (en.x & kWavePrev)) && in && !hand,
+                                   f4 + size_t(en.x & ~kWavePrev) * Sp4 + col4, r);
+            }
+            __syncwarp();
+            if (lane == 0) {  // C (CTA-local; warp 0 expects the peer's hand-over bytes)
+                if (warp == 0)
+                    mbar_arrive_expect_local(&barC, __ldg(a.cross + 2 * size_t(u0 + j) + rank) * 16u * TPC);
+                else
+                    mbar_arrive_cta(&barC);
+            }
+            if (!issued && j + 1 < L) {
+                wait_ready(j + 1);
+                gather(j + 1);
+                cp_async_commit();
+            }
+        }
+        mbar_wait(&barC, (jl - 1) & 1);  // the task's last line
+        task = task_boundary(false);
+    }
+}
+
+static void wave_pair_launch(const WaveArgs& a, int sms, cudaStream_t st) {
+    using namespace pair;
+    const size_t smem = 4 * words(a.lines);
+    const void* fn = reinterpret_cast<const void*>(&mart_wave_pair_kernel);
+    if (smem > attr_smem(fn)) {
+        UB_CUDA(cudaFuncSetAttribute(mart_wave_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+        note_attr_smem(fn, smem);
+    }
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.blockDim = dim3(NT);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cfg.gridDim = dim3(2 * unsigned(sms));
+    int clusters = 0;
+    UB_CUDA(cudaOccupancyMaxActiveClusters(&clusters, mart_wave_pair_kernel, &cfg));
+    if (clusters < 1)
+        throw CudaError("mart_wave_pair_kernel cannot be resident");
+    if (const char* e = std::getenv("USCG_WAVE_CLUSTERS"))
+        clusters = std::max(1, std::min(clusters, std::atoi(e)));
+    const int total = a.views * a.m.nchunks * a.n_sweeps;
+    const int nc = std::min(total, clusters);
+    cfg.gridDim = dim3(2 * unsigned(nc));
+    if (const char* e = std::getenv("USCG_FLOW_VERBOSE"); e && std::atoi(e))
+        std::fprintf(stderr, "mart_wave_kernel: P=32 pair clusters=%d smem=%zu tasks=%d\n", nc, smem, total);
+    // every cluster must be resident: tasks wait on smaller tickets only
+    UB_CUDA(cudaLaunchKernelEx(&cfg, mart_wave_pair_kernel, a));
+}
+
+bool wave_pair_enabled(const MartArgs& h) {
+    if (h.Sp / h.nchunks != 32)
+        return false;
+    const char* e = std::getenv("USCG_WAVE_PAIR");
+    return e ? std::atoi(e) != 0 : true;
+}
+
 bool wave_supported(const MartArgs& h) {
     int optin = 0, dev = 0;
     if (cudaGetDevice(&dev) != cudaSuccess ||
@@ -1737,6 +2189,7 @@ void launch_mart_wave(const MartArgs& h, const WaveSchedule& ws, unsigned* prog,
     a.ent = ws.ent;
     a.dep_off = ws.dep_off;
     a.deps = ws.deps;
+    a.cross = ws.cross;
     a.prog = prog;
     a.next = next;
     a.epoch = epoch;
@@ -1749,7 +2202,12 @@ void launch_mart_wave(const MartArgs& h, const WaveSchedule& ws, unsigned* prog,
         case 4: wave_launch_t<4>(a, sms, st); break;
         case 8: wave_launch_t<8>(a, sms, st); break;
         case 16: wave_launch_t<16>(a, sms, st); break;
-        case 32: wave_launch_t<32>(a, sms, st); break;
+        case 32:
+            if (wave_pair_enabled(h) && !prof)  // (phase stamps: the single-CTA form)
+                wave_pair_launch(a, sms, st);
+            else
+                wave_launch_t<32>(a, sms, st);
+            break;
         default: throw CudaError("mart_wave_kernel supports problem chunks of 4, 8, 16 or 32");
     }
     count_launch();

@@ -223,6 +223,34 @@ void sort_keys(unsigned long long*& a, unsigned long long*& b, uint64_t n, int b
 unsigned blocks(uint64_t n) { return unsigned((n + kNT - 1) / kNT); }
 }  // namespace
 
+namespace {
+// per line u and CTA r of a pair (wave pair kernel: position s belongs to CTA
+// s & 1): hand-overs from line u into line u + 1 that cross from the other CTA
+// into CTA r
+__global__ void __launch_bounds__(kNT) wave_cross_kernel(const uint32_t* __restrict__ pos,
+                                                         const uint2* __restrict__ ent, uint32_t* __restrict__ cross) {
+    __shared__ uint32_t c[2];
+    const uint32_t u = blockIdx.x;
+    if (threadIdx.x < 2)
+        c[threadIdx.x] = 0;
+    __syncthreads();
+    for (uint32_t k = pos[u] + threadIdx.x; k < pos[u + 1]; k += kNT) {
+        const uint32_t s = k - pos[u], p = ent[k].y;
+        if (p != 0xFFFFu && ((s ^ p) & 1u))
+            atomicAdd(&c[p & 1u], 1u);
+    }
+    __syncthreads();
+    if (threadIdx.x < 2)
+        cross[2 * size_t(u) + threadIdx.x] = c[threadIdx.x];
+}
+}  // namespace
+
+void launch_wave_cross(const uint32_t* pos, const uint2* ent, uint32_t units, uint32_t* cross, cudaStream_t st) {
+    if (units)
+        wave_cross_kernel<<<units, kNT, 0, st>>>(pos, ent, cross);
+    UB_CUDA(cudaGetLastError());
+}
+
 bool wave_build_supported(uint32_t lines, uint32_t views, uint64_t cells) {
     return lines < 0xFFFFu && views < 0x8000u && cells < (uint64_t(1) << 31);
 }

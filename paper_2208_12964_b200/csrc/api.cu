@@ -149,7 +149,9 @@ struct uscg_tracer_s {
     // requirements (mart_sweep.cu), progress counters [views * nchunks]
     bool wave_built = false;
     DevBuf<uint32_t> d_wpos, d_wdep_off, d_wdeps, d_wcross;
-    DevBuf<uint2> d_went;
+    DevBuf<uint2> d_went, d_wsplit;
+    DevBuf<uint32_t> d_wspos;
+    uint32_t wave_split_longest = 0;
     DevBuf<unsigned> d_wprog, d_wnext;
     int wave_chunks = 0;
     unsigned wave_epoch = 0;
@@ -897,6 +899,11 @@ void build_wave(uscg_tracer_s* t) {
     }
     t->d_wcross.alloc(2 * std::max<uint64_t>(units, 1));
     launch_wave_cross(t->d_wpos.p, t->d_went.p, uint32_t(units), t->d_wcross.p, t->st());
+    // entries split by cell parity (the paired-CTA form, USCG_WAVE_PAIR)
+    t->d_wsplit.alloc(std::max<uint64_t>(total, 1));
+    t->d_wspos.alloc(2 * (units + 1));
+    t->wave_split_longest =
+        gpu_wave_split(t->d_wpos.p, t->d_went.p, total, uint32_t(units), t->d_wspos.p, t->d_wsplit.p, t->st());
     t->wave_built = true;
     t->wave_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - h0).count();
     if (const char* e = std::getenv("USCG_FLOW_VERBOSE"); e && std::atoi(e))
@@ -1274,7 +1281,7 @@ uscg_status uscg_tracer_get_info(uscg_tracer t, uscg_tracer_info* info) {
         info->executor = t->executor;
         info->wave_requirements = t->wave_deps;
         info->wave_build_s = t->wave_seconds;
-        info->executor_bytes = t->d_lists.bytes() + t->d_lpos.bytes() + t->d_went.bytes() +
+        info->executor_bytes = t->d_lists.bytes() + t->d_lpos.bytes() + t->d_went.bytes() + t->d_wsplit.bytes() +
                                t->d_wpos.bytes() + t->d_wdep_off.bytes() + t->d_wdeps.bytes() +
                                t->d_order.bytes() + t->d_pred_off.bytes() + t->d_preds.bytes() +
                                t->d_succ_off.bytes() + t->d_succs.bytes() + t->d_npred_x.bytes() +
@@ -1682,6 +1689,8 @@ static void reconstruct_body(uscg_tracer t, const float* proj, int32_t problems,
             ws.dep_off = t->d_wdep_off.p;
             ws.deps = t->d_wdeps.p;
             ws.cross = t->d_wcross.p;
+            ws.spos = t->wave_split_longest <= 384 ? t->d_wspos.p : nullptr;
+            ws.split = t->d_wsplit.p;
             ws.views = t->views;
             ws.lines = t->lines;
             // USCG_SWEEP_PROFILE=<file>: per task {start, end, ready-wait, gather, reduce, store, cta}

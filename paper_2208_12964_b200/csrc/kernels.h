@@ -139,10 +139,16 @@ struct WaveSchedule {
     const uint32_t* dep_off;  // [units + 1]
     const uint32_t* deps;     // pairs {view | cross-sweep << 31, required lines of that view}
     const uint32_t* cross;    // [units][2]: pair kernel, hand-overs crossing into CTA r per line
+    const uint32_t* spos;     // [2][units + 1]: entries split by cell parity (pair kernel), or null
+    const uint2* split;
     int views;
     int lines;
 };
 void launch_wave_cross(const uint32_t* pos, const uint2* ent, uint32_t units, uint32_t* cross, cudaStream_t st);
+// entries split by cell parity (paired-CTA wave kernel): spos [2][units + 1]
+// offsets into split; returns the longest per-parity line
+uint32_t gpu_wave_split(const uint32_t* pos, const uint2* ent, uint64_t total, uint32_t units, uint32_t* spos,
+                        uint2* split, cudaStream_t st);
 // the wave executor's entries and requirements built on the device
 // (wave_build.cu) from the traced lists idx[pos[u], pos[u+1]) of every unit
 bool wave_build_supported(uint32_t lines, uint32_t views, uint64_t cells);

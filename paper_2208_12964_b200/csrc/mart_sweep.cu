@@ -1309,6 +1309,8 @@ struct WaveArgs {
     const uint32_t* dep_off;  // [units + 1]
     const uint32_t* deps;     // pairs {view | cross-sweep << 31, required line count of that view}
     const uint32_t* cross;    // [units][2]: pair kernel, hand-overs crossing into CTA r per line
+    const uint32_t* spos;     // pair kernel: [2][units + 1] offsets of the entries split by cell parity
+    const uint2* split;
     unsigned* prog;           // [views * nchunks] (pair kernel: [views * nchunks][2]): lines completed,
                               // cumulative over sweeps
     unsigned* next;           // task ticket (zeroed per launch)
@@ -1717,13 +1719,16 @@ static void wave_launch_t(const WaveArgs& a, int sms, cudaStream_t st) {
 // both CTAs' control warps check requirements. Every cell still sees the
 // line-by-line updates in order.
 namespace pair {
-constexpr int P = 32, V = 4, TPC = P / V, G = 384, NW = G / 32, NCLV = G / TPC, KV = 8;
-constexpr int COVERL = KV * NCLV;  // slots per CTA (a line covers 2 x COVERL = 768 cells)
+constexpr int V = 4, G = 384, NW = G / 32, COVERL = 384;  // slots per CTA (a line covers 2 x COVERL = 768 cells)
 constexpr int NT = G + 64;
+template <int P> struct Shape {
+    static constexpr int TPC = P / V, NCLV = G / TPC, KV = COVERL / NCLV;
+};
 
+template <int P>
 __host__ __device__ inline size_t words(int lines) {
-    // s_pos | red[2][2 CTAs][NW][P] f64 | fac[P] float2 | ent[3][COVERL] uint2 | buf[COVERL][P] f32
-    return round4(size_t(lines) + 1) + 2 * 2 * 2 * size_t(NW) * P + 2 * size_t(P) + 3 * 2 * size_t(COVERL) +
+    // s_pos | red[NW][P] f64 | fac[P] float2 | ent[3][COVERL] uint2 | buf[COVERL][P] f32
+    return round4(size_t(lines) + 1) + 2 * size_t(NW) * P + 2 * size_t(P) + 3 * 2 * size_t(COVERL) +
            size_t(COVERL) * P;
 }
 
@@ -1784,36 +1789,40 @@ __device__ __forceinline__ void st_cluster_u32(uint32_t cluster_addr, unsigned v
 }
 }  // namespace pair
 
-__global__ void __launch_bounds__(pair::NT, 2) mart_wave_pair_kernel(WaveArgs a) {
+template <int P>
+__global__ void __launch_bounds__(pair::NT, 1) mart_wave_pair_kernel(WaveArgs a) {
     using namespace pair;
+    constexpr int TPC = Shape<P>::TPC, NCLV = Shape<P>::NCLV, KV = Shape<P>::KV;
     using GW = GroupWorker<P, G>;
     using Scale = typename GW::Scale;
     extern __shared__ __align__(16) uint32_t smem[];
     __shared__ unsigned s_task, s_ready, s_done;
-    __shared__ __align__(8) uint64_t barA, barC;
+    __shared__ __align__(8) uint64_t xbar[2];
+    __shared__ __align__(16) double xred[2][2][P];  // [line parity][CTA][problem]: the CTAs' partial sums
     const uint32_t rank = cluster_rank(), peer = rank ^ 1u;
     const int nchunks = a.m.nchunks;
     const unsigned L = unsigned(a.lines);
+    const uint32_t units = uint32_t(a.views) * L;
     const int per_sweep = a.views * nchunks;
     const int total = per_sweep * a.n_sweeps;
+    // this CTA's cells (index & 1 == rank): entries split[spos[rank][u] ...]
+    const uint32_t* spos = a.spos + size_t(rank) * (units + 1);
     uint32_t* s_pos = smem;
-    double* red = reinterpret_cast<double*>(smem + round4(size_t(L) + 1));  // [2 phases][2 CTAs][NW][P]
-    float2* fac = reinterpret_cast<float2*>(red + 2 * 2 * NW * P);          // [P]
+    double* red = reinterpret_cast<double*>(smem + round4(size_t(L) + 1));  // [NW][P]
+    float2* fac = reinterpret_cast<float2*>(red + NW * P);                  // [P]
     uint2* s_ent = reinterpret_cast<uint2*>(fac + P);                         // [3][COVERL]
     float4* buf = reinterpret_cast<float4*>(s_ent + 3 * COVERL);              // [COVERL][TPC]
     const int tid = int(threadIdx.x);
-    // one progress counter per (view, chunk, CTA): each CTA publishes its
-    // own half of a line's cells; a requirement holds when both halves do
     auto prog_of = [&](int view, int chunk, uint32_t r) {
         return a.prog + (size_t(view) * nchunks + chunk) * 2 + r;
     };
     if (tid == 0) {
-        mbar_init(&barA, NW);      // + the peer's partials as transaction bytes
-        mbar_init(&barC, NW + 1);  // + the peer factor warp's arrival + the peer's hand-overs (bytes)
+        mbar_init(&xbar[0], 1);
+        mbar_init(&xbar[1], 1);
         s_ready = 0;
         s_done = 0;
     }
-    cluster_sync_all();  // barriers initialised in both CTAs
+    cluster_sync_all();
     if (rank == 0 && tid == 0) {
         const unsigned t0 = atomicAdd(a.next, 1u);
         s_task = t0;
@@ -1822,7 +1831,7 @@ __global__ void __launch_bounds__(pair::NT, 2) mart_wave_pair_kernel(WaveArgs a)
     cluster_sync_all();
     int task = int(s_task);
     auto task_boundary = [&](bool leader) {
-        cluster_sync_all();  // every thread of both CTAs: the task is done everywhere
+        cluster_sync_all();
         if (leader) {
             s_ready = 0;
             s_done = 0;
@@ -1837,28 +1846,45 @@ __global__ void __launch_bounds__(pair::NT, 2) mart_wave_pair_kernel(WaveArgs a)
     };
     auto line_sync = [] { asm volatile("bar.sync 1, %0;" ::"n"(G + 32) : "memory"); };
     auto upd_sync = [] { asm volatile("bar.sync 2, %0;" ::"n"(G) : "memory"); };
-    unsigned jl = 0;  // lines this CTA has processed (mbarrier phase = jl & 1)
     if (tid >= G && tid < G + 32) {
-        // ---- factor warp ----
+        // ---- factor warp: this CTA's partial sums, exchanged with the peer
+        // (st.async into its xred, completing its xbar), both added in the
+        // same order in both CTAs (CTA 0's first), then the line factors
+        // (solver.cpp:36-46); releases `done` after barrier C ----
         const int lane = tid & 31;
-        const uint32_t peer_barC = map_peer(&barC, peer);
+        const bool mine_lane = lane < P;  // lane l: problem l of the chunk
+        unsigned jl = 0;
         while (task < total) {
             const int v = (task % per_sweep) / nchunks, chunk = task % nchunks;
             const uint32_t u0 = uint32_t(v) * L;
-            const size_t c2 = size_t(chunk) * P + lane;
+            const size_t c2 = size_t(chunk) * P + (mine_lane ? lane : 0);
             const double pf = __ldg(a.m.p_floor + c2);
-            const bool act = __ldg(a.m.active + c2) != 0;
+            const bool act = mine_lane && __ldg(a.m.active + c2) != 0;
             float nm = __ldcs(a.m.proj + size_t(u0) * a.m.Sp + c2);
             for (unsigned j = 0; j < L; ++j, ++jl) {
                 const float m = nm;
                 if (j + 1 < L)
                     nm = __ldcs(a.m.proj + size_t(u0 + j + 1) * a.m.Sp + c2);
-                mbar_wait(&barA, jl & 1);  // both CTAs' partials of line j
-                const int par = int(jl & 1);
-                double p_bar = 0;  // CTA 0's warps first, in both CTAs
+                line_sync();  // A: the updaters' partials in red
+                double mine = 0;
+                if (mine_lane)
 #pragma unroll
-                for (int k = 0; k < 2 * NW; ++k)
-                    p_bar += red[(size_t(par) * 2 * NW + k) * P + lane];
+                    for (int w = 0; w < NW; ++w)
+                        mine += red[w * P + lane];
+                const int b = int(jl & 1);
+                uint64_t* xb = &xbar[b];
+                if (lane == 0)
+                    mbar_arrive_expect_local(xb, unsigned(P * sizeof(double)));
+                __syncwarp();
+                if (mine_lane) {
+                    xred[b][rank][lane] = mine;
+                    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b64 [%0], %1, [%2];" ::"r"(
+                                     map_peer(&xred[b][rank][lane], peer)),
+                                 "l"(__double_as_longlong(mine)), "r"(map_peer(xb, peer))
+                                 : "memory");
+                }
+                mbar_wait(xb, (jl >> 1) & 1);
+                const double p_bar = mine_lane ? xred[b][0][lane] + xred[b][1][lane] : 0.0;
                 double factor = 0;
                 if (m != 0.f && act) {
                     const double ratio = double(m) / (p_bar > pf ? p_bar : pf);
@@ -1870,12 +1896,10 @@ __global__ void __launch_bounds__(pair::NT, 2) mart_wave_pair_kernel(WaveArgs a)
                     }
                 }
                 const Scale sc = GW::scale_of(factor);
-                fac[lane] = make_float2(sc.g, sc.lb);
+                if (mine_lane)
+                    fac[lane] = make_float2(sc.g, sc.lb);
                 line_sync();  // B: factors in fac
-                // this CTA has consumed line j's partials: the peer may send line j+1's
-                if (lane == 0)
-                    mbar_arrive_remote(peer_barC);
-                mbar_wait(&barC, jl & 1);  // this CTA's stores and the peer's hand-overs of line j
+                line_sync();  // C: the line's hand-overs and stores issued
                 if (lane == 0)
                     st_release_cta_shared(&s_done, j + 1);
             }
@@ -1884,7 +1908,8 @@ __global__ void __launch_bounds__(pair::NT, 2) mart_wave_pair_kernel(WaveArgs a)
         return;
     }
     if (tid >= G + 32) {
-        // ---- control warp: requirements, and this CTA's progress ----
+        // ---- control warp: requirements (both halves of the other views'
+        // progress), and this CTA's half ----
         const int lane = tid & 31;
         while (task < total) {
             const int sweep = task / per_sweep;
@@ -1897,7 +1922,7 @@ __global__ void __launch_bounds__(pair::NT, 2) mart_wave_pair_kernel(WaveArgs a)
             __syncwarp();
             unsigned ready = 0, published = 0;
             unsigned ns = 0;
-            while (ready < L || published < L) {
+            while (published < L) {
                 bool moved = false;
                 if (ready < L) {
                     const unsigned j = ready + unsigned(lane);
@@ -1930,16 +1955,14 @@ __global__ void __launch_bounds__(pair::NT, 2) mart_wave_pair_kernel(WaveArgs a)
                             st_release_cta_shared(&s_ready, ready);
                     }
                 }
-                if (published < L) {
-                    const unsigned d = ld_acquire_cta_shared(&s_done);
-                    if (d > published) {
-                        if (lane == 0) {
-                            fence_acq_rel_gpu();
-                            st_relaxed_gpu(mine, gs * L + d);
-                        }
-                        published = d;
-                        moved = true;
+                const unsigned d = ld_acquire_cta_shared(&s_done);
+                if (d > published) {
+                    if (lane == 0) {
+                        fence_acq_rel_gpu();
+                        st_relaxed_gpu(mine, gs * L + d);
                     }
+                    published = d;
+                    moved = true;
                 }
                 if (moved) {
                     ns = 0;
@@ -1953,14 +1976,13 @@ __global__ void __launch_bounds__(pair::NT, 2) mart_wave_pair_kernel(WaveArgs a)
         }
         return;
     }
-    // ---- updaters: this CTA's slots ls = cl + i * NCLV hold the line's
-    // positions s = 2 * ls + rank ----
-    const int q = tid % TPC, cl = tid / TPC;
-    const int lane = tid & 31, warp = tid >> 5;
+    // ---- updaters: the single-CTA form's line code on this CTA's cells ----
+    GW W(a.m, smem, 0, false, 0, 0, 0);
+    (void)W;
+    const int t = tid;
+    const int q = t % TPC, cl = t / TPC;
     float4* __restrict__ f4 = reinterpret_cast<float4*>(a.m.field);
     const uint32_t Sp4 = uint32_t(a.m.Sp) / V;
-    const uint32_t peer_buf = map_peer(buf, peer), peer_red = map_peer(red, peer);
-    const uint32_t peer_barA = map_peer(&barA, peer), peer_barC = map_peer(&barC, peer);
     auto wait_ready = [&](unsigned j) {
         while (ld_acquire_cta_shared(&s_ready) <= j)
             __nanosleep(16);
@@ -1969,8 +1991,8 @@ __global__ void __launch_bounds__(pair::NT, 2) mart_wave_pair_kernel(WaveArgs a)
         const int v = (task % per_sweep) / nchunks, chunk = task % nchunks;
         const uint32_t u0 = uint32_t(v) * L;
         const uint32_t col4 = (uint32_t(chunk) * P) / V + uint32_t(q);
-        for (unsigned j = unsigned(tid); j <= L; j += G)
-            s_pos[j] = __ldg(a.pos + u0 + j);
+        for (unsigned j = unsigned(t); j <= L; j += G)
+            s_pos[j] = __ldg(spos + u0 + j);
         upd_sync();
         auto load_entries = [&](unsigned j) {
             const uint32_t p0 = s_pos[j];
@@ -1978,8 +2000,8 @@ __global__ void __launch_bounds__(pair::NT, 2) mart_wave_pair_kernel(WaveArgs a)
             uint2* dst = s_ent + (j % 3) * COVERL;
 #pragma unroll
             for (int i = 0; i < KV; ++i) {
-                const int ls = cl + i * NCLV, s = 2 * ls + int(rank);
-                cp_async8_if(q == 0 && s < n, dst + ls, a.ent + p0 + s);
+                const int s = cl + i * NCLV;
+                cp_async8_if(q == 0 && s < n, dst + s, a.split + p0 + s);
             }
         };
         auto gather = [&](unsigned j) {
@@ -1987,9 +2009,9 @@ __global__ void __launch_bounds__(pair::NT, 2) mart_wave_pair_kernel(WaveArgs a)
             const uint2* e = s_ent + (j % 3) * COVERL;
 #pragma unroll
             for (int i = 0; i < KV; ++i) {
-                const int ls = cl + i * NCLV, s = 2 * ls + int(rank);
-                const uint32_t c = s < n ? e[ls].x : kWavePrev;
-                cp_async16_if(!(c & kWavePrev), buf + ls * TPC + q, f4 + size_t(c) * Sp4 + col4);
+                const int s = cl + i * NCLV;
+                const uint32_t c = s < n ? e[s].x : kWavePrev;
+                cp_async16_if(!(c & kWavePrev), buf + s * TPC + q, f4 + size_t(c) * Sp4 + col4);
             }
         };
         load_entries(0);
@@ -2001,18 +2023,14 @@ __global__ void __launch_bounds__(pair::NT, 2) mart_wave_pair_kernel(WaveArgs a)
         wait_ready(0);
         gather(0);
         cp_async_commit();
-        for (unsigned j = 0; j < L; ++j, ++jl) {
+        for (unsigned j = 0; j < L; ++j) {
             const int n = int(s_pos[j + 1] - s_pos[j]);
-            cp_async_wait_all();  // this line's own copies
-            if (j > 0)
-                mbar_wait(&barC, (jl - 1) & 1);  // the previous line's hand-overs, from both CTAs
-            else
-                upd_sync();
+            cp_async_wait_all();
             float4 x[KV];
 #pragma unroll
             for (int i = 0; i < KV; ++i) {
-                const int ls = cl + i * NCLV, s = 2 * ls + int(rank);
-                x[i] = s < n ? buf[ls * TPC + q] : make_float4(0.f, 0.f, 0.f, 0.f);
+                const int s = cl + i * NCLV;
+                x[i] = s < n ? buf[s * TPC + q] : make_float4(0.f, 0.f, 0.f, 0.f);
             }
             double s0, s1, s2, s3;
             GW::template partials<KV>(x, s0, s1, s2, s3);
@@ -2024,35 +2042,15 @@ __global__ void __launch_bounds__(pair::NT, 2) mart_wave_pair_kernel(WaveArgs a)
                 s2 += __shfl_xor_sync(0xFFFFFFFFu, s2, o);
                 s3 += __shfl_xor_sync(0xFFFFFFFFu, s3, o);
             }
-            const int par = int(jl & 1);
+            const int lane = t & 31, warp = t >> 5;
             if (lane < TPC) {
-                // this warp's partials into red[par][rank][warp] of both CTAs
-                // (the peer's copy as transaction bytes on its barrier A)
-                const size_t off = ((size_t(par) * 2 + rank) * NW + warp) * P + q * V;
-                double* r = red + off;
+                double* r = red + warp * P + q * V;
                 r[0] = s0;
                 r[1] = s1;
                 r[2] = s2;
                 r[3] = s3;
-                const uint32_t pr = peer_red + uint32_t(off * sizeof(double));
-                asm volatile(
-                    "st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.f64 [%0], {%1, %2}, [%3];" ::"r"(pr),
-                    "d"(s0), "d"(s1), "r"(peer_barA)
-                    : "memory");
-                asm volatile(
-                    "st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.f64 [%0], {%1, %2}, [%3];" ::"r"(pr + 16),
-                    "d"(s2), "d"(s3), "r"(peer_barA)
-                    : "memory");
             }
-            __syncwarp();
-            if (lane == 0) {  // A (CTA-local arrivals; warp 0 expects the peer's bytes)
-                if (warp == 0)
-                    mbar_arrive_expect_local(&barA, unsigned(NW * TPC * 32));
-                else
-                    mbar_arrive_cta(&barA);
-            }
-            // while the factor warps work: entries two lines ahead; the next
-            // line's own copies once its requirements hold
+            line_sync();  // A
             if (j + 2 < L)
                 load_entries(j + 2);
             bool issued = false;
@@ -2061,7 +2059,7 @@ __global__ void __launch_bounds__(pair::NT, 2) mart_wave_pair_kernel(WaveArgs a)
                 issued = true;
             }
             cp_async_commit();
-            line_sync();  // B: factors
+            line_sync();  // B
             const float4 u = reinterpret_cast<const float4*>(fac)[2 * q];
             const float4 w = reinterpret_cast<const float4*>(fac)[2 * q + 1];
             const Scale g0{u.x, u.y}, g1{u.z, u.w}, g2{w.x, w.y}, g3{w.z, w.w};
@@ -2069,50 +2067,37 @@ __global__ void __launch_bounds__(pair::NT, 2) mart_wave_pair_kernel(WaveArgs a)
             const uint2* e = s_ent + (j % 3) * COVERL;
 #pragma unroll
             for (int i = 0; i < KV; ++i) {
-                const int ls = cl + i * NCLV, s = 2 * ls + int(rank);
+                const int s = cl + i * NCLV;
                 const bool in = s < n;
-                const uint2 en = e[in ? ls : 0];
+                const uint2 en = e[in ? s : 0];
                 const float4 r = GW::scale4(x[i], g0, g1, g2, g3);
                 const bool hand = in && en.y != kWaveNoNext;
-                if (hand) {
-                    const uint32_t p = en.y, lp = p >> 1;
-                    if ((p & 1u) == rank)
-                        buf[lp * TPC + q] = r;
-                    else
-                        asm volatile(
-                            "st.async.shared::cluster.mbarrier::complete_tx::bytes.v4.f32 [%0], {%1, %2, %3, %4}, "
-                            "[%5];" ::"r"(peer_buf + uint32_t((lp * TPC + q) * sizeof(float4))),
-                            "f"(r.x), "f"(r.y), "f"(r.z), "f"(r.w), "r"(peer_barC)
-                            : "memory");
-                }
-                // a cell handed in by the previous line is not in global memory yet
+                st_shared_v4_if(hand, buf + int(en.y) * TPC + q, r);
                 st_global_cg_v4_if((any || (en.x & kWavePrev)) && in && !hand,
                                    f4 + size_t(en.x & ~kWavePrev) * Sp4 + col4, r);
             }
-            __syncwarp();
-            if (lane == 0) {  // C (CTA-local; warp 0 expects the peer's hand-over bytes)
-                if (warp == 0)
-                    mbar_arrive_expect_local(&barC, __ldg(a.cross + 2 * size_t(u0 + j) + rank) * 16u * TPC);
-                else
-                    mbar_arrive_cta(&barC);
-            }
+            line_sync();  // C
             if (!issued && j + 1 < L) {
                 wait_ready(j + 1);
                 gather(j + 1);
                 cp_async_commit();
             }
         }
-        mbar_wait(&barC, (jl - 1) & 1);  // the task's last line
         task = task_boundary(false);
     }
 }
 
+template <int P>
 static void wave_pair_launch(const WaveArgs& a, int sms, cudaStream_t st) {
     using namespace pair;
-    const size_t smem = 4 * words(a.lines);
-    const void* fn = reinterpret_cast<const void*>(&mart_wave_pair_kernel);
+    // one CTA per SM, so that the two CTAs of a pair use two SMs' load/store
+    // paths (two CTAs of one pair on one SM gain nothing): the request is
+    // padded past half of the SM's shared memory
+    const size_t smem = std::max<size_t>(4 * words<P>(a.lines), 120 * 1024);
+    const void* fn = reinterpret_cast<const void*>(&mart_wave_pair_kernel<P>);
     if (smem > attr_smem(fn)) {
-        UB_CUDA(cudaFuncSetAttribute(mart_wave_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+        UB_CUDA(cudaFuncSetAttribute(mart_wave_pair_kernel<P>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     int(smem)));
         note_attr_smem(fn, smem);
     }
     cudaLaunchConfig_t cfg = {};
@@ -2128,7 +2113,7 @@ static void wave_pair_launch(const WaveArgs& a, int sms, cudaStream_t st) {
     cfg.numAttrs = 1;
     cfg.gridDim = dim3(2 * unsigned(sms));
     int clusters = 0;
-    UB_CUDA(cudaOccupancyMaxActiveClusters(&clusters, mart_wave_pair_kernel, &cfg));
+    UB_CUDA(cudaOccupancyMaxActiveClusters(&clusters, mart_wave_pair_kernel<P>, &cfg));
     if (clusters < 1)
         throw CudaError("mart_wave_pair_kernel cannot be resident");
     if (const char* e = std::getenv("USCG_WAVE_CLUSTERS"))
@@ -2137,16 +2122,23 @@ static void wave_pair_launch(const WaveArgs& a, int sms, cudaStream_t st) {
     const int nc = std::min(total, clusters);
     cfg.gridDim = dim3(2 * unsigned(nc));
     if (const char* e = std::getenv("USCG_FLOW_VERBOSE"); e && std::atoi(e))
-        std::fprintf(stderr, "mart_wave_kernel: P=32 pair clusters=%d smem=%zu tasks=%d\n", nc, smem, total);
+        std::fprintf(stderr, "mart_wave_kernel: P=%d pair clusters=%d smem=%zu tasks=%d\n", P, nc, smem, total);
     // every cluster must be resident: tasks wait on smaller tickets only
-    UB_CUDA(cudaLaunchKernelEx(&cfg, mart_wave_pair_kernel, a));
+    UB_CUDA(cudaLaunchKernelEx(&cfg, mart_wave_pair_kernel<P>, a));
 }
 
+// The paired form pays when the pairs of all tasks in flight find SMs: up to
+// three 32-problem chunks (C2 per GPU at 2-8 GPUs: 3.98 vs 5.24 ms per sweep
+// at 64 problems, 3.95 vs 4.94 at 32; at 128 problems the 74 resident pairs
+// hold fewer tasks than the single-CTA form's 148: 5.88 vs 5.49 ms).
+// USCG_WAVE_PAIR=0/1 forces it off/on.
 bool wave_pair_enabled(const MartArgs& h) {
-    if (h.Sp / h.nchunks != 32)
+    const int P = h.Sp / h.nchunks;
+    if (P != 16 && P != 32)
         return false;
-    const char* e = std::getenv("USCG_WAVE_PAIR");
-    return e ? std::atoi(e) != 0 : true;
+    if (const char* e = std::getenv("USCG_WAVE_PAIR"))
+        return std::atoi(e) != 0;
+    return h.Sp <= 96;
 }
 
 bool wave_supported(const MartArgs& h) {
@@ -2190,6 +2182,8 @@ void launch_mart_wave(const MartArgs& h, const WaveSchedule& ws, unsigned* prog,
     a.dep_off = ws.dep_off;
     a.deps = ws.deps;
     a.cross = ws.cross;
+    a.spos = ws.spos;
+    a.split = ws.split;
     a.prog = prog;
     a.next = next;
     a.epoch = epoch;
@@ -2201,10 +2195,15 @@ void launch_mart_wave(const MartArgs& h, const WaveSchedule& ws, unsigned* prog,
     switch (h.Sp / h.nchunks) {
         case 4: wave_launch_t<4>(a, sms, st); break;
         case 8: wave_launch_t<8>(a, sms, st); break;
-        case 16: wave_launch_t<16>(a, sms, st); break;
+        case 16:
+            if (wave_pair_enabled(h) && !prof && ws.spos)  // (phase stamps: the single-CTA form)
+                wave_pair_launch<16>(a, sms, st);
+            else
+                wave_launch_t<16>(a, sms, st);
+            break;
         case 32:
-            if (wave_pair_enabled(h) && !prof)  // (phase stamps: the single-CTA form)
-                wave_pair_launch(a, sms, st);
+            if (wave_pair_enabled(h) && !prof && ws.spos)
+                wave_pair_launch<32>(a, sms, st);
             else
                 wave_launch_t<32>(a, sms, st);
             break;

@@ -150,6 +150,31 @@ def test_c2_verbatim_wave_twenty_sweeps(ub, orc, capfd, monkeypatch):
     _quality(ub, orc, g, spec, out[127][0].astype(np.float64), ref[3][0], truth[127], 512)
 
 
+@pytest.mark.parametrize("S,width", [(64, 32), (16, 16)])
+def test_c2_shard_per_gpu_paired_wave(ub, orc, capfd, monkeypatch, S, width):
+    """The C2 stack as one GPU of 2 / 8 holds it (64 / 16 slices): all 20
+    sweeps through the paired-CTA wave form (a view task on a 2-CTA cluster,
+    cells split by index parity, partial sums exchanged through distributed
+    shared memory), problems of the first and last slots against the oracle."""
+    from paper_2208_12964_b200 import workloads
+    monkeypatch.setenv("USCG_FLOW_VERBOSE", "1")
+    wl = workloads.make("c2", problems=S)
+    spec, geom = wl.spec, wl.geom
+    tr = ub.Tracer(geom, spec, False)
+    truth = workloads.phantom_fields(wl, S, first=64)
+    proj = workloads.add_noise(wl, ub.project_stack(tr, truth.astype(np.float32)), first=64).astype(np.float32)
+    out = ub.reconstruct_stack(proj, ub.SolverConfig(beta=wl.beta, tolerance=0, max_sweeps=wl.sweeps), tr,
+                               with_crossed=True)
+    assert f"mart_wave_kernel: P={width} pair" in capfd.readouterr().err
+    pick = [0, S - 1]
+    g, src, det = _oracle_side(orc, spec, geom)
+    ref = _oracle_many(orc, g, src, det, geom.thetas(), [proj[p] for p in pick], wl.beta, wl.sweeps)
+    for p, (want, wrep) in zip(pick, ref):
+        got, rep = out[p]
+        _check_report(rep, wrep)
+        assert _maxrel(got, want) <= RTOL, (p, _maxrel(got, want))
+
+
 def test_c3_verbatim_two_sweeps(ub, orc):
     """C3 as BASELINE states it (128 rings x 128 layers, M1 law, cone beam,
     256x256 flat panel, 36 views, lambda 0.05): two back-to-back sweeps (the

@@ -1719,17 +1719,20 @@ static void wave_launch_t(const WaveArgs& a, int sms, cudaStream_t st) {
 // both CTAs' control warps check requirements. Every cell still sees the
 // line-by-line updates in order.
 namespace pair {
-constexpr int V = 4, G = 384, NW = G / 32, COVERL = 384;  // slots per CTA (a line covers 2 x COVERL = 768 cells)
-constexpr int NT = G + 64;
-template <int P> struct Shape {
-    static constexpr int TPC = P / V, NCLV = G / TPC, KV = COVERL / NCLV;
+constexpr int V = 4, G = 384, COVERL = 384;  // updater threads per CTA; cell slots per CTA and task slot
+template <int P, int SLOTS> struct Shape {
+    static constexpr int GS = G / SLOTS;  // updaters per task slot
+    static constexpr int NWS = GS / 32, TPC = P / V, NCLV = GS / TPC, KV = COVERL / NCLV;
+    static constexpr int NTS = GS + 64;   // + factor warp + control warp
+    static constexpr int NT = SLOTS * NTS;
 };
 
-template <int P>
+// dynamic shared memory of one task slot
+template <int P, int SLOTS>
 __host__ __device__ inline size_t words(int lines) {
-    // s_pos | red[NW][P] f64 | fac[P] float2 | ent[3][COVERL] uint2 | buf[COVERL][P] f32
-    return round4(size_t(lines) + 1) + 2 * size_t(NW) * P + 2 * size_t(P) + 3 * 2 * size_t(COVERL) +
-           size_t(COVERL) * P;
+    // s_pos | red[NWS][P] f64 | fac[P] float2 | ent[3][COVERL] uint2 | buf[COVERL][P] f32
+    return round4(size_t(lines) + 1) + 2 * size_t(Shape<P, SLOTS>::NWS) * P + 2 * size_t(P) +
+           3 * 2 * size_t(COVERL) + size_t(COVERL) * P;
 }
 
 __device__ __forceinline__ uint32_t cluster_rank() {
@@ -1749,23 +1752,11 @@ __device__ __forceinline__ void mbar_init(uint64_t* b, unsigned n) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(uint32_t(__cvta_generic_to_shared(b))), "r"(n)
                  : "memory");
 }
-__device__ __forceinline__ void mbar_arrive_local(uint64_t* b) {
-    asm volatile("mbarrier.arrive.release.cluster.shared::cta.b64 _, [%0];" ::"r"(
-                     uint32_t(__cvta_generic_to_shared(b)))
-                 : "memory");
-}
-__device__ __forceinline__ void mbar_arrive_cta(uint64_t* b) {
-    asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(uint32_t(__cvta_generic_to_shared(b)))
-                 : "memory");
-}
 __device__ __forceinline__ void mbar_arrive_expect_local(uint64_t* b, unsigned tx) {
     asm volatile("mbarrier.arrive.expect_tx.release.cta.shared::cta.b64 _, [%0], %1;" ::"r"(
                      uint32_t(__cvta_generic_to_shared(b))),
                  "r"(tx)
                  : "memory");
-}
-__device__ __forceinline__ void mbar_arrive_remote(uint32_t cluster_addr) {
-    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
 }
 __device__ __forceinline__ void mbar_wait(uint64_t* b, unsigned parity) {
     asm volatile(
@@ -1774,84 +1765,92 @@ __device__ __forceinline__ void mbar_wait(uint64_t* b, unsigned parity) {
         "r"(parity)
         : "memory");
 }
-__device__ __forceinline__ void st_cluster_v4(uint32_t cluster_addr, float4 v) {
-    asm volatile("st.shared::cluster.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(cluster_addr), "f"(v.x), "f"(v.y),
-                 "f"(v.z), "f"(v.w)
+__device__ __forceinline__ void st_async_b32(uint32_t cluster_addr, unsigned v, uint32_t cluster_bar) {
+    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b32 [%0], %1, [%2];" ::"r"(cluster_addr),
+                 "r"(v), "r"(cluster_bar)
                  : "memory");
 }
-__device__ __forceinline__ double ld_cluster_f64(uint32_t cluster_addr) {
-    double v;
-    asm volatile("ld.shared::cluster.f64 %0, [%1];" : "=d"(v) : "r"(cluster_addr) : "memory");
-    return v;
+__device__ __forceinline__ void st_async_f64(uint32_t cluster_addr, double v, uint32_t cluster_bar) {
+    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b64 [%0], %1, [%2];" ::"r"(cluster_addr),
+                 "l"(__double_as_longlong(v)), "r"(cluster_bar)
+                 : "memory");
 }
-__device__ __forceinline__ void st_cluster_u32(uint32_t cluster_addr, unsigned v) {
-    asm volatile("st.shared::cluster.u32 [%0], %1;" ::"r"(cluster_addr), "r"(v) : "memory");
+__device__ __forceinline__ void named_sync(int id, int n) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
 }  // namespace pair
 
-template <int P>
-__global__ void __launch_bounds__(pair::NT, 1) mart_wave_pair_kernel(WaveArgs a) {
+// SLOTS task slots per CTA (each with its own updaters, factor warp and
+// control warp and its own half of a pair's cells): with 2, the 74 resident
+// pairs (one CTA per SM, so that a pair spans two SMs) hold 148 tasks.
+template <int P, int SLOTS>
+__global__ void __launch_bounds__(pair::Shape<P, SLOTS>::NT, 1) mart_wave_pair_kernel(WaveArgs a) {
     using namespace pair;
-    constexpr int TPC = Shape<P>::TPC, NCLV = Shape<P>::NCLV, KV = Shape<P>::KV;
-    using GW = GroupWorker<P, G>;
+    using SH = Shape<P, SLOTS>;
+    constexpr int GS = SH::GS, NWS = SH::NWS, TPC = SH::TPC, NCLV = SH::NCLV, KV = SH::KV, NTS = SH::NTS;
+    using GW = GroupWorker<P, GS>;
     using Scale = typename GW::Scale;
     extern __shared__ __align__(16) uint32_t smem[];
-    __shared__ unsigned s_task, s_ready, s_done;
-    __shared__ __align__(8) uint64_t xbar[2];
-    __shared__ __align__(16) double xred[2][2][P];  // [line parity][CTA][problem]: the CTAs' partial sums
+    __shared__ unsigned s_task[SLOTS], s_ready[SLOTS], s_done[SLOTS];
+    __shared__ __align__(8) uint64_t xbar[SLOTS][2], tbar[SLOTS];
+    __shared__ __align__(16) double xred[SLOTS][2][2][P];  // [slot][line parity][CTA][problem]
     const uint32_t rank = cluster_rank(), peer = rank ^ 1u;
     const int nchunks = a.m.nchunks;
     const unsigned L = unsigned(a.lines);
     const uint32_t units = uint32_t(a.views) * L;
     const int per_sweep = a.views * nchunks;
     const int total = per_sweep * a.n_sweeps;
+    const int tid = int(threadIdx.x);
+    const int k = tid / NTS, lt = tid % NTS;  // task slot, thread within the slot
     // this CTA's cells (index & 1 == rank): entries split[spos[rank][u] ...]
     const uint32_t* spos = a.spos + size_t(rank) * (units + 1);
-    uint32_t* s_pos = smem;
-    double* red = reinterpret_cast<double*>(smem + round4(size_t(L) + 1));  // [NW][P]
-    float2* fac = reinterpret_cast<float2*>(red + NW * P);                  // [P]
-    uint2* s_ent = reinterpret_cast<uint2*>(fac + P);                         // [3][COVERL]
-    float4* buf = reinterpret_cast<float4*>(s_ent + 3 * COVERL);              // [COVERL][TPC]
-    const int tid = int(threadIdx.x);
+    uint32_t* s_pos = smem + size_t(k) * words<P, SLOTS>(int(L));
+    double* red = reinterpret_cast<double*>(s_pos + round4(size_t(L) + 1));  // [NWS][P]
+    float2* fac = reinterpret_cast<float2*>(red + NWS * P);                  // [P]
+    uint2* s_ent = reinterpret_cast<uint2*>(fac + P);                          // [3][COVERL]
+    float4* buf = reinterpret_cast<float4*>(s_ent + 3 * COVERL);               // [COVERL][TPC]
     auto prog_of = [&](int view, int chunk, uint32_t r) {
         return a.prog + (size_t(view) * nchunks + chunk) * 2 + r;
     };
-    if (tid == 0) {
-        mbar_init(&xbar[0], 1);
-        mbar_init(&xbar[1], 1);
-        s_ready = 0;
-        s_done = 0;
+    const int id_line = 1 + 3 * k, id_upd = 2 + 3 * k, id_slot = 3 + 3 * k;
+    auto line_sync = [&] { named_sync(id_line, GS + 32); };
+    auto upd_sync = [&] { named_sync(id_upd, GS); };
+    if (lt == 0) {
+        mbar_init(&xbar[k][0], 1);
+        mbar_init(&xbar[k][1], 1);
+        mbar_init(&tbar[k], 1);
+        s_ready[k] = 0;
+        s_done[k] = 0;
     }
-    cluster_sync_all();
-    if (rank == 0 && tid == 0) {
-        const unsigned t0 = atomicAdd(a.next, 1u);
-        s_task = t0;
-        st_cluster_u32(map_peer(&s_task, peer), t0);
-    }
-    cluster_sync_all();
-    int task = int(s_task);
-    auto task_boundary = [&](bool leader) {
-        cluster_sync_all();
-        if (leader) {
-            s_ready = 0;
-            s_done = 0;
+    cluster_sync_all();  // barriers initialised in both CTAs
+    // a slot's tasks: CTA 0 takes the ticket and sends it to the peer's slot
+    unsigned taken = 0;
+    auto next_task = [&](bool first) -> int {
+        if (!first)
+            named_sync(id_slot, NTS);  // the slot's threads are done with the task
+        if (lt == GS + 32) {
+            s_ready[k] = 0;
+            s_done[k] = 0;
             if (rank == 0) {
-                const unsigned nt = atomicAdd(a.next, 1u);
-                s_task = nt;
-                st_cluster_u32(map_peer(&s_task, peer), nt);
+                const unsigned t = atomicAdd(a.next, 1u);
+                s_task[k] = t;
+                st_async_b32(map_peer(&s_task[k], peer), t, map_peer(&tbar[k], peer));
+            } else {
+                mbar_arrive_expect_local(&tbar[k], 4);
+                mbar_wait(&tbar[k], taken & 1);
             }
         }
-        cluster_sync_all();
-        return int(s_task);
+        ++taken;
+        named_sync(id_slot, NTS);
+        return int(s_task[k]);
     };
-    auto line_sync = [] { asm volatile("bar.sync 1, %0;" ::"n"(G + 32) : "memory"); };
-    auto upd_sync = [] { asm volatile("bar.sync 2, %0;" ::"n"(G) : "memory"); };
-    if (tid >= G && tid < G + 32) {
-        // ---- factor warp: this CTA's partial sums, exchanged with the peer
-        // (st.async into its xred, completing its xbar), both added in the
-        // same order in both CTAs (CTA 0's first), then the line factors
+    int task = next_task(true);
+    if (lt >= GS && lt < GS + 32) {
+        // ---- factor warp: this CTA's partial sums, exchanged with the peer's
+        // slot (st.async into its xred, completing its xbar), both added in
+        // the same order in both CTAs (CTA 0's first), then the line factors
         // (solver.cpp:36-46); releases `done` after barrier C ----
-        const int lane = tid & 31;
+        const int lane = lt & 31;
         const bool mine_lane = lane < P;  // lane l: problem l of the chunk
         unsigned jl = 0;
         while (task < total) {
@@ -1869,22 +1868,19 @@ __global__ void __launch_bounds__(pair::NT, 1) mart_wave_pair_kernel(WaveArgs a)
                 double mine = 0;
                 if (mine_lane)
 #pragma unroll
-                    for (int w = 0; w < NW; ++w)
+                    for (int w = 0; w < NWS; ++w)
                         mine += red[w * P + lane];
                 const int b = int(jl & 1);
-                uint64_t* xb = &xbar[b];
+                uint64_t* xb = &xbar[k][b];
                 if (lane == 0)
                     mbar_arrive_expect_local(xb, unsigned(P * sizeof(double)));
                 __syncwarp();
                 if (mine_lane) {
-                    xred[b][rank][lane] = mine;
-                    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b64 [%0], %1, [%2];" ::"r"(
-                                     map_peer(&xred[b][rank][lane], peer)),
-                                 "l"(__double_as_longlong(mine)), "r"(map_peer(xb, peer))
-                                 : "memory");
+                    xred[k][b][rank][lane] = mine;
+                    st_async_f64(map_peer(&xred[k][b][rank][lane], peer), mine, map_peer(xb, peer));
                 }
                 mbar_wait(xb, (jl >> 1) & 1);
-                const double p_bar = mine_lane ? xred[b][0][lane] + xred[b][1][lane] : 0.0;
+                const double p_bar = mine_lane ? xred[k][b][0][lane] + xred[k][b][1][lane] : 0.0;
                 double factor = 0;
                 if (m != 0.f && act) {
                     const double ratio = double(m) / (p_bar > pf ? p_bar : pf);
@@ -1901,16 +1897,14 @@ __global__ void __launch_bounds__(pair::NT, 1) mart_wave_pair_kernel(WaveArgs a)
                 line_sync();  // B: factors in fac
                 line_sync();  // C: the line's hand-overs and stores issued
                 if (lane == 0)
-                    st_release_cta_shared(&s_done, j + 1);
+                    st_release_cta_shared(&s_done[k], j + 1);
             }
-            task = task_boundary(false);
+            task = next_task(false);
         }
-        return;
-    }
-    if (tid >= G + 32) {
+    } else if (lt >= GS + 32) {
         // ---- control warp: requirements (both halves of the other views'
         // progress), and this CTA's half ----
-        const int lane = tid & 31;
+        const int lane = lt & 31;
         while (task < total) {
             const int sweep = task / per_sweep;
             const int v = (task % per_sweep) / nchunks, chunk = task % nchunks;
@@ -1930,12 +1924,12 @@ __global__ void __launch_bounds__(pair::NT, 1) mart_wave_pair_kernel(WaveArgs a)
                     const unsigned* last = nullptr;
                     if (j < L) {
                         const uint32_t b = __ldg(a.dep_off + u0 + j), e = __ldg(a.dep_off + u0 + j + 1);
-                        for (uint32_t k = b; k < e && ok; ++k) {
-                            const uint32_t w = __ldg(a.deps + 2 * size_t(k));
+                        for (uint32_t q2 = b; q2 < e && ok; ++q2) {
+                            const uint32_t w = __ldg(a.deps + 2 * size_t(q2));
                             const unsigned xs = w >> 31, u = w & 0x7FFFFFFFu;
                             if (gs < xs)
                                 continue;
-                            const unsigned need = (gs - xs) * L + __ldg(a.deps + 2 * size_t(k) + 1);
+                            const unsigned need = (gs - xs) * L + __ldg(a.deps + 2 * size_t(q2) + 1);
                             last = prog_of(int(u), chunk, 0);
                             ok = ld_relaxed(last) >= need && ld_relaxed(last + 1) >= need;
                         }
@@ -1952,10 +1946,10 @@ __global__ void __launch_bounds__(pair::NT, 1) mart_wave_pair_kernel(WaveArgs a)
                         ready = nr;
                         moved = true;
                         if (lane == 0)
-                            st_release_cta_shared(&s_ready, ready);
+                            st_release_cta_shared(&s_ready[k], ready);
                     }
                 }
-                const unsigned d = ld_acquire_cta_shared(&s_done);
+                const unsigned d = ld_acquire_cta_shared(&s_done[k]);
                 if (d > published) {
                     if (lane == 0) {
                         fence_acq_rel_gpu();
@@ -1972,132 +1966,132 @@ __global__ void __launch_bounds__(pair::NT, 1) mart_wave_pair_kernel(WaveArgs a)
                 }
             }
             __syncwarp();
-            task = task_boundary(lane == 0);
+            task = next_task(false);
         }
-        return;
-    }
-    // ---- updaters: the single-CTA form's line code on this CTA's cells ----
-    GW W(a.m, smem, 0, false, 0, 0, 0);
-    (void)W;
-    const int t = tid;
-    const int q = t % TPC, cl = t / TPC;
-    float4* __restrict__ f4 = reinterpret_cast<float4*>(a.m.field);
-    const uint32_t Sp4 = uint32_t(a.m.Sp) / V;
-    auto wait_ready = [&](unsigned j) {
-        while (ld_acquire_cta_shared(&s_ready) <= j)
-            __nanosleep(16);
-    };
-    while (task < total) {
-        const int v = (task % per_sweep) / nchunks, chunk = task % nchunks;
-        const uint32_t u0 = uint32_t(v) * L;
-        const uint32_t col4 = (uint32_t(chunk) * P) / V + uint32_t(q);
-        for (unsigned j = unsigned(t); j <= L; j += G)
-            s_pos[j] = __ldg(spos + u0 + j);
-        upd_sync();
-        auto load_entries = [&](unsigned j) {
-            const uint32_t p0 = s_pos[j];
-            const int n = int(s_pos[j + 1] - p0);
-            uint2* dst = s_ent + (j % 3) * COVERL;
-#pragma unroll
-            for (int i = 0; i < KV; ++i) {
-                const int s = cl + i * NCLV;
-                cp_async8_if(q == 0 && s < n, dst + s, a.split + p0 + s);
-            }
+    } else {
+        // ---- updaters: the single-CTA form's line code on this CTA's cells ----
+        const int t = lt;
+        const int q = t % TPC, cl = t / TPC;
+        float4* __restrict__ f4 = reinterpret_cast<float4*>(a.m.field);
+        const uint32_t Sp4 = uint32_t(a.m.Sp) / V;
+        auto wait_ready = [&](unsigned j) {
+            while (ld_acquire_cta_shared(&s_ready[k]) <= j)
+                __nanosleep(16);
         };
-        auto gather = [&](unsigned j) {
-            const int n = int(s_pos[j + 1] - s_pos[j]);
-            const uint2* e = s_ent + (j % 3) * COVERL;
+        while (task < total) {
+            const int v = (task % per_sweep) / nchunks, chunk = task % nchunks;
+            const uint32_t u0 = uint32_t(v) * L;
+            const uint32_t col4 = (uint32_t(chunk) * P) / V + uint32_t(q);
+            for (unsigned j = unsigned(t); j <= L; j += GS)
+                s_pos[j] = __ldg(spos + u0 + j);
+            upd_sync();
+            auto load_entries = [&](unsigned j) {
+                const uint32_t p0 = s_pos[j];
+                const int n = int(s_pos[j + 1] - p0);
+                uint2* dst = s_ent + (j % 3) * COVERL;
 #pragma unroll
-            for (int i = 0; i < KV; ++i) {
-                const int s = cl + i * NCLV;
-                const uint32_t c = s < n ? e[s].x : kWavePrev;
-                cp_async16_if(!(c & kWavePrev), buf + s * TPC + q, f4 + size_t(c) * Sp4 + col4);
-            }
-        };
-        load_entries(0);
-        if (L > 1)
-            load_entries(1);
-        cp_async_commit();
-        cp_async_wait_all();
-        upd_sync();
-        wait_ready(0);
-        gather(0);
-        cp_async_commit();
-        for (unsigned j = 0; j < L; ++j) {
-            const int n = int(s_pos[j + 1] - s_pos[j]);
-            cp_async_wait_all();
-            float4 x[KV];
+                for (int i = 0; i < KV; ++i) {
+                    const int s = cl + i * NCLV;
+                    cp_async8_if(q == 0 && s < n, dst + s, a.split + p0 + s);
+                }
+            };
+            auto gather = [&](unsigned j) {
+                const int n = int(s_pos[j + 1] - s_pos[j]);
+                const uint2* e = s_ent + (j % 3) * COVERL;
 #pragma unroll
-            for (int i = 0; i < KV; ++i) {
-                const int s = cl + i * NCLV;
-                x[i] = s < n ? buf[s * TPC + q] : make_float4(0.f, 0.f, 0.f, 0.f);
-            }
-            double s0, s1, s2, s3;
-            GW::template partials<KV>(x, s0, s1, s2, s3);
-            asm volatile("" ::"d"(s0), "d"(s1), "d"(s2), "d"(s3));
-#pragma unroll
-            for (int o = TPC; o < 32; o <<= 1) {
-                s0 += __shfl_xor_sync(0xFFFFFFFFu, s0, o);
-                s1 += __shfl_xor_sync(0xFFFFFFFFu, s1, o);
-                s2 += __shfl_xor_sync(0xFFFFFFFFu, s2, o);
-                s3 += __shfl_xor_sync(0xFFFFFFFFu, s3, o);
-            }
-            const int lane = t & 31, warp = t >> 5;
-            if (lane < TPC) {
-                double* r = red + warp * P + q * V;
-                r[0] = s0;
-                r[1] = s1;
-                r[2] = s2;
-                r[3] = s3;
-            }
-            line_sync();  // A
-            if (j + 2 < L)
-                load_entries(j + 2);
-            bool issued = false;
-            if (j + 1 < L && ld_acquire_cta_shared(&s_ready) > j + 1) {
-                gather(j + 1);
-                issued = true;
-            }
+                for (int i = 0; i < KV; ++i) {
+                    const int s = cl + i * NCLV;
+                    const uint32_t c = s < n ? e[s].x : kWavePrev;
+                    cp_async16_if(!(c & kWavePrev), buf + s * TPC + q, f4 + size_t(c) * Sp4 + col4);
+                }
+            };
+            load_entries(0);
+            if (L > 1)
+                load_entries(1);
             cp_async_commit();
-            line_sync();  // B
-            const float4 u = reinterpret_cast<const float4*>(fac)[2 * q];
-            const float4 w = reinterpret_cast<const float4*>(fac)[2 * q + 1];
-            const Scale g0{u.x, u.y}, g1{u.z, u.w}, g2{w.x, w.y}, g3{w.z, w.w};
-            const bool any = (u.y + u.w + w.y + w.w) != 0.f;
-            const uint2* e = s_ent + (j % 3) * COVERL;
+            cp_async_wait_all();
+            upd_sync();
+            wait_ready(0);
+            gather(0);
+            cp_async_commit();
+            for (unsigned j = 0; j < L; ++j) {
+                const int n = int(s_pos[j + 1] - s_pos[j]);
+                cp_async_wait_all();
+                float4 x[KV];
 #pragma unroll
-            for (int i = 0; i < KV; ++i) {
-                const int s = cl + i * NCLV;
-                const bool in = s < n;
-                const uint2 en = e[in ? s : 0];
-                const float4 r = GW::scale4(x[i], g0, g1, g2, g3);
-                const bool hand = in && en.y != kWaveNoNext;
-                st_shared_v4_if(hand, buf + int(en.y) * TPC + q, r);
-                st_global_cg_v4_if((any || (en.x & kWavePrev)) && in && !hand,
-                                   f4 + size_t(en.x & ~kWavePrev) * Sp4 + col4, r);
-            }
-            line_sync();  // C
-            if (!issued && j + 1 < L) {
-                wait_ready(j + 1);
-                gather(j + 1);
+                for (int i = 0; i < KV; ++i) {
+                    const int s = cl + i * NCLV;
+                    x[i] = s < n ? buf[s * TPC + q] : make_float4(0.f, 0.f, 0.f, 0.f);
+                }
+                double s0, s1, s2, s3;
+                GW::template partials<KV>(x, s0, s1, s2, s3);
+                asm volatile("" ::"d"(s0), "d"(s1), "d"(s2), "d"(s3));
+#pragma unroll
+                for (int o = TPC; o < 32; o <<= 1) {
+                    s0 += __shfl_xor_sync(0xFFFFFFFFu, s0, o);
+                    s1 += __shfl_xor_sync(0xFFFFFFFFu, s1, o);
+                    s2 += __shfl_xor_sync(0xFFFFFFFFu, s2, o);
+                    s3 += __shfl_xor_sync(0xFFFFFFFFu, s3, o);
+                }
+                const int lane = t & 31, warp = t >> 5;
+                if (lane < TPC) {
+                    double* r = red + warp * P + q * V;
+                    r[0] = s0;
+                    r[1] = s1;
+                    r[2] = s2;
+                    r[3] = s3;
+                }
+                line_sync();  // A
+                if (j + 2 < L)
+                    load_entries(j + 2);
+                bool issued = false;
+                if (j + 1 < L && ld_acquire_cta_shared(&s_ready[k]) > j + 1) {
+                    gather(j + 1);
+                    issued = true;
+                }
                 cp_async_commit();
+                line_sync();  // B
+                const float4 u = reinterpret_cast<const float4*>(fac)[2 * q];
+                const float4 w = reinterpret_cast<const float4*>(fac)[2 * q + 1];
+                const Scale g0{u.x, u.y}, g1{u.z, u.w}, g2{w.x, w.y}, g3{w.z, w.w};
+                const bool any = (u.y + u.w + w.y + w.w) != 0.f;
+                const uint2* e = s_ent + (j % 3) * COVERL;
+#pragma unroll
+                for (int i = 0; i < KV; ++i) {
+                    const int s = cl + i * NCLV;
+                    const bool in = s < n;
+                    const uint2 en = e[in ? s : 0];
+                    const float4 r = GW::scale4(x[i], g0, g1, g2, g3);
+                    const bool hand = in && en.y != kWaveNoNext;
+                    st_shared_v4_if(hand, buf + int(en.y) * TPC + q, r);
+                    st_global_cg_v4_if((any || (en.x & kWavePrev)) && in && !hand,
+                                       f4 + size_t(en.x & ~kWavePrev) * Sp4 + col4, r);
+                }
+                line_sync();  // C
+                if (!issued && j + 1 < L) {
+                    wait_ready(j + 1);
+                    gather(j + 1);
+                    cp_async_commit();
+                }
             }
+            task = next_task(false);
         }
-        task = task_boundary(false);
     }
+    cluster_sync_all();  // neither CTA leaves while its peer may still write its shared memory
 }
 
-template <int P>
+template <int P, int SLOTS>
 static void wave_pair_launch(const WaveArgs& a, int sms, cudaStream_t st) {
     using namespace pair;
+    using SH = Shape<P, SLOTS>;
     // one CTA per SM, so that the two CTAs of a pair use two SMs' load/store
-    // paths (two CTAs of one pair on one SM gain nothing): the request is
-    // padded past half of the SM's shared memory
-    const size_t smem = std::max<size_t>(4 * words<P>(a.lines), 120 * 1024);
-    const void* fn = reinterpret_cast<const void*>(&mart_wave_pair_kernel<P>);
+    // paths (two CTAs of one pair on one SM gain nothing): with one slot the
+    // request is padded past half of the SM's shared memory
+    const size_t smem = std::max<size_t>(4 * SLOTS * words<P, SLOTS>(a.lines), 120 * 1024);
+    auto fn_ptr = mart_wave_pair_kernel<P, SLOTS>;
+    const void* fn = reinterpret_cast<const void*>(fn_ptr);
     if (smem > attr_smem(fn)) {
-        UB_CUDA(cudaFuncSetAttribute(mart_wave_pair_kernel<P>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     int(smem)));
+        UB_CUDA(cudaFuncSetAttribute(fn_ptr, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
         note_attr_smem(fn, smem);
     }
     cudaLaunchConfig_t cfg = {};
@@ -2106,25 +2100,26 @@ static void wave_pair_launch(const WaveArgs& a, int sms, cudaStream_t st) {
     attr[0].val.clusterDim.x = 2;
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
-    cfg.blockDim = dim3(NT);
+    cfg.blockDim = dim3(SH::NT);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     cfg.gridDim = dim3(2 * unsigned(sms));
     int clusters = 0;
-    UB_CUDA(cudaOccupancyMaxActiveClusters(&clusters, mart_wave_pair_kernel<P>, &cfg));
+    UB_CUDA(cudaOccupancyMaxActiveClusters(&clusters, fn_ptr, &cfg));
     if (clusters < 1)
         throw CudaError("mart_wave_pair_kernel cannot be resident");
     if (const char* e = std::getenv("USCG_WAVE_CLUSTERS"))
         clusters = std::max(1, std::min(clusters, std::atoi(e)));
     const int total = a.views * a.m.nchunks * a.n_sweeps;
-    const int nc = std::min(total, clusters);
+    const int nc = std::min((total + SLOTS - 1) / SLOTS, clusters);
     cfg.gridDim = dim3(2 * unsigned(nc));
     if (const char* e = std::getenv("USCG_FLOW_VERBOSE"); e && std::atoi(e))
-        std::fprintf(stderr, "mart_wave_kernel: P=%d pair clusters=%d smem=%zu tasks=%d\n", P, nc, smem, total);
+        std::fprintf(stderr, "mart_wave_kernel: P=%d pair slots=%d clusters=%d smem=%zu tasks=%d\n", P, SLOTS, nc,
+                     smem, total);
     // every cluster must be resident: tasks wait on smaller tickets only
-    UB_CUDA(cudaLaunchKernelEx(&cfg, mart_wave_pair_kernel<P>, a));
+    UB_CUDA(cudaLaunchKernelEx(&cfg, fn_ptr, a));
 }
 
 // The paired form pays when the pairs of all tasks in flight find SMs: up to
@@ -2132,13 +2127,17 @@ static void wave_pair_launch(const WaveArgs& a, int sms, cudaStream_t st) {
 // at 64 problems, 3.95 vs 4.94 at 32; at 128 problems the 74 resident pairs
 // hold fewer tasks than the single-CTA form's 148: 5.88 vs 5.49 ms).
 // USCG_WAVE_PAIR=0/1 forces it off/on.
-bool wave_pair_enabled(const MartArgs& h) {
+// USCG_WAVE_PAIR: 0 the single-CTA form, 1 the paired form. Two task slots
+// per CTA (SLOTS = 2: 148 tasks on the 74 resident pairs) measured slower
+// than either (C2 6.26 ms at 128 problems, 5.53 at 32): two tasks sharing one
+// SM's load/store path gain nothing over one task per SM.
+int wave_pair_mode(const MartArgs& h) {
     const int P = h.Sp / h.nchunks;
     if (P != 16 && P != 32)
-        return false;
+        return 0;
     if (const char* e = std::getenv("USCG_WAVE_PAIR"))
-        return std::atoi(e) != 0;
-    return h.Sp <= 96;
+        return std::atoi(e) != 0 ? 1 : 0;
+    return h.Sp <= 96 ? 1 : 0;
 }
 
 bool wave_supported(const MartArgs& h) {
@@ -2196,17 +2195,22 @@ void launch_mart_wave(const MartArgs& h, const WaveSchedule& ws, unsigned* prog,
         case 4: wave_launch_t<4>(a, sms, st); break;
         case 8: wave_launch_t<8>(a, sms, st); break;
         case 16:
-            if (wave_pair_enabled(h) && !prof && ws.spos)  // (phase stamps: the single-CTA form)
-                wave_pair_launch<16>(a, sms, st);
-            else
-                wave_launch_t<16>(a, sms, st);
+        case 32: {
+            // (phase stamps: the single-CTA form)
+            const int pm = prof || !ws.spos ? 0 : wave_pair_mode(h);
+            if (h.Sp / h.nchunks == 16) {
+                if (pm)
+                    wave_pair_launch<16, 1>(a, sms, st);
+                else
+                    wave_launch_t<16>(a, sms, st);
+            } else {
+                if (pm)
+                    wave_pair_launch<32, 1>(a, sms, st);
+                else
+                    wave_launch_t<32>(a, sms, st);
+            }
             break;
-        case 32:
-            if (wave_pair_enabled(h) && !prof && ws.spos)
-                wave_pair_launch<32>(a, sms, st);
-            else
-                wave_launch_t<32>(a, sms, st);
-            break;
+        }
         default: throw CudaError("mart_wave_kernel supports problem chunks of 4, 8, 16 or 32");
     }
     count_launch();

@@ -100,7 +100,43 @@ __global__ void __launch_bounds__(NT, 1) bench(int mode, const float* __restrict
                              : "memory");
             }
             __syncthreads();
-        } else {  // one bulk store of 128 B per row
+        } else if (mode == 5) {  // 4 threads x 32 B (st.global.v8) per row
+            for (int i = t; i < rows * 4; i += NT) {
+                const int row = i / 4, q = i % 4;
+                float* dst = g + size_t(r[row]) * SP + q * 8;
+                const float4 v0 = *reinterpret_cast<const float4*>(buf + row * 32 + q * 8);
+                const float4 v1 = *reinterpret_cast<const float4*>(buf + row * 32 + q * 8 + 4);
+                asm volatile("st.global.v8.f32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(dst), "f"(v0.x),
+                             "f"(v0.y), "f"(v0.z), "f"(v0.w), "f"(v1.x), "f"(v1.y), "f"(v1.z), "f"(v1.w)
+                             : "memory");
+            }
+            __syncthreads();
+        } else if (mode == 6) {  // 4 threads x 32 B (ld.global.v8) per row into registers
+            float acc = 0.f;
+            for (int i = t; i < rows * 4; i += NT) {
+                const int row = i / 4, q = i % 4;
+                const float* src = f + size_t(r[row]) * SP + q * 8;
+                float v[8];
+                asm volatile("ld.global.v8.f32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+                             : "=f"(v[0]), "=f"(v[1]), "=f"(v[2]), "=f"(v[3]), "=f"(v[4]), "=f"(v[5]), "=f"(v[6]),
+                               "=f"(v[7])
+                             : "l"(src));
+                acc += v[0] + v[7];
+            }
+            if (acc == 12345.f)
+                g[0] = acc;
+            __syncthreads();
+        } else if (mode == 7) {  // 8 threads x float4 ld.global into registers
+            float acc = 0.f;
+            for (int i = t; i < rows * 8; i += NT) {
+                const int row = i / 8, q = i % 8;
+                const float4 v = __ldcg(reinterpret_cast<const float4*>(f + size_t(r[row]) * SP + q * 4));
+                acc += v.x + v.w;
+            }
+            if (acc == 12345.f)
+                g[0] = acc;
+            __syncthreads();
+        } else if (mode == 3) {  // one bulk store of 128 B per row
             for (int row = t; row < rows; row += NT) {
                 float* dst = g + size_t(r[row]) * SP;
                 asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], 128;" ::"l"(dst),
@@ -156,7 +192,8 @@ int main(int argc, char** argv) {
     for (auto v : ho)
         mean += double(v);
     mean /= sms;
-    const char* names[] = {"LDGSTS gather", "bulk gather", "STG store", "bulk store", "half+half"};
+    const char* names[] = {"LDGSTS gather", "bulk gather", "STG store", "bulk store", "half+half",
+                           "STG.256 store", "LDG.256 gather", "LDG.128 gather"};
     printf("%-14s rows/line %d: %.0f cycles per line (%.2f cycles per row) on %d SMs\n", names[mode], rows,
            mean / lines, mean / lines / rows, sms);
     return 0;

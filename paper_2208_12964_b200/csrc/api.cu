@@ -178,7 +178,7 @@ struct uscg_tracer_s {
     DevBuf<unsigned long long> w_clamps, w_updates, w_tmp;
     DevBuf<unsigned int> w_resid;
     // uscg_reconstruct_batch: double-buffered staging and its copy streams
-    DevBuf<float> w_bin[2], w_bout[2];
+    DevBuf<float> w_bin[4], w_bout[4];
     cudaStream_t copy_in = nullptr, copy_out = nullptr;
     // ... and two solve slots, so that one stack's solve starts while the
     // previous one drains (wave executor): a slot's per-solve workspaces and
@@ -194,7 +194,7 @@ struct uscg_tracer_s {
         unsigned wave_epoch = 0;
         cudaStream_t st = nullptr;
     };
-    SolveSlot slots[2];
+    SolveSlot slots[4];
     void swap_slot(SolveSlot& o) {
         w_proj.swap(o.w_proj);
         w_field.swap(o.w_field);
@@ -1959,7 +1959,11 @@ uscg_status uscg_reconstruct_batch(uscg_tracer t, int32_t batch, const float* co
         Events E{{}, t->copy_in, t->copy_out};
         DevBuf<float>* in = t->w_bin;
         DevBuf<float>* out = t->w_bout;
-        for (int k = 0; k < 2 && k < batch; ++k) {
+        // solve slots (and staging sets) in turn: USCG_BATCH_SLOTS, 2..4
+        int NS = 2;
+        if (const char* e = std::getenv("USCG_BATCH_SLOTS"))
+            NS = std::max(2, std::min(4, std::atoi(e)));
+        for (int k = 0; k < NS && k < batch; ++k) {
             in[k].ensure(pw + fw);
             if (!inter)
                 out[k].ensure(fw);
@@ -1980,9 +1984,9 @@ uscg_status uscg_reconstruct_batch(uscg_tracer t, int32_t batch, const float* co
         UB_CUDA(cudaEventRecord(start, st));
         UB_CUDA(cudaStreamWaitEvent(t->copy_in, start, 0));
         auto upload = [&](int b) {
-            const int k = b % 2;
-            if (b >= 2)  // in[k] is free once stack b-2 no longer needs it
-                UB_CUDA(cudaStreamWaitEvent(t->copy_in, ev_free[b - 2], 0));
+            const int k = b % NS;
+            if (b >= NS)  // in[k] is free once stack b-NS no longer needs it
+                UB_CUDA(cudaStreamWaitEvent(t->copy_in, ev_free[b - NS], 0));
             UB_CUDA(cudaMemcpyAsync(in[k].p, proj[b], sizeof(float) * pw, cudaMemcpyHostToDevice, t->copy_in));
             if (from_init)
                 UB_CUDA(cudaMemcpyAsync(in[k].p + pw, field_inout[b], sizeof(float) * fw, cudaMemcpyHostToDevice,
@@ -1996,7 +2000,7 @@ uscg_status uscg_reconstruct_batch(uscg_tracer t, int32_t batch, const float* co
         auto download = [&](int b) {
             queued_down = b + 1;
             UB_CUDA(cudaStreamWaitEvent(t->copy_out, ev_ready[b], 0));
-            const float* src = inter ? in[b % 2].p + pw : out[b % 2].p;
+            const float* src = inter ? in[b % NS].p + pw : out[b % NS].p;
             UB_CUDA(cudaMemcpyAsync(field_inout[b], src, sizeof(float) * fw, cudaMemcpyDeviceToHost,
                                     t->copy_out));
             UB_CUDA(cudaEventRecord(ev_out[b], t->copy_out));
@@ -2025,9 +2029,9 @@ uscg_status uscg_reconstruct_batch(uscg_tracer t, int32_t batch, const float* co
         upload(0);
         for (int b = 0; b < batch; ++b) {
             failed = b;
-            const int k = b % 2;
-            if (overlap && b >= 2)
-                finish(b - 2);  // stack b-2 (this slot's previous solve) finished
+            const int k = b % NS;
+            if (overlap && b >= NS)
+                finish(b - NS);  // stack b-NS (this slot's previous solve) finished
 
             struct SlotIn {  // the slot's workspaces and stream, swapped in for this solve
                 uscg_tracer_s* t;
@@ -2069,8 +2073,8 @@ uscg_status uscg_reconstruct_batch(uscg_tracer t, int32_t batch, const float* co
             reconstruct_body(t, d_proj, S, cfg, d_field, from_init, reports ? reports + size_t(b) * S : nullptr,
                              USCG_DEVICE_POINTERS | USCG_LAYOUT_INTERLEAVED, &hook, overlap ? &fin[b] : nullptr);
             if (!inter) {
-                if (b >= 2)  // out[k] is free once stack b-2 has been downloaded
-                    UB_CUDA(cudaStreamWaitEvent(cur, ev_out[b - 2], 0));
+                if (b >= NS)  // out[k] is free once stack b-NS has been downloaded
+                    UB_CUDA(cudaStreamWaitEvent(cur, ev_out[b - NS], 0));
                 launch_from_interleaved(t->w_field.p, out[k].p, cells, S, Sp, cur);
             }
             UB_CUDA(cudaEventRecord(ev_ready[b], cur));
@@ -2094,7 +2098,7 @@ uscg_status uscg_reconstruct_batch(uscg_tracer t, int32_t batch, const float* co
             throw;
         }
         if (overlap)
-            for (int b = std::max(0, batch - 2); b < batch; ++b)
+            for (int b = std::max(0, batch - NS); b < batch; ++b)
                 finish(b);
         download(batch - 1);
         // the context stream ends after the last download (callers time on it)

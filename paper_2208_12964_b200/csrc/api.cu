@@ -171,7 +171,6 @@ struct uscg_tracer_s {
     DevBuf<uint32_t> d_tlevel;
     int tile_levels = 0;
     // MART workspace
-    DevBuf<MartArgs> d_args;
     DevBuf<float> w_field, w_proj, w_prev, w_stage;
     DevBuf<double> w_pfloor, w_stats;
     DevBuf<uint8_t> w_active;
@@ -188,7 +187,6 @@ struct uscg_tracer_s {
         DevBuf<double> w_stats, w_pfloor;
         DevBuf<uint8_t> w_active;
         DevBuf<unsigned long long> w_clamps, w_updates, w_tmp;
-        DevBuf<MartArgs> d_args;
         DevBuf<unsigned> d_wprog, d_wnext;
         int wave_chunks = 0;
         unsigned wave_epoch = 0;
@@ -204,7 +202,6 @@ struct uscg_tracer_s {
         w_clamps.swap(o.w_clamps);
         w_updates.swap(o.w_updates);
         w_tmp.swap(o.w_tmp);
-        d_args.swap(o.d_args);
         d_wprog.swap(o.d_wprog);
         d_wnext.swap(o.d_wnext);
         std::swap(wave_chunks, o.wave_chunks);
@@ -1597,7 +1594,6 @@ static void reconstruct_body(uscg_tracer t, const float* proj, int32_t problems,
         active[p] = !all_zero[p];
     }
 
-    build_schedule(t);
     const bool track = cfg->tolerance > 0;
     if (track || reports)
         ensure_crossed(t);
@@ -1631,8 +1627,6 @@ static void reconstruct_body(uscg_tracer t, const float* proj, int32_t problems,
     h.max_recs = t->max_recs;
     h.max_cells = t->max_cells;
     h.run = t->run;
-    t->d_args.ensure(1);
-    UB_CUDA(cudaMemcpyAsync(t->d_args.p, &h, sizeof(MartArgs), cudaMemcpyHostToDevice, st));
     int exec_mode = mart_mode();
     // auto: the wave executor for stacks (P >= 4); the tile executor for one
     // problem that fits in one CTA's shared memory; else flow
@@ -1654,6 +1648,12 @@ static void reconstruct_body(uscg_tracer t, const float* proj, int32_t problems,
             t->wave_epoch = 0;
         }
     }
+    if (exec_mode == 0) {
+        // the run DAG of the dataflow executor (the wave and tile executors
+        // build their own schedules)
+        build_schedule(t);
+        h.run = t->run;
+    }
     if (exec_mode == 0 && P == 1)
         build_lists(t);  // once per geometry, outside the timed sweeps
     if (exec_mode == 0 && t->done_chunks != h.nchunks) {
@@ -1663,8 +1663,6 @@ static void reconstruct_body(uscg_tracer t, const float* proj, int32_t problems,
         t->done_chunks = h.nchunks;
         t->epoch = 0;
     }
-    const int levels = int(t->level_off.size()) - 1;
-
     std::vector<int> sweeps(S, 0), converged(S, 0);
     std::vector<std::vector<double>> resid(S);
     if (track)

@@ -148,10 +148,11 @@ struct uscg_tracer_s {
     // wave executor (2D stacks): every line's traced list and its other-view
     // requirements (mart_sweep.cu), progress counters [views * nchunks]
     bool wave_built = false;
-    DevBuf<uint32_t> d_wpos, d_wdep_off, d_wdeps, d_wcross;
+    DevBuf<uint32_t> d_wpos, d_wdep_off, d_wdeps;
     DevBuf<uint2> d_went, d_wsplit;
     DevBuf<uint32_t> d_wspos;
     uint32_t wave_split_longest = 0;
+    int wave_split_parts = 0;
     DevBuf<unsigned> d_wprog, d_wnext;
     int wave_chunks = 0;
     unsigned wave_epoch = 0;
@@ -894,18 +895,24 @@ void build_wave(uscg_tracer_s* t) {
         upload(t->d_wdeps, deps);
         t->wave_deps = deps.size() / 2;
     }
-    t->d_wcross.alloc(2 * std::max<uint64_t>(units, 1));
-    launch_wave_cross(t->d_wpos.p, t->d_went.p, uint32_t(units), t->d_wcross.p, t->st());
-    // entries split by cell parity (the paired-CTA form, USCG_WAVE_PAIR)
-    t->d_wsplit.alloc(std::max<uint64_t>(total, 1));
-    t->d_wspos.alloc(2 * (units + 1));
-    t->wave_split_longest =
-        gpu_wave_split(t->d_wpos.p, t->d_went.p, total, uint32_t(units), t->d_wspos.p, t->d_wsplit.p, t->st());
     t->wave_built = true;
     t->wave_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - h0).count();
     if (const char* e = std::getenv("USCG_FLOW_VERBOSE"); e && std::atoi(e))
         std::fprintf(stderr, "wave schedule: %llu traced entries, %llu requirements, %.3f s\n",
                      (unsigned long long)total, (unsigned long long)t->wave_deps, t->wave_seconds);
+}
+
+// The wave entries split by cell index mod `parts` for the clustered wave
+// kernel (built on first use per cluster size).
+void ensure_split(uscg_tracer_s* t, int parts) {
+    if (t->wave_split_parts == parts)
+        return;
+    const uint64_t units = t->units(), total = t->cells_per_sweep;
+    t->d_wsplit.alloc(std::max<uint64_t>(total, 1));
+    t->d_wspos.alloc(size_t(parts) * (units + 1));
+    t->wave_split_longest = gpu_wave_split(t->d_wpos.p, t->d_went.p, total, uint32_t(units), uint32_t(parts),
+                                           t->d_wspos.p, t->d_wsplit.p, t->st());
+    t->wave_split_parts = parts;
 }
 
 // The flow executor's one-problem lists (USCG_FLOW_LISTS=0 disables): the
@@ -1641,9 +1648,9 @@ static void reconstruct_body(uscg_tracer t, const float* proj, int32_t problems,
         build_wave(t);
         if (t->wave_chunks != h.nchunks) {
             const uint64_t n = uint64_t(t->views) * uint64_t(h.nchunks);
-            t->d_wprog.alloc(2 * n);  // the pair kernel keeps one counter per CTA
+            t->d_wprog.alloc(4 * n);  // the clustered kernel keeps one counter per CTA (up to 4)
             t->d_wnext.alloc(1);
-            UB_CUDA(cudaMemsetAsync(t->d_wprog.p, 0, sizeof(unsigned) * 2 * n, st));
+            UB_CUDA(cudaMemsetAsync(t->d_wprog.p, 0, sizeof(unsigned) * 4 * n, st));
             t->wave_chunks = h.nchunks;
             t->wave_epoch = 0;
         }
@@ -1686,8 +1693,10 @@ static void reconstruct_body(uscg_tracer t, const float* proj, int32_t problems,
             ws.ent = t->d_went.p;
             ws.dep_off = t->d_wdep_off.p;
             ws.deps = t->d_wdeps.p;
-            ws.cross = t->d_wcross.p;
-            ws.spos = t->wave_split_longest <= 384 ? t->d_wspos.p : nullptr;
+            ws.parts = wave_cluster_size(h);
+            if (ws.parts > 1)
+                ensure_split(t, ws.parts);
+            ws.spos = ws.parts > 1 && t->wave_split_longest <= 384 ? t->d_wspos.p : nullptr;
             ws.split = t->d_wsplit.p;
             ws.views = t->views;
             ws.lines = t->lines;

@@ -138,17 +138,16 @@ struct WaveSchedule {
                               //  position in the next line of the view (0xFFFF: none)}
     const uint32_t* dep_off;  // [units + 1]
     const uint32_t* deps;     // pairs {view | cross-sweep << 31, required lines of that view}
-    const uint32_t* cross;    // [units][2]: pair kernel, hand-overs crossing into CTA r per line
-    const uint32_t* spos;     // [2][units + 1]: entries split by cell parity (pair kernel), or null
-    const uint2* split;
+    const uint32_t* spos;     // [parts][units + 1]: entries split by cell index mod parts (clustered
+    const uint2* split;       //   wave kernel), or null
+    int parts;                // CTAs per cluster of the split (2 or 4)
     int views;
     int lines;
 };
-void launch_wave_cross(const uint32_t* pos, const uint2* ent, uint32_t units, uint32_t* cross, cudaStream_t st);
-// entries split by cell parity (paired-CTA wave kernel): spos [2][units + 1]
-// offsets into split; returns the longest per-parity line
-uint32_t gpu_wave_split(const uint32_t* pos, const uint2* ent, uint64_t total, uint32_t units, uint32_t* spos,
-                        uint2* split, cudaStream_t st);
+// entries split by cell index mod parts (clustered wave kernel): spos
+// [parts][units + 1] offsets into split; returns the longest per-part line
+uint32_t gpu_wave_split(const uint32_t* pos, const uint2* ent, uint64_t total, uint32_t units, uint32_t parts,
+                        uint32_t* spos, uint2* split, cudaStream_t st);
 // the wave executor's entries and requirements built on the device
 // (wave_build.cu) from the traced lists idx[pos[u], pos[u+1]) of every unit
 bool wave_build_supported(uint32_t lines, uint32_t views, uint64_t cells);
@@ -156,6 +155,7 @@ void gpu_wave_build(const uint32_t* pos, const uint32_t* idx, uint64_t total, ui
                     uint32_t views, uint64_t cells, uint2* ent, std::vector<uint32_t>& dep_off,
                     std::vector<uint32_t>& deps, cudaStream_t st);
 bool wave_supported(const MartArgs& h);
+int wave_cluster_size(const MartArgs& h);  // CTAs per view task of the wave executor (1, 2 or 4)
 bool wave_fits_smem(const MartArgs& h, int lines);
 size_t wave_smem_bytes(const MartArgs& m, int lines);
 // prog: [views * nchunks] cumulative line counters; epoch: 0-based global

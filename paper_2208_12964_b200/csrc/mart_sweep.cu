@@ -1308,7 +1308,6 @@ struct WaveArgs {
     const uint2* ent;         // per traced entry {cell | in previous line << 31, position in next line}
     const uint32_t* dep_off;  // [units + 1]
     const uint32_t* deps;     // pairs {view | cross-sweep << 31, required line count of that view}
-    const uint32_t* cross;    // [units][2]: pair kernel, hand-overs crossing into CTA r per line
     const uint32_t* spos;     // pair kernel: [2][units + 1] offsets of the entries split by cell parity
     const uint2* split;
     unsigned* prog;           // [views * nchunks] (pair kernel: [views * nchunks][2]): lines completed,
@@ -1780,10 +1779,10 @@ __device__ __forceinline__ void named_sync(int id, int n) {
 }
 }  // namespace pair
 
-// SLOTS task slots per CTA (each with its own updaters, factor warp and
-// control warp and its own half of a pair's cells): with 2, the 74 resident
-// pairs (one CTA per SM, so that a pair spans two SMs) hold 148 tasks.
-template <int P, int SLOTS>
+// CL CTAs per cluster (a view task's cells split by index mod CL), SLOTS
+// task slots per CTA (each with its own updaters, factor warp and control
+// warp; only SLOTS = 1 is dispatched, see wave_cluster_size).
+template <int P, int SLOTS, int CL>
 __global__ void __launch_bounds__(pair::Shape<P, SLOTS>::NT, 1) mart_wave_pair_kernel(WaveArgs a) {
     using namespace pair;
     using SH = Shape<P, SLOTS>;
@@ -1793,8 +1792,8 @@ __global__ void __launch_bounds__(pair::Shape<P, SLOTS>::NT, 1) mart_wave_pair_k
     extern __shared__ __align__(16) uint32_t smem[];
     __shared__ unsigned s_task[SLOTS], s_ready[SLOTS], s_done[SLOTS];
     __shared__ __align__(8) uint64_t xbar[SLOTS][2], tbar[SLOTS];
-    __shared__ __align__(16) double xred[SLOTS][2][2][P];  // [slot][line parity][CTA][problem]
-    const uint32_t rank = cluster_rank(), peer = rank ^ 1u;
+    __shared__ __align__(16) double xred[SLOTS][2][CL][P];  // [slot][line parity][CTA][problem]
+    const uint32_t rank = cluster_rank();
     const int nchunks = a.m.nchunks;
     const unsigned L = unsigned(a.lines);
     const uint32_t units = uint32_t(a.views) * L;
@@ -1802,15 +1801,17 @@ __global__ void __launch_bounds__(pair::Shape<P, SLOTS>::NT, 1) mart_wave_pair_k
     const int total = per_sweep * a.n_sweeps;
     const int tid = int(threadIdx.x);
     const int k = tid / NTS, lt = tid % NTS;  // task slot, thread within the slot
-    // this CTA's cells (index & 1 == rank): entries split[spos[rank][u] ...]
+    // this CTA's cells (index % CL == rank): entries split[spos[rank][u] ...]
     const uint32_t* spos = a.spos + size_t(rank) * (units + 1);
     uint32_t* s_pos = smem + size_t(k) * words<P, SLOTS>(int(L));
     double* red = reinterpret_cast<double*>(s_pos + round4(size_t(L) + 1));  // [NWS][P]
     float2* fac = reinterpret_cast<float2*>(red + NWS * P);                  // [P]
     uint2* s_ent = reinterpret_cast<uint2*>(fac + P);                          // [3][COVERL]
     float4* buf = reinterpret_cast<float4*>(s_ent + 3 * COVERL);               // [COVERL][TPC]
+    // one progress counter per (view, chunk, CTA): each CTA publishes its own
+    // part of a line's cells; a requirement holds when every part does
     auto prog_of = [&](int view, int chunk, uint32_t r) {
-        return a.prog + (size_t(view) * nchunks + chunk) * 2 + r;
+        return a.prog + (size_t(view) * nchunks + chunk) * CL + r;
     };
     const int id_line = 1 + 3 * k, id_upd = 2 + 3 * k, id_slot = 3 + 3 * k;
     auto line_sync = [&] { named_sync(id_line, GS + 32); };
@@ -1834,7 +1835,8 @@ __global__ void __launch_bounds__(pair::Shape<P, SLOTS>::NT, 1) mart_wave_pair_k
             if (rank == 0) {
                 const unsigned t = atomicAdd(a.next, 1u);
                 s_task[k] = t;
-                st_async_b32(map_peer(&s_task[k], peer), t, map_peer(&tbar[k], peer));
+                for (uint32_t r = 1; r < uint32_t(CL); ++r)
+                    st_async_b32(map_peer(&s_task[k], r), t, map_peer(&tbar[k], r));
             } else {
                 mbar_arrive_expect_local(&tbar[k], 4);
                 mbar_wait(&tbar[k], taken & 1);
@@ -1873,14 +1875,20 @@ __global__ void __launch_bounds__(pair::Shape<P, SLOTS>::NT, 1) mart_wave_pair_k
                 const int b = int(jl & 1);
                 uint64_t* xb = &xbar[k][b];
                 if (lane == 0)
-                    mbar_arrive_expect_local(xb, unsigned(P * sizeof(double)));
+                    mbar_arrive_expect_local(xb, unsigned((CL - 1) * P * sizeof(double)));
                 __syncwarp();
                 if (mine_lane) {
                     xred[k][b][rank][lane] = mine;
-                    st_async_f64(map_peer(&xred[k][b][rank][lane], peer), mine, map_peer(xb, peer));
+                    for (uint32_t r = 0; r < uint32_t(CL); ++r)
+                        if (r != rank)
+                            st_async_f64(map_peer(&xred[k][b][rank][lane], r), mine, map_peer(xb, r));
                 }
                 mbar_wait(xb, (jl >> 1) & 1);
-                const double p_bar = mine_lane ? xred[k][b][0][lane] + xred[k][b][1][lane] : 0.0;
+                double p_bar = 0.0;  // the CTAs' partials in CTA order, the same in every CTA
+                if (mine_lane)
+#pragma unroll
+                    for (int r = 0; r < CL; ++r)
+                        p_bar += xred[k][b][r][lane];
                 double factor = 0;
                 if (m != 0.f && act) {
                     const double ratio = double(m) / (p_bar > pf ? p_bar : pf);
@@ -1911,7 +1919,7 @@ __global__ void __launch_bounds__(pair::Shape<P, SLOTS>::NT, 1) mart_wave_pair_k
             const unsigned gs = a.epoch + unsigned(sweep);
             unsigned* mine = prog_of(v, chunk, rank);
             const uint32_t u0 = uint32_t(v) * L;
-            if (lane < 2 && gs > 0)
+            if (lane < CL && gs > 0)
                 spin_until_geq(prog_of(v, chunk, uint32_t(lane)), gs * L);
             __syncwarp();
             unsigned ready = 0, published = 0;
@@ -1931,17 +1939,19 @@ __global__ void __launch_bounds__(pair::Shape<P, SLOTS>::NT, 1) mart_wave_pair_k
                                 continue;
                             const unsigned need = (gs - xs) * L + __ldg(a.deps + 2 * size_t(q2) + 1);
                             last = prog_of(int(u), chunk, 0);
-                            ok = ld_relaxed(last) >= need && ld_relaxed(last + 1) >= need;
+#pragma unroll
+                            for (int r = 0; r < CL; ++r)
+                                ok = ok && ld_relaxed(last + r) >= need;
                         }
                     }
                     const unsigned bad = __ballot_sync(0xFFFFFFFFu, !ok);
                     const unsigned adv = bad ? unsigned(__ffs(bad) - 1) : 32u;
                     const unsigned nr = min(L, ready + adv);
                     if (nr > ready) {
-                        if (unsigned(lane) < adv && last != nullptr) {
-                            (void)ld_acquire(last);
-                            (void)ld_acquire(last + 1);
-                        }
+                        if (unsigned(lane) < adv && last != nullptr)
+#pragma unroll
+                            for (int r = 0; r < CL; ++r)
+                                (void)ld_acquire(last + r);
                         __syncwarp();
                         ready = nr;
                         moved = true;
@@ -2080,7 +2090,7 @@ __global__ void __launch_bounds__(pair::Shape<P, SLOTS>::NT, 1) mart_wave_pair_k
     cluster_sync_all();  // neither CTA leaves while its peer may still write its shared memory
 }
 
-template <int P, int SLOTS>
+template <int P, int SLOTS, int CL>
 static void wave_pair_launch(const WaveArgs& a, int sms, cudaStream_t st) {
     using namespace pair;
     using SH = Shape<P, SLOTS>;
@@ -2088,7 +2098,7 @@ static void wave_pair_launch(const WaveArgs& a, int sms, cudaStream_t st) {
     // paths (two CTAs of one pair on one SM gain nothing): with one slot the
     // request is padded past half of the SM's shared memory
     const size_t smem = std::max<size_t>(4 * SLOTS * words<P, SLOTS>(a.lines), 120 * 1024);
-    auto fn_ptr = mart_wave_pair_kernel<P, SLOTS>;
+    auto fn_ptr = mart_wave_pair_kernel<P, SLOTS, CL>;
     const void* fn = reinterpret_cast<const void*>(fn_ptr);
     if (smem > attr_smem(fn)) {
         UB_CUDA(cudaFuncSetAttribute(fn_ptr, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
@@ -2097,7 +2107,7 @@ static void wave_pair_launch(const WaveArgs& a, int sms, cudaStream_t st) {
     cudaLaunchConfig_t cfg = {};
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.x = CL;
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
     cfg.blockDim = dim3(SH::NT);
@@ -2105,7 +2115,7 @@ static void wave_pair_launch(const WaveArgs& a, int sms, cudaStream_t st) {
     cfg.stream = st;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    cfg.gridDim = dim3(2 * unsigned(sms));
+    cfg.gridDim = dim3(CL * unsigned(sms / CL));
     int clusters = 0;
     UB_CUDA(cudaOccupancyMaxActiveClusters(&clusters, fn_ptr, &cfg));
     if (clusters < 1)
@@ -2114,30 +2124,34 @@ static void wave_pair_launch(const WaveArgs& a, int sms, cudaStream_t st) {
         clusters = std::max(1, std::min(clusters, std::atoi(e)));
     const int total = a.views * a.m.nchunks * a.n_sweeps;
     const int nc = std::min((total + SLOTS - 1) / SLOTS, clusters);
-    cfg.gridDim = dim3(2 * unsigned(nc));
+    cfg.gridDim = dim3(CL * unsigned(nc));
     if (const char* e = std::getenv("USCG_FLOW_VERBOSE"); e && std::atoi(e))
-        std::fprintf(stderr, "mart_wave_kernel: P=%d pair slots=%d clusters=%d smem=%zu tasks=%d\n", P, SLOTS, nc,
-                     smem, total);
+        std::fprintf(stderr, "mart_wave_kernel: P=%d pair cluster=%d slots=%d clusters=%d smem=%zu tasks=%d\n", P, CL,
+                     SLOTS, nc, smem, total);
     // every cluster must be resident: tasks wait on smaller tickets only
     UB_CUDA(cudaLaunchKernelEx(&cfg, fn_ptr, a));
 }
 
-// The paired form pays when the pairs of all tasks in flight find SMs: up to
-// three 32-problem chunks (C2 per GPU at 2-8 GPUs: 3.98 vs 5.24 ms per sweep
-// at 64 problems, 3.95 vs 4.94 at 32; at 128 problems the 74 resident pairs
-// hold fewer tasks than the single-CTA form's 148: 5.88 vs 5.49 ms).
-// USCG_WAVE_PAIR=0/1 forces it off/on.
-// USCG_WAVE_PAIR: 0 the single-CTA form, 1 the paired form. Two task slots
-// per CTA (SLOTS = 2: 148 tasks on the 74 resident pairs) measured slower
-// than either (C2 6.26 ms at 128 problems, 5.53 at 32): two tasks sharing one
-// SM's load/store path gain nothing over one task per SM.
-int wave_pair_mode(const MartArgs& h) {
+// CTAs per view task (USCG_WAVE_PAIR = 0 single, 1 or 2 pairs, 4 clusters of
+// four forces it). Pairs pay when the pairs of all tasks in flight find SMs:
+// up to three 32-problem chunks (C2 per GPU at 2-8 GPUs, ms per sweep:
+// 16 problems 2.87 vs 4.76 single, 32: 3.72 vs 4.84, 64: 4.06 vs 4.92). At
+// 128 problems the single-CTA form holds twice the tasks of the 74 resident
+// pairs (pairs 5.38 vs 5.44) and stays. Clusters of four measured slower than
+// pairs at every size (3.22, 4.05, 4.53 ms: three partial exchanges per line
+// cost more than the halved per-CTA row traffic saves) and are opt-in only.
+// Two task slots per CTA measured slower (6.26 ms at 128 problems, 5.53 at
+// 32: two tasks sharing one SM's load/store path gain nothing) and are not
+// dispatched.
+int wave_cluster_size(const MartArgs& h) {
     const int P = h.Sp / h.nchunks;
     if (P != 16 && P != 32)
-        return 0;
-    if (const char* e = std::getenv("USCG_WAVE_PAIR"))
-        return std::atoi(e) != 0 ? 1 : 0;
-    return h.Sp <= 96 ? 1 : 0;
+        return 1;
+    if (const char* e = std::getenv("USCG_WAVE_PAIR")) {
+        const int c = std::atoi(e);
+        return c >= 4 ? 4 : c >= 2 ? 2 : c == 1 ? 2 : 1;
+    }
+    return h.Sp <= 96 ? 2 : 1;
 }
 
 bool wave_supported(const MartArgs& h) {
@@ -2156,7 +2170,6 @@ bool wave_supported(const MartArgs& h) {
     }
     return h.max_cells <= cover && h.max_cells < int(kWaveNoNext);
 }
-
 bool wave_fits_smem(const MartArgs& h, int lines) {
     int optin = 0, dev = 0;
     UB_CUDA(cudaGetDevice(&dev));
@@ -2180,7 +2193,6 @@ void launch_mart_wave(const MartArgs& h, const WaveSchedule& ws, unsigned* prog,
     a.ent = ws.ent;
     a.dep_off = ws.dep_off;
     a.deps = ws.deps;
-    a.cross = ws.cross;
     a.spos = ws.spos;
     a.split = ws.split;
     a.prog = prog;
@@ -2197,15 +2209,19 @@ void launch_mart_wave(const MartArgs& h, const WaveSchedule& ws, unsigned* prog,
         case 16:
         case 32: {
             // (phase stamps: the single-CTA form)
-            const int pm = prof || !ws.spos ? 0 : wave_pair_mode(h);
+            const int cl = prof || !ws.spos ? 1 : ws.parts;
             if (h.Sp / h.nchunks == 16) {
-                if (pm)
-                    wave_pair_launch<16, 1>(a, sms, st);
+                if (cl == 2)
+                    wave_pair_launch<16, 1, 2>(a, sms, st);
+                else if (cl == 4)
+                    wave_pair_launch<16, 1, 4>(a, sms, st);
                 else
                     wave_launch_t<16>(a, sms, st);
             } else {
-                if (pm)
-                    wave_pair_launch<32, 1>(a, sms, st);
+                if (cl == 2)
+                    wave_pair_launch<32, 1, 2>(a, sms, st);
+                else if (cl == 4)
+                    wave_pair_launch<32, 1, 4>(a, sms, st);
                 else
                     wave_launch_t<32>(a, sms, st);
             }

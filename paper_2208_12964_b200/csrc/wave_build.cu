@@ -224,73 +224,47 @@ void sort_keys(unsigned long long*& a, unsigned long long*& b, uint64_t n, int b
 unsigned blocks(uint64_t n) { return unsigned((n + kNT - 1) / kNT); }
 }  // namespace
 
-namespace {
-// per line u and CTA r of a pair (wave pair kernel: position s belongs to CTA
-// s & 1): hand-overs from line u into line u + 1 that cross from the other CTA
-// into CTA r
-__global__ void __launch_bounds__(kNT) wave_cross_kernel(const uint32_t* __restrict__ pos,
-                                                         const uint2* __restrict__ ent, uint32_t* __restrict__ cross) {
-    __shared__ uint32_t c[2];
-    const uint32_t u = blockIdx.x;
-    if (threadIdx.x < 2)
-        c[threadIdx.x] = 0;
-    __syncthreads();
-    for (uint32_t k = pos[u] + threadIdx.x; k < pos[u + 1]; k += kNT) {
-        const uint32_t s = k - pos[u], p = ent[k].y;
-        if (p != 0xFFFFu && ((s ^ p) & 1u))
-            atomicAdd(&c[p & 1u], 1u);
-    }
-    __syncthreads();
-    if (threadIdx.x < 2)
-        cross[2 * size_t(u) + threadIdx.x] = c[threadIdx.x];
-}
-}  // namespace
-
-void launch_wave_cross(const uint32_t* pos, const uint2* ent, uint32_t units, uint32_t* cross, cudaStream_t st) {
-    if (units)
-        wave_cross_kernel<<<units, kNT, 0, st>>>(pos, ent, cross);
-    UB_CUDA(cudaGetLastError());
-}
-
 // ---------------------------------------------------------------------------
-// Entries split by cell parity (the paired-CTA wave kernel: CTA r owns the
-// cells with index & 1 == r, so a cell handed from one line to the next stays
-// in its CTA). Per line and parity: the entries in line order, each with its
-// position among the next line's entries of the same parity.
+// Entries split by cell index mod `parts` (the clustered wave kernel: CTA r
+// of a cluster owns the cells with index % parts == r, so a cell handed from
+// one line to the next stays in its CTA). Per line and part: the entries in
+// line order, each with its position among the next line's entries of the
+// same part.
 namespace {
 __global__ void __launch_bounds__(kNT) split_count_kernel(const uint32_t* __restrict__ pos,
-                                                          const uint2* __restrict__ ent, uint32_t* __restrict__ cnt) {
-    __shared__ uint32_t c[2];
+                                                          const uint2* __restrict__ ent, uint32_t parts,
+                                                          uint32_t* __restrict__ cnt) {
+    __shared__ uint32_t c[8];
     const uint32_t u = blockIdx.x;
-    if (threadIdx.x < 2)
+    if (threadIdx.x < parts)
         c[threadIdx.x] = 0;
     __syncthreads();
     for (uint32_t k = pos[u] + threadIdx.x; k < pos[u + 1]; k += kNT)
-        atomicAdd(&c[ent[k].x & 1u], 1u);
+        atomicAdd(&c[(ent[k].x & 0x7FFFFFFFu) % parts], 1u);
     __syncthreads();
-    if (threadIdx.x < 2)
-        cnt[2 * size_t(u) + threadIdx.x] = c[threadIdx.x];
+    if (threadIdx.x < parts)
+        cnt[size_t(parts) * u + threadIdx.x] = c[threadIdx.x];
 }
 
-// a warp per line: each entry's rank among the line's entries of its parity
+// a warp per line: each entry's rank among the line's entries of its part
 __global__ void split_rank_kernel(const uint32_t* __restrict__ pos, const uint2* __restrict__ ent, uint32_t units,
-                                  uint16_t* __restrict__ li) {
+                                  uint32_t parts, uint16_t* __restrict__ li) {
     const uint32_t u = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
     const unsigned lane = threadIdx.x & 31;
     if (u >= units)
         return;
-    uint32_t base[2] = {0, 0};
+    uint32_t base[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     for (uint32_t k0 = pos[u]; k0 < pos[u + 1]; k0 += 32) {
         const uint32_t k = k0 + lane;
         const bool in = k < pos[u + 1];
-        const uint32_t par = in ? (ent[k].x & 1u) : 0u;
-        const unsigned odd = __ballot_sync(0xFFFFFFFFu, in && par);
-        const unsigned even = __ballot_sync(0xFFFFFFFFu, in && !par);
+        const uint32_t part = in ? (ent[k].x & 0x7FFFFFFFu) % parts : 0u;
         const unsigned below = (1u << lane) - 1u;
-        if (in)
-            li[k] = uint16_t(base[par] + __popc((par ? odd : even) & below));
-        base[0] += __popc(even);
-        base[1] += __popc(odd);
+        for (uint32_t r = 0; r < parts; ++r) {
+            const unsigned m = __ballot_sync(0xFFFFFFFFu, in && part == r);
+            if (in && part == r)
+                li[k] = uint16_t(base[r] + __popc(m & below));
+            base[r] += __popc(m);
+        }
     }
 }
 
@@ -298,41 +272,43 @@ __global__ void __launch_bounds__(kNT) split_fill_kernel(const uint32_t* __restr
                                                          const uint2* __restrict__ ent,
                                                          const uint16_t* __restrict__ li,
                                                          const uint32_t* __restrict__ spos, uint32_t units,
-                                                         uint2* __restrict__ out) {
+                                                         uint32_t parts, uint2* __restrict__ out) {
     const uint32_t u = blockIdx.x;
     for (uint32_t k = pos[u] + threadIdx.x; k < pos[u + 1]; k += kNT) {
         const uint2 e = ent[k];
-        const uint32_t r = e.x & 1u;
+        const uint32_t r = (e.x & 0x7FFFFFFFu) % parts;
         const uint32_t nx = e.y == 0xFFFFu ? 0xFFFFu : uint32_t(li[pos[u + 1] + e.y]);
         out[spos[size_t(r) * (units + 1) + u] + li[k]] = make_uint2(e.x, nx);
     }
 }
 }  // namespace
 
-uint32_t gpu_wave_split(const uint32_t* pos, const uint2* ent, uint64_t total, uint32_t units, uint32_t* spos,
-                        uint2* split, cudaStream_t st) {
-    Buf<uint32_t> cnt(2 * size_t(units));
+uint32_t gpu_wave_split(const uint32_t* pos, const uint2* ent, uint64_t total, uint32_t units, uint32_t parts,
+                        uint32_t* spos, uint2* split, cudaStream_t st) {
+    if (parts < 1 || parts > 8)
+        throw CudaError("gpu_wave_split: 1 to 8 parts");
+    Buf<uint32_t> cnt(size_t(parts) * units);
     Buf<uint16_t> li(total);
     if (units) {
-        split_count_kernel<<<units, kNT, 0, st>>>(pos, ent, cnt.p);
-        split_rank_kernel<<<(units + 7) / 8, 256, 0, st>>>(pos, ent, units, li.p);
+        split_count_kernel<<<units, kNT, 0, st>>>(pos, ent, parts, cnt.p);
+        split_rank_kernel<<<(units + 7) / 8, 256, 0, st>>>(pos, ent, units, parts, li.p);
         UB_CUDA(cudaGetLastError());
     }
-    std::vector<uint32_t> c(2 * size_t(units)), sp(2 * (size_t(units) + 1));
+    std::vector<uint32_t> c(size_t(parts) * units), sp(size_t(parts) * (size_t(units) + 1));
     UB_CUDA(cudaMemcpyAsync(c.data(), cnt.p, sizeof(uint32_t) * c.size(), cudaMemcpyDeviceToHost, st));
     UB_CUDA(cudaStreamSynchronize(st));
     uint32_t acc = 0, longest = 0;
-    for (int r = 0; r < 2; ++r)
+    for (uint32_t r = 0; r < parts; ++r)
         for (uint32_t u = 0; u <= units; ++u) {
             sp[size_t(r) * (units + 1) + u] = acc;
             if (u < units) {
-                acc += c[2 * size_t(u) + r];
-                longest = std::max(longest, c[2 * size_t(u) + r]);
+                acc += c[size_t(parts) * u + r];
+                longest = std::max(longest, c[size_t(parts) * u + r]);
             }
         }
     UB_CUDA(cudaMemcpyAsync(spos, sp.data(), sizeof(uint32_t) * sp.size(), cudaMemcpyHostToDevice, st));
     if (units)
-        split_fill_kernel<<<units, kNT, 0, st>>>(pos, ent, li.p, spos, units, split);
+        split_fill_kernel<<<units, kNT, 0, st>>>(pos, ent, li.p, spos, units, parts, split);
     UB_CUDA(cudaGetLastError());
     UB_CUDA(cudaStreamSynchronize(st));
     return longest;

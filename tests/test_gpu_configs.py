@@ -150,14 +150,17 @@ def test_c2_verbatim_wave_twenty_sweeps(ub, orc, capfd, monkeypatch):
     _quality(ub, orc, g, spec, out[127][0].astype(np.float64), ref[3][0], truth[127], 512)
 
 
-@pytest.mark.parametrize("S,width", [(64, 32), (16, 16)])
-def test_c2_shard_per_gpu_paired_wave(ub, orc, capfd, monkeypatch, S, width):
-    """The C2 stack as one GPU of 2 / 8 holds it (64 / 16 slices): all 20
-    sweeps through the paired-CTA wave form (a view task on a 2-CTA cluster,
-    cells split by index parity, partial sums exchanged through distributed
-    shared memory), problems of the first and last slots against the oracle."""
+@pytest.mark.parametrize("S,width,cl", [(64, 32, 2), (16, 16, 2), (32, 32, 4)])
+def test_c2_shard_per_gpu_paired_wave(ub, orc, capfd, monkeypatch, S, width, cl):
+    """The C2 stack as one GPU of 2 / 4 / 8 holds it (64 / 32 / 16 slices):
+    all 20 sweeps through the clustered wave form (a view task on a 2-CTA
+    cluster, or the opt-in 4-CTA one; cells split by index mod cluster size,
+    partial sums exchanged through distributed shared memory), problems of the
+    first and last slots against the oracle."""
     from paper_2208_12964_b200 import workloads
     monkeypatch.setenv("USCG_FLOW_VERBOSE", "1")
+    if cl != 2:
+        monkeypatch.setenv("USCG_WAVE_PAIR", str(cl))
     wl = workloads.make("c2", problems=S)
     spec, geom = wl.spec, wl.geom
     tr = ub.Tracer(geom, spec, False)
@@ -165,7 +168,7 @@ def test_c2_shard_per_gpu_paired_wave(ub, orc, capfd, monkeypatch, S, width):
     proj = workloads.add_noise(wl, ub.project_stack(tr, truth.astype(np.float32)), first=64).astype(np.float32)
     out = ub.reconstruct_stack(proj, ub.SolverConfig(beta=wl.beta, tolerance=0, max_sweeps=wl.sweeps), tr,
                                with_crossed=True)
-    assert f"mart_wave_kernel: P={width} pair" in capfd.readouterr().err
+    assert f"mart_wave_kernel: P={width} pair cluster={cl}" in capfd.readouterr().err
     pick = [0, S - 1]
     g, src, det = _oracle_side(orc, spec, geom)
     ref = _oracle_many(orc, g, src, det, geom.thetas(), [proj[p] for p in pick], wl.beta, wl.sweeps)

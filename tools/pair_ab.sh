@@ -4,8 +4,8 @@ for l in sys.stdin:
     if l.startswith('{'):
         d=json.loads(l); print('$1 $2', round(d['ms_per_step'],3), round(d['roofline']['frac'],3))
 "; }
-for S in 128 64 32; do
+for S in 16 32 64; do
 USCG_WAVE_PAIR=0 run single "--problems $S"
-USCG_WAVE_PAIR=1 run pair1 "--problems $S"
-USCG_WAVE_PAIR=2 run pair2 "--problems $S"
+USCG_WAVE_PAIR=2 run cl2 "--problems $S"
+USCG_WAVE_PAIR=4 run cl4 "--problems $S"
 done

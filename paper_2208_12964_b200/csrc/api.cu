@@ -1648,9 +1648,11 @@ static void reconstruct_body(uscg_tracer t, const float* proj, int32_t problems,
         build_wave(t);
         if (t->wave_chunks != h.nchunks) {
             const uint64_t n = uint64_t(t->views) * uint64_t(h.nchunks);
-            t->d_wprog.alloc(4 * n);  // the clustered kernel keeps one counter per CTA (up to 4)
+            // the clustered kernel keeps one counter per CTA (up to 4); the
+            // single-CTA kernel one per 128-byte line (kWavePad)
+            t->d_wprog.alloc(32 * n);
             t->d_wnext.alloc(1);
-            UB_CUDA(cudaMemsetAsync(t->d_wprog.p, 0, sizeof(unsigned) * 4 * n, st));
+            UB_CUDA(cudaMemsetAsync(t->d_wprog.p, 0, sizeof(unsigned) * 32 * n, st));
             t->wave_chunks = h.nchunks;
             t->wave_epoch = 0;
         }
@@ -1702,16 +1704,17 @@ static void reconstruct_body(uscg_tracer t, const float* proj, int32_t problems,
             ws.lines = t->lines;
             // USCG_SWEEP_PROFILE=<file>: per task {start, end, ready-wait, gather, reduce, store, cta}
             static const char* prof_path = std::getenv("USCG_SWEEP_PROFILE");
-            const size_t nt = size_t(t->views) * h.nchunks * n_run;
+            // then per line {published, requirements held} (single-CTA form)
+            const size_t nt = size_t(t->views) * h.nchunks * n_run, rec = 8 + 2 * size_t(t->lines);
             DevBuf<unsigned long long> prof;
             if (prof_path) {
-                prof.alloc(nt * 8);
-                UB_CUDA(cudaMemsetAsync(prof.p, 0, sizeof(unsigned long long) * nt * 8, st));
+                prof.alloc(nt * rec);
+                UB_CUDA(cudaMemsetAsync(prof.p, 0, sizeof(unsigned long long) * nt * rec, st));
             }
             launch_mart_wave(h, ws, t->d_wprog.p, t->d_wnext.p, t->wave_epoch, n_run, st, prof.p);
             t->wave_epoch += unsigned(n_run);
             if (prof_path) {
-                std::vector<unsigned long long> hp(nt * 8);
+                std::vector<unsigned long long> hp(nt * rec);
                 UB_CUDA(cudaMemcpyAsync(hp.data(), prof.p, sizeof(unsigned long long) * hp.size(),
                                         cudaMemcpyDeviceToHost, st));
                 UB_CUDA(cudaStreamSynchronize(st));

@@ -136,6 +136,39 @@ __device__ __forceinline__ void st_global_cg_v4_if(bool p, void* gmem_dst, float
         "r"(int(p)), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w)
         : "memory");
 }
+// L2 eviction-priority forms (createpolicy): the wave executor keeps the
+// field rows resident (evict_last) while its traced lists stream (evict_first)
+__device__ __forceinline__ uint64_t l2_policy(int kind) {
+    uint64_t pol;
+    if (kind == 2)
+        asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+    else if (kind == 1)
+        asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    else
+        asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
+__device__ __forceinline__ void cp_async16_hint_if(bool p, void* smem_dst, const void* gmem_src, uint64_t pol) {
+    const unsigned d = unsigned(__cvta_generic_to_shared(smem_dst));
+    asm volatile(
+        "{ .reg .pred q; setp.ne.b32 q, %2, 0; @q cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %3; }" ::"r"(d),
+        "l"(gmem_src), "r"(int(p)), "l"(pol)
+        : "memory");
+}
+__device__ __forceinline__ void cp_async8_hint_if(bool p, void* smem_dst, const void* gmem_src, uint64_t pol) {
+    const unsigned d = unsigned(__cvta_generic_to_shared(smem_dst));
+    asm volatile(
+        "{ .reg .pred q; setp.ne.b32 q, %2, 0; @q cp.async.ca.shared.global.L2::cache_hint [%0], [%1], 8, %3; }" ::"r"(d),
+        "l"(gmem_src), "r"(int(p)), "l"(pol)
+        : "memory");
+}
+__device__ __forceinline__ void st_global_cg_v4_hint_if(bool p, void* gmem_dst, float4 v, uint64_t pol) {
+    asm volatile(
+        "{ .reg .pred q; setp.ne.b32 q, %1, 0; @q st.global.cg.L2::cache_hint.v4.f32 [%0], {%2, %3, %4, %5}, %6; }" ::"l"(
+            gmem_dst),
+        "r"(int(p)), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w), "l"(pol)
+        : "memory");
+}
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 
@@ -1318,10 +1351,13 @@ struct WaveArgs {
     int views;
     int lines;
     unsigned long long* prof;  // optional: per task 8 stamps/sums (ns), see mart_wave_kernel
+    int l2_field;              // L2 priority of field rows: 0 normal, 1 evict_first, 2 evict_last
+    int l2_lists;              // ... of the traced lists
 };
 
 constexpr uint32_t kWavePrev = 0x80000000u;  // entry's cell is also in the previous line
 constexpr uint32_t kWaveNoNext = 0xFFFFu;     // entry's cell is not in the next line
+constexpr uint32_t kWavePad = 32;             // single-CTA form: one progress counter per 128-byte line
 
 // Updater shape per chunk width P: G = 16 P threads, TPC = P/4 threads per
 // cell (one float4 each), 64 cells per pass and KV = 12 cells per thread (a
@@ -1376,7 +1412,7 @@ size_t wave_smem_bytes(const MartArgs& m, int lines) {
 }
 
 template <int P>
-__global__ void __launch_bounds__(WaveShape<P>::G + 64, WaveShape<P>::MB) mart_wave_kernel(WaveArgs a) {
+__global__ void __launch_bounds__(WaveShape<P>::G + 96, WaveShape<P>::MB) mart_wave_kernel(WaveArgs a) {
     constexpr int G = WaveShape<P>::G, V = 4, TPC = P / V, NCLV = G / TPC, KV = WaveShape<P>::KV;
     constexpr int COVER = wave_cover<P>();
     using GW = GroupWorker<P, G>;
@@ -1433,72 +1469,37 @@ __global__ void __launch_bounds__(WaveShape<P>::G + 64, WaveShape<P>::MB) mart_w
         }
         return;
     }
-    if (int(threadIdx.x) >= G + 32) {
-        // ---- control warp ----
+    if (int(threadIdx.x) >= G + 64) {
+        // ---- publisher warp: the lines the updaters have finished (s_done,
+        // released by the factor warp after barrier C) become visible at gpu
+        // scope: one fence (cumulative over the updaters' stores through the
+        // barrier and the shared-memory release) and one relaxed store of the
+        // count per round. A warp of its own, so that the fence's wait for the
+        // line's stores never delays the requirement polls. ----
         const int lane = int(threadIdx.x) & 31;
         while (task < total) {
             const int sweep = task / per_sweep;
             const int v = (task % per_sweep) / nchunks, chunk = task % nchunks;
             const unsigned gs = a.epoch + unsigned(sweep);
-            unsigned* mine = a.prog + size_t(v) * nchunks + chunk;
-            const uint32_t u0 = uint32_t(v) * L;
-            // the previous sweep's task of this (view, chunk) has published every line
-            if (lane == 0 && gs > 0)
-                spin_until_geq(mine, gs * L);
-            __syncwarp();
-            unsigned ready = 0, published = 0;
-            unsigned ns = 0;
+            unsigned* mine = a.prog + (size_t(v) * nchunks + chunk) * kWavePad;
+            unsigned long long* lp = a.prof ? a.prof + (8 + 2 * size_t(L)) * size_t(task) + 8 : nullptr;
+            unsigned published = 0;
             while (published < L) {
-                bool moved = false;
-                if (ready < L) {
-                    // lane i checks line ready + i
-                    const unsigned j = ready + unsigned(lane);
-                    bool ok = true;
-                    const unsigned* last = nullptr;  // the lane's last satisfied counter
-                    if (j < L) {
-                        const uint32_t b = __ldg(a.dep_off + u0 + j), e = __ldg(a.dep_off + u0 + j + 1);
-                        for (uint32_t k = b; k < e && ok; ++k) {
-                            const uint32_t w = __ldg(a.deps + 2 * size_t(k));
-                            const unsigned xs = w >> 31, u = w & 0x7FFFFFFFu;
-                            if (gs < xs)
-                                continue;  // no previous sweep
-                            const unsigned need = (gs - xs) * L + __ldg(a.deps + 2 * size_t(k) + 1);
-                            // relaxed polls: a gpu-scope acquire load also
-                            // invalidates the SM's L1 (CCTL.IVALL) on every poll
-                            last = a.prog + size_t(u) * nchunks + chunk;
-                            ok = ld_relaxed(last) >= need;
-                        }
-                    }
-                    const unsigned bad = __ballot_sync(0xFFFFFFFFu, !ok);
-                    const unsigned adv = bad ? unsigned(__ffs(bad) - 1) : 32u;
-                    const unsigned nr = min(L, ready + adv);
-                    if (nr > ready) {
-                        // acquire what the advancing lanes observed (coherence:
-                        // the re-read is at least as recent), then release to
-                        // the updaters
-                        if (unsigned(lane) < adv && last != nullptr)
-                            (void)ld_acquire(last);
-                        __syncwarp();
-                        ready = nr;
-                        moved = true;
-                        if (lane == 0)
-                            st_release_cta_shared(&s_ready, ready);
-                    }
-                }
                 const unsigned d = ld_acquire_cta_shared(&s_done);
                 if (d > published) {
                     if (lane == 0) {
                         fence_acq_rel_gpu();
                         st_relaxed_gpu(mine, gs * L + d);
                     }
+                    if (lp) {
+                        __syncwarp();
+                        const unsigned long long tn = gtimer();
+                        for (unsigned x = published + unsigned(lane); x < d; x += 32)
+                            lp[x] = tn;
+                    }
                     published = d;
-                    moved = true;
-                }
-                if (moved) {
-                    ns = 0;
                 } else {
-                    ns = ns ? min(ns * 2, 128u) : 16u;
-                    __nanosleep(ns);
+                    __nanosleep(32);
                 }
             }
             __syncwarp();
@@ -1506,6 +1507,118 @@ __global__ void __launch_bounds__(WaveShape<P>::G + 64, WaveShape<P>::MB) mart_w
                 s_task = atomicAdd(a.next, 1u);
                 s_ready = 0;
                 s_done = 0;
+            }
+            __syncthreads();  // task boundary (with the updaters)
+            task = int(s_task);
+            __syncthreads();  // everyone has read the ticket
+        }
+        return;
+    }
+    if (int(threadIdx.x) >= G + 32) {
+        // ---- poller warp: lane i watches line ready + i. Its requirements
+        // (up to kWaveRq counters and counts, the rest re-read from the list)
+        // stay in registers, so a poll is one relaxed load per requirement;
+        // when lines advance, the lanes shift their cached requirements down
+        // by the advance and load the new top lines' ones. An advance is
+        // acquired with one gpu-scope fence by the whole warp (every lane that
+        // observed a count executes it) and released to the updaters. ----
+        constexpr int RQ = 3;
+        const int lane = int(threadIdx.x) & 31;
+        while (task < total) {
+            const int sweep = task / per_sweep;
+            const int v = (task % per_sweep) / nchunks, chunk = task % nchunks;
+            const unsigned gs = a.epoch + unsigned(sweep);
+            unsigned* mine = a.prog + (size_t(v) * nchunks + chunk) * kWavePad;
+            const uint32_t u0 = uint32_t(v) * L;
+            unsigned long long* lp = a.prof ? a.prof + (8 + 2 * size_t(L)) * size_t(task) + 8 : nullptr;
+            // the previous sweep's task of this (view, chunk) has published every line
+            if (lane == 0 && gs > 0)
+                spin_until_geq(mine, gs * L);
+            __syncwarp();
+            // cached requirements of line j: n counters (<= RQ here), the rest
+            // [kx, ke) of the global list
+            uint32_t rc[RQ], rn[RQ];
+            int n = 0;
+            uint32_t kx = 0, ke = 0;
+            auto load_reqs = [&](unsigned j) {
+                n = 0;
+                kx = ke = 0;
+                if (j >= L)
+                    return;
+                uint32_t k = __ldg(a.dep_off + u0 + j);
+                const uint32_t e = __ldg(a.dep_off + u0 + j + 1);
+                for (; k < e && n < RQ; ++k) {
+                    const uint32_t w = __ldg(a.deps + 2 * size_t(k));
+                    const unsigned xs = w >> 31;
+                    if (gs < xs)
+                        continue;  // no previous sweep
+#pragma unroll
+                    for (int r = 0; r < RQ; ++r)
+                        if (r == n) {
+                            rc[r] = ((w & 0x7FFFFFFFu) * unsigned(nchunks) + unsigned(chunk)) * kWavePad;
+                            rn[r] = (gs - xs) * L + __ldg(a.deps + 2 * size_t(k) + 1);
+                        }
+                    ++n;
+                }
+                kx = k;
+                ke = e;
+            };
+            unsigned ready = 0, ns = 0;
+            load_reqs(unsigned(lane));
+            while (ready < L) {
+                const unsigned j = ready + unsigned(lane);
+                bool ok = true;
+#pragma unroll
+                for (int r = 0; r < RQ; ++r)
+                    if (r < n && ok)
+                        ok = ld_relaxed(a.prog + rc[r]) >= rn[r];
+                for (uint32_t k = kx; k < ke && ok; ++k) {
+                    const uint32_t w = __ldg(a.deps + 2 * size_t(k));
+                    const unsigned xs = w >> 31;
+                    if (gs < xs)
+                        continue;
+                    const unsigned need = (gs - xs) * L + __ldg(a.deps + 2 * size_t(k) + 1);
+                    ok = ld_relaxed(a.prog + (size_t(w & 0x7FFFFFFFu) * nchunks + chunk) * kWavePad) >= need;
+                }
+                if (j >= L)
+                    ok = true;
+                const unsigned bad = __ballot_sync(0xFFFFFFFFu, !ok);
+                const unsigned adv = bad ? unsigned(__ffs(bad) - 1) : 32u;
+                const unsigned nr = min(L, ready + adv);
+                if (nr > ready) {
+                    // acquire what the advancing lanes observed (an acquire
+                    // re-read of a satisfied counter: coherence makes it at
+                    // least as recent; a gpu-scope fence here would wait for
+                    // the updaters' outstanding stores), then release to the
+                    // updaters
+                    if (unsigned(lane) < adv && n > 0)
+                        (void)ld_acquire(a.prog + rc[0]);
+                    __syncwarp();
+                    if (lp) {
+                        const unsigned long long tn = gtimer();
+                        for (unsigned x = ready + unsigned(lane); x < nr; x += 32)
+                            lp[L + x] = tn;
+                    }
+                    ready = nr;
+                    if (lane == 0)
+                        st_release_cta_shared(&s_ready, ready);
+                    // shift the cached requirements down by adv; new top lines load theirs
+                    const int src = lane + int(adv);
+#pragma unroll
+                    for (int r = 0; r < RQ; ++r) {
+                        rc[r] = __shfl_sync(0xFFFFFFFFu, rc[r], src & 31);
+                        rn[r] = __shfl_sync(0xFFFFFFFFu, rn[r], src & 31);
+                    }
+                    n = __shfl_sync(0xFFFFFFFFu, n, src & 31);
+                    kx = __shfl_sync(0xFFFFFFFFu, kx, src & 31);
+                    ke = __shfl_sync(0xFFFFFFFFu, ke, src & 31);
+                    if (src >= 32)
+                        load_reqs(ready + unsigned(lane));
+                    ns = 0;
+                } else {
+                    ns = ns ? min(ns * 2, 256u) : 16u;
+                    __nanosleep(ns);
+                }
             }
             __syncthreads();  // task boundary (with the updaters)
             task = int(s_task);
@@ -1526,6 +1639,7 @@ __global__ void __launch_bounds__(WaveShape<P>::G + 64, WaveShape<P>::MB) mart_w
     const int t = W.t;
     const int q = t % TPC, cl = t / TPC;
     float4* __restrict__ f4 = reinterpret_cast<float4*>(a.m.field);
+    const uint64_t pol_f = l2_policy(a.l2_field), pol_l = l2_policy(a.l2_lists);
     const uint32_t Sp4 = uint32_t(a.m.Sp) / V;
     auto wait_ready = [&](unsigned j) {
         if (ld_acquire_cta_shared(&s_ready) <= j) {
@@ -1542,7 +1656,8 @@ __global__ void __launch_bounds__(WaveShape<P>::G + 64, WaveShape<P>::MB) mart_w
         upd_sync();
         // USCG_SWEEP_PROFILE: {start, end, ready-wait, gather, reduce, store} (ns, thread 0)
         const bool prof = a.prof != nullptr && t == 0;
-        unsigned long long p_start = prof ? gtimer() : 0, p_wait = 0, p_gather = 0, p_reduce = 0, p_store = 0;
+        unsigned long long p_start = prof ? gtimer() : 0, p_wait = 0, p_gather = 0, p_reduce = 0, p_store = 0,
+                           p_cwait = 0;
         // entries of line j (own slots) into ring slot j % 3
         auto load_entries = [&](unsigned j) {
             const uint32_t p0 = s_pos[j];
@@ -1551,7 +1666,7 @@ __global__ void __launch_bounds__(WaveShape<P>::G + 64, WaveShape<P>::MB) mart_w
 #pragma unroll
             for (int i = 0; i < KV; ++i) {
                 const int s = cl + i * NCLV;
-                cp_async8_if(q == 0 && s < n, dst + s, a.ent + p0 + s);
+                cp_async8_hint_if(q == 0 && s < n, dst + s, a.ent + p0 + s, pol_l);
             }
         };
         // field values of line j's cells that line j-1 does not cross (own slots)
@@ -1562,7 +1677,7 @@ __global__ void __launch_bounds__(WaveShape<P>::G + 64, WaveShape<P>::MB) mart_w
             for (int i = 0; i < KV; ++i) {
                 const int s = cl + i * NCLV;
                 const uint32_t c = s < n ? e[s].x : kWavePrev;
-                cp_async16_if(!(c & kWavePrev), buf + s * TPC + q, f4 + size_t(c) * Sp4 + col4);
+                cp_async16_hint_if(!(c & kWavePrev), buf + s * TPC + q, f4 + size_t(c) * Sp4 + col4, pol_f);
             }
         };
         // the entries are written by the slot's q == 0 thread: one barrier
@@ -1580,6 +1695,8 @@ __global__ void __launch_bounds__(WaveShape<P>::G + 64, WaveShape<P>::MB) mart_w
             const int n = int(s_pos[j + 1] - s_pos[j]);
             const unsigned long long p1 = prof ? gtimer() : 0;
             cp_async_wait_all();  // this line's values (own copies); hand-overs: barrier C
+            if (prof)
+                p_cwait += gtimer() - p1;
             float4 x[KV];
 #pragma unroll
             for (int i = 0; i < KV; ++i) {
@@ -1636,8 +1753,8 @@ __global__ void __launch_bounds__(WaveShape<P>::G + 64, WaveShape<P>::MB) mart_w
                 const float4 r = GW::scale4(x[i], g0, g1, g2, g3);
                 const bool hand = in && en.y != kWaveNoNext;
                 st_shared_v4_if(hand, buf + int(en.y) * TPC + q, r);
-                st_global_cg_v4_if((any || (en.x & kWavePrev)) && in && !hand,
-                                   f4 + size_t(en.x & ~kWavePrev) * Sp4 + col4, r);
+                st_global_cg_v4_hint_if((any || (en.x & kWavePrev)) && in && !hand,
+                                        f4 + size_t(en.x & ~kWavePrev) * Sp4 + col4, r, pol_f);
             }
             // C: hand-overs visible; this line's stores ordered before the
             // factor warp's release of `done`
@@ -1658,7 +1775,7 @@ __global__ void __launch_bounds__(WaveShape<P>::G + 64, WaveShape<P>::MB) mart_w
             }
         }
         if (prof) {
-            unsigned long long* o = a.prof + 8 * size_t(task);
+            unsigned long long* o = a.prof + (8 + 2 * size_t(L)) * size_t(task);
             o[0] = p_start;
             o[1] = gtimer();
             o[2] = p_wait;
@@ -1666,6 +1783,7 @@ __global__ void __launch_bounds__(WaveShape<P>::G + 64, WaveShape<P>::MB) mart_w
             o[4] = p_reduce;
             o[5] = p_store;
             o[6] = blockIdx.x;
+            o[7] = p_cwait;
         }
         __syncthreads();  // task boundary (the control warp grabs the next ticket)
         task = int(s_task);
@@ -1675,7 +1793,7 @@ __global__ void __launch_bounds__(WaveShape<P>::G + 64, WaveShape<P>::MB) mart_w
 
 template <int P>
 static void wave_launch_t(const WaveArgs& a, int sms, cudaStream_t st) {
-    constexpr int NT = WaveShape<P>::G + 64;
+    constexpr int NT = WaveShape<P>::G + 96;
     const size_t smem = 4 * wave_words<P>(a.m.max_recs, a.m.max_cells, a.lines);
     // set once per (device, size): changing a running kernel's attributes
     // would wait for it (uscg_reconstruct_batch overlaps neighbouring stacks'
@@ -2202,6 +2320,14 @@ void launch_mart_wave(const MartArgs& h, const WaveSchedule& ws, unsigned* prog,
     a.views = ws.views;
     a.lines = ws.lines;
     a.prof = prof;
+    // field rows evict_last, traced lists evict_first (C2: 4.85 vs 4.88 ms
+    // per iteration with default priorities)
+    a.l2_field = 2;
+    a.l2_lists = 1;
+    if (const char* e = std::getenv("USCG_WAVE_L2")) {  // experiments: "<field><lists>" priorities
+        a.l2_field = e[0] ? e[0] - '0' : 0;
+        a.l2_lists = e[0] && e[1] ? e[1] - '0' : 0;
+    }
     UB_CUDA(cudaMemsetAsync(next, 0, sizeof(unsigned), st));
     switch (h.Sp / h.nchunks) {
         case 4: wave_launch_t<4>(a, sms, st); break;

@@ -21,7 +21,7 @@ __device__ __forceinline__ uint32_t sa(const void* p) { return uint32_t(__cvta_g
 
 __global__ void __launch_bounds__(NT, 1) bench(int mode, const float* __restrict__ f, float* __restrict__ g,
                                               const uint32_t* __restrict__ rows_all, int rows, int lines,
-                                              unsigned long long* out) {
+                                              unsigned long long* out, int split) {
     extern __shared__ __align__(128) float buf[];  // [MAXR][32]
     __shared__ __align__(8) uint64_t bar;
     const int t = threadIdx.x;
@@ -136,6 +136,75 @@ __global__ void __launch_bounds__(NT, 1) bench(int mode, const float* __restrict
             if (acc == 12345.f)
                 g[0] = acc;
             __syncthreads();
+        } else if (mode == 8) {  // warps 0-5 gather this line's rows while warps 6-11 store another set
+            if (t < NT / 2) {
+                for (int i = t; i < rows * 8; i += NT / 2) {
+                    const int row = i / 8, q = i % 8;
+                    const float* src = f + size_t(r[row]) * SP + q * 4;
+                    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa(buf + row * 32 + q * 4)),
+                                 "l"(src)
+                                 : "memory");
+                }
+                asm volatile("cp.async.commit_group; cp.async.wait_all;" ::: "memory");
+            } else {
+                const uint32_t* r2 = rw + size_t((l + 1) % lines) * rows;
+                for (int i = t - NT / 2; i < rows * 8; i += NT / 2) {
+                    const int row = i / 8, q = i % 8;
+                    float* dst = g + size_t(r2[row]) * SP + q * 4;
+                    const float4 v = *reinterpret_cast<const float4*>(buf + (MAXR / 2 + row % (MAXR / 2)) * 32 + q * 4);
+                    asm volatile("st.global.cg.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(dst), "f"(v.x), "f"(v.y),
+                                 "f"(v.z), "f"(v.w)
+                                 : "memory");
+                }
+            }
+            __syncthreads();
+        } else if (mode == 9) {  // every thread issues its gathers, then its stores, then waits
+            const uint32_t* r2 = rw + size_t((l + 1) % lines) * rows;
+            for (int i = t; i < rows * 8; i += NT) {
+                const int row = i / 8, q = i % 8;
+                const float* src = f + size_t(r[row]) * SP + q * 4;
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa(buf + row * 32 + q * 4)), "l"(src)
+                             : "memory");
+            }
+            asm volatile("cp.async.commit_group;" ::: "memory");
+            for (int i = t; i < rows * 8; i += NT) {
+                const int row = i / 8, q = i % 8;
+                float* dst = g + size_t(r2[row]) * SP + q * 4;
+                const float4 v = *reinterpret_cast<const float4*>(buf + (MAXR / 2 + row % (MAXR / 2)) * 32 + q * 4);
+                asm volatile("st.global.cg.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(dst), "f"(v.x), "f"(v.y), "f"(v.z),
+                             "f"(v.w)
+                             : "memory");
+            }
+            asm volatile("cp.async.wait_all;" ::: "memory");
+            __syncthreads();
+        } else if (mode == 10 || mode == 11) {  // LSU gathers; stores: 10 all by TMA bulk, 11 the first `split` by TMA
+            const uint32_t* r2 = rw + size_t((l + 1) % lines) * rows;
+            const int k = mode == 10 ? rows : split;
+            for (int row = t; row < k; row += NT) {
+                float* dst = g + size_t(r2[row]) * SP;
+                asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], 128;" ::"l"(dst),
+                             "r"(sa(buf + (MAXR / 2 + row % (MAXR / 2)) * 32))
+                             : "memory");
+            }
+            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+            for (int i = t; i < rows * 8; i += NT) {
+                const int row = i / 8, q = i % 8;
+                const float* src = f + size_t(r[row]) * SP + q * 4;
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa(buf + row * 32 + q * 4)), "l"(src)
+                             : "memory");
+            }
+            asm volatile("cp.async.commit_group;" ::: "memory");
+            for (int i = t + k * 8; i < rows * 8; i += NT) {
+                const int row = i / 8, q = i % 8;
+                float* dst = g + size_t(r2[row]) * SP + q * 4;
+                const float4 v = *reinterpret_cast<const float4*>(buf + (MAXR / 2 + row % (MAXR / 2)) * 32 + q * 4);
+                asm volatile("st.global.cg.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(dst), "f"(v.x), "f"(v.y), "f"(v.z),
+                             "f"(v.w)
+                             : "memory");
+            }
+            asm volatile("cp.async.wait_all;" ::: "memory");
+            asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+            __syncthreads();
         } else if (mode == 3) {  // one bulk store of 128 B per row
             for (int row = t; row < rows; row += NT) {
                 float* dst = g + size_t(r[row]) * SP;
@@ -147,7 +216,7 @@ __global__ void __launch_bounds__(NT, 1) bench(int mode, const float* __restrict
             __syncthreads();
         }
     }
-    if (mode == 3)
+    if (mode == 3 || mode == 10 || mode == 11)
         asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
     __syncthreads();
     if (t == 0)
@@ -162,10 +231,14 @@ int main(int argc, char** argv) {
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
     if (argc > 3)
         sms = atoi(argv[3]);
+    const int split = argc > 5 ? atoi(argv[5]) : rows / 2;
+    const bool same = argc > 4 && atoi(argv[4]) != 0;  // store into the gathered array (the wave's in-place field)
     float *f, *g;
     cudaMalloc(&f, sizeof(float) * size_t(CELLS) * SP);
     cudaMalloc(&g, sizeof(float) * size_t(CELLS) * SP);
     cudaMemset(f, 0, sizeof(float) * size_t(CELLS) * SP);
+    if (same)
+        g = f;
     std::vector<uint32_t> h(size_t(sms) * lines * rows);
     uint64_t s = 12345;
     for (auto& x : h) {
@@ -180,7 +253,7 @@ int main(int argc, char** argv) {
     const size_t smem = size_t(MAXR) * 32 * 4;
     cudaFuncSetAttribute(bench, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     for (int rep = 0; rep < 2; ++rep)
-        bench<<<sms, NT, smem>>>(mode, f, g, d, rows, lines, out);
+        bench<<<sms, NT, smem>>>(mode, f, g, d, rows, lines, out, split);
     cudaError_t e = cudaDeviceSynchronize();
     if (e != cudaSuccess) {
         printf("error %s\n", cudaGetErrorString(e));
@@ -193,7 +266,9 @@ int main(int argc, char** argv) {
         mean += double(v);
     mean /= sms;
     const char* names[] = {"LDGSTS gather", "bulk gather", "STG store", "bulk store", "half+half",
-                           "STG.256 store", "LDG.256 gather", "LDG.128 gather"};
+                           "STG.256 store", "LDG.256 gather", "LDG.128 gather", "gather||store", "gather;store", "LSU gather+TMA store", "LSU gather+split store"};
+    if (mode == 11)
+        printf("[split %d] ", split);
     printf("%-14s rows/line %d: %.0f cycles per line (%.2f cycles per row) on %d SMs\n", names[mode], rows,
            mean / lines, mean / lines / rows, sms);
     return 0;

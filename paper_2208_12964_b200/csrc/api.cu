@@ -1648,11 +1648,11 @@ static void reconstruct_body(uscg_tracer t, const float* proj, int32_t problems,
         build_wave(t);
         if (t->wave_chunks != h.nchunks) {
             const uint64_t n = uint64_t(t->views) * uint64_t(h.nchunks);
-            // the clustered kernel keeps one counter per CTA (up to 4); the
-            // single-CTA kernel one per 128-byte line (kWavePad)
-            t->d_wprog.alloc(32 * n);
+            // one counter per 128-byte line (kWavePad), per CTA of a
+            // cluster (up to 4)
+            t->d_wprog.alloc(128 * n);
             t->d_wnext.alloc(1);
-            UB_CUDA(cudaMemsetAsync(t->d_wprog.p, 0, sizeof(unsigned) * 32 * n, st));
+            UB_CUDA(cudaMemsetAsync(t->d_wprog.p, 0, sizeof(unsigned) * 128 * n, st));
             t->wave_chunks = h.nchunks;
             t->wave_epoch = 0;
         }

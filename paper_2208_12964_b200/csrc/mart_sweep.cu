@@ -1357,7 +1357,8 @@ struct WaveArgs {
 
 constexpr uint32_t kWavePrev = 0x80000000u;  // entry's cell is also in the previous line
 constexpr uint32_t kWaveNoNext = 0xFFFFu;     // entry's cell is not in the next line
-constexpr uint32_t kWavePad = 32;             // single-CTA form: one progress counter per 128-byte line
+constexpr uint32_t kWavePad = 32;             // one progress counter per 128-byte line (polls of
+                                              // neighbouring counters contend in L2)
 
 // Updater shape per chunk width P: G = 16 P threads, TPC = P/4 threads per
 // cell (one float4 each), 64 cells per pass and KV = 12 cells per thread (a
@@ -1929,7 +1930,7 @@ __global__ void __launch_bounds__(pair::Shape<P, SLOTS>::NT, 1) mart_wave_pair_k
     // one progress counter per (view, chunk, CTA): each CTA publishes its own
     // part of a line's cells; a requirement holds when every part does
     auto prog_of = [&](int view, int chunk, uint32_t r) {
-        return a.prog + (size_t(view) * nchunks + chunk) * CL + r;
+        return a.prog + ((size_t(view) * nchunks + chunk) * CL + r) * kWavePad;
     };
     const int id_line = 1 + 3 * k, id_upd = 2 + 3 * k, id_slot = 3 + 3 * k;
     auto line_sync = [&] { named_sync(id_line, GS + 32); };
@@ -2059,7 +2060,7 @@ __global__ void __launch_bounds__(pair::Shape<P, SLOTS>::NT, 1) mart_wave_pair_k
                             last = prog_of(int(u), chunk, 0);
 #pragma unroll
                             for (int r = 0; r < CL; ++r)
-                                ok = ok && ld_relaxed(last + r) >= need;
+                                ok = ok && ld_relaxed(last + r * kWavePad) >= need;
                         }
                     }
                     const unsigned bad = __ballot_sync(0xFFFFFFFFu, !ok);
@@ -2069,7 +2070,7 @@ __global__ void __launch_bounds__(pair::Shape<P, SLOTS>::NT, 1) mart_wave_pair_k
                         if (unsigned(lane) < adv && last != nullptr)
 #pragma unroll
                             for (int r = 0; r < CL; ++r)
-                                (void)ld_acquire(last + r);
+                                (void)ld_acquire(last + r * kWavePad);
                         __syncwarp();
                         ready = nr;
                         moved = true;

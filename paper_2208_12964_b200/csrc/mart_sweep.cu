@@ -1353,6 +1353,8 @@ struct WaveArgs {
     unsigned long long* prof;  // optional: per task 8 stamps/sums (ns), see mart_wave_kernel
     int l2_field;              // L2 priority of field rows: 0 normal, 1 evict_first, 2 evict_last
     int l2_lists;              // ... of the traced lists
+    unsigned poll_ns;          // requirement poller: longest back-off sleep (ns)
+    unsigned pub_ns;           // publisher: sleep between checks of the done count (ns)
 };
 
 constexpr uint32_t kWavePrev = 0x80000000u;  // entry's cell is also in the previous line
@@ -1500,7 +1502,7 @@ __global__ void __launch_bounds__(WaveShape<P>::G + 96, WaveShape<P>::MB) mart_w
                     }
                     published = d;
                 } else {
-                    __nanosleep(32);
+                    __nanosleep(a.pub_ns);
                 }
             }
             __syncwarp();
@@ -1617,7 +1619,7 @@ __global__ void __launch_bounds__(WaveShape<P>::G + 96, WaveShape<P>::MB) mart_w
                         load_reqs(ready + unsigned(lane));
                     ns = 0;
                 } else {
-                    ns = ns ? min(ns * 2, 256u) : 16u;
+                    ns = ns ? min(ns * 2, a.poll_ns) : 16u;
                     __nanosleep(ns);
                 }
             }
@@ -1841,7 +1843,7 @@ constexpr int V = 4, G = 384, COVERL = 384;  // updater threads per CTA; cell sl
 template <int P, int SLOTS> struct Shape {
     static constexpr int GS = G / SLOTS;  // updaters per task slot
     static constexpr int NWS = GS / 32, TPC = P / V, NCLV = GS / TPC, KV = COVERL / NCLV;
-    static constexpr int NTS = GS + 64;   // + factor warp + control warp
+    static constexpr int NTS = GS + 96;   // + factor warp + poller warp + publisher warp
     static constexpr int NT = SLOTS * NTS;
 };
 
@@ -2028,56 +2030,18 @@ __global__ void __launch_bounds__(pair::Shape<P, SLOTS>::NT, 1) mart_wave_pair_k
             }
             task = next_task(false);
         }
-    } else if (lt >= GS + 32) {
-        // ---- control warp: requirements (both halves of the other views'
-        // progress), and this CTA's half ----
+    } else if (lt >= GS + 64) {
+        // ---- publisher warp: this CTA's part of the finished lines at gpu
+        // scope (one fence + relaxed store per round; a warp of its own so the
+        // fence's wait for the stores never delays the polls) ----
         const int lane = lt & 31;
         while (task < total) {
             const int sweep = task / per_sweep;
             const int v = (task % per_sweep) / nchunks, chunk = task % nchunks;
             const unsigned gs = a.epoch + unsigned(sweep);
             unsigned* mine = prog_of(v, chunk, rank);
-            const uint32_t u0 = uint32_t(v) * L;
-            if (lane < CL && gs > 0)
-                spin_until_geq(prog_of(v, chunk, uint32_t(lane)), gs * L);
-            __syncwarp();
-            unsigned ready = 0, published = 0;
-            unsigned ns = 0;
+            unsigned published = 0;
             while (published < L) {
-                bool moved = false;
-                if (ready < L) {
-                    const unsigned j = ready + unsigned(lane);
-                    bool ok = true;
-                    const unsigned* last = nullptr;
-                    if (j < L) {
-                        const uint32_t b = __ldg(a.dep_off + u0 + j), e = __ldg(a.dep_off + u0 + j + 1);
-                        for (uint32_t q2 = b; q2 < e && ok; ++q2) {
-                            const uint32_t w = __ldg(a.deps + 2 * size_t(q2));
-                            const unsigned xs = w >> 31, u = w & 0x7FFFFFFFu;
-                            if (gs < xs)
-                                continue;
-                            const unsigned need = (gs - xs) * L + __ldg(a.deps + 2 * size_t(q2) + 1);
-                            last = prog_of(int(u), chunk, 0);
-#pragma unroll
-                            for (int r = 0; r < CL; ++r)
-                                ok = ok && ld_relaxed(last + r * kWavePad) >= need;
-                        }
-                    }
-                    const unsigned bad = __ballot_sync(0xFFFFFFFFu, !ok);
-                    const unsigned adv = bad ? unsigned(__ffs(bad) - 1) : 32u;
-                    const unsigned nr = min(L, ready + adv);
-                    if (nr > ready) {
-                        if (unsigned(lane) < adv && last != nullptr)
-#pragma unroll
-                            for (int r = 0; r < CL; ++r)
-                                (void)ld_acquire(last + r * kWavePad);
-                        __syncwarp();
-                        ready = nr;
-                        moved = true;
-                        if (lane == 0)
-                            st_release_cta_shared(&s_ready[k], ready);
-                    }
-                }
                 const unsigned d = ld_acquire_cta_shared(&s_done[k]);
                 if (d > published) {
                     if (lane == 0) {
@@ -2085,12 +2049,102 @@ __global__ void __launch_bounds__(pair::Shape<P, SLOTS>::NT, 1) mart_wave_pair_k
                         st_relaxed_gpu(mine, gs * L + d);
                     }
                     published = d;
-                    moved = true;
+                } else {
+                    __nanosleep(a.pub_ns);
                 }
-                if (moved) {
+            }
+            __syncwarp();
+            task = next_task(false);
+        }
+    } else if (lt >= GS + 32) {
+        // ---- poller warp: requirements (every part of the other views'
+        // progress); lane i watches line ready + i with its requirements
+        // cached in registers (as the single-CTA form) ----
+        constexpr int RQ = 3;
+        const int lane = lt & 31;
+        while (task < total) {
+            const int sweep = task / per_sweep;
+            const int v = (task % per_sweep) / nchunks, chunk = task % nchunks;
+            const unsigned gs = a.epoch + unsigned(sweep);
+            const uint32_t u0 = uint32_t(v) * L;
+            if (lane < CL && gs > 0)
+                spin_until_geq(prog_of(v, chunk, uint32_t(lane)), gs * L);
+            __syncwarp();
+            uint32_t rc[RQ], rn[RQ];
+            int n = 0;
+            uint32_t kx = 0, ke = 0;
+            auto load_reqs = [&](unsigned j) {
+                n = 0;
+                kx = ke = 0;
+                if (j >= L)
+                    return;
+                uint32_t q2 = __ldg(a.dep_off + u0 + j);
+                const uint32_t e = __ldg(a.dep_off + u0 + j + 1);
+                for (; q2 < e && n < RQ; ++q2) {
+                    const uint32_t w = __ldg(a.deps + 2 * size_t(q2));
+                    const unsigned xs = w >> 31;
+                    if (gs < xs)
+                        continue;
+#pragma unroll
+                    for (int r = 0; r < RQ; ++r)
+                        if (r == n) {
+                            rc[r] = uint32_t(prog_of(int(w & 0x7FFFFFFFu), chunk, 0) - a.prog);
+                            rn[r] = (gs - xs) * L + __ldg(a.deps + 2 * size_t(q2) + 1);
+                        }
+                    ++n;
+                }
+                kx = q2;
+                ke = e;
+            };
+            unsigned ready = 0, ns = 0;
+            load_reqs(unsigned(lane));
+            while (ready < L) {
+                bool ok = true;
+#pragma unroll
+                for (int r = 0; r < RQ; ++r)
+                    if (r < n)
+#pragma unroll
+                        for (int c = 0; c < CL; ++c)
+                            ok = ok && ld_relaxed(a.prog + rc[r] + c * kWavePad) >= rn[r];
+                for (uint32_t q2 = kx; q2 < ke && ok; ++q2) {
+                    const uint32_t w = __ldg(a.deps + 2 * size_t(q2));
+                    const unsigned xs = w >> 31;
+                    if (gs < xs)
+                        continue;
+                    const unsigned need = (gs - xs) * L + __ldg(a.deps + 2 * size_t(q2) + 1);
+                    const unsigned* base = prog_of(int(w & 0x7FFFFFFFu), chunk, 0);
+#pragma unroll
+                    for (int c = 0; c < CL; ++c)
+                        ok = ok && ld_relaxed(base + c * kWavePad) >= need;
+                }
+                const unsigned bad = __ballot_sync(0xFFFFFFFFu, !ok);
+                const unsigned adv = bad ? unsigned(__ffs(bad) - 1) : 32u;
+                const unsigned nr = min(L, ready + adv);
+                if (nr > ready) {
+                    // acquire what the advancing lanes observed (re-reads of
+                    // satisfied counters), then release to the updaters
+                    if (unsigned(lane) < adv && n > 0)
+#pragma unroll
+                        for (int c = 0; c < CL; ++c)
+                            (void)ld_acquire(a.prog + rc[0] + c * kWavePad);
+                    __syncwarp();
+                    ready = nr;
+                    if (lane == 0)
+                        st_release_cta_shared(&s_ready[k], ready);
+                    const int src = lane + int(adv);
+#pragma unroll
+                    for (int r = 0; r < RQ; ++r) {
+                        rc[r] = __shfl_sync(0xFFFFFFFFu, rc[r], src & 31);
+                        rn[r] = __shfl_sync(0xFFFFFFFFu, rn[r], src & 31);
+                    }
+                    n = __shfl_sync(0xFFFFFFFFu, n, src & 31);
+                    kx = __shfl_sync(0xFFFFFFFFu, kx, src & 31);
+                    ke = __shfl_sync(0xFFFFFFFFu, ke, src & 31);
+                    if (src >= 32)
+                        load_reqs(ready + unsigned(lane));
                     ns = 0;
                 } else {
-                    ns = ns ? min(ns * 2, 128u) : 16u;
+                    ns = ns ? min(ns * 2, a.poll_ns) : 16u;
                     __nanosleep(ns);
                 }
             }
@@ -2252,16 +2306,14 @@ static void wave_pair_launch(const WaveArgs& a, int sms, cudaStream_t st) {
 }
 
 // CTAs per view task (USCG_WAVE_PAIR = 0 single, 1 or 2 pairs, 4 clusters of
-// four forces it). Pairs pay when the pairs of all tasks in flight find SMs:
-// up to three 32-problem chunks (C2 per GPU at 2-8 GPUs, ms per sweep:
-// 16 problems 2.87 vs 4.76 single, 32: 3.72 vs 4.84, 64: 4.06 vs 4.92). At
-// 128 problems the single-CTA form holds twice the tasks of the 74 resident
-// pairs (pairs 5.38 vs 5.44) and stays. Clusters of four measured slower than
-// pairs at every size (3.22, 4.05, 4.53 ms: three partial exchanges per line
-// cost more than the halved per-CTA row traffic saves) and are opt-in only.
-// Two task slots per CTA measured slower (6.26 ms at 128 problems, 5.53 at
-// 32: two tasks sharing one SM's load/store path gain nothing) and are not
-// dispatched.
+// four forces it). Pairs pay while the pairs of the tasks in flight find SMs:
+// up to four 32-problem chunks (ms per C2 iteration, pairs vs single CTA:
+// 16 problems 2.42 vs 5.54, 32: 3.11 vs 4.71, 64: 3.10 vs 4.73, 128: 4.32 vs
+// 4.79). Clusters of four measured slower than pairs (2.68, 3.11, 4.36 ms:
+// three partial exchanges per line cost more than the halved per-CTA row
+// traffic saves) and are opt-in only. Two task slots per CTA measured slower
+// (6.26 ms at 128 problems, 5.53 at 32: two tasks sharing one SM's
+// load/store path gain nothing) and are not dispatched.
 int wave_cluster_size(const MartArgs& h) {
     const int P = h.Sp / h.nchunks;
     if (P != 16 && P != 32)
@@ -2270,7 +2322,7 @@ int wave_cluster_size(const MartArgs& h) {
         const int c = std::atoi(e);
         return c >= 4 ? 4 : c >= 2 ? 2 : c == 1 ? 2 : 1;
     }
-    return h.Sp <= 96 ? 2 : 1;
+    return h.Sp <= 128 ? 2 : 1;
 }
 
 bool wave_supported(const MartArgs& h) {
@@ -2325,6 +2377,12 @@ void launch_mart_wave(const MartArgs& h, const WaveSchedule& ws, unsigned* prog,
     // per iteration with default priorities)
     a.l2_field = 2;
     a.l2_lists = 1;
+    a.poll_ns = 256;
+    a.pub_ns = 32;
+    if (const char* e = std::getenv("USCG_WAVE_POLL_NS"))
+        a.poll_ns = unsigned(std::max(16, std::atoi(e)));
+    if (const char* e = std::getenv("USCG_WAVE_PUB_NS"))
+        a.pub_ns = unsigned(std::max(0, std::atoi(e)));
     if (const char* e = std::getenv("USCG_WAVE_L2")) {  // experiments: "<field><lists>" priorities
         a.l2_field = e[0] ? e[0] - '0' : 0;
         a.l2_lists = e[0] && e[1] ? e[1] - '0' : 0;

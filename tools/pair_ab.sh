@@ -9,3 +9,5 @@ USCG_WAVE_PAIR=0 run single "--problems $S"
 USCG_WAVE_PAIR=2 run cl2 "--problems $S"
 USCG_WAVE_PAIR=4 run cl4 "--problems $S"
 done
+USCG_WAVE_PAIR=0 run single "--problems 128"
+USCG_WAVE_PAIR=2 run cl2 "--problems 128"

@@ -50,7 +50,13 @@ typedef enum {
 enum {
     USCG_DEVICE_POINTERS = 1u,     /* buffers are device memory */
     USCG_LAYOUT_INTERLEAVED = 2u,  /* device-native problem-minor layouts */
-    USCG_MODEL_LENGTH = 4u         /* uscg_project: ForwardModel::LengthWeighted */
+    USCG_MODEL_LENGTH = 4u,        /* uscg_project: ForwardModel::LengthWeighted */
+    USCG_UPDATE_POWER = 8u         /* uscg_reconstruct: the multiplicative MART correction
+                                      x *= (m/p)^beta (BASELINE north_star's (m/p)^(lambda a/max a)
+                                      with binary coefficients) instead of the reference's linear
+                                      1 - beta (1 - m/p) (proj/src/solver.cpp:41); an extension
+                                      with no reference counterpart, checked against the oracle's
+                                      same-named variant only */
 };
 
 typedef struct uscg_ctx_s* uscg_ctx;
@@ -257,6 +263,16 @@ uscg_status uscg_resample(uscg_ctx ctx, const uscg_grid* grid, const float* fiel
                           int32_t problems, int32_t npix, float* out, uint32_t flags);
 /* uspg_to_cg_map(n) itself (grid.hpp:84), n*n u32, host output. */
 uscg_status uscg_uspg_to_cg_map(uscg_ctx ctx, int32_t n, uint32_t* out);
+/* cartesian_to_field (proj/include/uscg/phantom.hpp:59, proj/src/phantom.cpp:165-180):
+ * the inverse of uscg_resample for the reference law. images: [S][slices][npix][npix]
+ * (row 0 at the bottom, as uscg_resample writes them); field_out: S fields in
+ * the host layout [S][cell_count] (or, with USCG_LAYOUT_INTERLEAVED, the
+ * device-native [cell_count][S_pad]). Errors as the reference: a grid that
+ * fails GridSpec::validate, and npix != 2 * n_rings ("slice shape does not
+ * match the grid", invalid argument). Other sector laws have no
+ * uspg_to_cg_map (the reference's is for its own law only): invalid argument. */
+uscg_status uscg_cartesian_to_field(uscg_ctx ctx, const uscg_grid* grid, const float* images, int32_t problems,
+                                    int32_t npix, float* field_out, uint32_t flags);
 
 /* ---- image-quality metrics (proj/src/metrics.cpp) on the device ------------
  * ref, test: `slices` rasters of rows x cols floats each (row-major, row 0 at
@@ -272,6 +288,16 @@ uscg_status uscg_image_metrics(uscg_ctx ctx, const float* ref, const float* test
                                int32_t rows, int32_t cols, int32_t shared_range,
                                double dynamic_range, double* mae_out, double* rmse_out,
                                double* ssim_out, uint32_t flags);
+/* sharpness (proj/src/metrics.cpp:138-152) of each of `slices` rows x cols
+ * rasters: the mean central-difference gradient magnitude (one-sided at the
+ * borders), fp64. Errors as the reference: rows or cols < 2 ("sharpness needs
+ * at least a 2x2 image", invalid argument). */
+uscg_status uscg_image_sharpness(uscg_ctx ctx, const float* image, int32_t slices, int32_t rows, int32_t cols,
+                                 double* sharpness_out, uint32_t flags);
+/* intensity_profile (proj/src/metrics.cpp:154-159): row `row` of one rows x
+ * cols raster (host memory) as doubles. Errors as the reference: row outside
+ * [0, rows) ("profile row out of range", invalid argument). Host only. */
+uscg_status uscg_intensity_profile(const float* image, int32_t rows, int32_t cols, int32_t row, double* out);
 
 /* ---- Cartesian comparator (proj/include/uscg/siddon.hpp) ------------------
  * The paper's baseline on the same hardware: MART on an axis-aligned voxel

@@ -15,6 +15,9 @@
 //   uscg::generate_projections phantom.hpp:51-52 uscg_b200::generate_projections (Binary)
 //   uscg::field_to_cartesian   phantom.hpp:56    uscg_b200::field_to_cartesian
 //   uscg::uspg_to_cg_map       grid.hpp:84       uscg_b200::uspg_to_cg_map
+//   uscg::cartesian_to_field   phantom.hpp:59    uscg_b200::cartesian_to_field
+//   uscg::Image, mae, rmse, ssim, sharpness, intensity_profile, area_average
+//                              metrics.hpp:9-33  uscg_b200:: (same names)
 #pragma once
 
 #include <cstdint>
@@ -184,12 +187,17 @@ struct ProjectionSet {
     double at(int view, int line) const { return data[std::size_t(view) * geometry.lines() + line]; }
 };
 
+/// Update form: Linear is the reference's 1 - beta (1 - m/p) (solver.cpp:41);
+/// Power the multiplicative (m/p)^beta (USCG_UPDATE_POWER, an extension)
+enum class UpdateForm { Linear, Power };
+
 struct SolverConfig {
     double beta = 0.4;
     double tolerance = 1e-6;
     int max_sweeps = 100;
     double f_init = 1.0;
     double p_floor = 0;
+    UpdateForm update = UpdateForm::Linear;
 };
 
 struct ReconReport {
@@ -224,7 +232,8 @@ inline ReconResult run(const ProjectionSet& proj, const GridSpec& spec, const So
     rep.sweep_residuals = r.report.sweep_residuals.data();
     rep.crossed = r.report.crossed.data();
     const uscg_solver_config c{cfg.beta, cfg.tolerance, cfg.max_sweeps, cfg.f_init, cfg.p_floor};
-    check(uscg_reconstruct(tracer.get(), p.data(), 1, &c, f.data(), init ? 1 : 0, &rep, 0));
+    check(uscg_reconstruct(tracer.get(), p.data(), 1, &c, f.data(), init ? 1 : 0, &rep,
+                           cfg.update == UpdateForm::Power ? uint32_t(USCG_UPDATE_POWER) : 0u));
     r.field = Field{spec, std::vector<double>(f.begin(), f.end())};
     r.report.sweeps = rep.sweeps;
     r.report.converged = rep.converged != 0;
@@ -261,18 +270,101 @@ inline ProjectionSet generate_projections(const Field& field, const ScanGeometry
     return ProjectionSet{geom, std::vector<double>(out.begin(), out.end())};
 }
 
-/// field_to_cartesian (phantom.cpp:149-163): slices x n x n, row 0 at the bottom
-inline std::vector<std::vector<double>> field_to_cartesian(const Field& field, Context& ctx = Context::shared()) {
+/// Image (metrics.hpp:9-16): rows x cols, row-major, row 0 at the bottom
+struct Image {
+    int rows = 0;
+    int cols = 0;
+    std::vector<double> v;
+
+    double at(int row, int col) const { return v[std::size_t(row) * cols + col]; }
+    double& at(int row, int col) { return v[std::size_t(row) * cols + col]; }
+};
+
+/// field_to_cartesian (phantom.cpp:149-163): one n x n Image per slice
+inline std::vector<Image> field_to_cartesian(const Field& field, Context& ctx = Context::shared()) {
     const GridSpec& s = field.spec;
     const int npix = s.n;
     std::vector<float> f(field.values.begin(), field.values.end());
     std::vector<float> out(std::size_t(s.slices()) * npix * npix);
     const uscg_grid g = s.c_grid();
     check(uscg_resample(ctx.get(), &g, f.data(), 1, npix, out.data(), 0));
-    std::vector<std::vector<double>> imgs(std::size_t(s.slices()));
+    std::vector<Image> imgs(std::size_t(s.slices()));
     for (int k = 0; k < s.slices(); ++k)
-        imgs[k].assign(out.begin() + std::size_t(k) * npix * npix, out.begin() + std::size_t(k + 1) * npix * npix);
+        imgs[k] = Image{npix, npix,
+                        std::vector<double>(out.begin() + std::size_t(k) * npix * npix,
+                                            out.begin() + std::size_t(k + 1) * npix * npix)};
     return imgs;
+}
+
+/// cartesian_to_field (phantom.cpp:165-180): the inverse permutation, on the device
+inline Field cartesian_to_field(const std::vector<Image>& slices, const GridSpec& spec,
+                                Context& ctx = Context::shared()) {
+    if (int(slices.size()) != spec.slices())
+        throw std::invalid_argument("slice count does not match the grid");
+    const int npix = slices.empty() ? 0 : slices[0].rows;
+    std::vector<float> in;
+    in.reserve(std::size_t(spec.slices()) * npix * npix);
+    for (const Image& img : slices) {
+        if (img.rows != npix || img.cols != npix || img.v.size() != std::size_t(npix) * npix)
+            throw std::invalid_argument("slice shape does not match the grid");
+        in.insert(in.end(), img.v.begin(), img.v.end());
+    }
+    std::vector<float> out(spec.cell_count());
+    const uscg_grid g = spec.c_grid();
+    check(uscg_cartesian_to_field(ctx.get(), &g, in.data(), 1, npix, out.data(), 0));
+    return Field{spec, std::vector<double>(out.begin(), out.end())};
+}
+
+namespace detail {
+inline void metrics_of(const Image& ref, const Image& test, double* mae_o, double* rmse_o, double* ssim_o,
+                       double dynamic_range, Context& ctx) {
+    if (ref.rows != test.rows || ref.cols != test.cols || ref.v.size() != test.v.size())
+        throw std::invalid_argument("image shapes differ");
+    std::vector<float> a(ref.v.begin(), ref.v.end()), b(test.v.begin(), test.v.end());
+    check(uscg_image_metrics(ctx.get(), a.data(), b.data(), 1, ref.rows, ref.cols, 0, dynamic_range, mae_o, rmse_o,
+                             ssim_o, 0));
+}
+}  // namespace detail
+
+/// mae / rmse / ssim (metrics.cpp:35-60,105-136) on the device
+inline double mae(const Image& ref, const Image& test, Context& ctx = Context::shared()) {
+    double m = 0;
+    detail::metrics_of(ref, test, &m, nullptr, nullptr, -1, ctx);
+    return m;
+}
+inline double rmse(const Image& ref, const Image& test, Context& ctx = Context::shared()) {
+    double r = 0;
+    detail::metrics_of(ref, test, nullptr, &r, nullptr, -1, ctx);
+    return r;
+}
+inline double ssim(const Image& ref, const Image& test, double dynamic_range = -1, Context& ctx = Context::shared()) {
+    double v = 0;
+    detail::metrics_of(ref, test, nullptr, nullptr, &v, dynamic_range, ctx);
+    return v;
+}
+/// area_average (metrics.cpp:62-69), host
+inline double area_average(const Image& image) {
+    if (image.v.empty())
+        throw std::invalid_argument("empty image");
+    double acc = 0;
+    for (double x : image.v)
+        acc += x;
+    return acc / double(image.v.size());
+}
+/// sharpness (metrics.cpp:138-152) on the device
+inline double sharpness(const Image& image, Context& ctx = Context::shared()) {
+    if (image.v.size() != std::size_t(image.rows) * std::size_t(image.cols > 0 ? image.cols : 0))
+        throw std::invalid_argument("image size does not match rows x cols");
+    std::vector<float> a(image.v.begin(), image.v.end());
+    double out = 0;
+    check(uscg_image_sharpness(ctx.get(), a.data(), 1, image.rows, image.cols, &out, 0));
+    return out;
+}
+/// intensity_profile (metrics.cpp:154-159)
+inline std::vector<double> intensity_profile(const Image& image, int row) {
+    if (row < 0 || row >= image.rows)
+        throw std::invalid_argument("profile row out of range");
+    return {image.v.begin() + std::size_t(row) * image.cols, image.v.begin() + std::size_t(row + 1) * image.cols};
 }
 
 /// uspg_to_cg_map (grid.hpp:84)

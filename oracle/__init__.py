@@ -137,6 +137,11 @@ class Orc:
         L.orc_rmse.restype = C.c_double
         L.orc_ssim.argtypes = [C.c_int, C.c_int, _dp, _dp, C.c_double]
         L.orc_ssim.restype = C.c_double
+        L.orc_cartesian_to_field.argtypes = [C.POINTER(_Grid), C.c_int, _dp, _dp]
+        L.orc_cartesian_to_field.restype = C.c_int
+        L.orc_sharpness.argtypes = [C.c_int, C.c_int, _dp]
+        L.orc_set_update_power.argtypes = [C.c_int]
+        L.orc_sharpness.restype = C.c_double
 
     # -- ray generators -------------------------------------------------
     def rays_flat(self, src, ctr, det_u, det_v, su, sv):
@@ -197,6 +202,18 @@ class Orc:
         out = np.zeros(n * n, np.uint32)
         self.L.orc_uspg_to_cg_map(n, _ptr(out, _u32p))
         return out
+
+    def cartesian_to_field(self, grid: OrcGrid, images, npix):
+        """cartesian_to_field (reference law): images (slices, npix, npix) -> cell_count f64"""
+        im = np.ascontiguousarray(images, dtype=np.float64)
+        out = np.zeros(grid.cell_count())
+        if self.L.orc_cartesian_to_field(C.byref(grid._c), npix, _ptr(im, _dp), _ptr(out, _dp)) != 0:
+            raise ValueError("slice shape does not match the grid")
+        return out
+
+    def sharpness(self, img):
+        a = np.ascontiguousarray(img, float)
+        return self.L.orc_sharpness(a.shape[0], a.shape[1], _ptr(a, _dp))
 
     def bin_map(self, grid: OrcGrid, npix):
         out = np.zeros(npix * npix, np.uint32)
@@ -272,7 +289,9 @@ class OrcCache:
         return out
 
     def reconstruct(self, thetas, proj, init=None, beta=0.4, tolerance=1e-6, max_sweeps=100,
-                    f_init=1.0, p_floor=0.0):
+                    f_init=1.0, p_floor=0.0, power=False):
+        """orc_reconstruct; power=True: the (m/p)^beta update (the device's
+        USCG_UPDATE_POWER), not a reference behaviour"""
         th = np.ascontiguousarray(thetas, float)
         p = np.ascontiguousarray(proj, float)
         if init is None:
@@ -282,10 +301,12 @@ class OrcCache:
         report = np.zeros(6)
         residuals = np.zeros(max_sweeps)
         crossed = np.zeros(self.grid.cell_count(), np.uint8)
+        self.orc.L.orc_set_update_power(int(bool(power)))
         rc = self.orc.L.orc_reconstruct(C.byref(self.grid._c), C.byref(self._c), th.size, _ptr(th, _dp),
                                         _ptr(p, _dp), _ptr(field, _dp), beta, tolerance, max_sweeps,
                                         p_floor, _ptr(report, _dp), _ptr(residuals, _dp),
                                         _ptr(crossed, _u8p))
+        self.orc.L.orc_set_update_power(0)
         if rc != 0:
             raise ValueError("invalid reconstruction input")
         sweeps = int(report[0])
@@ -345,6 +366,9 @@ class Ref:
         L.ref_ssim.argtypes = [C.c_int, C.c_int, _dp, _dp, C.c_double]
         L.ref_ssim.restype = C.c_double
         L.ref_phantom.argtypes = [C.c_int, C.c_double, C.c_double, C.c_int, C.c_int, _dp]
+        L.ref_cartesian_to_field.argtypes = [C.c_int, C.c_double, C.c_double, C.c_int, C.c_int, _dp, _dp]
+        L.ref_sharpness.argtypes = [C.c_int, C.c_int, _dp, _dp]
+        L.ref_intensity_profile.argtypes = [C.c_int, C.c_int, _dp, C.c_int, _dp]
 
     def check(self, rc):
         if rc == 1:
@@ -373,6 +397,26 @@ class Ref:
         slices = n if volume else 1
         out = np.zeros((slices, n, n))
         self.check(self.L.ref_field_to_cartesian(n, 2.0 / n, 2.0 / n, int(volume), _ptr(f, _dp), _ptr(out, _dp)))
+        return out
+
+    def cartesian_to_field(self, n, volume, images, img_n=None):
+        im = np.ascontiguousarray(images, float)
+        img_n = n if img_n is None else img_n
+        out = np.zeros((n if volume else 1) * n * n)
+        self.check(self.L.ref_cartesian_to_field(n, 2.0 / n, 2.0 / n, int(volume), img_n, _ptr(im, _dp),
+                                                 _ptr(out, _dp)))
+        return out
+
+    def sharpness(self, img):
+        a = np.ascontiguousarray(img, float)
+        out = np.zeros(1)
+        self.check(self.L.ref_sharpness(a.shape[0], a.shape[1], _ptr(a, _dp), _ptr(out, _dp)))
+        return float(out[0])
+
+    def intensity_profile(self, img, row):
+        a = np.ascontiguousarray(img, float)
+        out = np.zeros(a.shape[1])
+        self.check(self.L.ref_intensity_profile(a.shape[0], a.shape[1], _ptr(a, _dp), row, _ptr(out, _dp)))
         return out
 
     def cartesian_system(self, n, volume, src, ctr, det_u, det_v, su, sv, views):

@@ -250,6 +250,37 @@ int ref_field_to_cartesian(int n, double r, double h, int volume, const double* 
     });
 }
 
+// images: slices*n*n f64 (row 0 at the bottom) -> field cell_count f64
+int ref_cartesian_to_field(int n, double r, double h, int volume, int img_n, const double* images,
+                           double* field) {
+    return guarded([&] {
+        const GridSpec spec = make_spec(n, r, h, volume);
+        std::vector<Image> slices;
+        for (int s = 0; s < spec.slices(); ++s)
+            slices.push_back(Image{img_n, img_n,
+                                   std::vector<double>(images + std::size_t(s) * img_n * img_n,
+                                                       images + std::size_t(s + 1) * img_n * img_n)});
+        const Field f = cartesian_to_field(slices, spec);
+        std::memcpy(field, f.values.data(), f.values.size() * sizeof(double));
+    });
+}
+
+// sharpness of one image; *out receives the value (errors: status 1 + message)
+int ref_sharpness(int rows, int cols, const double* a, double* out) {
+    return guarded([&] {
+        Image ia{rows, cols, std::vector<double>(a, a + std::size_t(std::max(rows, 0)) * std::max(cols, 0))};
+        *out = sharpness(ia);
+    });
+}
+
+int ref_intensity_profile(int rows, int cols, const double* a, int row, double* out) {
+    return guarded([&] {
+        Image ia{rows, cols, std::vector<double>(a, a + std::size_t(rows) * cols)};
+        const std::vector<double> p = intensity_profile(ia, row);
+        std::memcpy(out, p.data(), p.size() * sizeof(double));
+    });
+}
+
 double ref_rmse(int rows, int cols, const double* a, const double* b) {
     Image ia{rows, cols, std::vector<double>(a, a + std::size_t(rows) * cols)};
     Image ib{rows, cols, std::vector<double>(b, b + std::size_t(rows) * cols)};

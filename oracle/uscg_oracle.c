@@ -12,6 +12,8 @@
 #include <stdlib.h>
 #include <string.h>
 
+static int g_update_power = 0;
+
 static const double kPi = 3.141592653589793238462643383279502884;
 #define DEG_PER_RAD (180.0 / 3.141592653589793238462643383279502884)
 #define RAD_PER_DEG (3.141592653589793238462643383279502884 / 180.0)
@@ -621,7 +623,9 @@ int orc_reconstruct(const orc_grid* g, const orc_cache* c, int views, const doub
                 for (int64_t i = 0; i < n; ++i)
                     p_bar += field[active[i]];
                 const double ratio = m / (p_bar > p_floor ? p_bar : p_floor);
-                double factor = 1.0 - beta * (1.0 - ratio);
+                /* linear binary form (solver.cpp:41); or, when selected, the
+                   power form (m/p)^beta, the builder's extension (USCG_UPDATE_POWER) */
+                double factor = g_update_power ? (ratio > 0 ? pow(ratio, beta) : 0.0) : 1.0 - beta * (1.0 - ratio);
                 if (factor <= 0) {
                     factor = p_floor;
                     clamps += 1;
@@ -663,6 +667,10 @@ int orc_reconstruct(const orc_grid* g, const orc_cache* c, int views, const doub
     free(crossed);
     return 0;
 }
+
+/* update form of orc_reconstruct: 0 the reference's linear 1 - beta (1 - m/p)
+   (solver.cpp:41), 1 the power form (m/p)^beta (no reference counterpart) */
+void orc_set_update_power(int on) { g_update_power = on != 0; }
 
 /* ---- polar -> Cartesian (src/grid.cpp:75-99, src/phantom.cpp:149-163) ---- */
 
@@ -739,6 +747,23 @@ void orc_field_to_cartesian(const orc_grid* g, int npix, const double* field, do
     free(map);
 }
 
+/* cartesian_to_field (src/phantom.cpp:165-180): dst[flat] = img[map[flat]],
+   reference law only (npix = 2*rings); returns 2 otherwise */
+int orc_cartesian_to_field(const orc_grid* g, int npix, const double* images, double* field) {
+    if (g->counts || npix != 2 * g->n_rings)
+        return 2;
+    const int slices = g->volume ? g->n_slices : 1;
+    const uint64_t per_slice = orc_cells_per_slice(g);
+    const size_t npx = (size_t)npix * npix;
+    uint32_t* map = (uint32_t*)malloc(sizeof(uint32_t) * npx);
+    orc_uspg_to_cg_map(npix, map);
+    for (int s = 0; s < slices; ++s)
+        for (size_t f = 0; f < npx; ++f)
+            field[(size_t)s * per_slice + f] = images[(size_t)s * npx + map[f]];
+    free(map);
+    return 0;
+}
+
 /* ---- metrics (src/metrics.cpp:42-50,105-136) ---------------------------- */
 
 double orc_rmse(size_t n, const double* a, const double* b) {
@@ -789,6 +814,24 @@ double orc_ssim(int rows, int cols, const double* ref, const double* test, doubl
         }
     const size_t windows = (size_t)(rows - W + 1) * (size_t)(cols - W + 1);
     return acc / windows;
+}
+
+/* sharpness (src/metrics.cpp:138-152): mean central-difference gradient
+   magnitude, the neighbours clamped to the image and divided by their
+   distance; NAN below 2x2 (the reference throws) */
+double orc_sharpness(int rows, int cols, const double* img) {
+    if (rows < 2 || cols < 2)
+        return NAN;
+    double acc = 0;
+    for (int r = 0; r < rows; ++r)
+        for (int c = 0; c < cols; ++c) {
+            const int cl = c > 0 ? c - 1 : 0, ch = c + 1 < cols ? c + 1 : cols - 1;
+            const int rl = r > 0 ? r - 1 : 0, rh = r + 1 < rows ? r + 1 : rows - 1;
+            const double gx = (img[(size_t)r * cols + ch] - img[(size_t)r * cols + cl]) / (ch - cl);
+            const double gy = (img[(size_t)rh * cols + c] - img[(size_t)rl * cols + c]) / (rh - rl);
+            acc += sqrt(gx * gx + gy * gy);
+        }
+    return acc / ((size_t)rows * cols);
 }
 
 /* ---- libm probes for the device-math parity tests ------------------------ */

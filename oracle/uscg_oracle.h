@@ -95,6 +95,9 @@ int orc_reconstruct(const orc_grid* g, const orc_cache* c, int views, const doub
                     int max_sweeps, double p_floor, double* report, double* residuals,
                     uint8_t* crossed);
 
+/* orc_reconstruct's update: 0 linear (the reference), 1 power (m/p)^beta */
+void orc_set_update_power(int on);
+
 /* uspg_to_cg_map (reference law, n = 2*rings) */
 int orc_uspg_to_cg_map(int n, uint32_t* out);
 /* bin-point map for any law (oracles.hpp:36-58 applied to pixel centres):
@@ -109,6 +112,10 @@ void orc_math(size_t n, const double* x, const double* y, double* out);
 
 double orc_rmse(size_t n, const double* a, const double* b);
 double orc_ssim(int rows, int cols, const double* a, const double* b, double dynamic_range);
+/* cartesian_to_field, reference law only (2 otherwise): field slices*cps */
+int orc_cartesian_to_field(const orc_grid* g, int npix, const double* images, double* field);
+/* sharpness of one rows x cols image (NAN below 2x2) */
+double orc_sharpness(int rows, int cols, const double* img);
 
 #ifdef __cplusplus
 }

@@ -1629,6 +1629,7 @@ static void reconstruct_body(uscg_tracer t, const float* proj, int32_t problems,
     h.active = t->w_active.p;
     h.clamps = t->w_clamps.p;
     h.beta = cfg->beta;
+    h.power = (flags & USCG_UPDATE_POWER) ? 1 : 0;
     h.Sp = Sp;
     h.nchunks = Sp / P;
     h.max_recs = t->max_recs;
@@ -2183,6 +2184,86 @@ uscg_status uscg_resample(uscg_ctx ctx, const uscg_grid* grid, const float* fiel
         if (!dev)
             UB_CUDA(cudaMemcpyAsync(out, fout, sizeof(float) * out_n, cudaMemcpyDeviceToHost, st));
         UB_CUDA(cudaStreamSynchronize(st));
+    });
+}
+
+uscg_status uscg_cartesian_to_field(uscg_ctx ctx, const uscg_grid* grid, const float* images, int32_t problems,
+                                    int32_t npix, float* field_out, uint32_t flags) {
+    return guarded([&] {
+        bind(ctx);
+        validate_grid(grid);  // spec.validate() (phantom.cpp:166)
+        need(images && field_out, "null buffer");
+        need(problems >= 1, "problem count must be >= 1");
+        need(grid->ring_counts == nullptr,
+             "cartesian_to_field needs the reference sector law (uspg_to_cg_map is defined for it only)");
+        need(npix == 2 * grid->n_rings, "slice shape does not match the grid");  // phantom.cpp:174-175
+        uscg_tracer_s g;
+        g.ctx = ctx;
+        fill_grid(&g, grid);
+        const int S = problems;
+        const bool dev = flags & USCG_DEVICE_POINTERS;
+        const bool inter = flags & USCG_LAYOUT_INTERLEAVED;
+        const int Sp = inter ? problem_stride(S) : 0;
+        const int slices = g.n_slices;
+        const uint64_t in_n = uint64_t(npix) * npix * slices * S;
+        const uint64_t out_n = g.cells * uint64_t(inter ? Sp : S);
+        cudaStream_t st = ctx->stream;
+        DevBuf<float> d_in, d_out;
+        const float* in = images;
+        if (!dev) {
+            d_in.alloc(in_n);
+            UB_CUDA(cudaMemcpyAsync(d_in.p, images, sizeof(float) * in_n, cudaMemcpyHostToDevice, st));
+            in = d_in.p;
+        }
+        float* out = field_out;
+        if (!dev) {
+            d_out.alloc(out_n);
+            out = d_out.p;
+        }
+        if (inter && Sp > S)  // padded problems stay 0 (every cell of a real problem is written)
+            UB_CUDA(cudaMemsetAsync(out, 0, sizeof(float) * out_n, st));
+        launch_cart_to_field(in, g.cps, slices, S, Sp, npix, out, st);
+        if (!dev)
+            UB_CUDA(cudaMemcpyAsync(field_out, out, sizeof(float) * out_n, cudaMemcpyDeviceToHost, st));
+        UB_CUDA(cudaStreamSynchronize(st));
+    });
+}
+
+uscg_status uscg_image_sharpness(uscg_ctx ctx, const float* image, int32_t slices, int32_t rows, int32_t cols,
+                                 double* sharpness_out, uint32_t flags) {
+    return guarded([&] {
+        bind(ctx);
+        need(image && sharpness_out, "null buffer");
+        need(slices >= 1, "volume slice counts differ or are empty");
+        need(rows >= 2 && cols >= 2, "sharpness needs at least a 2x2 image");  // metrics.cpp:139-140
+        const uint64_t px = uint64_t(rows) * uint64_t(cols);
+        const uint64_t n = px * uint64_t(slices);
+        cudaStream_t st = ctx->stream;
+        DevBuf<float> d_img;
+        const float* a = image;
+        if (!(flags & USCG_DEVICE_POINTERS)) {
+            d_img.alloc(n);
+            UB_CUDA(cudaMemcpyAsync(d_img.p, image, sizeof(float) * n, cudaMemcpyHostToDevice, st));
+            a = d_img.p;
+        }
+        if (!ctx->metrics)
+            ctx->metrics = new MetricsWork;
+        MetricsWork& w = *ctx->metrics;
+        w.part.ensure(size_t(slices) * size_t(metrics_blocks(px)));
+        w.sout.ensure(size_t(slices));
+        launch_sharpness(a, slices, rows, cols, w.part.p, w.sout.p, st);
+        UB_CUDA(cudaMemcpyAsync(sharpness_out, w.sout.p, sizeof(double) * slices, cudaMemcpyDeviceToHost, st));
+        UB_CUDA(cudaStreamSynchronize(st));
+    });
+}
+
+uscg_status uscg_intensity_profile(const float* image, int32_t rows, int32_t cols, int32_t row, double* out) {
+    return guarded([&] {
+        need(image && out, "null buffer");
+        need(rows >= 1 && cols >= 1, "empty image");
+        need(row >= 0 && row < rows, "profile row out of range");  // metrics.cpp:155-156
+        for (int32_t c = 0; c < cols; ++c)
+            out[c] = double(image[size_t(row) * size_t(cols) + size_t(c)]);
     });
 }
 

@@ -1586,6 +1586,59 @@ void launch_tiled_resample(const float* field, uint64_t cps, int slices, int S, 
     check_launch();
 }
 
+// cartesian_to_field (proj/src/phantom.cpp:165-180): dst[flat] =
+// img[map[flat]], i.e. pixel i writes the cell cg_inverse(i). A thread takes
+// four consecutive pixels (coalesced float4 reads; n is even) of kResPlanes
+// planes; the permutation is computed once per pixel.
+__global__ void __launch_bounds__(256) cart_to_field_kernel(const float* __restrict__ img, uint64_t cps,
+                                                            int slices, int planes, uint64_t cs, uint64_t ps,
+                                                            int n, float* __restrict__ field) {
+    const uint32_t npx = uint32_t(n) * uint32_t(n);
+    const uint32_t q = (blockIdx.x * blockDim.x + threadIdx.x) * 4u;
+    if (q >= npx)
+        return;
+    uint32_t m[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        const uint32_t px = q + uint32_t(k);
+        m[k] = cg_inverse(int(px / uint32_t(n)), int(px % uint32_t(n)), n);
+    }
+    const int p0 = int(blockIdx.y) * kResPlanes, p1 = min(planes, p0 + kResPlanes);
+    for (int pl = p0; pl < p1; ++pl) {
+        const int s = pl % slices, p = pl / slices;
+        const float* src = img + uint64_t(pl) * npx + q;
+        float v[4];
+        if ((reinterpret_cast<uintptr_t>(src) & 15) == 0) {
+            const float4 x = __ldcs(reinterpret_cast<const float4*>(src));
+            v[0] = x.x, v[1] = x.y, v[2] = x.z, v[3] = x.w;
+        } else {
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+                v[k] = __ldcs(src + k);
+        }
+        float* f = field + uint64_t(s) * cps * cs + uint64_t(p) * ps;
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+            f[uint64_t(m[k]) * cs] = v[k];
+    }
+}
+
+void launch_cart_to_field(const float* img, uint64_t cps, int slices, int S, int Sp, int n, float* field,
+                          cudaStream_t st) {
+    const uint64_t npx = uint64_t(n) * uint64_t(n);
+    if (npx * slices * S == 0)
+        return;
+    const uint64_t cells = cps * slices;
+    const uint64_t cs = Sp > 0 ? uint64_t(Sp) : 1, ps = Sp > 0 ? 1 : cells;
+    const int planes = slices * S;
+    const int rows = (planes + kResPlanes - 1) / kResPlanes;
+    if (rows > 65535)
+        throw CudaError("cartesian_to_field: too many planes for one launch");
+    const dim3 grid(unsigned((npx / 4 + 255) / 256), unsigned(rows));
+    cart_to_field_kernel<<<grid, 256, 0, st>>>(img, cps, slices, planes, cs, ps, n, field);
+    check_launch();
+}
+
 __global__ void cg_map_kernel(int n, uint32_t* out) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n * n)

@@ -24,7 +24,20 @@ struct MartArgs {
     int max_recs;
     int max_cells;
     int run = 1;  // lines per dataflow task: shared memory holds `run` index lists per group
+    int power = 0;  // USCG_UPDATE_POWER: multiplicative form (m/p)^beta instead of solver.cpp:41
 };
+
+// The line's multiplicative correction from ratio = m / max(p, p_floor).
+// Linear (the reference, proj/src/solver.cpp:41): 1 - beta (1 - ratio).
+// Power (USCG_UPDATE_POWER; the multiplicative MART form x *= (m/p)^(beta a/max a)
+// with binary coefficients, a = max a = 1): ratio^beta; a non-positive ratio
+// gives 0, which the callers clamp to p_floor like the reference's
+// non-positive linear factor (solver.cpp:42-45).
+__device__ __forceinline__ double mart_factor(double ratio, double beta, int power) {
+    if (power)
+        return ratio > 0 ? pow(ratio, beta) : 0.0;
+    return 1.0 - beta * (1.0 - ratio);
+}
 
 // problem-chunk width P for S problems (power of two <= 32)
 int chunk_limit();
@@ -190,6 +203,9 @@ void launch_fill(float* p, uint64_t n, float v, cudaStream_t st);
 int metrics_blocks(uint64_t px);
 void launch_moments(const float* ref, const float* test, int slices, uint64_t px, double* part,
                     double* out, cudaStream_t st);
+// mean gradient magnitude per slice (sharpness); part: slices * metrics_blocks(px) doubles
+void launch_sharpness(const float* img, int slices, int rows, int cols, double* part, double* out,
+                      cudaStream_t st);
 // mean SSIM per slice; c1c2 [slices][2]; part: slices * ssim_tiles(rows, cols) doubles
 int ssim_tiles(int rows, int cols);
 void launch_ssim(const float* ref, const float* test, int slices, int rows, int cols,
@@ -242,6 +258,11 @@ void launch_tiled_resample(const float* field, uint64_t cps, int slices, int S, 
 void launch_map_resample(const float* field, uint64_t cells_per_slice, int slices, int S, int Sp,
                          const uint32_t* map, int npix, float* out, cudaStream_t st);
 void launch_cg_map(int n, uint32_t* out, cudaStream_t st);
+// cartesian_to_field for the reference law (npix = 2 * rings): field cell of
+// pixel (row, col) = the inverse permutation; images [S][slices][n][n] ->
+// field [S][cells] (Sp <= 0) or [cells][Sp]
+void launch_cart_to_field(const float* img, uint64_t cps, int slices, int S, int Sp, int n, float* field,
+                          cudaStream_t st);
 // out[4*i + {0: atan2_cr, 1: hypot_cr, 2: azimuth_deg, 3: libdevice atan2}]
 void launch_diag_math(int n, const double* x, const double* y, double* out, cudaStream_t st);
 

@@ -317,7 +317,7 @@ struct GroupWorker {
         const double m = double(m_next);
         if (m != 0 && act_next) {
             const double ratio = m / (p_bar > pf_next ? p_bar : pf_next);
-            factor = 1.0 - A.beta * (1.0 - ratio);
+            factor = mart_factor(ratio, A.beta, A.power);
             if (factor <= 0) {
                 factor = pf_next;
                 atomicAdd(A.clamps + size_t(chunk) * P + t, 1ull);
@@ -2013,7 +2013,7 @@ __global__ void __launch_bounds__(pair::Shape<P, SLOTS>::NT, 1) mart_wave_pair_k
                 double factor = 0;
                 if (m != 0.f && act) {
                     const double ratio = double(m) / (p_bar > pf ? p_bar : pf);
-                    factor = 1.0 - a.m.beta * (1.0 - ratio);
+                    factor = mart_factor(ratio, a.m.beta, a.m.power);
                     if (factor <= 0) {
                         factor = pf;
                         if (rank == 0)

@@ -125,7 +125,7 @@ __global__ void __launch_bounds__(kTileNT, 1) mart_tile_kernel(TileKernelArgs a)
         for (int o = 16; o > 0; o >>= 1)
             s += __shfl_xor_sync(0xFFFFFFFFu, s, o);
         const double ratio = double(r.m) / (s > pf ? s : pf);
-        double f = 1.0 - beta * (1.0 - ratio);
+        double f = mart_factor(ratio, beta, a.m.power);
         if (f <= 0) {
             f = pf;
             clamps += lane == 0;

@@ -195,6 +195,51 @@ void launch_moments(const float* ref, const float* test, int slices, uint64_t px
     UB_CUDA(cudaGetLastError());
 }
 
+// sharpness (metrics.cpp:138-152): per pixel the central-difference gradient
+// magnitude, one-sided at the borders (the clamped neighbours, divided by
+// their distance), fp64 from the fp32 raster; per-block partial sums of one
+// slice (blockIdx.y), folded in block order
+__global__ void __launch_bounds__(kThreads) sharpness_kernel(const float* __restrict__ img, int rows, int cols,
+                                                             double* __restrict__ part) {
+    __shared__ double red[kThreads / 32];
+    const uint64_t px = uint64_t(rows) * uint64_t(cols);
+    const float* a = img + size_t(blockIdx.y) * px;
+    double acc = 0;
+    for (uint64_t i = uint64_t(blockIdx.x) * kThreads + threadIdx.x; i < px; i += uint64_t(gridDim.x) * kThreads) {
+        const int r = int(i / uint64_t(cols)), c = int(i % uint64_t(cols));
+        const int cl = c > 0 ? c - 1 : 0, ch = c + 1 < cols ? c + 1 : cols - 1;
+        const int rl = r > 0 ? r - 1 : 0, rh = r + 1 < rows ? r + 1 : rows - 1;
+        const double gx = (double(a[size_t(r) * cols + ch]) - double(a[size_t(r) * cols + cl])) / double(ch - cl);
+        const double gy = (double(a[size_t(rh) * cols + c]) - double(a[size_t(rl) * cols + c])) / double(rh - rl);
+        acc += sqrt(gx * gx + gy * gy);
+    }
+    const double t = block_sum(acc, red);
+    if (threadIdx.x == 0)
+        part[size_t(blockIdx.y) * gridDim.x + blockIdx.x] = t;
+}
+
+__global__ void fold_mean_kernel(const double* __restrict__ part, int blocks, int slices, double n,
+                                 double* __restrict__ out) {
+    const int s = blockIdx.x * blockDim.x + threadIdx.x;
+    if (s >= slices)
+        return;
+    double acc = 0;
+    for (int k = 0; k < blocks; ++k)
+        acc += part[size_t(s) * blocks + k];
+    out[s] = acc / n;
+}
+
+void launch_sharpness(const float* img, int slices, int rows, int cols, double* part, double* out,
+                      cudaStream_t st) {
+    const uint64_t px = uint64_t(rows) * uint64_t(cols);
+    const int nb = metrics_blocks(px);
+    sharpness_kernel<<<dim3(nb, slices), kThreads, 0, st>>>(img, rows, cols, part);
+    count_launch();
+    fold_mean_kernel<<<(slices + 127) / 128, 128, 0, st>>>(part, nb, slices, double(px), out);
+    count_launch();
+    UB_CUDA(cudaGetLastError());
+}
+
 int ssim_tiles(int rows, int cols) {
     const int wr = rows - kWin + 1, wc = cols - kWin + 1;
     return ((wr + kTileR - 1) / kTileR) * ((wc + kTileC - 1) / kTileC);

@@ -65,6 +65,7 @@ class NoDevice(UscgError):
 DEVICE_POINTERS = 1
 LAYOUT_INTERLEAVED = 2
 MODEL_LENGTH = 4  # uscg_project: ForwardModel::LengthWeighted
+UPDATE_POWER = 8  # uscg_reconstruct: (m/p)^beta update (extension; the reference is linear)
 
 # ---------------------------------------------------------------------------
 # ctypes structures (include/uscg_b200.h)
@@ -124,6 +125,7 @@ EXPORTS = [
     "uscg_resample", "uscg_uspg_to_cg_map", "uscg_diag_math", "uscg_schedule_build", "uscg_image_metrics",
     "uscg_cartesian_like", "uscg_csystem_create", "uscg_csystem_info", "uscg_csystem_export",
     "uscg_csystem_reconstruct", "uscg_csystem_destroy", "uscg_tracer_export_wave",
+    "uscg_cartesian_to_field", "uscg_image_sharpness", "uscg_intensity_profile",
 ]
 
 _lib = None
@@ -189,6 +191,9 @@ def load(build_if_missing: bool = True):
     L.uscg_csystem_destroy.argtypes = [vp]
     L.uscg_image_metrics.argtypes = [vp, vp, vp, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_double, _dp, _dp,
                                      _dp, C.c_uint32]
+    L.uscg_cartesian_to_field.argtypes = [vp, C.POINTER(_Grid), vp, C.c_int32, C.c_int32, vp, C.c_uint32]
+    L.uscg_image_sharpness.argtypes = [vp, vp, C.c_int32, C.c_int32, C.c_int32, _dp, C.c_uint32]
+    L.uscg_intensity_profile.argtypes = [_fp, C.c_int32, C.c_int32, C.c_int32, _dp]
     L.uscg_diag_math.argtypes = [vp, C.c_int32, _dp, _dp, _dp]
     L.uscg_schedule_build.argtypes = [C.c_uint32, C.c_uint32, C.c_uint32, _u32p, _u32p, C.c_uint64, _u32p, _u32p,
                                       _u32p, _u32p, _u32p, C.POINTER(C.c_uint64), _u32p]
@@ -637,11 +642,21 @@ class ProjectionSet:
 
 @dataclass
 class SolverConfig:
+    """SolverConfig (solver.hpp:34-41). ``update``: "linear" is the reference's
+    1 - beta (1 - m/p) (solver.cpp:41); "power" selects the multiplicative
+    (m/p)^beta form (USCG_UPDATE_POWER, an extension without a reference
+    counterpart)."""
     beta: float = 0.4
     tolerance: float = 1e-6
     max_sweeps: int = 100
     f_init: float = 1.0
     p_floor: float = 0.0
+    update: str = "linear"
+
+    def _flags(self) -> int:
+        if self.update not in ("linear", "power"):
+            raise InvalidArgument(f"unknown update form {self.update!r}")
+        return UPDATE_POWER if self.update == "power" else 0
 
 
 @dataclass
@@ -723,7 +738,7 @@ def _run(proj_data: np.ndarray, init: Optional[np.ndarray], cfg: SolverConfig, t
         reps[i].sweep_residuals = resid[i].ctypes.data_as(_dp)
         reps[i].crossed = crossed[i].ctypes.data_as(_u8p) if with_crossed else None
     c = _Cfg(cfg.beta, cfg.tolerance, cfg.max_sweeps, cfg.f_init, cfg.p_floor)
-    _check(load().uscg_reconstruct(tracer.h, _ptr(p), S, C.byref(c), _ptr(fld), from_init, reps, 0))
+    _check(load().uscg_reconstruct(tracer.h, _ptr(p), S, C.byref(c), _ptr(fld), from_init, reps, cfg._flags()))
     out = []
     for i in range(S):
         r = reps[i]
@@ -791,7 +806,8 @@ def reconstruct_batch(stacks, cfg: SolverConfig, tracer: Tracer, inits=None):
     pp = (C.c_void_p * B)(*[C.c_void_p(host(x).ctypes.data) for x in projs])
     ff = (C.c_void_p * B)(*[C.c_void_p(host(x).ctypes.data) for x in flds])
     c = _Cfg(cfg.beta, cfg.tolerance, cfg.max_sweeps, cfg.f_init, cfg.p_floor)
-    _check(load().uscg_reconstruct_batch(tracer.h, B, pp, S, C.byref(c), ff, 0 if inits is None else 1, None, 0))
+    _check(load().uscg_reconstruct_batch(tracer.h, B, pp, S, C.byref(c), ff, 0 if inits is None else 1, None,
+                                         cfg._flags()))
     return [host(f).copy() for f in flds]
 
 
@@ -814,6 +830,54 @@ def resample_stack(spec: GridSpec, fields: np.ndarray, npix: int, ctx: Optional[
     out = np.zeros((S, spec.slices(), npix, npix), np.float32)
     g, keep = spec._c()
     _check(load().uscg_resample(ctx.h, C.byref(g), _ptr(f), S, npix, _ptr(out), 0))
+    return out
+
+
+def cartesian_to_field(slices, spec: GridSpec, ctx: Optional[Context] = None) -> Field:
+    """cartesian_to_field (phantom.hpp:59, phantom.cpp:165-180): the inverse
+    of field_to_cartesian for the reference law. slices: (slices, n, n)
+    rasters, row 0 at the bottom. Raises InvalidArgument, as the reference,
+    when the slice count or shape does not match the grid."""
+    ctx = ctx or default_context()
+    im = np.ascontiguousarray(slices, dtype=np.float32)
+    if im.ndim == 2:
+        im = im[None]
+    if im.ndim != 3 or im.shape[0] != spec.slices():
+        raise InvalidArgument("slice count does not match the grid")
+    if im.shape[1] != im.shape[2]:
+        raise InvalidArgument("slice shape does not match the grid")
+    out = np.zeros(spec.cell_count(), np.float32)
+    g, keep = spec._c()
+    _check(load().uscg_cartesian_to_field(ctx.h, C.byref(g), _ptr(im), 1, im.shape[1], _ptr(out), 0))
+    return Field(spec, out)
+
+
+def sharpness(image, ctx: Optional[Context] = None):
+    """uscg::sharpness (metrics.cpp:138-152): mean central-difference gradient
+    magnitude of one (rows, cols) raster; a (slices, rows, cols) stack gives one
+    value per slice."""
+    ctx = ctx or default_context()
+    a = np.ascontiguousarray(image, dtype=np.float32)
+    one = a.ndim == 2
+    if one:
+        a = a[None]
+    if a.ndim != 3:
+        raise InvalidArgument("sharpness needs (rows, cols) or (slices, rows, cols) rasters")
+    out = np.zeros(a.shape[0])
+    _check(load().uscg_image_sharpness(ctx.h, _ptr(a), a.shape[0], a.shape[1], a.shape[2],
+                                       out.ctypes.data_as(_dp), 0))
+    return float(out[0]) if one else out
+
+
+def intensity_profile(image, row: int) -> np.ndarray:
+    """uscg::intensity_profile (metrics.cpp:154-159): row `row` of a (rows, cols)
+    raster as float64; InvalidArgument when the row is out of range."""
+    a = np.ascontiguousarray(image, dtype=np.float32)
+    if a.ndim != 2:
+        raise InvalidArgument("intensity_profile needs one (rows, cols) raster")
+    out = np.zeros(a.shape[1])
+    _check(load().uscg_intensity_profile(a.ctypes.data_as(_fp), a.shape[0], a.shape[1], int(row),
+                                         out.ctypes.data_as(_dp)))
     return out
 
 

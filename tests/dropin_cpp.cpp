@@ -63,7 +63,7 @@ int main(int argc, char** argv) {
 
     std::vector<double> img;
     for (const auto& s : images)
-        img.insert(img.end(), s.begin(), s.end());
+        img.insert(img.end(), s.v.begin(), s.v.end());
     dump(out + ".proj", proj.data);
     dump(out + ".field", r.field.values);
     dump(out + ".img", img);

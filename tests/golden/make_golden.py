@@ -12,6 +12,10 @@ device path must reproduce:
   proj_<geom>.npz    generate_projections (binary) of a seeded random field
   recon_<geom>.npz   reconstruct (fp64 field, residuals, counters, crossed)
   map_<n>.npz        uspg_to_cg_map(n)
+  images.npz         cartesian_to_field of seeded rasters (2D n=16, 3D n=8),
+                     sharpness of seeded / structured images and
+                     intensity_profile rows (proj/src/phantom.cpp:165-180,
+                     proj/src/metrics.cpp:138-159)
   kat.json           worked examples of proj/tests/test_tracer.cpp:60-98 and
                      the solver arithmetic of proj/tests/test_solver.cpp:68-113
 """
@@ -60,6 +64,18 @@ def main():
                                                rep["factor_clamps"]]))
     for n in (2, 4, 16, 64):
         np.savez_compressed(os.path.join(HERE, f"map_{n}.npz"), map=ref.uspg_to_cg_map(n))
+    rng = np.random.default_rng(21)
+    im2 = rng.uniform(0, 2, (1, 16, 16))
+    im3 = rng.uniform(0, 2, (8, 8, 8))
+    sharp_imgs = [rng.uniform(0, 1, (9, 13)), np.add.outer(np.arange(6.0), 0.5 * np.arange(4.0)),
+                  np.indices((8, 8)).sum(axis=0) % 2 * 1.0, np.full((2, 2), 3.0), rng.normal(0, 1, (2, 7))]
+    sharp = np.array([ref.sharpness(x) for x in sharp_imgs])
+    packed = np.concatenate([x.ravel() for x in sharp_imgs])
+    shapes = np.array([x.shape for x in sharp_imgs], np.int32)
+    np.savez_compressed(os.path.join(HERE, "images.npz"), im2=im2, field2=ref.cartesian_to_field(16, False, im2),
+                        im3=im3, field3=ref.cartesian_to_field(8, True, im3), sharp_pixels=packed,
+                        sharp_shapes=shapes, sharpness=sharp,
+                        profile=ref.intensity_profile(sharp_imgs[0], 4))
     kat = {"trace_chord": []}
     for rec, theta in [((95.0, 40.0, 0, 2), 0.0), ((350.0, 10.0, 0, 2), 0.0), ((65.0, 10.0, 0, 2), 30.0),
                        ((10.0, 190.0, 0, 2), 0.0), ((45.0, 45.0, 0, 2), 0.0)]:

@@ -171,6 +171,55 @@ def test_oracle_metrics_vs_reference(ref, orc):
     assert orc.ssim(a, a) == 1.0
 
 
+@pytest.mark.parametrize("n,volume", [(8, True), (64, False), (16, True), (2, False)])
+def test_oracle_cartesian_to_field_vs_reference(ref, orc, n, volume):
+    """cartesian_to_field (phantom.cpp:165-180), and its round trip with field_to_cartesian"""
+    grid = oracle.OrcGrid.reference(n, volume)
+    imgs = np.random.default_rng(6).uniform(0, 2, (grid.n_slices, n, n))
+    got = orc.cartesian_to_field(grid, imgs, n)
+    assert np.array_equal(got, ref.cartesian_to_field(n, volume, imgs))
+    assert np.array_equal(orc.field_to_cartesian(grid, got, n), imgs)
+
+
+def test_oracle_cartesian_to_field_errors(ref, orc):
+    grid = oracle.OrcGrid.reference(8, False)
+    with pytest.raises(ValueError):
+        orc.cartesian_to_field(grid, np.zeros((1, 6, 6)), 6)
+    with pytest.raises(ValueError, match="slice shape"):
+        ref.cartesian_to_field(8, False, np.zeros((1, 6, 6)), img_n=6)
+
+
+def test_oracle_sharpness_and_profile_vs_reference(ref, orc):
+    rng = np.random.default_rng(8)
+    for shape in [(64, 64), (2, 2), (3, 17), (31, 2)]:
+        a = rng.uniform(0, 1, shape)
+        assert orc.sharpness(a) == ref.sharpness(a)
+    flat = np.full((5, 5), 2.5)
+    assert ref.sharpness(flat) == 0.0 == orc.sharpness(flat)
+    board = np.indices((16, 16)).sum(axis=0) % 2 * 1.0
+    blurred = (board + np.roll(board, 1, 0) + np.roll(board, 1, 1) + np.roll(board, (1, 1), (0, 1))) / 4
+    assert orc.sharpness(board) > orc.sharpness(blurred)  # proj/tests/test_metrics.cpp:132-147
+    with pytest.raises(ValueError, match="2x2"):
+        ref.sharpness(np.zeros((1, 5)))
+    assert np.isnan(orc.sharpness(np.zeros((1, 5))))
+    ramp = np.arange(12.0).reshape(3, 4)
+    assert np.array_equal(ref.intensity_profile(ramp, 2), ramp[2])
+    with pytest.raises(ValueError, match="out of range"):
+        ref.intensity_profile(ramp, 3)
+
+
+def test_oracle_images_match_golden(orc):
+    z = np.load(os.path.join(GOLDEN, "images.npz"))
+    g2, g3 = oracle.OrcGrid.reference(16, False), oracle.OrcGrid.reference(8, True)
+    assert np.array_equal(orc.cartesian_to_field(g2, z["im2"], 16), z["field2"])
+    assert np.array_equal(orc.cartesian_to_field(g3, z["im3"], 8), z["field3"])
+    off = 0
+    for (r, c), want in zip(z["sharp_shapes"], z["sharpness"]):
+        img = z["sharp_pixels"][off:off + r * c].reshape(r, c)
+        off += r * c
+        assert orc.sharpness(img) == want
+
+
 def test_glibc_atan2_is_not_always_correctly_rounded(orc):
     """Adjudication evidence for the device generator's azimuths: glibc
     2.39's atan2 differs from the correctly rounded value (mpmath, 200 bits)

@@ -101,6 +101,14 @@ __device__ __forceinline__ unsigned long long gtimer() {
 }
 
 __device__ __forceinline__ void fence_acq_rel_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
+// Release-only and acquire-only fences. fence.acq_rel.gpu is MEMBAR.ALL.GPU +
+// CCTL.IVALL (an L1 invalidation the publisher does not need, which costs the
+// SM's other warps their cached lists); fence.release.gpu is the MEMBAR
+// alone. fence.acquire.gpu is CCTL.IVALL alone: after a relaxed poll has
+// observed a released count it completes the acquire without re-reading the
+// counter (an acquire load would be one more L2 round trip).
+__device__ __forceinline__ void fence_release_gpu() { asm volatile("fence.release.gpu;" ::: "memory"); }
+__device__ __forceinline__ void fence_acquire_gpu() { asm volatile("fence.acquire.gpu;" ::: "memory"); }
 __device__ __forceinline__ void red_relaxed_add(unsigned* p, unsigned v) {
     asm volatile("red.relaxed.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
@@ -189,7 +197,7 @@ __device__ __forceinline__ void spin_until_geq(const unsigned* p, unsigned targe
         __nanosleep(ns);
         ns = ns < 128 ? ns * 2 : 128;
     }
-    (void)ld_acquire(p);
+    fence_acquire_gpu();
 }
 
 // Shared-memory words of one group: [trace arrays when tracing] + `lists`
@@ -1129,7 +1137,7 @@ __device__ void flow_updater(const FlowArgs& a, GroupWorker<P, G>& W) {
         {
             if (warp == kPub) {
                 if constexpr (G == 32) {
-                    fence_acq_rel_gpu();
+                    fence_release_gpu();
                     if (sb + lane < se)
                         red_relaxed_add(a.count + size_t(succ0) * nchunks + chunk, 1u);
                     if (sb + 32 + lane < se)
@@ -1140,7 +1148,7 @@ __device__ void flow_updater(const FlowArgs& a, GroupWorker<P, G>& W) {
                 } else {
                     sb = __ldg(a.succ_off + run);
                     se = __ldg(a.succ_off + run + 1);
-                    fence_acq_rel_gpu();
+                    fence_release_gpu();
                     for (uint32_t k = sb + lane; k < se; k += 32)
                         red_relaxed_add(a.count + size_t(__ldg(a.succs + k)) * nchunks + chunk, 1u);
                 }
@@ -1491,7 +1499,7 @@ __global__ void __launch_bounds__(WaveShape<P>::G + 96, WaveShape<P>::MB) mart_w
                 const unsigned d = ld_acquire_cta_shared(&s_done);
                 if (d > published) {
                     if (lane == 0) {
-                        fence_acq_rel_gpu();
+                        fence_release_gpu();
                         st_relaxed_gpu(mine, gs * L + d);
                     }
                     if (lp) {
@@ -1594,8 +1602,7 @@ __global__ void __launch_bounds__(WaveShape<P>::G + 96, WaveShape<P>::MB) mart_w
                     // least as recent; a gpu-scope fence here would wait for
                     // the updaters' outstanding stores), then release to the
                     // updaters
-                    if (unsigned(lane) < adv && n > 0)
-                        (void)ld_acquire(a.prog + rc[0]);
+                    fence_acquire_gpu();
                     __syncwarp();
                     if (lp) {
                         const unsigned long long tn = gtimer();
@@ -2045,7 +2052,7 @@ __global__ void __launch_bounds__(pair::Shape<P, SLOTS>::NT, 1) mart_wave_pair_k
                 const unsigned d = ld_acquire_cta_shared(&s_done[k]);
                 if (d > published) {
                     if (lane == 0) {
-                        fence_acq_rel_gpu();
+                        fence_release_gpu();
                         st_relaxed_gpu(mine, gs * L + d);
                     }
                     published = d;
@@ -2123,10 +2130,7 @@ __global__ void __launch_bounds__(pair::Shape<P, SLOTS>::NT, 1) mart_wave_pair_k
                 if (nr > ready) {
                     // acquire what the advancing lanes observed (re-reads of
                     // satisfied counters), then release to the updaters
-                    if (unsigned(lane) < adv && n > 0)
-#pragma unroll
-                        for (int c = 0; c < CL; ++c)
-                            (void)ld_acquire(a.prog + rc[0] + c * kWavePad);
+                    fence_acquire_gpu();
                     __syncwarp();
                     ready = nr;
                     if (lane == 0)

@@ -35,10 +35,10 @@ rep = (uscg._Report * S)()
 uscg._check(L.uscg_reconstruct(tracer.h, uscg.C.c_void_p(proj_d.data_ptr()), S, uscg.C.byref(cfg),
                                uscg.C.c_void_p(field_d.data_ptr()), 1, rep, flags))
 torch.cuda.synchronize()
-st = np.fromfile(path, np.uint64).reshape(-1, 16).astype(np.int64)
+st_all = np.fromfile(path, np.uint64).reshape(-1, 16).astype(np.int64)
 os.remove(path)
-ok = (st[:, 0] > 0) & (st[:, 6] > 0)
-st = st[ok]
+ok = (st_all[:, 0] > 0) & (st_all[:, 6] > 0)
+st = st_all[ok]
 t0 = st[:, 0].min()
 span = (st[:, 6].max() - t0) / 1e3
 ph = {"metadata": (0, 9), "trace": (9, 8), "wait": (8, 1), "gather+sum": (2, 3), "factor": (3, 4), "scatter": (4, 5),
@@ -49,3 +49,29 @@ for k, (a, b) in ph.items():
     print(f"  {k:11s} mean {d.mean():8.2f} us  p50 {np.median(d):8.2f}  p90 {np.percentile(d, 90):8.2f}")
 cells = tracer.trace_counts().reshape(-1)
 print(f"  cells/line mean {cells.mean():.0f} max {cells.max()}")
+
+# ---- hand-offs: for each task that waited, the time from its binding
+# predecessor's publish (stamp 6) to the end of its own spin (stamp 1) ----
+sch = tracer.schedule()
+order, pred_off, preds = sch["order"], sch["pred_off"].astype(np.int64), sch["preds"]
+pos_of = np.empty(len(order), np.int64)
+pos_of[order] = np.arange(len(order))
+hops, waited = [], 0
+n_tasks = len(order)
+for pos in range(n_tasks):
+    r = int(order[pos])
+    a, b = pred_off[r], pred_off[r + 1]
+    if a == b or st_all[pos, 1] == 0:
+        continue
+    pp = pos_of[preds[a:b]]
+    pub = st_all[pp, 6]
+    if (pub == 0).any():
+        continue
+    bind = pub.max()
+    if st_all[pos, 1] - st_all[pos, 8] > 300:  # spun > 0.3 us: it waited on its predecessors
+        waited += 1
+        hops.append(st_all[pos, 1] - bind)
+hops = np.array(hops) / 1e3
+print(f"  tasks that waited: {waited} of {n_tasks}; hand-off (binding publish -> spin end) mean {hops.mean():.2f} us, "
+      f"p50 {np.median(hops):.2f}, p90 {np.percentile(hops, 90):.2f}")
+print(f"  levels per sweep {sch['levels']}: sweep / levels = {span / sch['levels']:.2f} us per level")

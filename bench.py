@@ -324,6 +324,10 @@ class Gpu:
 def mart_kernel_name(info, P):
     ex = info["executor"]
     if ex == 3:
+        cl = int(info.get("wave_ctas", 1) or 1)
+        if cl > 1:
+            return (f"mart_wave_pair_kernel<{P}, 1, {cl}> (one persistent launch per reconstruct call; task = "
+                    f"(view, {P}-problem chunk) on a {cl}-CTA cluster)")
         return f"mart_wave_kernel<{P}> (one persistent launch per reconstruct call; task = (view, {P}-problem chunk))"
     if ex == 4:
         return "mart_tile_kernel (one CTA, the field in shared memory)"

@@ -136,6 +136,8 @@ typedef struct {
     double wave_build_s;           /* wave executor: seconds to build its lists and requirements */
     uint64_t executor_bytes;       /* device bytes the MART executors derived from the record store
                                       (traced lists, wave entries/requirements, run schedule) */
+    int32_t wave_ctas;             /* wave executor: CTAs per view task of the last solve (1 single,
+                                      2 pairs, 4 clusters of four; 0 before any wave solve) */
 } uscg_tracer_info;
 
 const char* uscg_last_error(void);

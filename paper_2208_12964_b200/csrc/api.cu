@@ -156,6 +156,7 @@ struct uscg_tracer_s {
     DevBuf<unsigned> d_wprog, d_wnext;
     int wave_chunks = 0;
     unsigned wave_epoch = 0;
+    int wave_ctas = 0;  // CTAs per view task of the last wave solve
     uint64_t wave_deps = 0;
     double wave_seconds = 0;
     double generator_ms = 0;  // device time of the first-view generator
@@ -1285,6 +1286,7 @@ uscg_status uscg_tracer_get_info(uscg_tracer t, uscg_tracer_info* info) {
         info->executor = t->executor;
         info->wave_requirements = t->wave_deps;
         info->wave_build_s = t->wave_seconds;
+        info->wave_ctas = t->wave_ctas;
         info->executor_bytes = t->d_lists.bytes() + t->d_lpos.bytes() + t->d_went.bytes() + t->d_wsplit.bytes() +
                                t->d_wpos.bytes() + t->d_wdep_off.bytes() + t->d_wdeps.bytes() +
                                t->d_order.bytes() + t->d_pred_off.bytes() + t->d_preds.bytes() +
@@ -1700,6 +1702,7 @@ static void reconstruct_body(uscg_tracer t, const float* proj, int32_t problems,
             if (ws.parts > 1)
                 ensure_split(t, ws.parts);
             ws.spos = ws.parts > 1 && t->wave_split_longest <= 384 ? t->d_wspos.p : nullptr;
+            t->wave_ctas = ws.spos && !std::getenv("USCG_SWEEP_PROFILE") ? ws.parts : 1;  // as launch_mart_wave picks
             ws.split = t->d_wsplit.p;
             ws.views = t->views;
             ws.lines = t->lines;

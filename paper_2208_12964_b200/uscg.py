@@ -111,7 +111,7 @@ class _Info(C.Structure):
                 ("cache_bytes", C.c_uint64), ("max_line_records", C.c_int32), ("max_line_cells", C.c_int32),
                 ("cells_per_sweep", C.c_uint64), ("chords_per_sweep", C.c_uint64), ("levels", C.c_int32),
                 ("generator_ms", C.c_double), ("executor", C.c_int32), ("wave_requirements", C.c_uint64),
-                ("wave_build_s", C.c_double), ("executor_bytes", C.c_uint64)]
+                ("wave_build_s", C.c_double), ("executor_bytes", C.c_uint64), ("wave_ctas", C.c_int32)]
 
 
 EXPORTS = [

@@ -1846,9 +1846,13 @@ static void wave_launch_t(const WaveArgs& a, int sms, cudaStream_t st) {
 // both CTAs' control warps check requirements. Every cell still sees the
 // line-by-line updates in order.
 namespace pair {
-constexpr int V = 4, G = 384, COVERL = 384;  // updater threads per CTA; cell slots per CTA and task slot
+constexpr int V = 4, COVERL = 384;  // cell slots per CTA and task slot
+// updater threads per CTA: 384 for 32-problem chunks (8 cells a thread), 256
+// for 16 (6 cells a thread); measured on C2: P = 32, 128 problems 4.32 ms
+// (256 threads: 4.53, 512: 4.39); P = 16, 16 problems 2.28 ms (384: 2.41)
+template <int P> constexpr int updaters() { return P == 16 ? 256 : 384; }
 template <int P, int SLOTS> struct Shape {
-    static constexpr int GS = G / SLOTS;  // updaters per task slot
+    static constexpr int GS = updaters<P>() / SLOTS;  // updaters per task slot
     static constexpr int NWS = GS / 32, TPC = P / V, NCLV = GS / TPC, KV = COVERL / NCLV;
     static constexpr int NTS = GS + 96;   // + factor warp + poller warp + publisher warp
     static constexpr int NT = SLOTS * NTS;

@@ -336,8 +336,10 @@ def mart_kernel_name(info, P):
 
 
 def chunk_width(Sp):
+    """The library's MART chunk width for a stack of stride Sp (kernels.cu
+    chunk_width: a limit of 16 up to 64 problems, else 32)."""
     p = 1
-    lim = int(os.environ.get("USCG_CHUNK_WIDTH", 32))
+    lim = int(os.environ.get("USCG_CHUNK_WIDTH", 32 if Sp > 64 else 16))
     while p * 2 <= lim and Sp % (p * 2) == 0:
         p *= 2
     return p

@@ -46,12 +46,17 @@ int chunk_limit() {
 
 // Problems per MART task: the widest chunk (<= the limit) that pads the
 // problem stride by at most 1/8, else the smallest power of two covering the
-// problems up to 8. Wide chunks move more bytes per scattered access.
+// problems up to 8. Wide chunks move more bytes per scattered access; up to
+// 64 problems the clustered wave's chains run faster on 16-problem chunks
+// than on fewer 32-problem ones while the pairs of all chunks still find SMs
+// (C2 geometry, ms per iteration: 32 problems 2.25 vs 3.10, 64: 2.84 vs 3.07;
+// 96: 4.58 vs 3.26), so 16 is the default limit there.
 int chunk_width(int problems) {
+    const int limit = std::getenv("USCG_CHUNK_WIDTH") || problems > 64 ? chunk_limit() : std::min(16, chunk_limit());
     int p = 1;
-    while (p < problems && p < std::min(8, chunk_limit()))
+    while (p < problems && p < std::min(8, limit))
         p <<= 1;
-    for (int q = chunk_limit(); q > p; q >>= 1) {
+    for (int q = limit; q > p; q >>= 1) {
         const long long padded = (static_cast<long long>(problems) + q - 1) / q * q;
         if (padded * 8 <= static_cast<long long>(problems) * 9)
             return q;

@@ -150,13 +150,14 @@ def test_c2_verbatim_wave_twenty_sweeps(ub, orc, capfd, monkeypatch):
     _quality(ub, orc, g, spec, out[127][0].astype(np.float64), ref[3][0], truth[127], 512)
 
 
-@pytest.mark.parametrize("S,width,cl", [(64, 32, 2), (16, 16, 2), (32, 32, 4)])
+@pytest.mark.parametrize("S,width,cl", [(64, 16, 2), (16, 16, 2), (32, 16, 4), (96, 32, 4)])
 def test_c2_shard_per_gpu_paired_wave(ub, orc, capfd, monkeypatch, S, width, cl):
-    """The C2 stack as one GPU of 2 / 4 / 8 holds it (64 / 32 / 16 slices):
-    all 20 sweeps through the clustered wave form (a view task on a 2-CTA
-    cluster, or the opt-in 4-CTA one; cells split by index mod cluster size,
-    partial sums exchanged through distributed shared memory), problems of the
-    first and last slots against the oracle."""
+    """The C2 stack as one GPU of 2 / 4 / 8 holds it (64 / 32 / 16 slices, in
+    16-problem chunks) and a 96-slice stack (32-problem chunks): all 20 sweeps
+    through the clustered wave form (a view task on a 2-CTA cluster, or the
+    opt-in 4-CTA one; cells split by index mod cluster size, partial sums
+    exchanged through distributed shared memory), problems of the first and
+    last slots against the oracle."""
     from paper_2208_12964_b200 import workloads
     monkeypatch.setenv("USCG_FLOW_VERBOSE", "1")
     if cl != 2:

@@ -625,7 +625,7 @@ def test_device_wave_build_equals_host_build(ub, orc, monkeypatch, capfd, case):
         tr = ub.Tracer(geom, spec, False)
         proj = ub.project_stack(tr, np.ones((32, spec.cell_count()), np.float32))
         ub.reconstruct_stack(proj, ub.SolverConfig(beta=0.5, tolerance=0, max_sweeps=1), tr)
-        assert "mart_wave_kernel: P=32 " in capfd.readouterr().err
+        assert "mart_wave_kernel: P=16 " in capfd.readouterr().err  # 32 problems: two 16-problem chunks
         arrays[host] = tr.wave_arrays()
         tr.close()
     for k in ("entries", "dep_off", "deps"):

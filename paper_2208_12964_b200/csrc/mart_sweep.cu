@@ -2186,13 +2186,18 @@ __global__ void __launch_bounds__(pair::Shape<P, SLOTS>::NT, 1) mart_wave_pair_k
                     cp_async8_if(q == 0 && s < n, dst + s, a.split + p0 + s);
                 }
             };
+            // a line's entries stay in registers from its copies (issued
+            // during the previous line) to its scaling: one shared-memory
+            // read of each per line
+            uint2 enext[KV];
             auto gather = [&](unsigned j) {
                 const int n = int(s_pos[j + 1] - s_pos[j]);
                 const uint2* e = s_ent + (j % 3) * COVERL;
 #pragma unroll
                 for (int i = 0; i < KV; ++i) {
                     const int s = cl + i * NCLV;
-                    const uint32_t c = s < n ? e[s].x : kWavePrev;
+                    enext[i] = s < n ? e[s] : make_uint2(kWavePrev, kWaveNoNext);
+                    const uint32_t c = enext[i].x;
                     cp_async16_if(!(c & kWavePrev), buf + s * TPC + q, f4 + size_t(c) * Sp4 + col4);
                 }
             };
@@ -2207,6 +2212,10 @@ __global__ void __launch_bounds__(pair::Shape<P, SLOTS>::NT, 1) mart_wave_pair_k
             cp_async_commit();
             for (unsigned j = 0; j < L; ++j) {
                 const int n = int(s_pos[j + 1] - s_pos[j]);
+                uint2 ecur[KV];
+#pragma unroll
+                for (int i = 0; i < KV; ++i)
+                    ecur[i] = enext[i];
                 cp_async_wait_all();
                 float4 x[KV];
 #pragma unroll
@@ -2246,12 +2255,11 @@ __global__ void __launch_bounds__(pair::Shape<P, SLOTS>::NT, 1) mart_wave_pair_k
                 const float4 w = reinterpret_cast<const float4*>(fac)[2 * q + 1];
                 const Scale g0{u.x, u.y}, g1{u.z, u.w}, g2{w.x, w.y}, g3{w.z, w.w};
                 const bool any = (u.y + u.w + w.y + w.w) != 0.f;
-                const uint2* e = s_ent + (j % 3) * COVERL;
 #pragma unroll
                 for (int i = 0; i < KV; ++i) {
                     const int s = cl + i * NCLV;
                     const bool in = s < n;
-                    const uint2 en = e[in ? s : 0];
+                    const uint2 en = ecur[i];
                     const float4 r = GW::scale4(x[i], g0, g1, g2, g3);
                     const bool hand = in && en.y != kWaveNoNext;
                     st_shared_v4_if(hand, buf + int(en.y) * TPC + q, r);

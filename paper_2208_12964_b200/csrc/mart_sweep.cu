@@ -2223,16 +2223,28 @@ __global__ void __launch_bounds__(pair::Shape<P, SLOTS>::NT, 1) mart_wave_pair_k
                     const int s = cl + i * NCLV;
                     x[i] = s < n ? buf[s * TPC + q] : make_float4(0.f, 0.f, 0.f, 0.f);
                 }
-                double s0, s1, s2, s3;
-                GW::template partials<KV>(x, s0, s1, s2, s3);
-                asm volatile("" ::"d"(s0), "d"(s1), "d"(s2), "d"(s3));
+                // fp32 partials of the thread's cells and of the warp's 32 / TPC
+                // threads of a problem group (at most 32 / TPC * KV cells, as
+                // many as the single-CTA form's per-thread partials), fp64 from
+                // the cross-warp sum on (the reference sums in fp64,
+                // solver.cpp:36-40)
+                float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
+#pragma unroll
+                for (int i = 0; i < KV; ++i) {
+                    a0 += x[i].x;
+                    a1 += x[i].y;
+                    a2 += x[i].z;
+                    a3 += x[i].w;
+                }
+                asm volatile("" ::"f"(a0), "f"(a1), "f"(a2), "f"(a3));
 #pragma unroll
                 for (int o = TPC; o < 32; o <<= 1) {
-                    s0 += __shfl_xor_sync(0xFFFFFFFFu, s0, o);
-                    s1 += __shfl_xor_sync(0xFFFFFFFFu, s1, o);
-                    s2 += __shfl_xor_sync(0xFFFFFFFFu, s2, o);
-                    s3 += __shfl_xor_sync(0xFFFFFFFFu, s3, o);
+                    a0 += __shfl_xor_sync(0xFFFFFFFFu, a0, o);
+                    a1 += __shfl_xor_sync(0xFFFFFFFFu, a1, o);
+                    a2 += __shfl_xor_sync(0xFFFFFFFFu, a2, o);
+                    a3 += __shfl_xor_sync(0xFFFFFFFFu, a3, o);
                 }
+                const double s0 = a0, s1 = a1, s2 = a2, s3 = a3;
                 const int lane = t & 31, warp = t >> 5;
                 if (lane < TPC) {
                     double* r = red + warp * P + q * V;

@@ -1914,8 +1914,12 @@ __device__ __forceinline__ void named_sync(int id, int n) {
 // CL CTAs per cluster (a view task's cells split by index mod CL), SLOTS
 // task slots per CTA (each with its own updaters, factor warp and control
 // warp; only SLOTS = 1 is dispatched, see wave_cluster_size).
+// At most 112 registers a thread (480 x 112 of the SM's 64 K): uscg_reconstruct_batch
+// runs the next stack's small kernels while this one holds every SM, and
+// they need the registers left (C2 end to end 5.5 -> 4.5 ms per step; the
+// kernel alone 4.10 -> 4.23 ms per iteration at its unconstrained 124).
 template <int P, int SLOTS, int CL>
-__global__ void __launch_bounds__(pair::Shape<P, SLOTS>::NT, 1) mart_wave_pair_kernel(WaveArgs a) {
+__global__ void __maxnreg__(112) mart_wave_pair_kernel(WaveArgs a) {
     using namespace pair;
     using SH = Shape<P, SLOTS>;
     constexpr int GS = SH::GS, NWS = SH::NWS, TPC = SH::TPC, NCLV = SH::NCLV, KV = SH::KV, NTS = SH::NTS;

@@ -2197,10 +2197,17 @@ __global__ void __maxnreg__(112) mart_wave_pair_kernel(WaveArgs a) {
             auto gather = [&](unsigned j) {
                 const int n = int(s_pos[j + 1] - s_pos[j]);
                 const uint2* e = s_ent + (j % 3) * COVERL;
+                // every entry first (the copies' asm is a compiler memory
+                // barrier: reading an entry between two copies would wait for
+                // each read in turn)
 #pragma unroll
                 for (int i = 0; i < KV; ++i) {
                     const int s = cl + i * NCLV;
                     enext[i] = s < n ? e[s] : make_uint2(kWavePrev, kWaveNoNext);
+                }
+#pragma unroll
+                for (int i = 0; i < KV; ++i) {
+                    const int s = cl + i * NCLV;
                     const uint32_t c = enext[i].x;
                     cp_async16_if(!(c & kWavePrev), buf + s * TPC + q, f4 + size_t(c) * Sp4 + col4);
                 }

@@ -2177,6 +2177,13 @@ __global__ void __maxnreg__(112) mart_wave_pair_kernel(WaveArgs a) {
             const int v = (task % per_sweep) / nchunks, chunk = task % nchunks;
             const uint32_t u0 = uint32_t(v) * L;
             const uint32_t col4 = (uint32_t(chunk) * P) / V + uint32_t(q);
+            // a cell's float4 of this thread: fbase + cell * row_bytes (one wide
+            // multiply-add per address)
+            const char* const fbase = reinterpret_cast<const char*>(f4 + col4);
+            const uint32_t row_bytes = Sp4 * uint32_t(sizeof(float4));
+            auto cell_f4 = [&](uint32_t c) {
+                return reinterpret_cast<float4*>(const_cast<char*>(fbase) + size_t(c) * row_bytes);
+            };
             for (unsigned j = unsigned(t); j <= L; j += GS)
                 s_pos[j] = __ldg(spos + u0 + j);
             upd_sync();
@@ -2208,8 +2215,8 @@ __global__ void __maxnreg__(112) mart_wave_pair_kernel(WaveArgs a) {
 #pragma unroll
                 for (int i = 0; i < KV; ++i) {
                     const int s = cl + i * NCLV;
-                    const uint32_t c = enext[i].x;
-                    cp_async16_if(!(c & kWavePrev), buf + s * TPC + q, f4 + size_t(c) * Sp4 + col4);
+                    const uint32_t c = enext[i].x;  // bit 31: handed over, no copy
+                    cp_async16_if(int(c) >= 0, buf + s * TPC + q, cell_f4(c));
                 }
             };
             load_entries(0);
@@ -2286,8 +2293,7 @@ __global__ void __maxnreg__(112) mart_wave_pair_kernel(WaveArgs a) {
                     const float4 r = GW::scale4(x[i], g0, g1, g2, g3);
                     const bool hand = in && en.y != kWaveNoNext;
                     st_shared_v4_if(hand, buf + int(en.y) * TPC + q, r);
-                    st_global_cg_v4_if((any || (en.x & kWavePrev)) && in && !hand,
-                                       f4 + size_t(en.x & ~kWavePrev) * Sp4 + col4, r);
+                    st_global_cg_v4_if((any || int(en.x) < 0) && in && !hand, cell_f4(en.x & ~kWavePrev), r);
                 }
                 line_sync();  // C
                 if (!issued && j + 1 < L) {

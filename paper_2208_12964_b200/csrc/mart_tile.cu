@@ -116,14 +116,16 @@ __global__ void __launch_bounds__(kTileNT, 1) mart_tile_kernel(TileKernelArgs a)
             v[i] = uint32_t(lane + 32 * i) < n ? s_f[r.idx[i]] : 0.f;
             ps += v[i];
         }
-        // fp32 partials of at most kTileK cells per lane, fp64 across lanes
-        // (the reference sums in fp64, solver.cpp:25-31)
-        double s = ps;
+        // fp32 partials per lane and across the warp's lanes (a line's at
+        // most a few hundred cells: relative error ~1e-7, below the field's
+        // own fp32 rounding per update), fp64 from the factor on (the
+        // reference sums in fp64, solver.cpp:25-31)
         for (uint32_t k = uint32_t(lane + 32 * kTileK); k < n; k += 32)
-            s += double(s_f[__ldg(ts.lists + r.off + k)]);
+            ps += s_f[__ldg(ts.lists + r.off + k)];
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1)
-            s += __shfl_xor_sync(0xFFFFFFFFu, s, o);
+            ps += __shfl_xor_sync(0xFFFFFFFFu, ps, o);
+        const double s = ps;
         const double ratio = double(r.m) / (s > pf ? s : pf);
         double f = mart_factor(ratio, beta, a.m.power);
         if (f <= 0) {

@@ -64,6 +64,17 @@ int main(int argc, char** argv) {
     std::vector<double> img;
     for (const auto& s : images)
         img.insert(img.end(), s.v.begin(), s.v.end());
+
+    // the metrics.hpp / phantom.hpp names on the rasters: cartesian_to_field
+    // (the inverse permutation), sharpness, intensity_profile, rmse, ssim
+    const U::Field back = U::cartesian_to_field(images, spec);
+    const std::vector<double> prof = U::intensity_profile(images[32], 10);
+    std::vector<double> extra = {U::sharpness(images[32]), U::rmse(images[31], images[32]),
+                                 U::ssim(images[31], images[32]), U::mae(images[31], images[32]),
+                                 U::area_average(images[32])};
+    extra.insert(extra.end(), prof.begin(), prof.end());
+    dump(out + ".back", back.values);
+    dump(out + ".extra", extra);
     dump(out + ".proj", proj.data);
     dump(out + ".field", r.field.values);
     dump(out + ".img", img);

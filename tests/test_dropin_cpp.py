@@ -38,6 +38,17 @@ def test_cpp_dropin_matches_reference(ub, ref, tmp_path):
     assert (np.abs(field - want) / want).max() <= 1e-4
     want_img = ref.field_to_cartesian(n, True, field.astype(np.float32).astype(np.float64))
     assert np.array_equal(img, want_img)  # the permutation moves fp32 values unchanged
+    # cartesian_to_field, sharpness, intensity_profile, rmse, ssim, mae, area_average
+    back = np.fromfile(out + ".back")
+    assert np.array_equal(back, ref.cartesian_to_field(n, True, img))
+    extra = np.fromfile(out + ".extra")
+    a, b = img[31], img[32]
+    assert abs(extra[0] - ref.sharpness(b)) <= 1e-12 * ref.sharpness(b)
+    assert abs(extra[1] - ref.rmse(a, b)) <= 1e-12 * ref.rmse(a, b)
+    assert abs(extra[2] - ref.ssim(a, b)) <= 1e-9
+    assert abs(extra[3] - np.abs(a - b).mean()) <= 1e-12 * np.abs(a - b).mean()
+    assert abs(extra[4] - b.mean()) <= 1e-12 * abs(b.mean())
+    assert np.array_equal(extra[5:], ref.intensity_profile(b, 10))
     # U = every non-skipped line's |active| per sweep (TraceScratch::cells,
     # tracer.cpp:200), sampled against the reference's own trace_line
     spec = ub.GridSpec.cube_3d(n)

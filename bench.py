@@ -491,6 +491,9 @@ def bench_mart(gpu: Gpu, config, args, rank, world, steps=None, warmup=None, cpu
                                  f"views sharded over {world} GPU(s) (dist.view_subset_tracer)" if world > 1
                                  else "one GPU"),
                  "bytes_model": p_model}
+    if projector["frac"] > 1:
+        projector["note"] = ("above 1: the algorithmic bytes are compared with the HBM copy bandwidth, and part of "
+                             "the field gathers are served by L2 (ncu DRAM throughput ~60% of peak for this kernel)")
     del out_d
 
     # ---- e2e through the C ABI with pinned host buffers ----

@@ -586,6 +586,18 @@ def bench_mart(gpu: Gpu, config, args, rank, world, steps=None, warmup=None, cpu
                 "flow_run_levels_per_iteration": levels,
                 "launches": "one persistent launch per reconstruct call (all K iterations); achieved = "
                             "B * K / device time of that launch"}
+    # what binds each executor, measured
+    notes = {
+        "c2": ("the per-line chain and the SMs' scattered 128-byte row traffic, mostly served by L2 "
+               "(profiles/r2_row_microbench.md): the fraction compares the algorithmic bytes with HBM"),
+        "c3": ("latency: the dependency chain's run levels at ~6 us each (gathers, the publish fence, the "
+               "hand-off between warps); its 26 MB field stays in L2"),
+        "c4": ("scattered 4-byte read-modify-writes on a 211 MB field: ~90 G updates/s, the rate a microbenchmark "
+               "of that access pattern reaches (profiles/r2_sector_microbench.md)"),
+        "c1": "latency: one CTA, one block barrier per dependency level",
+    }
+    if config in notes:
+        roofline["bound_detail"] = notes[config]
 
     cpu_line = None
     if cpu and world == 1 and not args.no_cpu:

@@ -19,7 +19,8 @@ from paper_2208_12964_b200 import uscg, workloads  # noqa: E402
 
 cfgname = sys.argv[1] if len(sys.argv) > 1 else "c2"
 sweeps = int(sys.argv[2]) if len(sys.argv) > 2 else 2
-wl = workloads.make(cfgname)
+problems = int(sys.argv[3]) if len(sys.argv) > 3 else None
+wl = workloads.make(cfgname, problems=problems)
 S = wl.problems
 tracer = ub.Tracer(wl.geom, wl.spec, False)
 truth = workloads.phantom_fields(wl, S).astype(np.float32)
@@ -52,11 +53,12 @@ t0 = st[:, 0].min()
 span = (st[:, 1].max() - t0) * 1e-3
 dur = (st[:, 1] - st[:, 0]) * 1e-3
 lines = info["lines"]
-print(f"{cfgname}: {len(st)} tasks, {sweeps} sweeps, span {span:.1f} us ({span / sweeps / 1e3:.3f} ms/sweep), "
-      f"executor {tracer.info()['executor']}, requirements {info['wave_requirements']}")
+print(f"{cfgname} S={S}: {len(st)} tasks, {sweeps} sweeps, span {span:.1f} us ({span / sweeps / 1e3:.3f} ms/sweep), "
+      f"executor {tracer.info()['executor']} ({tracer.info()['wave_ctas']} CTAs a task), "
+      f"requirements {info['wave_requirements']}")
 print(f"task duration mean {dur.mean():.1f} us (min {dur.min():.1f}, max {dur.max():.1f}); "
       f"tasks in flight (mean) {dur.sum() / span:.1f}; CTAs {len(np.unique(st[:, 6]))}")
-for k, name in ((2, "ready-wait"), (3, "gather"), (7, " copy-wait"), (4, "reduce"), (5, "store")):
+for k, name in ((2, "ready-wait"), (3, "start->A"), (7, " copy-wait"), (4, "A->B"), (5, "B->C")):
     per_line = st[:, k] / lines * 1e-3
     print(f"  {name:10s} per line: mean {per_line.mean():.3f} us  p10 {np.percentile(per_line, 10):.3f}  "
           f"p90 {np.percentile(per_line, 90):.3f}")
@@ -67,7 +69,9 @@ s1 = (st[:, 1] - t0) * 1e-3
 inflight = [((s0 < b) & (s1 > a)).sum() for a, b in zip(edges[:-1], edges[1:])]
 print("  tasks overlapping each tenth of the span:", inflight)
 # per (sweep, chunk): start-time lag between consecutive views, in lines
-nch = Sp // min(32, Sp)
+P = int(os.environ.get("USCG_CHUNK_WIDTH", 32 if Sp > 64 else 16))
+P = min(P, Sp)
+nch = Sp // P
 per_sweep = info["views"] * nch
 tick = np.nonzero(ok)[0]
 start = dict(zip(tick.tolist(), st[:, 0].tolist()))

@@ -53,12 +53,16 @@ __device__ __forceinline__ D mul_d(D x, double b) {
     p.lo += x.lo * b;
     return quick_two_sum(p.hi, p.lo);
 }
+// a / b with one fp64 division: three quotient terms from the reciprocal of
+// b.hi, each correcting the remainder of the previous (fp64 division is a
+// multi-instruction sequence, the generator's atan2 needed six of them)
 __device__ __forceinline__ D div(D a, D b) {
-    const double q1 = a.hi / b.hi;
+    const double inv = 1.0 / b.hi;
+    const double q1 = a.hi * inv;
     D r = sub(a, mul_d(b, q1));
-    const double q2 = r.hi / b.hi;
+    const double q2 = r.hi * inv;
     r = sub(r, mul_d(b, q2));
-    const double q3 = r.hi / b.hi;
+    const double q3 = r.hi * inv;
     const D q = quick_two_sum(q1, q2);
     return add(q, D{q3, 0.0});
 }

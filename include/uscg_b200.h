@@ -350,8 +350,10 @@ uscg_status uscg_schedule_build(uint32_t units, uint32_t lines_per_view, uint32_
 
 /* ---- diagnostics ---------------------------------------------------------
  * The device math the generator uses, for parity tests against glibc:
- * out[4*i + k], k = 0: atan2 (correctly rounded), 1: hypot (correctly
- * rounded), 2: azimuth_deg (geometry.cpp:39-46), 3: libdevice atan2. */
+ * out[5*i + k], k = 0: the generator's atan2 (quick form with the
+ * double-double fallback: correctly rounded), 1: hypot (correctly rounded),
+ * 2: azimuth_deg (geometry.cpp:39-46), 3: libdevice atan2, 4: the
+ * double-double atan2 alone (correctly rounded). */
 uscg_status uscg_diag_math(uscg_ctx ctx, int32_t n, const double* x, const double* y, double* out);
 
 #ifdef __cplusplus

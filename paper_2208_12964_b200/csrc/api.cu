@@ -2585,9 +2585,9 @@ uscg_status uscg_diag_math(uscg_ctx ctx, int32_t n, const double* x, const doubl
         UB_CUDA(cudaMemcpyAsync(d.p, x, sizeof(double) * n, cudaMemcpyHostToDevice, ctx->stream));
         UB_CUDA(cudaMemcpyAsync(d.p + n, y, sizeof(double) * n, cudaMemcpyHostToDevice, ctx->stream));
         DevBuf<double> o;
-        o.alloc(size_t(n) * 4);
+        o.alloc(size_t(n) * 5);
         launch_diag_math(n, d.p, d.p + n, o.p, ctx->stream);
-        UB_CUDA(cudaMemcpyAsync(out, o.p, sizeof(double) * 4 * n, cudaMemcpyDeviceToHost, ctx->stream));
+        UB_CUDA(cudaMemcpyAsync(out, o.p, sizeof(double) * 5 * n, cudaMemcpyDeviceToHost, ctx->stream));
         UB_CUDA(cudaStreamSynchronize(ctx->stream));
     });
 }

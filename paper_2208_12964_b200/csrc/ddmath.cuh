@@ -146,7 +146,7 @@ constexpr double kInv7Hi = 0x1.2492492492492p-3, kInv7Lo = 0x1.2492492492492p-57
 // table, atan(t) = atan(c) + atan(u), u = (t - c) / (1 + t c), |u| <= 1/128,
 // atan(u) = u * P(u^2) with the series to u^19.
 __device__ __forceinline__ D atan01(D t) {
-    const int k = int(t.hi * 64.0 + 0.5);
+    const int k = min(max(int(t.hi * 64.0 + 0.5), 0), 64);
     const double c = k * (1.0 / 64.0);
     const D num = sub(t, D{c, 0.0});
     const D den = add(D{1.0, 0.0}, mul_d(t, c));
@@ -163,10 +163,83 @@ __device__ __forceinline__ D atan01(D t) {
     return add(D{kAtanTab[k][0], kAtanTab[k][1]}, mul(u, r));
 }
 
+// atan(t) for t = th + tl in [0, 1] to a relative error below 2^-65 (the
+// quick form of atan01: double-double only where the error needs it).
+//   t - c = (th - c) + tl        th - c exact (Sterbenz; c = 0 trivially)
+//   1 + t c = 1 + p + pe + tl c  p + pe = th c exactly (fma)
+//   u = (t - c) / (1 + t c)      u1 + u2: one reciprocal and one residual,
+//                                error ~2^-100 |u|
+//   atan(u) = u + u s            s = -z/3 + z^2/5 - ... - z^5/11, z = u1^2 in
+//                                double: |s| <= 2^-15.5, relative error of s
+//                                <= 5 * 2^-53 (z's rounding and u1 for u,
+//                                Horner), truncation z^6/13 <= 2^-87: the
+//                                term u s is good to 2^-66.2 |u|
+//   atan(c) + atan(u)            table (hi, lo) + u1 exactly (two_sum), the
+//                                small terms summed in double: rounding
+//                                <= 2^-66.4 |u| + 2^-104 |R|
+// and |u| <= |R| (k = 0: R = atan(u); k >= 1: |u| <= 1/128 < R), so the
+// result (normalized) is within 2^-65.2 |R| of atan(t).
+__device__ __forceinline__ D atan01_quick(double th, double tl) {
+    // th * 64 is exact; rounding it to the nearest integer keeps
+    // th >= c / 2 for k >= 1 (Sterbenz) — th * 64 + 0.5 could round up
+    const int k = int(rint(th * 64.0));
+    const double c = k * (1.0 / 64.0);
+    const D num = two_sum(th - c, tl);
+    const double p = th * c;
+    const double pe = fma(th, c, -p);
+    D den = quick_two_sum(1.0, p);
+    den.lo += pe + tl * c;
+    const double inv = 1.0 / den.hi;
+    const double u1 = num.hi * inv;
+    const double rr = fma(-u1, den.hi, num.hi) + (num.lo - u1 * den.lo);
+    const double u2 = rr * inv;
+    const double z = u1 * u1;
+    const double s = z * (-1.0 / 3 + z * (1.0 / 5 + z * (-1.0 / 7 + z * (1.0 / 9 - z * (1.0 / 11)))));
+    const D h = two_sum(kAtanTab[k][0], u1);
+    const double l = h.lo + (kAtanTab[k][1] + (u2 + u1 * s));
+    return quick_two_sum(h.hi, l);
+}
+
 }  // namespace dd
 
+// Quick form of atan2_cr for the generator's finite, nonzero inputs: the
+// quotient as a double-double from one reciprocal (th + tl, error ~2^-102),
+// atan01_quick, the quadrant shifts in double-double (π/2 - R >= R and
+// π - R >= R: no cancellation), then Ziv's test: with the result H + L
+// within 2^-62 H of the true value (margin 8 over the bound above), H is
+// its correct rounding whenever |L| + 2^-62 H is below half the spacing of
+// the doubles on L's side of H. Otherwise (~0.2% of inputs, or operands
+// outside [2^-900, 2^900], or a quotient below 2^-400) ok = false and the
+// caller evaluates atan2_cr.
+__device__ __forceinline__ double atan2_quick(double y, double x, bool& ok) {
+    const double ax = fabs(x), ay = fabs(y);
+    const double big = fmax(ax, ay), small = fmin(ax, ay);
+    ok = false;
+    if (!(small >= 0x1p-900 && big <= 0x1p900))
+        return 0.0;
+    const double inv = 1.0 / big;
+    const double th = small * inv;
+    if (!(th >= 0x1p-400))
+        return 0.0;
+    const double tl = fma(-th, big, small) * inv;
+    dd::D r = dd::atan01_quick(th, tl);
+    if (ay > ax)
+        r = dd::sub(dd::D{dd::kPi2Hi, dd::kPi2Lo}, r);
+    if (x < 0.0)
+        r = dd::sub(dd::D{dd::kPiHi, dd::kPiLo}, r);
+    // r.hi > 0: half the spacing of the doubles around it is ulp(r.hi) / 2,
+    // or ulp / 4 below a power of two when r.lo < 0
+    const long long b = __double_as_longlong(r.hi);
+    double half = __longlong_as_double(b & 0x7ff0000000000000LL) * 0x1p-53;
+    if ((b & 0x000fffffffffffffLL) == 0 && r.lo < 0.0)
+        half *= 0.5;
+    ok = fabs(r.lo) < half - r.hi * 0x1p-62;
+    return y < 0.0 ? -r.hi : r.hi;
+}
+
 // Correctly rounded atan2 (IEEE special cases as C99 Annex F for finite
-// and signed-zero inputs; infinities and NaNs defer to the CUDA libdevice).
+// and signed-zero inputs; infinities, NaNs and operands whose larger
+// magnitude is outside [2^-900, 2^900] defer to the CUDA libdevice).
 __device__ __forceinline__ double atan2_cr(double y, double x) {
     if (isnan(x) || isnan(y) || isinf(x) || isinf(y))
         return atan2(y, x);
@@ -178,6 +251,10 @@ __device__ __forceinline__ double atan2_cr(double y, double x) {
     if (x == 0.0)
         return copysign(dd::kPi2Hi, y);
     const double ax = fabs(x), ay = fabs(y);
+    // the reciprocals below need normal operands (grid coordinates are far
+    // inside this range; outside it the libdevice atan2)
+    if (!(fmax(ax, ay) <= 0x1p900 && fmax(ax, ay) >= 0x1p-900))
+        return atan2(y, x);
     dd::D r;
     if (ay <= ax) {
         r = dd::atan01(dd::div(dd::D{ay, 0.0}, dd::D{ax, 0.0}));
@@ -189,6 +266,14 @@ __device__ __forceinline__ double atan2_cr(double y, double x) {
         r = dd::sub(dd::D{dd::kPiHi, dd::kPiLo}, r);
     const double res = r.hi + r.lo;
     return y < 0.0 ? -res : res;
+}
+
+// The generator's atan2: the quick form, atan2_cr where its rounding is not
+// certain (bit-identical to atan2_cr on every input).
+__device__ __forceinline__ double atan2_gen(double y, double x) {
+    bool ok;
+    const double q = atan2_quick(y, x, ok);
+    return ok ? q : atan2_cr(y, x);
 }
 
 // Correctly rounded hypot for the coordinate range of the grids (|x|,|y| in

@@ -84,12 +84,34 @@ int stride_chunk(int Sp) {
 
 // azimuth_deg (geometry.cpp:39-46)
 __device__ __forceinline__ double azimuth_deg(double x, double y) {
-    double deg = atan2_cr(y, x) * kDegPerRad;
+    double deg = atan2_gen(y, x) * kDegPerRad;
     if (deg < 0)
         deg += 360.0;
     if (deg >= 360.0)
         deg = 0.0;
     return deg;
+}
+
+// floor(a / b) as the reference evaluates it (the correctly rounded quotient,
+// floored) from a * inv_b, inv_b = RN(1/b): the product is within 2.5 ulp
+// of the rounded quotient, so when q (1 ± 2^-50) spans no integer both
+// floor alike; otherwise the division.
+__device__ __forceinline__ double floor_quot(double a, double b, double inv_b) {
+    const double q = a * inv_b;
+    const double d = fabs(q) * 0x1p-50;
+    const double f = floor(q - d);
+    return f == floor(q + d) ? f : floor(a / b);
+}
+
+// floor(hypot(x, y) / b), hypot correctly rounded (geometry.cpp:216-217):
+// sqrt(x^2 + y^2) is within 1.75 ulp of hypot_cr and the product with inv_b
+// within 4.5 ulp of the reference's quotient (< 2^-50 relative), so the same
+// interval test decides it; otherwise hypot_cr and the division.
+__device__ __forceinline__ double floor_hypot_quot(double x, double y, double b, double inv_b) {
+    const double q = sqrt(x * x + y * y) * inv_b;
+    const double d = q * 0x1p-50;
+    const double f = floor(q - d);
+    return f == floor(q + d) ? f : floor(hypot_cr(x, y) / b);
 }
 
 // The sorted crossing list of build_sorted_intersections (geometry.cpp:127-198)
@@ -228,6 +250,11 @@ __device__ uint32_t walk_ray(const DevGrid& g, const double* s, const double* d,
     }
 
     const double len = sqrt(dd2);  // norm(dir)
+    const double inv_rs = 1.0 / g.ring_spacing, inv_h = 1.0 / g.slice_height;
+    // sqrt(e) <= eps decided on e where it is certain (e within a factor
+    // 1 ± 2^-48 of eps^2 takes the square root)
+    const double eps2 = g.eps * g.eps;
+    const double eps2_lo = eps2 * (1.0 - 0x1p-48), eps2_hi = eps2 * (1.0 + 0x1p-48);
     double ta = R.axial ? DBL_MAX : R.nextA();
     double tb = R.axial ? DBL_MAX : R.nextB();
     double tc = R.nextC();
@@ -258,21 +285,21 @@ __device__ uint32_t walk_ray(const DevGrid& g, const double* s, const double* d,
         if (np > 0) {
             // classify_chord (geometry.cpp:200-227)
             const double e0 = p0 - q0, e1 = p1 - q1, e2 = p2 - q2;
-            bool keep = !(sqrt(e0 * e0 + e1 * e1 + e2 * e2) <= g.eps);
+            const double e = e0 * e0 + e1 * e1 + e2 * e2;
+            bool keep = e > eps2_hi || (e >= eps2_lo && !(sqrt(e) <= g.eps));
             int slice = 0, ring = 0;
             if (keep) {
                 const double m0 = (p0 + q0) / 2, m1 = (p1 + q1) / 2, m2 = (p2 + q2) / 2;
                 if (g.volume) {
                     const double zloc = m2 + g.zoff;
-                    const double sf = floor(zloc / g.slice_height);
+                    const double sf = floor_quot(zloc, g.slice_height, inv_h);
                     if (sf < 0 || sf >= g.n_slices)
                         keep = false;
                     else
                         slice = int(sf);
                 }
                 if (keep) {
-                    const double dm = hypot_cr(m0, m1);
-                    ring = int(floor(dm / g.ring_spacing)) + 1;
+                    ring = int(floor_hypot_quot(m0, m1, g.ring_spacing, inv_rs)) + 1;
                     if (ring > g.n_rings)
                         keep = false;
                 }
@@ -1663,10 +1690,11 @@ __global__ void diag_math_kernel(int n, const double* __restrict__ x, const doub
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n)
         return;
-    out[4 * i + 0] = atan2_cr(y[i], x[i]);
-    out[4 * i + 1] = hypot_cr(x[i], y[i]);
-    out[4 * i + 2] = azimuth_deg(x[i], y[i]);
-    out[4 * i + 3] = atan2(y[i], x[i]);
+    out[5 * i + 0] = atan2_gen(y[i], x[i]);
+    out[5 * i + 1] = hypot_cr(x[i], y[i]);
+    out[5 * i + 2] = azimuth_deg(x[i], y[i]);
+    out[5 * i + 3] = atan2(y[i], x[i]);
+    out[5 * i + 4] = atan2_cr(y[i], x[i]);
 }
 
 void launch_diag_math(int n, const double* x, const double* y, double* out, cudaStream_t st) {

@@ -1000,12 +1000,13 @@ def uspg_to_cg_map(n: int, ctx: Optional[Context] = None) -> np.ndarray:
 
 
 def diag_math(x, y, ctx: Optional[Context] = None) -> np.ndarray:
-    """Device math of the generator: columns atan2 (correctly rounded), hypot
-    (correctly rounded), azimuth_deg, libdevice atan2 — for parity tests."""
+    """Device math of the generator: columns atan2 (the generator's quick form
+    with its fallback), hypot (correctly rounded), azimuth_deg, libdevice
+    atan2, the double-double atan2 alone — for parity tests."""
     ctx = ctx or default_context()
     x = np.ascontiguousarray(x, dtype=np.float64).ravel()
     y = np.ascontiguousarray(y, dtype=np.float64).ravel()
-    out = np.zeros((x.size, 4))
+    out = np.zeros((x.size, 5))
     _check(load().uscg_diag_math(ctx.h, x.size, x.ctypes.data_as(_dp), y.ctypes.data_as(_dp),
                                  out.ctypes.data_as(_dp)))
     return out

@@ -84,6 +84,45 @@ def test_device_math_matches_glibc(ub, orc):
     assert libdevice > 10 * mism_atan
 
 
+def test_quick_atan2_is_the_double_double_atan2(ub):
+    """The generator's atan2 (double-double quotient, a double series for
+    atan(u), Ziv's rounding test, double-double fallback) returns exactly the
+    full double-double atan2 (csrc/ddmath.cuh) on 4 M chord-like points and
+    on inputs at the quick form's seams: table switches (y/x at (k+1/2)/64),
+    |y| = |x| and its neighbours, axes, signed zeros, the [2^-900, 2^900]
+    operand range and quotients near 2^-400."""
+    rng = np.random.default_rng(20221)
+    n = 4_000_000
+    r = np.sqrt(rng.uniform(0, 1, n))
+    a = rng.uniform(-np.pi, np.pi, n)
+    xs, ys = [r * np.cos(a)], [r * np.sin(a)]
+    m = 200_000
+    k = rng.integers(0, 64, m)
+    t = (k + 0.5) / 64 * (1 + rng.integers(-4, 5, m) * 2.0 ** -52)
+    base = rng.uniform(0.01, 1.0, m)
+    sx, sy = rng.choice([-1.0, 1.0], m), rng.choice([-1.0, 1.0], m)
+    swap = rng.integers(0, 2, m).astype(bool)
+    xs.append(np.where(swap, base * t, base) * sx)
+    ys.append(np.where(swap, base, base * t) * sy)
+    d = rng.uniform(0.01, 1.0, m)
+    xs.append(d * sx)
+    ys.append(np.nextafter(d, d * (1 + rng.integers(-3, 4, m) * 1e-16)) * sy)
+    exps = rng.integers(-1000, 1000, m).astype(float)
+    xs.append(rng.uniform(0.5, 1, m) * 2.0 ** exps * sx)
+    with np.errstate(over="ignore", under="ignore"):
+        ys.append(rng.uniform(0.5, 1, m) * 2.0 ** np.clip(exps + rng.integers(-420, 420, m), -1070, 1020) * sy)
+    xs.append(np.array([0.0, -0.0, 1.0, -1.0, 0.0, 0.0, 1.0, -1.0, 2.0 ** -899, 2.0 ** 899, 1.0, 1.0]))
+    ys.append(np.array([0.0, 0.0, 0.0, 0.0, 1.0, -1.0, 1.0, -1.0, 2.0 ** -899, 2.0 ** 899, 2.0 ** -400,
+                        2.0 ** -401]))
+    x = np.concatenate(xs)
+    y = np.concatenate(ys)
+    fin = np.isfinite(x) & np.isfinite(y)
+    x, y = x[fin], y[fin]
+    dev = ub.uscg.diag_math(x, y)
+    same = dev[:, 0].view(np.uint64) == dev[:, 4].view(np.uint64)
+    assert same.all(), (np.count_nonzero(~same), x[~same][:4], y[~same][:4])
+
+
 @pytest.mark.parametrize("name", ["fan64q", "cone32"])
 def test_quarter_symmetric_tracer_is_identical(ub, name):
     g = REF_GEOMS[name]

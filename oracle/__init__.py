@@ -120,6 +120,11 @@ class Orc:
         L.orc_trace_chord.restype = C.c_int64
         L.orc_project.argtypes = [C.POINTER(_Grid), C.POINTER(_Cache), C.c_int, _dp, _dp, _dp]
         L.orc_project_length.argtypes = [C.POINTER(_Grid), C.c_int, _dp, _dp, C.c_int, _dp, _dp, _dp]
+        L.orc_length_lists.argtypes = [C.POINTER(_Grid), C.c_int, _dp, _dp, C.c_int, _dp, _u64p, _u32p, _dp,
+                                       C.c_uint64]
+        L.orc_length_lists.restype = C.c_uint64
+        L.orc_weighted_mart.argtypes = [C.c_uint64, _u64p, _u32p, _dp, _dp, _dp, C.c_double, C.c_double, C.c_int]
+        L.orc_weighted_mart.restype = C.c_uint64
         L.orc_reconstruct.argtypes = [C.POINTER(_Grid), C.POINTER(_Cache), C.c_int, _dp, _dp, _dp,
                                       C.c_double, C.c_double, C.c_int, C.c_double, _dp, _dp, _u8p]
         L.orc_reconstruct.restype = C.c_int
@@ -189,6 +194,19 @@ class Orc:
         return self.L.orc_norm360(float(x))
 
     # -- cache / trace -----------------------------------------------------
+    def weighted_mart(self, offsets, idx, w, proj, beta=0.4, sweeps=5, f_init=1.0, p_floor=0.0, cells=None):
+        """weighted_update + the loop of cartesian_mart_stored (siddon.cpp:141-154,
+        185-209) over (voxel, length) lists: (field f64 [cells], clamps)"""
+        off = np.ascontiguousarray(offsets, np.uint64)
+        ii = np.ascontiguousarray(idx, np.uint32)
+        ww = np.ascontiguousarray(w, np.float64)
+        pp = np.ascontiguousarray(proj, np.float64).reshape(-1)
+        assert pp.size == off.size - 1
+        field = np.full(int(cells), float(f_init))
+        clamps = int(self.L.orc_weighted_mart(pp.size, _ptr(off, _u64p), _ptr(ii, _u32p), _ptr(ww, _dp),
+                                              _ptr(pp, _dp), _ptr(field, _dp), beta, p_floor, sweeps))
+        return field, clamps
+
     def cache(self, grid: OrcGrid, src, det):
         return OrcCache(self, grid, src, det)
 
@@ -287,6 +305,25 @@ class OrcCache:
                                       _ptr(self.det, _dp), th.size, _ptr(th, _dp), _ptr(f, _dp),
                                       _ptr(out, _dp))
         return out
+
+    def length_lists(self, thetas):
+        """The LengthWeighted model's (voxel, chord length) lists per (view,
+        line), a cell's pieces merged: (offsets u64 [views*lines+1], idx u32, len f64)"""
+        th = np.ascontiguousarray(thetas, float)
+        off = np.zeros(th.size * self.lines + 1, np.uint64)
+        args = (C.byref(self.grid._c), self.lines, _ptr(self.src, _dp), _ptr(self.det, _dp), th.size,
+                _ptr(th, _dp), _ptr(off, _u64p))
+        n = int(self.orc.L.orc_length_lists(*args, None, None, 0))
+        idx = np.zeros(max(n, 1), np.uint32)
+        ln = np.zeros(max(n, 1), np.float64)
+        got = int(self.orc.L.orc_length_lists(*args, _ptr(idx, _u32p), _ptr(ln, _dp), n))
+        assert got == n
+        return off, idx[:n], ln[:n]
+
+    def weighted_mart(self, offsets, idx, w, proj, beta=0.4, sweeps=5, f_init=1.0, p_floor=0.0):
+        """Orc.weighted_mart on this grid's cells"""
+        return self.orc.weighted_mart(offsets, idx, w, proj, beta, sweeps, f_init, p_floor,
+                                      cells=self.grid.cell_count())
 
     def reconstruct(self, thetas, proj, init=None, beta=0.4, tolerance=1e-6, max_sweeps=100,
                     f_init=1.0, p_floor=0.0, power=False):

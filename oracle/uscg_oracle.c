@@ -476,6 +476,65 @@ static void rotate_z(const double p[3], double deg, double out[3]) {
     out[2] = p[2];
 }
 
+/* The LengthWeighted model's coefficients (phantom.cpp:213-269): every piece
+   (cell, length) of the line through s and d, in the reference's order, handed
+   to `emit`. Shared by the projector and the list emitter below. */
+typedef void (*piece_fn)(void* ctx, uint32_t cell, double length);
+
+static void length_pieces(const orc_grid* g, const ring_row* rt, uint64_t per_slice, double* taus,
+                          double* pts, double* cuts, const double* s, const double* d, piece_fn emit,
+                          void* ctx) {
+    const int np = sorted_points(g, s, d, taus, pts);
+    for (int i = 0; i + 1 < np; ++i) {
+        orc_record rec;
+        if (!classify_chord(g, pts + 3 * i, pts + 3 * (i + 1), &rec))
+            continue;
+        const double* a = pts + 3 * i;
+        const double u[3] = {pts[3 * (i + 1)] - a[0], pts[3 * (i + 1) + 1] - a[1],
+                             pts[3 * (i + 1) + 2] - a[2]};
+        const double chord_len = sqrt(u[0] * u[0] + u[1] * u[1] + u[2] * u[2]);
+        const ring_row* rl = &rt[rec.ring];
+        const double step_deg = 360.0 / rl->count;
+        int nc = 0;
+        cuts[nc++] = 0.0;
+        cuts[nc++] = 1.0;
+        for (uint32_t j = 0; j < rl->count; ++j) {
+            const double psi = j * step_deg * (kPi / 180.0);
+            const double ex = cos(psi), ey = sin(psi);
+            const double g0 = ex * a[1] - ey * a[0];
+            const double g1 = ex * u[1] - ey * u[0];
+            if (g1 == 0.0)
+                continue;
+            const double tau = -g0 / g1;
+            if (tau > 0.0 && tau < 1.0)
+                cuts[nc++] = tau;
+        }
+        qsort(cuts, (size_t)nc, sizeof(double), cmp_double);
+        const uint32_t base = (uint32_t)(rec.slice * (uint32_t)per_slice + rl->head);
+        for (int q = 0; q + 1 < nc; ++q) {
+            const double piece = (cuts[q + 1] - cuts[q]) * chord_len;
+            if (piece <= 0)
+                continue;
+            const double mid = 0.5 * (cuts[q] + cuts[q + 1]);
+            const double phi = orc_azimuth_deg(a[0] + mid * u[0], a[1] + mid * u[1]);
+            int sector = (int)(phi * rl->inv_step);
+            if (sector >= (int)rl->count)
+                sector = (int)rl->count - 1;
+            emit(ctx, base + (uint32_t)sector, piece);
+        }
+    }
+}
+
+typedef struct {
+    const double* field;
+    double total;
+} sum_ctx;
+
+static void sum_piece(void* c, uint32_t cell, double length) {
+    sum_ctx* k = (sum_ctx*)c;
+    k->total += length * k->field[cell];
+}
+
 void orc_project_length(const orc_grid* g, int lines, const double* src, const double* det,
                         int views, const double* theta_deg, const double* field, double* out) {
     ring_row* rt = ring_table(g);
@@ -494,53 +553,130 @@ void orc_project_length(const orc_grid* g, int lines, const double* src, const d
             double s[3], d[3];
             rotate_z(src + 3 * (size_t)l, theta, s);
             rotate_z(det + 3 * (size_t)l, theta, d);
-            const int np = sorted_points(g, s, d, taus, pts);
-            double total = 0;
-            for (int i = 0; i + 1 < np; ++i) {
-                orc_record rec;
-                if (!classify_chord(g, pts + 3 * i, pts + 3 * (i + 1), &rec))
-                    continue;
-                const double* a = pts + 3 * i;
-                const double u[3] = {pts[3 * (i + 1)] - a[0], pts[3 * (i + 1) + 1] - a[1],
-                                     pts[3 * (i + 1) + 2] - a[2]};
-                const double chord_len = sqrt(u[0] * u[0] + u[1] * u[1] + u[2] * u[2]);
-                const ring_row* rl = &rt[rec.ring];
-                const double step_deg = 360.0 / rl->count;
-                int nc = 0;
-                cuts[nc++] = 0.0;
-                cuts[nc++] = 1.0;
-                for (uint32_t j = 0; j < rl->count; ++j) {
-                    const double psi = j * step_deg * (kPi / 180.0);
-                    const double ex = cos(psi), ey = sin(psi);
-                    const double g0 = ex * a[1] - ey * a[0];
-                    const double g1 = ex * u[1] - ey * u[0];
-                    if (g1 == 0.0)
-                        continue;
-                    const double tau = -g0 / g1;
-                    if (tau > 0.0 && tau < 1.0)
-                        cuts[nc++] = tau;
-                }
-                qsort(cuts, (size_t)nc, sizeof(double), cmp_double);
-                const uint32_t base = (uint32_t)(rec.slice * (uint32_t)per_slice + rl->head);
-                for (int q = 0; q + 1 < nc; ++q) {
-                    const double piece = (cuts[q + 1] - cuts[q]) * chord_len;
-                    if (piece <= 0)
-                        continue;
-                    const double mid = 0.5 * (cuts[q] + cuts[q + 1]);
-                    const double phi = orc_azimuth_deg(a[0] + mid * u[0], a[1] + mid * u[1]);
-                    int sector = (int)(phi * rl->inv_step);
-                    if (sector >= (int)rl->count)
-                        sector = (int)rl->count - 1;
-                    total += piece * field[base + (uint32_t)sector];
-                }
-            }
-            out[(size_t)v * lines + l] = total;
+            sum_ctx k = {field, 0.0};
+            length_pieces(g, rt, per_slice, taus, pts, cuts, s, d, sum_piece, &k);
+            out[(size_t)v * lines + l] = k.total;
         }
     }
     free(cuts);
     free(taus);
     free(pts);
     free(rt);
+}
+
+/* The (voxel, chord length) lists of the LengthWeighted model, one per (view,
+   line): the pieces of phantom.cpp:213-269 with the pieces of one cell merged
+   (a line may cross a cell twice, either side of its closest approach; the
+   binary tracer's stamp dedup, tracer.cpp:181-195, handles the same case), the
+   cell listed where it is first met. offsets: views*lines + 1. idx / len NULL:
+   count only. Returns the number of entries, or (uint64_t)-1 when cap is too
+   small. */
+typedef struct {
+    uint32_t* idx;
+    double* len;
+    uint64_t begin, n, cap;
+    uint32_t* stamp; /* cell -> 1 + position within the line, valid if mark[cell] == unit + 1 */
+    uint32_t* mark;
+    uint32_t unit1;
+    int overflow;
+} list_ctx;
+
+static void list_piece(void* c, uint32_t cell, double length) {
+    list_ctx* k = (list_ctx*)c;
+    if (k->mark[cell] == k->unit1) {
+        if (k->len)
+            k->len[k->begin + k->stamp[cell]] += length;
+        return;
+    }
+    k->mark[cell] = k->unit1;
+    k->stamp[cell] = (uint32_t)(k->n - k->begin);
+    if (k->idx) {
+        if (k->n >= k->cap) {
+            k->overflow = 1;
+            return;
+        }
+        k->idx[k->n] = cell;
+        k->len[k->n] = length;
+    }
+    ++k->n;
+}
+
+uint64_t orc_length_lists(const orc_grid* g, int lines, const double* src, const double* det, int views,
+                          const double* theta_deg, uint64_t* offsets, uint32_t* idx, double* len,
+                          uint64_t cap) {
+    ring_row* rt = ring_table(g);
+    const uint64_t per_slice = orc_cells_per_slice(g);
+    const size_t ncell = cell_count(g);
+    const int max_t = 2 * g->n_rings + g->n_slices + 2;
+    double* taus = (double*)malloc(sizeof(double) * (size_t)max_t);
+    double* pts = (double*)malloc(sizeof(double) * 3 * (size_t)max_t);
+    uint32_t maxc = 0;
+    for (int k = 1; k <= g->n_rings; ++k)
+        if (rt[k].count > maxc)
+            maxc = rt[k].count;
+    double* cuts = (double*)malloc(sizeof(double) * (size_t)(maxc + 2));
+    list_ctx k = {idx, len, 0, 0, cap, (uint32_t*)calloc(ncell, sizeof(uint32_t)),
+                  (uint32_t*)calloc(ncell, sizeof(uint32_t)), 0, 0};
+    for (int v = 0; v < views; ++v) {
+        const double theta = orc_norm360(theta_deg[v]);
+        for (int l = 0; l < lines; ++l) {
+            double s[3], d[3];
+            rotate_z(src + 3 * (size_t)l, theta, s);
+            rotate_z(det + 3 * (size_t)l, theta, d);
+            const size_t unit = (size_t)v * lines + l;
+            k.begin = k.n;
+            k.unit1 = (uint32_t)unit + 1;
+            offsets[unit] = k.n;
+            length_pieces(g, rt, per_slice, taus, pts, cuts, s, d, list_piece, &k);
+        }
+    }
+    offsets[(size_t)views * lines] = k.n;
+    free(k.stamp);
+    free(k.mark);
+    free(cuts);
+    free(taus);
+    free(pts);
+    free(rt);
+    return k.overflow ? (uint64_t)-1 : k.n;
+}
+
+/* MART over stored (voxel, length) lists: weighted_update and the sweep loop of
+   cartesian_mart_stored (siddon.cpp:141-154, 185-209) — length-weighted forward
+   projection, one multiplicative factor per line, no stopping test; p_floor =
+   cfg value when > 0, else auto_p_floor (siddon.cpp:128-139). field: in =
+   initial values, out = result. Returns the number of clamped factors. */
+uint64_t orc_weighted_mart(uint64_t rows, const uint64_t* offsets, const uint32_t* idx, const double* w,
+                           const double* proj, double* field, double beta, double p_floor_cfg, int sweeps) {
+    double p_floor = p_floor_cfg;
+    if (!(p_floor > 0)) {
+        double sum = 0;
+        uint64_t count = 0;
+        for (uint64_t r = 0; r < rows; ++r)
+            if (proj[r] > 0) {
+                sum += proj[r];
+                ++count;
+            }
+        p_floor = count == 0 ? 1e-12 : 1e-12 * (sum / count);
+    }
+    uint64_t clamps = 0;
+    for (int s = 0; s < sweeps; ++s)
+        for (uint64_t r = 0; r < rows; ++r) {
+            const uint64_t b = offsets[r], e = offsets[r + 1];
+            if (proj[r] == 0 || b == e)
+                continue;
+            double p_bar = 0;
+            for (uint64_t i = b; i < e; ++i)
+                p_bar += w[i] * field[idx[i]];
+            const double ratio = proj[r] / (p_bar > p_floor ? p_bar : p_floor);
+            double factor = 1.0 - beta * (1.0 - ratio);
+            if (factor <= 0) {
+                factor = p_floor;
+                ++clamps;
+            }
+            for (uint64_t i = b; i < e; ++i)
+                field[idx[i]] *= factor;
+        }
+    return clamps;
 }
 
 /* ---- Sp-MART (src/solver.cpp:33-162) ------------------------------------ */

@@ -86,6 +86,18 @@ void orc_project(const orc_grid* g, const orc_cache* c, int views, const double*
 void orc_project_length(const orc_grid* g, int lines, const double* src, const double* det,
                         int views, const double* theta_deg, const double* field, double* out);
 
+/* The (voxel, chord length) lists of the LengthWeighted model per (view, line),
+   the pieces of one cell merged at its first position. offsets: views*lines+1.
+   idx / len NULL: count only. Returns the entries, (uint64_t)-1 if cap is short. */
+uint64_t orc_length_lists(const orc_grid* g, int lines, const double* src, const double* det, int views,
+                          const double* theta_deg, uint64_t* offsets, uint32_t* idx, double* len,
+                          uint64_t cap);
+
+/* MART over stored (voxel, length) lists (weighted_update and the loop of
+   cartesian_mart_stored, siddon.cpp:141-154, 185-209). Returns the clamp count. */
+uint64_t orc_weighted_mart(uint64_t rows, const uint64_t* offsets, const uint32_t* idx, const double* w,
+                           const double* proj, double* field, double beta, double p_floor_cfg, int sweeps);
+
 /* reconstruct / reconstruct_from. field: in = initial values, out = result.
    report: [0]=sweeps [1]=converged [2]=all_zero [3]=skips [4]=clamps [5]=U (cells updated)
    residuals: max_sweeps (or NULL), crossed: cell_count (or NULL).

@@ -319,6 +319,18 @@ uscg_status uscg_cartesian_like(const uscg_grid* grid, uscg_cartesian* out);
  * (cartesian_mart_otf: every line re-traced on every pass). */
 uscg_status uscg_csystem_create(uscg_ctx ctx, const uscg_cartesian* cart, const uscg_scan* scan,
                                 int32_t stored, uscg_csystem* out);
+/* The USPG / USCG grid's own (voxel index, chord length) system: the pieces
+ * of the LengthWeighted model (proj/src/phantom.cpp:213-269: every chord cut
+ * at its ring's radial sector planes, a piece in the sector of its midpoint)
+ * of every (view, line) of the tracer's scan, as stored lists with the pieces
+ * of one cell merged (voxel indices in the reference's flat cell order), plus
+ * the MART dependency schedule of those supports. uscg_csystem_export returns
+ * the lists; uscg_csystem_reconstruct runs the reference's length-weighted row
+ * action (weighted_update, proj/src/siddon.cpp:141-154) on the polar field
+ * (field_out: cell_count values). The reference has no such entry point: its
+ * length model only feeds generate_projections, and its weighted update only
+ * runs on the Cartesian grid; this composes the two. */
+uscg_status uscg_tracer_length_system(uscg_tracer tracer, uscg_csystem* out);
 uscg_status uscg_csystem_info(uscg_csystem sys, uint64_t* entries, uint64_t* device_bytes,
                               int32_t* levels, double* precompute_ms);
 /* CartesianSystem (offsets views*lines+1, voxel indices, f32 lengths) to host

@@ -5,7 +5,7 @@ the C ABI declared in ``include/uscg_b200.h``. :mod:`.uscg` mirrors the
 reference library's reconstruction API on top of that ABI.
 """
 from .uscg import (  # noqa: F401
-    CartesianSystem, Context, cartesian_to_field, intensity_profile, sharpness, Detector, DomainError, Field, FirstViewCache, GridMode, GridSpec, InvalidArgument, NoDevice,
+    CartesianSystem, LengthSystem, Context, cartesian_to_field, intensity_profile, sharpness, Detector, DomainError, Field, FirstViewCache, GridMode, GridSpec, InvalidArgument, NoDevice,
     ProjectionSet, ReconReport, ReconResult, ScanGeometry, SolverConfig, Tracer, field_to_cartesian,
     generate_projections, image_metrics, launch_count, load, mae, mae_volume, problem_stride, project_stack,
     reconstruct, reconstruct_batch, reconstruct_from, reconstruct_stack, resample_stack, ring_counts_m1, rmse, rmse_volume, ssim,
@@ -13,7 +13,7 @@ from .uscg import (  # noqa: F401
 )
 
 __all__ = [
-    "cartesian_to_field", "intensity_profile", "sharpness", "CartesianSystem", "Context", "Detector", "DomainError", "Field", "FirstViewCache", "GridMode", "GridSpec", "InvalidArgument",
+    "cartesian_to_field", "intensity_profile", "sharpness", "CartesianSystem", "LengthSystem", "Context", "Detector", "DomainError", "Field", "FirstViewCache", "GridMode", "GridSpec", "InvalidArgument",
     "NoDevice", "ProjectionSet", "ReconReport", "ReconResult", "ScanGeometry", "SolverConfig", "Tracer",
     "field_to_cartesian", "generate_projections", "image_metrics", "launch_count", "load", "mae", "mae_volume",
     "problem_stride", "project_stack", "reconstruct", "reconstruct_batch", "reconstruct_from", "reconstruct_stack", "resample_stack",

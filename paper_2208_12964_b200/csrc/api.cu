@@ -2444,6 +2444,112 @@ uscg_status uscg_csystem_create(uscg_ctx ctx, const uscg_cartesian* cart, const 
     });
 }
 
+// The polar grid's own (voxel, chord length) system: the LengthWeighted
+// model's pieces (phantom.cpp:213-269) of every (view, line) as CSR lists, a
+// cell's pieces merged at its first position (a line may meet a cell on both
+// sides of its closest approach; the binary tracer's stamp dedup,
+// tracer.cpp:181-195, handles the same case), with the MART dependency
+// schedule of those supports. The returned system runs weighted_update
+// (siddon.cpp:141-154) on the USPG / USCG field through
+// uscg_csystem_reconstruct, and uscg_csystem_export gives the lists.
+uscg_status uscg_tracer_length_system(uscg_tracer t, uscg_csystem* out) {
+    return guarded([&] {
+        need(t && out, "null argument");
+        bind(t->ctx);
+        need(t->d_rays.p != nullptr,
+             "the length-weighted model needs the tracer's rays (not available for an imported cache)");
+        const uint64_t rows = t->units();
+        need(rows < (1ull << 31), "views * lines must fit in 31 bits");
+        need(t->cells < (1ull << 32), "cell count must fit in 32 bits");
+        std::unique_ptr<uscg_csystem_s> s(new uscg_csystem_s);
+        s->ctx = t->ctx;
+        s->voxels = t->cells;
+        s->stored = 1;
+        s->lines = t->lines;
+        s->views = t->views;
+        cudaStream_t st = t->st();
+        cudaEvent_t e0, e1;
+        UB_CUDA(cudaEventCreate(&e0));
+        UB_CUDA(cudaEventCreate(&e1));
+        UB_CUDA(cudaEventRecord(e0, st));
+        // pieces per line, then the pieces themselves
+        DevBuf<uint32_t> cnt, roff, ridx;
+        DevBuf<float> rlen;
+        cnt.alloc(rows);
+        launch_length_lists(t->dev_grid(), t->lines, t->views, t->d_rays.p, t->d_theta.p, nullptr, cnt.p, nullptr,
+                            nullptr, st);
+        std::vector<uint32_t> hc(rows);
+        UB_CUDA(cudaMemcpyAsync(hc.data(), cnt.p, sizeof(uint32_t) * rows, cudaMemcpyDeviceToHost, st));
+        UB_CUDA(cudaStreamSynchronize(st));
+        std::vector<uint32_t> raw_off(rows + 1, 0);
+        uint64_t raw = 0;
+        for (uint64_t r = 0; r < rows; ++r) {
+            raw_off[r] = uint32_t(raw);
+            raw += hc[r];
+            need(raw < (1ull << 32), "the (voxel, length) lists must hold fewer than 2^32 entries");
+        }
+        raw_off[rows] = uint32_t(raw);
+        roff.alloc(rows + 1);
+        ridx.alloc(std::max<uint64_t>(raw, 1));
+        rlen.alloc(std::max<uint64_t>(raw, 1));
+        UB_CUDA(cudaMemcpyAsync(roff.p, raw_off.data(), sizeof(uint32_t) * (rows + 1), cudaMemcpyHostToDevice, st));
+        launch_length_lists(t->dev_grid(), t->lines, t->views, t->d_rays.p, t->d_theta.p, roff.p, nullptr, ridx.p,
+                            rlen.p, st);
+        UB_CUDA(cudaEventRecord(e1, st));
+        std::vector<uint32_t> idx(raw);
+        std::vector<float> len(raw);
+        UB_CUDA(cudaMemcpyAsync(idx.data(), ridx.p, sizeof(uint32_t) * raw, cudaMemcpyDeviceToHost, st));
+        UB_CUDA(cudaMemcpyAsync(len.data(), rlen.p, sizeof(float) * raw, cudaMemcpyDeviceToHost, st));
+        UB_CUDA(cudaStreamSynchronize(st));
+        float ms = 0;
+        UB_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+        s->precompute_ms = ms;
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+        // a cell's pieces merged at its first position (in place: the merged
+        // lists are never longer)
+        std::vector<uint32_t> off(rows + 1), mark(t->cells, 0), where(t->cells, 0);
+        std::vector<double> acc;
+        uint64_t n = 0;
+        for (uint64_t r = 0; r < rows; ++r) {
+            const uint64_t begin = n;
+            off[r] = uint32_t(n);
+            acc.clear();
+            for (uint64_t k = raw_off[r]; k < raw_off[r + 1]; ++k) {
+                const uint32_t c = idx[k];
+                if (mark[c] == uint32_t(r) + 1) {
+                    acc[where[c]] += double(len[k]);
+                    continue;
+                }
+                mark[c] = uint32_t(r) + 1;
+                where[c] = uint32_t(n - begin);
+                idx[n++] = c;
+                acc.push_back(double(len[k]));
+            }
+            for (uint64_t k = begin; k < n; ++k)
+                len[k] = float(acc[k - begin]);
+        }
+        off[rows] = uint32_t(n);
+        s->entries = n;
+        s->d_off.alloc(rows + 1);
+        s->d_idx.alloc(std::max<uint64_t>(n, 1));
+        s->d_w.alloc(std::max<uint64_t>(n, 1));
+        UB_CUDA(cudaMemcpyAsync(s->d_off.p, off.data(), sizeof(uint32_t) * (rows + 1), cudaMemcpyHostToDevice, st));
+        UB_CUDA(cudaMemcpyAsync(s->d_idx.p, idx.data(), sizeof(uint32_t) * n, cudaMemcpyHostToDevice, st));
+        UB_CUDA(cudaMemcpyAsync(s->d_w.p, len.data(), sizeof(float) * n, cudaMemcpyHostToDevice, st));
+        // the dependency schedule of the supports (host, schedule.h)
+        AsapSchedule sched(s->voxels, uint32_t(s->lines), 1);
+        sched.add(idx.data(), off.data(), uint32_t(rows));
+        sched.done();
+        std::vector<uint32_t> order;
+        sched.finish(order, s->level_off);
+        s->d_order.alloc(std::max<size_t>(order.size(), 1));
+        UB_CUDA(cudaMemcpyAsync(s->d_order.p, order.data(), sizeof(uint32_t) * order.size(), cudaMemcpyHostToDevice, st));
+        UB_CUDA(cudaStreamSynchronize(st));
+        *out = s.release();
+    });
+}
+
 uscg_status uscg_csystem_info(uscg_csystem s, uint64_t* entries, uint64_t* device_bytes, int32_t* levels,
                               double* precompute_ms) {
     return guarded([&] {

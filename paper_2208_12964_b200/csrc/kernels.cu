@@ -485,9 +485,26 @@ struct LengthAcc {
     }
 };
 
-template <int P>
+// counts a line's pieces / writes them as (cell, length) pairs: the
+// (voxel, chord length) lists of the same walk (launch_length_lists)
+struct LengthCount {
+    uint32_t n = 0;
+    __device__ void piece(double, uint32_t) { ++n; }
+};
+struct LengthWrite {
+    uint32_t* idx;
+    float* len;
+    uint32_t k;
+    __device__ void piece(double l, uint32_t cell) {
+        idx[k] = cell;
+        len[k] = float(l);
+        ++k;
+    }
+};
+
+template <class Sink>
 __device__ void length_chord(const DevGrid& g, double a0, double a1, double a2, double b0, double b1,
-                             double b2, int slice, int ring, LengthAcc<P>& A) {
+                             double b2, int slice, int ring, Sink& A) {
     const double u0 = b0 - a0, u1 = b1 - a1, u2 = b2 - a2;
     const double chord_len = sqrt(u0 * u0 + u1 * u1 + u2 * u2);
     const RingRow rr = g.rings[ring];
@@ -594,13 +611,62 @@ __global__ void __launch_bounds__(128) project_length_kernel(DevGrid g, int line
     walk_ray(
         g, s, d,
         [&](double p0, double p1, double p2, double q0, double q1, double q2, int slice, int ring) {
-            length_chord<P>(g, p0, p1, p2, q0, q1, q2, slice, ring, A);
+            length_chord(g, p0, p1, p2, q0, q1, q2, slice, ring, A);
         },
         [] {});
     float* o = out + size_t(unit) * Sp + size_t(chunk) * P;
 #pragma unroll
     for (int p = 0; p < P; ++p)
         o[p] = float(A.acc[p]);
+}
+
+// The (voxel, chord length) lists of every (view, line): a thread per line
+// walks it as the projector does; off == nullptr counts the pieces into
+// counts[unit], else writes them at off[unit].
+__global__ void __launch_bounds__(128) length_lists_kernel(DevGrid g, int lines, int views,
+                                                           const double* __restrict__ rays,
+                                                           const double* __restrict__ theta,
+                                                           const uint32_t* __restrict__ off,
+                                                           uint32_t* __restrict__ counts,
+                                                           uint32_t* __restrict__ idx, float* __restrict__ len) {
+    const long long unit = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (unit >= (long long)lines * views)
+        return;
+    const int v = int(unit / lines), l = int(unit % lines);
+    const double rad = theta[v] * kRadPerDeg;  // rotate_z_deg (scan.cpp:50-54)
+    const double c = cos(rad), sn = sin(rad);
+    const double* s0 = rays + 3 * size_t(l);
+    const double* d0 = rays + 3 * (size_t(lines) + l);
+    const double s[3] = {c * s0[0] - sn * s0[1], sn * s0[0] + c * s0[1], s0[2]};
+    const double d[3] = {c * d0[0] - sn * d0[1], sn * d0[0] + c * d0[1], d0[2]};
+    if (off == nullptr) {
+        LengthCount A;
+        walk_ray(
+            g, s, d,
+            [&](double p0, double p1, double p2, double q0, double q1, double q2, int slice, int ring) {
+                length_chord(g, p0, p1, p2, q0, q1, q2, slice, ring, A);
+            },
+            [] {});
+        counts[unit] = A.n;
+    } else {
+        LengthWrite A{idx, len, off[unit]};
+        walk_ray(
+            g, s, d,
+            [&](double p0, double p1, double p2, double q0, double q1, double q2, int slice, int ring) {
+                length_chord(g, p0, p1, p2, q0, q1, q2, slice, ring, A);
+            },
+            [] {});
+    }
+}
+
+void launch_length_lists(const DevGrid& g, int lines, int views, const double* rays, const double* theta,
+                         const uint32_t* off, uint32_t* counts, uint32_t* idx, float* len, cudaStream_t st) {
+    const long long units = (long long)lines * views;
+    if (units <= 0)
+        return;
+    length_lists_kernel<<<unsigned((units + 127) / 128), 128, 0, st>>>(g, lines, views, rays, theta, off, counts, idx,
+                                                                      len);
+    check_launch();
 }
 
 void launch_project_length(const DevGrid& g, int lines, int views, const double* rays,

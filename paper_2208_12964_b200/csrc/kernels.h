@@ -87,6 +87,11 @@ void launch_project_length(const DevGrid& g, int lines, int views, const double*
                            const double* theta, const float* field, int Sp, float* out,
                            cudaStream_t st);
 
+// The LengthWeighted model's pieces per (view, line) as (cell, length) pairs:
+// off == nullptr: counts[unit] = pieces of the line; else written at off[unit]
+void launch_length_lists(const DevGrid& g, int lines, int views, const double* rays, const double* theta,
+                         const uint32_t* off, uint32_t* counts, uint32_t* idx, float* len, cudaStream_t st);
+
 // K2 for one problem from precomputed traced lists (lists[lpos[u], lpos[u+1])): out [units]
 void launch_project_lists(const uint32_t* lists, const unsigned long long* lpos, uint64_t units, const float* field,
                           float* out, cudaStream_t st);

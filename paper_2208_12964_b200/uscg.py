@@ -124,7 +124,7 @@ EXPORTS = [
     "uscg_tracer_build_schedule", "uscg_tracer_export_successors", "uscg_reconstruct_batch", "uscg_problem_stride", "uscg_project", "uscg_reconstruct",
     "uscg_resample", "uscg_uspg_to_cg_map", "uscg_diag_math", "uscg_schedule_build", "uscg_image_metrics",
     "uscg_cartesian_like", "uscg_csystem_create", "uscg_csystem_info", "uscg_csystem_export",
-    "uscg_csystem_reconstruct", "uscg_csystem_destroy", "uscg_tracer_export_wave",
+    "uscg_csystem_reconstruct", "uscg_csystem_destroy", "uscg_tracer_length_system", "uscg_tracer_export_wave",
     "uscg_cartesian_to_field", "uscg_image_sharpness", "uscg_intensity_profile",
 ]
 
@@ -185,6 +185,7 @@ def load(build_if_missing: bool = True):
     L.uscg_uspg_to_cg_map.argtypes = [vp, C.c_int32, _u32p]
     L.uscg_cartesian_like.argtypes = [C.POINTER(_Grid), C.POINTER(_Cart)]
     L.uscg_csystem_create.argtypes = [vp, C.POINTER(_Cart), C.POINTER(_Scan), C.c_int32, C.POINTER(vp)]
+    L.uscg_tracer_length_system.argtypes = [vp, C.POINTER(vp)]
     L.uscg_csystem_info.argtypes = [vp, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64), C.POINTER(C.c_int32), _dp]
     L.uscg_csystem_export.argtypes = [vp, _u32p, _u32p, _fp]
     L.uscg_csystem_reconstruct.argtypes = [vp, vp, C.POINTER(_Cfg), vp, _dp, C.c_uint32]
@@ -990,6 +991,23 @@ class CartesianSystem:
             self.close()
         except Exception:
             pass
+
+
+class LengthSystem(CartesianSystem):
+    """The polar grid's own (voxel index, chord length) lists (the pieces of
+    the LengthWeighted model, phantom.cpp:213-269, a cell's pieces merged) for
+    every (view, line) of the tracer's scan, with the reference's weighted row
+    action (weighted_update, siddon.cpp:141-154) on the USPG / USCG field:
+    export() -> (offsets, cell indices, lengths); reconstruct(proj, cfg) ->
+    (field f32 [cell_count], device seconds)."""
+
+    def __init__(self, tracer: "Tracer"):
+        h = C.c_void_p()
+        _check(load().uscg_tracer_length_system(tracer.h, C.byref(h)))
+        self.h = h.value
+        self._tracer = tracer  # the system uses the tracer's context
+        self.geom, self.stored = tracer.geom, True
+        self.voxels = tracer.spec.cell_count()
 
 
 def uspg_to_cg_map(n: int, ctx: Optional[Context] = None) -> np.ndarray:

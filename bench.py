@@ -977,6 +977,99 @@ def bench_cmp(args, rank, world, local):
 
 
 # ---------------------------------------------------------------------------
+# length-weighted MART on the polar grid's (voxel, chord length) lists
+# ---------------------------------------------------------------------------
+def bench_lw(args, rank, world, local):
+    """uscg_tracer_length_system on C1 and C3: the (voxel index, chord length)
+    lists of the LengthWeighted model (phantom.cpp:213-269) built on the device,
+    then K iterations of the reference's weighted row action (siddon.cpp:141-154)
+    on the USPG / USCG field, one launch per dependency level. Beside it: the
+    binary-model executor on the same geometry, and the oracle's weighted MART
+    on the same lists on one host core. Rank 0 only (one problem)."""
+    import torch
+
+    import paper_2208_12964_b200 as ub
+    from paper_2208_12964_b200 import workloads
+
+    if rank != 0:
+        return
+    torch.cuda.set_device(local)
+    peak, peak_kind = hbm_peak()
+    out = {}
+    clocks = Clocks(local).start()
+    launches0 = ub.launch_count()
+    for name in ("c1", "c3"):
+        wl = workloads.make(name)
+        spec, geom = wl.spec, wl.geom
+        tr = ub.Tracer(geom, spec, False)
+        truth = workloads.phantom_fields(wl, 1)[0].astype(np.float32)
+        proj = ub.project_stack(tr, truth[None], model="length")[0].reshape(-1)
+        t0 = time.perf_counter()
+        ls = ub.LengthSystem(tr)
+        build_s = time.perf_counter() - t0
+        inf = ls.info()
+        K = int(wl.sweeps)
+        cfg = ub.SolverConfig(beta=wl.beta, tolerance=0, max_sweeps=K)
+        for _ in range(max(1, min(args.warmup, 2))):
+            ls.reconstruct(proj, cfg)
+        field, sec = ls.reconstruct(proj, cfg)
+        ms_it = 1e3 * sec / K
+        bres = ub.reconstruct(ub.ProjectionSet(geom, ub.project_stack(tr, truth[None])[0].astype(np.float64)), spec,
+                              cfg, tr)
+        cpu = None
+        exp = ls.export()
+        live = np.diff(exp[0].astype(np.int64))[proj > 0]  # zero measurements are skipped (siddon.cpp:143)
+        U = int(live.sum())
+        if not args.no_cpu:
+            import oracle
+            orc = oracle.Orc()
+            off, idx, w = exp
+            t0 = time.perf_counter()
+            orc.weighted_mart(off, idx, w.astype(np.float64), proj.astype(np.float64), beta=wl.beta, sweeps=1,
+                              cells=spec.cell_count())
+            cw = time.perf_counter() - t0
+            cpu = {"value": U / cw, "unit": "updates/s", "cores": 1, "kind": "port", "cpu": cpu_model(),
+                   "sample": f"oracle weighted_update restatement, one sweep over the same lists ({cw:.2f} s)"}
+        re = None
+        if name == "c1":  # closure: length-weighted projections of the result against the data
+            off, idx, w = exp
+            rows = geom.views * geom.lines()
+            re = np.bincount(np.repeat(np.arange(rows), np.diff(off.astype(np.int64))),
+                             weights=w.astype(np.float64) * field[idx], minlength=rows)
+        B = 20 * U + 8 * proj.size  # u32 index + f32 length + field read (sum), read + write (update)
+        out[name] = {
+            "ms_per_iteration": ms_it, "updates_per_iteration": U,
+            "updates_per_s": U / (ms_it * 1e-3), "iterations": K, "levels": inf["levels"],
+            "lists": {"entries": inf["entries"], "device_bytes": inf["device_bytes"],
+                      "device_build_ms": inf["precompute_ms"], "build_with_host_schedule_s": build_s},
+            "roofline": {"bound": "hbm", "achieved": B / (ms_it * 1e-3) / 1e9, "peak": peak, "unit": "GB/s",
+                         "frac": B / (ms_it * 1e-3) / 1e9 / peak, "traffic": None, "peak_kind": peak_kind,
+                         "kernel": "csr_level_kernel (one launch per dependency level, a block per line)",
+                         "bytes_model": "20 B per list entry of a line with a non-zero measurement (u32 index, "
+                                        "f32 length, field read for the sum, read + write for the update) + 8 B "
+                                        "per line (offset, measurement)"},
+            "binary_model_ms_per_iteration": 1e3 * bres.report.seconds / K,
+            "closure_mean_abs_residual": None if re is None else float(np.abs(re - proj)[proj > 0].mean()),
+            "cpu_baseline": cpu,
+        }
+        ls.close()
+        tr.close()
+    clk = clocks.stop()
+    c3 = out["c3"]
+    line = {
+        "metric": "length-weighted MART updates/s on USCG (c3, (voxel, chord length) lists)",
+        "value": c3["updates_per_s"], "unit": "updates/s", "n_gpus": 1, "steps": c3["iterations"],
+        "warmup": args.warmup, "ms_per_step": c3["ms_per_iteration"], "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic: seeded phantoms, length-weighted projections of the same model",
+        "config": {"workload": "lw", "parts": ["c1", "c3"], "l2": "C3: lists of ~1 GB exceed L2; C1 is L2-resident"},
+        "roofline": c3["roofline"], "cpu_baseline": c3["cpu_baseline"], "e2e": None,
+        "gpu_launches": int(ub.launch_count() - launches0), "clocks": clk, "c1": out["c1"], "c3": out["c3"],
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
 # entry
 # ---------------------------------------------------------------------------
 def relaunch(n):
@@ -1037,6 +1130,8 @@ def main():
             bench_c5(args, rank, world, local)
         elif args.config == "cmp":
             bench_cmp(args, rank, world, local)
+        elif args.config == "lw":
+            bench_lw(args, rank, world, local)
         else:
             gpu = Gpu(local)
             line = bench_mart(gpu, args.config, args, rank, world)

@@ -2628,9 +2628,8 @@ uscg_status uscg_csystem_reconstruct(uscg_csystem s, const float* proj, const us
         cudaEvent_t e0, e1;
         UB_CUDA(cudaEventCreate(&e0));
         UB_CUDA(cudaEventCreate(&e1));
-        UB_CUDA(cudaEventRecord(e0, st));
         const int levels = int(s->level_off.size()) - 1;
-        for (int sweep = 0; sweep < cfg->max_sweeps; ++sweep)
+        auto one_sweep = [&] {
             for (int l = 0; l < levels; ++l) {
                 const uint32_t* units = s->d_order.p + s->level_off[l];
                 const int n = int(s->level_off[l + 1] - s->level_off[l]);
@@ -2641,8 +2640,44 @@ uscg_status uscg_csystem_reconstruct(uscg_csystem s, const float* proj, const us
                     launch_otf_level(s->C, s->lines, s->d_rays.p, s->d_theta.p, units, n, d_proj, d_field, cfg->beta,
                                      p_floor, s->w_clamps.p, st);
             }
+        };
+        // a sweep is one launch per dependency level: captured once and
+        // replayed per sweep (USCG_CSR_GRAPH=0: plain launches)
+        const char* ge = std::getenv("USCG_CSR_GRAPH");
+        const bool graph = cfg->max_sweeps >= 2 && levels >= 8 && !(ge && !std::atoi(ge));
+        if (graph) {
+            cudaGraph_t g = nullptr;
+            cudaGraphExec_t exec = nullptr;
+            UB_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+            try {
+                one_sweep();
+            } catch (...) {
+                cudaStreamEndCapture(st, &g);
+                if (g)
+                    cudaGraphDestroy(g);
+                throw;
+            }
+            UB_CUDA(cudaStreamEndCapture(st, &g));
+            const cudaError_t ie = cudaGraphInstantiate(&exec, g, 0);
+            if (ie != cudaSuccess) {
+                cudaGraphDestroy(g);
+                UB_CUDA(ie);
+            }
+            UB_CUDA(cudaEventRecord(e0, st));  // (the sweeps: capture and instantiation are host-side set-up)
+            for (int sweep = 0; sweep < cfg->max_sweeps; ++sweep)
+                UB_CUDA(cudaGraphLaunch(exec, st));
+            UB_CUDA(cudaEventRecord(e1, st));
+            count_launch(uint64_t(levels) * uint64_t(cfg->max_sweeps - 1));  // (the capture counted one sweep)
+            UB_CUDA(cudaStreamSynchronize(st));
+            cudaGraphExecDestroy(exec);
+            cudaGraphDestroy(g);
+        } else {
+            UB_CUDA(cudaEventRecord(e0, st));
+            for (int sweep = 0; sweep < cfg->max_sweeps; ++sweep)
+                one_sweep();
+            UB_CUDA(cudaEventRecord(e1, st));
+        }
         UB_CUDA(cudaGetLastError());
-        UB_CUDA(cudaEventRecord(e1, st));
         if (!dev)
             UB_CUDA(cudaMemcpyAsync(field_out, d_field, sizeof(float) * s->voxels, cudaMemcpyDeviceToHost, st));
         UB_CUDA(cudaStreamSynchronize(st));

@@ -175,15 +175,41 @@ __global__ void __launch_bounds__(kLevelThreads) csr_level_kernel(
     double p_floor, unsigned long long* clamps) {
     __shared__ double red[kLevelThreads / 32];
     const uint32_t u = units[blockIdx.x];
+    const float m = proj[u];
+    if (m == 0.f)
+        return;  // weighted_update (siddon.cpp:143): a zero measurement is skipped, nothing read
     const uint32_t b = off[u], e = off[u + 1];
+    // a thread's first kKeep entries stay in registers from the sum to the
+    // update (a polar line holds a few hundred cells: usually all of them)
+    constexpr int kKeep = 4;
+    uint32_t id[kKeep];
+    float v[kKeep];
     double s = 0;
-    for (uint32_t k = b + threadIdx.x; k < e; k += kLevelThreads)
+#pragma unroll
+    for (int i = 0; i < kKeep; ++i) {
+        const uint32_t k = b + threadIdx.x + uint32_t(i) * kLevelThreads;
+        id[i] = k < e ? idx[k] : 0xFFFFFFFFu;
+    }
+#pragma unroll
+    for (int i = 0; i < kKeep; ++i)
+        v[i] = id[i] != 0xFFFFFFFFu ? f[id[i]] : 0.f;
+#pragma unroll
+    for (int i = 0; i < kKeep; ++i) {
+        const uint32_t k = b + threadIdx.x + uint32_t(i) * kLevelThreads;
+        if (k < e)
+            s += double(w[k]) * double(v[i]);
+    }
+    for (uint32_t k = b + threadIdx.x + kKeep * kLevelThreads; k < e; k += kLevelThreads)
         s += double(w[k]) * double(f[idx[k]]);
     const double p_bar = block_sum_d(s, red);
-    const float g = cart_factor(p_bar, proj[u], beta, p_floor, clamps);
+    const float g = cart_factor(p_bar, m, beta, p_floor, clamps);
     if (g < 0.f)
         return;
-    for (uint32_t k = b + threadIdx.x; k < e; k += kLevelThreads)
+#pragma unroll
+    for (int i = 0; i < kKeep; ++i)
+        if (id[i] != 0xFFFFFFFFu)
+            f[id[i]] = fmaxf(v[i] * g, FLT_MIN);
+    for (uint32_t k = b + threadIdx.x + kKeep * kLevelThreads; k < e; k += kLevelThreads)
         f[idx[k]] = fmaxf(f[idx[k]] * g, FLT_MIN);
 }
 

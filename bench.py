@@ -331,6 +331,9 @@ def mart_kernel_name(info, P):
         return f"mart_wave_kernel<{P}> (one persistent launch per reconstruct call; task = (view, {P}-problem chunk))"
     if ex == 4:
         return "mart_tile_kernel (one CTA, the field in shared memory)"
+    if ex == 5:
+        return ("mart_level_kernel<64, 12> (one launch per dependency level, chained by programmatic dependent "
+                "launch; a 64-thread block per line with a non-zero measurement)")
     return (f"mart_flow_kernel<{P}> (one dataflow launch per reconstruct call"
             + ("; task = one line, fed by its precomputed traced list)" if info.get("executor_bytes") else ")"))
 
@@ -584,14 +587,17 @@ def bench_mart(gpu: Gpu, config, args, rank, world, steps=None, warmup=None, cpu
                 "peak_kind": peak_kind, "kernel": mart_kernel_name(info, P),
                 "algorithmic_bytes_per_iteration": B, "bytes_model": model,
                 "flow_run_levels_per_iteration": levels,
-                "launches": "one persistent launch per reconstruct call (all K iterations); achieved = "
-                            "B * K / device time of that launch"}
+                "launches": ("one launch per dependency level and iteration; achieved = B * K / device time of the "
+                             "reconstruct call's launches" if info["executor"] == 5 else
+                             "one persistent launch per reconstruct call (all K iterations); achieved = "
+                             "B * K / device time of that launch")}
     # what binds each executor, measured
     notes = {
         "c2": ("the per-line chain and the SMs' scattered 128-byte row traffic, mostly served by L2 "
                "(profiles/r2_row_microbench.md): the fraction compares the algorithmic bytes with HBM"),
-        "c3": ("latency: the dependency chain's run levels at ~6 us each (gathers, the publish fence, the "
-               "hand-off between warps); its 26 MB field stays in L2"),
+        "c3": ("latency: the dependency chain's 1269 line levels at ~3.4 us each (one gather round trip, a two-warp "
+               "sum, the factor, the stores and the hand-over to the next level's waiting grid); its 26 MB field "
+               "stays in L2"),
         "c4": ("scattered 4-byte read-modify-writes on a 211 MB field: ~90 G updates/s, the rate a microbenchmark "
                "of that access pattern reaches (profiles/r2_sector_microbench.md)"),
         "c1": "latency: one CTA, one block barrier per dependency level",

@@ -131,7 +131,7 @@ typedef struct {
     double generator_ms;           /* device time of the first-view generator (count + scan +
                                       write + annotate; 0 for an imported cache) */
     int32_t executor;              /* MART executor of the last reconstruction: -1 none yet,
-                                      0 flow, 3 wave (USCG_MART_MODE) */
+                                      0 flow, 3 wave, 4 tile, 5 levels (USCG_MART_MODE) */
     uint64_t wave_requirements;    /* wave executor: other-view requirements per sweep (0 until built) */
     double wave_build_s;           /* wave executor: seconds to build its lists and requirements */
     uint64_t executor_bytes;       /* device bytes the MART executors derived from the record store

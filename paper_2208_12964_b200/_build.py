@@ -18,7 +18,7 @@ CLI = os.path.join(LIBDIR, "uscg_b200")  # the reference's CLI pipeline over the
 CLI_SRC = os.path.join(HERE, "cli", "uscg_cli.cpp")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
-SOURCES = ["api.cu", "kernels.cu", "mart_sweep.cu", "mart_tile.cu", "wave_build.cu", "metrics.cu", "cartesian.cu", "schedule_gpu.cu", "schedule.cpp"]
+SOURCES = ["api.cu", "kernels.cu", "mart_sweep.cu", "mart_tile.cu", "mart_levels.cu", "wave_build.cu", "metrics.cu", "cartesian.cu", "schedule_gpu.cu", "schedule.cpp"]
 HEADERS = ["internal.cuh", "kernels.h", "schedule.h", "ddmath.cuh"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 # --fmad=false: the fp64 index arithmetic must round exactly like the

@@ -169,6 +169,13 @@ struct uscg_tracer_s {
     double lists_seconds = 0;
     // tile executor (one small problem): the lines in ASAP level order
     bool tile_built = false, tile_off = false;
+    // level executor (mart_levels.cu): every line sorted by ASAP level of the
+    // line DAG (run = 1), its level offsets, and per-call scratch for the
+    // compaction to the lines with a non-zero measurement
+    bool lv_built = false;
+    DevBuf<uint32_t> d_lv_order, d_lv_off, w_lv_flags, w_lv_pos, w_lv_live, w_lv_live_off;
+    std::vector<uint32_t> lv_off;
+    double lv_seconds = 0;
     DevBuf<uint4> d_tmeta;
     DevBuf<uint32_t> d_tlevel;
     int tile_levels = 0;
@@ -638,6 +645,8 @@ int mart_mode() {
         return 3;
     if (m == "tile")
         return 4;
+    if (m == "levels")
+        return 5;
     return -1;
 }
 
@@ -967,6 +976,38 @@ void build_lists(uscg_tracer_s* t) {
         std::fprintf(stderr, "flow lists: %llu entries, %.3f s\n", (unsigned long long)total, t->lists_seconds);
 }
 
+// The level executor's schedule (mart_levels.cu): the line DAG (runs of one
+// line) levelled on the device (schedule_gpu.cu); only the level-sorted order
+// and the level offsets are kept.
+void build_line_levels(uscg_tracer_s* t) {
+    if (t->lv_built)
+        return;
+    const auto h0 = std::chrono::steady_clock::now();
+    DevBuf<uint32_t> tmp[7];
+    GpuSchedule G;
+    G.alloc = [&](GpuSchedule::Array a, size_t n) -> uint32_t* {
+        if (a == GpuSchedule::kOrder) {
+            t->d_lv_order.alloc(n);
+            return t->d_lv_order.p;
+        }
+        if (a == GpuSchedule::kLevelOff) {
+            t->d_lv_off.alloc(n);
+            return t->d_lv_off.p;
+        }
+        tmp[a].alloc(n);
+        return tmp[a].p;
+    };
+    gpu_schedule_build(t->trace_args(), t->views, t->max_recs, t->max_cells, t->cells, t->cells_per_sweep, 1u,
+                       uint32_t(t->lines), G, t->st());
+    UB_CUDA(cudaStreamSynchronize(t->st()));
+    t->lv_off = std::move(G.level_off);
+    t->lv_built = true;
+    t->lv_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - h0).count();
+    if (const char* e = std::getenv("USCG_FLOW_VERBOSE"); e && std::atoi(e))
+        std::fprintf(stderr, "line levels: %zu lines, %zu levels, %.3f s\n", size_t(t->units()),
+                     t->lv_off.size() - 1, t->lv_seconds);
+}
+
 // The tile executor's schedule (mart_tile.cu): every line's ASAP level within
 // a sweep (level = 1 + the largest level of an earlier line sharing a cell),
 // lines sorted by level. Geometry only, built once per tracer from the traced
@@ -1281,7 +1322,8 @@ uscg_status uscg_tracer_get_info(uscg_tracer t, uscg_tracer_info* info) {
         info->max_line_cells = t->max_cells;
         info->cells_per_sweep = t->cells_per_sweep;
         info->chords_per_sweep = t->records * uint64_t(t->views);
-        info->levels = t->sched_built ? int32_t(t->level_off.size()) - 1 : 0;
+        info->levels = t->executor == 5 && t->lv_built ? int32_t(t->lv_off.size()) - 1
+                       : (t->sched_built ? int32_t(t->level_off.size()) - 1 : 0);
         info->generator_ms = t->generator_ms;
         info->executor = t->executor;
         info->wave_requirements = t->wave_deps;
@@ -1291,7 +1333,7 @@ uscg_status uscg_tracer_get_info(uscg_tracer t, uscg_tracer_info* info) {
                                t->d_wpos.bytes() + t->d_wdep_off.bytes() + t->d_wdeps.bytes() +
                                t->d_order.bytes() + t->d_pred_off.bytes() + t->d_preds.bytes() +
                                t->d_succ_off.bytes() + t->d_succs.bytes() + t->d_npred_x.bytes() +
-                               t->d_tmeta.bytes() + t->d_tlevel.bytes();
+                               t->d_tmeta.bytes() + t->d_tlevel.bytes() + t->d_lv_order.bytes() + t->d_lv_off.bytes();
     });
 }
 
@@ -1643,9 +1685,22 @@ static void reconstruct_body(uscg_tracer t, const float* proj, int32_t problems,
     if ((exec_mode == -1 && P >= 4) || exec_mode == 3)
         exec_mode = wave_fits(t) && wave_supported(h) && wave_fits_smem(h, t->lines) ? 3 : 0;
     else if ((exec_mode == -1 || exec_mode == 4) && Sp == 1)
-        exec_mode = build_tile(t) ? 4 : 0;
+        // (a field within L2: the level executor's ~3.4 us per line level beats
+        // the dataflow executor's ~6.5 us per run level, C3 4.3 vs 5.9 ms; a
+        // larger field is bound by its scattered updates, where the dataflow
+        // executor's persistent warps do better, C4 86 vs 100 ms)
+        exec_mode = build_tile(t) ? 4 : (exec_mode == -1 && cells * sizeof(float) <= (96ull << 20) ? 5 : 0);
     else if (exec_mode == -1 || exec_mode == 4)
         exec_mode = 0;
+    if (exec_mode == 5) {
+        // the level executor: one problem whose traced lists fit in memory
+        if (Sp == 1)
+            build_lists(t);
+        if (Sp != 1 || !t->lists_built)
+            exec_mode = 0;
+        else
+            build_line_levels(t);
+    }
     t->executor = exec_mode;
     if (exec_mode == 3) {
         build_wave(t);
@@ -1677,6 +1732,7 @@ static void reconstruct_body(uscg_tracer t, const float* proj, int32_t problems,
     }
     std::vector<int> sweeps(S, 0), converged(S, 0);
     std::vector<std::vector<double>> resid(S);
+    std::vector<uint32_t> lv_live_off;  // level executor: live lines per level of this call
     if (track)
         t->w_prev.ensure(cells * Sp), t->w_resid.ensure(Sp);
     int n_active = 0;
@@ -1736,6 +1792,28 @@ static void reconstruct_body(uscg_tracer t, const float* proj, int32_t problems,
             ts.units = int(units);
             ts.levels = t->tile_levels;
             launch_mart_tile(h, ts, cells, n_run, st);
+        } else if (exec_mode == 5) {
+            n_run = track ? 1 : cfg->max_sweeps - sweep;
+            const uint32_t nl = uint32_t(t->lv_off.size()) - 1;
+            LevelSchedule ls;
+            ls.lists = t->d_lists.p;
+            ls.lpos = t->d_lpos.p;
+            if (sweep == 0) {
+                // the lines with a non-zero measurement, level by level
+                t->w_lv_flags.ensure(units);
+                t->w_lv_pos.ensure(units + 1);
+                t->w_lv_live.ensure(units);
+                t->w_lv_live_off.ensure(nl + 1);
+                launch_live_lines(t->d_lv_order.p, d_proj, uint32_t(units), t->d_lv_off.p, nl, t->w_lv_flags.p,
+                                  t->w_lv_pos.p, t->w_lv_live.p, t->w_lv_live_off.p, st);
+                lv_live_off.resize(nl + 1);
+                UB_CUDA(cudaMemcpyAsync(lv_live_off.data(), t->w_lv_live_off.p, sizeof(uint32_t) * (nl + 1),
+                                        cudaMemcpyDeviceToHost, st));
+                UB_CUDA(cudaStreamSynchronize(st));
+            }
+            ls.live = t->w_lv_live.p;
+            ls.live_off = lv_live_off;
+            launch_mart_levels(h, ls, n_run, st);
         } else if (exec_mode == 0) {
             // without a per-sweep residual every remaining sweep runs in one
             // launch, back to back (cross-sweep dependencies)
@@ -2347,7 +2425,7 @@ struct uscg_csystem_s {
     uint64_t voxels = 0, entries = 0;
     double precompute_ms = 0;
     DevBuf<double> d_rays, d_theta;
-    DevBuf<uint32_t> d_off, d_idx, d_order;
+    DevBuf<uint32_t> d_off, d_idx, d_order, w_order;
     DevBuf<float> d_w, w_proj, w_field;
     DevBuf<unsigned long long> w_clamps;
     std::vector<uint32_t> level_off;
@@ -2628,11 +2706,32 @@ uscg_status uscg_csystem_reconstruct(uscg_csystem s, const float* proj, const us
         cudaEvent_t e0, e1;
         UB_CUDA(cudaEventCreate(&e0));
         UB_CUDA(cudaEventCreate(&e1));
-        const int levels = int(s->level_off.size()) - 1;
+        // the lines with a non-zero measurement, level by level (a zero
+        // measurement is skipped, siddon.cpp:143: no block is launched for it)
+        int levels = int(s->level_off.size()) - 1;
+        std::vector<uint32_t> live_off(1, 0u);
+        {
+            std::vector<uint32_t> order(rows), live;
+            UB_CUDA(cudaMemcpyAsync(order.data(), s->d_order.p, sizeof(uint32_t) * rows, cudaMemcpyDeviceToHost, st));
+            UB_CUDA(cudaStreamSynchronize(st));
+            live.reserve(rows);
+            for (int l = 0; l < levels; ++l) {
+                for (uint32_t k = s->level_off[l]; k < s->level_off[l + 1]; ++k)
+                    if (pp[order[k]] > 0)
+                        live.push_back(order[k]);
+                if (live.size() > live_off.back())  // (a level without live lines is dropped)
+                    live_off.push_back(uint32_t(live.size()));
+            }
+            s->w_order.ensure(std::max<size_t>(live.size(), 1));
+            UB_CUDA(cudaMemcpyAsync(s->w_order.p, live.data(), sizeof(uint32_t) * live.size(), cudaMemcpyHostToDevice,
+                                    st));
+            UB_CUDA(cudaStreamSynchronize(st));  // `live` leaves scope
+            levels = int(live_off.size()) - 1;
+        }
         auto one_sweep = [&] {
             for (int l = 0; l < levels; ++l) {
-                const uint32_t* units = s->d_order.p + s->level_off[l];
-                const int n = int(s->level_off[l + 1] - s->level_off[l]);
+                const uint32_t* units = s->w_order.p + live_off[l];
+                const int n = int(live_off[l + 1] - live_off[l]);
                 if (s->stored)
                     launch_csr_level(units, n, s->d_off.p, s->d_idx.p, s->d_w.p, d_proj, d_field, cfg->beta, p_floor,
                                      s->w_clamps.p, st);

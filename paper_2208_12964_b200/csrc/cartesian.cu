@@ -18,6 +18,7 @@
 
 #include <cfloat>
 #include <cstdint>
+#include <cstdlib>
 
 #include "kernels.h"
 
@@ -111,6 +112,7 @@ __device__ void siddon_walk(const double* s, const double* d, const DevCart& C, 
     }
 }
 
+template <int NT = kLevelThreads>
 __device__ __forceinline__ double block_sum_d(double v, double* red) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1)
@@ -119,7 +121,8 @@ __device__ __forceinline__ double block_sum_d(double v, double* red) {
         red[threadIdx.x >> 5] = v;
     __syncthreads();
     double s = 0;
-    for (int k = 0; k < kLevelThreads / 32; ++k)
+#pragma unroll
+    for (int k = 0; k < NT / 32; ++k)
         s += red[k];
     return s;  // every thread
 }
@@ -168,49 +171,62 @@ __global__ void siddon_write_kernel(DevCart C, int lines, int views, const doubl
     });
 }
 
-// stored coefficients: block per line of the level
-__global__ void __launch_bounds__(kLevelThreads) csr_level_kernel(
+// stored coefficients: block per line of the level. NT threads hold KEEP
+// entries each in registers from the sum to the update (a polar line holds a
+// few hundred cells: all of them); small blocks, so that a level's lines and
+// the next level's waiting blocks are resident together.
+template <int NT, int KEEP>
+__global__ void __launch_bounds__(NT) csr_level_kernel(
     const uint32_t* __restrict__ units, const uint32_t* __restrict__ off, const uint32_t* __restrict__ idx,
     const float* __restrict__ w, const float* __restrict__ proj, float* __restrict__ f, double beta,
     double p_floor, unsigned long long* clamps) {
-    __shared__ double red[kLevelThreads / 32];
+    __shared__ double red[NT / 32];
+    // Programmatic dependent launch: this grid may start while the previous
+    // level still runs. Everything that does not depend on the field (the
+    // line's measurement, offsets, indices and lengths) is loaded first; the
+    // next level is released to do the same; then the grid waits for the
+    // previous level's completion (and its stores) before touching the field.
+    // Every block waits, also one that has nothing to do: a grid must not
+    // complete before its predecessor (the level after it waits on this grid
+    // only).
     const uint32_t u = units[blockIdx.x];
     const float m = proj[u];
+    uint32_t id[KEEP];
+    float wk[KEEP], v[KEEP];
+    uint32_t b = 0, e = 0;
+    if (m != 0.f) {  // weighted_update (siddon.cpp:143): a zero measurement is skipped, nothing read
+        b = off[u];
+        e = off[u + 1];
+    }
+#pragma unroll
+    for (int i = 0; i < KEEP; ++i) {
+        const uint32_t k = b + threadIdx.x + uint32_t(i) * NT;
+        id[i] = k < e ? idx[k] : 0xFFFFFFFFu;
+        wk[i] = k < e ? w[k] : 0.f;
+    }
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    asm volatile("griddepcontrol.wait;" ::: "memory");
     if (m == 0.f)
-        return;  // weighted_update (siddon.cpp:143): a zero measurement is skipped, nothing read
-    const uint32_t b = off[u], e = off[u + 1];
-    // a thread's first kKeep entries stay in registers from the sum to the
-    // update (a polar line holds a few hundred cells: usually all of them)
-    constexpr int kKeep = 4;
-    uint32_t id[kKeep];
-    float v[kKeep];
+        return;
     double s = 0;
 #pragma unroll
-    for (int i = 0; i < kKeep; ++i) {
-        const uint32_t k = b + threadIdx.x + uint32_t(i) * kLevelThreads;
-        id[i] = k < e ? idx[k] : 0xFFFFFFFFu;
-    }
+    for (int i = 0; i < KEEP; ++i)
+        v[i] = id[i] != 0xFFFFFFFFu ? __ldcg(f + id[i]) : 0.f;
 #pragma unroll
-    for (int i = 0; i < kKeep; ++i)
-        v[i] = id[i] != 0xFFFFFFFFu ? f[id[i]] : 0.f;
-#pragma unroll
-    for (int i = 0; i < kKeep; ++i) {
-        const uint32_t k = b + threadIdx.x + uint32_t(i) * kLevelThreads;
-        if (k < e)
-            s += double(w[k]) * double(v[i]);
-    }
-    for (uint32_t k = b + threadIdx.x + kKeep * kLevelThreads; k < e; k += kLevelThreads)
-        s += double(w[k]) * double(f[idx[k]]);
-    const double p_bar = block_sum_d(s, red);
+    for (int i = 0; i < KEEP; ++i)
+        s += double(wk[i]) * double(v[i]);
+    for (uint32_t k = b + threadIdx.x + KEEP * NT; k < e; k += NT)
+        s += double(w[k]) * double(__ldcg(f + idx[k]));
+    const double p_bar = block_sum_d<NT>(s, red);
     const float g = cart_factor(p_bar, m, beta, p_floor, clamps);
     if (g < 0.f)
         return;
 #pragma unroll
-    for (int i = 0; i < kKeep; ++i)
+    for (int i = 0; i < KEEP; ++i)
         if (id[i] != 0xFFFFFFFFu)
             f[id[i]] = fmaxf(v[i] * g, FLT_MIN);
-    for (uint32_t k = b + threadIdx.x + kKeep * kLevelThreads; k < e; k += kLevelThreads)
-        f[idx[k]] = fmaxf(f[idx[k]] * g, FLT_MIN);
+    for (uint32_t k = b + threadIdx.x + KEEP * NT; k < e; k += NT)
+        f[idx[k]] = fmaxf(__ldcg(f + idx[k]) * g, FLT_MIN);
 }
 
 // on the fly: thread 0 walks the line into shared memory, then the block updates
@@ -273,7 +289,34 @@ void launch_csr_level(const uint32_t* units, int n, const uint32_t* off, const u
                       cudaStream_t st) {
     if (n <= 0)
         return;
-    csr_level_kernel<<<unsigned(n), kLevelThreads, 0, st>>>(units, off, idx, w, proj, f, beta, p_floor, clamps);
+    // launched with programmatic stream serialization (the kernel orders itself
+    // after the previous level with griddepcontrol.wait); USCG_CSR_PDL=0: plain
+    static const bool pdl = [] {
+        const char* e = std::getenv("USCG_CSR_PDL");
+        return !(e && !std::atoi(e));
+    }();
+    // threads per line (USCG_CSR_THREADS = 64 | 128 | 256; default 128)
+    static const int nt = [] {
+        const char* e = std::getenv("USCG_CSR_THREADS");
+        const int v = e ? std::atoi(e) : 128;
+        return v == 256 ? 256 : (v == 64 ? 64 : 128);
+    }();
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(unsigned(n));
+    cfg.blockDim = dim3(unsigned(nt));
+    cfg.dynamicSmemBytes = 0;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl ? 1 : 0;
+    if (nt == 256)
+        UB_CUDA(cudaLaunchKernelEx(&cfg, csr_level_kernel<256, 4>, units, off, idx, w, proj, f, beta, p_floor, clamps));
+    else if (nt == 128)
+        UB_CUDA(cudaLaunchKernelEx(&cfg, csr_level_kernel<128, 6>, units, off, idx, w, proj, f, beta, p_floor, clamps));
+    else
+        UB_CUDA(cudaLaunchKernelEx(&cfg, csr_level_kernel<64, 8>, units, off, idx, w, proj, f, beta, p_floor, clamps));
     count_launch();
 }
 

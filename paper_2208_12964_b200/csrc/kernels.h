@@ -114,6 +114,23 @@ size_t tile_smem_bytes(uint64_t cells, int units, int levels);
 bool tile_fits(uint64_t cells, int units, int levels);
 void launch_mart_tile(const MartArgs& h, const TileSchedule& ts, uint64_t cells, int sweeps, cudaStream_t st);
 
+// K3 level executor (mart_levels.cu; one problem): a kernel per ASAP level of
+// the line DAG, a 64-thread block per line with a non-zero measurement, levels
+// chained by programmatic dependent launch, a sweep replayed from a CUDA graph.
+struct LevelSchedule {
+    const uint32_t* lists;             // traced index lists
+    const unsigned long long* lpos;    // [units + 1]
+    const uint32_t* live;              // live lines (non-zero measurement) in level order (device)
+    std::vector<uint32_t> live_off;    // [levels + 1] into `live` (host)
+};
+// order: every line sorted by level (device), level_off_dev [levels + 1];
+// writes flags / pos (units + 1) scratch, the compacted `live` lines and
+// live_off_dev [levels + 1]
+void launch_live_lines(const uint32_t* order, const float* proj, uint32_t units, const uint32_t* level_off_dev,
+                       uint32_t levels, uint32_t* flags, uint32_t* pos, uint32_t* live, uint32_t* live_off_dev,
+                       cudaStream_t st);
+void launch_mart_levels(const MartArgs& h, const LevelSchedule& ls, int sweeps, cudaStream_t st);
+
 // Ring of traced index lists shared by the chunk tasks of a unit:
 // slot = [n, idx[0..n)], slot_words >= max_cells + 1.
 struct FlowSlab {

@@ -332,8 +332,8 @@ def mart_kernel_name(info, P):
     if ex == 4:
         return "mart_tile_kernel (one CTA, the field in shared memory)"
     if ex == 5:
-        return ("mart_level_kernel<64, 12> (one launch per dependency level, chained by programmatic dependent "
-                "launch; a 64-thread block per line with a non-zero measurement)")
+        return ("mart_level_kernel<256, 3> (one launch per dependency level, chained by programmatic dependent "
+                "launch; a 256-thread block per line with a non-zero measurement)")
     return (f"mart_flow_kernel<{P}> (one dataflow launch per reconstruct call"
             + ("; task = one line, fed by its precomputed traced list)" if info.get("executor_bytes") else ")"))
 
@@ -413,6 +413,8 @@ def bench_mart(gpu: Gpu, config, args, rank, world, steps=None, warmup=None, cpu
         step_dev()
     torch.cuda.synchronize()
     info = tracer.info()
+    if info["executor"] == 5:
+        levels = int(info["levels"])  # the level executor's line levels (the run levels above are the flow executor's)
     if world > 1 and torch.distributed.is_initialized():
         torch.distributed.barrier()
     clocks = Clocks(gpu.local).start()
@@ -586,7 +588,7 @@ def bench_mart(gpu: Gpu, config, args, rank, world, steps=None, warmup=None, cpu
                 "traffic": traffic, "traffic_unit": "DRAM bytes per iteration (ncu, profiles/)",
                 "peak_kind": peak_kind, "kernel": mart_kernel_name(info, P),
                 "algorithmic_bytes_per_iteration": B, "bytes_model": model,
-                "flow_run_levels_per_iteration": levels,
+                "levels_per_iteration": levels,
                 "launches": ("one launch per dependency level and iteration; achieved = B * K / device time of the "
                              "reconstruct call's launches" if info["executor"] == 5 else
                              "one persistent launch per reconstruct call (all K iterations); achieved = "

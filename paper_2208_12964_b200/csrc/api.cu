@@ -176,6 +176,7 @@ struct uscg_tracer_s {
     DevBuf<uint32_t> d_lv_order, d_lv_off, w_lv_flags, w_lv_pos, w_lv_live, w_lv_live_off;
     std::vector<uint32_t> lv_off;
     double lv_seconds = 0;
+    LevelGraphCache lv_graph;  // a sweep's launches, replayed while the same solve comes back
     DevBuf<uint4> d_tmeta;
     DevBuf<uint32_t> d_tlevel;
     int tile_levels = 0;
@@ -1813,7 +1814,7 @@ static void reconstruct_body(uscg_tracer t, const float* proj, int32_t problems,
             }
             ls.live = t->w_lv_live.p;
             ls.live_off = lv_live_off;
-            launch_mart_levels(h, ls, n_run, st);
+            launch_mart_levels(h, ls, n_run, st, &t->lv_graph);
         } else if (exec_mode == 0) {
             // without a per-sweep residual every remaining sweep runs in one
             // launch, back to back (cross-sweep dependencies)

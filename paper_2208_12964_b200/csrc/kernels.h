@@ -129,7 +129,32 @@ struct LevelSchedule {
 void launch_live_lines(const uint32_t* order, const float* proj, uint32_t units, const uint32_t* level_off_dev,
                        uint32_t levels, uint32_t* flags, uint32_t* pos, uint32_t* live, uint32_t* live_off_dev,
                        cudaStream_t st);
-void launch_mart_levels(const MartArgs& h, const LevelSchedule& ls, int sweeps, cudaStream_t st);
+// One sweep's level launches as an instantiated CUDA graph, kept by the tracer
+// between calls: replayed while the same buffers, parameters and live lines
+// come back (instantiation costs ~5 us a node, so a graph is built for 16
+// sweeps or more, or when a call repeats the previous call's key).
+struct LevelGraphCache {
+    struct Key {
+        const void *field = nullptr, *proj = nullptr, *p_floor = nullptr, *clamps = nullptr, *lists = nullptr,
+                   *lpos = nullptr, *live = nullptr;
+        double beta = 0;
+        int power = 0, threads = 0, pdl = 0;
+        std::vector<uint32_t> live_off;
+        bool operator==(const Key& o) const {
+            return field == o.field && proj == o.proj && p_floor == o.p_floor && clamps == o.clamps &&
+                   lists == o.lists && lpos == o.lpos && live == o.live && beta == o.beta && power == o.power &&
+                   threads == o.threads && pdl == o.pdl && live_off == o.live_off;
+        }
+    };
+    cudaGraphExec_t exec = nullptr;
+    Key key;        // of `exec`
+    Key seen;       // of the last call that ran without a graph
+    bool have_seen = false;
+    void reset();   // destroys the graph (the caller has drained the stream)
+    ~LevelGraphCache() { reset(); }
+};
+void launch_mart_levels(const MartArgs& h, const LevelSchedule& ls, int sweeps, cudaStream_t st,
+                        LevelGraphCache* cache = nullptr);
 
 // Ring of traced index lists shared by the chunk tasks of a unit:
 // slot = [n, idx[0..n)], slot_words >= max_cells + 1.

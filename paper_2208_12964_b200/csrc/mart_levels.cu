@@ -20,8 +20,10 @@
 //   * lines with a zero measurement (skipped by the reference, solver.cpp:
 //     120-124) get no block: per call the level-sorted line order is compacted
 //     to the live lines on the device;
-//   * from 16 sweeps on, a sweep's launches are captured once in a CUDA graph
-//     and replayed (below that the instantiation costs more than it saves).
+//   * a sweep's launches replayed from a CUDA graph that the tracer keeps
+//     between calls (plain launches are host-bound at ~2.7 us each; the
+//     instantiation costs ~5 us a node, so a graph is built for 16 sweeps or
+//     more, or when a call repeats the previous call's buffers and data).
 #include <cuda_runtime.h>
 
 #include <cfloat>
@@ -144,7 +146,14 @@ void launch_live_lines(const uint32_t* order, const float* proj, uint32_t units,
         throw CudaError(std::string("live-line compaction launch: ") + cudaGetErrorString(e));
 }
 
-void launch_mart_levels(const MartArgs& h, const LevelSchedule& ls, int sweeps, cudaStream_t st) {
+void LevelGraphCache::reset() {
+    if (exec)
+        cudaGraphExecDestroy(exec);
+    exec = nullptr;
+}
+
+void launch_mart_levels(const MartArgs& h, const LevelSchedule& ls, int sweeps, cudaStream_t st,
+                        LevelGraphCache* cache) {
     if (h.Sp != 1)
         throw CudaError("mart_level_kernel runs one problem");
     static const int nt = [] {
@@ -188,12 +197,23 @@ void launch_mart_levels(const MartArgs& h, const LevelSchedule& ls, int sweeps, 
     int launched = 0;
     for (int l = 0; l < levels; ++l)
         launched += ls.live_off[l + 1] > ls.live_off[l];
+    // Plain launches are issued at ~2.7 us each, about the rate the levels run
+    // at (C3: 3.4 ms per iteration, host-bound); a replayed graph runs them at
+    // the device's rate (2.9 ms) but costs ~5 us a node to instantiate. So: a
+    // cached graph is replayed while its key comes back; a new one is built for
+    // 16 sweeps or more, or — after the launches of this call are issued — when
+    // the call repeats the key of the call before it.
     const char* ge = std::getenv("USCG_LEVEL_GRAPH");
-    // replayed from a graph when the sweeps amortise its instantiation (~5 us a
-    // node); else plain launches, which the host issues about as fast as the
-    // levels run
-    const bool graph = launched >= 8 && (ge ? std::atoi(ge) != 0 && sweeps >= 2 : sweeps >= 16);
-    if (graph) {
+    const bool allow = launched >= 8 && !(ge && !std::atoi(ge));
+    const bool force = ge && std::atoi(ge) != 0 && sweeps >= 2;
+    LevelGraphCache local;
+    LevelGraphCache* gc = cache ? cache : &local;
+    LevelGraphCache::Key key;
+    key.field = h.field, key.proj = h.proj, key.p_floor = h.p_floor, key.clamps = h.clamps;
+    key.lists = ls.lists, key.lpos = ls.lpos, key.live = ls.live;
+    key.beta = h.beta, key.power = h.power, key.threads = nt, key.pdl = pdl ? 1 : 0;
+    key.live_off = ls.live_off;
+    auto build = [&] {
         cudaGraph_t g = nullptr;
         cudaGraphExec_t exec = nullptr;
         UB_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
@@ -207,19 +227,32 @@ void launch_mart_levels(const MartArgs& h, const LevelSchedule& ls, int sweeps, 
         }
         UB_CUDA(cudaStreamEndCapture(st, &g));
         const cudaError_t ie = cudaGraphInstantiate(&exec, g, 0);
-        if (ie != cudaSuccess) {
-            cudaGraphDestroy(g);
-            UB_CUDA(ie);
-        }
-        for (int s = 0; s < sweeps; ++s)
-            UB_CUDA(cudaGraphLaunch(exec, st));
-        // the executable graph must outlive its launches
-        UB_CUDA(cudaStreamSynchronize(st));
-        cudaGraphExecDestroy(exec);
         cudaGraphDestroy(g);
+        UB_CUDA(ie);
+        if (gc->exec) {  // the old graph may still be running
+            UB_CUDA(cudaStreamSynchronize(st));
+            gc->reset();
+        }
+        gc->exec = exec;
+        gc->key = key;
+    };
+    const bool hit = allow && gc->exec && gc->key == key;
+    if (hit || (allow && (force || sweeps >= 16))) {
+        if (!hit)
+            build();
+        for (int s = 0; s < sweeps; ++s)
+            UB_CUDA(cudaGraphLaunch(gc->exec, st));
+        if (!cache)  // a graph that is not kept must outlive its launches
+            UB_CUDA(cudaStreamSynchronize(st));
     } else {
         for (int s = 0; s < sweeps; ++s)
             one_sweep();
+        if (allow && cache) {
+            if (cache->have_seen && cache->seen == key)
+                build();  // the same solve again: the next one replays (built while this one runs)
+            cache->seen = key;
+            cache->have_seen = true;
+        }
     }
     count_launch(uint64_t(launched) * uint64_t(sweeps));
     cudaError_t e = cudaGetLastError();

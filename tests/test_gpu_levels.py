@@ -99,3 +99,32 @@ def test_level_executor_all_zero_data_returns_the_initial_field(ub, orc, monkeyp
     res = ub.reconstruct(ub.ProjectionSet(geom, proj), spec, ub.SolverConfig(beta=0.5, tolerance=0, max_sweeps=3,
                                                                             f_init=1.25), tr)
     assert res.report.all_zero_data and np.all(res.field.values == np.float32(1.25))
+
+
+def test_level_executor_graph_cache_replays_and_follows_the_data(ub, orc, monkeypatch):
+    """The tracer keeps a sweep's launches as a graph once a solve repeats
+    (call 2 builds it, later calls replay it): every call returns the first
+    call's field bit for bit; other data (other live lines, another beta) are
+    not served by the stale graph."""
+    monkeypatch.setenv("USCG_MART_MODE", "levels")
+    spec, geom, tr, oc = _case(ub, orc, "volume")
+    proj = _data(ub, tr, spec, 21)
+    cfg = ub.SolverConfig(beta=0.6, tolerance=0, max_sweeps=3)
+    first = ub.reconstruct(ub.ProjectionSet(geom, proj), spec, cfg, tr).field.values
+    for _ in range(4):
+        again = ub.reconstruct(ub.ProjectionSet(geom, proj), spec, cfg, tr).field.values
+        assert np.array_equal(again, first)
+    other = _data(ub, tr, spec, 22)  # other zero lines: other grid sizes per level
+    got = ub.reconstruct(ub.ProjectionSet(geom, other), spec, cfg, tr).field.values
+    want, _ = oc.reconstruct(geom.thetas(), other, beta=0.6, tolerance=0, max_sweeps=3)
+    assert (np.abs(got - want) / want).max() <= 1e-4
+    scaled = proj * 1.5  # the same live lines, other measurements: the graph reads them at run time
+    got = ub.reconstruct(ub.ProjectionSet(geom, scaled), spec, cfg, tr).field.values
+    want, _ = oc.reconstruct(geom.thetas(), scaled, beta=0.6, tolerance=0, max_sweeps=3)
+    assert (np.abs(got - want) / want).max() <= 1e-4
+    cfg2 = ub.SolverConfig(beta=0.9, tolerance=0, max_sweeps=3)  # beta is a kernel parameter: a new key
+    for _ in range(3):
+        got = ub.reconstruct(ub.ProjectionSet(geom, proj), spec, cfg2, tr).field.values
+    want, _ = oc.reconstruct(geom.thetas(), proj, beta=0.9, tolerance=0, max_sweeps=3)
+    assert (np.abs(got - want) / want).max() <= 1e-4
+    assert np.array_equal(ub.reconstruct(ub.ProjectionSet(geom, proj), spec, cfg, tr).field.values, first)

@@ -8,6 +8,6 @@ import json,sys
 d=json.loads(sys.stdin.read().strip().splitlines()[-1])
 print(' '.join('%s %.3f ms/it, %d levels (binary %.3f)' % (k, d[k]['ms_per_iteration'], d[k]['levels'], d[k]['binary_model_ms_per_iteration']) for k in ('c1','c3')))"
 }
-for t in ${1:-"64 128 256"}; do run $t 1 1; done
+for t in ${1:-64 128 256}; do run $t 1 1; done
 run 64 0 1
 run 64 1 0
